@@ -1,0 +1,227 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (needs /root/reference):
+
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py
+
+Writes ``tests/golden/*.npz``.  Every array in them is an input or an output
+of the unmodified reference package ``kronblur`` (``pkg/src/kronblur``); the
+oracle (``oracle/``) and the CUDA path are checked against these files, which
+travel to the GPU box (the reference itself does not).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from kronblur.blurmodel import Psf, build_blur_matrix, make_test_image  # noqa: E402
+from kronblur.cgls import CglsConfig, cgls_solve  # noqa: E402
+from kronblur.exceptions import RankDeficiencyError  # noqa: E402
+from kronblur.kronop import assemble  # noqa: E402
+from kronblur.linalg import cast, orthonormalize, svd_small, vec  # noqa: E402
+from kronblur.lowrank import EgkbConfig, RsvdConfig, egkb, rsvd  # noqa: E402
+from kronblur.rearrange import BlockScheme, rearrange  # noqa: E402
+from kronblur.splitbregman import SbConfig, sb_run  # noqa: E402
+
+from paper_2410_00233_b200 import datagen  # noqa: E402
+
+
+def spectral_matrix(rng, m, n, sigmas):
+    """Same construction as the reference's tests/conftest.py:45-51."""
+    sigmas = np.asarray(sigmas, dtype=np.float64)
+    r = sigmas.size
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return (u * sigmas) @ v.T
+
+
+def geometric(count, ratio=2.0):
+    return ratio ** (-np.arange(count, dtype=np.float64))
+
+
+def trace_dict(tr):
+    return dict(alphas=np.array(tr.alphas), ts=np.array(tr.ts), zetas=np.array(tr.zetas),
+                nus=np.array(tr.nus), chosen_k=tr.chosen_k, k_p=tr.k_p,
+                stop_reason=tr.stop_reason, breakdown=tr.breakdown)
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def egkb_case(prefix, b_mat, cfg_kwargs, out, y0=None):
+    svd, tr = egkb(b_mat, EgkbConfig(**cfg_kwargs), y0=y0)
+    out[prefix + "u"] = svd.u
+    out[prefix + "sigma"] = svd.sigma
+    out[prefix + "v"] = svd.v
+    for k, v in trace_dict(tr).items():
+        out[prefix + "tr_" + k] = np.asarray(v)
+    out[prefix + "cfg"] = np.asarray(json.dumps(cfg_kwargs))
+
+
+def main():
+    rng = np.random.default_rng(12345)
+
+    # 1. structured R(A) closed form vs the reference's dense rearrange(build_blur_matrix)
+    ra = {}
+    for i, (kh, kw, n) in enumerate([(3, 5, 7), (5, 3, 6), (9, 9, 10), (1, 3, 6), (7, 7, 12)]):
+        psf = Psf(rng.random((kh, kw)))
+        r_mat = rearrange(build_blur_matrix(psf, n), BlockScheme.square_image(n))
+        q = rng.standard_normal(n * n)
+        s = rng.standard_normal(n * n)
+        ra[f"c{i}_psf"] = psf.kernel
+        ra[f"c{i}_n"] = n
+        ra[f"c{i}_q"] = q
+        ra[f"c{i}_s"] = s
+        ra[f"c{i}_Rq"] = r_mat @ q
+        ra[f"c{i}_RTs"] = r_mat.T @ s
+        ra[f"c{i}_sigma"] = np.linalg.svd(r_mat, compute_uv=False)
+    # padded even PSF (SURVEY §7 hard part 4) with the config generator, n=16
+    n = 16
+    kpad = datagen.rotated_gaussian_psf(n)
+    psf = Psf(kpad)
+    a_mat = build_blur_matrix(psf, n)
+    r_mat = rearrange(a_mat, BlockScheme.square_image(n))
+    q = rng.standard_normal(n * n)
+    s = rng.standard_normal(n * n)
+    x_img = datagen.cartoon_image(n)
+    ra.update(pad_psf=psf.kernel, pad_n=n, pad_q=q, pad_s=s, pad_Rq=r_mat @ q,
+              pad_RTs=r_mat.T @ s, pad_sigma=np.linalg.svd(r_mat, compute_uv=False),
+              pad_x=vec(x_img), pad_Ax=a_mat @ vec(x_img))
+    save("ra_structured", **ra)
+
+    # 2. eGKB known-answer cases (shapes from the reference tests/test_lowrank.py)
+    eg = {}
+    egkb_case("diag_", np.diag([5.0, 3.0, 1.0]), dict(k_max=3, k_min=3, seed=1), eg)
+    b = spectral_matrix(rng, 40, 30, geometric(5))
+    eg["rank5_b"] = b
+    egkb_case("rank5_", b, dict(k_max=10, p=2, tau=1e-30, seed=3), eg)
+    b = spectral_matrix(rng, 50, 40, geometric(40, 1.15))
+    eg["fact_b"] = b
+    egkb_case("fact64_", b, dict(k_max=12, p=2, tau=1e-30, k_min=12, seed=0), eg)
+    egkb_case("fact32_", cast(b, "single"), dict(k_max=12, p=2, tau=1e-30, k_min=12, seed=0), eg)
+    b = spectral_matrix(rng, 40, 40, geometric(20, 8.0))
+    eg["decay_b"] = b
+    egkb_case("decay_", b, dict(k_max=15, p=2, tau=1e-6, seed=5), eg)
+    egkb_case("decay32_", cast(b, "single"), dict(k_max=15, p=3, tau=1e-6, seed=5), eg)
+    b = spectral_matrix(rng, 60, 40, geometric(20, 2.0))
+    eg["accept3_b"] = b
+    egkb_case("accept3_", b, dict(k_max=15, p=4, tau=2e-5, seed=1), eg)
+    egkb_case("accept3s_", cast(b, "single"), dict(k_max=15, p=4, tau=2e-5, seed=1), eg)
+    b = spectral_matrix(rng, 20, 15, geometric(15, 1.5))
+    y0 = rng.standard_normal(20)
+    eg["y0_b"] = b
+    eg["y0_y0"] = y0
+    egkb_case("y0_", b, dict(k_max=5, k_min=5, tau=1e-30), eg, y0=y0)
+    # blur configs at small n (fp32 dense R, the reference's "SP" path)
+    for name, side in (("n64", 32), ("n256", 48)):
+        prob = datagen.make_problem(name, n=side)
+        r32 = cast(rearrange(build_blur_matrix(Psf(prob.psf), side), BlockScheme.square_image(side)), "single")
+        eg[f"blur_{name}_psf"] = prob.psf
+        eg[f"blur_{name}_n"] = side
+        egkb_case(f"blur_{name}_", r32, dict(prob.egkb), eg)
+    save("egkb_kat", **eg)
+
+    # 3. RSVD + orthonormalize
+    rs = {}
+    b = spectral_matrix(rng, 60, 50, geometric(30))
+    rs["sig_b"] = b
+    for tag, mat in (("d", b), ("s", cast(b, "single"))):
+        svd = rsvd(mat, RsvdConfig(k=5, p=8, q=2, seed=2))
+        rs[f"sig{tag}_u"], rs[f"sig{tag}_sigma"], rs[f"sig{tag}_v"] = svd.u, svd.sigma, svd.v
+    b = spectral_matrix(rng, 30, 80, geometric(20))
+    rs["wide_b"] = b
+    svd = rsvd(b, RsvdConfig(k=4, p=6, q=2, seed=3))
+    rs["wide_u"], rs["wide_sigma"], rs["wide_v"] = svd.u, svd.sigma, svd.v
+    b = spectral_matrix(rng, 20, 15, [3.0, 1.0])
+    rs["rankdef_b"] = b
+    try:
+        rsvd(b, RsvdConfig(k=4, p=2, q=1, seed=5))
+        rs["rankdef_col"] = -1
+    except RankDeficiencyError as err:
+        rs["rankdef_col"] = err.column
+    m = rng.standard_normal((50, 8))
+    rs["orth_in"] = m
+    rs["orth_out"] = orthonormalize(m)
+    rs["orth32_out"] = orthonormalize(cast(m, "single"))
+    save("rsvd_kat", **rs)
+
+    # 4. CGLS on small dense systems
+    cg = {}
+    for i in range(4):
+        a = rng.standard_normal((30, 10))
+        bb = rng.standard_normal(30)
+        res = cgls_solve(a, bb, CglsConfig(i_max=40, tau=1e-6 if i % 2 else 0.0))
+        cg[f"c{i}_a"], cg[f"c{i}_b"], cg[f"c{i}_x"] = a, bb, res.x
+        cg[f"c{i}_iters"], cg[f"c{i}_stop"] = res.iters, res.stop
+        cg[f"c{i}_rc"], cg[f"c{i}_res"] = np.array(res.rc_history), np.array(res.resnorms)
+    save("cgls_kat", **cg)
+
+    # 5. split Bregman: interchange case (test_splitbregman.py:147-162) and blur configs
+    sbd = {}
+    n = 8
+    a = build_blur_matrix(Psf(rng.random((3, 3)) + 0.05), n)
+    svd = svd_small(rearrange(a, BlockScheme.square_image(n)))
+    op = assemble(svd, BlockScheme.square_image(n))
+    bb = a @ vec(make_test_image(n))
+    cfg = SbConfig(lam=0.1, beta=0.005, tau=0.0, l_max=5, cgls=CglsConfig(i_max=12, tau=0.0))
+    sbd["inter_a"], sbd["inter_b"] = a, bb
+    sbd["inter_ax"], sbd["inter_ay"] = np.stack(op.ax), np.stack(op.ay)
+    sbd["inter_dense_x"] = sb_run(a, bb, cfg).x
+    sbd["inter_kron_x"] = sb_run(op, bb, cfg).x
+
+    for name, side, variants in (("n64", 32, ("anisotropic", "isotropic")),):
+        prob = datagen.make_problem(name, n=side)
+        r32 = cast(rearrange(build_blur_matrix(Psf(prob.psf), side), BlockScheme.square_image(side)), "single")
+        svd, _ = egkb(r32, EgkbConfig(**prob.egkb))
+        op = assemble(svd, BlockScheme.square_image(side))
+        sbd[f"{name}_ax"], sbd[f"{name}_ay"] = np.stack(op.ax), np.stack(op.ay)
+        sbd[f"{name}_b"], sbd[f"{name}_xtrue"] = prob.b, prob.x_true
+        for variant in variants:
+            # short protocol: the strict 1e-9 bar
+            short = SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=variant, tau=0.0, l_max=5,
+                             cgls=CglsConfig(i_max=20, tau=0.0))
+            res = sb_run(op, prob.b, short, x_true=prob.x_true)
+            sbd[f"{name}_{variant}_short_x"] = res.x
+            sbd[f"{name}_{variant}_short_re"] = np.array(res.re_history)
+            # configured protocol, truncated to 10 outer sweeps
+            full = SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=variant, tau=0.0, l_max=10,
+                            cgls=CglsConfig(i_max=100, tau=1e-4))
+            res = sb_run(op, prob.b, full, x_true=prob.x_true)
+            sbd[f"{name}_{variant}_cfg_x"] = res.x
+            sbd[f"{name}_{variant}_cfg_iters"] = np.array(res.cgls_iters)
+            sbd[f"{name}_{variant}_cfg_rc"] = np.array(res.rc_history)
+            sbd[f"{name}_{variant}_cfg_re"] = np.array(res.re_history)
+            sbd[f"{name}_{variant}_cfg_isnr"] = np.array(res.isnr_history)
+    save("sb_kat", **sbd)
+
+    # 6. configs[0] at full size (n=64): reference eGKB on the dense fp32 R(A)
+    prob = datagen.make_problem("n64")
+    a_mat = build_blur_matrix(Psf(prob.psf), 64)
+    r32 = cast(rearrange(a_mat, BlockScheme.square_image(64)), "single")
+    cf = {"psf": prob.psf, "b": prob.b, "x_true": prob.x_true, "Ax_true": a_mat @ prob.x_true}
+    svd, tr = egkb(r32, EgkbConfig(**prob.egkb))
+    cf.update(u=svd.u, sigma=svd.sigma, v=svd.v)
+    for k, v in trace_dict(tr).items():
+        cf["tr_" + k] = np.asarray(v)
+    svd_auto, tr_auto = egkb(r32, EgkbConfig(k_max=20))
+    cf.update(auto_sigma=svd_auto.sigma, auto_chosen=tr_auto.chosen_k, auto_kp=tr_auto.k_p,
+              auto_reason=tr_auto.stop_reason, auto_nus=np.array(tr_auto.nus))
+    op = assemble(svd, BlockScheme.square_image(64))
+    short = SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant="anisotropic", tau=0.0, l_max=5,
+                     cgls=CglsConfig(i_max=20, tau=0.0))
+    cf["sb_short_x"] = sb_run(op, prob.b, short).x
+    save("config_n64", **cf)
+
+
+if __name__ == "__main__":
+    main()
