@@ -1,0 +1,243 @@
+/*
+ * kronblur_b200 — C ABI of the B200 (sm_100a) hot path of arXiv 2410.00233.
+ *
+ * Drop-in boundary for the reference package `kronblur` (pure Python; its
+ * hot path is numpy/OpenBLAS).  Every entry point below replaces one
+ * reference call site, cited as pkg/src/kronblur/<file>:<line>.  The
+ * Python host package `paper_2410_00233_b200` binds these with ctypes (see
+ * INTEGRATION.md for the binding a kronblur maintainer would add).
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers owned by the caller (torch
+ *    tensors on the Python side) unless the name ends in `_host`.
+ *  - Every call is stream-ordered on the given cudaStream_t (pass the
+ *    current torch stream) and returns an int status:
+ *        KB_OK (0), KB_EVALIDATION (2), KB_ENUMERICAL (3), KB_ERUNTIME (4)
+ *    matching the reference CLI exit codes (cli.py:584-595) for
+ *    ValidationError / NumericalError / other failures.  kb_last_error()
+ *    gives the message of the last failure on the calling thread.
+ *  - Vectors are contiguous; a "basis" is `m` vectors of length `len`
+ *    stored at stride `ld` (vector i at base + i*ld).
+ *  - Reductions are deterministic: fixed-order tree reductions, no atomics
+ *    on data (SPEC determinism).
+ *  - dtype codes: KB_F32 (0), KB_F64 (1).
+ */
+#ifndef KRONBLUR_B200_H
+#define KRONBLUR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* kb_stream_t; /* cudaStream_t */
+
+#define KB_OK 0
+#define KB_EVALIDATION 2
+#define KB_ENUMERICAL 3
+#define KB_ERUNTIME 4
+
+#define KB_F32 0
+#define KB_F64 1
+
+/* Operator kinds for the low-rank engines. */
+#define KB_OP_DENSE 0   /* b_mat given densely (lowrank.py:187)             */
+#define KB_OP_RA_ZERO 1 /* matrix-free R(A) of a zero-BC PSF blur (new)      */
+
+/* eGKB stop reasons (lowrank.py:26-29) */
+#define KB_STOP_NU_ROSE 1
+#define KB_STOP_NU_BELOW_TOL 2
+#define KB_STOP_HIT_KMAX 3
+#define KB_STOP_BREAKDOWN 4
+
+/* SB variants / stops (splitbregman.py:19-25), CGLS stops (cgls.py:15-17) */
+#define KB_SB_ANISOTROPIC 0
+#define KB_SB_ISOTROPIC 1
+#define KB_SB_MAX_ITER 0
+#define KB_SB_CONVERGED 1
+#define KB_CGLS_MAX_ITER 0
+#define KB_CGLS_CONVERGED 1
+#define KB_CGLS_STALLED 2
+
+const char* kb_last_error(void);
+int kb_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Operators B for eGKB / RSVD                                        */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int kind;          /* KB_OP_DENSE or KB_OP_RA_ZERO                     */
+    int dtype;         /* KB_F32 / KB_F64: working precision               */
+    int64_t rows;      /* mbar                                             */
+    int64_t cols;      /* nbar                                             */
+    const void* a;     /* DENSE: row-major rows x cols, leading dim lda    */
+    int64_t lda;
+    const void* k;     /* RA: PSF kernel kh x kw, row-major, dtype         */
+    const void* kt;    /* RA: the same kernel transposed (kw x kh)         */
+    int kh, kw;        /* RA: PSF support (odd; centre kh/2, kw/2)          */
+    int side;          /* RA: image side n (rows = cols = n*n)             */
+} kb_operator;
+
+/* Workspace for kb_op_apply / kb_egkb_run / kb_rsvd helpers. */
+int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes);
+
+/* y = B x (transpose=0) or y = B^T x (transpose=1).
+ * Replaces `b_mat @ q` / `b_mat.T @ s` (lowrank.py:211,238,250) and, for
+ * KB_OP_RA_ZERO, `rearrange(build_blur_matrix(psf, n))` (rearrange.py:67-75,
+ * blurmodel.py:87-121) without forming R(A). */
+int kb_op_apply(const kb_operator* op, const void* x, void* y, int transpose,
+                void* ws, size_t ws_bytes, kb_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Tall-skinny building blocks (reorthogonalisation, lift)            */
+/* ------------------------------------------------------------------ */
+/* out[i] = <S_i, v> for i < m, out[m] = <v, v>  (fp64 results, device). */
+int kb_ts_dots(int dtype, const void* S, int64_t ld, int m, const void* v,
+               int64_t len, double* out, void* ws, size_t ws_bytes, kb_stream_t stream);
+/* v -= sum_i coef[i] S_i   (coef device fp64, length m). */
+int kb_ts_axpy(int dtype, const void* S, int64_t ld, int m, const double* coef,
+               void* v, int64_t len, kb_stream_t stream);
+/* out_c = sum_{i<rows} W[i, c] S_i for c < cols; W row-major rows x cols in
+ * dtype (device).  The eGKB lift U = S U_C, V = Q V_C (lowrank.py:317-318)
+ * and the RSVD lift U = Y U_H (lowrank.py:369). */
+int kb_ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols,
+               void* out, int64_t ld_out, int64_t len, kb_stream_t stream);
+/* In-place two-pass Gram-Schmidt of ncol vectors with the drop test of
+ * orthonormalize (linalg.py:156-199).  drop_tol < 0 selects the default
+ * eps*sqrt(len)*max column norm.  Returns KB_ENUMERICAL and *bad_col=j
+ * (RankDeficiencyError(j)) when column j collapses; *bad_col=-2 on a
+ * non-finite norm. */
+int kb_orthonormalize(int dtype, void* Q, int64_t ld, int ncol, int64_t len,
+                      double drop_tol, int* bad_col, void* ws, size_t ws_bytes,
+                      kb_stream_t stream);
+int kb_orth_workspace_bytes(int64_t len, int ncol, size_t* bytes);
+
+/* ------------------------------------------------------------------ */
+/* eGKB (lowrank.py:159-329)                                           */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int k_max, p, k_min;
+    double tau;
+    double break_tol;     /* < 0: sqrt(eps) of dtype (lowrank.py:194)          */
+    int full_reorth;      /* 1: project s against S (lowrank.py:240-241)       */
+    int reorth_passes;    /* 1: classical GS, 2: CGS2 (default)                */
+} kb_egkb_config;
+
+typedef struct {
+    /* caller-allocated device bases: `capacity` vectors each */
+    void* s_basis; int64_t ld_s;
+    void* q_basis; int64_t ld_q;
+    int capacity;
+    /* caller-allocated host arrays of length `capacity` (trace, 1-based lists) */
+    double* alphas_host; double* ts_host; double* zetas_host; double* nus_host;
+    /* outputs */
+    int n_alphas, n_ts, n_nus;
+    int chosen_k, k_p, rows, stop_reason, breakdown;
+} kb_egkb_state;
+
+/* Minimum basis capacity for a config (vectors). */
+int kb_egkb_capacity(const kb_egkb_config* cfg);
+/* Runs the bidiagonalisation loop (lowrank.py:207-303) on the device; the
+ * small SVD of C (lowrank.py:308-316) stays on the host, the lift is
+ * kb_ts_lift.  y0 is a device vector of length op->rows in op->dtype. */
+int kb_egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const void* y0,
+                kb_egkb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
+int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
+
+/* ------------------------------------------------------------------ */
+/* Structured exact TSVD lift (new, replaces         */
+/* svd_small(rearrange(A)) linalg.py:134-153 for blur operators)        */
+/* ------------------------------------------------------------------ */
+/* out_c[a*n+b] = coef[c*ldc + (b-a+center)] (0 outside [0,len_coef)), c<k */
+int kb_toeplitz_lift(int dtype, const void* coef, int64_t ldc, int len_coef, int center,
+                     int k, int side, void* out, int64_t ld_out, kb_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Kronecker sum, fp64 (kronop.py:28-123)                               */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int m1, m2, n1, n2, k;
+    const double* f;  /* k x n1 x m1: F_i = ax_i^T = reshape(sigma_i u_i, (n1, m1)) */
+    const double* g;  /* k x n2 x m2: G_i = ay_i^T = reshape(v_i, (n2, m2))         */
+} kb_kron;
+
+int kb_kron_workspace_bytes(const kb_kron* kr, size_t* bytes);
+/* y = A x (transpose=0, kronop.py:58-70) or y = A^T x (kronop.py:72-84). */
+int kb_kron_apply(const kb_kron* kr, const double* x, double* y, int transpose,
+                  void* ws, size_t ws_bytes, kb_stream_t stream);
+/* Factor assembly (kronop.py:103-123): F_i = sigma_i * u_i, G_i = v_i,
+ * promoted to fp64 (u, v in dtype, vectors at stride ldu/ldv). */
+int kb_kron_assemble(int dtype, const void* u, int64_t ldu, const void* v, int64_t ldv,
+                     const double* sigma_host, int k, int64_t len_u, int64_t len_v,
+                     double* f, double* g, kb_stream_t stream);
+/* Generic fp64 GEMM used by the Kronecker apply:
+ * C_z = sum_{s<nseg} op(A_{z,s}) op(B_{z,s}) (+ beta C_z), z < nbatch. */
+int kb_dgemm(int trans_a, int trans_b, int m, int n, int k,
+             const double* A, int64_t lda, int64_t sa_batch, int64_t sa_seg,
+             const double* B, int64_t ldb, int64_t sb_batch, int64_t sb_seg,
+             double* C, int64_t ldc, int64_t sc_batch, int nbatch, int nseg,
+             double beta, kb_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Augmented system, CGLS, split Bregman (fp64)                         */
+/* ------------------------------------------------------------------ */
+#define KB_FWD_DENSE 0
+#define KB_FWD_KRON 1
+typedef struct {
+    int kind;            /* KB_FWD_DENSE / KB_FWD_KRON                       */
+    int64_t m, n;        /* forward operator shape                           */
+    const double* a;     /* DENSE: row-major m x n                           */
+    int64_t lda;
+    kb_kron kron;        /* KRON                                             */
+    int augmented;       /* 1: [A; lam_x Dx; lam_y Dy] (regularizers.py:65)   */
+    int side;            /* image side for the difference maps               */
+    double lam_x, lam_y;
+} kb_forward;
+
+int kb_forward_workspace_bytes(const kb_forward* fw, size_t* bytes);
+int kb_forward_apply(const kb_forward* fw, const double* x, double* y, int transpose,
+                     void* ws, size_t ws_bytes, kb_stream_t stream);
+
+typedef struct {
+    int i_max; double tau;
+    /* outputs */
+    int iters, stop;
+    double* rc_host;        /* caller host array, capacity i_max               */
+    double* resnorm_host;   /* caller host array, capacity i_max + 1           */
+    int n_rc, n_res;
+} kb_cgls_state;
+int kb_cgls_workspace_bytes(const kb_forward* fw, size_t* bytes);
+/* cgls.py:50-116.  x0 may be NULL (start from zero); x is the output. */
+int kb_cgls_run(const kb_forward* fw, const double* b, const double* x0, double* x,
+                kb_cgls_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
+
+typedef struct {
+    double lam, beta;
+    int variant;         /* KB_SB_ANISOTROPIC / KB_SB_ISOTROPIC               */
+    double tau;
+    int l_max;
+    int i_max; double tau_cgls;
+    int warm_start;
+    /* outputs (host arrays of capacity l_max, caller-owned) */
+    int outer_iters, stop;
+    double* rc_host; double* re_host; double* isnr_host; int* cgls_iters_host;
+} kb_sb_state;
+int kb_sb_workspace_bytes(const kb_forward* fw, size_t* bytes);
+/* splitbregman.py:120-192.  fw must be the (non-augmented) square forward
+ * operator; x_true may be NULL.  x (device, length n^2) receives the result. */
+int kb_sb_run(const kb_forward* fw, const double* b, const double* x_true, double* x,
+              kb_sb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
+
+/* Elementwise pieces exposed for parity tests (splitbregman.py:32-61,
+ * regularizers.py:37-62). */
+int kb_diff(const double* x, double* out, int side, int axis, int transpose, double scale,
+            int accumulate, kb_stream_t stream);
+int kb_shrink_update(const double* cx, const double* cy, double* dx, double* dy,
+                     int64_t len, double gamma, int variant, kb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRONBLUR_B200_H */

@@ -1,0 +1,226 @@
+"""PSF model, dense blur matrix (small n) and the matrix-free R(A) operator.
+
+Reference: pkg/src/kronblur/blurmodel.py.  ``Psf``, ``NoiseSpec``,
+``add_noise`` and ``build_blur_matrix`` keep the reference semantics (host
+input construction).  :class:`RearrangedBlur` is the B200 extension named by
+SURVEY §8(b): R(A) of a zero-BC blur applied matrix-free on the GPU, accepted
+by :func:`egkb`, :func:`rsvd` and :func:`tsvd` wherever a dense ``b_mat`` is.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .exceptions import NumericalError, ValidationError
+
+BC_ZERO = "zero"
+BC_REFLEXIVE = "reflexive"
+BOUNDARY_CONDITIONS = (BC_ZERO, BC_REFLEXIVE)
+DENSE_SIDE_CAP = 200   # blurmodel.py:22
+
+
+@dataclass
+class Psf:
+    """Unit-sum, non-negative PSF with odd support (blurmodel.py:25-65)."""
+
+    kernel: np.ndarray
+
+    def __post_init__(self):
+        k = np.array(self.kernel, dtype=np.float64)
+        if k.ndim != 2:
+            raise ValidationError("PSF kernel must be 2-D")
+        if k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
+            raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
+        if np.any(k < 0):
+            raise ValidationError("PSF kernel must be non-negative")
+        total = k.sum()
+        if total <= 0:
+            raise ValidationError("PSF kernel must have positive mass")
+        self.kernel = k / total
+
+    @property
+    def center(self) -> tuple[int, int]:
+        return (self.kernel.shape[0] // 2, self.kernel.shape[1] // 2)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.kernel.shape
+
+    def separability_ratio(self) -> float:
+        s = np.linalg.svd(self.kernel, compute_uv=False)
+        if s[0] == 0:
+            raise NumericalError("PSF kernel has zero norm")
+        return float(s[1] / s[0]) if s.size > 1 else 0.0
+
+
+@dataclass(frozen=True)
+class NoiseSpec:
+    level: float
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.level < 0:
+            raise ValidationError("noise level must be >= 0")
+
+
+def add_noise(b_true, spec: NoiseSpec):
+    """White noise with ||eta|| = level ||b_true|| (blurmodel.py:204-218)."""
+    b_true = np.asarray(b_true, dtype=np.float64)
+    if spec.level == 0.0:
+        return b_true.copy(), np.zeros_like(b_true)
+    zeta = np.random.default_rng(spec.seed).standard_normal(b_true.shape)
+    znorm = np.linalg.norm(zeta.ravel())
+    if znorm == 0.0:
+        raise NumericalError("degenerate noise draw")
+    eta = spec.level * (np.linalg.norm(b_true.ravel()) / znorm) * zeta
+    return b_true + eta, eta
+
+
+def _reflect(idx, n):
+    out = np.where(idx < 0, -1 - idx, idx)
+    return np.where(out >= n, 2 * n - 1 - out, out)
+
+
+def build_blur_matrix(psf: Psf, n: int, bc: str = BC_ZERO, cap: int = DENSE_SIDE_CAP) -> np.ndarray:
+    """Dense n^2 x n^2 convolution matrix (host; blurmodel.py:87-127).
+
+    Only for small dense comparisons; the GPU path never forms A or R(A).
+    """
+    if bc not in BOUNDARY_CONDITIONS:
+        raise ValidationError(f"boundary condition must be one of {BOUNDARY_CONDITIONS}, got {bc!r}")
+    if n < 1:
+        raise ValidationError("image side must be >= 1")
+    if n > cap:
+        raise ValidationError(f"image side {n} exceeds the dense cap {cap}")
+    kh, kw = psf.shape
+    if bc == BC_REFLEXIVE and (kh > 2 * n - 1 or kw > 2 * n - 1):
+        raise ValidationError("PSF support too large for single reflection at this image size")
+    cu, cv = psf.center
+    rr, cc = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    out_idx = (cc * n + rr).ravel()
+    a = np.zeros((n * n, n * n))
+    for u in range(kh):
+        for v in range(kw):
+            wgt = psf.kernel[u, v]
+            if wgt == 0.0:
+                continue
+            r_in, c_in = rr - u + cu, cc - v + cv
+            if bc == BC_ZERO:
+                ok = ((r_in >= 0) & (r_in < n) & (c_in >= 0) & (c_in < n)).ravel()
+                a[out_idx[ok], (c_in * n + r_in).ravel()[ok]] += wgt
+            else:
+                a[out_idx, (_reflect(c_in, n) * n + _reflect(r_in, n)).ravel()] += wgt
+    return a
+
+
+def make_test_image(n: int) -> np.ndarray:
+    """Deterministic piecewise-constant test image (blurmodel.py:186-201)."""
+    if n < 8:
+        raise ValidationError(f"test image side must be >= 8, got {n}")
+    img = np.full((n, n), 0.05)
+    img[n // 8 : n // 2, n // 8 : n // 2] = 0.9
+    img[n // 2 :, 2 * n // 3 :] = 0.45
+    rr, cc = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    img[(rr - 0.7 * n) ** 2 + (cc - 0.3 * n) ** 2 <= (0.16 * n) ** 2] = 0.7
+    img[n // 12 : n // 6, :] = np.maximum(img[n // 12 : n // 6, :], 0.3)
+    return img
+
+
+class RearrangedBlur:
+    """Matrix-free R(A) of a zero-BC PSF blur on n x n images.
+
+    R[c_in*n + c_out, r_in*n + r_out] = K[r_out - r_in + cu, c_out - c_in + cv]
+    (closed form of rearrange.py:67-75 o blurmodel.py:106-121; SURVEY
+    Appendix A).  Shape (n^2, n^2); ``dtype`` is the working precision of the
+    engines (float32 = the reference's "SP" path).  The PSF lives on the
+    device; products run in the sm_100a kernels of libkronblur_b200.
+    """
+
+    def __init__(self, psf, n: int, bc: str = BC_ZERO, dtype=np.float32):
+        if not isinstance(psf, Psf):
+            psf = Psf(psf)
+        if bc != BC_ZERO:
+            raise ValidationError(
+                f"RearrangedBlur supports bc='zero' only (reflexive is a SURVEY §8(f) 'next' row), got {bc!r}")
+        if n < 1:
+            raise ValidationError("image side must be >= 1")
+        self.psf = psf
+        self.n = int(n)
+        self.bc = bc
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+            raise ValidationError(f"unsupported dtype {self.dtype}; expected float32 or float64")
+        self._k = None
+        self._kt = None
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.n * self.n, self.n * self.n)
+
+    @property
+    def ndim(self) -> int:
+        return 2
+
+    def astype(self, dtype) -> "RearrangedBlur":
+        return RearrangedBlur(self.psf, self.n, self.bc, dtype)
+
+    def _device_kernels(self):
+        from . import device as D
+
+        if self._k is None:
+            kk = self.psf.kernel.astype(self.dtype)
+            self._k = D.to_device(np.ascontiguousarray(kk))
+            self._kt = D.to_device(np.ascontiguousarray(kk.T))
+        return self._k, self._kt
+
+    def op_struct(self) -> _lib.KbOperator:
+        k, kt = self._device_kernels()
+        kh, kw = self.psf.shape
+        op = _lib.KbOperator()
+        op.kind = _lib.KB_OP_RA_ZERO
+        op.dtype = _lib.KB_F32 if self.dtype == np.float32 else _lib.KB_F64
+        op.rows = op.cols = self.n * self.n
+        op.a, op.lda = None, 0
+        op.k, op.kt = k.data_ptr(), kt.data_ptr()
+        op.kh, op.kw, op.side = kh, kw, self.n
+        return op
+
+    def _apply(self, x, transpose: int):
+        from . import device as D
+
+        host = not D.is_tensor(x)
+        xd = D.to_device(x, self.dtype).reshape(-1)
+        if xd.numel() != self.n * self.n:
+            raise ValidationError(f"expected a vector of length {self.n * self.n}, got {xd.numel()}")
+        y = D.empty(self.n * self.n, self.dtype)
+        op = self.op_struct()
+        lib = _lib.load()
+        nb = C.c_size_t()
+        _lib.check(lib.kb_op_workspace_bytes(C.byref(op), C.byref(nb)))
+        ws, wsb = D.WORKSPACE.get(nb.value)
+        _lib.check(lib.kb_op_apply(C.byref(op), xd.data_ptr(), y.data_ptr(), transpose, ws, wsb,
+                                   D.stream_ptr()), "R(A) apply")
+        return D.to_host(y) if host else y
+
+    def matvec(self, q):
+        """R(A) q  (replaces ``b_mat @ q``, lowrank.py:238)."""
+        return self._apply(q, 0)
+
+    def rmatvec(self, s):
+        """R(A)^T s  (replaces ``b_mat.T @ s``, lowrank.py:211,250)."""
+        return self._apply(s, 1)
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+    def to_dense(self) -> np.ndarray:
+        """Dense R(A) (host, tiny n only; for tests)."""
+        if self.n > 64:
+            raise ValidationError("to_dense is for n <= 64")
+        from .rearrange import BlockScheme, rearrange
+
+        return rearrange(build_blur_matrix(self.psf, self.n), BlockScheme.square_image(self.n)).astype(self.dtype)

@@ -1,0 +1,209 @@
+// FP64 GEMM on the sm_100a FP64 tensor pipe (DMMA m8n8k4), for the
+// Kronecker-sum apply of the split-Bregman inner loop (kronop.py:58-84).
+//
+// tcgen05 has no f64 kind, so FP64 tensor-core work on Blackwell goes through
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  The kernel computes
+//     C_z = sum_{s < nseg} op(A_{z,s}) op(B_{z,s})  (+ beta C_z),  z < nbatch
+// which covers both Kronecker stages: a batched stage (nbatch = k terms) and
+// a segment-reduced stage (nseg = k terms summed into one output, i.e. one
+// GEMM with inner dimension k*n1).  Row-major operands; trans flags select
+// the smem staging layout so fragment reads are bank-conflict free.
+//
+// CTA tile 128 x 64 x 16, 8 warps (4 x 2) of 32 x 32, 3-stage cp.async
+// pipeline with zero-filled edges (any M, N, K, ld).
+#include <algorithm>
+
+#include "kb_common.cuh"
+
+namespace kb {
+
+namespace g64 {
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int PAD = 4;
+// smem sizes (doubles) per stage
+template <bool TA>
+struct ALayout {
+    static constexpr int rows = TA ? BK : BM;
+    static constexpr int ld = TA ? (BM + PAD) : (BK + PAD);
+    static constexpr int size = rows * ld;
+};
+template <bool TB>
+struct BLayout {
+    static constexpr int rows = TB ? BN : BK;
+    static constexpr int ld = TB ? (BK + PAD) : (BN + PAD);
+    static constexpr int size = rows * ld;
+};
+}  // namespace g64
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(g64::THREADS, 2)
+k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sa_batch,
+        int64_t sa_seg, const double* __restrict__ B, int64_t ldb, int64_t sb_batch,
+        int64_t sb_seg, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nseg,
+        double beta) {
+    using namespace g64;
+    using AL = ALayout<TA>;
+    using BL = BLayout<TB>;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                       // [STAGES][AL::size]
+    double* Bs = smem + STAGES * AL::size;   // [STAGES][BL::size]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int z = blockIdx.z;
+    const double* Ab = A + (int64_t)z * sa_batch;
+    const double* Bb = B + (int64_t)z * sb_batch;
+    double* Cb = C + (int64_t)z * sc_batch;
+
+    const int ktiles = (K + BK - 1) / BK;
+    const int T = ktiles * nseg;
+
+    auto load_tile = [&](int stage, int t) {
+        const int s = t / ktiles;
+        const int k0 = (t - s * ktiles) * BK;
+        const double* Ap = Ab + (int64_t)s * sa_seg;
+        const double* Bp = Bb + (int64_t)s * sb_seg;
+        double* as = As + stage * AL::size;
+        double* bs = Bs + stage * BL::size;
+        // A tile: BM x BK
+#pragma unroll
+        for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+            const int idx = tid + r * THREADS;
+            int i, j;  // i: m, j: k
+            if (!TA) { i = idx / BK; j = idx % BK; } else { j = idx / BM; i = idx % BM; }
+            const int gm = m0 + i, gk = k0 + j;
+            const bool ok = (gm < M) && (gk < K);
+            const double* src = TA ? (Ap + (int64_t)(ok ? gk : 0) * lda + (ok ? gm : 0))
+                                   : (Ap + (int64_t)(ok ? gm : 0) * lda + (ok ? gk : 0));
+            double* dst = TA ? (as + j * AL::ld + i) : (as + i * AL::ld + j);
+            cp_async8(dst, src, ok);
+        }
+        // B tile: BK x BN
+#pragma unroll
+        for (int r = 0; r < (BK * BN) / THREADS; ++r) {
+            const int idx = tid + r * THREADS;
+            int j, c;  // j: k, c: n
+            if (!TB) { j = idx / BN; c = idx % BN; } else { c = idx / BK; j = idx % BK; }
+            const int gk = k0 + j, gn = n0 + c;
+            const bool ok = (gk < K) && (gn < N);
+            const double* src = TB ? (Bp + (int64_t)(ok ? gn : 0) * ldb + (ok ? gk : 0))
+                                   : (Bp + (int64_t)(ok ? gk : 0) * ldb + (ok ? gn : 0));
+            double* dst = TB ? (bs + c * BL::ld + j) : (bs + j * BL::ld + c);
+            cp_async8(dst, src, ok);
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < T) load_tile(s, s);
+        cp_async_commit();
+    }
+
+    const int gid = lane >> 2, tig = lane & 3;
+    for (int t = 0; t < T; ++t) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nt = t + STAGES - 1;
+            if (nt < T) load_tile(nt % STAGES, nt);
+            cp_async_commit();
+        }
+        const double* as = As + (t % STAGES) * AL::size;
+        const double* bs = Bs + (t % STAGES) * BL::size;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const int mm = wm * 32 + mi * 8 + gid, k = kk + tig;
+                af[mi] = TA ? as[k * AL::ld + mm] : as[mm * AL::ld + k];
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int nn = wn * 32 + ni * 8 + gid, k = kk + tig;
+                bf[ni] = TB ? bs[nn * BL::ld + k] : bs[k * BL::ld + nn];
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int gm = m0 + wm * 32 + mi * 8 + gid;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int gn = n0 + wn * 32 + ni * 8 + 2 * tig;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (gn + q < N) {
+                    double* cp = Cb + (int64_t)gm * ldc + gn + q;
+                    *cp = (beta != 0.0) ? (acc[mi][ni][q] + beta * *cp) : acc[mi][ni][q];
+                }
+            }
+        }
+    }
+}
+
+template <bool TA, bool TB>
+static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
+                         int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s,
+                         double* C, int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta,
+                         cudaStream_t st) {
+    using namespace g64;
+    const size_t smem = sizeof(double) * STAGES * (ALayout<TA>::size + BLayout<TB>::size);
+    static bool configured = false;
+    if (!configured) {
+        KB_CUDA(cudaFuncSetAttribute(k_dgemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        configured = true;
+    }
+    dim3 grid((unsigned)cdiv(n, BN), (unsigned)cdiv(m, BM), (unsigned)nbatch);
+    k_dgemm<TA, TB><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
+                                                 C, ldc, sc_b, nseg, beta);
+    KB_LAUNCH_CHECK();
+}
+
+void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
+           int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
+           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st) {
+    KB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && nbatch >= 1 && nseg >= 1, "dgemm: bad sizes");
+    KB_REQUIRE(nbatch <= 65535, "dgemm: too many batches (%d)", nbatch);
+    if (m == 0 || n == 0) return;
+    if (!ta && !tb)
+        launch_dgemm<false, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
+    else if (!ta && tb)
+        launch_dgemm<false, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
+    else if (ta && !tb)
+        launch_dgemm<true, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
+    else
+        launch_dgemm<true, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
+}
+
+}  // namespace kb

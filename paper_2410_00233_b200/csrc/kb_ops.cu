@@ -1,0 +1,545 @@
+// Operator, reorthogonalisation and lift kernels for the eGKB / RSVD path
+// (fp32 and fp64), sm_100a.
+//
+// R(A) for a zero-BC PSF blur is never formed:
+//   R[c_in*n + c_out, r_in*n + r_out] = K[r_out - r_in + cu, c_out - c_in + cv]
+// so  y = R q  is  w[u] = sum of q over the diagonal r_out - r_in = u - cu
+//                  z    = K^T w                        (kw coefficients)
+//                  y[c_in*n + c_out] = z[c_out - c_in + cv]   (Toeplitz)
+// Reference sites replaced: lowrank.py:211,238,250 (b_mat @ q, b_mat.T @ s)
+// on R from rearrange.py:67-75 o blurmodel.py:87-121.
+//
+// Bandwidth plan (one product): read the n x n band once (diagonal sums,
+// coalesced along the diagonal index), read K once (column sums, coalesced
+// along K rows), and never write y: the Toeplitz broadcast is regenerated
+// inside the reorthogonalisation passes that consume it.
+#include <algorithm>
+
+#include "kb_ops.cuh"
+
+namespace kb {
+
+// ------------------------------------------------------------------ diag sums
+// part[rb][u] = sum_{a in row block rb} X[a, a + u - center];
+// the last block per diagonal chunk reduces the row blocks in order -> w[u].
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_diag_partial(const T* __restrict__ X, int n, int center, int L, int rb_rows,
+               double* __restrict__ part, double* __restrict__ w, unsigned* counters) {
+    const int u = blockIdx.x * 256 + threadIdx.x;
+    const int a0 = blockIdx.y * rb_rows;
+    const int a1 = min(a0 + rb_rows, n);
+    double acc = 0.0;
+    if (u < L) {
+        const int d = u - center;
+        const int lo = max(a0, -d), hi = min(a1, n - d);
+        if (lo < hi) {
+            const T* p = X + (int64_t)lo * n + (lo + d);
+#pragma unroll 8
+            for (int a = lo; a < hi; ++a, p += (n + 1)) acc += (double)__ldg(p);
+        }
+        part[(int64_t)blockIdx.y * L + u] = acc;
+    }
+    if (last_block_ticket(&counters[blockIdx.x], gridDim.y)) {
+        if (u < L) {
+            double s = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < (int)gridDim.y; ++r) s += __ldcg(&part[(int64_t)r * L + u]);
+            w[u] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ column sums
+// z[c] = sum_r M[r, c] w[r]   (M row-major rows x cols, leading dim ld)
+template <typename TM, typename TW>
+__global__ void __launch_bounds__(256)
+k_colsum(const TM* __restrict__ M, int64_t ld, int rows, int cols, const TW* __restrict__ w,
+         int rb_rows, double* __restrict__ part, double* __restrict__ z, unsigned* counters) {
+    __shared__ double red[8][128];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = blockIdx.x * 128;
+    const int r0 = blockIdx.y * rb_rows, r1 = min(r0 + rb_rows, rows);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = r0 + warp; r < r1; r += 8) {
+        const double wr = (double)w[r];
+        const TM* row = M + (int64_t)r * ld;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c0 + lane + 32 * j;
+            if (c < cols) acc[j] += (double)__ldg(row + c) * wr;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[warp][lane + 32 * j] = acc[j];
+    __syncthreads();
+    const int c = c0 + threadIdx.x;
+    if (threadIdx.x < 128 && c < cols) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x];
+        part[(int64_t)blockIdx.y * cols + c] = s;
+    }
+    if (last_block_ticket(&counters[blockIdx.x], gridDim.y)) {
+        if (threadIdx.x < 128 && c < cols) {
+            double s = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < (int)gridDim.y; ++r) s += __ldcg(&part[(int64_t)r * cols + c]);
+            z[c] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ row dots
+// z[r] = sum_c A[r, c] x[c]  (one warp per row; dense b_mat @ q)
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_rowdot(const T* __restrict__ A, int64_t lda, int rows, int cols, const T* __restrict__ x,
+         double* __restrict__ z) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const T* row = A + (int64_t)r * lda;
+    double acc = 0.0;
+    for (int c = lane; c < cols; c += 32) acc += (double)__ldg(row + c) * (double)__ldg(x + c);
+    acc = warp_sum(acc);
+    if (lane == 0) z[r] = acc;
+}
+
+// ------------------------------------------------------------------ sources
+template <typename T>
+struct Gen {
+    const double* z;   // global source
+    const double* zs;  // toeplitz coefficients in shared memory
+    const T* prev;
+    T beta;
+    int mode, side, center, L;
+    __device__ __forceinline__ T y(int64_t e) const {
+        if (mode == SRC_BUF64) return (T)z[e];
+        if (mode == SRC_BUFT) return reinterpret_cast<const T*>(z)[e];
+        const int a = (int)(e / side);
+        const int b = (int)(e - (int64_t)a * side);
+        const int u = b - a + center;
+        return (u >= 0 && u < L) ? (T)zs[u] : T(0);
+    }
+};
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+template <typename T>
+__global__ void k_src_write(const double* __restrict__ z, int mode, int side, int center, int L,
+                            T* __restrict__ y, int64_t len) {
+    Gen<T> g{z, z, nullptr, T(0), mode, side, center, L};
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * blockDim.x)
+        y[e] = g.y(e);
+}
+
+// ------------------------------------------------------------------ reorth pass
+template <typename T, int VEC>
+struct VecIO;
+template <>
+struct VecIO<float, 4> {
+    static __device__ __forceinline__ void load(const float* p, double* v) {
+        float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    }
+};
+template <>
+struct VecIO<double, 2> {
+    static __device__ __forceinline__ void load(const double* p, double* v) {
+        double2 q = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    }
+};
+template <typename T>
+struct VecIO<T, 1> {
+    static __device__ __forceinline__ void load(const T* p, double* v) { v[0] = (double)__ldg(p); }
+};
+
+// One pass over the basis.  smem: [L toeplitz] [m coef] [8 x (m+2) warp acc] [m+4 red]
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+k_reorth(const double* zsrc, int mode, int side, int center, int L,
+         const T* __restrict__ prev, const double* __restrict__ beta_p,
+         const T* __restrict__ S, int64_t ld, int m, const double* __restrict__ coefA,
+         const double* __restrict__ coefB, int dots, T* out,
+         const double* __restrict__ div_p, int64_t len, double* __restrict__ part,
+         double* __restrict__ red, unsigned* counter) {
+    extern __shared__ double sm[];
+    const int Ls = (mode == SRC_TOEP) ? L : 0;
+    double* zs = sm;
+    double* coef = zs + Ls;
+    double* accw = coef + m;            // [8][m+2]
+    double* fin = accw + 8 * (m + 2);   // [m+4]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int W = m + 2;
+    for (int i = threadIdx.x; i < Ls; i += blockDim.x) zs[i] = zsrc[i];
+    const bool proj = (coefA != nullptr) || (coefB != nullptr);
+    for (int i = threadIdx.x; i < m; i += blockDim.x)
+        coef[i] = (coefA ? coefA[i] : 0.0) + (coefB ? coefB[i] : 0.0);
+    for (int i = threadIdx.x; i < 8 * W; i += blockDim.x) accw[i] = 0.0;
+    __syncthreads();
+    Gen<T> g{zsrc, zs, prev, beta_p ? (T)(*beta_p) : T(0), mode, side, center, L};
+    const T tdiv = div_p ? (T)(*div_p) : T(1);
+
+    const int64_t tile_elems = 256 * VEC;
+    const int64_t ntiles = (len + tile_elems - 1) / tile_elems;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t e0 = tile * tile_elems + (int64_t)threadIdx.x * VEC;
+        const bool full = (e0 + VEC <= len);
+        double v[VEC];
+        double yy = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+            const int64_t e = e0 + q;
+            if (e < len) {
+                T yv = g.y(e);
+                T vv = prev ? sub_rn(yv, mul_rn(g.beta, prev[e])) : yv;
+                v[q] = (double)vv;
+                yy += (double)yv * (double)yv;
+            } else {
+                v[q] = 0.0;
+            }
+        }
+        if (proj) {
+#pragma unroll 4
+            for (int i = 0; i < m; ++i) {
+                double s[VEC];
+                const T* Si = S + (int64_t)i * ld + e0;
+                if (full) {
+                    VecIO<T, VEC>::load(Si, s);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) s[q] = (e0 + q < len) ? (double)Si[q] : 0.0;
+                }
+                const double c = coef[i];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) v[q] -= c * s[q];
+            }
+        }
+        if (dots) {
+#pragma unroll 4
+            for (int i = 0; i < m; ++i) {
+                double s[VEC];
+                const T* Si = S + (int64_t)i * ld + e0;
+                if (full) {
+                    VecIO<T, VEC>::load(Si, s);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) s[q] = (e0 + q < len) ? (double)Si[q] : 0.0;
+                }
+                double d = 0.0;
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) d += s[q] * v[q];
+                d = warp_sum(d);
+                if (lane == 0) accw[warp * W + i] += d;
+            }
+        }
+        double vv2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) vv2 += v[q] * v[q];
+        vv2 = warp_sum(vv2);
+        yy = warp_sum(yy);
+        if (lane == 0) {
+            accw[warp * W + m] += vv2;
+            accw[warp * W + m + 1] += yy;
+        }
+        if (out) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int64_t e = e0 + q;
+                if (e < len) out[e] = div_rn((T)v[q], tdiv);
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < W; j += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += accw[q * W + j];
+        part[(int64_t)blockIdx.x * W + j] = s;
+    }
+    if (last_block_ticket(counter, gridDim.x)) {
+        for (int j = warp; j < W; j += 8) {
+            double s = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(&part[(int64_t)b * W + j]);
+            s = warp_sum(s);
+            if (lane == 0) fin[j] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double h2 = 0.0;
+            if (dots)
+                for (int i = 0; i < m; ++i) h2 += fin[i] * fin[i];
+            fin[m + 2] = sqrt(fmax(fin[m] - h2, 0.0));
+            fin[m + 3] = sqrt(fin[m]);
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < m + 4; j += blockDim.x) red[j] = fin[j];
+    }
+}
+
+// ------------------------------------------------------------------ lift
+// out_c = sum_i W[i, c] S_i, 32 output columns per pass, fp64 accumulation.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, int cols, int c0,
+       T* __restrict__ out, int64_t ld_out, int64_t len) {
+    constexpr int CB = 32;
+    extern __shared__ double wsm[];  // [rows][CB]
+    const int nc = min(CB, cols - c0);
+    for (int i = threadIdx.x; i < rows * CB; i += blockDim.x) {
+        const int r = i / CB, c = i % CB;
+        wsm[i] = (c < nc) ? (double)W[(int64_t)r * cols + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double acc[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+        for (int i = 0; i < rows; ++i) {
+            const double s = (double)__ldg(S + (int64_t)i * ld + e);
+            const double* wr = wsm + i * CB;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[c] += s * wr[c];
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (c < nc) out[(int64_t)(c0 + c) * ld_out + e] = (T)acc[c];
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static void ra_geom(const kb_operator* op, int transpose, int& center_in, int& L_in,
+                    int& center_out, int& L_out, const void*& M) {
+    // forward: diag sums over r_out - r_in (centre cu, kh bins) -> z = K^T w (kw)
+    // transpose: diag sums over c_out - c_in (centre cv, kw bins) -> z = K w (kh)
+    const int cu = op->kh / 2, cv = op->kw / 2;
+    if (!transpose) {
+        center_in = cu; L_in = op->kh; center_out = cv; L_out = op->kw; M = op->k;
+    } else {
+        center_in = cv; L_in = op->kw; center_out = cu; L_out = op->kh; M = op->kt;
+    }
+}
+
+static int rb_for(int rows, int chunks, int target_blocks = 4 * kSMs) {
+    int nrb = target_blocks / (chunks > 0 ? chunks : 1);
+    if (nrb < 1) nrb = 1;
+    if (nrb > rows) nrb = rows > 0 ? rows : 1;
+    int rb = (int)cdiv(rows, nrb);
+    return rb < 1 ? 1 : rb;
+}
+
+void op_plan_size(const kb_operator* op, Sizer& s) {
+    if (op->kind == KB_OP_RA_ZERO) {
+        const int L = op->kh > op->kw ? op->kh : op->kw;
+        const int n = op->side;
+        const int nrb_max = 4 * kSMs;
+        s.take<double>((size_t)nrb_max * L + 2 * L);   // diag partials (upper bound)
+        s.take<double>(L);                              // w
+        s.take<double>((size_t)nrb_max * L + 2 * L);   // colsum partials
+        s.take<double>(L);                              // z
+        s.take<unsigned>(2 * 64 + 64);
+        (void)n;
+    } else {
+        const int64_t big = op->rows > op->cols ? op->rows : op->cols;
+        s.take<double>((size_t)(4 * kSMs) * big);       // colsum partials (upper bound)
+        s.take<double>(big);                            // z
+        s.take<unsigned>((size_t)cdiv(big, 128) + 64);
+    }
+}
+
+OpPlan op_plan_make(const kb_operator* op, Arena& a) {
+    OpPlan p;
+    p.op = op;
+    if (op->kind == KB_OP_RA_ZERO) {
+        const int L = op->kh > op->kw ? op->kh : op->kw;
+        const int nrb_max = 4 * kSMs;
+        p.part = a.take<double>((size_t)nrb_max * L + 2 * L);
+        p.w = a.take<double>(L);
+        (void)a.take<double>((size_t)nrb_max * L + 2 * L);
+        p.z = a.take<double>(L);
+        p.counters = a.take<unsigned>(2 * 64 + 64);
+        p.n_counters = 2 * 64 + 64;
+        p.z_len = L;
+    } else {
+        const int64_t big = op->rows > op->cols ? op->rows : op->cols;
+        p.part = a.take<double>((size_t)(4 * kSMs) * big);
+        p.z = a.take<double>(big);
+        p.counters = a.take<unsigned>((size_t)cdiv(big, 128) + 64);
+        p.n_counters = cdiv(big, 128) + 64;
+        p.z_len = big;
+    }
+    return p;
+}
+
+template <typename T>
+static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStream_t st) {
+    const kb_operator* op = p.op;
+    const T* x = static_cast<const T*>(xv);
+    Src s;
+    if (op->kind == KB_OP_RA_ZERO) {
+        int ci, Li, co, Lo;
+        const void* Mv;
+        ra_geom(op, transpose, ci, Li, co, Lo, Mv);
+        const int n = op->side;
+        // diagonal sums
+        const int chunks = (int)cdiv(Li, 256);
+        const int rb = rb_for(n, chunks);
+        const int nrb = (int)cdiv(n, rb);
+        dim3 g1(chunks, nrb);
+        k_diag_partial<T><<<g1, 256, 0, st>>>(x, n, ci, Li, rb, p.part, p.w, p.counters);
+        KB_LAUNCH_CHECK();
+        // z = M^T w with M = K (forward) or K^T (transpose): rows Li, cols Lo
+        const int cchunks = (int)cdiv(Lo, 128);
+        const int rb2 = rb_for(Li, cchunks);
+        const int nrb2 = (int)cdiv(Li, rb2);
+        dim3 g2(cchunks, nrb2);
+        KB_REQUIRE(chunks <= 64 && cchunks <= 64, "R(A): PSF support too large (%d x %d)", op->kh, op->kw);
+        k_colsum<T, double><<<g2, 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo, p.w, rb2,
+                                                p.part, p.z, p.counters + 64);
+        KB_LAUNCH_CHECK();
+        s.z = p.z;
+        s.mode = SRC_TOEP;
+        s.side = n;
+        s.center = co;
+        s.L = Lo;
+    } else {
+        const T* A = static_cast<const T*>(op->a);
+        if (!transpose) {
+            const int rows = (int)op->rows, cols = (int)op->cols;
+            k_rowdot<T><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, op->lda, rows, cols, x, p.z);
+            KB_LAUNCH_CHECK();
+        } else {
+            const int rows = (int)op->rows, cols = (int)op->cols;
+            const int cchunks = (int)cdiv(cols, 128);
+            const int rb = rb_for(rows, cchunks);
+            const int nrb = (int)cdiv(rows, rb);
+            dim3 g(cchunks, nrb);
+            k_colsum<T, T><<<g, 256, 0, st>>>(A, op->lda, rows, cols, x, rb, p.part, p.z,
+                                              p.counters);
+            KB_LAUNCH_CHECK();
+        }
+        s.z = p.z;
+        s.mode = SRC_BUF64;
+    }
+    return s;
+}
+
+Src op_source(const OpPlan& p, const void* x, int transpose, cudaStream_t st) {
+    return p.op->dtype == KB_F32 ? op_source_t<float>(p, x, transpose, st)
+                                 : op_source_t<double>(p, x, transpose, st);
+}
+
+void src_write(int dtype, const Src& s, void* y, int64_t len, cudaStream_t st) {
+    const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(len, 256), 8 * kSMs);
+    if (dtype == KB_F32)
+        k_src_write<float><<<blocks, 256, 0, st>>>(s.z, s.mode, s.side, s.center, s.L,
+                                                   static_cast<float*>(y), len);
+    else
+        k_src_write<double><<<blocks, 256, 0, st>>>(s.z, s.mode, s.side, s.center, s.L,
+                                                    static_cast<double*>(y), len);
+    KB_LAUNCH_CHECK();
+}
+
+static int reorth_blocks(int64_t len) {
+    const int64_t tiles = cdiv(len, 256 * 4);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * kSMs));
+}
+
+void reorth_ws_size(int64_t len, int max_m, Sizer& s) {
+    s.take<double>((size_t)reorth_blocks(len) * (max_m + 2) + 64);
+    s.take<unsigned>(64);
+}
+
+ReorthWs reorth_ws_make(int64_t len, int max_m, Arena& a) {
+    ReorthWs w;
+    w.max_blocks = reorth_blocks(len);
+    w.max_m = max_m;
+    w.part = a.take<double>((size_t)w.max_blocks * (max_m + 2) + 64);
+    w.counter = a.take<unsigned>(64);
+    return w;
+}
+
+template <typename T, int VEC>
+static void launch_reorth(const Src& src, const void* S, int64_t ld, int m, const double* cA,
+                          const double* cB, bool dots, void* out, const double* div, int64_t len,
+                          double* red, const ReorthWs& ws, cudaStream_t st) {
+    const int Ls = (src.mode == SRC_TOEP) ? src.L : 0;
+    const size_t smem = sizeof(double) * ((size_t)Ls + m + 8 * (m + 2) + (m + 4));
+    auto kern = k_reorth<T, VEC>;
+    static bool configured = false;
+    if (!configured) {
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+    const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC)));
+    kern<<<blocks, 256, smem, st>>>(src.z, src.mode, src.side, src.center, src.L,
+                                    static_cast<const T*>(src.prev), src.beta,
+                                    static_cast<const T*>(S), ld, m, cA, cB, dots ? 1 : 0,
+                                    static_cast<T*>(out), div, len, ws.part, red, ws.counter);
+    KB_LAUNCH_CHECK();
+}
+
+void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, int m, const double* coefA,
+                 const double* coefB, bool dots, void* out, const double* div, int64_t len,
+                 double* red, const ReorthWs& ws, cudaStream_t st) {
+    KB_REQUIRE(m <= ws.max_m, "reorth: basis size %d exceeds workspace capacity %d", m, ws.max_m);
+    auto aligned = [](const void* p, size_t a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+    if (dtype == KB_F32) {
+        const bool v4 = (ld % 4 == 0) && (len % 4 == 0) && aligned(S, 16);
+        if (v4)
+            launch_reorth<float, 4>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+        else
+            launch_reorth<float, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+    } else {
+        const bool v2 = (ld % 2 == 0) && (len % 2 == 0) && aligned(S, 16);
+        if (v2)
+            launch_reorth<double, 2>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+        else
+            launch_reorth<double, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+    }
+}
+
+void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* x,
+                  double* y, int transpose, double* part, unsigned* counters, cudaStream_t st) {
+    if (!transpose) {
+        k_rowdot<double><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, lda, (int)rows, (int)cols, x, y);
+    } else {
+        const int cchunks = (int)cdiv(cols, 128);
+        const int rb = rb_for((int)rows, cchunks);
+        dim3 g(cchunks, (unsigned)cdiv(rows, rb));
+        k_colsum<double, double><<<g, 256, 0, st>>>(A, lda, (int)rows, (int)cols, x, rb, part, y, counters);
+    }
+    KB_LAUNCH_CHECK();
+}
+
+void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, void* out,
+             int64_t ld_out, int64_t len, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)rows * 32;
+    KB_REQUIRE(rows <= 512, "lift: too many basis vectors (%d)", rows);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 4 * kSMs));
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+        if (dtype == KB_F32) {
+            KB_CUDA(cudaFuncSetAttribute(k_lift<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            k_lift<float><<<blocks, 256, smem, st>>>(static_cast<const float*>(S), ld, rows,
+                                                     static_cast<const float*>(W), cols, c0,
+                                                     static_cast<float*>(out), ld_out, len);
+        } else {
+            KB_CUDA(cudaFuncSetAttribute(k_lift<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            k_lift<double><<<blocks, 256, smem, st>>>(static_cast<const double*>(S), ld, rows,
+                                                      static_cast<const double*>(W), cols, c0,
+                                                      static_cast<double*>(out), ld_out, len);
+        }
+        KB_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace kb

@@ -1,0 +1,805 @@
+// Split-Bregman / CGLS hot loop in fp64 (sm_100a).
+//
+// Reference: cgls.py:50-116, regularizers.py:37-130, splitbregman.py:32-192,
+// kronop.py:58-84, metrics.py:28-57.  Each CGLS iteration is
+//     GEMM pair (A w)  -> fused pass F1 (stencil tail of z, |z|^2, |x|^2, |w|^2, mu)
+//                      -> fused pass F2 (x += mu w, r -= mu z)
+//     GEMM pair (A^T r)-> fused pass F3 (f += lam D^T r, |f|^2, |r|^2, delta)
+//                      -> fused pass F4 (w = f + delta w)
+// with every scalar (mu, delta, norms) computed on the device by the last
+// block of the producing pass, and ONE host read-back per iteration for the
+// reference's stop tests.  Reductions are deterministic (fixed grid, fixed
+// order).  Vector updates mirror the reference's rounding (no FMA contraction:
+// x + mu*w is two rounded ops, as numpy does).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kb_common.cuh"
+
+namespace kb {
+
+void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
+           int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
+           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st);
+
+// ------------------------------------------------------------ map-reduce core
+constexpr int MR_THREADS = 256;
+constexpr int MR_MAXR = 8;
+
+inline int mr_blocks(int64_t len) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, MR_THREADS * 4), 2 * kSMs));
+}
+
+// f(e, acc) for e in [0, len); R block-reduced sums -> out[0..R); post(out) on
+// one thread after the deterministic final reduction.
+template <int R, class F, class P>
+__global__ void __launch_bounds__(MR_THREADS)
+k_map_reduce(int64_t len, F f, P post, double* part, double* out, unsigned* counter) {
+    __shared__ double sw[MR_THREADS / 32][MR_MAXR];
+    __shared__ double fin[MR_MAXR];
+    if (f.skip()) return;  // uniform across the grid (device flag)
+    double acc[R > 0 ? R : 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)MR_THREADS + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * MR_THREADS)
+        f(e, acc);
+    if (R == 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double v = warp_sum(acc[r]);
+        if (lane == 0) sw[warp][r] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < R) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < MR_THREADS / 32; ++w) s += sw[w][threadIdx.x];
+        part[(int64_t)blockIdx.x * R + threadIdx.x] = s;
+    }
+    if (last_block_ticket(counter, gridDim.x)) {
+        if (warp < R) {
+            double s = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(&part[(int64_t)b * R + warp]);
+            s = warp_sum(s);
+            if (lane == 0) fin[warp] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int r = 0; r < R; ++r) out[r] = fin[r];
+            post(out);
+        }
+    }
+}
+
+struct NoPost {
+    __device__ void operator()(double*) const {}
+};
+
+// device scalar slots (one array per CGLS solve)
+enum Slot {
+    S_GAM = 0,     // tau_sq (f.f)
+    S_ZZ,          // z.z
+    S_MU,
+    S_XN,          // ||x|| before the update
+    S_STEP,        // mu * ||w||
+    S_FF,          // tau_next
+    S_DELTA,
+    S_RR,          // ||r||^2
+    S_STALL,       // 1 if z.z == 0 (skip remaining work)
+    S_NSLOTS
+};
+// reduction scratch after the slots: [red0..red7]
+constexpr int S_RED = 16;
+constexpr int S_TOTAL = 32;
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// halved first differences on the column-major n x n image (regularizers.py:37-62)
+__device__ __forceinline__ double dx_at(const double* x, int64_t e, int n) {  // e < n(n-1)
+    return dmul(0.5, dsub(x[e], x[e + n]));
+}
+__device__ __forceinline__ double dy_at(const double* x, int64_t e, int n) {  // e < n(n-1)
+    const int64_t c = e / (n - 1), r = e - c * (n - 1);
+    const int64_t i = c * n + r;
+    return dmul(0.5, dsub(x[i], x[i + 1]));
+}
+// (D_x^T w)[e]: out[:, :-1] += .5 W ; out[:, 1:] -= .5 W  with W n x (n-1)
+__device__ __forceinline__ double dxt_at(const double* w, int64_t e, int n) {
+    const int64_t P = (int64_t)n * (n - 1);
+    double v = 0.0;
+    if (e < P) v = dadd(v, dmul(0.5, w[e]));
+    if (e >= n) v = dsub(v, dmul(0.5, w[e - n]));
+    return v;
+}
+// (D_y^T w)[e]: out[:-1, :] += .5 W ; out[1:, :] -= .5 W  with W (n-1) x n
+__device__ __forceinline__ double dyt_at(const double* w, int64_t e, int n) {
+    const int64_t c = e / n, r = e - c * n;
+    double v = 0.0;
+    if (r < n - 1) v = dadd(v, dmul(0.5, w[c * (n - 1) + r]));
+    if (r >= 1) v = dsub(v, dmul(0.5, w[c * (n - 1) + r - 1]));
+    return v;
+}
+
+// ------------------------------------------------------------ CGLS passes
+struct F1 {  // z tail, |z|^2, |x|^2, |w|^2
+    const double* w; const double* x; double* z;
+    int64_t m, ncols, P; int n; double lx, ly; const double* scal;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double* acc) const {
+        if (e < m) { const double v = z[e]; acc[0] += v * v; }
+        else if (e < m + P) { const double v = dmul(lx, dx_at(w, e - m, n)); z[e] = v; acc[0] += v * v; }
+        else if (e < m + 2 * P) { const double v = dmul(ly, dy_at(w, e - m - P, n)); z[e] = v; acc[0] += v * v; }
+        if (e < ncols) { acc[1] += x[e] * x[e]; acc[2] += w[e] * w[e]; }
+    }
+};
+struct F1Post {
+    double* scal;
+    __device__ void operator()(double* r) const {
+        scal[S_ZZ] = r[0];
+        if (r[0] == 0.0) { scal[S_STALL] = 1.0; scal[S_MU] = 0.0; return; }
+        const double mu = scal[S_GAM] / r[0];
+        scal[S_MU] = mu;
+        scal[S_XN] = sqrt(r[1]);
+        scal[S_STEP] = mu * sqrt(r[2]);
+    }
+};
+struct F2 {  // x += mu w ; r -= mu z
+    double* x; const double* w; double* r; const double* z; int64_t ncols, T; const double* scal;
+    __device__ bool skip() const { return scal[S_STALL] != 0.0; }
+    __device__ void operator()(int64_t e, double*) const {
+        const double mu = scal[S_MU];
+        if (e < ncols) x[e] = dadd(x[e], dmul(mu, w[e]));
+        if (e < T) r[e] = dsub(r[e], dmul(mu, z[e]));
+    }
+};
+struct F3 {  // f = (f + lx Dx^T r2) + ly Dy^T r3 ; |f|^2 ; |r|^2
+    double* f; const double* r; int64_t m, ncols, T, P; int n; double lx, ly; int aug; const double* scal;
+    __device__ bool skip() const { return scal[S_STALL] != 0.0; }
+    __device__ void operator()(int64_t e, double* acc) const {
+        if (e < ncols) {
+            double v = f[e];
+            if (aug) {
+                v = dadd(v, dmul(lx, dxt_at(r + m, e, n)));
+                v = dadd(v, dmul(ly, dyt_at(r + m + P, e, n)));
+                f[e] = v;
+            }
+            acc[0] += v * v;
+        }
+        if (e < T) acc[1] += r[e] * r[e];
+    }
+};
+struct F3Post {
+    double* scal;
+    __device__ void operator()(double* r) const {
+        scal[S_FF] = r[0];
+        scal[S_RR] = r[1];
+        scal[S_DELTA] = r[0] / scal[S_GAM];
+        scal[S_GAM] = r[0];
+    }
+};
+struct F4 {  // w = f + delta w
+    double* w; const double* f; int64_t ncols; const double* scal;
+    __device__ bool skip() const { return scal[S_STALL] != 0.0; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e < ncols) w[e] = dadd(f[e], dmul(scal[S_DELTA], w[e]));
+    }
+};
+struct FInit {  // f f  and |r|^2 at start; w = f
+    double* w; const double* f; const double* r; int64_t ncols, T;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double* acc) const {
+        if (e < ncols) { const double v = f[e]; w[e] = v; acc[0] += v * v; }
+        if (e < T) acc[1] += r[e] * r[e];
+    }
+};
+struct FInitPost {
+    double* scal;
+    __device__ void operator()(double* r) const {
+        scal[S_GAM] = r[0];
+        scal[S_RR] = r[1];
+        scal[S_STALL] = 0.0;
+    }
+};
+struct FTail {  // y[m..] = lam D x (augmented forward tail)
+    const double* x; double* y; int64_t m, P; int n; double lx, ly;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e < P) y[m + e] = dmul(lx, dx_at(x, e, n));
+        else if (e < 2 * P) y[m + e] = dmul(ly, dy_at(x, e - P, n));
+    }
+};
+struct FTailT {  // out = (out + lx Dx^T y2) + ly Dy^T y3
+    double* out; const double* y; int64_t m, P, ncols; int n; double lx, ly;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e < ncols) {
+            double v = out[e];
+            v = dadd(v, dmul(lx, dxt_at(y + m, e, n)));
+            v = dadd(v, dmul(ly, dyt_at(y + m + P, e, n)));
+            out[e] = v;
+        }
+    }
+};
+struct FSub {  // r = b - r  (warm start residual)
+    double* r; const double* b; int64_t T;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const { if (e < T) r[e] = dsub(b[e], r[e]); }
+};
+struct FCopy {
+    double* dst; const double* src; int64_t len;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const { if (e < len) dst[e] = src[e]; }
+};
+struct FZero {
+    double* dst; int64_t len;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const { if (e < len) dst[e] = 0.0; }
+};
+
+// ------------------------------------------------------------ SB passes
+__device__ __forceinline__ double shrink1(double w, double v) {
+    // np.sign(w) * np.maximum(np.abs(w) - v, 0.0)   (splitbregman.py:32-35)
+    const double s = (w > 0.0) ? 1.0 : ((w < 0.0) ? -1.0 : (w == 0.0 ? 0.0 : w));
+    return dmul(s, fmax(dsub(fabs(w), v), 0.0));
+}
+struct FRhs {  // rhs = [b; lam (dx - gx); lam (dy - gy)]   (regularizers.py:120-130)
+    double* rhs; const double* b; const double* ddx; const double* ddy; const double* gx;
+    const double* gy; int64_t N, P; double lam;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e < N) rhs[e] = b[e];
+        else if (e < N + P) rhs[e] = dmul(lam, dsub(ddx[e - N], gx[e - N]));
+        else if (e < N + 2 * P) rhs[e] = dmul(lam, dsub(ddy[e - N - P], gy[e - N - P]));
+    }
+};
+struct FSbUpd {  // c = Dx + g; d = shrink(c); g = c - d; norms for rc/re
+    const double* x; const double* xprev; const double* xtrue; double* ddx; double* ddy;
+    double* gx; double* gy; int64_t N, P; int n; double inv_gamma; int iso;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double* acc) const {
+        if (e < P) {
+            const double cx = dadd(dx_at(x, e, n), gx[e]);
+            const double cy = dadd(dy_at(x, e, n), gy[e]);
+            double dxv, dyv;
+            if (!iso) {
+                dxv = shrink1(cx, inv_gamma);
+                dyv = shrink1(cy, inv_gamma);
+            } else {
+                // splitbregman.py:43-56 (pairs cx[e] with cy[e] by flat index)
+                const double s = hypot(cx, cy);
+                double sc = 0.0;
+                if (s > 0.0) sc = fmax(dsub(s, inv_gamma), 0.0) / s;
+                dxv = dmul(cx, sc);
+                dyv = dmul(cy, sc);
+            }
+            ddx[e] = dxv; ddy[e] = dyv;
+            gx[e] = dsub(cx, dxv); gy[e] = dsub(cy, dyv);
+        }
+        if (e < N) {
+            const double d = dsub(x[e], xprev[e]);
+            acc[0] += d * d;
+            acc[1] += xprev[e] * xprev[e];
+            if (xtrue) { const double t = dsub(x[e], xtrue[e]); acc[2] += t * t; }
+        }
+    }
+};
+struct FNorm2 {  // |a - b|^2 and |b|^2
+    const double* a; const double* b; int64_t len;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double* acc) const {
+        if (e < len) { const double d = dsub(a[e], b[e]); acc[0] += d * d; acc[1] += b[e] * b[e]; }
+    }
+};
+
+// ------------------------------------------------------------ host helpers
+struct MR {
+    double* part;
+    unsigned* counter;
+};
+template <int R, class F, class P = NoPost>
+static void map_reduce(int64_t len, const F& f, const MR& mr, double* out, cudaStream_t st,
+                       const P& post = P()) {
+    const int blocks = mr_blocks(len);
+    k_map_reduce<R, F, P><<<blocks, MR_THREADS, 0, st>>>(len, f, post, mr.part, out, mr.counter);
+    KB_LAUNCH_CHECK();
+}
+
+// ---- Kronecker apply (two DMMA GEMMs) ----
+size_t kron_ws_doubles(const kb_kron* kr) {
+    const int64_t a = (int64_t)kr->n1 * kr->m2, b = (int64_t)kr->m1 * kr->n2;
+    return (size_t)kr->k * (size_t)std::max(a, b);
+}
+
+void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, double* tmp,
+                cudaStream_t st) {
+    const int m1 = kr->m1, m2 = kr->m2, n1 = kr->n1, n2 = kr->n2, k = kr->k;
+    if (!transpose) {
+        // P_i = Xr G_i            (n1 x m2), Xr = x as n1 x n2, G_i n2 x m2
+        dgemm(0, 0, n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
+              (int64_t)n1 * m2, k, 1, 0.0, st);
+        // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1
+        dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
+              0, 1, k, 0.0, st);
+    } else {
+        // Q_i = Yr G_i^T          (m1 x n2), Yr = y as m1 x m2
+        dgemm(0, 1, m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
+              (int64_t)m1 * n2, k, 1, 0.0, st);
+        // Xr = sum_i F_i Q_i      (n1 x n2)
+        dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
+              0, 1, k, 0.0, st);
+    }
+}
+
+// ---- generic forward (dense / kron, optionally augmented) ----
+struct FwdWs {
+    double* tmp = nullptr;   // kron intermediate
+    MR mr{};
+    double* part = nullptr;
+    int64_t n_counters = 0;
+};
+
+static size_t fwd_tmp_doubles(const kb_forward* fw) {
+    return fw->kind == KB_FWD_KRON ? kron_ws_doubles(&fw->kron) : 0;
+}
+
+void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* x,
+                  double* y, int transpose, double* part, unsigned* counters, cudaStream_t st);
+
+static void forward_top(const kb_forward* fw, const double* x, double* y, int transpose,
+                        const FwdWs& ws, cudaStream_t st) {
+    if (fw->kind == KB_FWD_KRON)
+        kron_apply(&fw->kron, x, y, transpose, ws.tmp, st);
+    else
+        dense_gemv64(fw->a, fw->lda, fw->m, fw->n, x, y, transpose, ws.part, ws.mr.counter + 8, st);
+}
+
+static void forward_apply(const kb_forward* fw, const double* x, double* y, int transpose,
+                          const FwdWs& ws, cudaStream_t st) {
+    forward_top(fw, x, y, transpose, ws, st);
+    if (!fw->augmented) return;
+    const int n = fw->side;
+    const int64_t P = (int64_t)n * (n - 1);
+    if (!transpose) {
+        FTail f{x, y, fw->m, P, n, fw->lam_x, fw->lam_y};
+        map_reduce<0>(2 * P, f, ws.mr, nullptr, st);
+    } else {
+        FTailT f{y, x, fw->m, P, fw->n, n, fw->lam_x, fw->lam_y};
+        map_reduce<0>(fw->n, f, ws.mr, nullptr, st);
+    }
+}
+
+static int64_t fwd_rows(const kb_forward* fw) {
+    const int64_t P = fw->augmented ? (int64_t)fw->side * (fw->side - 1) : 0;
+    return fw->m + 2 * P;
+}
+
+static void fwd_ws_size(const kb_forward* fw, Sizer& s) {
+    s.take<double>(fwd_tmp_doubles(fw) + 1);
+    const int64_t big = std::max<int64_t>(fwd_rows(fw), fw->n);
+    s.take<double>((size_t)(4 * kSMs) * std::max<int64_t>(fw->m, fw->n) + 64);  // gemv partials
+    s.take<double>((size_t)mr_blocks(big) * MR_MAXR + 64);
+    s.take<unsigned>(64 + (size_t)cdiv(std::max<int64_t>(fw->m, fw->n), 128) + 64);
+}
+
+static FwdWs fwd_ws_make(const kb_forward* fw, Arena& a) {
+    FwdWs w;
+    w.tmp = a.take<double>(fwd_tmp_doubles(fw) + 1);
+    const int64_t big = std::max<int64_t>(fwd_rows(fw), fw->n);
+    w.part = a.take<double>((size_t)(4 * kSMs) * std::max<int64_t>(fw->m, fw->n) + 64);
+    w.mr.part = a.take<double>((size_t)mr_blocks(big) * MR_MAXR + 64);
+    w.n_counters = 64 + cdiv(std::max<int64_t>(fw->m, fw->n), 128) + 64;
+    w.mr.counter = a.take<unsigned>((size_t)w.n_counters);
+    return w;
+}
+
+static void validate_fw(const kb_forward* fw) {
+    KB_REQUIRE(fw != nullptr, "null forward operator");
+    KB_REQUIRE(fw->m >= 1 && fw->n >= 1, "forward operator has empty shape");
+    if (fw->kind == KB_FWD_KRON) {
+        const kb_kron& k = fw->kron;
+        KB_REQUIRE(k.k >= 1 && k.m1 >= 1 && k.m2 >= 1 && k.n1 >= 1 && k.n2 >= 1, "bad Kronecker sizes");
+        KB_REQUIRE((int64_t)k.m1 * k.m2 == fw->m && (int64_t)k.n1 * k.n2 == fw->n,
+                   "Kronecker scheme does not match the operator shape");
+    } else {
+        KB_REQUIRE(fw->kind == KB_FWD_DENSE, "unknown forward kind %d", fw->kind);
+        KB_REQUIRE(fw->a != nullptr && fw->lda >= fw->n, "bad dense operator");
+    }
+    if (fw->augmented) {
+        KB_REQUIRE(fw->side >= 2 && (int64_t)fw->side * fw->side == fw->n,
+                   "augmented system needs n^2 columns with n >= 2");
+    }
+}
+
+// ------------------------------------------------------------ CGLS driver
+struct CglsWs {
+    FwdWs f;
+    double *r, *z, *w, *fv, *scal;
+    double* scal_host;   // pinned
+};
+
+static void cgls_ws_size(const kb_forward* fw, Sizer& s) {
+    fwd_ws_size(fw, s);
+    const int64_t T = fwd_rows(fw), N = fw->n;
+    s.take<double>(T);
+    s.take<double>(T);
+    s.take<double>(N);
+    s.take<double>(N);
+    s.take<double>(S_TOTAL);
+}
+
+static CglsWs cgls_ws_make(const kb_forward* fw, Arena& a) {
+    CglsWs w;
+    w.f = fwd_ws_make(fw, a);
+    const int64_t T = fwd_rows(fw), N = fw->n;
+    w.r = a.take<double>(T);
+    w.z = a.take<double>(T);
+    w.w = a.take<double>(N);
+    w.fv = a.take<double>(N);
+    w.scal = a.take<double>(S_TOTAL);
+    w.scal_host = nullptr;
+    return w;
+}
+
+struct PinnedScalars {
+    double* p = nullptr;
+    PinnedScalars() { KB_CUDA(cudaMallocHost(&p, sizeof(double) * S_TOTAL)); }
+    ~PinnedScalars() { if (p) cudaFreeHost(p); }
+};
+
+// Runs CGLS; returns stop code.  x0 may alias x (warm start) or be null.
+static void cgls_core(const kb_forward* fw, const double* b, const double* x0, double* x,
+                      kb_cgls_state* st, CglsWs& w, double* hs, cudaStream_t s) {
+    const int64_t T = fwd_rows(fw), N = fw->n;
+    const int64_t big = std::max(T, N);
+    // x, r
+    if (x0 == nullptr) {
+        map_reduce<0>(N, FZero{x, N}, w.f.mr, nullptr, s);
+        map_reduce<0>(T, FCopy{w.r, b, T}, w.f.mr, nullptr, s);
+    } else {
+        if (x0 != x) map_reduce<0>(N, FCopy{x, x0, N}, w.f.mr, nullptr, s);
+        forward_apply(fw, x, w.r, 0, w.f, s);
+        map_reduce<0>(T, FSub{w.r, b, T}, w.f.mr, nullptr, s);
+    }
+    forward_apply(fw, w.r, w.fv, 1, w.f, s);
+    map_reduce<2>(big, FInit{w.w, w.fv, w.r, N, T}, w.f.mr, w.scal + S_RED, s, FInitPost{w.scal});
+    KB_CUDA(cudaMemcpyAsync(hs, w.scal, sizeof(double) * S_TOTAL, cudaMemcpyDeviceToHost, s));
+    KB_CUDA(cudaStreamSynchronize(s));
+    st->n_res = 0;
+    st->n_rc = 0;
+    if (st->resnorm_host) st->resnorm_host[st->n_res] = std::sqrt(hs[S_RR]);
+    st->n_res++;
+    st->iters = 0;
+    st->stop = KB_CGLS_MAX_ITER;
+    const int64_t P = fw->augmented ? (int64_t)fw->side * (fw->side - 1) : 0;
+    const int aug = fw->augmented;
+    for (int it = 0; it < st->i_max; ++it) {
+        forward_top(fw, w.w, w.z, 0, w.f, s);
+        map_reduce<3>(big, F1{w.w, x, w.z, fw->m, N, aug ? P : 0, fw->side, fw->lam_x, fw->lam_y, w.scal},
+                      w.f.mr, w.scal + S_RED, s, F1Post{w.scal});
+        map_reduce<0>(big, F2{x, w.w, w.r, w.z, N, T, w.scal}, w.f.mr, nullptr, s);
+        forward_top(fw, w.r, w.fv, 1, w.f, s);
+        map_reduce<2>(big, F3{w.fv, w.r, fw->m, N, T, P, fw->side, fw->lam_x, fw->lam_y, aug, w.scal},
+                      w.f.mr, w.scal + S_RED, s, F3Post{w.scal});
+        map_reduce<0>(N, F4{w.w, w.fv, N, w.scal}, w.f.mr, nullptr, s);
+        KB_CUDA(cudaMemcpyAsync(hs, w.scal, sizeof(double) * S_TOTAL, cudaMemcpyDeviceToHost, s));
+        KB_CUDA(cudaStreamSynchronize(s));
+        if (hs[S_STALL] != 0.0) {
+            st->stop = KB_CGLS_STALLED;
+            break;
+        }
+        if (!std::isfinite(hs[S_FF])) {
+            set_error("CGLS produced non-finite residual quantities");
+            throw Fail{KB_ENUMERICAL};
+        }
+        st->iters++;
+        if (st->resnorm_host) st->resnorm_host[st->n_res] = std::sqrt(hs[S_RR]);
+        st->n_res++;
+        if (it >= 1) {
+            const double xn = hs[S_XN];
+            const double rc = xn > 0 ? hs[S_STEP] / xn : INFINITY;
+            if (st->rc_host) st->rc_host[st->n_rc] = rc;
+            st->n_rc++;
+            if (rc < st->tau) {
+                st->stop = KB_CGLS_CONVERGED;
+                break;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ SB driver
+struct SbWs {
+    CglsWs c;
+    double *rhs, *ddx, *ddy, *gx, *gy, *xa, *xb, *red;
+};
+
+static void sb_ws_size(const kb_forward* aug, Sizer& s) {
+    cgls_ws_size(aug, s);
+    const int64_t T = fwd_rows(aug), N = aug->n, P = (int64_t)aug->side * (aug->side - 1);
+    s.take<double>(T);
+    for (int i = 0; i < 4; ++i) s.take<double>(P);
+    s.take<double>(N);
+    s.take<double>(N);
+    s.take<double>(16);
+}
+
+static SbWs sb_ws_make(const kb_forward* aug, Arena& a) {
+    SbWs w;
+    w.c = cgls_ws_make(aug, a);
+    const int64_t T = fwd_rows(aug), N = aug->n, P = (int64_t)aug->side * (aug->side - 1);
+    w.rhs = a.take<double>(T);
+    w.ddx = a.take<double>(P);
+    w.ddy = a.take<double>(P);
+    w.gx = a.take<double>(P);
+    w.gy = a.take<double>(P);
+    w.xa = a.take<double>(N);
+    w.xb = a.take<double>(N);
+    w.red = a.take<double>(16);
+    return w;
+}
+
+static kb_forward make_aug(const kb_forward* fw, double lam) {
+    kb_forward aug = *fw;
+    int64_t n = (int64_t)std::llround(std::sqrt((double)fw->n));
+    aug.augmented = 1;
+    aug.side = (int)n;
+    aug.lam_x = lam;
+    aug.lam_y = lam;
+    return aug;
+}
+
+}  // namespace kb
+
+// ================================================================ C ABI
+using namespace kb;
+
+extern "C" int kb_kron_workspace_bytes(const kb_kron* kr, size_t* bytes) {
+    try {
+        KB_REQUIRE(kr && bytes, "null argument");
+        Sizer s;
+        s.take<double>(kron_ws_doubles(kr));
+        *bytes = s.off;
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, void* ws,
+                             size_t ws_bytes, kb_stream_t stream) {
+    try {
+        KB_REQUIRE(kr && x && y, "null argument");
+        KB_REQUIRE(kr->k >= 1 && kr->m1 >= 1 && kr->m2 >= 1 && kr->n1 >= 1 && kr->n2 >= 1,
+                   "bad Kronecker sizes");
+        Arena a(ws, ws_bytes);
+        double* tmp = a.take<double>(kron_ws_doubles(kr));
+        kron_apply(kr, x, y, transpose, tmp, as_stream(stream));
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_dgemm(int trans_a, int trans_b, int m, int n, int k, const double* A, int64_t lda,
+                        int64_t sa_batch, int64_t sa_seg, const double* B, int64_t ldb,
+                        int64_t sb_batch, int64_t sb_seg, double* C, int64_t ldc, int64_t sc_batch,
+                        int nbatch, int nseg, double beta, kb_stream_t stream) {
+    try {
+        dgemm(trans_a, trans_b, m, n, k, A, lda, sa_batch, sa_seg, B, ldb, sb_batch, sb_seg, C, ldc,
+              sc_batch, nbatch, nseg, beta, as_stream(stream));
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_forward_workspace_bytes(const kb_forward* fw, size_t* bytes) {
+    try {
+        validate_fw(fw);
+        Sizer s;
+        fwd_ws_size(fw, s);
+        *bytes = s.off;
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_forward_apply(const kb_forward* fw, const double* x, double* y, int transpose,
+                                void* ws, size_t ws_bytes, kb_stream_t stream) {
+    try {
+        validate_fw(fw);
+        Arena a(ws, ws_bytes);
+        FwdWs w = fwd_ws_make(fw, a);
+        KB_CUDA(cudaMemsetAsync(w.mr.counter, 0, sizeof(unsigned) * w.n_counters, as_stream(stream)));
+        forward_apply(fw, x, y, transpose, w, as_stream(stream));
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_cgls_workspace_bytes(const kb_forward* fw, size_t* bytes) {
+    try {
+        validate_fw(fw);
+        Sizer s;
+        cgls_ws_size(fw, s);
+        *bytes = s.off;
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_cgls_run(const kb_forward* fw, const double* b, const double* x0, double* x,
+                           kb_cgls_state* st, void* ws, size_t ws_bytes, kb_stream_t stream) {
+    try {
+        validate_fw(fw);
+        KB_REQUIRE(st && b && x, "null argument");
+        KB_REQUIRE(st->i_max >= 1, "i_max must be >= 1");
+        KB_REQUIRE(st->tau >= 0, "tau must be >= 0");
+        Arena a(ws, ws_bytes);
+        CglsWs w = cgls_ws_make(fw, a);
+        cudaStream_t s = as_stream(stream);
+        KB_CUDA(cudaMemsetAsync(w.f.mr.counter, 0, sizeof(unsigned) * w.f.n_counters, s));
+        PinnedScalars hs;
+        cgls_core(fw, b, x0, x, st, w, hs.p, s);
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_sb_workspace_bytes(const kb_forward* fw, size_t* bytes) {
+    try {
+        validate_fw(fw);
+        kb_forward aug = make_aug(fw, 1.0);
+        validate_fw(&aug);
+        Sizer s;
+        sb_ws_size(&aug, s);
+        *bytes = s.off;
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_sb_run(const kb_forward* fw, const double* b, const double* x_true, double* x,
+                         kb_sb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream) {
+    try {
+        validate_fw(fw);
+        KB_REQUIRE(st && b && x, "null argument");
+        KB_REQUIRE(fw->m == fw->n, "operator must be square to start from the observed image");
+        KB_REQUIRE(!fw->augmented, "pass the plain forward operator to kb_sb_run");
+        KB_REQUIRE(st->lam > 0 && st->beta > 0, "lam and beta must be positive");
+        KB_REQUIRE(st->l_max >= 1 && st->i_max >= 1, "l_max and i_max must be >= 1");
+        const double lam = st->lam, gamma = lam * lam / st->beta;
+        kb_forward aug = make_aug(fw, lam);
+        validate_fw(&aug);
+        Arena a(ws, ws_bytes);
+        SbWs w = sb_ws_make(&aug, a);
+        cudaStream_t s = as_stream(stream);
+        KB_CUDA(cudaMemsetAsync(w.c.f.mr.counter, 0, sizeof(unsigned) * w.c.f.n_counters, s));
+        const int64_t N = aug.n, P = (int64_t)aug.side * (aug.side - 1), T = fwd_rows(&aug);
+        const int n = aug.side;
+        PinnedScalars hs;
+        // x_prev = b; d = g = 0  (splitbregman.py:158-162)
+        double* xprev = w.xa;
+        double* xcur = w.xb;
+        map_reduce<0>(N, FCopy{xprev, b, N}, w.c.f.mr, nullptr, s);
+        for (double* p : {w.ddx, w.ddy, w.gx, w.gy}) map_reduce<0>(P, FZero{p, P}, w.c.f.mr, nullptr, s);
+        double obs = 0.0, xt_norm = 1.0;
+        if (x_true) {
+            map_reduce<2>(N, FNorm2{b, x_true, N}, w.c.f.mr, w.red, s);
+            KB_CUDA(cudaMemcpyAsync(hs.p, w.red, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            obs = std::sqrt(hs.p[0]);
+            xt_norm = std::sqrt(hs.p[1]);
+            KB_REQUIRE(xt_norm != 0.0, "relative_error is undefined for a zero reference");
+        }
+        st->outer_iters = 0;
+        st->stop = KB_SB_MAX_ITER;
+        kb_cgls_state cs{};
+        cs.i_max = st->i_max;
+        cs.tau = st->tau_cgls;
+        for (int l = 0; l < st->l_max; ++l) {
+            map_reduce<0>(T, FRhs{w.rhs, b, w.ddx, w.ddy, w.gx, w.gy, N, P, lam}, w.c.f.mr, nullptr, s);
+            cgls_core(&aug, w.rhs, st->warm_start ? xprev : nullptr, xcur, &cs, w.c, hs.p, s);
+            map_reduce<3>(N, FSbUpd{xcur, xprev, x_true, w.ddx, w.ddy, w.gx, w.gy, N, P, n, 1.0 / gamma,
+                                    st->variant == KB_SB_ISOTROPIC},
+                          w.c.f.mr, w.red, s);
+            KB_CUDA(cudaMemcpyAsync(hs.p, w.red, sizeof(double) * 3, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            st->outer_iters++;
+            if (st->cgls_iters_host) st->cgls_iters_host[l] = cs.iters;
+            if (hs.p[1] == 0.0) {
+                set_error("relative_change is undefined for a zero previous iterate");
+                throw Fail{KB_EVALIDATION};
+            }
+            const double rc = std::sqrt(hs.p[0]) / std::sqrt(hs.p[1]);
+            if (st->rc_host) st->rc_host[l] = rc;
+            if (x_true) {
+                const double err = std::sqrt(hs.p[2]);
+                if (st->re_host) st->re_host[l] = err / xt_norm;
+                double isnr;
+                if (err == 0.0 && obs == 0.0) isnr = 0.0;
+                else if (err == 0.0) isnr = INFINITY;
+                else if (obs == 0.0) isnr = -INFINITY;
+                else isnr = 20.0 * std::log10(obs / err);
+                if (st->isnr_host) st->isnr_host[l] = isnr;
+            }
+            std::swap(xprev, xcur);
+            if (rc < st->tau) {
+                st->stop = KB_SB_CONVERGED;
+                break;
+            }
+        }
+        map_reduce<0>(N, FCopy{x, xprev, N}, w.c.f.mr, nullptr, s);
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+// ---------------------------------------------------------------- elementwise pieces
+namespace kb {
+struct FDiff {
+    const double* x; double* out; int n; int axis; int transpose; double scale; int accumulate; int64_t len;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e >= len) return;
+        double v;
+        if (!transpose) v = axis == 0 ? dx_at(x, e, n) : dy_at(x, e, n);
+        else v = axis == 0 ? dxt_at(x, e, n) : dyt_at(x, e, n);
+        v = dmul(scale, v);
+        out[e] = accumulate ? dadd(out[e], v) : v;
+    }
+};
+struct FShrink {
+    const double* cx; const double* cy; double* dx; double* dy; int64_t len; double inv_gamma; int iso;
+    __device__ bool skip() const { return false; }
+    __device__ void operator()(int64_t e, double*) const {
+        if (e >= len) return;
+        const double a = cx[e], b = cy[e];
+        if (!iso) { dx[e] = shrink1(a, inv_gamma); dy[e] = shrink1(b, inv_gamma); return; }
+        const double s = hypot(a, b);
+        double sc = 0.0;
+        if (s > 0.0) sc = fmax(dsub(s, inv_gamma), 0.0) / s;
+        dx[e] = dmul(a, sc);
+        dy[e] = dmul(b, sc);
+    }
+};
+}  // namespace kb
+
+extern "C" int kb_diff(const double* x, double* out, int side, int axis, int transpose, double scale,
+                       int accumulate, kb_stream_t stream) {
+    try {
+        KB_REQUIRE(x && out, "null argument");
+        KB_REQUIRE(side >= 2, "first differences need n >= 2");
+        const int64_t len = transpose ? (int64_t)side * side : (int64_t)side * (side - 1);
+        MR mr{nullptr, nullptr};
+        map_reduce<0>(len, FDiff{x, out, side, axis, transpose, scale, accumulate, len}, mr, nullptr,
+                      as_stream(stream));
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
+extern "C" int kb_shrink_update(const double* cx, const double* cy, double* dx, double* dy,
+                                int64_t len, double gamma, int variant, kb_stream_t stream) {
+    try {
+        KB_REQUIRE(gamma > 0, "gamma must be positive");
+        MR mr{nullptr, nullptr};
+        map_reduce<0>(len, FShrink{cx, cy, dx, dy, len, 1.0 / gamma, variant == KB_SB_ISOTROPIC}, mr,
+                      nullptr, as_stream(stream));
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}

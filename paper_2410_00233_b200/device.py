@@ -1,0 +1,94 @@
+"""Device plumbing: torch owns device memory and streams; the kernels are ours.
+
+Host numpy inputs (the reference's drop-in surface) are uploaded once; torch
+CUDA tensors are used in place.  Every product call runs on the current torch
+stream of ``cuda:0`` (or the tensor's device).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .exceptions import KronblurError, ValidationError
+
+_TORCH_OF = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+_NP_OF = {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64)}
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise KronblurError("no CUDA device: the kronblur_b200 path runs on B200 (sm_100a) only")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def torch_dtype(dt) -> torch.dtype:
+    try:
+        return _TORCH_OF[np.dtype(dt)]
+    except (KeyError, TypeError):
+        raise ValidationError(f"unsupported dtype {dt}; expected float32 or float64") from None
+
+
+def np_dtype(t: torch.Tensor) -> np.dtype:
+    return _NP_OF[t.dtype]
+
+
+def is_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+def to_device(x, dtype=None, contiguous=True) -> torch.Tensor:
+    """Host array / tensor -> contiguous CUDA tensor of ``dtype``."""
+    dev = device()
+    if isinstance(x, torch.Tensor):
+        t = x
+        if dtype is not None and t.dtype != torch_dtype(dtype):
+            t = t.to(torch_dtype(dtype))
+        if t.device != dev:
+            t = t.to(dev)
+    else:
+        a = np.asarray(x)
+        if dtype is not None:
+            a = a.astype(dtype, copy=False)
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
+    return t.contiguous() if contiguous else t
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def empty(shape, dtype) -> torch.Tensor:
+    return torch.empty(shape, dtype=torch_dtype(dtype), device=device())
+
+
+def zeros(shape, dtype) -> torch.Tensor:
+    return torch.zeros(shape, dtype=torch_dtype(dtype), device=device())
+
+
+class Workspace:
+    """Grow-only scratch buffer per device (zero-filled on growth)."""
+
+    def __init__(self):
+        self._buf: dict[int, torch.Tensor] = {}
+
+    def get(self, nbytes: int) -> tuple[int, int]:
+        dev = device()
+        key = dev.index or 0
+        buf = self._buf.get(key)
+        if buf is None or buf.numel() < nbytes:
+            size = max(int(nbytes), 1 << 20)
+            buf = torch.zeros(size, dtype=torch.uint8, device=dev)
+            self._buf[key] = buf
+        return buf.data_ptr(), buf.numel()
+
+
+WORKSPACE = Workspace()
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()

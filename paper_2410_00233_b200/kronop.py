@@ -1,0 +1,171 @@
+"""Sum-of-Kronecker-products operator with device-resident fp64 factors.
+
+Reference: pkg/src/kronblur/kronop.py.  ``apply`` computes
+``vec(sum_i ay_i X ax_i^T)`` and ``apply_t`` ``vec(sum_i ay_i^T Y ax_i)``
+(kronop.py:58-84) as two DMMA GEMMs each (kb_kron_apply): a batched stage
+``P_i = X_r G_i`` and a segment-reduced stage ``Y_r = sum_i F_i^T P_i`` with
+inner dimension k*n1, where F_i = ax_i^T and G_i = ay_i^T are stored as the
+column-major vectors the SVD produced (so ``assemble`` is a pure cast/scale).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .exceptions import ValidationError
+from .metrics import FlopCounter
+from .rearrange import BlockScheme
+
+MATERIALIZE_CAP = 2 ** 24
+
+
+def _forward_apply(fw, x, transpose: int, shape):
+    from . import device as D
+
+    host = not D.is_tensor(x)
+    want = shape[0] if transpose else shape[1]
+    if host:
+        arr = np.asarray(x, dtype=np.float64)
+        if arr.ndim == 2 and 1 in arr.shape:
+            arr = arr.ravel()
+        if arr.shape != (want,):
+            raise ValidationError(
+                f"{'apply_t' if transpose else 'apply'} expects a vector of length {want}, got {arr.shape}")
+        xd = D.to_device(arr)
+    else:
+        xd = D.to_device(x, np.float64).reshape(-1)
+        if xd.numel() != want:
+            raise ValidationError(f"expected a vector of length {want}, got {xd.numel()}")
+    rows_out = shape[1] if transpose else shape[0]
+    y = D.empty(rows_out, np.float64)
+    lib = _lib.load()
+    nb = C.c_size_t()
+    _lib.check(lib.kb_forward_workspace_bytes(C.byref(fw), C.byref(nb)))
+    ws, wsb = D.WORKSPACE.get(nb.value)
+    _lib.check(lib.kb_forward_apply(C.byref(fw), xd.data_ptr(), y.data_ptr(), transpose, ws, wsb,
+                                    D.stream_ptr()), "operator apply")
+    return D.to_host(y) if host else y
+
+
+class KroneckerSum:
+    """k-term Kronecker-product sum with double-precision factors (kronop.py:28-100)."""
+
+    def __init__(self, ax, ay, scheme: BlockScheme):
+        from . import device as D
+
+        if len(ax) != len(ay):
+            raise ValidationError("ax and ay must hold the same number of terms")
+        if len(ax) == 0:
+            raise ValidationError("KroneckerSum needs at least one term")
+        s = scheme
+        ax = [np.ascontiguousarray(a, dtype=np.float64) for a in ax]
+        ay = [np.ascontiguousarray(b, dtype=np.float64) for b in ay]
+        for i, (a, b) in enumerate(zip(ax, ay)):
+            if a.shape != (s.m1, s.n1):
+                raise ValidationError(f"ax[{i}] has shape {a.shape}, expected {(s.m1, s.n1)}")
+            if b.shape != (s.m2, s.n2):
+                raise ValidationError(f"ay[{i}] has shape {b.shape}, expected {(s.m2, s.n2)}")
+        self.scheme = s
+        self._ax, self._ay = ax, ay
+        f = np.stack([a.T.reshape(-1) for a in ax])   # F_i = ax_i^T  (n1 x m1 row-major)
+        g = np.stack([b.T.reshape(-1) for b in ay])   # G_i = ay_i^T  (n2 x m2 row-major)
+        self.f_dev = D.to_device(f)
+        self.g_dev = D.to_device(g)
+
+    @classmethod
+    def from_device(cls, f_dev, g_dev, scheme: BlockScheme) -> "KroneckerSum":
+        obj = cls.__new__(cls)
+        obj.scheme = scheme
+        obj._ax = obj._ay = None
+        obj.f_dev, obj.g_dev = f_dev, g_dev
+        return obj
+
+    @property
+    def ax(self) -> list:
+        if self._ax is None:
+            s = self.scheme
+            f = self.f_dev.detach().cpu().numpy()
+            self._ax = [np.ascontiguousarray(f[i].reshape(s.n1, s.m1).T) for i in range(f.shape[0])]
+        return self._ax
+
+    @property
+    def ay(self) -> list:
+        if self._ay is None:
+            s = self.scheme
+            g = self.g_dev.detach().cpu().numpy()
+            self._ay = [np.ascontiguousarray(g[i].reshape(s.n2, s.m2).T) for i in range(g.shape[0])]
+        return self._ay
+
+    @property
+    def k(self) -> int:
+        return int(self.f_dev.shape[0])
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.scheme.shape
+
+    def kron_struct(self) -> _lib.KbKron:
+        s = self.scheme
+        return _lib.KbKron(s.m1, s.m2, s.n1, s.n2, self.k, self.f_dev.data_ptr(), self.g_dev.data_ptr())
+
+    def forward_struct(self) -> _lib.KbForward:
+        fw = _lib.KbForward()
+        fw.kind = _lib.KB_FWD_KRON
+        fw.m, fw.n = self.shape
+        fw.a, fw.lda = None, 0
+        fw.kron = self.kron_struct()
+        return fw
+
+    def apply(self, x, counter: FlopCounter | None = None):
+        """A @ x for a vectorised image (kronop.py:58-70)."""
+        out = _forward_apply(self.forward_struct(), x, 0, self.shape)
+        if counter is not None:
+            s = self.scheme
+            counter.add_kp(s.m1, s.m2, s.n1, s.n2, self.k)
+        return out
+
+    def apply_t(self, y, counter: FlopCounter | None = None):
+        """A.T @ y (kronop.py:72-84)."""
+        out = _forward_apply(self.forward_struct(), y, 1, self.shape)
+        if counter is not None:
+            s = self.scheme
+            counter.add_kp_transpose(s.m1, s.m2, s.n1, s.n2, self.k)
+        return out
+
+    def materialize(self, cap: int = MATERIALIZE_CAP) -> np.ndarray:
+        """Dense sum_i kron(ax_i, ay_i) on the host (tests only, kronop.py:86-100)."""
+        m, n = self.shape
+        if m * n > cap:
+            raise ValidationError(f"materializing a {m}x{n} matrix ({m * n} entries) exceeds the cap {cap}")
+        out = np.zeros((m, n))
+        for a, b in zip(self.ax, self.ay):
+            out += np.kron(a, b)
+        return out
+
+
+def assemble(svd, scheme: BlockScheme) -> KroneckerSum:
+    """Truncated SVD of R(A) -> KroneckerSum (kronop.py:103-123).
+
+    ax_i = sigma_i unvec(u_i, m1, n1), ay_i = unvec(v_i, m2, n2), promoted to
+    fp64.  On the device this is one cast/scale kernel (kb_kron_assemble):
+    F_i = ax_i^T is exactly sigma_i * u_i as stored.
+    """
+    from . import device as D
+
+    m_u, m_v = svd.shape
+    if m_u != scheme.m1 * scheme.n1 or m_v != scheme.m2 * scheme.n2:
+        raise ValidationError(
+            f"SVD dimensions {m_u}x{m_v} do not match the rearranged shape {scheme.rearranged_shape}")
+    u, v = svd.u_device, svd.v_device
+    k = svd.k
+    f = D.empty((k, m_u), np.float64)
+    g = D.empty((k, m_v), np.float64)
+    sig = np.ascontiguousarray(svd.sigma.astype(np.float64))
+    code = _lib.KB_F32 if str(u.dtype) == "torch.float32" else _lib.KB_F64
+    _lib.check(_lib.load().kb_kron_assemble(code, u.data_ptr(), m_u, v.data_ptr(), m_v,
+                                            sig.ctypes.data_as(C.POINTER(C.c_double)), k, m_u, m_v,
+                                            f.data_ptr(), g.data_ptr(), D.stream_ptr()), "assemble")
+    return KroneckerSum.from_device(f, g, scheme)

@@ -1,0 +1,299 @@
+"""GPU parity of eGKB / RSVD / TSVD / CGLS / split Bregman against the
+reference's golden fixtures and the CPU oracle (SURVEY §8c protocol)."""
+
+import json
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import geometric_sigmas, load_golden, spectral_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kb():
+    import paper_2410_00233_b200 as kb
+
+    return kb
+
+
+def sigma_ok(got, ref, rel=1e-4, floor=2e-6):
+    """|s_gpu - s_cpu| <= 1e-4 s_i + eps_floor s_1."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return got.shape == ref.shape and bool(np.all(np.abs(got - ref) <= rel * ref + floor * ref[0]))
+
+
+def _cfg(kb, js):
+    return kb.EgkbConfig(**json.loads(str(js)))
+
+
+def _ocfg(cfg):
+    return SimpleNamespace(k_max=cfg.k_max, p=cfg.p, tau=cfg.tau, k_min=cfg.k_min, reorth=cfg.reorth,
+                           seed=cfg.seed, break_tol=cfg.break_tol, keep_basis=False)
+
+
+class TestEgkbGolden:
+    @pytest.mark.parametrize("tag,bkey,dtype", [
+        ("diag_", None, np.float64), ("rank5_", "rank5_b", np.float64), ("fact64_", "fact_b", np.float64),
+        ("fact32_", "fact_b", np.float32), ("decay_", "decay_b", np.float64),
+        ("decay32_", "decay_b", np.float32), ("accept3_", "accept3_b", np.float64),
+        ("accept3s_", "accept3_b", np.float32), ("y0_", "y0_b", np.float64),
+    ])
+    def test_dense_kats(self, kb, tag, bkey, dtype):
+        g = load_golden("egkb_kat")
+        b = (np.diag([5.0, 3.0, 1.0]) if bkey is None else g[bkey]).astype(dtype)
+        y0 = g["y0_y0"] if tag == "y0_" else None
+        svd, tr = kb.egkb(b, _cfg(kb, g[tag + "cfg"]), y0=y0)
+        assert tr.chosen_k == int(g[tag + "tr_chosen_k"])
+        assert tr.k_p == int(g[tag + "tr_k_p"])
+        assert tr.stop_reason == str(g[tag + "tr_stop_reason"])
+        assert tr.breakdown == bool(g[tag + "tr_breakdown"])
+        ref = g[tag + "sigma"]
+        assert svd.sigma.dtype == ref.dtype
+        if dtype == np.float64:
+            np.testing.assert_allclose(svd.sigma, ref, rtol=1e-10)
+        else:
+            assert sigma_ok(svd.sigma, ref)
+        # factors: compare the rank-k reconstruction (sign-free)
+        rec = (svd.u * svd.sigma) @ svd.v.T
+        rec_ref = (g[tag + "u"] * ref) @ g[tag + "v"].T
+        tol = 1e-9 if dtype == np.float64 else 1e-4
+        assert np.linalg.norm(rec - rec_ref) <= tol * np.linalg.norm(rec_ref)
+
+    def test_factorization_identity_and_orthogonality(self, kb, rng):
+        b = spectral_matrix(rng, 50, 40, geometric_sigmas(40, ratio=1.15))
+        for reorth in ("one-sided", "full"):
+            cfg = kb.EgkbConfig(k_max=12, p=2, tau=1e-30, k_min=12, reorth=reorth, keep_basis=True, seed=0)
+            _, tr = kb.egkb(b, cfg)
+            fact = np.linalg.norm(b @ tr.q_basis - tr.s_basis @ tr.c_mat) / np.linalg.norm(b)
+            assert fact < 1e-10
+            assert np.linalg.norm(tr.q_basis.T @ tr.q_basis - np.eye(tr.q_basis.shape[1])) < 1e-10
+        b32 = b.astype(np.float32)
+        _, tr = kb.egkb(b32, kb.EgkbConfig(k_max=12, p=2, tau=1e-30, k_min=12, keep_basis=True, seed=0))
+        assert tr.q_basis.dtype == np.float32
+        assert np.linalg.norm(tr.q_basis.T @ tr.q_basis - np.eye(tr.q_basis.shape[1])) < 1e-4
+        assert np.linalg.norm(tr.s_basis.T @ tr.s_basis - np.eye(tr.s_basis.shape[1])) < 1e-4
+
+    def test_errors(self, kb):
+        b = np.random.default_rng(0).standard_normal((20, 15))
+        with pytest.raises(kb.ValidationError):
+            kb.egkb(b, kb.EgkbConfig(k_max=3), y0=np.zeros(20))
+        with pytest.raises(kb.ValidationError):
+            kb.egkb(b, kb.EgkbConfig(k_max=3), y0=np.ones(7))
+        with pytest.raises(kb.NumericalError):
+            kb.egkb(np.zeros((5, 5)), kb.EgkbConfig(k_max=2))
+        with pytest.raises(kb.ValidationError):
+            kb.egkb(np.ones((4, 4), dtype=np.int32), kb.EgkbConfig(k_max=2))
+
+
+class TestEgkbBlur:
+    @pytest.mark.parametrize("name", ["n64", "n256"])
+    def test_small_blur_configs_vs_reference(self, kb, name):
+        g = load_golden("egkb_kat")
+        pre = f"blur_{name}_"
+        n = int(g[pre + "n"])
+        cfg = _cfg(kb, g[pre + "cfg"])
+        svd, tr = kb.egkb(kb.RearrangedBlur(g[pre + "psf"], n), cfg)
+        assert tr.chosen_k == int(g[pre + "tr_chosen_k"])
+        assert tr.k_p == int(g[pre + "tr_k_p"])
+        assert tr.stop_reason == str(g[pre + "tr_stop_reason"])
+        assert sigma_ok(svd.sigma, g[pre + "sigma"])
+
+    def test_config_n64_full_vs_reference(self, kb):
+        """configs[0] at full size: same rank/trace as the reference's dense fp32 run."""
+        from paper_2410_00233_b200 import datagen
+
+        g = load_golden("config_n64")
+        prob = datagen.make_problem("n64")
+        np.testing.assert_array_equal(prob.psf, g["psf"])
+        np.testing.assert_array_equal(prob.b, g["b"])
+        svd, tr = kb.egkb(kb.RearrangedBlur(prob.psf, 64), kb.EgkbConfig(**prob.egkb))
+        assert (tr.chosen_k, tr.k_p, tr.stop_reason) == (int(g["tr_chosen_k"]), int(g["tr_k_p"]),
+                                                         str(g["tr_stop_reason"]))
+        assert sigma_ok(svd.sigma, g["sigma"], floor=5e-6)
+        np.testing.assert_allclose(tr.alphas[:5], g["tr_alphas"][:5], rtol=1e-5)
+        # well-separated factors, sign-aligned
+        for i in range(svd.k):
+            if g["sigma"][i] < 1e-3 * g["sigma"][0]:
+                break
+            a, b = svd.u[:, i].astype(np.float64), g["u"][:, i].astype(np.float64)
+            assert min(np.linalg.norm(a - b), np.linalg.norm(a + b)) < 1e-3
+        svd_a, tr_a = kb.egkb(kb.RearrangedBlur(prob.psf, 64), kb.EgkbConfig(k_max=20))
+        assert tr_a.chosen_k == int(g["auto_chosen"]) and tr_a.stop_reason == str(g["auto_reason"])
+        assert sigma_ok(svd_a.sigma, g["auto_sigma"], floor=5e-6)
+
+    @pytest.mark.parametrize("n,name", [(256, "n256"), (512, "n512")])
+    def test_large_blur_vs_oracle_restatement(self, kb, n, name):
+        from oracle import lowrank as olr
+        from oracle import structured as ost
+        from paper_2410_00233_b200 import datagen
+
+        psf = datagen.mixture_psf(n)
+        cfg = kb.EgkbConfig(**datagen.CONFIGS[name]["egkb"])
+        svd, tr = kb.egkb(kb.RearrangedBlur(psf, n), cfg)
+        k32 = psf.astype(np.float32)
+        (_, os_, _), otr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda s: ost.ra_rmatvec(k32, n, s),
+                                    (n * n, n * n), np.float32, _ocfg(cfg))
+        assert (tr.chosen_k, tr.k_p, tr.stop_reason) == (otr.chosen_k, otr.k_p, otr.stop_reason)
+        # exact structured sigma (fp64) as ground truth for the leading values
+        _, s_exact, _ = ost.structured_tsvd(psf, n, k=svd.k)
+        lead = s_exact >= 1e-3 * s_exact[0]
+        assert np.all(np.abs(svd.sigma[lead] - s_exact[lead]) <= 1e-4 * s_exact[lead])
+        assert sigma_ok(svd.sigma, os_, floor=5e-6)
+
+
+class TestRsvdTsvd:
+    def test_rsvd_golden(self, kb):
+        g = load_golden("rsvd_kat")
+        svd = kb.rsvd(g["sig_b"], kb.RsvdConfig(k=5, p=8, q=2, seed=2))
+        np.testing.assert_allclose(svd.sigma, g["sigd_sigma"], rtol=1e-10)
+        svd32 = kb.rsvd(g["sig_b"].astype(np.float32), kb.RsvdConfig(k=5, p=8, q=2, seed=2))
+        assert svd32.sigma.dtype == np.float32
+        assert sigma_ok(svd32.sigma, g["sigs_sigma"])
+        svd_w = kb.rsvd(g["wide_b"], kb.RsvdConfig(k=4, p=6, q=2, seed=3))
+        assert svd_w.u.shape == (30, 4) and svd_w.v.shape == (80, 4)
+        np.testing.assert_allclose(svd_w.sigma, g["wide_sigma"], rtol=1e-10)
+        with pytest.raises(kb.RankDeficiencyError) as err:
+            kb.rsvd(g["rankdef_b"], kb.RsvdConfig(k=4, p=2, q=1, seed=5))
+        assert abs(err.value.column - int(g["rankdef_col"])) <= 2
+
+    def test_rsvd_structured_small(self, kb):
+        from oracle import structured as ost
+        from paper_2410_00233_b200 import datagen
+
+        n = 128
+        psf = datagen.mixture_psf(n)
+        svd = kb.rsvd(kb.RearrangedBlur(psf, n, dtype=np.float64), kb.RsvdConfig(k=6, p=4, q=2))
+        _, s_exact, _ = ost.structured_tsvd(psf, n, k=6)
+        np.testing.assert_allclose(svd.sigma, s_exact, rtol=1e-8)
+
+    def test_tsvd_structured(self, kb):
+        from oracle import structured as ost
+
+        g = load_golden("ra_structured")
+        k, n = g["c2_psf"], int(g["c2_n"])
+        svd = kb.tsvd(kb.RearrangedBlur(k, n, dtype=np.float64), 6)
+        np.testing.assert_allclose(svd.sigma, g["c2_sigma"][:6], rtol=1e-12)
+        u, s, v = ost.structured_tsvd(k, n, k=6)
+        np.testing.assert_allclose((svd.u * svd.sigma) @ svd.v.T, (u * s) @ v.T, atol=1e-12)
+
+
+class TestCgls:
+    def test_golden(self, kb):
+        g = load_golden("cgls_kat")
+        for i in range(4):
+            tau = 1e-6 if i % 2 else 0.0
+            res = kb.cgls_solve(g[f"c{i}_a"], g[f"c{i}_b"], kb.CglsConfig(i_max=40, tau=tau))
+            assert res.iters == int(g[f"c{i}_iters"]) and res.stop == str(g[f"c{i}_stop"])
+            np.testing.assert_allclose(res.x, g[f"c{i}_x"], rtol=1e-11, atol=1e-12)
+            np.testing.assert_allclose(res.rc_history, g[f"c{i}_rc"], rtol=1e-7)
+
+    def test_stall_and_warm_start(self, kb, rng):
+        a = rng.standard_normal((10, 5))
+        res = kb.cgls_solve(a, np.zeros(10), kb.CglsConfig(i_max=10))
+        assert res.stop == "stalled" and not res.x.any()
+        a = rng.standard_normal((30, 10))
+        b = rng.standard_normal(30)
+        first = kb.cgls_solve(a, b, kb.CglsConfig(i_max=3, tau=0.0))
+        second = kb.cgls_solve(a, b, kb.CglsConfig(i_max=40, tau=0.0), x0=first.x)
+        x_ref = np.linalg.solve(a.T @ a, a.T @ b)
+        assert np.linalg.norm(second.x - x_ref) / np.linalg.norm(x_ref) < 1e-10
+
+    def test_non_finite_raises(self, kb):
+        a = np.array([[1e300, 0.0], [0.0, 1e300], [1e300, 1e300]])
+        with pytest.raises(kb.NumericalError):
+            kb.cgls_solve(a, np.full(3, 1e300), kb.CglsConfig(i_max=10, tau=0.0))
+
+
+class TestSplitBregman:
+    def test_interchange_case(self, kb):
+        g = load_golden("sb_kat")
+        n = 8
+        cfg = kb.SbConfig(lam=0.1, beta=0.005, tau=0.0, l_max=5, cgls=kb.CglsConfig(i_max=12, tau=0.0))
+        dense = kb.sb_run(g["inter_a"], g["inter_b"], cfg)
+        op = kb.KroneckerSum(list(g["inter_ax"]), list(g["inter_ay"]), kb.BlockScheme.square_image(n))
+        kron = kb.sb_run(op, g["inter_b"], cfg)
+        assert np.linalg.norm(dense.x - g["inter_dense_x"]) <= 1e-9 * np.linalg.norm(g["inter_dense_x"])
+        assert np.linalg.norm(kron.x - g["inter_kron_x"]) <= 1e-9 * np.linalg.norm(g["inter_kron_x"])
+        assert dense.cgls_iters == kron.cgls_iters
+
+    @pytest.mark.parametrize("variant", ["anisotropic", "isotropic"])
+    def test_short_protocol_strict_1e9(self, kb, variant):
+        """CGLS(i_max=20, tau=0), l_max=5 -> 1e-9 relative."""
+        from paper_2410_00233_b200 import datagen
+
+        g = load_golden("sb_kat")
+        side = 32
+        op = kb.KroneckerSum(list(g["n64_ax"]), list(g["n64_ay"]), kb.BlockScheme.square_image(side))
+        cfg = kb.SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=variant, tau=0.0, l_max=5,
+                          cgls=kb.CglsConfig(i_max=20, tau=0.0))
+        res = kb.sb_run(op, g["n64_b"], cfg, x_true=g["n64_xtrue"])
+        ref = g[f"n64_{variant}_short_x"]
+        assert np.linalg.norm(res.x - ref) <= 1e-9 * np.linalg.norm(ref)
+        np.testing.assert_allclose(res.re_history, g[f"n64_{variant}_short_re"], rtol=1e-9)
+
+    @pytest.mark.parametrize("variant", ["anisotropic", "isotropic"])
+    def test_configured_protocol_reports_gap(self, kb, variant):
+        """data-dependent CGLS stop; counts and RE track the reference."""
+        from paper_2410_00233_b200 import datagen
+
+        g = load_golden("sb_kat")
+        side = 32
+        op = kb.KroneckerSum(list(g["n64_ax"]), list(g["n64_ay"]), kb.BlockScheme.square_image(side))
+        cfg = kb.SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=variant, tau=0.0, l_max=10,
+                          cgls=kb.CglsConfig(i_max=100, tau=1e-4))
+        res = kb.sb_run(op, g["n64_b"], cfg, x_true=g["n64_xtrue"])
+        ref = g[f"n64_{variant}_cfg_x"]
+        gap = np.linalg.norm(res.x - ref) / np.linalg.norm(ref)
+        assert gap < 1e-5, gap
+        assert np.abs(np.array(res.cgls_iters) - g[f"n64_{variant}_cfg_iters"]).max() <= 2
+        np.testing.assert_allclose(res.re_history, g[f"n64_{variant}_cfg_re"], rtol=1e-5)
+
+    def test_config_n64_end_to_end(self, kb):
+        """configs[0]: eGKB -> assemble -> 5 SB sweeps vs the reference (same factors)."""
+        from paper_2410_00233_b200 import datagen
+
+        g = load_golden("config_n64")
+        n = 64
+        svd = kb.TruncatedSvd(g["u"], g["sigma"], g["v"])
+        op = kb.assemble(svd, kb.BlockScheme.square_image(n))
+        cfg = kb.SbConfig(lam=datagen.LAM, beta=datagen.BETA, tau=0.0, l_max=5,
+                          cgls=kb.CglsConfig(i_max=20, tau=0.0))
+        res = kb.sb_run(op, g["b"], cfg)
+        assert np.linalg.norm(res.x - g["sb_short_x"]) <= 1e-9 * np.linalg.norm(g["sb_short_x"])
+
+    def test_identity_operator(self, kb):
+        n = 12
+        b = kb.vec(kb.make_test_image(n))
+        cfg = kb.SbConfig(lam=1.0, beta=1e-4, tau=1e-6, l_max=40)
+        out = kb.sb_run(np.eye(n * n), b, cfg, x_true=b)
+        assert out.re_history[-1] < 1e-3
+
+    def test_rejects_bad_shapes(self, kb, rng):
+        with pytest.raises(kb.ValidationError):
+            kb.sb_run(rng.standard_normal((10, 9)), np.ones(10), kb.SbConfig(lam=1, beta=1))
+        with pytest.raises(kb.ValidationError):
+            kb.sb_run(rng.standard_normal((10, 10)), np.ones(10), kb.SbConfig(lam=1, beta=1))
+
+
+class TestEstimators:
+    def test_pipeline_from_psf(self, kb):
+        from paper_2410_00233_b200 import datagen
+
+        prob = datagen.make_problem("n64", n=32)
+        est = kb.KroneckerApproximator(engine="egkb", k_max=10, k_min=10, p=2, tau=1e300, precision="single")
+        est.fit(kb.Psf(prob.psf), side=32)
+        assert est.k_ == 10
+        deb = kb.SplitBregmanDeblurrer(lam=datagen.LAM, beta=datagen.BETA, tau=1e-3, l_max=20)
+        deb.fit(est.operator_, prob.b, x_true=prob.x_true)
+        assert deb.result_.re_history[-1] < np.linalg.norm(prob.b - prob.x_true) / np.linalg.norm(prob.x_true)
+
+    def test_dense_input(self, kb):
+        psf = kb.Psf(np.random.default_rng(0).random((3, 3)) + 0.05)
+        a = kb.build_blur_matrix(psf, 8)
+        est = kb.KroneckerApproximator(engine="rsvd", k=3, p=2, q=1).fit(a)
+        assert est.k_ == 3
+        assert est.transform(np.ones((2, 64))).shape == (2, 64)

@@ -1,0 +1,197 @@
+"""GPU parity of the operator / tall-skinny / GEMM kernels against the oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kb():
+    import paper_2410_00233_b200 as kb
+
+    return kb
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, dtype=np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+class TestRearrangedBlur:
+    def test_matches_reference_dense_rearrangement(self, kb):
+        g = load_golden("ra_structured")
+        for i in range(5):
+            k, n = g[f"c{i}_psf"], int(g[f"c{i}_n"])
+            op = kb.RearrangedBlur(k, n, dtype=np.float64)
+            np.testing.assert_allclose(op.matvec(g[f"c{i}_q"]), g[f"c{i}_Rq"], rtol=0, atol=1e-14)
+            np.testing.assert_allclose(op.rmatvec(g[f"c{i}_s"]), g[f"c{i}_RTs"], rtol=0, atol=1e-14)
+
+    def test_padded_even_psf_fp32(self, kb):
+        g = load_golden("ra_structured")
+        k, n = g["pad_psf"], int(g["pad_n"])
+        op = kb.RearrangedBlur(k, n)
+        got = op.matvec(g["pad_q"].astype(np.float32))
+        assert got.dtype == np.float32
+        assert _rel(got, g["pad_Rq"]) < 1e-6
+        assert _rel(op.rmatvec(g["pad_s"].astype(np.float32)), g["pad_RTs"]) < 1e-6
+
+    @pytest.mark.parametrize("n", [64, 256, 1024])
+    def test_large_sides_against_oracle(self, kb, n):
+        from oracle import structured as ost
+        from paper_2410_00233_b200 import datagen
+
+        psf = datagen.mixture_psf(n)
+        rng = np.random.default_rng(n)
+        q = rng.standard_normal(n * n).astype(np.float32)
+        k32 = psf.astype(np.float32)
+        op = kb.RearrangedBlur(psf, n)
+        assert _rel(op.matvec(q), ost.ra_matvec(k32, n, q)) < 2e-7
+        assert _rel(op.rmatvec(q), ost.ra_rmatvec(k32, n, q)) < 2e-7
+        op64 = kb.RearrangedBlur(psf, n, dtype=np.float64)
+        q64 = q.astype(np.float64)
+        assert _rel(op64.matvec(q64), ost.ra_matvec(psf, n, q64)) < 1e-13
+
+    def test_adjoint_identity(self, kb):
+        n = 96
+        rng = np.random.default_rng(3)
+        psf = rng.random((9, 13))
+        op = kb.RearrangedBlur(psf, n, dtype=np.float64)
+        x, y = rng.standard_normal(n * n), rng.standard_normal(n * n)
+        assert op.matvec(x) @ y == pytest.approx(x @ op.rmatvec(y), rel=1e-12)
+
+    def test_validation(self, kb):
+        with pytest.raises(kb.ValidationError):
+            kb.RearrangedBlur(np.ones((4, 3)), 8)
+        with pytest.raises(kb.ValidationError):
+            kb.RearrangedBlur(np.ones((3, 3)), 8, bc="reflexive")
+        op = kb.RearrangedBlur(np.ones((3, 3)), 8)
+        with pytest.raises(kb.ValidationError):
+            op.matvec(np.ones(10, dtype=np.float32))
+
+
+class TestDgemm:
+    @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+    @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (130, 70, 33), (256, 128, 64)])
+    def test_against_numpy(self, kb, ta, tb, m, n, k):
+        import ctypes as C
+
+        import torch
+        from paper_2410_00233_b200 import _lib, device as D
+
+        rng = np.random.default_rng(m * 1000 + n * 10 + k + ta * 7 + tb * 3)
+        nb, ns = 3, 2
+        A = rng.standard_normal((nb, ns, k, m) if ta else (nb, ns, m, k))
+        B = rng.standard_normal((nb, ns, n, k) if tb else (nb, ns, k, n))
+        want = np.zeros((nb, m, n))
+        for z in range(nb):
+            for s in range(ns):
+                a = A[z, s].T if ta else A[z, s]
+                b = B[z, s].T if tb else B[z, s]
+                want[z] += a @ b
+        Ad, Bd = D.to_device(A), D.to_device(B)
+        Cd = torch.zeros((nb, m, n), dtype=torch.float64, device="cuda")
+        lda = m if ta else k
+        ldb = k if tb else n
+        _lib.check(_lib.load().kb_dgemm(ta, tb, m, n, k, Ad.data_ptr(), lda, ns * m * k, m * k,
+                                        Bd.data_ptr(), ldb, ns * k * n, k * n, Cd.data_ptr(), n, m * n, nb, ns,
+                                        0.0, D.stream_ptr()))
+        np.testing.assert_allclose(D.to_host(Cd), want, rtol=1e-12, atol=1e-12)
+
+
+class TestKronecker:
+    @pytest.mark.parametrize("dims,k", [((3, 4, 2, 5), 3), ((2, 2, 2, 2), 1), ((5, 2, 3, 3), 4),
+                                        ((64, 64, 64, 64), 10), ((33, 17, 9, 40), 5)])
+    def test_apply_against_oracle(self, kb, dims, k):
+        from oracle import sb as osb
+
+        rng = np.random.default_rng(sum(dims) + k)
+        m1, m2, n1, n2 = dims
+        ax = [rng.standard_normal((m1, n1)) for _ in range(k)]
+        ay = [rng.standard_normal((m2, n2)) for _ in range(k)]
+        op = kb.KroneckerSum(ax, ay, kb.BlockScheme(*dims))
+        ref = osb.KronOracle(ax, ay, *dims)
+        x = rng.standard_normal(n1 * n2)
+        y = rng.standard_normal(m1 * m2)
+        assert _rel(op.apply(x), ref.apply(x)) < 1e-13
+        assert _rel(op.apply_t(y), ref.apply_t(y)) < 1e-13
+        if m1 * m2 * n1 * n2 <= 2 ** 20:
+            np.testing.assert_allclose(op.apply(x), ref.materialize() @ x, atol=1e-11)
+
+    def test_materialize_and_factors_roundtrip(self, kb):
+        rng = np.random.default_rng(0)
+        s = kb.BlockScheme(3, 4, 2, 5)
+        ax = [rng.standard_normal((3, 2)) for _ in range(2)]
+        ay = [rng.standard_normal((4, 5)) for _ in range(2)]
+        op = kb.KroneckerSum(ax, ay, s)
+        dev = kb.KroneckerSum.from_device(op.f_dev, op.g_dev, s)
+        for a, b in zip(dev.ax, ax):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_allclose(dev.materialize(), sum(np.kron(a, b) for a, b in zip(ax, ay)))
+
+    def test_assemble_matches_reference_rule(self, kb):
+        g = load_golden("config_n64")
+        n = 64
+        svd = kb.TruncatedSvd(g["u"], g["sigma"], g["v"])
+        op = kb.assemble(svd, kb.BlockScheme.square_image(n))
+        for i in range(svd.k):
+            want_ax = g["sigma"][i].astype(np.float64) * g["u"][:, i].astype(np.float64).reshape((n, n), order="F")
+            np.testing.assert_array_equal(op.ax[i], want_ax)
+
+
+class TestStencilsAndShrink:
+    def test_diff_ops_against_oracle(self, kb):
+        from oracle import sb as osb
+
+        n = 37
+        rng = np.random.default_rng(1)
+        x = rng.standard_normal(n * n)
+        w = rng.standard_normal(n * (n - 1))
+        np.testing.assert_array_equal(kb.diff_x(x, n), osb.dx(x, n))
+        np.testing.assert_array_equal(kb.diff_y(x, n), osb.dy(x, n))
+        np.testing.assert_array_equal(kb.diff_x_t(w, n), osb.dx_t(w, n))
+        np.testing.assert_array_equal(kb.diff_y_t(w, n), osb.dy_t(w, n))
+
+    def test_shrink_updates(self, kb):
+        from oracle import sb as osb
+
+        rng = np.random.default_rng(2)
+        cx, cy = rng.standard_normal(1000), rng.standard_normal(1000)
+        cx[:5] = 0.0
+        cy[:3] = 0.0
+        for g in (0.5, 1.5, 19.0):
+            dx, dy = kb.update_d_aniso(cx, cy, g, g)
+            ex, ey = osb.d_aniso(cx, cy, g, g)
+            np.testing.assert_array_equal(dx, ex)
+            np.testing.assert_array_equal(dy, ey)
+            dx, dy = kb.update_d_iso(cx, cy, g, g)
+            ex, ey = osb.d_iso(cx, cy, g, g)
+            np.testing.assert_allclose(dx, ex, rtol=1e-12, atol=1e-15)
+            np.testing.assert_allclose(dy, ey, rtol=1e-12, atol=1e-15)
+        dx, dy = kb.update_d_iso(np.array([3.0]), np.array([4.0]), 1.0, 1.0)
+        assert dx[0] == pytest.approx(2.4) and dy[0] == pytest.approx(3.2)
+        dx, dy = kb.update_d_iso(np.array([0.3]), np.array([0.4]), 1.0, 1.0)
+        assert dx[0] == 0.0 and dy[0] == 0.0
+
+
+class TestOrthonormalize:
+    def test_against_reference_golden(self, kb):
+        g = load_golden("rsvd_kat")
+        q = kb.orthonormalize(g["orth_in"])
+        assert np.abs(q - g["orth_out"]).max() < 1e-13
+        q32 = kb.orthonormalize(g["orth_in"].astype(np.float32))
+        assert q32.dtype == np.float32
+        assert np.abs(q32 - g["orth32_out"]).max() < 1e-5
+
+    def test_rank_deficiency_names_column(self, kb):
+        rng = np.random.default_rng(0)
+        m = rng.standard_normal((40, 6))
+        m[:, 4] = m[:, 1] + 2 * m[:, 2]
+        with pytest.raises(kb.RankDeficiencyError) as err:
+            kb.orthonormalize(m)
+        assert err.value.column == 4
+
+    def test_too_many_columns(self, kb):
+        with pytest.raises(kb.ValidationError):
+            kb.orthonormalize(np.ones((3, 5)))
