@@ -1,0 +1,367 @@
+"""Benchmark of the hot path on BASELINE.json configs[3] (n=1024).
+
+One STEP = one Kronecker-product approximation of the n=1024 blur: fp32 eGKB
+on the matrix-free R(A) with the config's "rank 30 + enlargement p=2"
+(EgkbConfig(k_max=30, k_min=30, p=2, tau=1e300); the fp32 recurrence breaks
+down at the numerical rank, as the reference does) followed by `assemble`
+into fp64 Kronecker factors.  `value` = approximations/s over all ranks with
+inputs resident in HBM; `e2e` = the same through the public API from host
+arrays (PSF + reference-style host y0 uploaded, trace/sigma read back) each
+step.  The same run also measures the fp64 split-Bregman solve that consumes
+the factors (isotropic, CGLS i_max=100 tau=1e-4) and reports outer / CGLS
+iterations per second in "sb", and the R(A) product in "ra_matvec".
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (torchrun): independent replicas (weak scaling), max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "n1024"
+FP64_PEAK_TFLOPS = 37.2   # DMMA m8n8k4 issue rate measured on this pool (profiles/fp64_peak_r01.txt)
+METRIC = "R(A) matvec GB/s & KP-approx time at n=1024; SB iter/s; % of roofline"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def egkb_cfg_kwargs():
+    from paper_2410_00233_b200 import datagen
+
+    return dict(datagen.CONFIGS[CONFIG]["egkb"])
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, prob):
+    """The reference's algorithm on the host CPU (oracle port; the reference is
+    pure Python and cannot be installed on the GPU box)."""
+    from types import SimpleNamespace
+
+    from oracle import lowrank as olr
+    from oracle import structured as ost
+
+    n = prob.n
+    k32 = prob.psf.astype(np.float32)
+    cfg = SimpleNamespace(reorth=None, seed=0, break_tol=None, keep_basis=False, **egkb_cfg_kwargs())
+    cfg.tau = float(cfg.tau)
+
+    def step():
+        (u, s, v), tr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda x: ost.ra_rmatvec(k32, n, x),
+                                 (n * n, n * n), np.float32, cfg)
+        # assemble: fp64 factors sigma_i u_i, v_i (kronop.py:103-123)
+        _ = [s[i].astype(np.float64) * u[:, i].astype(np.float64) for i in range(u.shape[1])]
+        _ = [v[:, i].astype(np.float64) for i in range(v.shape[1])]
+        return tr
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tr = step()
+    dt = (time.perf_counter() - t0) / args.steps
+    cores = os.cpu_count()
+    val = 1.0 / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "KP-approx/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 -> assemble", "n": n,
+                   "egkb": egkb_cfg_kwargs() | {"tau": "1e300"}, "chosen_k": tr.chosen_k, "k_p": tr.k_p},
+        "cpu_baseline": {"value": val, "unit": "KP-approx/s", "cores": cores, "kind": "port",
+                         "sample": "full eGKB+assemble per step (oracle/lowrank.py restatement of lowrank.py:159-329 "
+                                   "on the numpy structured R(A), MGS as the reference)"},
+        "e2e": {"value": val, "unit": "KP-approx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- our arm
+def prof_read(lib, cls):
+    import ctypes as C
+
+    ms, n, by, fl = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+    lib.kb_prof_query(cls, C.byref(ms), C.byref(n), C.byref(by), C.byref(fl))
+    return ms.value, n.value, by.value, fl.value
+
+
+def run_ours(args, prob, rank, world, dist):
+    import torch
+
+    import paper_2410_00233_b200 as kb
+    from paper_2410_00233_b200 import _lib
+    from paper_2410_00233_b200 import device as D
+
+    lib = _lib.load()
+    n = prob.n
+    N = n * n
+    cfg = kb.EgkbConfig(**egkb_cfg_kwargs())
+    scheme = kb.BlockScheme.square_image(n)
+    blur = kb.RearrangedBlur(prob.psf, n)          # PSF resident on the device
+    y0_host = np.random.default_rng(cfg.seed).standard_normal(N).astype(np.float32)
+    y0 = D.to_device(y0_host)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=D.device())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def step_resident():
+        svd, tr = kb.egkb(blur, cfg, y0=y0)
+        op = kb.assemble(svd, scheme)
+        return svd, tr, op
+
+    for _ in range(max(args.warmup, 3)):
+        step_resident()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs), L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    lib.kb_prof_enable(1)
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        ev[i][0].record()
+        svd, tr, op = step_resident()
+        ev[i][1].record()
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    prof = {c: prof_read(lib, c) for c in range(6)}
+    lib.kb_prof_enable(0)
+    gpu_launches = sum(v[1] for v in prof.values())
+
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device=D.device())
+    if dist is not None:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    total_ms = float(t_max.item())
+    ms_per_step = total_ms / args.steps
+    value = world * args.steps / (total_ms * 1e-3)
+
+    # ---- e2e: public API from host arrays, every step
+    psf_host = prob.psf
+    h2d = 2 * psf_host.size * 4 + N * 4
+    e2e_ms = []
+    for i in range(max(args.steps, 1)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        blur_i = kb.RearrangedBlur(psf_host, n)                 # uploads K, K^T
+        svd_i, tr_i = kb.egkb(blur_i, cfg)                      # host y0 (reference RNG), uploads it
+        op_i = kb.assemble(svd_i, scheme)
+        sig = np.asarray(svd_i.sigma)                           # result on the host
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    iters = len(tr.alphas) + 1
+    d2h = 8 * 4 * iters + 16 + sig.nbytes
+    h2d += 8 * 2 * (tr.k_p + 1) * tr.chosen_k                  # lift coefficient uploads
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=D.device())
+    if dist is not None:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world / (float(e2e_t.item()) * 1e-3)
+
+    # ---- split Bregman on the fresh factors (same run): one outer sweep
+    sb_cfg = kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=args.sb_outer,
+                         cgls=kb.CglsConfig(i_max=100, tau=1e-4))
+    b_dev = D.to_device(prob.b)
+    kb.sb_run(op, b_dev, kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=1,
+                                     cgls=kb.CglsConfig(i_max=2, tau=0.0)))   # warm-up
+    torch.cuda.synchronize()
+    lib.kb_prof_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sb_res = kb.sb_run(op, b_dev, sb_cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    sb_ms = e0.elapsed_time(e1)
+    g_ms, g_n, g_by, g_fl = prof_read(lib, 3)
+    v_ms, v_n, _, _ = prof_read(lib, 4)
+    lib.kb_prof_enable(0)
+    clk = clocks.stop() if clocks is not None else None
+    if rank != 0:
+        return
+
+    hbm, hbm_src = peaks()
+    # dominant kernel of the step: the class with the largest device time
+    names = {0: "reorth pass (k_reorth)", 1: "R(A) diagonal sums (k_diag_partial)",
+             2: "R(A) K-column sums (k_colsum)", 3: "fp64 GEMM (k_dgemm, DMMA)", 4: "CGLS/SB vector passes",
+             5: "lift (k_lift)"}
+    dom = max(range(6), key=lambda c: prof[c][0])
+    d_ms, d_n, d_by, d_fl = prof[dom]
+    achieved = (d_by / d_n) / ((d_ms / d_n) * 1e-3) / 1e9 if d_n else 0.0
+    step_share = d_ms / total_ms if total_ms else 0.0
+    # R(A) product: one diag pass + one column pass per product
+    mv_ms = prof[1][0] + prof[2][0]
+    mv_n = prof[1][1]
+    mv_bytes_alg = 4.0 * (2 * N + (n + 1) ** 2)             # SURVEY §8d B_mv per product
+    mv_bytes_moved = (prof[1][2] + prof[2][2]) / max(mv_n, 1)
+    mv_t = (mv_ms / max(mv_n, 1)) * 1e-3
+    ra = {"products": mv_n, "us_per_product": mv_t * 1e6,
+          "GBps_survey_Bmv": mv_bytes_alg / mv_t / 1e9 if mv_t else None,
+          "GBps_bytes_moved": mv_bytes_moved / mv_t / 1e9 if mv_t else None,
+          "frac_survey_Bmv": mv_bytes_alg / mv_t / 1e9 / hbm if mv_t else None,
+          "note": "B_mv = 4(2N+(n+1)^2) per SURVEY §8d; the y write is fused into the reorth pass that "
+                  "consumes it, so bytes_moved = band read + K read"}
+    cg = int(sum(sb_res.cgls_iters))
+    sb = {"variant": "isotropic", "k_terms": op.k, "outer_iters": sb_res.outer_iters, "cgls_iters": cg,
+          "ms": sb_ms, "outer_it_per_s": sb_res.outer_iters / (sb_ms * 1e-3),
+          "cgls_it_per_s": cg / (sb_ms * 1e-3),
+          "gemm_tflops": g_fl / (g_ms * 1e-3) / 1e12 if g_ms else None,
+          "gemm_frac_fp64_peak": (g_fl / (g_ms * 1e-3) / 1e12) / FP64_PEAK_TFLOPS if g_ms else None,
+          "gemm_share": g_ms / sb_ms if sb_ms else None, "vector_pass_ms": v_ms,
+          "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_src": "measured DMMA issue rate, tools/fp64_peak"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "KP-approx/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 (matrix-free R(A)) -> assemble", "n": n,
+                   "egkb": {k: (str(v) if k == "tau" else v) for k, v in egkb_cfg_kwargs().items()},
+                   "chosen_k": tr.chosen_k, "k_p": tr.k_p, "stop_reason": tr.stop_reason,
+                   "breakdown": tr.breakdown, "parallelism": f"replicas x{world}",
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "launches": d_n,
+                     "share_of_step": step_share, "peak_src": hbm_src},
+        "ra_matvec": ra,
+        "sb": sb,
+        "e2e": {"value": e2e_value, "unit": "KP-approx/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
+        "gpu_launches": int(gpu_launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(prob)
+    print(json.dumps(line))
+
+
+def cpu_baseline(prob):
+    from types import SimpleNamespace
+
+    from oracle import lowrank as olr
+    from oracle import sb as osb
+    from oracle import structured as ost
+
+    n = prob.n
+    k32 = prob.psf.astype(np.float32)
+    cfg = SimpleNamespace(reorth=None, seed=0, break_tol=None, keep_basis=False, **egkb_cfg_kwargs())
+    t0 = time.perf_counter()
+    (u, s, v), tr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda x: ost.ra_rmatvec(k32, n, x),
+                             (n * n, n * n), np.float32, cfg)
+    t_egkb = time.perf_counter() - t0
+    ax = [s[i].astype(np.float64) * u[:, i].astype(np.float64).reshape((n, n), order="F") for i in range(s.size)]
+    ay = [v[:, i].astype(np.float64).reshape((n, n), order="F") for i in range(s.size)]
+    op = osb.KronOracle(ax, ay, n, n, n, n)
+    aug = osb.AugOracle(op, n, 0.1150, 0.1150)
+    rhs = np.concatenate([prob.b, np.zeros(2 * n * (n - 1))])
+    t0 = time.perf_counter()
+    osb.cgls(aug, rhs, i_max=2, tau=0.0)
+    t_cg = (time.perf_counter() - t0) / 2.5   # 1 initial transpose + 2 x (forward + transpose)
+    return {"value": 1.0 / t_egkb, "unit": "KP-approx/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": "one full eGKB+assemble at n=1024 (oracle restatement, numpy structured R(A)); "
+                      f"SB: 2 CGLS iterations of the k={s.size} augmented system",
+            "egkb_s": t_egkb, "cgls_it_per_s": 1.0 / t_cg, "chosen_k": tr.chosen_k}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sb-outer", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2410_00233_b200 import datagen
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(args, datagen.make_problem(CONFIG))
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    else:
+        torch.cuda.set_device(0)
+    prob = datagen.make_problem(CONFIG)
+    run_ours(args, prob, rank, world, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

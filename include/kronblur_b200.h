@@ -64,6 +64,13 @@ typedef void* kb_stream_t; /* cudaStream_t */
 const char* kb_last_error(void);
 int kb_version(void);
 
+/* Optional device timing per kernel class (CUDA events on the launching
+ * stream): 0 reorth/normalise passes, 1 R(A) diagonal sums, 2 R(A)/dense
+ * column sums + row dots, 3 FP64 GEMM, 4 SB/CGLS vector passes, 5 lifts.
+ * kb_prof_enable(1) clears the record; kb_prof_query sums a class. */
+void kb_prof_enable(int on);
+int kb_prof_query(int cls, double* ms, long long* launches, double* bytes, double* flops);
+
 /* ------------------------------------------------------------------ */
 /* Operators B for eGKB / RSVD                                        */
 /* ------------------------------------------------------------------ */

@@ -77,6 +77,8 @@ SZ = C.c_size_t
 _SIGS = {
     "kb_last_error": (C.c_char_p, []),
     "kb_version": (C.c_int, []),
+    "kb_prof_enable": (None, [C.c_int]),
+    "kb_prof_query": (C.c_int, [C.c_int, dp, C.POINTER(C.c_longlong), dp, dp]),
     "kb_op_workspace_bytes": (C.c_int, [P(KbOperator), P(SZ)]),
     "kb_op_apply": (C.c_int, [P(KbOperator), vp, vp, C.c_int, vp, SZ, vp]),
     "kb_ts_dots": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, vp, vp, SZ, vp]),

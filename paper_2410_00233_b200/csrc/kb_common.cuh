@@ -71,6 +71,21 @@ struct Sizer {
     void take(size_t count) { off += align_up(count * sizeof(T)); }
 };
 
+// ---------------------------------------------------------------- profiling
+// Optional per-kernel-class device timing (CUDA events on the launching
+// stream), used by bench.py for the live roofline numbers.  Off by default.
+enum ProfClass { PROF_REORTH = 0, PROF_RA_DIAG, PROF_RA_COLSUM, PROF_DGEMM, PROF_SBVEC, PROF_LIFT,
+                 PROF_NCLASS };
+extern bool g_prof;
+void prof_record(cudaStream_t st, int cls, double bytes, double flops, bool start);
+struct ProfScope {
+    cudaStream_t st; int cls; double bytes, flops; bool on;
+    ProfScope(cudaStream_t s, int c, double b, double f = 0.0) : st(s), cls(c), bytes(b), flops(f), on(g_prof) {
+        if (on) prof_record(st, cls, bytes, flops, true);
+    }
+    ~ProfScope() { if (on) prof_record(st, cls, bytes, flops, false); }
+};
+
 // ---------------------------------------------------------------- device side
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -24,6 +24,31 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+// ------------------------------------------------------------------ profiling
+bool g_prof = false;
+struct ProfRec { cudaEvent_t a, b; int cls; double bytes, flops; };
+static std::vector<ProfRec> g_recs;
+static size_t g_nrec = 0;
+
+void prof_record(cudaStream_t st, int cls, double bytes, double flops, bool start) {
+    if (start) {
+        if (g_nrec == g_recs.size()) {
+            ProfRec r{};
+            cudaEventCreate(&r.a);
+            cudaEventCreate(&r.b);
+            g_recs.push_back(r);
+        }
+        ProfRec& r = g_recs[g_nrec];
+        r.cls = cls;
+        r.bytes = bytes;
+        r.flops = flops;
+        cudaEventRecord(r.a, st);
+    } else {
+        cudaEventRecord(g_recs[g_nrec].b, st);
+        ++g_nrec;
+    }
+}
+
 void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* x,
                   double* y, int transpose, double* part, unsigned* counters, cudaStream_t st);
 
@@ -359,6 +384,7 @@ static void orthonormalize(int dtype, void* Q, int64_t ld, int ncol, int64_t len
 using namespace kb;
 
 extern "C" const char* kb_last_error(void) { return g_err; }
+
 extern "C" int kb_version(void) { return 1; }
 
 #define KB_GUARD(...)                                               \
@@ -372,6 +398,32 @@ extern "C" int kb_version(void) { return 1; }
         return KB_ERUNTIME;                                         \
     }
 
+extern "C" void kb_prof_enable(int on) {
+    g_prof = on != 0;
+    g_nrec = 0;
+}
+
+extern "C" int kb_prof_query(int cls, double* ms, long long* launches, double* bytes, double* flops) {
+    KB_GUARD({
+        double t = 0, by = 0, fl = 0;
+        long long n = 0;
+        for (size_t i = 0; i < g_nrec; ++i) {
+            const ProfRec& r = g_recs[i];
+            if (r.cls != cls) continue;
+            KB_CUDA(cudaEventSynchronize(r.b));
+            float e = 0;
+            KB_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+            t += e;
+            by += r.bytes;
+            fl += r.flops;
+            ++n;
+        }
+        *ms = t;
+        *launches = n;
+        *bytes = by;
+        *flops = fl;
+    })
+}
 extern "C" int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes) {
     KB_GUARD({
         validate_op(op);

@@ -185,6 +185,9 @@ static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int6
         configured = true;
     }
     dim3 grid((unsigned)cdiv(n, BN), (unsigned)cdiv(m, BM), (unsigned)nbatch);
+    const double nb = (double)nbatch, ns = (double)nseg;
+    ProfScope ps(st, PROF_DGEMM, 8.0 * nb * (ns * ((double)m * k + (double)k * n) + (double)m * n),
+                 2.0 * m * n * (double)k * nb * ns);
     k_dgemm<TA, TB><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
                                                  C, ldc, sc_b, nseg, beta);
     KB_LAUNCH_CHECK();

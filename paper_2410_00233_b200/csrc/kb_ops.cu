@@ -395,17 +395,25 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
         const int rb = rb_for(n, chunks);
         const int nrb = (int)cdiv(n, rb);
         dim3 g1(chunks, nrb);
-        k_diag_partial<T><<<g1, 256, 0, st>>>(x, n, ci, Li, rb, p.part, p.w, p.counters);
-        KB_LAUNCH_CHECK();
+        {
+            double band = 0;
+            for (int u = 0; u < Li; ++u) band += std::max(n - std::abs(u - ci), 0);
+            ProfScope ps(st, PROF_RA_DIAG, band * sizeof(T));
+            k_diag_partial<T><<<g1, 256, 0, st>>>(x, n, ci, Li, rb, p.part, p.w, p.counters);
+            KB_LAUNCH_CHECK();
+        }
         // z = M^T w with M = K (forward) or K^T (transpose): rows Li, cols Lo
         const int cchunks = (int)cdiv(Lo, 128);
         const int rb2 = rb_for(Li, cchunks);
         const int nrb2 = (int)cdiv(Li, rb2);
         dim3 g2(cchunks, nrb2);
         KB_REQUIRE(chunks <= 64 && cchunks <= 64, "R(A): PSF support too large (%d x %d)", op->kh, op->kw);
-        k_colsum<T, double><<<g2, 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo, p.w, rb2,
-                                                p.part, p.z, p.counters + 64);
-        KB_LAUNCH_CHECK();
+        {
+            ProfScope ps(st, PROF_RA_COLSUM, (double)Li * Lo * sizeof(T));
+            k_colsum<T, double><<<g2, 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo, p.w, rb2,
+                                                    p.part, p.z, p.counters + 64);
+            KB_LAUNCH_CHECK();
+        }
         s.z = p.z;
         s.mode = SRC_TOEP;
         s.side = n;
@@ -415,6 +423,7 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
         const T* A = static_cast<const T*>(op->a);
         if (!transpose) {
             const int rows = (int)op->rows, cols = (int)op->cols;
+            ProfScope ps(st, PROF_RA_COLSUM, (double)rows * cols * sizeof(T));
             k_rowdot<T><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, op->lda, rows, cols, x, p.z);
             KB_LAUNCH_CHECK();
         } else {
@@ -423,6 +432,7 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
             const int rb = rb_for(rows, cchunks);
             const int nrb = (int)cdiv(rows, rb);
             dim3 g(cchunks, nrb);
+            ProfScope ps(st, PROF_RA_COLSUM, (double)rows * cols * sizeof(T));
             k_colsum<T, T><<<g, 256, 0, st>>>(A, op->lda, rows, cols, x, rb, p.part, p.z,
                                               p.counters);
             KB_LAUNCH_CHECK();
@@ -481,6 +491,9 @@ static void launch_reorth(const Src& src, const void* S, int64_t ld, int m, cons
         configured = true;
     }
     const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC)));
+    double vecs = (double)m + (src.prev ? 1 : 0) + (out ? 1 : 0) + (src.mode == SRC_BUFT ? 1 : 0);
+    double bytes = vecs * len * sizeof(T) + (src.mode == SRC_BUF64 ? 8.0 * len : 0.0);
+    ProfScope ps(st, PROF_REORTH, bytes);
     kern<<<blocks, 256, smem, st>>>(src.z, src.mode, src.side, src.center, src.L,
                                     static_cast<const T*>(src.prev), src.beta,
                                     static_cast<const T*>(S), ld, m, cA, cB, dots ? 1 : 0,
@@ -510,6 +523,7 @@ void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, int m, co
 
 void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, const double* x,
                   double* y, int transpose, double* part, unsigned* counters, cudaStream_t st) {
+    ProfScope ps(st, PROF_RA_COLSUM, 8.0 * rows * cols);
     if (!transpose) {
         k_rowdot<double><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, lda, (int)rows, (int)cols, x, y);
     } else {
@@ -526,7 +540,9 @@ void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int 
     const size_t smem = sizeof(double) * (size_t)rows * 32;
     KB_REQUIRE(rows <= 512, "lift: too many basis vectors (%d)", rows);
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 4 * kSMs));
+    const size_t esz = dtype == KB_F32 ? 4 : 8;
     for (int c0 = 0; c0 < cols; c0 += 32) {
+        ProfScope ps(st, PROF_LIFT, (double)esz * len * (rows + std::min(32, cols - c0)));
         if (dtype == KB_F32) {
             KB_CUDA(cudaFuncSetAttribute(k_lift<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
             k_lift<float><<<blocks, 256, smem, st>>>(static_cast<const float*>(S), ld, rows,

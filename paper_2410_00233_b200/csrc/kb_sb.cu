@@ -305,6 +305,7 @@ template <int R, class F, class P = NoPost>
 static void map_reduce(int64_t len, const F& f, const MR& mr, double* out, cudaStream_t st,
                        const P& post = P()) {
     const int blocks = mr_blocks(len);
+    ProfScope ps(st, PROF_SBVEC, 0.0);
     k_map_reduce<R, F, P><<<blocks, MR_THREADS, 0, st>>>(len, f, post, mr.part, out, mr.counter);
     KB_LAUNCH_CHECK();
 }

@@ -201,13 +201,17 @@ def _lift(code, basis, nrows, W, out_rows):
 
 
 # ----------------------------------------------------------------- eGKB
-def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 2):
+def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     """Enlarged Golub-Kahan bidiagonalisation with automatic rank choice
     (lowrank.py:159-329), on the GPU.
 
-    ``reorth_passes`` = 2 (default) projects with classical Gram-Schmidt
-    twice (CGS2) where the reference runs one modified-GS pass
-    (lowrank.py:153-156); 1 selects a single classical pass.
+    ``reorth_passes`` = 1 (default) projects once against the whole basis,
+    as the reference's single modified-GS pass does (lowrank.py:153-156),
+    with the coefficients formed in one fused pass (classical GS, fp64
+    accumulation).  One pass is what reproduces the reference's breakdown
+    and rank decisions beyond the fp32 numerical rank (a second pass keeps
+    a noise-level recurrence alive where the reference stops; see
+    DESIGN.md); ``reorth_passes=2`` selects CGS2.
     """
     from . import device as D
 
@@ -220,14 +224,18 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 2):
     if reorth is None:
         reorth = REORTH_FULL if dtype == np.float32 else REORTH_ONE_SIDED
 
-    rng = np.random.default_rng(config.seed)
     if y0 is None:
-        y0 = rng.standard_normal(mbar).astype(dtype)
+        # host RNG, exactly as the reference draws it (lowrank.py:199-201)
+        y0d = D.to_device(np.random.default_rng(config.seed).standard_normal(mbar).astype(dtype))
+    elif D.is_tensor(y0):
+        y0d = D.to_device(y0, dtype)
+        if tuple(y0d.shape) != (mbar,):
+            raise ValidationError(f"y0 must have length {mbar}, got shape {tuple(y0d.shape)}")
     else:
-        y0 = np.asarray(y0.detach().cpu() if D.is_tensor(y0) else y0, dtype=dtype)
+        y0 = np.asarray(y0, dtype=dtype)
         if y0.shape != (mbar,):
             raise ValidationError(f"y0 must have length {mbar}, got shape {y0.shape}")
-    y0d = D.to_device(y0)
+        y0d = D.to_device(y0)
 
     cfg = _lib.KbEgkbConfig(config.k_max, config.p, config.k_min, float(config.tau), float(break_tol),
                             1 if reorth == REORTH_FULL else 0, int(reorth_passes))
