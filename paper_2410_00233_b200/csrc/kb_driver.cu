@@ -75,19 +75,23 @@ __global__ void k_toeplitz_lift(const T* __restrict__ coef, int64_t ldc, int L, 
     const int64_t len = (int64_t)side * side;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int a = (int)(e / side), b = (int)(e - (int64_t)a * side);
-        const int u = b - a + center;
+        const unsigned a = (unsigned)e / (unsigned)side;
+        const int u = (int)((unsigned)e - a * (unsigned)side) - (int)a + center;
         const bool ok = (u >= 0 && u < L);
         for (int c = 0; c < k; ++c) out[(int64_t)c * ld_out + e] = ok ? coef[(int64_t)c * ldc + u] : T(0);
     }
 }
 
+struct SigmaParam {
+    double v[256];
+};
+
 template <typename T>
 __global__ void k_assemble(const T* __restrict__ u, int64_t ldu, const T* __restrict__ v, int64_t ldv,
-                           const double* __restrict__ sigma, int k, int64_t len_u, int64_t len_v,
+                           const SigmaParam sigma, int k, int64_t len_u, int64_t len_v,
                            double* __restrict__ f, double* __restrict__ g) {
     const int i = blockIdx.y;
-    const double s = sigma[i];
+    const double s = sigma.v[i];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len_u || e < len_v;
          e += (int64_t)gridDim.x * blockDim.x) {
         if (e < len_u) f[(int64_t)i * len_u + e] = s * (double)u[(int64_t)i * ldu + e];
@@ -206,9 +210,8 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     EgkbWs w = egkb_ws_make(op, cap, a);
     KB_CUDA(cudaMemsetAsync(w.plan.counters, 0, sizeof(unsigned) * w.plan.n_counters, s));
     KB_CUDA(cudaMemsetAsync(w.rw.counter, 0, sizeof(unsigned) * 64, s));
-    double* hp = nullptr;
-    KB_CUDA(cudaMallocHost(&hp, sizeof(double) * 8));
-    struct PinGuard { double* p; ~PinGuard() { cudaFreeHost(p); } } guard{hp};
+    static thread_local double* hp = nullptr;   // pinned scalar mailbox, allocated once per thread
+    if (hp == nullptr) KB_CUDA(cudaMallocHost(&hp, sizeof(double) * 8));
 
     const double tol = cfg->break_tol >= 0 ? cfg->break_tol : std::sqrt(eps_of(op->dtype));
     const int passes = cfg->reorth_passes >= 2 ? 2 : 1;
@@ -220,13 +223,6 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     sy.mode = SRC_BUFT;
     reorth_pass(op->dtype, sy, nullptr, 0, 0, nullptr, nullptr, false, nullptr, nullptr, M, w.red[0], w.rw, s);
     scalars(s, w.red[0] + 3, w.cur + 1, w.red[0] + 3, w.hist + 0);
-    KB_CUDA(cudaMemcpyAsync(hp, w.hist, sizeof(double), cudaMemcpyDeviceToHost, s));
-    KB_CUDA(cudaStreamSynchronize(s));
-    const double t1 = hp[0];
-    if (t1 == 0.0) {
-        set_error("starting vector must be nonzero");
-        throw Fail{KB_EVALIDATION};
-    }
     reorth_pass(op->dtype, sy, nullptr, 0, 0, nullptr, nullptr, false, slot(st->s_basis, st->ld_s, 0),
                 w.cur + 1, M, w.red[1], w.rw, s);
     // --- q1 = B^T s1 / alpha1   (lowrank.py:211-215)
@@ -239,6 +235,11 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     }
     KB_CUDA(cudaMemcpyAsync(hp, w.hist, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     KB_CUDA(cudaStreamSynchronize(s));
+    const double t1 = hp[0];
+    if (t1 == 0.0) {
+        set_error("starting vector must be nonzero");
+        throw Fail{KB_EVALIDATION};
+    }
     const double alpha1 = hp[2];
     if (alpha1 == 0.0) {
         set_error("operator annihilates the starting vector");
@@ -554,11 +555,10 @@ extern "C" int kb_kron_assemble(int dtype, const void* u, int64_t ldu, const voi
                                 double* g, kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(u && v && sigma_host && f && g && k >= 1, "bad arguments");
-        KB_REQUIRE(k <= 65535, "too many terms");
+        KB_REQUIRE(k <= 256, "too many terms (%d > 256)", k);
         cudaStream_t s = as_stream(stream);
-        double* sig = nullptr;
-        KB_CUDA(cudaMallocAsync(&sig, sizeof(double) * k, s));
-        KB_CUDA(cudaMemcpyAsync(sig, sigma_host, sizeof(double) * k, cudaMemcpyHostToDevice, s));
+        SigmaParam sig{};
+        for (int i = 0; i < k; ++i) sig.v[i] = sigma_host[i];
         dim3 grid((unsigned)std::min<int64_t>(cdiv(std::max(len_u, len_v), 256), 4 * kSMs), (unsigned)k);
         if (dtype == KB_F32)
             k_assemble<float><<<grid, 256, 0, s>>>(static_cast<const float*>(u), ldu,
@@ -567,7 +567,5 @@ extern "C" int kb_kron_assemble(int dtype, const void* u, int64_t ldu, const voi
             k_assemble<double><<<grid, 256, 0, s>>>(static_cast<const double*>(u), ldu,
                                                     static_cast<const double*>(v), ldv, sig, k, len_u, len_v, f, g);
         KB_LAUNCH_CHECK();
-        KB_CUDA(cudaFreeAsync(sig, s));
-        KB_CUDA(cudaStreamSynchronize(s));
     })
 }

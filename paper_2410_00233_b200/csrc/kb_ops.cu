@@ -50,6 +50,58 @@ k_diag_partial(const T* __restrict__ X, int n, int center, int L, int rb_rows,
     }
 }
 
+// One-pass variant: each CTA owns 8 consecutive diagonals over ALL rows, so
+// every diagonal sum is complete inside one CTA (no cross-CTA partials, no
+// counters; deterministic).  Lane layout: tid&7 = diagonal, tid>>3 = row
+// group; for a fixed row the 8 diagonals are 8 consecutive columns (one
+// 32-byte sector), so each warp load moves 4 full sectors.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_diag_sums(const T* __restrict__ X, int n, int center, int L, double* __restrict__ w) {
+    __shared__ double red[32][9];
+    const int du = threadIdx.x & 7, grp = threadIdx.x >> 3;
+    const int u = blockIdx.x * 8 + du;
+    const int d = u - center;
+    double acc = 0.0;
+    if (u < L) {
+        const int lo = max(0, -d), hi = min(n, n - d);
+        int a = lo + ((grp - lo) % 32 + 32) % 32;   // first row >= lo with a % 32 == grp
+#pragma unroll 8
+        for (; a < hi; a += 32) acc += (double)__ldg(X + (int64_t)a * n + (a + d));
+    }
+    red[grp][du] = acc;
+    __syncthreads();
+    if (threadIdx.x < 8 && blockIdx.x * 8 + threadIdx.x < L) {
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
+        w[blockIdx.x * 8 + threadIdx.x] = s;
+    }
+}
+
+// z[c] = sum_r M[r, c] w[r], one CTA per 8 columns over all rows (one pass).
+template <typename TM>
+__global__ void __launch_bounds__(256)
+k_colsum_full(const TM* __restrict__ M, int64_t ld, int rows, int cols, const double* __restrict__ w,
+              double* __restrict__ z) {
+    __shared__ double red[32][9];
+    const int dc = threadIdx.x & 7, grp = threadIdx.x >> 3;
+    const int c = blockIdx.x * 8 + dc;
+    double acc = 0.0;
+    if (c < cols) {
+#pragma unroll 8
+        for (int r = grp; r < rows; r += 32) acc += (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
+    }
+    red[grp][dc] = acc;
+    __syncthreads();
+    if (threadIdx.x < 8 && blockIdx.x * 8 + threadIdx.x < cols) {
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
+        z[blockIdx.x * 8 + threadIdx.x] = s;
+    }
+}
+
 // ------------------------------------------------------------------ column sums
 // z[c] = sum_r M[r, c] w[r]   (M row-major rows x cols, leading dim ld)
 template <typename TM, typename TW>
@@ -117,9 +169,9 @@ struct Gen {
     __device__ __forceinline__ T y(int64_t e) const {
         if (mode == SRC_BUF64) return (T)z[e];
         if (mode == SRC_BUFT) return reinterpret_cast<const T*>(z)[e];
-        const int a = (int)(e / side);
-        const int b = (int)(e - (int64_t)a * side);
-        const int u = b - a + center;
+        const unsigned ee = (unsigned)e;            // n^2 < 2^32 for n <= 65535
+        const unsigned a = ee / (unsigned)side;
+        const int u = (int)(ee - a * (unsigned)side) - (int)a + center;
         return (u >= 0 && u < L) ? (T)zs[u] : T(0);
     }
 };
@@ -390,28 +442,19 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
         const void* Mv;
         ra_geom(op, transpose, ci, Li, co, Lo, Mv);
         const int n = op->side;
-        // diagonal sums
-        const int chunks = (int)cdiv(Li, 256);
-        const int rb = rb_for(n, chunks);
-        const int nrb = (int)cdiv(n, rb);
-        dim3 g1(chunks, nrb);
+        // diagonal sums (one pass, 8 diagonals per CTA)
         {
             double band = 0;
             for (int u = 0; u < Li; ++u) band += std::max(n - std::abs(u - ci), 0);
             ProfScope ps(st, PROF_RA_DIAG, band * sizeof(T));
-            k_diag_partial<T><<<g1, 256, 0, st>>>(x, n, ci, Li, rb, p.part, p.w, p.counters);
+            k_diag_sums<T><<<(unsigned)cdiv(Li, 8), 256, 0, st>>>(x, n, ci, Li, p.w);
             KB_LAUNCH_CHECK();
         }
         // z = M^T w with M = K (forward) or K^T (transpose): rows Li, cols Lo
-        const int cchunks = (int)cdiv(Lo, 128);
-        const int rb2 = rb_for(Li, cchunks);
-        const int nrb2 = (int)cdiv(Li, rb2);
-        dim3 g2(cchunks, nrb2);
-        KB_REQUIRE(chunks <= 64 && cchunks <= 64, "R(A): PSF support too large (%d x %d)", op->kh, op->kw);
         {
             ProfScope ps(st, PROF_RA_COLSUM, (double)Li * Lo * sizeof(T));
-            k_colsum<T, double><<<g2, 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo, p.w, rb2,
-                                                    p.part, p.z, p.counters + 64);
+            k_colsum_full<T><<<(unsigned)cdiv(Lo, 8), 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo,
+                                                                    p.w, p.z);
             KB_LAUNCH_CHECK();
         }
         s.z = p.z;
@@ -461,7 +504,7 @@ void src_write(int dtype, const Src& s, void* y, int64_t len, cudaStream_t st) {
 
 static int reorth_blocks(int64_t len) {
     const int64_t tiles = cdiv(len, 256 * 4);
-    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * kSMs));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4 * kSMs));
 }
 
 void reorth_ws_size(int64_t len, int max_m, Sizer& s) {
@@ -543,13 +586,20 @@ void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int 
     const size_t esz = dtype == KB_F32 ? 4 : 8;
     for (int c0 = 0; c0 < cols; c0 += 32) {
         ProfScope ps(st, PROF_LIFT, (double)esz * len * (rows + std::min(32, cols - c0)));
-        if (dtype == KB_F32) {
+        static bool cfg32 = false, cfg64 = false;
+        if (dtype == KB_F32 && !cfg32) {
             KB_CUDA(cudaFuncSetAttribute(k_lift<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            cfg32 = true;
+        }
+        if (dtype == KB_F64 && !cfg64) {
+            KB_CUDA(cudaFuncSetAttribute(k_lift<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            cfg64 = true;
+        }
+        if (dtype == KB_F32) {
             k_lift<float><<<blocks, 256, smem, st>>>(static_cast<const float*>(S), ld, rows,
                                                      static_cast<const float*>(W), cols, c0,
                                                      static_cast<float*>(out), ld_out, len);
         } else {
-            KB_CUDA(cudaFuncSetAttribute(k_lift<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
             k_lift<double><<<blocks, 256, smem, st>>>(static_cast<const double*>(S), ld, rows,
                                                       static_cast<const double*>(W), cols, c0,
                                                       static_cast<double*>(out), ld_out, len);

@@ -104,8 +104,8 @@ __device__ __forceinline__ double dx_at(const double* x, int64_t e, int n) {  //
     return dmul(0.5, dsub(x[e], x[e + n]));
 }
 __device__ __forceinline__ double dy_at(const double* x, int64_t e, int n) {  // e < n(n-1)
-    const int64_t c = e / (n - 1), r = e - c * (n - 1);
-    const int64_t i = c * n + r;
+    const unsigned c = (unsigned)e / (unsigned)(n - 1), r = (unsigned)e - c * (unsigned)(n - 1);
+    const int64_t i = (int64_t)c * n + r;
     return dmul(0.5, dsub(x[i], x[i + 1]));
 }
 // (D_x^T w)[e]: out[:, :-1] += .5 W ; out[:, 1:] -= .5 W  with W n x (n-1)
@@ -118,7 +118,7 @@ __device__ __forceinline__ double dxt_at(const double* w, int64_t e, int n) {
 }
 // (D_y^T w)[e]: out[:-1, :] += .5 W ; out[1:, :] -= .5 W  with W (n-1) x n
 __device__ __forceinline__ double dyt_at(const double* w, int64_t e, int n) {
-    const int64_t c = e / n, r = e - c * n;
+    const int64_t c = (unsigned)e / (unsigned)n, r = (unsigned)e - (unsigned)c * (unsigned)n;
     double v = 0.0;
     if (r < n - 1) v = dadd(v, dmul(0.5, w[c * (n - 1) + r]));
     if (r >= 1) v = dsub(v, dmul(0.5, w[c * (n - 1) + r - 1]));
