@@ -40,6 +40,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
     const int sz = pred ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -50,12 +55,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-template <bool TA, bool TB>
+// V16: operands 16-byte aligned with even leading dims and even M/N/K, so
+// tiles move as 16-byte cp.async chunks (half the LSU ops of the 8-byte path).
+// Split-K: blockIdx.z = batch * splits + split; split s handles k-tiles
+// [s*T/splits, (s+1)*T/splits) and writes its own partial C (reduced later).
+template <bool TA, bool TB, bool V16>
 __global__ void __launch_bounds__(g64::THREADS, 2)
 k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sa_batch,
         int64_t sa_seg, const double* __restrict__ B, int64_t ldb, int64_t sb_batch,
         int64_t sb_seg, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nseg,
-        double beta) {
+        double beta, int splits, int64_t split_stride) {
     using namespace g64;
     using AL = ALayout<TA>;
     using BL = BLayout<TB>;
@@ -66,21 +75,52 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    const int z = blockIdx.z;
+    const int z = blockIdx.z / splits, split = blockIdx.z - z * splits;
     const double* Ab = A + (int64_t)z * sa_batch;
     const double* Bb = B + (int64_t)z * sb_batch;
-    double* Cb = C + (int64_t)z * sc_batch;
+    double* Cb = C + (int64_t)z * sc_batch + (int64_t)split * split_stride;
 
     const int ktiles = (K + BK - 1) / BK;
-    const int T = ktiles * nseg;
+    const int Ttot = ktiles * nseg;
+    const int t_begin = (int)((int64_t)Ttot * split / splits);
+    const int T = (int)((int64_t)Ttot * (split + 1) / splits) - t_begin;
 
-    auto load_tile = [&](int stage, int t) {
+    auto load_tile = [&](int stage, int tt) {
+        const int t = tt + t_begin;
         const int s = t / ktiles;
         const int k0 = (t - s * ktiles) * BK;
         const double* Ap = Ab + (int64_t)s * sa_seg;
         const double* Bp = Bb + (int64_t)s * sb_seg;
         double* as = As + stage * AL::size;
         double* bs = Bs + stage * BL::size;
+        if constexpr (V16) {
+            // A tile: BM x BK in 16-byte chunks (2 doubles along the contiguous dim)
+#pragma unroll
+            for (int r = 0; r < (BM * BK) / (2 * THREADS); ++r) {
+                const int idx = tid + r * THREADS;
+                int i, j;
+                if (!TA) { i = idx / (BK / 2); j = (idx % (BK / 2)) * 2; } else { j = idx / (BM / 2); i = (idx % (BM / 2)) * 2; }
+                const int gm = m0 + i, gk = k0 + j;
+                const bool ok = (gm < M) && (gk < K);
+                const double* src = TA ? (Ap + (int64_t)(ok ? gk : 0) * lda + (ok ? gm : 0))
+                                       : (Ap + (int64_t)(ok ? gm : 0) * lda + (ok ? gk : 0));
+                double* dst = TA ? (as + j * AL::ld + i) : (as + i * AL::ld + j);
+                cp_async16(dst, src, ok);
+            }
+#pragma unroll
+            for (int r = 0; r < (BK * BN) / (2 * THREADS); ++r) {
+                const int idx = tid + r * THREADS;
+                int j, c;
+                if (!TB) { j = idx / (BN / 2); c = (idx % (BN / 2)) * 2; } else { c = idx / (BK / 2); j = (idx % (BK / 2)) * 2; }
+                const int gk = k0 + j, gn = n0 + c;
+                const bool ok = (gk < K) && (gn < N);
+                const double* src = TB ? (Bp + (int64_t)(ok ? gn : 0) * ldb + (ok ? gk : 0))
+                                       : (Bp + (int64_t)(ok ? gk : 0) * ldb + (ok ? gn : 0));
+                double* dst = TB ? (bs + c * BL::ld + j) : (bs + j * BL::ld + c);
+                cp_async16(dst, src, ok);
+            }
+            return;
+        }
         // A tile: BM x BK
 #pragma unroll
         for (int r = 0; r < (BM * BK) / THREADS; ++r) {
@@ -171,42 +211,92 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     }
 }
 
-template <bool TA, bool TB>
+__global__ void k_split_reduce(const double* __restrict__ part, int splits, int64_t split_stride, int M,
+                               int N, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nbatch,
+                               double beta) {
+    const int64_t per = (int64_t)M * N, total = per * nbatch;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = e / per, rem = e - z * per;
+        const int64_t i = rem / N, j = rem - i * N;
+        const double* p = part + z * sc_batch + i * ldc + j;   // partials share C's layout
+        double s = 0.0;
+        for (int q = 0; q < splits; ++q) s += p[(int64_t)q * split_stride];
+        double* c = C + z * sc_batch + i * ldc + j;
+        *c = (beta != 0.0) ? (s + beta * *c) : s;
+    }
+}
+
+template <bool TA, bool TB, bool V16>
 static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
                          int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s,
                          double* C, int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta,
-                         cudaStream_t st) {
+                         int splits, double* part, int64_t split_stride, cudaStream_t st) {
     using namespace g64;
     const size_t smem = sizeof(double) * STAGES * (ALayout<TA>::size + BLayout<TB>::size);
     static bool configured = false;
     if (!configured) {
-        KB_CUDA(cudaFuncSetAttribute(k_dgemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        KB_CUDA(cudaFuncSetAttribute(k_dgemm<TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         configured = true;
     }
-    dim3 grid((unsigned)cdiv(n, BN), (unsigned)cdiv(m, BM), (unsigned)nbatch);
+    dim3 grid((unsigned)cdiv(n, BN), (unsigned)cdiv(m, BM), (unsigned)(nbatch * splits));
     const double nb = (double)nbatch, ns = (double)nseg;
     ProfScope ps(st, PROF_DGEMM, 8.0 * nb * (ns * ((double)m * k + (double)k * n) + (double)m * n),
                  2.0 * m * n * (double)k * nb * ns);
-    k_dgemm<TA, TB><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
-                                                 C, ldc, sc_b, nseg, beta);
+    if (splits == 1) {
+        k_dgemm<TA, TB, V16><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C,
+                                                          ldc, sc_b, nseg, beta, 1, 0);
+    } else {
+        k_dgemm<TA, TB, V16><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
+                                                          part, ldc, sc_b, nseg, 0.0, splits, split_stride);
+        KB_LAUNCH_CHECK();
+        const int64_t total = (int64_t)m * n * nbatch;
+        k_split_reduce<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(
+            part, splits, split_stride, m, n, C, ldc, sc_b, nbatch, beta);
+    }
     KB_LAUNCH_CHECK();
+}
+
+// Number of K splits so that the grid fills >= 2 waves of 2 CTAs/SM.
+int dgemm_splits(int m, int n, int k, int nbatch, int nseg) {
+    using namespace g64;
+    const int64_t tiles = cdiv(n, BN) * cdiv(m, BM) * (int64_t)nbatch;
+    const int64_t ktot = cdiv(k, BK) * (int64_t)nseg;
+    int s = 1;
+    while (tiles * s < 4 * kSMs && ktot / (s * 2) >= 8) s *= 2;
+    return s;
 }
 
 void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
            int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
-           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st) {
+           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
+           double* part, int64_t part_doubles) {
     KB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && nbatch >= 1 && nseg >= 1, "dgemm: bad sizes");
-    KB_REQUIRE(nbatch <= 65535, "dgemm: too many batches (%d)", nbatch);
     if (m == 0 || n == 0) return;
-    if (!ta && !tb)
-        launch_dgemm<false, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
-    else if (!ta && tb)
-        launch_dgemm<false, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
-    else if (ta && !tb)
-        launch_dgemm<true, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
-    else
-        launch_dgemm<true, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st);
+    int splits = dgemm_splits(m, n, k, nbatch, nseg);
+    // partials use C's layout at split_stride apart
+    const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;
+    if (part == nullptr || (int64_t)splits * span > part_doubles) splits = 1;
+    KB_REQUIRE(nbatch * splits <= 65535, "dgemm: too many batches (%d)", nbatch);
+    auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    const bool v16 = al16(A) && al16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (sa_b % 2 == 0) &&
+                     (sa_s % 2 == 0) && (sb_b % 2 == 0) && (sb_s % 2 == 0) && (m % 2 == 0) &&
+                     (n % 2 == 0) && (k % 2 == 0);
+#define KB_DG(TA_, TB_)                                                                              \
+    do {                                                                                             \
+        if (v16)                                                                                     \
+            launch_dgemm<TA_, TB_, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc,     \
+                                         sc_b, nbatch, nseg, beta, splits, part, span, st);          \
+        else                                                                                         \
+            launch_dgemm<TA_, TB_, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc,    \
+                                          sc_b, nbatch, nseg, beta, splits, part, span, st);         \
+    } while (0)
+    if (!ta && !tb) KB_DG(false, false);
+    else if (!ta && tb) KB_DG(false, true);
+    else if (ta && !tb) KB_DG(true, false);
+    else KB_DG(true, true);
+#undef KB_DG
 }
 
 }  // namespace kb

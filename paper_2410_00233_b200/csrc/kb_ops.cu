@@ -50,55 +50,95 @@ k_diag_partial(const T* __restrict__ X, int n, int center, int L, int rb_rows,
     }
 }
 
-// One-pass variant: each CTA owns 8 consecutive diagonals over ALL rows, so
-// every diagonal sum is complete inside one CTA (no cross-CTA partials, no
-// counters; deterministic).  Lane layout: tid&7 = diagonal, tid>>3 = row
-// group; for a fixed row the 8 diagonals are 8 consecutive columns (one
-// 32-byte sector), so each warp load moves 4 full sectors.
+// Segmented variant used by the R(A) product: a CTA owns 32 consecutive
+// diagonals (lane = diagonal, so a warp load is one 128-byte row segment)
+// over one of RA_SEGS row segments (warp = row phase, 8 rows in flight per
+// row step, 16+ independent loads per thread at n >= 1024).  The last CTA of
+// a diagonal chunk sums the RA_SEGS partials in fixed order (deterministic).
+constexpr int RA_SEGS = 8;
+
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_diag_sums(const T* __restrict__ X, int n, int center, int L, double* __restrict__ w) {
-    __shared__ double red[32][9];
-    const int du = threadIdx.x & 7, grp = threadIdx.x >> 3;
-    const int u = blockIdx.x * 8 + du;
+k_diag_seg(const T* __restrict__ X, int n, int center, int L, double* __restrict__ part,
+           double* __restrict__ w, unsigned* counters) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int u = blockIdx.x * 32 + lane;
     const int d = u - center;
+    const int seg = blockIdx.y, nseg = gridDim.y;
+    const int s0 = (int)((int64_t)n * seg / nseg), s1 = (int)((int64_t)n * (seg + 1) / nseg);
     double acc = 0.0;
     if (u < L) {
-        const int lo = max(0, -d), hi = min(n, n - d);
-        int a = lo + ((grp - lo) % 32 + 32) % 32;   // first row >= lo with a % 32 == grp
-#pragma unroll 8
-        for (; a < hi; a += 32) acc += (double)__ldg(X + (int64_t)a * n + (a + d));
+        const int lo = max(s0, -d), hi = min(s1, n - d);
+        const T* p = X + (int64_t)lo * n + (lo + d);
+        const int64_t step = 8 * (int64_t)(n + 1);
+        int a = lo + warp;
+        p += (int64_t)warp * (n + 1);
+        for (; a + 24 < hi; a += 32, p += 4 * step) {   // 4 independent loads per trip
+            const T v0 = __ldg(p), v1 = __ldg(p + step), v2 = __ldg(p + 2 * step), v3 = __ldg(p + 3 * step);
+            acc += (double)v0;
+            acc += (double)v1;
+            acc += (double)v2;
+            acc += (double)v3;
+        }
+        for (; a < hi; a += 8, p += step) acc += (double)__ldg(p);
     }
-    red[grp][du] = acc;
+    red[warp][lane] = acc;
     __syncthreads();
-    if (threadIdx.x < 8 && blockIdx.x * 8 + threadIdx.x < L) {
-        double s = 0.0;
+    if (warp == 0 && u < L) {
+        double t = 0.0;
 #pragma unroll
-        for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
-        w[blockIdx.x * 8 + threadIdx.x] = s;
+        for (int q = 0; q < 8; ++q) t += red[q][lane];
+        part[(int64_t)seg * L + u] = t;
+    }
+    if (last_block_ticket(&counters[blockIdx.x], nseg)) {
+        if (warp == 0 && u < L) {
+            double t = 0.0;
+            for (int q = 0; q < nseg; ++q) t += __ldcg(&part[(int64_t)q * L + u]);
+            w[u] = t;
+        }
     }
 }
 
-// z[c] = sum_r M[r, c] w[r], one CTA per 8 columns over all rows (one pass).
+// z[c] = sum_r M[r, c] w[r]: CTA = 32 columns x one row segment (same layout).
 template <typename TM>
 __global__ void __launch_bounds__(256)
-k_colsum_full(const TM* __restrict__ M, int64_t ld, int rows, int cols, const double* __restrict__ w,
-              double* __restrict__ z) {
-    __shared__ double red[32][9];
-    const int dc = threadIdx.x & 7, grp = threadIdx.x >> 3;
-    const int c = blockIdx.x * 8 + dc;
+k_colsum_seg(const TM* __restrict__ M, int64_t ld, int rows, int cols, const double* __restrict__ w,
+             double* __restrict__ part, double* __restrict__ z, unsigned* counters) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + lane;
+    const int seg = blockIdx.y, nseg = gridDim.y;
+    const int r0 = (int)((int64_t)rows * seg / nseg), r1 = (int)((int64_t)rows * (seg + 1) / nseg);
     double acc = 0.0;
     if (c < cols) {
-#pragma unroll 8
-        for (int r = grp; r < rows; r += 32) acc += (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
+        int r = r0 + warp;
+        for (; r + 24 < r1; r += 32) {
+            const double a0 = (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
+            const double a1 = (double)__ldg(M + (int64_t)(r + 8) * ld + c) * __ldg(w + r + 8);
+            const double a2 = (double)__ldg(M + (int64_t)(r + 16) * ld + c) * __ldg(w + r + 16);
+            const double a3 = (double)__ldg(M + (int64_t)(r + 24) * ld + c) * __ldg(w + r + 24);
+            acc += a0;
+            acc += a1;
+            acc += a2;
+            acc += a3;
+        }
+        for (; r < r1; r += 8) acc += (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
     }
-    red[grp][dc] = acc;
+    red[warp][lane] = acc;
     __syncthreads();
-    if (threadIdx.x < 8 && blockIdx.x * 8 + threadIdx.x < cols) {
-        double s = 0.0;
+    if (warp == 0 && c < cols) {
+        double t = 0.0;
 #pragma unroll
-        for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
-        z[blockIdx.x * 8 + threadIdx.x] = s;
+        for (int q = 0; q < 8; ++q) t += red[q][lane];
+        part[(int64_t)seg * cols + c] = t;
+    }
+    if (last_block_ticket(&counters[blockIdx.x], nseg)) {
+        if (warp == 0 && c < cols) {
+            double t = 0.0;
+            for (int q = 0; q < nseg; ++q) t += __ldcg(&part[(int64_t)q * cols + c]);
+            z[c] = t;
+        }
     }
 }
 
@@ -215,7 +255,10 @@ struct VecIO<T, 1> {
 };
 
 // One pass over the basis.  smem: [L toeplitz] [m coef] [8 x (m+2) warp acc] [m+4 red]
-template <typename T, int VEC>
+// Each thread owns R groups of VEC consecutive elements per tile (groups
+// strided by 256*VEC so every warp load is contiguous); per basis vector it
+// issues R independent vector loads and does ONE warp reduction per tile.
+template <typename T, int VEC, int R>
 __global__ void __launch_bounds__(256)
 k_reorth(const double* zsrc, int mode, int side, int center, int L,
          const T* __restrict__ prev, const double* __restrict__ beta_p,
@@ -240,89 +283,107 @@ k_reorth(const double* zsrc, int mode, int side, int center, int L,
     Gen<T> g{zsrc, zs, prev, beta_p ? (T)(*beta_p) : T(0), mode, side, center, L};
     const T tdiv = div_p ? (T)(*div_p) : T(1);
 
-    const int64_t tile_elems = 256 * VEC;
-    const int64_t ntiles = (len + tile_elems - 1) / tile_elems;
+    constexpr int64_t GROUP = 256 * VEC;
+    constexpr int64_t TILE = GROUP * R;
+    const int64_t ntiles = (len + TILE - 1) / TILE;
+    double ysq = 0.0, vsq = 0.0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t e0 = tile * tile_elems + (int64_t)threadIdx.x * VEC;
-        const bool full = (e0 + VEC <= len);
-        double v[VEC];
-        double yy = 0.0;
+        const int64_t base = tile * TILE + (int64_t)threadIdx.x * VEC;
+        double v[R][VEC];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-            const int64_t e = e0 + q;
-            if (e < len) {
-                T yv = g.y(e);
-                T vv = prev ? sub_rn(yv, mul_rn(g.beta, prev[e])) : yv;
-                v[q] = (double)vv;
-                yy += (double)yv * (double)yv;
-            } else {
-                v[q] = 0.0;
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int64_t e = base + r * GROUP + q;
+                if (e < len) {
+                    const T yv = g.y(e);
+                    const T vv = prev ? sub_rn(yv, mul_rn(g.beta, prev[e])) : yv;
+                    v[r][q] = (double)vv;
+                    ysq += (double)yv * (double)yv;
+                } else {
+                    v[r][q] = 0.0;
+                }
             }
         }
         if (proj) {
-#pragma unroll 4
+#pragma unroll 2
             for (int i = 0; i < m; ++i) {
-                double s[VEC];
-                const T* Si = S + (int64_t)i * ld + e0;
-                if (full) {
-                    VecIO<T, VEC>::load(Si, s);
-                } else {
+                const T* Si = S + (int64_t)i * ld + base;
+                double sv[R][VEC];
 #pragma unroll
-                    for (int q = 0; q < VEC; ++q) s[q] = (e0 + q < len) ? (double)Si[q] : 0.0;
+                for (int r = 0; r < R; ++r) {
+                    const int64_t e0 = base + r * GROUP;
+                    if (e0 + VEC <= len) {
+                        VecIO<T, VEC>::load(Si + r * GROUP, sv[r]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) sv[r][q] = (e0 + q < len) ? (double)Si[r * GROUP + q] : 0.0;
+                    }
                 }
                 const double c = coef[i];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) v[q] -= c * s[q];
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) v[r][q] -= c * sv[r][q];
             }
         }
         if (dots) {
-#pragma unroll 4
+#pragma unroll 2
             for (int i = 0; i < m; ++i) {
-                double s[VEC];
-                const T* Si = S + (int64_t)i * ld + e0;
-                if (full) {
-                    VecIO<T, VEC>::load(Si, s);
-                } else {
+                const T* Si = S + (int64_t)i * ld + base;
+                double sv[R][VEC];
 #pragma unroll
-                    for (int q = 0; q < VEC; ++q) s[q] = (e0 + q < len) ? (double)Si[q] : 0.0;
+                for (int r = 0; r < R; ++r) {
+                    const int64_t e0 = base + r * GROUP;
+                    if (e0 + VEC <= len) {
+                        VecIO<T, VEC>::load(Si + r * GROUP, sv[r]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) sv[r][q] = (e0 + q < len) ? (double)Si[r * GROUP + q] : 0.0;
+                    }
                 }
                 double d = 0.0;
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) d += s[q] * v[q];
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) d += sv[r][q] * v[r][q];
                 d = warp_sum(d);
                 if (lane == 0) accw[warp * W + i] += d;
             }
         }
-        double vv2 = 0.0;
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) vv2 += v[q] * v[q];
-        vv2 = warp_sum(vv2);
-        yy = warp_sum(yy);
-        if (lane == 0) {
-            accw[warp * W + m] += vv2;
-            accw[warp * W + m + 1] += yy;
-        }
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) vsq += v[r][q] * v[r][q];
         if (out) {
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-                const int64_t e = e0 + q;
-                if (e < len) out[e] = div_rn((T)v[q], tdiv);
-            }
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) {
+                    const int64_t e = base + r * GROUP + q;
+                    if (e < len) out[e] = div_rn((T)v[r][q], tdiv);
+                }
         }
+    }
+    vsq = warp_sum(vsq);
+    ysq = warp_sum(ysq);
+    if (lane == 0) {
+        accw[warp * W + m] += vsq;
+        accw[warp * W + m + 1] += ysq;
     }
     __syncthreads();
     for (int j = threadIdx.x; j < W; j += blockDim.x) {
-        double s = 0.0;
+        double t = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += accw[q * W + j];
-        part[(int64_t)blockIdx.x * W + j] = s;
+        for (int q = 0; q < 8; ++q) t += accw[q * W + j];
+        part[(int64_t)blockIdx.x * W + j] = t;
     }
     if (last_block_ticket(counter, gridDim.x)) {
         for (int j = warp; j < W; j += 8) {
-            double s = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(&part[(int64_t)b * W + j]);
-            s = warp_sum(s);
-            if (lane == 0) fin[j] = s;
+            double t = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(&part[(int64_t)b * W + j]);
+            t = warp_sum(t);
+            if (lane == 0) fin[j] = t;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -442,19 +503,24 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
         const void* Mv;
         ra_geom(op, transpose, ci, Li, co, Lo, Mv);
         const int n = op->side;
-        // diagonal sums (one pass, 8 diagonals per CTA)
+        const int segs = std::max(1, std::min(RA_SEGS, n / 64));
+        KB_REQUIRE(cdiv(Li, 32) <= 64 && cdiv(Lo, 32) <= 64, "R(A): PSF support too large (%d x %d)",
+                   op->kh, op->kw);
+        // diagonal sums: 32 diagonals x 1 row segment per CTA
         {
             double band = 0;
             for (int u = 0; u < Li; ++u) band += std::max(n - std::abs(u - ci), 0);
             ProfScope ps(st, PROF_RA_DIAG, band * sizeof(T));
-            k_diag_sums<T><<<(unsigned)cdiv(Li, 8), 256, 0, st>>>(x, n, ci, Li, p.w);
+            k_diag_seg<T><<<dim3((unsigned)cdiv(Li, 32), segs), 256, 0, st>>>(x, n, ci, Li, p.part, p.w,
+                                                                              p.counters);
             KB_LAUNCH_CHECK();
         }
         // z = M^T w with M = K (forward) or K^T (transpose): rows Li, cols Lo
         {
+            const int segs2 = std::max(1, std::min(RA_SEGS, Li / 64));
             ProfScope ps(st, PROF_RA_COLSUM, (double)Li * Lo * sizeof(T));
-            k_colsum_full<T><<<(unsigned)cdiv(Lo, 8), 256, 0, st>>>(static_cast<const T*>(Mv), Lo, Li, Lo,
-                                                                    p.w, p.z);
+            k_colsum_seg<T><<<dim3((unsigned)cdiv(Lo, 32), segs2), 256, 0, st>>>(
+                static_cast<const T*>(Mv), Lo, Li, Lo, p.w, p.part, p.z, p.counters + 64);
             KB_LAUNCH_CHECK();
         }
         s.z = p.z;
@@ -502,8 +568,9 @@ void src_write(int dtype, const Src& s, void* y, int64_t len, cudaStream_t st) {
     KB_LAUNCH_CHECK();
 }
 
+constexpr int REORTH_R = 4;
 static int reorth_blocks(int64_t len) {
-    const int64_t tiles = cdiv(len, 256 * 4);
+    const int64_t tiles = cdiv(len, 256 * REORTH_R);   // VEC >= 1
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4 * kSMs));
 }
 
@@ -527,13 +594,13 @@ static void launch_reorth(const Src& src, const void* S, int64_t ld, int m, cons
                           double* red, const ReorthWs& ws, cudaStream_t st) {
     const int Ls = (src.mode == SRC_TOEP) ? src.L : 0;
     const size_t smem = sizeof(double) * ((size_t)Ls + m + 8 * (m + 2) + (m + 4));
-    auto kern = k_reorth<T, VEC>;
+    auto kern = k_reorth<T, VEC, REORTH_R>;
     static bool configured = false;
     if (!configured) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC)));
+    const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC * REORTH_R)));
     double vecs = (double)m + (src.prev ? 1 : 0) + (out ? 1 : 0) + (src.mode == SRC_BUFT ? 1 : 0);
     double bytes = vecs * len * sizeof(T) + (src.mode == SRC_BUF64 ? 8.0 * len : 0.0);
     ProfScope ps(st, PROF_REORTH, bytes);

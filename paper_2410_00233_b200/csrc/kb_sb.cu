@@ -21,7 +21,8 @@ namespace kb {
 
 void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
            int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
-           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st);
+           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
+           double* part = nullptr, int64_t part_doubles = 0);
 
 // ------------------------------------------------------------ map-reduce core
 constexpr int MR_THREADS = 256;
@@ -311,28 +312,34 @@ static void map_reduce(int64_t len, const F& f, const MR& mr, double* out, cudaS
 }
 
 // ---- Kronecker apply (two DMMA GEMMs) ----
+// intermediate P/Q (k blocks) + split-K partials of the reduced stage (8 x output)
+constexpr int KRON_SPLIT_MAX = 8;
 size_t kron_ws_doubles(const kb_kron* kr) {
     const int64_t a = (int64_t)kr->n1 * kr->m2, b = (int64_t)kr->m1 * kr->n2;
-    return (size_t)kr->k * (size_t)std::max(a, b);
+    const int64_t out = std::max((int64_t)kr->m1 * kr->m2, (int64_t)kr->n1 * kr->n2);
+    return (size_t)kr->k * (size_t)std::max(a, b) + (size_t)KRON_SPLIT_MAX * out + 64;
 }
 
 void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, double* tmp,
                 cudaStream_t st) {
     const int m1 = kr->m1, m2 = kr->m2, n1 = kr->n1, n2 = kr->n2, k = kr->k;
+    const int64_t pq = (int64_t)k * std::max((int64_t)n1 * m2, (int64_t)m1 * n2);
+    double* part = tmp + ((pq + 31) / 32) * 32;
+    const int64_t part_n = (int64_t)KRON_SPLIT_MAX * std::max((int64_t)m1 * m2, (int64_t)n1 * n2);
     if (!transpose) {
         // P_i = Xr G_i            (n1 x m2), Xr = x as n1 x n2, G_i n2 x m2
         dgemm(0, 0, n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
               (int64_t)n1 * m2, k, 1, 0.0, st);
         // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1
         dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
-              0, 1, k, 0.0, st);
+              0, 1, k, 0.0, st, part, part_n);
     } else {
         // Q_i = Yr G_i^T          (m1 x n2), Yr = y as m1 x m2
         dgemm(0, 1, m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
               (int64_t)m1 * n2, k, 1, 0.0, st);
         // Xr = sum_i F_i Q_i      (n1 x n2)
         dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
-              0, 1, k, 0.0, st);
+              0, 1, k, 0.0, st, part, part_n);
     }
 }
 

@@ -60,6 +60,20 @@ def main():
         t = timeit(fn)
         print(f"{name:28s} {t * 1e3:8.3f} ms  {flops / t / 1e12:6.2f} TFLOP/s")
 
+    # the real Kronecker apply (both stages, split-K on the reduced stage)
+    fk = f.reshape(k, n * n).contiguous()
+    gk = g.reshape(k, n * n).contiguous()
+    kr = _lib.KbKron(n, n, n, n, k, fk.data_ptr(), gk.data_ptr())
+    nb = C.c_size_t()
+    lib.kb_kron_workspace_bytes(C.byref(kr), C.byref(nb))
+    wsb = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+    xv = torch.randn(n * n, dtype=torch.float64, device=dev)
+    yv = torch.empty(n * n, dtype=torch.float64, device=dev)
+    for tr in (0, 1):
+        t = timeit(lambda: lib.kb_kron_apply(C.byref(kr), xv.data_ptr(), yv.data_ptr(), tr, wsb.data_ptr(),
+                                              nb.value, st))
+        print(f"kron_apply transpose={tr}       {t * 1e3:8.3f} ms  {2 * flops / t / 1e12:6.2f} TFLOP/s")
+
     # correctness spot check of ours vs torch
     ours_stage1()
     ref = torch.matmul(x.unsqueeze(0), g)
