@@ -119,68 +119,120 @@ static void validate_op(const kb_operator* op) {
 static int64_t op_len(const kb_operator* op) { return std::max(op->rows, op->cols); }
 
 // ------------------------------------------------------------------ eGKB
+// The whole bidiagonalisation (lowrank.py:207-303) is ONE CUDA graph: an
+// init stage (s1 = y0/|y0|, q1 = B^T s1/alpha1) followed by a conditional
+// WHILE node whose body is one Golub-Kahan iteration (two operator products,
+// the reorthogonalisation passes) plus a one-thread control kernel that
+// applies the reference's breakdown tests and nu rank rule on the device and
+// sets the loop condition.  Kernels address basis slot `done` through
+// device-resolved references, so the body is captured once and replayed.
+// The host reads the trace back once, after the graph.  A host-driven
+// ("eager") replay of the same body is used when kernel profiling is on.
+enum { H_DONE = 0, H_FIRED, H_REASON, H_STOP, H_BREAK, H_TBREAK, H_OVERFLOW, H_ERR, H_NA, H_NT, H_NN,
+       H_COUNT = 16 };
+
+struct EgkbCtl {
+    int* hdr;
+    double *alphas, *ts, *zetas, *nus;
+    const double *t_ptr, *u2_ptr, *a_ptr, *p2_ptr;
+    double tol, tau;
+    int k_max, p, k_min, cap;
+    cudaGraphConditionalHandle handle;
+    int use_cond;
+};
+
+__global__ void k_egkb_init(EgkbCtl c) {
+    if (threadIdx.x != 0) return;
+    int* h = c.hdr;
+    for (int i = 0; i < H_COUNT; ++i) h[i] = 0;
+    h[H_FIRED] = -1;
+    h[H_DONE] = 1;
+    const double t1 = *c.t_ptr, a1 = *c.a_ptr;   // here: |y0| and |B^T s1|
+    c.ts[0] = t1;
+    c.alphas[0] = a1;
+    c.zetas[0] = a1 * t1;
+    c.nus[0] = 1e308;
+    h[H_NA] = h[H_NT] = h[H_NN] = 1;
+    if (t1 == 0.0) h[H_ERR] = 1;          // ValidationError: zero starting vector
+    else if (a1 == 0.0) h[H_ERR] = 2;     // NumericalError: operator annihilates y0
+    if (h[H_ERR]) h[H_STOP] = 1;
+    if (c.use_cond) cudaGraphSetConditional(c.handle, h[H_STOP] ? 0u : 1u);
+}
+
+__global__ void k_egkb_control(EgkbCtl c) {
+    if (threadIdx.x != 0) return;
+    int* h = c.hdr;
+    const double t_new = *c.t_ptr, unorm = sqrt(*c.u2_ptr);
+    const double a_new = *c.a_ptr, pre = sqrt(*c.p2_ptr);
+    if (t_new <= c.tol * unorm) {                        // lowrank.py:243-246
+        h[H_BREAK] = h[H_TBREAK] = 1;
+        h[H_STOP] = 1;
+    } else if (a_new <= c.tol * pre) {                   // lowrank.py:255-259
+        h[H_BREAK] = 1;
+        c.ts[h[H_NT]++] = t_new;
+        h[H_STOP] = 1;
+    } else {                                             // lowrank.py:260-277
+        c.ts[h[H_NT]++] = t_new;
+        c.alphas[h[H_NA]++] = a_new;
+        const double zeta = a_new * t_new;
+        const double nu = sqrt(zeta * c.zetas[h[H_NN] - 1]);
+        c.zetas[h[H_NN]] = zeta;
+        c.nus[h[H_NN]] = nu;
+        h[H_NN]++;
+        const int done = ++h[H_DONE];
+        if (h[H_FIRED] < 0) {
+            const double prev = c.nus[h[H_NN] - 2];
+            if (nu > prev) {
+                h[H_FIRED] = max(done - 1, c.k_min);
+                h[H_REASON] = KB_STOP_NU_ROSE;
+            } else if (nu < c.tau) {
+                h[H_FIRED] = max(done, c.k_min);
+                h[H_REASON] = KB_STOP_NU_BELOW_TOL;
+            }
+        }
+        const int limit = h[H_FIRED] >= 0 ? h[H_FIRED] + c.p + 1 : c.k_max + 1;
+        if (done >= limit) h[H_STOP] = 1;
+        if (done + 1 > c.cap) { h[H_STOP] = 1; h[H_OVERFLOW] = 1; }
+    }
+    if (c.use_cond) cudaGraphSetConditional(c.handle, h[H_STOP] ? 0u : 1u);
+}
+
 struct EgkbWs {
     OpPlan plan;
     ReorthWs rw;
-    double* red[6];     // s1 s2 s3 q1 q2 q3, each capacity + 8
-    double* cur;        // [0]=alpha, [1]=t
-    double* hist;       // [4]: t, |u|^2, alpha, |B^T s|^2
+    double* red_s;      // coefficient slots (capacity + 8)
+    double* red_s2;
+    double* red_q;
+    double* red_q2;
+    double* fx;         // fixed scalars: [0..15] s-step, [16..31] q-step, [32..47] init
+    int* hdr;
+    double* trace;      // alphas | ts | zetas | nus   (4 x capacity)
+    void* y0slot;       // private copy of y0 (graph input)
 };
 
 static void egkb_ws_size(const kb_operator* op, int capacity, Sizer& s) {
     op_plan_size(op, s);
     reorth_ws_size(op_len(op), capacity + 1, s);
-    for (int i = 0; i < 6; ++i) s.take<double>(capacity + 16);
-    s.take<double>(8);
-    s.take<double>(8);
+    for (int i = 0; i < 4; ++i) s.take<double>(capacity + 16);
+    s.take<double>(64);
+    s.take<int>(H_COUNT);
+    s.take<double>(4 * (size_t)capacity);
+    s.take<double>((size_t)op->rows);
 }
 
 static EgkbWs egkb_ws_make(const kb_operator* op, int capacity, Arena& a) {
     EgkbWs w;
     w.plan = op_plan_make(op, a);
     w.rw = reorth_ws_make(op_len(op), capacity + 1, a);
-    for (int i = 0; i < 6; ++i) w.red[i] = a.take<double>(capacity + 16);
-    w.cur = a.take<double>(8);
-    w.hist = a.take<double>(8);
+    w.red_s = a.take<double>(capacity + 16);
+    w.red_s2 = a.take<double>(capacity + 16);
+    w.red_q = a.take<double>(capacity + 16);
+    w.red_q2 = a.take<double>(capacity + 16);
+    w.fx = a.take<double>(64);
+    w.hdr = a.take<int>(H_COUNT);
+    w.trace = a.take<double>(4 * (size_t)capacity);
+    w.y0slot = a.take<double>((size_t)op->rows);
     return w;
-}
-
-// One half step: out = normalise(reorth(y - beta*prev)) with y = B x (or B^T x).
-// Returns the device pointer of the new norm (t or alpha) and of |y|^2.
-struct HalfOut {
-    const double* norm;
-    const double* ynorm2;
-};
-
-static HalfOut half_step(const kb_operator* op, EgkbWs& w, int transpose, const void* x,
-                         const void* prev, const double* beta, const void* S, int64_t ld, int m,
-                         int passes, void* out, double** red, cudaStream_t st) {
-    const int64_t len = transpose ? op->cols : op->rows;
-    Src src = op_source(w.plan, x, transpose, st);
-    src.prev = prev;
-    src.beta = beta;
-    HalfOut h;
-    reorth_pass(op->dtype, src, S, ld, m, nullptr, nullptr, m > 0, nullptr, nullptr, len, red[0],
-                w.rw, st);
-    h.ynorm2 = red[0] + m + 1;
-    if (m == 0) {
-        h.norm = red[0] + m + 3;
-        reorth_pass(op->dtype, src, S, ld, 0, nullptr, nullptr, false, out, h.norm, len, red[2], w.rw, st);
-    } else if (passes >= 2) {
-        reorth_pass(op->dtype, src, S, ld, m, red[0], nullptr, true, nullptr, nullptr, len, red[1],
-                    w.rw, st);
-        h.norm = red[1] + m + 2;
-        reorth_pass(op->dtype, src, S, ld, m, red[0], red[1], false, out, h.norm, len, red[2], w.rw, st);
-    } else {
-        // classical GS: write the projected vector, then normalise in place
-        reorth_pass(op->dtype, src, S, ld, m, red[0], nullptr, false, out, nullptr, len, red[1], w.rw, st);
-        h.norm = red[1] + m + 3;
-        Src self;
-        self.z = static_cast<const double*>(out);
-        self.mode = SRC_BUFT;
-        reorth_pass(op->dtype, self, S, ld, 0, nullptr, nullptr, false, out, h.norm, len, red[2], w.rw, st);
-    }
-    return h;
 }
 
 static double eps_of(int dtype) { return dtype == KB_F32 ? 1.1920928955078125e-07 : 2.220446049250313e-16; }
@@ -189,6 +241,174 @@ static int egkb_capacity(const kb_egkb_config* c) {
     // Loop limit is fired_k + p + 1 with fired_k <= max(k_max, k_min), else
     // k_max + 1; the left basis may hold one more vector than iterations.
     return std::max(c->k_max, c->k_min) + c->p + 3;
+}
+
+// One half step on device-resolved slots: out[done] = normalise(reorth(B x - beta prev)).
+// Returns pointers to the new norm (t or alpha) and |B x|^2 (fixed addresses).
+static void half_step(const kb_operator* op, EgkbWs& w, int transpose, const VecRef& x, const VecRef& prev,
+                      const double* beta, const void* S, int64_t ld, const MRef& m, int passes,
+                      const VecRef& out, double* red1, double* red2, double* fx, const double** norm,
+                      const double** y2, cudaStream_t st) {
+    const int64_t len = transpose ? op->cols : op->rows;
+    Src src = op_source(w.plan, x, transpose, st);
+    src.prev = prev;
+    src.beta = beta;
+    const bool proj = m.max > 0;
+    reorth_pass(op->dtype, src, S, ld, m, nullptr, nullptr, proj, VecRef(), nullptr, len, red1, fx + 0, w.rw, st);
+    *y2 = fx + 1;
+    if (!proj) {
+        *norm = fx + 3;
+        reorth_pass(op->dtype, src, S, ld, m, nullptr, nullptr, false, out, fx + 3, len, nullptr, fx + 8, w.rw, st);
+    } else if (passes >= 2) {
+        reorth_pass(op->dtype, src, S, ld, m, red1, nullptr, true, VecRef(), nullptr, len, red2, fx + 4, w.rw, st);
+        *norm = fx + 6;   // Pythagorean norm after the second projection
+        reorth_pass(op->dtype, src, S, ld, m, red1, red2, false, out, fx + 6, len, nullptr, fx + 8, w.rw, st);
+    } else {
+        // one classical GS pass: write the projected vector, then normalise in place
+        reorth_pass(op->dtype, src, S, ld, m, red1, nullptr, false, out, nullptr, len, nullptr, fx + 4, w.rw, st);
+        *norm = fx + 7;
+        Src self;
+        self.z = out;
+        self.mode = SRC_BUFT;
+        reorth_pass(op->dtype, self, S, ld, MRef::fixed(0), nullptr, nullptr, false, out, fx + 7, len, nullptr,
+                    fx + 8, w.rw, st);
+    }
+}
+
+struct EgkbPlan {
+    const kb_operator* op;
+    const kb_egkb_config* cfg;
+    kb_egkb_state* st;
+    EgkbWs w;
+    EgkbCtl ctl;
+};
+
+static void enqueue_init(EgkbPlan& P, cudaStream_t s) {
+    const kb_operator* op = P.op;
+    EgkbWs& w = P.w;
+    double* fxi = w.fx + 32;
+    // s1 = y0 / |y0|   (lowrank.py:207-210)
+    Src sy;
+    sy.z = VecRef::at(w.y0slot);
+    sy.mode = SRC_BUFT;
+    reorth_pass(op->dtype, sy, nullptr, 0, MRef::fixed(0), nullptr, nullptr, false, VecRef(), nullptr, op->rows,
+                nullptr, fxi + 0, w.rw, s);
+    reorth_pass(op->dtype, sy, nullptr, 0, MRef::fixed(0), nullptr, nullptr, false, VecRef::at(P.st->s_basis),
+                fxi + 3, op->rows, nullptr, fxi + 4, w.rw, s);
+    // q1 = B^T s1 / alpha1   (lowrank.py:211-215); alpha1 lands where the loop reads alpha
+    Src src = op_source(w.plan, VecRef::at(P.st->s_basis), 1, s);
+    double* fq = w.fx + 16;
+    reorth_pass(op->dtype, src, nullptr, 0, MRef::fixed(0), nullptr, nullptr, false, VecRef(), nullptr, op->cols,
+                nullptr, fq + 4, w.rw, s);
+    reorth_pass(op->dtype, src, nullptr, 0, MRef::fixed(0), nullptr, nullptr, false, VecRef::at(P.st->q_basis),
+                fq + 7, op->cols, nullptr, fq + 8, w.rw, s);
+    EgkbCtl c = P.ctl;
+    c.t_ptr = fxi + 3;
+    c.a_ptr = fq + 7;
+    k_egkb_init<<<1, 32, 0, s>>>(c);
+    KB_LAUNCH_CHECK();
+}
+
+static void enqueue_body(EgkbPlan& P, cudaStream_t s) {
+    const kb_operator* op = P.op;
+    const kb_egkb_config* cfg = P.cfg;
+    kb_egkb_state* st = P.st;
+    EgkbWs& w = P.w;
+    const int* done = w.hdr + H_DONE;
+    const int cap = st->capacity;
+    const int passes = cfg->reorth_passes >= 2 ? 2 : 1;
+    double* fs = w.fx;
+    double* fq = w.fx + 16;
+    const double *t_ptr, *u2, *a_ptr, *p2;
+    // s step (lowrank.py:237-247): u = B q_done-1 ; s_raw = u - alpha s_done-1 ; MGS vs S
+    MRef ms;
+    if (cfg->full_reorth) { ms.idx = done; ms.mul = 1; ms.add = 0; ms.max = cap; }
+    half_step(op, w, 0, VecRef::slot(st->q_basis, done, -1, st->ld_q), VecRef::slot(st->s_basis, done, -1, st->ld_s),
+              fq + (passes >= 2 ? 6 : 7), st->s_basis, st->ld_s, ms, passes,
+              VecRef::slot(st->s_basis, done, 0, st->ld_s), w.red_s, w.red_s2, fs, &t_ptr, &u2, s);
+    // q step (lowrank.py:249-260): B^T s_new - t q_done-1 ; MGS vs Q (always)
+    MRef mq;
+    mq.idx = done; mq.mul = 1; mq.add = 0; mq.max = cap;
+    half_step(op, w, 1, VecRef::slot(st->s_basis, done, 0, st->ld_s), VecRef::slot(st->q_basis, done, -1, st->ld_q),
+              t_ptr, st->q_basis, st->ld_q, mq, passes, VecRef::slot(st->q_basis, done, 0, st->ld_q), w.red_q,
+              w.red_q2, fq, &a_ptr, &p2, s);
+    EgkbCtl c = P.ctl;
+    c.t_ptr = t_ptr;
+    c.u2_ptr = u2;
+    c.a_ptr = a_ptr;
+    c.p2_ptr = p2;
+    k_egkb_control<<<1, 32, 0, s>>>(c);
+    KB_LAUNCH_CHECK();
+}
+
+// graph cache (one entry per distinct argument set)
+struct GraphKey {
+    kb_operator op;
+    kb_egkb_config cfg;
+    void *s_basis, *q_basis, *ws;
+    int64_t ld_s, ld_q;
+    int cap;
+    size_t ws_bytes;
+    bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+};
+static std::vector<GraphEntry> g_graphs;
+static cudaStream_t g_capture_stream = nullptr;
+
+static cudaGraphExec_t build_graph(EgkbPlan& P) {
+    if (!g_capture_stream) KB_CUDA(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = g_capture_stream;
+    const bool prof = g_prof;
+    g_prof = false;   // no event timing inside a graph
+    cudaGraph_t g = nullptr;
+    try {
+        KB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t capg;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphConditionalHandle h;
+        KB_CUDA(cudaGraphConditionalHandleCreate(&h, capg, 1, cudaGraphCondAssignDefault));
+        P.ctl.handle = h;
+        P.ctl.use_cond = 1;
+        enqueue_init(P, cs);
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        KB_CUDA(cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        KB_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+        KB_CUDA(cudaStreamEndCapture(cs, &g));
+        // body: one iteration, captured into the while node's graph
+        KB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_body(P, cs);
+        cudaGraph_t body_out;
+        KB_CUDA(cudaStreamEndCapture(cs, &body_out));
+        cudaGraphExec_t exec;
+        KB_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        KB_CUDA(cudaGraphDestroy(g));
+        g_prof = prof;
+        return exec;
+    } catch (...) {
+        g_prof = prof;
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+            cudaGraph_t junk;
+            cudaStreamEndCapture(cs, &junk);
+            if (junk) cudaGraphDestroy(junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
 }
 
 static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const void* y0,
@@ -203,119 +423,110 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     KB_REQUIRE(st->s_basis && st->q_basis && st->alphas_host && st->ts_host && st->zetas_host &&
                    st->nus_host, "missing basis / trace buffers");
     const size_t esz = op->dtype == KB_F32 ? 4 : 8;
-    auto slot = [&](void* base, int64_t ld, int i) -> void* {
-        return static_cast<char*>(base) + (size_t)i * ld * esz;
-    };
     Arena a(wsp, ws_bytes);
-    EgkbWs w = egkb_ws_make(op, cap, a);
-    KB_CUDA(cudaMemsetAsync(w.plan.counters, 0, sizeof(unsigned) * w.plan.n_counters, s));
-    KB_CUDA(cudaMemsetAsync(w.rw.counter, 0, sizeof(unsigned) * 64, s));
-    static thread_local double* hp = nullptr;   // pinned scalar mailbox, allocated once per thread
-    if (hp == nullptr) KB_CUDA(cudaMallocHost(&hp, sizeof(double) * 8));
+    EgkbPlan P;
+    P.op = op;
+    P.cfg = cfg;
+    P.st = st;
+    P.w = egkb_ws_make(op, cap, a);
+    EgkbCtl& c = P.ctl;
+    c.hdr = P.w.hdr;
+    c.alphas = P.w.trace;
+    c.ts = P.w.trace + cap;
+    c.zetas = P.w.trace + 2 * cap;
+    c.nus = P.w.trace + 3 * cap;
+    c.tol = cfg->break_tol >= 0 ? cfg->break_tol : std::sqrt(eps_of(op->dtype));
+    c.tau = cfg->tau;
+    c.k_max = cfg->k_max;
+    c.p = cfg->p;
+    c.k_min = cfg->k_min;
+    c.cap = cap;
+    c.handle = 0;
+    c.use_cond = 0;
 
-    const double tol = cfg->break_tol >= 0 ? cfg->break_tol : std::sqrt(eps_of(op->dtype));
-    const int passes = cfg->reorth_passes >= 2 ? 2 : 1;
-    const int64_t M = op->rows, N = op->cols;
+    KB_CUDA(cudaMemsetAsync(P.w.plan.counters, 0, sizeof(unsigned) * P.w.plan.n_counters, s));
+    KB_CUDA(cudaMemsetAsync(P.w.rw.counter, 0, sizeof(unsigned) * 64, s));
+    KB_CUDA(cudaMemcpyAsync(P.w.y0slot, y0, esz * (size_t)op->rows, cudaMemcpyDeviceToDevice, s));
 
-    // --- s1 = y0 / |y0|   (lowrank.py:207-210)
-    Src sy;
-    sy.z = static_cast<const double*>(y0);
-    sy.mode = SRC_BUFT;
-    reorth_pass(op->dtype, sy, nullptr, 0, 0, nullptr, nullptr, false, nullptr, nullptr, M, w.red[0], w.rw, s);
-    scalars(s, w.red[0] + 3, w.cur + 1, w.red[0] + 3, w.hist + 0);
-    reorth_pass(op->dtype, sy, nullptr, 0, 0, nullptr, nullptr, false, slot(st->s_basis, st->ld_s, 0),
-                w.cur + 1, M, w.red[1], w.rw, s);
-    // --- q1 = B^T s1 / alpha1   (lowrank.py:211-215)
-    {
-        Src src = op_source(w.plan, slot(st->s_basis, st->ld_s, 0), 1, s);
-        reorth_pass(op->dtype, src, nullptr, 0, 0, nullptr, nullptr, false, nullptr, nullptr, N, w.red[3], w.rw, s);
-        scalars(s, w.red[3] + 3, w.cur + 0, w.red[3] + 3, w.hist + 2);
-        reorth_pass(op->dtype, src, nullptr, 0, 0, nullptr, nullptr, false, slot(st->q_basis, st->ld_q, 0),
-                    w.cur + 0, N, w.red[4], w.rw, s);
+    static thread_local char* hbuf = nullptr;   // pinned trace mailbox
+    static thread_local size_t hbuf_bytes = 0;
+    const size_t need = sizeof(int) * H_COUNT + sizeof(double) * 4 * (size_t)cap;
+    if (hbuf_bytes < need) {
+        if (hbuf) cudaFreeHost(hbuf);
+        KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hbuf), need));
+        hbuf_bytes = need;
     }
-    KB_CUDA(cudaMemcpyAsync(hp, w.hist, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+    int* hh = reinterpret_cast<int*>(hbuf);
+    double* ht = reinterpret_cast<double*>(hbuf + sizeof(int) * H_COUNT);
+
+    if (!g_prof) {
+        GraphKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.op = *op;
+        key.cfg = *cfg;
+        key.s_basis = st->s_basis;
+        key.q_basis = st->q_basis;
+        key.ws = wsp;
+        key.ld_s = st->ld_s;
+        key.ld_q = st->ld_q;
+        key.cap = cap;
+        key.ws_bytes = ws_bytes;
+        cudaGraphExec_t exec = nullptr;
+        for (auto& e : g_graphs)
+            if (e.key == key) exec = e.exec;
+        if (!exec) {
+            exec = build_graph(P);
+            if (g_graphs.size() >= 16) {
+                cudaGraphExecDestroy(g_graphs.front().exec);
+                g_graphs.erase(g_graphs.begin());
+            }
+            g_graphs.push_back({key, exec});
+        }
+        KB_CUDA(cudaGraphLaunch(exec, s));
+    } else {
+        // eager replay of the same kernels (per-kernel event timing)
+        enqueue_init(P, s);
+        for (;;) {
+            KB_CUDA(cudaMemcpyAsync(hh, P.w.hdr, sizeof(int) * H_COUNT, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            if (hh[H_STOP]) break;
+            enqueue_body(P, s);
+        }
+    }
+    KB_CUDA(cudaMemcpyAsync(hh, P.w.hdr, sizeof(int) * H_COUNT, cudaMemcpyDeviceToHost, s));
+    KB_CUDA(cudaMemcpyAsync(ht, P.w.trace, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost, s));
     KB_CUDA(cudaStreamSynchronize(s));
-    const double t1 = hp[0];
-    if (t1 == 0.0) {
+    if (hh[H_ERR] == 1) {
         set_error("starting vector must be nonzero");
         throw Fail{KB_EVALIDATION};
     }
-    const double alpha1 = hp[2];
-    if (alpha1 == 0.0) {
+    if (hh[H_ERR] == 2) {
         set_error("operator annihilates the starting vector");
         throw Fail{KB_ENUMERICAL};
     }
-    std::vector<double> alphas{alpha1}, ts{t1}, zetas{alpha1 * t1}, nus{1e308};
-
-    int fired = -1;
-    int fired_reason = 0;
-    bool breakdown = false, t_break = false;
-    int done = 1;
-    auto limit = [&]() { return fired >= 0 ? fired + cfg->p + 1 : cfg->k_max + 1; };
-    while (done < limit()) {
-        KB_REQUIRE(done + 1 <= cap, "eGKB basis capacity exhausted (%d)", cap);
-        // s step (lowrank.py:237-247)
-        const int ms = cfg->full_reorth ? done : 0;
-        HalfOut hs = half_step(op, w, 0, slot(st->q_basis, st->ld_q, done - 1),
-                               slot(st->s_basis, st->ld_s, done - 1), w.cur + 0, st->s_basis, st->ld_s,
-                               ms, passes, slot(st->s_basis, st->ld_s, done), &w.red[0], s);
-        scalars(s, hs.norm, w.cur + 1, hs.norm, w.hist + 0, hs.ynorm2, w.hist + 1);
-        // q step (lowrank.py:249-260)
-        HalfOut hq = half_step(op, w, 1, slot(st->s_basis, st->ld_s, done),
-                               slot(st->q_basis, st->ld_q, done - 1), w.cur + 1, st->q_basis, st->ld_q,
-                               done, passes, slot(st->q_basis, st->ld_q, done), &w.red[3], s);
-        scalars(s, hq.norm, w.cur + 0, hq.norm, w.hist + 2, hq.ynorm2, w.hist + 3);
-        KB_CUDA(cudaMemcpyAsync(hp, w.hist, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
-        KB_CUDA(cudaStreamSynchronize(s));
-        const double t_new = hp[0], unorm = std::sqrt(hp[1]);
-        const double a_new = hp[2], pre = std::sqrt(hp[3]);
-        if (t_new <= tol * unorm) {
-            breakdown = t_break = true;
-            break;
-        }
-        if (a_new <= tol * pre) {
-            breakdown = true;
-            ts.push_back(t_new);
-            break;
-        }
-        ts.push_back(t_new);
-        alphas.push_back(a_new);
-        const double zeta = a_new * t_new;
-        const double nu = std::sqrt(zeta * zetas.back());
-        zetas.push_back(zeta);
-        nus.push_back(nu);
-        done += 1;
-        if (fired < 0) {
-            const double prev = nus[nus.size() - 2];
-            if (nu > prev) {
-                fired = std::max(done - 1, cfg->k_min);
-                fired_reason = KB_STOP_NU_ROSE;
-            } else if (nu < cfg->tau) {
-                fired = std::max(done, cfg->k_min);
-                fired_reason = KB_STOP_NU_BELOW_TOL;
-            }
-        }
-    }
+    KB_REQUIRE(!hh[H_OVERFLOW], "eGKB basis capacity exhausted (%d)", cap);
+    const int done = hh[H_DONE];
+    const bool breakdown = hh[H_BREAK] != 0, t_break = hh[H_TBREAK] != 0;
+    const int fired = hh[H_FIRED];
     int k_p, rows;
     if (breakdown && t_break) { k_p = done; rows = done; }
     else if (breakdown) { k_p = done; rows = done + 1; }
     else { k_p = done - 1; rows = done; }
     int chosen, reason;
-    if (fired >= 0) { chosen = std::min(fired, k_p); reason = fired_reason; }
+    if (fired >= 0) { chosen = std::min(fired, k_p); reason = hh[H_REASON]; }
     else if (breakdown) { chosen = k_p; reason = KB_STOP_BREAKDOWN; }
     else { chosen = std::min(cfg->k_max, k_p); reason = KB_STOP_HIT_KMAX; }
     if (chosen < 1 || k_p < 1) {
         set_error("bidiagonalization broke down before producing any factors");
         throw Fail{KB_ENUMERICAL};
     }
-    KB_REQUIRE((int)alphas.size() <= cap && (int)ts.size() <= cap, "trace overflow");
-    std::copy(alphas.begin(), alphas.end(), st->alphas_host);
-    std::copy(ts.begin(), ts.end(), st->ts_host);
-    std::copy(zetas.begin(), zetas.end(), st->zetas_host);
-    std::copy(nus.begin(), nus.end(), st->nus_host);
-    st->n_alphas = (int)alphas.size();
-    st->n_ts = (int)ts.size();
-    st->n_nus = (int)nus.size();
+    st->n_alphas = hh[H_NA];
+    st->n_ts = hh[H_NT];
+    st->n_nus = hh[H_NN];
+    std::copy(ht, ht + st->n_alphas, st->alphas_host);
+    std::copy(ht + cap, ht + cap + st->n_ts, st->ts_host);
+    std::copy(ht + 2 * cap, ht + 2 * cap + st->n_nus, st->zetas_host);
+    std::copy(ht + 3 * cap, ht + 3 * cap + st->n_nus, st->nus_host);
     st->chosen_k = chosen;
     st->k_p = k_p;
     st->rows = rows;
@@ -342,20 +553,22 @@ static void orthonormalize(int dtype, void* Q, int64_t ld, int ncol, int64_t len
     for (int i = 0; i < 3; ++i) red[i] = a.take<double>(ncol + 16);
     double* hist = a.take<double>(2 * (size_t)ncol + 16);  // [t_j | raw_j]
     KB_CUDA(cudaMemsetAsync(rw.counter, 0, sizeof(unsigned) * 64, s));
+    double* fx = red[2];
     const size_t esz = dtype == KB_F32 ? 4 : 8;
     for (int j = 0; j < ncol; ++j) {
         void* col = static_cast<char*>(Q) + (size_t)j * ld * esz;
         Src src;
-        src.z = static_cast<const double*>(col);
+        src.z = VecRef::at(col);
         src.mode = SRC_BUFT;
-        const int m = j;
-        reorth_pass(dtype, src, Q, ld, m, nullptr, nullptr, m > 0, nullptr, nullptr, len, red[0], rw, s);
-        reorth_pass(dtype, src, Q, ld, m, m > 0 ? red[0] : nullptr, nullptr, true, nullptr, nullptr, len,
-                    red[1], rw, s);
-        const double* t = red[1] + m + 2;
-        reorth_pass(dtype, src, Q, ld, m, m > 0 ? red[0] : nullptr, m > 0 ? red[1] : nullptr, false, col, t,
-                    len, red[2], rw, s);
-        scalars(s, t, hist + j, red[0] + m + 3, hist + ncol + j);
+        const MRef m = MRef::fixed(j);
+        const bool any = j > 0;
+        // CGS2: coefficients, second-pass coefficients, then the projected, normalised column
+        reorth_pass(dtype, src, Q, ld, m, nullptr, nullptr, any, VecRef(), nullptr, len, red[0], fx + 0, rw, s);
+        reorth_pass(dtype, src, Q, ld, m, any ? red[0] : nullptr, nullptr, true, VecRef(), nullptr, len, red[1],
+                    fx + 4, rw, s);
+        reorth_pass(dtype, src, Q, ld, m, any ? red[0] : nullptr, any ? red[1] : nullptr, false, VecRef::at(col),
+                    fx + 6, len, nullptr, fx + 8, rw, s);
+        scalars(s, fx + 6, hist + j, fx + 3, hist + ncol + j);
     }
     std::vector<double> h(2 * (size_t)ncol);
     KB_CUDA(cudaMemcpyAsync(h.data(), hist, sizeof(double) * 2 * ncol, cudaMemcpyDeviceToHost, s));
@@ -445,7 +658,7 @@ extern "C" int kb_op_apply(const kb_operator* op, const void* x, void* y, int tr
         OpPlan p = op_plan_make(op, a);
         cudaStream_t s = as_stream(stream);
         KB_CUDA(cudaMemsetAsync(p.counters, 0, sizeof(unsigned) * p.n_counters, s));
-        Src src = op_source(p, x, transpose, s);
+        Src src = op_source(p, VecRef::at(x), transpose, s);
         src_write(op->dtype, src, y, transpose ? op->cols : op->rows, s);
     })
 }
@@ -456,14 +669,16 @@ extern "C" int kb_ts_dots(int dtype, const void* S, int64_t ld, int m, const voi
         KB_REQUIRE(v && out && (S || m == 0), "null argument");
         Arena a(ws, ws_bytes);
         ReorthWs rw = reorth_ws_make(len, m, a);
-        double* red = a.take<double>(m + 8);
+        double* red = a.take<double>(m + 16);
         cudaStream_t s = as_stream(stream);
         KB_CUDA(cudaMemsetAsync(rw.counter, 0, sizeof(unsigned) * 64, s));
         Src src;
-        src.z = static_cast<const double*>(v);
+        src.z = VecRef::at(v);
         src.mode = SRC_BUFT;
-        reorth_pass(dtype, src, S, ld, m, nullptr, nullptr, true, nullptr, nullptr, len, red, rw, s);
-        KB_CUDA(cudaMemcpyAsync(out, red, sizeof(double) * (m + 1), cudaMemcpyDeviceToDevice, s));
+        double* fix = red + m + 1;
+        reorth_pass(dtype, src, S, ld, MRef::fixed(m), nullptr, nullptr, true, VecRef(), nullptr, len, red, fix, rw, s);
+        KB_CUDA(cudaMemcpyAsync(out, red, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+        KB_CUDA(cudaMemcpyAsync(out + m, fix, sizeof(double), cudaMemcpyDeviceToDevice, s));
     })
 }
 
@@ -487,10 +702,10 @@ extern "C" int kb_ts_axpy(int dtype, const void* S, int64_t ld, int m, const dou
         ReorthWs rw = reorth_ws_make(len, m, a);
         double* red = a.take<double>(m + 8);
         Src src;
-        src.z = static_cast<const double*>(v);
+        src.z = VecRef::at(v);
         src.mode = SRC_BUFT;
-        reorth_pass(dtype, src, S, ld, m, coef, nullptr, false, v, nullptr, len, red, rw,
-                    as_stream(stream));
+        reorth_pass(dtype, src, S, ld, MRef::fixed(m), coef, nullptr, false, VecRef::at(v), nullptr, len, nullptr,
+                    red, rw, as_stream(stream));
     })
 }
 

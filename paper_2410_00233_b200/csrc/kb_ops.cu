@@ -20,36 +20,6 @@
 namespace kb {
 
 // ------------------------------------------------------------------ diag sums
-// part[rb][u] = sum_{a in row block rb} X[a, a + u - center];
-// the last block per diagonal chunk reduces the row blocks in order -> w[u].
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_diag_partial(const T* __restrict__ X, int n, int center, int L, int rb_rows,
-               double* __restrict__ part, double* __restrict__ w, unsigned* counters) {
-    const int u = blockIdx.x * 256 + threadIdx.x;
-    const int a0 = blockIdx.y * rb_rows;
-    const int a1 = min(a0 + rb_rows, n);
-    double acc = 0.0;
-    if (u < L) {
-        const int d = u - center;
-        const int lo = max(a0, -d), hi = min(a1, n - d);
-        if (lo < hi) {
-            const T* p = X + (int64_t)lo * n + (lo + d);
-#pragma unroll 8
-            for (int a = lo; a < hi; ++a, p += (n + 1)) acc += (double)__ldg(p);
-        }
-        part[(int64_t)blockIdx.y * L + u] = acc;
-    }
-    if (last_block_ticket(&counters[blockIdx.x], gridDim.y)) {
-        if (u < L) {
-            double s = 0.0;
-#pragma unroll 8
-            for (int r = 0; r < (int)gridDim.y; ++r) s += __ldcg(&part[(int64_t)r * L + u]);
-            w[u] = s;
-        }
-    }
-}
-
 // Segmented variant used by the R(A) product: a CTA owns 32 consecutive
 // diagonals (lane = diagonal, so a warp load is one 128-byte row segment)
 // over one of RA_SEGS row segments (warp = row phase, 8 rows in flight per
@@ -59,8 +29,9 @@ constexpr int RA_SEGS = 8;
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_diag_seg(const T* __restrict__ X, int n, int center, int L, double* __restrict__ part,
+k_diag_seg(const VecRef xr, int n, int center, int L, double* __restrict__ part,
            double* __restrict__ w, unsigned* counters) {
+    const T* __restrict__ X = resolve<const T>(xr);
     __shared__ double red[8][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int u = blockIdx.x * 32 + lane;
@@ -74,12 +45,12 @@ k_diag_seg(const T* __restrict__ X, int n, int center, int L, double* __restrict
         const int64_t step = 8 * (int64_t)(n + 1);
         int a = lo + warp;
         p += (int64_t)warp * (n + 1);
-        for (; a + 24 < hi; a += 32, p += 4 * step) {   // 4 independent loads per trip
-            const T v0 = __ldg(p), v1 = __ldg(p + step), v2 = __ldg(p + 2 * step), v3 = __ldg(p + 3 * step);
-            acc += (double)v0;
-            acc += (double)v1;
-            acc += (double)v2;
-            acc += (double)v3;
+        for (; a + 56 < hi; a += 64, p += 8 * step) {   // 8 independent loads per trip
+            T v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(p + q * step);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += (double)v[q];
         }
         for (; a < hi; a += 8, p += step) acc += (double)__ldg(p);
     }
@@ -113,15 +84,16 @@ k_colsum_seg(const TM* __restrict__ M, int64_t ld, int rows, int cols, const dou
     double acc = 0.0;
     if (c < cols) {
         int r = r0 + warp;
-        for (; r + 24 < r1; r += 32) {
-            const double a0 = (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
-            const double a1 = (double)__ldg(M + (int64_t)(r + 8) * ld + c) * __ldg(w + r + 8);
-            const double a2 = (double)__ldg(M + (int64_t)(r + 16) * ld + c) * __ldg(w + r + 16);
-            const double a3 = (double)__ldg(M + (int64_t)(r + 24) * ld + c) * __ldg(w + r + 24);
-            acc += a0;
-            acc += a1;
-            acc += a2;
-            acc += a3;
+        for (; r + 56 < r1; r += 64) {                  // 8 independent loads per trip
+            TM mv[8];
+            double wv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                mv[q] = __ldg(M + (int64_t)(r + 8 * q) * ld + c);
+                wv[q] = __ldg(w + r + 8 * q);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += (double)mv[q] * wv[q];
         }
         for (; r < r1; r += 8) acc += (double)__ldg(M + (int64_t)r * ld + c) * __ldg(w + r);
     }
@@ -146,8 +118,9 @@ k_colsum_seg(const TM* __restrict__ M, int64_t ld, int rows, int cols, const dou
 // z[c] = sum_r M[r, c] w[r]   (M row-major rows x cols, leading dim ld)
 template <typename TM, typename TW>
 __global__ void __launch_bounds__(256)
-k_colsum(const TM* __restrict__ M, int64_t ld, int rows, int cols, const TW* __restrict__ w,
+k_colsum(const TM* __restrict__ M, int64_t ld, int rows, int cols, const VecRef wr,
          int rb_rows, double* __restrict__ part, double* __restrict__ z, unsigned* counters) {
+    const TW* __restrict__ w = resolve<const TW>(wr);
     __shared__ double red[8][128];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c0 = blockIdx.x * 128;
@@ -186,8 +159,9 @@ k_colsum(const TM* __restrict__ M, int64_t ld, int rows, int cols, const TW* __r
 // z[r] = sum_c A[r, c] x[c]  (one warp per row; dense b_mat @ q)
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_rowdot(const T* __restrict__ A, int64_t lda, int rows, int cols, const T* __restrict__ x,
+k_rowdot(const T* __restrict__ A, int64_t lda, int rows, int cols, const VecRef xr,
          double* __restrict__ z) {
+    const T* __restrict__ x = resolve<const T>(xr);
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= rows) return;
@@ -201,14 +175,15 @@ k_rowdot(const T* __restrict__ A, int64_t lda, int rows, int cols, const T* __re
 // ------------------------------------------------------------------ sources
 template <typename T>
 struct Gen {
-    const double* z;   // global source
+    const double* z;   // global fp64 source (BUF64 / TOEP)
+    const T* zt;       // T source (BUFT)
     const double* zs;  // toeplitz coefficients in shared memory
     const T* prev;
     T beta;
     int mode, side, center, L;
     __device__ __forceinline__ T y(int64_t e) const {
         if (mode == SRC_BUF64) return (T)z[e];
-        if (mode == SRC_BUFT) return reinterpret_cast<const T*>(z)[e];
+        if (mode == SRC_BUFT) return zt[e];
         const unsigned ee = (unsigned)e;            // n^2 < 2^32 for n <= 65535
         const unsigned a = ee / (unsigned)side;
         const int u = (int)(ee - a * (unsigned)side) - (int)a + center;
@@ -224,9 +199,10 @@ __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, 
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 
 template <typename T>
-__global__ void k_src_write(const double* __restrict__ z, int mode, int side, int center, int L,
-                            T* __restrict__ y, int64_t len) {
-    Gen<T> g{z, z, nullptr, T(0), mode, side, center, L};
+__global__ void k_src_write(const VecRef zr, int mode, int side, int center, int L, T* __restrict__ y,
+                            int64_t len) {
+    const double* z = resolve<const double>(zr);
+    Gen<T> g{z, resolve<const T>(zr), z, nullptr, T(0), mode, side, center, L};
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * blockDim.x)
         y[e] = g.y(e);
@@ -254,33 +230,39 @@ struct VecIO<T, 1> {
     static __device__ __forceinline__ void load(const T* p, double* v) { v[0] = (double)__ldg(p); }
 };
 
-// One pass over the basis.  smem: [L toeplitz] [m coef] [8 x (m+2) warp acc] [m+4 red]
+// One pass over the basis.  smem: [L toeplitz] [mmax coef] [8 x (mmax+2) warp acc] [mmax+4 fin]
 // Each thread owns R groups of VEC consecutive elements per tile (groups
 // strided by 256*VEC so every warp load is contiguous); per basis vector it
 // issues R independent vector loads and does ONE warp reduction per tile.
+// All vector / size arguments may be resolved on the device (VecRef/MRef),
+// so the same launch serves every iteration of a captured eGKB graph.
 template <typename T, int VEC, int R>
 __global__ void __launch_bounds__(256)
-k_reorth(const double* zsrc, int mode, int side, int center, int L,
-         const T* __restrict__ prev, const double* __restrict__ beta_p,
-         const T* __restrict__ S, int64_t ld, int m, const double* __restrict__ coefA,
-         const double* __restrict__ coefB, int dots, T* out,
+k_reorth(const VecRef zr, int mode, int side, int center, int L, const VecRef prevr,
+         const double* __restrict__ beta_p, const T* __restrict__ S, int64_t ld, const MRef mr,
+         const double* __restrict__ coefA, const double* __restrict__ coefB, int dots, const VecRef outr,
          const double* __restrict__ div_p, int64_t len, double* __restrict__ part,
-         double* __restrict__ red, unsigned* counter) {
+         double* __restrict__ red, double* __restrict__ fix, unsigned* counter) {
     extern __shared__ double sm[];
+    const int m = mr.idx ? (*mr.idx) * mr.mul + mr.add : mr.add;
+    const int mmax = mr.max;
     const int Ls = (mode == SRC_TOEP) ? L : 0;
     double* zs = sm;
     double* coef = zs + Ls;
-    double* accw = coef + m;            // [8][m+2]
-    double* fin = accw + 8 * (m + 2);   // [m+4]
+    double* accw = coef + mmax;            // [8][m+2]
+    double* fin = accw + 8 * (mmax + 2);   // [m+4]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int W = m + 2;
+    const double* zsrc = resolve<const double>(zr);
     for (int i = threadIdx.x; i < Ls; i += blockDim.x) zs[i] = zsrc[i];
     const bool proj = (coefA != nullptr) || (coefB != nullptr);
     for (int i = threadIdx.x; i < m; i += blockDim.x)
         coef[i] = (coefA ? coefA[i] : 0.0) + (coefB ? coefB[i] : 0.0);
     for (int i = threadIdx.x; i < 8 * W; i += blockDim.x) accw[i] = 0.0;
     __syncthreads();
-    Gen<T> g{zsrc, zs, prev, beta_p ? (T)(*beta_p) : T(0), mode, side, center, L};
+    const T* prev = prevr.base ? resolve<const T>(prevr) : nullptr;
+    T* out = outr.base ? resolve<T>(outr) : nullptr;
+    Gen<T> g{zsrc, resolve<const T>(zr), zs, prev, beta_p ? (T)(*beta_p) : T(0), mode, side, center, L};
     const T tdiv = div_p ? (T)(*div_p) : T(1);
 
     constexpr int64_t GROUP = 256 * VEC;
@@ -390,42 +372,46 @@ k_reorth(const double* zsrc, int mode, int side, int center, int L,
             double h2 = 0.0;
             if (dots)
                 for (int i = 0; i < m; ++i) h2 += fin[i] * fin[i];
-            fin[m + 2] = sqrt(fmax(fin[m] - h2, 0.0));
-            fin[m + 3] = sqrt(fin[m]);
+            fix[0] = fin[m];
+            fix[1] = fin[m + 1];
+            fix[2] = sqrt(fmax(fin[m] - h2, 0.0));
+            fix[3] = sqrt(fin[m]);
         }
-        __syncthreads();
-        for (int j = threadIdx.x; j < m + 4; j += blockDim.x) red[j] = fin[j];
+        if (red)
+            for (int j = threadIdx.x; j < m; j += blockDim.x) red[j] = fin[j];
     }
 }
 
 // ------------------------------------------------------------------ lift
-// out_c = sum_i W[i, c] S_i, 32 output columns per pass, fp64 accumulation.
-template <typename T>
+// out_c = sum_i W[i, c] S_i for CB output columns per pass, accumulated in T
+// (fp32 like the reference's sgemm for the fp32 path).  One element per
+// thread, W broadcast from shared memory.
+template <typename T, int CB>
 __global__ void __launch_bounds__(256)
 k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, int cols, int c0,
        T* __restrict__ out, int64_t ld_out, int64_t len) {
-    constexpr int CB = 32;
-    extern __shared__ double wsm[];  // [rows][CB]
+    extern __shared__ double wraw[];
+    T* wsm = reinterpret_cast<T*>(wraw);  // [rows][CB]
     const int nc = min(CB, cols - c0);
     for (int i = threadIdx.x; i < rows * CB; i += blockDim.x) {
         const int r = i / CB, c = i % CB;
-        wsm[i] = (c < nc) ? (double)W[(int64_t)r * cols + c0 + c] : 0.0;
+        wsm[i] = (c < nc) ? W[(int64_t)r * cols + c0 + c] : T(0);
     }
     __syncthreads();
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * blockDim.x) {
-        double acc[CB];
+        T acc[CB];
 #pragma unroll
-        for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+        for (int c = 0; c < CB; ++c) acc[c] = T(0);
         for (int i = 0; i < rows; ++i) {
-            const double s = (double)__ldg(S + (int64_t)i * ld + e);
-            const double* wr = wsm + i * CB;
+            const T s = __ldg(S + (int64_t)i * ld + e);
+            const T* wr = wsm + i * CB;
 #pragma unroll
-            for (int c = 0; c < CB; ++c) acc[c] += s * wr[c];
+            for (int c = 0; c < CB; ++c) acc[c] = fma(s, wr[c], acc[c]);
         }
 #pragma unroll
         for (int c = 0; c < CB; ++c)
-            if (c < nc) out[(int64_t)(c0 + c) * ld_out + e] = (T)acc[c];
+            if (c < nc) out[(int64_t)(c0 + c) * ld_out + e] = acc[c];
     }
 }
 
@@ -494,9 +480,8 @@ OpPlan op_plan_make(const kb_operator* op, Arena& a) {
 }
 
 template <typename T>
-static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStream_t st) {
+static Src op_source_t(const OpPlan& p, const VecRef& x, int transpose, cudaStream_t st) {
     const kb_operator* op = p.op;
-    const T* x = static_cast<const T*>(xv);
     Src s;
     if (op->kind == KB_OP_RA_ZERO) {
         int ci, Li, co, Lo;
@@ -523,7 +508,7 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
                 static_cast<const T*>(Mv), Lo, Li, Lo, p.w, p.part, p.z, p.counters + 64);
             KB_LAUNCH_CHECK();
         }
-        s.z = p.z;
+        s.z = VecRef::at(p.z);
         s.mode = SRC_TOEP;
         s.side = n;
         s.center = co;
@@ -546,13 +531,13 @@ static Src op_source_t(const OpPlan& p, const void* xv, int transpose, cudaStrea
                                               p.counters);
             KB_LAUNCH_CHECK();
         }
-        s.z = p.z;
+        s.z = VecRef::at(p.z);
         s.mode = SRC_BUF64;
     }
     return s;
 }
 
-Src op_source(const OpPlan& p, const void* x, int transpose, cudaStream_t st) {
+Src op_source(const OpPlan& p, const VecRef& x, int transpose, cudaStream_t st) {
     return p.op->dtype == KB_F32 ? op_source_t<float>(p, x, transpose, st)
                                  : op_source_t<double>(p, x, transpose, st);
 }
@@ -568,7 +553,7 @@ void src_write(int dtype, const Src& s, void* y, int64_t len, cudaStream_t st) {
     KB_LAUNCH_CHECK();
 }
 
-constexpr int REORTH_R = 4;
+constexpr int REORTH_R = 2;
 static int reorth_blocks(int64_t len) {
     const int64_t tiles = cdiv(len, 256 * REORTH_R);   // VEC >= 1
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4 * kSMs));
@@ -589,11 +574,12 @@ ReorthWs reorth_ws_make(int64_t len, int max_m, Arena& a) {
 }
 
 template <typename T, int VEC>
-static void launch_reorth(const Src& src, const void* S, int64_t ld, int m, const double* cA,
-                          const double* cB, bool dots, void* out, const double* div, int64_t len,
-                          double* red, const ReorthWs& ws, cudaStream_t st) {
+static void launch_reorth(const Src& src, const void* S, int64_t ld, const MRef& m, const double* cA,
+                          const double* cB, bool dots, const VecRef& out, const double* div, int64_t len,
+                          double* red, double* fix, const ReorthWs& ws, cudaStream_t st) {
     const int Ls = (src.mode == SRC_TOEP) ? src.L : 0;
-    const size_t smem = sizeof(double) * ((size_t)Ls + m + 8 * (m + 2) + (m + 4));
+    const int mm = m.max;
+    const size_t smem = sizeof(double) * ((size_t)Ls + mm + 8 * (mm + 2) + (mm + 4));
     auto kern = k_reorth<T, VEC, REORTH_R>;
     static bool configured = false;
     if (!configured) {
@@ -601,33 +587,34 @@ static void launch_reorth(const Src& src, const void* S, int64_t ld, int m, cons
         configured = true;
     }
     const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC * REORTH_R)));
-    double vecs = (double)m + (src.prev ? 1 : 0) + (out ? 1 : 0) + (src.mode == SRC_BUFT ? 1 : 0);
+    // algorithmic bytes (with m at its upper bound when resolved on the device)
+    double vecs = (double)mm + (src.prev.null() ? 0 : 1) + (out.null() ? 0 : 1) + (src.mode == SRC_BUFT ? 1 : 0);
     double bytes = vecs * len * sizeof(T) + (src.mode == SRC_BUF64 ? 8.0 * len : 0.0);
     ProfScope ps(st, PROF_REORTH, bytes);
-    kern<<<blocks, 256, smem, st>>>(src.z, src.mode, src.side, src.center, src.L,
-                                    static_cast<const T*>(src.prev), src.beta,
-                                    static_cast<const T*>(S), ld, m, cA, cB, dots ? 1 : 0,
-                                    static_cast<T*>(out), div, len, ws.part, red, ws.counter);
+    kern<<<blocks, 256, smem, st>>>(src.z, src.mode, src.side, src.center, src.L, src.prev, src.beta,
+                                    static_cast<const T*>(S), ld, m, cA, cB, dots ? 1 : 0, out, div, len,
+                                    ws.part, red, fix, ws.counter);
     KB_LAUNCH_CHECK();
 }
 
-void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, int m, const double* coefA,
-                 const double* coefB, bool dots, void* out, const double* div, int64_t len,
-                 double* red, const ReorthWs& ws, cudaStream_t st) {
-    KB_REQUIRE(m <= ws.max_m, "reorth: basis size %d exceeds workspace capacity %d", m, ws.max_m);
+void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, const MRef& m,
+                 const double* coefA, const double* coefB, bool dots, const VecRef& out,
+                 const double* div, int64_t len, double* red, double* fix, const ReorthWs& ws,
+                 cudaStream_t st) {
+    KB_REQUIRE(m.max <= ws.max_m, "reorth: basis size %d exceeds workspace capacity %d", m.max, ws.max_m);
     auto aligned = [](const void* p, size_t a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
     if (dtype == KB_F32) {
         const bool v4 = (ld % 4 == 0) && (len % 4 == 0) && aligned(S, 16);
         if (v4)
-            launch_reorth<float, 4>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+            launch_reorth<float, 4>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, fix, ws, st);
         else
-            launch_reorth<float, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+            launch_reorth<float, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, fix, ws, st);
     } else {
         const bool v2 = (ld % 2 == 0) && (len % 2 == 0) && aligned(S, 16);
         if (v2)
-            launch_reorth<double, 2>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+            launch_reorth<double, 2>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, fix, ws, st);
         else
-            launch_reorth<double, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, ws, st);
+            launch_reorth<double, 1>(src, S, ld, m, coefA, coefB, dots, out, div, len, red, fix, ws, st);
     }
 }
 
@@ -635,43 +622,46 @@ void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, cons
                   double* y, int transpose, double* part, unsigned* counters, cudaStream_t st) {
     ProfScope ps(st, PROF_RA_COLSUM, 8.0 * rows * cols);
     if (!transpose) {
-        k_rowdot<double><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, lda, (int)rows, (int)cols, x, y);
+        k_rowdot<double><<<(unsigned)cdiv(rows, 8), 256, 0, st>>>(A, lda, (int)rows, (int)cols, VecRef::at(x), y);
     } else {
         const int cchunks = (int)cdiv(cols, 128);
         const int rb = rb_for((int)rows, cchunks);
         dim3 g(cchunks, (unsigned)cdiv(rows, rb));
-        k_colsum<double, double><<<g, 256, 0, st>>>(A, lda, (int)rows, (int)cols, x, rb, part, y, counters);
+        k_colsum<double, double><<<g, 256, 0, st>>>(A, lda, (int)rows, (int)cols, VecRef::at(x), rb, part, y, counters);
     }
+    KB_LAUNCH_CHECK();
+}
+
+template <typename T, int CB>
+static void launch_lift(const void* S, int64_t ld, int rows, const void* W, int cols, int c0, void* out,
+                        int64_t ld_out, int64_t len, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        KB_CUDA(cudaFuncSetAttribute(k_lift<T, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        configured = true;
+    }
+    const size_t smem = sizeof(T) * (size_t)rows * CB;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 8 * kSMs));
+    ProfScope ps(st, PROF_LIFT, (double)sizeof(T) * len * (rows + std::min(CB, cols - c0)));
+    k_lift<T, CB><<<blocks, 256, smem, st>>>(static_cast<const T*>(S), ld, rows, static_cast<const T*>(W), cols,
+                                             c0, static_cast<T*>(out), ld_out, len);
     KB_LAUNCH_CHECK();
 }
 
 void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, void* out,
              int64_t ld_out, int64_t len, cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)rows * 32;
-    KB_REQUIRE(rows <= 512, "lift: too many basis vectors (%d)", rows);
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 4 * kSMs));
-    const size_t esz = dtype == KB_F32 ? 4 : 8;
+    KB_REQUIRE(rows <= 1024, "lift: too many basis vectors (%d)", rows);
     for (int c0 = 0; c0 < cols; c0 += 32) {
-        ProfScope ps(st, PROF_LIFT, (double)esz * len * (rows + std::min(32, cols - c0)));
-        static bool cfg32 = false, cfg64 = false;
-        if (dtype == KB_F32 && !cfg32) {
-            KB_CUDA(cudaFuncSetAttribute(k_lift<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-            cfg32 = true;
-        }
-        if (dtype == KB_F64 && !cfg64) {
-            KB_CUDA(cudaFuncSetAttribute(k_lift<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-            cfg64 = true;
-        }
+        const int nc = std::min(32, cols - c0);
         if (dtype == KB_F32) {
-            k_lift<float><<<blocks, 256, smem, st>>>(static_cast<const float*>(S), ld, rows,
-                                                     static_cast<const float*>(W), cols, c0,
-                                                     static_cast<float*>(out), ld_out, len);
+            if (nc <= 8) launch_lift<float, 8>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
+            else if (nc <= 16) launch_lift<float, 16>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
+            else launch_lift<float, 32>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
         } else {
-            k_lift<double><<<blocks, 256, smem, st>>>(static_cast<const double*>(S), ld, rows,
-                                                      static_cast<const double*>(W), cols, c0,
-                                                      static_cast<double*>(out), ld_out, len);
+            if (nc <= 8) launch_lift<double, 8>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
+            else if (nc <= 16) launch_lift<double, 16>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
+            else launch_lift<double, 32>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
         }
-        KB_LAUNCH_CHECK();
     }
 }
 

@@ -5,19 +5,50 @@
 
 namespace kb {
 
+// A vector argument that may be resolved on the device at run time:
+//   ptr = base + (idx ? (*idx + off) : 0) * ld        (in elements)
+// so that one captured CUDA graph can address basis slot `done` of the
+// iteration it is executing (the eGKB loop body is a graph while-node).
+struct VecRef {
+    const void* base = nullptr;
+    const int* idx = nullptr;
+    int off = 0;
+    int64_t ld = 0;
+    static VecRef at(const void* p) { VecRef r; r.base = p; return r; }
+    static VecRef slot(const void* b, const int* i, int o, int64_t l) {
+        VecRef r; r.base = b; r.idx = i; r.off = o; r.ld = l; return r;
+    }
+    bool null() const { return base == nullptr; }
+};
+
+template <typename T>
+__device__ __forceinline__ T* resolve(const VecRef& r) {
+    T* p = reinterpret_cast<T*>(const_cast<void*>(r.base));
+    return r.idx ? p + (int64_t)(*r.idx + r.off) * r.ld : p;
+}
+
+// Basis size resolved on the device: m = idx ? (*idx) * mul + add : add.
+struct MRef {
+    const int* idx = nullptr;
+    int mul = 0;
+    int add = 0;
+    int max = 0;   // upper bound (shared-memory sizing)
+    static MRef fixed(int m) { MRef r; r.add = m; r.max = m; return r; }
+};
+
 // Source of the generated vector v in the reorthogonalisation passes:
-//   SRC_BUFT   : y[e] = ((const T*) z)[e]                          (a stored vector)
-//   SRC_BUF64  : y[e] = (T) z[e]                                   (dense op)
-//   SRC_TOEP   : y[a*n+b] = (T) z[b - a + center], 0 outside [0,L) (R(A))
+//   SRC_BUFT   : y[e] = x[e]       (a stored vector in T, e.g. y0 or a slot)
+//   SRC_BUF64  : y[e] = (T) z[e]   (dense operator product, fp64 accumulated)
+//   SRC_TOEP   : y[a*n+b] = (T) z[b - a + center], 0 outside [0,L)  (R(A))
 enum SrcMode { SRC_BUFT = 0, SRC_BUF64 = 1, SRC_TOEP = 2 };
 
 struct Src {
-    const double* z = nullptr;
+    VecRef z;                     // BUFT: T vector; BUF64/TOEP: fp64 array
     int mode = SRC_BUF64;
     int side = 0;
     int center = 0;
     int L = 0;
-    const void* prev = nullptr;   // v = y - beta * prev   (prev in T)
+    VecRef prev;                  // v = y - beta * prev   (prev in T)
     const double* beta = nullptr; // device scalar
 };
 
@@ -25,7 +56,6 @@ struct Src {
 // the Toeplitz coefficient array z for R(A)).
 struct OpPlan {
     const kb_operator* op;
-    // workspace pieces
     double* part = nullptr;      // partial sums
     double* w = nullptr;         // diagonal sums (R(A))
     double* z = nullptr;         // output coefficients / full vector
@@ -37,15 +67,16 @@ struct OpPlan {
 void op_plan_size(const kb_operator* op, Sizer& s);
 OpPlan op_plan_make(const kb_operator* op, Arena& a);
 // Computes the fp64 source for y = op x (or op^T x); returns the Src.
-Src op_source(const OpPlan& p, const void* x, int transpose, cudaStream_t st);
+Src op_source(const OpPlan& p, const VecRef& x, int transpose, cudaStream_t st);
 // Writes y (dtype T) from a source.
 void src_write(int dtype, const Src& s, void* y, int64_t len, cudaStream_t st);
 
 // Reorthogonalisation pass over basis S (m vectors at stride ld):
 //   v = y - beta*prev - S (coefA + coefB)       (coef may be null)
-//   red[0..m) = S^T v (if dots), red[m] = ||v||^2, red[m+1] = ||y||^2,
-//   red[m+2] = sqrt(max(red[m] - sum_i red[i]^2, 0)), red[m+3] = sqrt(red[m])
-//   out = v / *div (if out)
+//   red[0..m) = S^T v (if dots)
+//   fix[0] = ||v||^2, fix[1] = ||y||^2, fix[2] = sqrt(max(fix[0] - sum red_i^2, 0)),
+//   fix[3] = sqrt(fix[0])               (four fixed-address scalars)
+//   out = v / *div (if out; div may be null)
 struct ReorthWs {
     double* part = nullptr;
     unsigned* counter = nullptr;
@@ -54,9 +85,10 @@ struct ReorthWs {
 };
 void reorth_ws_size(int64_t len, int max_m, Sizer& s);
 ReorthWs reorth_ws_make(int64_t len, int max_m, Arena& a);
-void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, int m, const double* coefA,
-                 const double* coefB, bool dots, void* out, const double* div, int64_t len,
-                 double* red, const ReorthWs& ws, cudaStream_t st);
+void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, const MRef& m,
+                 const double* coefA, const double* coefB, bool dots, const VecRef& out,
+                 const double* div, int64_t len, double* red, double* fix, const ReorthWs& ws,
+                 cudaStream_t st);
 
 void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, void* out,
              int64_t ld_out, int64_t len, cudaStream_t st);
