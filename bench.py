@@ -175,10 +175,9 @@ def run_ours(args, prob, rank, world, dist):
         step_resident()
     torch.cuda.synchronize()
 
-    # ---- timed region (device-resident inputs), L2 flushed between steps
+    # ---- timed region (device-resident inputs, graph path), L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
-    lib.kb_prof_enable(1)
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -188,16 +187,29 @@ def run_ours(args, prob, rank, world, dist):
         ev[i][1].record()
         torch.cuda.synchronize()
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    prof = {c: prof_read(lib, c) for c in range(6)}
-    lib.kb_prof_enable(0)
-    gpu_launches = sum(v[1] for v in prof.values())
-
     t_max = torch.tensor([total_ms], dtype=torch.float64, device=D.device())
     if dist is not None:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     total_ms = float(t_max.item())
     ms_per_step = total_ms / args.steps
     value = world * args.steps / (total_ms * 1e-3)
+
+    # ---- profiled replay: same kernels launched eagerly, CUDA events around each
+    # launch on the launching stream (per-kernel device time for the roofline)
+    lib.kb_prof_enable(1)
+    prof_ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step_resident()
+        b.record()
+        torch.cuda.synchronize()
+        prof_ms += a.elapsed_time(b)
+    prof = {c: prof_read(lib, c) for c in range(6)}
+    lib.kb_prof_enable(0)
+    gpu_launches = sum(v[1] for v in prof.values())
 
     # ---- e2e: public API from host arrays, every step
     psf_host = prob.psf
@@ -229,13 +241,18 @@ def run_ours(args, prob, rank, world, dist):
     kb.sb_run(op, b_dev, kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=1,
                                      cgls=kb.CglsConfig(i_max=2, tau=0.0)))   # warm-up
     torch.cuda.synchronize()
-    lib.kb_prof_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sb_res = kb.sb_run(op, b_dev, sb_cfg)
     e1.record()
     torch.cuda.synchronize()
     sb_ms = e0.elapsed_time(e1)
+    lib.kb_prof_enable(1)                      # profiled replay for the GEMM share
+    e0.record()
+    kb.sb_run(op, b_dev, sb_cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    sb_prof_ms = e0.elapsed_time(e1)
     g_ms, g_n, g_by, g_fl = prof_read(lib, 3)
     v_ms, v_n, _, _ = prof_read(lib, 4)
     lib.kb_prof_enable(0)
@@ -251,7 +268,7 @@ def run_ours(args, prob, rank, world, dist):
     dom = max(range(6), key=lambda c: prof[c][0])
     d_ms, d_n, d_by, d_fl = prof[dom]
     achieved = (d_by / d_n) / ((d_ms / d_n) * 1e-3) / 1e9 if d_n else 0.0
-    step_share = d_ms / total_ms if total_ms else 0.0
+    step_share = d_ms / prof_ms if prof_ms else 0.0
     # R(A) product: one diag pass + one column pass per product
     mv_ms = prof[1][0] + prof[2][0]
     mv_n = prof[1][1]
@@ -270,7 +287,7 @@ def run_ours(args, prob, rank, world, dist):
           "cgls_it_per_s": cg / (sb_ms * 1e-3),
           "gemm_tflops": g_fl / (g_ms * 1e-3) / 1e12 if g_ms else None,
           "gemm_frac_fp64_peak": (g_fl / (g_ms * 1e-3) / 1e12) / FP64_PEAK_TFLOPS if g_ms else None,
-          "gemm_share": g_ms / sb_ms if sb_ms else None, "vector_pass_ms": v_ms,
+          "gemm_share": g_ms / sb_prof_ms if sb_prof_ms else None, "vector_pass_ms": v_ms,
           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_src": "measured DMMA issue rate, tools/fp64_peak"}
     line = {
         "metric": METRIC, "value": value, "unit": "KP-approx/s", "n_gpus": world, "steps": args.steps,
@@ -283,7 +300,10 @@ def run_ours(args, prob, rank, world, dist):
                    "l2": "flushed (512 MB write) before every timed step"},
         "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "launches": d_n,
-                     "share_of_step": step_share, "peak_src": hbm_src},
+                     "share_of_step": step_share, "peak_src": hbm_src,
+                     "timing": "CUDA events around every launch in an eager replay of the timed steps "
+                               "(the timed steps themselves run as one CUDA graph per approximation)",
+                     "profiled_ms_per_step": prof_ms / args.steps},
         "ra_matvec": ra,
         "sb": sb,
         "e2e": {"value": e2e_value, "unit": "KP-approx/s", "h2d_bytes_per_step": int(h2d),

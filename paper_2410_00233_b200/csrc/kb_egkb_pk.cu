@@ -1,0 +1,563 @@
+// Persistent cooperative eGKB for the matrix-free R(A) (fp32 / fp64), sm_100a.
+//
+// The whole bidiagonalisation (lowrank.py:207-303) runs in ONE kernel launch:
+// 2 CTAs per SM, grid-wide barriers (cooperative groups) between the phases
+// of each half step, and the reference's breakdown tests and nu rank rule
+// evaluated redundantly (and identically) by every CTA, so the loop needs no
+// host round trip and no per-phase kernel launch.  One half step is
+//
+//   diag   : partial diagonal sums of the input basis vector  (R(A) product, part 1)
+//   colsum : partial K (or K^T) column sums                     (part 2)
+//   dots   : z -> Toeplitz y ; v = y - beta*prev ; h = S^T v ; |v|^2 ; |y|^2
+//   apply  : v1 = v - S h (one classical GS pass), |v1|^2      (v kept in registers)
+//   write  : out = v1 / t                                      (t = |v1|)
+//
+// with 5 grid barriers; the vector v never leaves registers between dots,
+// apply and write (each thread owns up to MAXG*VEC elements), so one pass
+// writes the new basis vector and the reorthogonalisation reads the basis
+// twice (coefficients, update).  All cross-CTA sums are fixed-order
+// (per-CTA partials reduced in index order), so results are deterministic.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kb_ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kb {
+
+constexpr int PK_THREADS = 256;
+constexpr int PK_SEGS = 8;
+
+struct PkParams {
+    const void* K;    // kh x kw
+    const void* Kt;   // kw x kh
+    int kh, kw, n;
+    void* S;
+    void* Q;
+    int64_t ld_s, ld_q;
+    int cap;
+    const void* y0;
+    int* hdr;
+    double *alphas, *ts, *zetas, *nus;
+    double tol, tau;
+    int k_max, p, k_min, full_reorth;
+    double* diag_part;   // [PK_SEGS][Lmax]
+    double* col_part;    // [PK_SEGS][Lmax]
+    double* blk_part;    // [grid][cap + 4]
+    double* norm_part;   // [grid]
+    int ng;              // element groups per thread
+    int lmax;
+};
+
+enum { PH_DONE = 0, PH_FIRED, PH_REASON, PH_STOP, PH_BREAK, PH_TBREAK, PH_OVERFLOW, PH_ERR, PH_NA, PH_NT,
+       PH_NN };
+
+template <typename T, int VEC>
+struct PkIO;
+template <>
+struct PkIO<float, 4> {
+    static __device__ __forceinline__ void load(const float* p, float* v) {
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    }
+    static __device__ __forceinline__ void store(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct PkIO<double, 2> {
+    static __device__ __forceinline__ void load(const double* p, double* v) {
+        const double2 q = __ldcg(reinterpret_cast<const double2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    }
+    static __device__ __forceinline__ void store(double* p, const double* v) {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    }
+};
+
+__device__ __forceinline__ float pk_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double pk_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float pk_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double pk_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float pk_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double pk_div(double a, double b) { return __ddiv_rn(a, b); }
+
+// Fixed-order sum over the grid's per-CTA partials for slots [0, nslots):
+// warp w reduces slots w, w+8, ...; lanes stride over CTAs.  Result -> out[].
+__device__ __forceinline__ void pk_reduce_slots(const double* part, int stride, int nblk, int nslots,
+                                                double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = warp; j < nslots; j += PK_THREADS / 32) {
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += __ldcg(part + (int64_t)b * stride + j);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = s;
+    }
+}
+
+template <typename T>
+struct PkHalf {
+    const T* x;      // input basis vector of the R(A) product
+    const T* prev;   // previous basis vector (v = y - beta prev)
+    T beta;
+    const T* S;      // basis to project against
+    int64_t ld;
+    int m;           // basis vectors in S
+    T* out;          // new basis slot
+    int transpose;   // 0: y = R x (s step), 1: y = R^T x (q step)
+};
+
+// One half step.  Returns t = |v1| (and |y|^2 via ysq) identically in every CTA.
+template <typename T, int VEC, int MAXG>
+__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VEC], double* sm, double& ysq_out,
+                          cg::grid_group& grid) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    const int nblk = gridDim.x;
+    const int cu = P.kh / 2, cv = P.kw / 2;
+    const int ci = H.transpose ? cv : cu, Li = H.transpose ? P.kw : P.kh;
+    const int co = H.transpose ? cu : cv, Lo = H.transpose ? P.kh : P.kw;
+    const T* M = static_cast<const T*>(H.transpose ? P.Kt : P.K);   // Li x Lo row-major
+    double* zs = sm;                              // [lmax]
+    double* red = zs + P.lmax;                    // [cap + 4]
+    double* acc = red + P.cap + 4;                // [8][max(cap + 2, 33)]
+
+    // ---- diag: part[s][u] = sum_{rows a in segment s} x[a, a + u - ci]
+    {
+        const int chunks = (Li + 31) / 32;
+        const int items = chunks * PK_SEGS;
+        for (int it = blockIdx.x; it < items; it += nblk) {
+            const int c = it % chunks, seg = it / chunks;
+            const int u = c * 32 + lane;
+            const int d = u - ci;
+            const int s0 = (int)((int64_t)n * seg / PK_SEGS), s1 = (int)((int64_t)n * (seg + 1) / PK_SEGS);
+            double a = 0.0;
+            if (u < Li) {
+                const int lo = max(s0, -d), hi = min(s1, n - d);
+                int r = lo + warp;
+                const T* p = H.x + (int64_t)r * n + (r + d);
+                const int64_t step = 8 * (int64_t)(n + 1);
+                for (; r + 56 < hi; r += 64, p += 8 * step) {
+                    T q[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + k * step);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) a += (double)q[k];
+                }
+                for (; r < hi; r += 8, p += step) a += (double)__ldcg(p);
+            }
+            acc[warp * 33 + lane] = a;
+            __syncthreads();
+            if (warp == 0 && u < Li) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
+                P.diag_part[(int64_t)seg * P.lmax + u] = t;
+            }
+            __syncthreads();
+        }
+    }
+    grid.sync();
+    // ---- colsum: part[s][c] = sum_{rows r in segment s} M[r, c] * w[r],  w[r] = sum_s diag_part[s][r]
+    {
+        const int chunks = (Lo + 31) / 32;
+        const int items = chunks * PK_SEGS;
+        for (int it = blockIdx.x; it < items; it += nblk) {
+            const int cc = it % chunks, seg = it / chunks;
+            const int c = cc * 32 + lane;
+            const int r0 = (int)((int64_t)Li * seg / PK_SEGS), r1 = (int)((int64_t)Li * (seg + 1) / PK_SEGS);
+            double a = 0.0;
+            for (int r = r0 + warp; r < r1; r += 8) {
+                double w = 0.0;
+#pragma unroll
+                for (int q = 0; q < PK_SEGS; ++q) w += __ldcg(P.diag_part + (int64_t)q * P.lmax + r);
+                if (c < Lo) a += (double)__ldg(M + (int64_t)r * Lo + c) * w;
+            }
+            acc[warp * 33 + lane] = a;
+            __syncthreads();
+            if (warp == 0 && c < Lo) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
+                P.col_part[(int64_t)seg * P.lmax + c] = t;
+            }
+            __syncthreads();
+        }
+    }
+    grid.sync();
+    // ---- z (Toeplitz coefficients) into shared memory, fixed-order over segments
+    for (int c = tid; c < Lo; c += PK_THREADS) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < PK_SEGS; ++q) t += __ldcg(P.col_part + (int64_t)q * P.lmax + c);
+        zs[c] = t;
+    }
+    const int W = H.m + 2;
+    for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
+    __syncthreads();
+    // ---- dots: v = y - beta prev ; h = S^T v
+    const int64_t G = (int64_t)nblk * PK_THREADS;
+    const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
+    double ysq = 0.0, vsq = 0.0;
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+        const int64_t e0 = (g * G + gt) * VEC;
+        if (g < P.ng && e0 < N) {
+            T pv[VEC];
+            if (H.prev) {
+                PkIO<T, VEC>::load(H.prev + e0, pv);
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) pv[q] = T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const unsigned e = (unsigned)(e0 + q);
+                const unsigned a = e / (unsigned)n;
+                const int u = (int)(e - a * (unsigned)n) - (int)a + co;
+                const T yv = (u >= 0 && u < Lo) ? (T)zs[u] : T(0);
+                ysq += (double)yv * (double)yv;
+                v[g][q] = pk_sub(yv, pk_mul(H.beta, pv[q]));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) v[g][q] = T(0);
+        }
+    }
+#pragma unroll 2
+    for (int i = 0; i < H.m; ++i) {
+        const T* Si = H.S + (int64_t)i * H.ld;
+        double d = 0.0;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            const int64_t e0 = (g * G + gt) * VEC;
+            if (g < P.ng && e0 < N) {
+                T sv[VEC];
+                PkIO<T, VEC>::load(Si + e0, sv);
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) d += (double)sv[q] * (double)v[g][q];
+            }
+        }
+        d = warp_sum(d);
+        if (lane == 0) acc[warp * W + i] += d;
+    }
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) vsq += (double)v[g][q] * (double)v[g][q];
+    vsq = warp_sum(vsq);
+    ysq = warp_sum(ysq);
+    if (lane == 0) {
+        acc[warp * W + H.m] += vsq;
+        acc[warp * W + H.m + 1] += ysq;
+    }
+    __syncthreads();
+    for (int j = tid; j < W; j += PK_THREADS) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += acc[w * W + j];
+        P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
+    }
+    grid.sync();
+    pk_reduce_slots(P.blk_part, P.cap + 4, nblk, W, red);
+    __syncthreads();
+    ysq_out = red[H.m + 1];
+    double t;
+    if (H.m == 0) {
+        t = sqrt(red[0]);
+    } else {
+        // ---- apply: v1 = v - S h (fp64 accumulation, rounded once), |v1|^2
+        double v1sq = 0.0;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            const int64_t e0 = (g * G + gt) * VEC;
+            if (g < P.ng && e0 < N) {
+                double a[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) a[q] = (double)v[g][q];
+#pragma unroll 4
+                for (int i = 0; i < H.m; ++i) {
+                    T sv[VEC];
+                    PkIO<T, VEC>::load(H.S + (int64_t)i * H.ld + e0, sv);
+                    const double c = red[i];
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) a[q] -= c * (double)sv[q];
+                }
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) {
+                    v[g][q] = (T)a[q];
+                    v1sq += a[q] * a[q];
+                }
+            }
+        }
+        v1sq = warp_sum(v1sq);
+        __syncthreads();
+        if (lane == 0) acc[warp] = v1sq;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) s += acc[w];
+            P.norm_part[blockIdx.x] = s;
+        }
+        grid.sync();
+        pk_reduce_slots(P.norm_part, 1, nblk, 1, red + P.cap + 2);
+        __syncthreads();
+        t = sqrt(red[P.cap + 2]);
+    }
+    // ---- write: out = v1 / t
+    const T td = (T)t;
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+        const int64_t e0 = (g * G + gt) * VEC;
+        if (g < P.ng && e0 < N) {
+            T o[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) o[q] = pk_div(v[g][q], td);
+            PkIO<T, VEC>::store(H.out + e0, o);
+        }
+    }
+    grid.sync();
+    return t;
+}
+
+template <typename T, int VEC, int MAXG>
+__global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    const int nblk = gridDim.x;
+    T* S = static_cast<T*>(P.S);
+    T* Q = static_cast<T*>(P.Q);
+    const T* y0 = static_cast<const T*>(P.y0);
+    double* red = sm + P.lmax;
+    double* acc = red + P.cap + 4;
+    T v[MAXG][VEC];
+    const int64_t G = (int64_t)nblk * PK_THREADS;
+    const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
+
+    // ---- s1 = y0 / |y0|   (lowrank.py:207-210)
+    double vsq = 0.0;
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+        const int64_t e0 = (g * G + gt) * VEC;
+        if (g < P.ng && e0 < N) {
+            PkIO<T, VEC>::load(y0 + e0, v[g]);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) vsq += (double)v[g][q] * (double)v[g][q];
+        }
+    }
+    vsq = warp_sum(vsq);
+    if (lane == 0) acc[warp] = vsq;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += acc[w];
+        P.norm_part[blockIdx.x] = s;
+    }
+    grid.sync();
+    pk_reduce_slots(P.norm_part, 1, nblk, 1, red);
+    __syncthreads();
+    const double t1 = sqrt(red[0]);
+    {
+        const T td = (T)t1;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            const int64_t e0 = (g * G + gt) * VEC;
+            if (g < P.ng && e0 < N) {
+                T o[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) o[q] = pk_div(v[g][q], td);
+                PkIO<T, VEC>::store(S + e0, o);
+            }
+        }
+    }
+    grid.sync();
+    // ---- q1 = B^T s1 / alpha1   (lowrank.py:211-215)
+    double ysq = 0.0;
+    PkHalf<T> h1{S, nullptr, T(0), Q, P.ld_q, 0, Q, 1};
+    const double a1 = pk_half<T, VEC, MAXG>(P, h1, v, sm, ysq, grid);
+
+    int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
+    int na = 1, nt = 1, nn = 1;
+    double zeta_last = a1 * t1, nu_last = 1e308, alpha_cur = a1;
+    if (blockIdx.x == 0 && tid == 0) {
+        P.ts[0] = t1;
+        P.alphas[0] = a1;
+        P.zetas[0] = zeta_last;
+        P.nus[0] = nu_last;
+    }
+    if (t1 == 0.0) err = 1;
+    else if (a1 == 0.0) err = 2;
+    if (err) stop = 1;
+
+    while (!stop) {
+        // s step (lowrank.py:237-247)
+        PkHalf<T> hs{Q + (int64_t)(done - 1) * P.ld_q, S + (int64_t)(done - 1) * P.ld_s, (T)alpha_cur, S, P.ld_s,
+                     P.full_reorth ? done : 0, S + (int64_t)done * P.ld_s, 0};
+        double u2 = 0.0;
+        const double t_new = pk_half<T, VEC, MAXG>(P, hs, v, sm, u2, grid);
+        // q step (lowrank.py:249-260)
+        PkHalf<T> hq{S + (int64_t)done * P.ld_s, Q + (int64_t)(done - 1) * P.ld_q, (T)t_new, Q, P.ld_q, done,
+                     Q + (int64_t)done * P.ld_q, 1};
+        double p2 = 0.0;
+        const double a_new = pk_half<T, VEC, MAXG>(P, hq, v, sm, p2, grid);
+        // control (identical in every CTA; CTA 0 records the trace)
+        const bool rec = (blockIdx.x == 0 && tid == 0);
+        if (t_new <= P.tol * sqrt(u2)) {
+            breakdown = tbreak = 1;
+            stop = 1;
+        } else if (a_new <= P.tol * sqrt(p2)) {
+            breakdown = 1;
+            if (rec) P.ts[nt] = t_new;
+            ++nt;
+            stop = 1;
+        } else {
+            if (rec) {
+                P.ts[nt] = t_new;
+                P.alphas[na] = a_new;
+            }
+            ++nt;
+            ++na;
+            const double zeta = a_new * t_new;
+            const double nu = sqrt(zeta * zeta_last);
+            if (rec) {
+                P.zetas[nn] = zeta;
+                P.nus[nn] = nu;
+            }
+            ++nn;
+            zeta_last = zeta;
+            const double nu_prev = nu_last;
+            nu_last = nu;
+            alpha_cur = a_new;
+            ++done;
+            if (fired < 0) {
+                if (nu > nu_prev) {
+                    fired = max(done - 1, P.k_min);
+                    reason = KB_STOP_NU_ROSE;
+                } else if (nu < P.tau) {
+                    fired = max(done, P.k_min);
+                    reason = KB_STOP_NU_BELOW_TOL;
+                }
+            }
+            const int limit = fired >= 0 ? fired + P.p + 1 : P.k_max + 1;
+            if (done >= limit) stop = 1;
+            if (done + 1 > P.cap) {
+                stop = 1;
+                overflow = 1;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        int* h = P.hdr;
+        h[PH_DONE] = done;
+        h[PH_FIRED] = fired;
+        h[PH_REASON] = reason;
+        h[PH_STOP] = stop;
+        h[PH_BREAK] = breakdown;
+        h[PH_TBREAK] = tbreak;
+        h[PH_OVERFLOW] = overflow;
+        h[PH_ERR] = err;
+        h[PH_NA] = na;
+        h[PH_NT] = nt;
+        h[PH_NN] = nn;
+    }
+}
+
+// ------------------------------------------------------------------ host side
+constexpr int PK_MAXG_F32 = 16, PK_MAXG_F64 = 16;
+
+template <typename T, int VEC, int MAXG>
+static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
+    auto kern = k_egkb_persistent<T, VEC, MAXG>;
+    const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33) + 64);
+    static bool configured = false;
+    if (!configured) {
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        configured = true;
+    }
+    int per_sm = 0;
+    KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PK_THREADS, smem));
+    if (per_sm < 1) return false;
+    int dev = 0, sms = 0;
+    KB_CUDA(cudaGetDevice(&dev));
+    KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = sms * std::min(per_sm, 2);
+    const int64_t N = (int64_t)P.n * P.n;
+    const int64_t per = (int64_t)grid * PK_THREADS * VEC;
+    P.ng = (int)((N + per - 1) / per);
+    if (P.ng > MAXG) return false;
+    void* args[] = {&P};
+    ProfScope ps(st, PROF_REORTH, 0.0);
+    KB_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, PK_THREADS, args, smem, st));
+    grid_out = grid;
+    return true;
+}
+
+// Sizes of the scratch the persistent kernel needs (doubles).
+size_t pk_scratch_doubles(int lmax, int cap) {
+    return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs + 256;
+}
+
+// Returns false when the configuration is outside the persistent kernel's
+// envelope (the caller then uses the graph path).
+bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_state* st, const void* y0,
+                     int* hdr, double* trace, double* scratch, double tol, cudaStream_t s) {
+    if (op->kind != KB_OP_RA_ZERO) return false;
+    if (cfg->reorth_passes >= 2) return false;
+    const int n = op->side;
+    const int lmax = std::max(op->kh, op->kw);
+    const int64_t N = (int64_t)n * n;
+    const int vec = op->dtype == KB_F32 ? 4 : 2;
+    if (N % vec != 0 || st->ld_s % vec != 0 || st->ld_q % vec != 0) return false;
+    if (((uintptr_t)st->s_basis % 16) || ((uintptr_t)st->q_basis % 16) || ((uintptr_t)y0 % 16)) return false;
+    const int cap = st->capacity;
+    PkParams P{};
+    P.K = op->k;
+    P.Kt = op->kt;
+    P.kh = op->kh;
+    P.kw = op->kw;
+    P.n = n;
+    P.S = st->s_basis;
+    P.Q = st->q_basis;
+    P.ld_s = st->ld_s;
+    P.ld_q = st->ld_q;
+    P.cap = cap;
+    P.y0 = y0;
+    P.hdr = hdr;
+    P.alphas = trace;
+    P.ts = trace + cap;
+    P.zetas = trace + 2 * cap;
+    P.nus = trace + 3 * cap;
+    P.tol = tol;
+    P.tau = cfg->tau;
+    P.k_max = cfg->k_max;
+    P.p = cfg->p;
+    P.k_min = cfg->k_min;
+    P.full_reorth = cfg->full_reorth;
+    P.lmax = lmax;
+    P.diag_part = scratch;
+    P.col_part = scratch + (size_t)PK_SEGS * lmax;
+    P.blk_part = scratch + 2 * (size_t)PK_SEGS * lmax;
+    P.norm_part = P.blk_part + (size_t)(8 * kSMs) * (cap + 4);
+    int grid = 0;
+    // smallest register footprint that covers N with 2 CTAs per SM
+    const int64_t per = (int64_t)2 * kSMs * PK_THREADS * vec;
+    const int64_t ng = (N + per - 1) / per;
+    if (op->dtype == KB_F32) {
+        if (ng <= 4) return pk_launch<float, 4, 4>(P, s, grid);
+        if (ng <= 8) return pk_launch<float, 4, 8>(P, s, grid);
+        return pk_launch<float, 4, PK_MAXG_F32>(P, s, grid);
+    }
+    if (ng <= 4) return pk_launch<double, 2, 4>(P, s, grid);
+    if (ng <= 8) return pk_launch<double, 2, 8>(P, s, grid);
+    return pk_launch<double, 2, PK_MAXG_F64>(P, s, grid);
+}
+
+}  // namespace kb

@@ -588,7 +588,7 @@ static void launch_reorth(const Src& src, const void* S, int64_t ld, const MRef&
     }
     const int blocks = std::max(1, std::min<int>(ws.max_blocks, (int)cdiv(len, 256 * VEC * REORTH_R)));
     // algorithmic bytes (with m at its upper bound when resolved on the device)
-    double vecs = (double)mm + (src.prev.null() ? 0 : 1) + (out.null() ? 0 : 1) + (src.mode == SRC_BUFT ? 1 : 0);
+    double vecs = (double)(m.acct >= 0 ? m.acct : mm) + (src.prev.null() ? 0 : 1) + (out.null() ? 0 : 1) + (src.mode == SRC_BUFT ? 1 : 0);
     double bytes = vecs * len * sizeof(T) + (src.mode == SRC_BUF64 ? 8.0 * len : 0.0);
     ProfScope ps(st, PROF_REORTH, bytes);
     kern<<<blocks, 256, smem, st>>>(src.z, src.mode, src.side, src.center, src.L, src.prev, src.beta,

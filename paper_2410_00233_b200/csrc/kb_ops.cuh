@@ -33,7 +33,8 @@ struct MRef {
     int mul = 0;
     int add = 0;
     int max = 0;   // upper bound (shared-memory sizing)
-    static MRef fixed(int m) { MRef r; r.add = m; r.max = m; return r; }
+    int acct = -1; // host-known value for byte accounting (-1: unknown, use max)
+    static MRef fixed(int m) { MRef r; r.add = m; r.max = m; r.acct = m; return r; }
 };
 
 // Source of the generated vector v in the reorthogonalisation passes:

@@ -201,6 +201,24 @@ def _lift(code, basis, nrows, W, out_rows):
 
 
 # ----------------------------------------------------------------- eGKB
+_BASES: dict = {}
+
+
+def _bases(cap, mbar, nbar, dtype):
+    """Persistent Krylov bases per shape: stable addresses let kb_egkb_run
+    replay its cached CUDA graph instead of re-capturing it."""
+    from . import device as D
+
+    key = (cap, mbar, nbar, np.dtype(dtype).str, D.device().index)
+    hit = _BASES.get(key)
+    if hit is None:
+        if len(_BASES) >= 4:
+            _BASES.pop(next(iter(_BASES)))
+        hit = (D.empty((cap, mbar), dtype), D.empty((cap, nbar), dtype))
+        _BASES[key] = hit
+    return hit
+
+
 def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     """Enlarged Golub-Kahan bidiagonalisation with automatic rank choice
     (lowrank.py:159-329), on the GPU.
@@ -241,8 +259,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
                             1 if reorth == REORTH_FULL else 0, int(reorth_passes))
     lib = _lib.load()
     cap = lib.kb_egkb_capacity(C.byref(cfg))
-    s_basis = D.empty((cap, mbar), dtype)
-    q_basis = D.empty((cap, nbar), dtype)
+    s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
     hist = np.zeros((4, cap), dtype=np.float64)
     dp = C.POINTER(C.c_double)
     st = _lib.KbEgkbState()
