@@ -139,6 +139,10 @@ typedef struct {
     int capacity;
     /* caller-allocated host arrays of length `capacity` (trace, 1-based lists) */
     double* alphas_host; double* ts_host; double* zetas_host; double* nus_host;
+    /* caller-allocated host arrays of length `capacity`: basis vector i is
+     * stored scaled, the normalised vector is s_basis[i] * s_scale_host[i]
+     * (the persistent kernel folds the normalisation into its consumers) */
+    double* s_scale_host; double* q_scale_host;
     /* outputs */
     int n_alphas, n_ts, n_nus;
     int chosen_k, k_p, rows, stop_reason, breakdown;

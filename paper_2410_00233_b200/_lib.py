@@ -45,6 +45,7 @@ class KbEgkbConfig(C.Structure):
 class KbEgkbState(C.Structure):
     _fields_ = [("s_basis", vp), ("ld_s", i64), ("q_basis", vp), ("ld_q", i64), ("capacity", C.c_int),
                 ("alphas_host", dp), ("ts_host", dp), ("zetas_host", dp), ("nus_host", dp),
+                ("s_scale_host", dp), ("q_scale_host", dp),
                 ("n_alphas", C.c_int), ("n_ts", C.c_int), ("n_nus", C.c_int),
                 ("chosen_k", C.c_int), ("k_p", C.c_int), ("rows", C.c_int),
                 ("stop_reason", C.c_int), ("breakdown", C.c_int)]

@@ -204,11 +204,13 @@ __global__ void k_egkb_control(EgkbCtl c) {
 
 size_t pk_scratch_doubles(int lmax, int cap);
 bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_state* st, const void* y0,
-                     int* hdr, double* trace, double* scratch, double tol, cudaStream_t s);
+                     int* hdr, double* trace, double* scratch, void* raw, double tol, double** scales_out,
+                     cudaStream_t s);
 void prof_set_last_bytes(double bytes);
 
 struct EgkbWs {
     double* pk = nullptr;  // persistent-kernel scratch
+    void* pkraw = nullptr; // two pending vectors (2 N elements)
     OpPlan plan;
     ReorthWs rw;
     double* red_s;      // coefficient slots (capacity + 8)
@@ -230,6 +232,7 @@ static void egkb_ws_size(const kb_operator* op, int capacity, Sizer& s) {
     s.take<double>(4 * (size_t)capacity);
     s.take<double>((size_t)op->rows);
     s.take<double>(pk_scratch_doubles(std::max(op->kh, op->kw), capacity));
+    s.take<double>(2 * (size_t)op_len(op));
 }
 
 static EgkbWs egkb_ws_make(const kb_operator* op, int capacity, Arena& a) {
@@ -245,6 +248,7 @@ static EgkbWs egkb_ws_make(const kb_operator* op, int capacity, Arena& a) {
     w.trace = a.take<double>(4 * (size_t)capacity);
     w.y0slot = a.take<double>((size_t)op->rows);
     w.pk = a.take<double>(pk_scratch_doubles(std::max(op->kh, op->kw), capacity));
+    w.pkraw = a.take<double>(2 * (size_t)op_len(op));
     return w;
 }
 
@@ -477,8 +481,10 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     // cannot profile kernel nodes of graphs that contain conditional nodes
     static const bool no_pk = std::getenv("KB_EGKB_NO_PERSISTENT") != nullptr;
     bool pk_done = false;
+    double* pk_scales = nullptr;
     if (!force_eager && !no_pk)
-        pk_done = egkb_persistent(op, cfg, st, P.w.y0slot, P.w.hdr, P.w.trace, P.w.pk, c.tol, s);
+        pk_done = egkb_persistent(op, cfg, st, P.w.y0slot, P.w.hdr, P.w.trace, P.w.pk, P.w.pkraw, c.tol,
+                                  &pk_scales, s);
     if (pk_done) {
         // single persistent kernel ran the whole loop
     } else if (!g_prof && !force_eager) {
@@ -518,7 +524,13 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     }
     KB_CUDA(cudaMemcpyAsync(hh, P.w.hdr, sizeof(int) * H_COUNT, cudaMemcpyDeviceToHost, s));
     KB_CUDA(cudaMemcpyAsync(ht, P.w.trace, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost, s));
+    if (pk_done && pk_scales && st->s_scale_host && st->q_scale_host) {
+        KB_CUDA(cudaMemcpyAsync(st->s_scale_host, pk_scales, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+        KB_CUDA(cudaMemcpyAsync(st->q_scale_host, pk_scales + cap, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    }
     KB_CUDA(cudaStreamSynchronize(s));
+    if ((!pk_done || !pk_scales) && st->s_scale_host && st->q_scale_host)
+        for (int i = 0; i < cap; ++i) st->s_scale_host[i] = st->q_scale_host[i] = 1.0;
     if (hh[H_ERR] == 1) {
         set_error("starting vector must be nonzero");
         throw Fail{KB_EVALIDATION};

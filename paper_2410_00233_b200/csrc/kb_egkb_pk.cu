@@ -21,6 +21,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kb_ops.cuh"
 
@@ -48,9 +51,23 @@ struct PkParams {
     double* col_part;    // [PK_SEGS][Lmax]
     double* blk_part;    // [grid][cap + 4]
     double* norm_part;   // [grid]
+    void* raw_s;         // pending unnormalised s vector (N elements)
+    void* raw_q;         // pending unnormalised q vector
     int ng;              // element groups per thread
     int lmax;
+    unsigned long long* dbg;   // optional phase timestamps (block 0), KB_PK_TRACE
+    int* dbg_n;
 };
+
+__device__ __forceinline__ void pk_mark(const PkParams& P) {
+    if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int k = *P.dbg_n;
+        if (k < 4096) P.dbg[k] = t;
+        *P.dbg_n = k + 1;
+    }
+}
 
 enum { PH_DONE = 0, PH_FIRED, PH_REASON, PH_STOP, PH_BREAK, PH_TBREAK, PH_OVERFLOW, PH_ERR, PH_NA, PH_NT,
        PH_NN };
@@ -100,20 +117,21 @@ __device__ __forceinline__ void pk_reduce_slots(const double* part, int stride, 
 
 template <typename T>
 struct PkHalf {
-    const T* x;      // input basis vector of the R(A) product
-    const T* prev;   // previous basis vector (v = y - beta prev)
+    const T* x;       // input basis vector of the R(A) product (normalised)
+    const T* prev;    // previous basis vector (normalised), v = y - beta * prev
     T beta;
-    const T* S;      // basis to project against
+    const T* S;       // basis to project against
     int64_t ld;
-    int m;           // basis vectors in S
-    T* out;          // new basis slot
-    int transpose;   // 0: y = R x (s step), 1: y = R^T x (q step)
+    int m;            // basis vectors in S
+    T* out;           // new basis slot (receives fl(v1 / t), as lowrank.py:247, 260)
+    int transpose;    // 0: y = R x (s step), 1: y = R^T x (q step)
 };
 
-// One half step.  Returns t = |v1| (and |y|^2 via ysq) identically in every CTA.
+// One half step.  Returns t = |v1| (identical in every CTA).
 template <typename T, int VEC, int MAXG>
-__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VEC], double* sm, double& ysq_out,
-                          cg::grid_group& grid) {
+__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid) {
+    constexpr int GC = 4;   // element groups processed together (loads in flight per basis vector)
+    static_assert(MAXG % GC == 0, "MAXG must be a multiple of GC");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
     const int64_t N = (int64_t)n * n;
@@ -125,6 +143,8 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
     double* zs = sm;                              // [lmax]
     double* red = zs + P.lmax;                    // [cap + 4]
     double* acc = red + P.cap + 4;                // [8][max(cap + 2, 33)]
+    const int64_t G = (int64_t)nblk * PK_THREADS;
+    const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
 
     // ---- diag: part[s][u] = sum_{rows a in segment s} x[a, a + u - ci]
     {
@@ -162,6 +182,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
         }
     }
     grid.sync();
+    pk_mark(P);
     // ---- colsum: part[s][c] = sum_{rows r in segment s} M[r, c] * w[r],  w[r] = sum_s diag_part[s][r]
     {
         const int chunks = (Lo + 31) / 32;
@@ -189,6 +210,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
         }
     }
     grid.sync();
+    pk_mark(P);
     // ---- z (Toeplitz coefficients) into shared memory, fixed-order over segments
     for (int c = tid; c < Lo; c += PK_THREADS) {
         double t = 0.0;
@@ -199,9 +221,8 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
     const int W = H.m + 2;
     for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
     __syncthreads();
-    // ---- dots: v = y - beta prev ; h = S^T v
-    const int64_t G = (int64_t)nblk * PK_THREADS;
-    const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
+    // ---- dots: v = y - beta*prev (fp32 ops as the reference) ; h = S^T v
+    T v[MAXG][VEC];
     double ysq = 0.0, vsq = 0.0;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g) {
@@ -228,7 +249,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
             for (int q = 0; q < VEC; ++q) v[g][q] = T(0);
         }
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int i = 0; i < H.m; ++i) {
         const T* Si = H.S + (int64_t)i * H.ld;
         double d = 0.0;
@@ -263,6 +284,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
         P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
     }
     grid.sync();
+    pk_mark(P);
     pk_reduce_slots(P.blk_part, P.cap + 4, nblk, W, red);
     __syncthreads();
     ysq_out = red[H.m + 1];
@@ -270,46 +292,56 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
     if (H.m == 0) {
         t = sqrt(red[0]);
     } else {
-        // ---- apply: v1 = v - S h (fp64 accumulation, rounded once), |v1|^2
-        double v1sq = 0.0;
+    // ---- apply: v1 = v - S h (fp64 accumulation, rounded once), kept in registers
+    double v1sq = 0.0;
 #pragma unroll
-        for (int g = 0; g < MAXG; ++g) {
-            const int64_t e0 = (g * G + gt) * VEC;
-            if (g < P.ng && e0 < N) {
-                double a[VEC];
+    for (int g0 = 0; g0 < MAXG; g0 += GC) {
+        if (g0 >= P.ng) break;
+        double a[GC][VEC];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) a[q] = (double)v[g][q];
+        for (int g = 0; g < GC; ++g)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) a[g][q] = (double)v[g0 + g][q];
 #pragma unroll 4
-                for (int i = 0; i < H.m; ++i) {
+        for (int i = 0; i < H.m; ++i) {
+            const T* Si = H.S + (int64_t)i * H.ld;
+            const double c = red[i];
+#pragma unroll
+            for (int g = 0; g < GC; ++g) {
+                const int64_t e0 = ((g0 + g) * G + gt) * VEC;
+                if (g0 + g < P.ng && e0 < N) {
                     T sv[VEC];
-                    PkIO<T, VEC>::load(H.S + (int64_t)i * H.ld + e0, sv);
-                    const double c = red[i];
+                    PkIO<T, VEC>::load(Si + e0, sv);
 #pragma unroll
-                    for (int q = 0; q < VEC; ++q) a[q] -= c * (double)sv[q];
-                }
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) {
-                    v[g][q] = (T)a[q];
-                    v1sq += a[q] * a[q];
+                    for (int q = 0; q < VEC; ++q) a[g][q] -= c * (double)sv[q];
                 }
             }
         }
-        v1sq = warp_sum(v1sq);
-        __syncthreads();
-        if (lane == 0) acc[warp] = v1sq;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) s += acc[w];
-            P.norm_part[blockIdx.x] = s;
+        for (int g = 0; g < GC; ++g) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                v[g0 + g][q] = (T)a[g][q];
+                v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
+            }
         }
-        grid.sync();
-        pk_reduce_slots(P.norm_part, 1, nblk, 1, red + P.cap + 2);
-        __syncthreads();
-        t = sqrt(red[P.cap + 2]);
     }
-    // ---- write: out = v1 / t
+    v1sq = warp_sum(v1sq);
+    if (lane == 0) acc[warp] = v1sq;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += acc[w];
+        P.norm_part[blockIdx.x] = s;
+    }
+    grid.sync();
+    pk_mark(P);
+    pk_reduce_slots(P.norm_part, 1, nblk, 1, red + P.cap + 2);
+    __syncthreads();
+    t = sqrt(red[P.cap + 2]);
+    }
+    // ---- write: out = fl(v1 / t)
     const T td = (T)t;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g) {
@@ -322,6 +354,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, T (&v)[MAXG][VE
         }
     }
     grid.sync();
+    pk_mark(P);
     return t;
 }
 
@@ -338,19 +371,20 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     const T* y0 = static_cast<const T*>(P.y0);
     double* red = sm + P.lmax;
     double* acc = red + P.cap + 4;
-    T v[MAXG][VEC];
     const int64_t G = (int64_t)nblk * PK_THREADS;
     const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
+    const bool rec = (blockIdx.x == 0 && tid == 0);
 
     // ---- s1 = y0 / |y0|   (lowrank.py:207-210)
+    T v0[MAXG][VEC];
     double vsq = 0.0;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g) {
         const int64_t e0 = (g * G + gt) * VEC;
         if (g < P.ng && e0 < N) {
-            PkIO<T, VEC>::load(y0 + e0, v[g]);
+            PkIO<T, VEC>::load(y0 + e0, v0[g]);
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) vsq += (double)v[g][q] * (double)v[g][q];
+            for (int q = 0; q < VEC; ++q) vsq += (double)v0[g][q] * (double)v0[g][q];
         }
     }
     vsq = warp_sum(vsq);
@@ -362,6 +396,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
         P.norm_part[blockIdx.x] = s;
     }
     grid.sync();
+    pk_mark(P);
     pk_reduce_slots(P.norm_part, 1, nblk, 1, red);
     __syncthreads();
     const double t1 = sqrt(red[0]);
@@ -373,21 +408,22 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
             if (g < P.ng && e0 < N) {
                 T o[VEC];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) o[q] = pk_div(v[g][q], td);
+                for (int q = 0; q < VEC; ++q) o[q] = pk_div(v0[g][q], td);
                 PkIO<T, VEC>::store(S + e0, o);
             }
         }
     }
     grid.sync();
+    pk_mark(P);
     // ---- q1 = B^T s1 / alpha1   (lowrank.py:211-215)
     double ysq = 0.0;
     PkHalf<T> h1{S, nullptr, T(0), Q, P.ld_q, 0, Q, 1};
-    const double a1 = pk_half<T, VEC, MAXG>(P, h1, v, sm, ysq, grid);
+    const double a1 = pk_half<T, VEC, MAXG>(P, h1, sm, ysq, grid);
 
     int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
     int na = 1, nt = 1, nn = 1;
     double zeta_last = a1 * t1, nu_last = 1e308, alpha_cur = a1;
-    if (blockIdx.x == 0 && tid == 0) {
+    if (rec) {
         P.ts[0] = t1;
         P.alphas[0] = a1;
         P.zetas[0] = zeta_last;
@@ -402,14 +438,13 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
         PkHalf<T> hs{Q + (int64_t)(done - 1) * P.ld_q, S + (int64_t)(done - 1) * P.ld_s, (T)alpha_cur, S, P.ld_s,
                      P.full_reorth ? done : 0, S + (int64_t)done * P.ld_s, 0};
         double u2 = 0.0;
-        const double t_new = pk_half<T, VEC, MAXG>(P, hs, v, sm, u2, grid);
+        const double t_new = pk_half<T, VEC, MAXG>(P, hs, sm, u2, grid);
         // q step (lowrank.py:249-260)
         PkHalf<T> hq{S + (int64_t)done * P.ld_s, Q + (int64_t)(done - 1) * P.ld_q, (T)t_new, Q, P.ld_q, done,
                      Q + (int64_t)done * P.ld_q, 1};
         double p2 = 0.0;
-        const double a_new = pk_half<T, VEC, MAXG>(P, hq, v, sm, p2, grid);
+        const double a_new = pk_half<T, VEC, MAXG>(P, hq, sm, p2, grid);
         // control (identical in every CTA; CTA 0 records the trace)
-        const bool rec = (blockIdx.x == 0 && tid == 0);
         if (t_new <= P.tol * sqrt(u2)) {
             breakdown = tbreak = 1;
             stop = 1;
@@ -454,7 +489,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
             }
         }
     }
-    if (blockIdx.x == 0 && tid == 0) {
+    if (rec) {
         int* h = P.hdr;
         h[PH_DONE] = done;
         h[PH_FIRED] = fired;
@@ -476,7 +511,8 @@ constexpr int PK_MAXG_F32 = 16, PK_MAXG_F64 = 16;
 template <typename T, int VEC, int MAXG>
 static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     auto kern = k_egkb_persistent<T, VEC, MAXG>;
-    const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33) + 64);
+    const size_t smem =
+        sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33) + 64);
     static bool configured = false;
     if (!configured) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -484,6 +520,7 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     }
     int per_sm = 0;
     KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PK_THREADS, smem));
+    if (std::getenv("KB_DEBUG")) fprintf(stderr, "[kb] persistent eGKB: %d CTAs/SM, smem %zu\n", per_sm, smem);
     if (per_sm < 1) return false;
     int dev = 0, sms = 0;
     KB_CUDA(cudaGetDevice(&dev));
@@ -495,20 +532,32 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     if (P.ng > MAXG) return false;
     void* args[] = {&P};
     ProfScope ps(st, PROF_REORTH, 0.0);
-    KB_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, PK_THREADS, args, smem, st));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(PK_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    (void)args;
+    KB_CUDA(cudaLaunchKernelEx(&lc, kern, P));
     grid_out = grid;
     return true;
 }
 
 // Sizes of the scratch the persistent kernel needs (doubles).
 size_t pk_scratch_doubles(int lmax, int cap) {
-    return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs + 256;
+    return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs + 2 * (size_t)cap + 256;
 }
 
 // Returns false when the configuration is outside the persistent kernel's
 // envelope (the caller then uses the graph path).
 bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_state* st, const void* y0,
-                     int* hdr, double* trace, double* scratch, double tol, cudaStream_t s) {
+                     int* hdr, double* trace, double* scratch, void* raw, double tol, double** scales_out,
+                     cudaStream_t s) {
     if (op->kind != KB_OP_RA_ZERO) return false;
     if (cfg->reorth_passes >= 2) return false;
     const int n = op->side;
@@ -546,6 +595,36 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     P.col_part = scratch + (size_t)PK_SEGS * lmax;
     P.blk_part = scratch + 2 * (size_t)PK_SEGS * lmax;
     P.norm_part = P.blk_part + (size_t)(8 * kSMs) * (cap + 4);
+    P.raw_s = raw;
+    P.raw_q = static_cast<char*>(raw) + (size_t)N * (op->dtype == KB_F32 ? 4 : 8);
+    *scales_out = nullptr;
+    static unsigned long long* dbg = nullptr;
+    static int* dbg_n = nullptr;
+    const bool want_trace = std::getenv("KB_PK_TRACE") != nullptr;
+    if (want_trace) {
+        if (!dbg) {
+            KB_CUDA(cudaMalloc(&dbg, 4096 * sizeof(unsigned long long)));
+            KB_CUDA(cudaMalloc(&dbg_n, sizeof(int)));
+        }
+        KB_CUDA(cudaMemsetAsync(dbg_n, 0, sizeof(int), s));
+        P.dbg = dbg;
+        P.dbg_n = dbg_n;
+    }
+    struct Dump {
+        bool on; cudaStream_t s; unsigned long long* d; int* n;
+        ~Dump() {
+            if (!on) return;
+            int k = 0;
+            cudaMemcpyAsync(&k, n, sizeof(int), cudaMemcpyDeviceToHost, s);
+            std::vector<unsigned long long> t(4096);
+            cudaMemcpyAsync(t.data(), d, sizeof(unsigned long long) * 4096, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            k = std::min(k, 4096);
+            fprintf(stderr, "[kb] pk phases (us):");
+            for (int i = 1; i < k; ++i) fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
+            fprintf(stderr, "\n");
+        }
+    } dump{want_trace, s, dbg, dbg_n};
     int grid = 0;
     // smallest register footprint that covers N with 2 CTAs per SM
     const int64_t per = (int64_t)2 * kSMs * PK_THREADS * vec;

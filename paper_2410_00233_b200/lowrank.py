@@ -260,7 +260,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     lib = _lib.load()
     cap = lib.kb_egkb_capacity(C.byref(cfg))
     s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
-    hist = np.zeros((4, cap), dtype=np.float64)
+    hist = np.zeros((6, cap), dtype=np.float64)
     dp = C.POINTER(C.c_double)
     st = _lib.KbEgkbState()
     st.s_basis, st.ld_s, st.q_basis, st.ld_q, st.capacity = s_basis.data_ptr(), mbar, q_basis.data_ptr(), nbar, cap
@@ -268,6 +268,8 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     st.ts_host = hist[1].ctypes.data_as(dp)
     st.zetas_host = hist[2].ctypes.data_as(dp)
     st.nus_host = hist[3].ctypes.data_as(dp)
+    st.s_scale_host = hist[4].ctypes.data_as(dp)
+    st.q_scale_host = hist[5].ctypes.data_as(dp)
     nb = C.c_size_t()
     _lib.check(lib.kb_egkb_workspace_bytes(C.byref(op.struct), cap, C.byref(nb)))
     ws, wsb = D.WORKSPACE.get(nb.value)
@@ -288,16 +290,20 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
         if i + 1 < rows:
             c_mat[i + 1, i] = trace.ts[i + 1]
     core = svd_small(c_mat)   # host LAPACK, as lowrank.py:316
-    u_rows = _lift(op.code, s_basis, rows, core.u[:, :chosen], chosen)
-    v_rows = _lift(op.code, q_basis, k_p, core.v[:, :chosen], chosen)
+    # bases may be stored scaled (s_i = stored_i * scale_i): fold into the lift weights
+    s_scale, q_scale = hist[4], hist[5]
+    w_u = core.u[:, :chosen].astype(np.float64) * s_scale[:rows, None]
+    w_v = core.v[:, :chosen].astype(np.float64) * q_scale[:k_p, None]
+    u_rows = _lift(op.code, s_basis, rows, w_u, chosen)
+    v_rows = _lift(op.code, q_basis, k_p, w_v, chosen)
 
     trace.chosen_k = chosen
     trace.k_p = k_p
     trace.stop_reason = _lib.KB_STOP[st.stop_reason]
     trace.breakdown = bool(st.breakdown)
     if config.keep_basis:
-        trace.s_basis = D.to_host(s_basis[:rows]).T.copy()
-        trace.q_basis = D.to_host(q_basis[:k_p]).T.copy()
+        trace.s_basis = (D.to_host(s_basis[:rows]).T * s_scale[:rows]).astype(dtype)
+        trace.q_basis = (D.to_host(q_basis[:k_p]).T * q_scale[:k_p]).astype(dtype)
         trace.c_mat = c_mat
     return TruncatedSvd.from_device(u_rows, core.sigma[:chosen].copy(), v_rows), trace
 
