@@ -9,31 +9,14 @@
 // GEMM with inner dimension k*n1).  Row-major operands; trans flags select
 // the smem staging layout so fragment reads are bank-conflict free.
 //
-// CTA tile 128 x 64 x 16, 8 warps (4 x 2) of 32 x 32, 3-stage cp.async
-// pipeline with zero-filled edges (any M, N, K, ld).
+// Tile configurations below (default: 128 x 64 x 16, 8 warps of 32 x 32,
+// 3-stage cp.async ring, zero-filled edges for any M, N, K, ld).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kb_common.cuh"
 
 namespace kb {
-
-namespace g64 {
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int PAD = 4;
-// smem sizes (doubles) per stage
-template <bool TA>
-struct ALayout {
-    static constexpr int rows = TA ? BK : BM;
-    static constexpr int ld = TA ? (BM + PAD) : (BK + PAD);
-    static constexpr int size = rows * ld;
-};
-template <bool TB>
-struct BLayout {
-    static constexpr int rows = TB ? BN : BK;
-    static constexpr int ld = TB ? (BK + PAD) : (BN + PAD);
-    static constexpr int size = rows * ld;
-};
-}  // namespace g64
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -55,25 +38,52 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// Tile configuration: CTA tile BM x BN x BK, STAGES-deep cp.async ring,
+// WM x WN warps each owning a (BM/WM) x (BN/WN) accumulator tile of 8x8 DMMA
+// blocks.  Padding keeps the 64-bit fragment reads bank-conflict free.
+template <int BM_, int BN_, int BK_, int ST_, int WM_, int WN_, int MINB_>
+struct GCfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = ST_, WM = WM_, WN = WN_, MINB = MINB_;
+    static constexpr int THREADS = WM * WN * 32;
+    static constexpr int WTM = BM / WM, WTN = BN / WN, MI = WTM / 8, NI = WTN / 8;
+    static constexpr int PAD = 4;
+    template <bool TA>
+    struct A {
+        static constexpr int rows = TA ? BK : BM;
+        static constexpr int ld = TA ? (BM + PAD) : (BK + PAD);
+        static constexpr int size = rows * ld;
+    };
+    template <bool TB>
+    struct B {
+        static constexpr int rows = TB ? BN : BK;
+        static constexpr int ld = TB ? (BK + PAD) : (BN + PAD);
+        static constexpr int size = rows * ld;
+    };
+    template <bool TA, bool TB>
+    static constexpr size_t smem() { return sizeof(double) * STAGES * (A<TA>::size + B<TB>::size); }
+};
+
 // V16: operands 16-byte aligned with even leading dims and even M/N/K, so
 // tiles move as 16-byte cp.async chunks (half the LSU ops of the 8-byte path).
 // Split-K: blockIdx.z = batch * splits + split; split s handles k-tiles
 // [s*T/splits, (s+1)*T/splits) and writes its own partial C (reduced later).
-template <bool TA, bool TB, bool V16>
-__global__ void __launch_bounds__(g64::THREADS, 2)
+template <class CF, bool TA, bool TB, bool V16>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sa_batch,
         int64_t sa_seg, const double* __restrict__ B, int64_t ldb, int64_t sb_batch,
         int64_t sb_seg, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nseg,
         double beta, int splits, int64_t split_stride) {
-    using namespace g64;
-    using AL = ALayout<TA>;
-    using BL = BLayout<TB>;
+    constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES, THREADS = CF::THREADS;
+    constexpr int MI = CF::MI, NI = CF::NI;
+    using AL = typename CF::template A<TA>;
+    using BL = typename CF::template B<TB>;
+    static_assert((BM * BK) % (2 * THREADS) == 0 && (BK * BN) % (2 * THREADS) == 0, "tile/threads mismatch");
     extern __shared__ __align__(16) double smem[];
     double* As = smem;                       // [STAGES][AL::size]
     double* Bs = smem + STAGES * AL::size;   // [STAGES][BL::size]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+    const int wm = warp % CF::WM, wn = warp / CF::WM;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int z = blockIdx.z / splits, split = blockIdx.z - z * splits;
     const double* Ab = A + (int64_t)z * sa_batch;
@@ -94,7 +104,6 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
         double* as = As + stage * AL::size;
         double* bs = Bs + stage * BL::size;
         if constexpr (V16) {
-            // A tile: BM x BK in 16-byte chunks (2 doubles along the contiguous dim)
 #pragma unroll
             for (int r = 0; r < (BM * BK) / (2 * THREADS); ++r) {
                 const int idx = tid + r * THREADS;
@@ -119,41 +128,39 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
                 double* dst = TB ? (bs + c * BL::ld + j) : (bs + j * BL::ld + c);
                 cp_async16(dst, src, ok);
             }
-            return;
-        }
-        // A tile: BM x BK
+        } else {
 #pragma unroll
-        for (int r = 0; r < (BM * BK) / THREADS; ++r) {
-            const int idx = tid + r * THREADS;
-            int i, j;  // i: m, j: k
-            if (!TA) { i = idx / BK; j = idx % BK; } else { j = idx / BM; i = idx % BM; }
-            const int gm = m0 + i, gk = k0 + j;
-            const bool ok = (gm < M) && (gk < K);
-            const double* src = TA ? (Ap + (int64_t)(ok ? gk : 0) * lda + (ok ? gm : 0))
-                                   : (Ap + (int64_t)(ok ? gm : 0) * lda + (ok ? gk : 0));
-            double* dst = TA ? (as + j * AL::ld + i) : (as + i * AL::ld + j);
-            cp_async8(dst, src, ok);
-        }
-        // B tile: BK x BN
+            for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+                const int idx = tid + r * THREADS;
+                int i, j;
+                if (!TA) { i = idx / BK; j = idx % BK; } else { j = idx / BM; i = idx % BM; }
+                const int gm = m0 + i, gk = k0 + j;
+                const bool ok = (gm < M) && (gk < K);
+                const double* src = TA ? (Ap + (int64_t)(ok ? gk : 0) * lda + (ok ? gm : 0))
+                                       : (Ap + (int64_t)(ok ? gm : 0) * lda + (ok ? gk : 0));
+                double* dst = TA ? (as + j * AL::ld + i) : (as + i * AL::ld + j);
+                cp_async8(dst, src, ok);
+            }
 #pragma unroll
-        for (int r = 0; r < (BK * BN) / THREADS; ++r) {
-            const int idx = tid + r * THREADS;
-            int j, c;  // j: k, c: n
-            if (!TB) { j = idx / BN; c = idx % BN; } else { c = idx / BK; j = idx % BK; }
-            const int gk = k0 + j, gn = n0 + c;
-            const bool ok = (gk < K) && (gn < N);
-            const double* src = TB ? (Bp + (int64_t)(ok ? gn : 0) * ldb + (ok ? gk : 0))
-                                   : (Bp + (int64_t)(ok ? gk : 0) * ldb + (ok ? gn : 0));
-            double* dst = TB ? (bs + c * BL::ld + j) : (bs + j * BL::ld + c);
-            cp_async8(dst, src, ok);
+            for (int r = 0; r < (BK * BN) / THREADS; ++r) {
+                const int idx = tid + r * THREADS;
+                int j, c;
+                if (!TB) { j = idx / BN; c = idx % BN; } else { c = idx / BK; j = idx % BK; }
+                const int gk = k0 + j, gn = n0 + c;
+                const bool ok = (gk < K) && (gn < N);
+                const double* src = TB ? (Bp + (int64_t)(ok ? gn : 0) * ldb + (ok ? gk : 0))
+                                       : (Bp + (int64_t)(ok ? gk : 0) * ldb + (ok ? gn : 0));
+                double* dst = TB ? (bs + c * BL::ld + j) : (bs + j * BL::ld + c);
+                cp_async8(dst, src, ok);
+            }
         }
     };
 
-    double acc[4][4][2];
+    double acc[MI][NI][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MI; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -174,32 +181,32 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
         const double* bs = Bs + (t % STAGES) * BL::size;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double af[4], bf[4];
+            double af[MI], bf[NI];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) {
-                const int mm = wm * 32 + mi * 8 + gid, k = kk + tig;
+            for (int mi = 0; mi < MI; ++mi) {
+                const int mm = wm * CF::WTM + mi * 8 + gid, k = kk + tig;
                 af[mi] = TA ? as[k * AL::ld + mm] : as[mm * AL::ld + k];
             }
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int nn = wn * 32 + ni * 8 + gid, k = kk + tig;
+            for (int ni = 0; ni < NI; ++ni) {
+                const int nn = wn * CF::WTN + ni * 8 + gid, k = kk + tig;
                 bf[ni] = TB ? bs[nn * BL::ld + k] : bs[k * BL::ld + nn];
             }
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
     }
     cp_async_wait<0>();
 
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const int gm = m0 + wm * 32 + mi * 8 + gid;
+    for (int mi = 0; mi < MI; ++mi) {
+        const int gm = m0 + wm * CF::WTM + mi * 8 + gid;
         if (gm >= M) continue;
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const int gn = n0 + wn * 32 + ni * 8 + 2 * tig;
+        for (int ni = 0; ni < NI; ++ni) {
+            const int gn = n0 + wn * CF::WTN + ni * 8 + 2 * tig;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (gn + q < N) {
@@ -227,29 +234,35 @@ __global__ void k_split_reduce(const double* __restrict__ part, int splits, int6
     }
 }
 
-template <bool TA, bool TB, bool V16>
+// Tile configurations (selected by kb_dgemm_config / KB_DGEMM_CFG for tuning).
+using Cfg0 = GCfg<128, 64, 16, 3, 4, 2, 2>;    // 8 warps of 32x32, 2 CTAs/SM
+using Cfg1 = GCfg<128, 64, 32, 2, 4, 2, 2>;    // BK 32: half the barriers per flop
+using Cfg2 = GCfg<128, 128, 16, 3, 2, 4, 1>;   // 8 warps of 64x32, 1 CTA/SM
+using Cfg3 = GCfg<128, 128, 32, 2, 2, 4, 1>;
+static int g_dgemm_cfg = -1;
+
+template <class CF, bool TA, bool TB, bool V16>
 static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
                          int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s,
                          double* C, int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta,
                          int splits, double* part, int64_t split_stride, cudaStream_t st) {
-    using namespace g64;
-    const size_t smem = sizeof(double) * STAGES * (ALayout<TA>::size + BLayout<TB>::size);
+    const size_t smem = CF::template smem<TA, TB>();
     static bool configured = false;
     if (!configured) {
-        KB_CUDA(cudaFuncSetAttribute(k_dgemm<TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        KB_CUDA(cudaFuncSetAttribute(k_dgemm<CF, TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         configured = true;
     }
-    dim3 grid((unsigned)cdiv(n, BN), (unsigned)cdiv(m, BM), (unsigned)(nbatch * splits));
+    dim3 grid((unsigned)cdiv(n, CF::BN), (unsigned)cdiv(m, CF::BM), (unsigned)(nbatch * splits));
     const double nb = (double)nbatch, ns = (double)nseg;
     ProfScope ps(st, PROF_DGEMM, 8.0 * nb * (ns * ((double)m * k + (double)k * n) + (double)m * n),
                  2.0 * m * n * (double)k * nb * ns);
     if (splits == 1) {
-        k_dgemm<TA, TB, V16><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C,
-                                                          ldc, sc_b, nseg, beta, 1, 0);
+        k_dgemm<CF, TA, TB, V16><<<grid, CF::THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
+                                                                  C, ldc, sc_b, nseg, beta, 1, 0);
     } else {
-        k_dgemm<TA, TB, V16><<<grid, THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
-                                                          part, ldc, sc_b, nseg, 0.0, splits, split_stride);
+        k_dgemm<CF, TA, TB, V16><<<grid, CF::THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
+                                                                  part, ldc, sc_b, nseg, 0.0, splits, split_stride);
         KB_LAUNCH_CHECK();
         const int64_t total = (int64_t)m * n * nbatch;
         k_split_reduce<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(
@@ -258,39 +271,37 @@ static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int6
     KB_LAUNCH_CHECK();
 }
 
-// Number of K splits so that the grid fills >= 2 waves of 2 CTAs/SM.
-int dgemm_splits(int m, int n, int k, int nbatch, int nseg) {
-    using namespace g64;
-    const int64_t tiles = cdiv(n, BN) * cdiv(m, BM) * (int64_t)nbatch;
-    const int64_t ktot = cdiv(k, BK) * (int64_t)nseg;
+// Number of K splits so that the grid fills >= 2 waves.
+template <class CF>
+static int dgemm_splits(int m, int n, int k, int nbatch, int nseg) {
+    const int64_t tiles = cdiv(n, CF::BN) * cdiv(m, CF::BM) * (int64_t)nbatch;
+    const int64_t ktot = cdiv(k, CF::BK) * (int64_t)nseg;
     int s = 1;
-    while (tiles * s < 4 * kSMs && ktot / (s * 2) >= 8) s *= 2;
+    while (tiles * s < 2 * CF::MINB * kSMs && ktot / (s * 2) >= 8) s *= 2;
     return s;
 }
 
-void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
-           int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
-           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
-           double* part, int64_t part_doubles) {
-    KB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && nbatch >= 1 && nseg >= 1, "dgemm: bad sizes");
-    if (m == 0 || n == 0) return;
-    int splits = dgemm_splits(m, n, k, nbatch, nseg);
-    // partials use C's layout at split_stride apart
-    const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;
+template <class CF>
+static void dgemm_cfg(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
+                      int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
+                      int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
+                      double* part, int64_t part_doubles) {
+    int splits = dgemm_splits<CF>(m, n, k, nbatch, nseg);
+    const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;   // partials use C's layout
     if (part == nullptr || (int64_t)splits * span > part_doubles) splits = 1;
     KB_REQUIRE(nbatch * splits <= 65535, "dgemm: too many batches (%d)", nbatch);
     auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     const bool v16 = al16(A) && al16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (sa_b % 2 == 0) &&
                      (sa_s % 2 == 0) && (sb_b % 2 == 0) && (sb_s % 2 == 0) && (m % 2 == 0) &&
                      (n % 2 == 0) && (k % 2 == 0);
-#define KB_DG(TA_, TB_)                                                                              \
-    do {                                                                                             \
-        if (v16)                                                                                     \
-            launch_dgemm<TA_, TB_, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc,     \
-                                         sc_b, nbatch, nseg, beta, splits, part, span, st);          \
-        else                                                                                         \
-            launch_dgemm<TA_, TB_, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc,    \
-                                          sc_b, nbatch, nseg, beta, splits, part, span, st);         \
+#define KB_DG(TA_, TB_)                                                                                    \
+    do {                                                                                                   \
+        if (v16)                                                                                           \
+            launch_dgemm<CF, TA_, TB_, true>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, \
+                                             nbatch, nseg, beta, splits, part, span, st);                  \
+        else                                                                                               \
+            launch_dgemm<CF, TA_, TB_, false>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc,     \
+                                              sc_b, nbatch, nseg, beta, splits, part, span, st);          \
     } while (0)
     if (!ta && !tb) KB_DG(false, false);
     else if (!ta && tb) KB_DG(false, true);
@@ -299,4 +310,23 @@ void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, in
 #undef KB_DG
 }
 
+void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
+           int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
+           int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
+           double* part, int64_t part_doubles) {
+    KB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && nbatch >= 1 && nseg >= 1, "dgemm: bad sizes");
+    if (m == 0 || n == 0) return;
+    if (g_dgemm_cfg < 0) {
+        const char* e = std::getenv("KB_DGEMM_CFG");
+        g_dgemm_cfg = e ? std::atoi(e) : 1;   // Cfg1 measured best on B200 (tools/gemm_bench.py)
+    }
+    switch (g_dgemm_cfg) {
+        default: dgemm_cfg<Cfg1>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles); break;
+        case 2: dgemm_cfg<Cfg2>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles); break;
+        case 3: dgemm_cfg<Cfg3>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles); break;
+        case 0: dgemm_cfg<Cfg0>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles); break;
+    }
+}
+
 }  // namespace kb
+
