@@ -234,6 +234,61 @@ def run_ours(args, prob, rank, world, dist):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world / (float(e2e_t.item()) * 1e-3)
 
+    # ---- standalone R(A) product (kb_op_apply): 50 products per CUDA-graph replay
+    import ctypes as C
+
+    q_d = torch.randn(N, dtype=torch.float32, device=D.device())
+    y_d = torch.empty_like(q_d)
+    ops = blur.op_struct()
+    nb = C.c_size_t()
+    lib.kb_op_workspace_bytes(C.byref(ops), C.byref(nb))
+    mv_ws = torch.zeros(nb.value, dtype=torch.uint8, device=D.device())
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for tr_ in (0, 1):
+            lib.kb_op_apply(C.byref(ops), q_d.data_ptr(), y_d.data_ptr(), tr_, mv_ws.data_ptr(), nb.value,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.current_stream().wait_stream(side)
+    mv_graph = torch.cuda.CUDAGraph()
+    n_mv = 50
+    with torch.cuda.graph(mv_graph):
+        st_ptr = torch.cuda.current_stream().cuda_stream
+        for i_ in range(n_mv):
+            lib.kb_op_apply(C.byref(ops), q_d.data_ptr(), y_d.data_ptr(), i_ & 1, mv_ws.data_ptr(), nb.value, st_ptr)
+    mv_graph.replay()
+    torch.cuda.synchronize()
+    mv_e0, mv_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    mv_e0.record()
+    for _ in range(5):
+        mv_graph.replay()
+    mv_e1.record()
+    torch.cuda.synchronize()
+    mv_t = mv_e0.elapsed_time(mv_e1) * 1e-3 / (5 * n_mv)
+    # block product (16 vectors per launch: the RSVD block products)
+    nvb = 16
+    Xb = torch.randn(nvb, N, dtype=torch.float32, device=D.device())
+    Yb = torch.empty_like(Xb)
+    blk_graph = torch.cuda.CUDAGraph()
+    lib.kb_op_apply_block(C.byref(ops), Xb.data_ptr(), N, Yb.data_ptr(), N, nvb, 0, mv_ws.data_ptr(), nb.value,
+                          torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(blk_graph):
+        st_ptr = torch.cuda.current_stream().cuda_stream
+        for i_ in range(10):
+            lib.kb_op_apply_block(C.byref(ops), Xb.data_ptr(), N, Yb.data_ptr(), N, nvb, i_ & 1, mv_ws.data_ptr(),
+                                  nb.value, st_ptr)
+    blk_graph.replay()
+    torch.cuda.synchronize()
+    flush.zero_()
+    mv_e0.record()
+    for _ in range(5):
+        blk_graph.replay()
+    mv_e1.record()
+    torch.cuda.synchronize()
+    blk_t = mv_e0.elapsed_time(mv_e1) * 1e-3 / 50
+
     # ---- split Bregman on the fresh factors (same run): one outer sweep
     sb_cfg = kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=args.sb_outer,
                          cgls=kb.CglsConfig(i_max=100, tau=1e-4))
@@ -262,25 +317,23 @@ def run_ours(args, prob, rank, world, dist):
 
     hbm, hbm_src = peaks()
     # dominant kernel of the step: the class with the largest device time
-    names = {0: "reorth pass (k_reorth)", 1: "R(A) diagonal sums (k_diag_partial)",
-             2: "R(A) K-column sums (k_colsum)", 3: "fp64 GEMM (k_dgemm, DMMA)", 4: "CGLS/SB vector passes",
+    names = {0: "persistent eGKB (k_egkb_persistent)", 1: "R(A) diagonal sums (k_diag_seg)",
+             2: "R(A) K-column sums (k_colsum_seg)", 3: "fp64 GEMM (k_dgemm, DMMA)", 4: "CGLS/SB vector passes",
              5: "lift (k_lift)"}
     dom = max(range(6), key=lambda c: prof[c][0])
     d_ms, d_n, d_by, d_fl = prof[dom]
     achieved = (d_by / d_n) / ((d_ms / d_n) * 1e-3) / 1e9 if d_n else 0.0
     step_share = d_ms / prof_ms if prof_ms else 0.0
-    # R(A) product: one diag pass + one column pass per product
-    mv_ms = prof[1][0] + prof[2][0]
-    mv_n = prof[1][1]
-    mv_bytes_alg = 4.0 * (2 * N + (n + 1) ** 2)             # SURVEY §8d B_mv per product
-    mv_bytes_moved = (prof[1][2] + prof[2][2]) / max(mv_n, 1)
-    mv_t = (mv_ms / max(mv_n, 1)) * 1e-3
-    ra = {"products": mv_n, "us_per_product": mv_t * 1e6,
-          "GBps_survey_Bmv": mv_bytes_alg / mv_t / 1e9 if mv_t else None,
-          "GBps_bytes_moved": mv_bytes_moved / mv_t / 1e9 if mv_t else None,
-          "frac_survey_Bmv": mv_bytes_alg / mv_t / 1e9 / hbm if mv_t else None,
-          "note": "B_mv = 4(2N+(n+1)^2) per SURVEY §8d; the y write is fused into the reorth pass that "
-                  "consumes it, so bytes_moved = band read + K read"}
+    # standalone R(A) product (x read, y written, K read: SURVEY §8d B_mv)
+    mv_bytes_alg = 4.0 * (2 * N + (n + 1) ** 2)
+    ra = {"us_per_product": mv_t * 1e6, "GBps": mv_bytes_alg / mv_t / 1e9,
+          "frac": mv_bytes_alg / mv_t / 1e9 / hbm, "bytes_per_product": mv_bytes_alg,
+          "timing": f"{n_mv} products (alternating R x / R^T x) per CUDA-graph replay, 5 replays, CUDA events",
+          "kernel": "k_ra_block<float> (one cooperative launch: diagonal sums | K column sums | Toeplitz write)",
+          "block16": {"us_per_launch": blk_t * 1e6,
+                      "GBps": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9,
+                      "frac": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9 / hbm,
+                      "note": "16 vectors per launch (RSVD block product): K read once per block"}}
     cg = int(sum(sb_res.cgls_iters))
     sb = {"variant": "isotropic", "k_terms": op.k, "outer_iters": sb_res.outer_iters, "cgls_iters": cg,
           "ms": sb_ms, "outer_it_per_s": sb_res.outer_iters / (sb_ms * 1e-3),
@@ -299,7 +352,7 @@ def run_ours(args, prob, rank, world, dist):
                    "breakdown": tr.breakdown, "parallelism": f"replicas x{world}",
                    "l2": "flushed (512 MB write) before every timed step"},
         "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "launches": d_n,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(dom), "launches": d_n,
                      "share_of_step": step_share, "peak_src": hbm_src,
                      "timing": "CUDA events around every launch in an eager replay of the timed steps "
                                "(the timed steps themselves run as one CUDA graph per approximation)",
@@ -314,6 +367,17 @@ def run_ours(args, prob, rank, world, dist):
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(prob)
     print(json.dumps(line))
+
+
+def ncu_traffic(cls):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed `ncu --set full` capture (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(str(cls))
+    except Exception:
+        return None
 
 
 def cpu_baseline(prob):

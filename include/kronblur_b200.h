@@ -97,6 +97,12 @@ int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes);
 int kb_op_apply(const kb_operator* op, const void* x, void* y, int transpose,
                 void* ws, size_t ws_bytes, kb_stream_t stream);
 
+/* Block product Y = B X (or B^T X) for nv vectors (stride ldx / ldy): the
+ * RSVD block products (lowrank.py:363-367).  For R(A) one cooperative kernel
+ * per 16 vectors reads K once for the block. */
+int kb_op_apply_block(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                      int nv, int transpose, void* ws, size_t ws_bytes, kb_stream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* Tall-skinny building blocks (reorthogonalisation, lift)            */
 /* ------------------------------------------------------------------ */

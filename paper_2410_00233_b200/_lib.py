@@ -82,6 +82,7 @@ _SIGS = {
     "kb_prof_query": (C.c_int, [C.c_int, dp, C.POINTER(C.c_longlong), dp, dp]),
     "kb_op_workspace_bytes": (C.c_int, [P(KbOperator), P(SZ)]),
     "kb_op_apply": (C.c_int, [P(KbOperator), vp, vp, C.c_int, vp, SZ, vp]),
+    "kb_op_apply_block": (C.c_int, [P(KbOperator), vp, i64, vp, i64, C.c_int, C.c_int, vp, SZ, vp]),
     "kb_ts_dots": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, vp, vp, SZ, vp]),
     "kb_ts_axpy": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, vp, i64, vp]),
     "kb_ts_lift": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, C.c_int, vp, i64, i64, vp]),

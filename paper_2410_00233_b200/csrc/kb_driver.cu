@@ -207,6 +207,10 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
                      int* hdr, double* trace, double* scratch, void* raw, double tol, double** scales_out,
                      cudaStream_t s);
 void prof_set_last_bytes(double bytes);
+size_t ra_block_scratch_doubles(int lmax, int nv);
+bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv,
+                    int transpose, double* scratch, cudaStream_t st);
+constexpr int KB_BLOCK_MAXV = 16;
 
 struct EgkbWs {
     double* pk = nullptr;  // persistent-kernel scratch
@@ -694,6 +698,7 @@ extern "C" int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes) {
         Sizer s;
         op_plan_size(op, s);
         s.take<unsigned>(8);
+        if (op->kind == KB_OP_RA_ZERO) s.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
         *bytes = s.off;
     })
 }
@@ -705,10 +710,44 @@ extern "C" int kb_op_apply(const kb_operator* op, const void* x, void* y, int tr
         KB_REQUIRE(x && y, "null argument");
         Arena a(ws, ws_bytes);
         OpPlan p = op_plan_make(op, a);
+        (void)a.take<unsigned>(8);
         cudaStream_t s = as_stream(stream);
+        if (op->kind == KB_OP_RA_ZERO) {
+            double* scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+            if (ra_block_apply(op, x, op->cols, y, op->rows, 1, transpose, scr, s)) return KB_OK;
+        }
         KB_CUDA(cudaMemsetAsync(p.counters, 0, sizeof(unsigned) * p.n_counters, s));
         Src src = op_source(p, VecRef::at(x), transpose, s);
         src_write(op->dtype, src, y, transpose ? op->cols : op->rows, s);
+    })
+}
+
+extern "C" int kb_op_apply_block(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                                 int nv, int transpose, void* ws, size_t ws_bytes, kb_stream_t stream) {
+    KB_GUARD({
+        validate_op(op);
+        KB_REQUIRE(X && Y && nv >= 0, "bad arguments");
+        cudaStream_t s = as_stream(stream);
+        const size_t esz = op->dtype == KB_F32 ? 4 : 8;
+        const int64_t in_len = transpose ? op->rows : op->cols, out_len = transpose ? op->cols : op->rows;
+        KB_REQUIRE(ldx >= in_len && ldy >= out_len, "leading dimensions too small");
+        Arena a(ws, ws_bytes);
+        OpPlan p = op_plan_make(op, a);
+        (void)a.take<unsigned>(8);
+        double* scr = nullptr;
+        if (op->kind == KB_OP_RA_ZERO)
+            scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+        for (int v0 = 0; v0 < nv; v0 += KB_BLOCK_MAXV) {
+            const int cnt = std::min(KB_BLOCK_MAXV, nv - v0);
+            const char* xs = static_cast<const char*>(X) + (size_t)v0 * ldx * esz;
+            char* ys = static_cast<char*>(Y) + (size_t)v0 * ldy * esz;
+            if (scr && ra_block_apply(op, xs, ldx, ys, ldy, cnt, transpose, scr, s)) continue;
+            KB_CUDA(cudaMemsetAsync(p.counters, 0, sizeof(unsigned) * p.n_counters, s));
+            for (int v = 0; v < cnt; ++v) {
+                Src src = op_source(p, VecRef::at(xs + (size_t)v * ldx * esz), transpose, s);
+                src_write(op->dtype, src, ys + (size_t)v * ldy * esz, out_len, s);
+            }
+        }
     })
 }
 

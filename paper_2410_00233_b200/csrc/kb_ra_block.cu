@@ -1,0 +1,239 @@
+// One-launch R(A) product for a block of vectors (cooperative, sm_100a).
+//
+//   Y = R(A) X  (or R(A)^T X),  X, Y: nv vectors of length n^2
+//
+// R(A) = W_c K^T W_r^T: per vector, diagonal sums of the
+// n x n image (w), a small GEMV with K (z = K^T w), and a Toeplitz broadcast
+// y[a*n+b] = z[b - a + c].  The three steps are phases of ONE cooperative
+// kernel separated by grid barriers; K is read once for the whole block (the
+// RSVD block products, lowrank.py:361-369, and the standalone product
+// lowrank.py:211,238,250 with nv = 1).  Fixed-order reductions throughout.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "kb_ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kb {
+
+constexpr int RB_THREADS = 256;
+constexpr int RB_SEGS = 8;
+constexpr int RB_MAXV = 16;
+
+struct RaBlockParams {
+    const void* X;
+    void* Y;
+    int64_t ldx, ldy;
+    int nv;
+    const void* M;     // Li x Lo row-major (K for the forward product, K^T for the transpose)
+    int n, ci, Li, co, Lo, lmax;
+    double* diag_part; // [RB_SEGS][nv][lmax]
+    double* w;         // [nv][lmax]
+    double* col_part;  // [RB_SEGS][nv][lmax]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    double* zs = sm;                       // [lmax]
+    double* acc = sm + P.lmax;             // [8][33 * RB_MAXV]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = P.n, nv = P.nv, L = P.lmax;
+    const int nblk = gridDim.x;
+    const T* X = static_cast<const T*>(P.X);
+    T* Y = static_cast<T*>(P.Y);
+    const T* M = static_cast<const T*>(P.M);
+
+    // ---- phase 1: diagonal-sum partials, items = (32-diagonal chunk, row segment)
+    {
+        const int chunks = (P.Li + 31) / 32;
+        const int items = chunks * RB_SEGS;
+        for (int it = blockIdx.x; it < items; it += nblk) {
+            const int c = it % chunks, seg = it / chunks;
+            const int u = c * 32 + lane;
+            const int d = u - P.ci;
+            const int s0 = (int)((int64_t)n * seg / RB_SEGS), s1 = (int)((int64_t)n * (seg + 1) / RB_SEGS);
+            const int lo = max(s0, -d), hi = min(s1, n - d);
+            const int64_t step = 8 * (int64_t)(n + 1);
+            for (int v = 0; v < nv; ++v) {
+                double a = 0.0;
+                if (u < P.Li) {
+                    int r = lo + warp;
+                    const T* p = X + (int64_t)v * P.ldx + (int64_t)r * n + (r + d);
+                    for (; r + 56 < hi; r += 64, p += 8 * step) {
+                        T q[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) q[k] = __ldg(p + k * step);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) a += (double)q[k];
+                    }
+                    for (; r < hi; r += 8, p += step) a += (double)__ldg(p);
+                }
+                acc[warp * 33 + lane] = a;
+                __syncthreads();
+                if (warp == 0 && u < P.Li) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
+                    P.diag_part[((int64_t)seg * nv + v) * L + u] = t;
+                }
+                __syncthreads();
+            }
+        }
+    }
+    grid.sync();
+    // ---- phase 1b (nv > 1): w[v][u] = sum_seg diag_part[seg][v][u], fixed order
+    if (nv > 1) {
+        for (int64_t e = blockIdx.x * (int64_t)RB_THREADS + tid; e < (int64_t)nv * P.Li;
+             e += (int64_t)nblk * RB_THREADS) {
+            const int v = (int)(e / P.Li), u = (int)(e - (int64_t)v * P.Li);
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < RB_SEGS; ++q) t += __ldcg(P.diag_part + ((int64_t)q * nv + v) * L + u);
+            P.w[(int64_t)v * L + u] = t;
+        }
+        grid.sync();
+    }
+    // ---- phase 2: K column-sum partials, items = (32-column chunk, row segment); K read once
+    {
+        const int chunks = (P.Lo + 31) / 32;
+        const int items = chunks * RB_SEGS;
+        for (int it = blockIdx.x; it < items; it += nblk) {
+            const int cc = it % chunks, seg = it / chunks;
+            const int c = cc * 32 + lane;
+            const int r0 = (int)((int64_t)P.Li * seg / RB_SEGS), r1 = (int)((int64_t)P.Li * (seg + 1) / RB_SEGS);
+            double a[RB_MAXV];
+#pragma unroll
+            for (int v = 0; v < RB_MAXV; ++v) a[v] = 0.0;
+            for (int r = r0 + warp; r < r1; r += 8) {
+                const double mk = (c < P.Lo) ? (double)__ldg(M + (int64_t)r * P.Lo + c) : 0.0;
+                if (nv == 1) {
+                    double w = 0.0;
+#pragma unroll
+                    for (int q = 0; q < RB_SEGS; ++q) w += __ldcg(P.diag_part + (int64_t)q * L + r);
+                    a[0] += mk * w;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < RB_MAXV; ++v)
+                        if (v < nv) a[v] += mk * __ldcg(P.w + (int64_t)v * L + r);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < RB_MAXV; ++v)
+                if (v < nv) acc[warp * (33 * RB_MAXV) + v * 33 + lane] = a[v];
+            __syncthreads();
+            for (int j = tid; j < nv * 32; j += RB_THREADS) {
+                const int v = j >> 5, l = j & 31, col = cc * 32 + l;
+                if (col < P.Lo) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) t += acc[w * (33 * RB_MAXV) + v * 33 + l];
+                    P.col_part[((int64_t)seg * nv + v) * L + col] = t;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    grid.sync();
+    // ---- phase 3: z_v into shared memory, Toeplitz broadcast into y_v
+    const int64_t N = (int64_t)n * n;
+    for (int v = 0; v < nv; ++v) {
+        for (int c = tid; c < P.Lo; c += RB_THREADS) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < RB_SEGS; ++q) t += __ldcg(P.col_part + ((int64_t)q * nv + v) * L + c);
+            zs[c] = t;
+        }
+        __syncthreads();
+        T* y = Y + (int64_t)v * P.ldy;
+        for (int64_t e0 = (blockIdx.x * (int64_t)RB_THREADS + tid) * 4; e0 < N;
+             e0 += (int64_t)nblk * RB_THREADS * 4) {
+            T o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t e = e0 + q;
+                const unsigned a = (unsigned)e / (unsigned)n;
+                const int u = (int)((unsigned)e - a * (unsigned)n) - (int)a + P.co;
+                o[q] = (e < N && u >= 0 && u < P.Lo) ? (T)zs[u] : T(0);
+            }
+            if (e0 + 4 <= N && ((P.ldy & 3) == 0)) {
+                if constexpr (sizeof(T) == 4) {
+                    *reinterpret_cast<float4*>(y + e0) = make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+                    *reinterpret_cast<double2*>(y + e0) = make_double2(o[0], o[1]);
+                    *reinterpret_cast<double2*>(y + e0 + 2) = make_double2(o[2], o[3]);
+                }
+            } else {
+                for (int q = 0; q < 4; ++q)
+                    if (e0 + q < N) y[e0 + q] = o[q];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t ra_block_scratch_doubles(int lmax, int nv) {
+    return (size_t)(2 * RB_SEGS + 1) * nv * lmax + 64;
+}
+
+// Returns false if the cooperative launch is not possible (caller falls back).
+bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv,
+                    int transpose, double* scratch, cudaStream_t st) {
+    if (op->kind != KB_OP_RA_ZERO || nv < 1 || nv > RB_MAXV) return false;
+    if (((uintptr_t)Y & 15) != 0) return false;
+    RaBlockParams P{};
+    const int cu = op->kh / 2, cv = op->kw / 2;
+    P.X = X;
+    P.Y = Y;
+    P.ldx = ldx;
+    P.ldy = ldy;
+    P.nv = nv;
+    P.n = op->side;
+    if (!transpose) { P.ci = cu; P.Li = op->kh; P.co = cv; P.Lo = op->kw; P.M = op->k; }
+    else { P.ci = cv; P.Li = op->kw; P.co = cu; P.Lo = op->kh; P.M = op->kt; }
+    P.lmax = std::max(op->kh, op->kw);
+    P.diag_part = scratch;
+    P.w = scratch + (size_t)RB_SEGS * nv * P.lmax;
+    P.col_part = P.w + (size_t)nv * P.lmax;
+    const size_t smem = sizeof(double) * ((size_t)P.lmax + 8 * 33 * RB_MAXV);
+    const int64_t N = (int64_t)P.n * P.n;
+    const double bytes = (double)(op->dtype == KB_F32 ? 4 : 8) * (2.0 * nv * N + (double)op->kh * op->kw);
+    ProfScope ps(st, PROF_RA_DIAG, bytes);
+    cudaLaunchConfig_t lc = {};
+    lc.blockDim = dim3(RB_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int per_sm = 0;
+    if (op->dtype == KB_F32) {
+        static bool cfg = false;
+        if (!cfg) {
+            KB_CUDA(cudaFuncSetAttribute(k_ra_block<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<float>, RB_THREADS, smem));
+        if (per_sm < 1) return false;
+        lc.gridDim = dim3(kSMs * std::min(per_sm, 2));
+        KB_CUDA(cudaLaunchKernelEx(&lc, k_ra_block<float>, P));
+    } else {
+        static bool cfg = false;
+        if (!cfg) {
+            KB_CUDA(cudaFuncSetAttribute(k_ra_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<double>, RB_THREADS, smem));
+        if (per_sm < 1) return false;
+        lc.gridDim = dim3(kSMs * std::min(per_sm, 2));
+        KB_CUDA(cudaLaunchKernelEx(&lc, k_ra_block<double>, P));
+    }
+    return true;
+}
+
+}  // namespace kb

@@ -177,13 +177,18 @@ class _EngineOp:
         return out
 
     def apply_block(self, X, transpose: int):
-        """Rows of X are vectors; returns rows B x_i (or B^T x_i)."""
+        """Rows of X are vectors; returns rows B x_i (or B^T x_i) (kb_op_apply_block)."""
         from . import device as D
 
         rows_out = self.shape[1] if transpose else self.shape[0]
+        X = X.contiguous()
         out = D.empty((X.shape[0], rows_out), self.dtype)
-        for i in range(X.shape[0]):
-            self.apply(X[i], transpose, out[i])
+        lib = _lib.load()
+        nb = C.c_size_t()
+        _lib.check(lib.kb_op_workspace_bytes(C.byref(self.struct), C.byref(nb)))
+        ws, wsb = D.WORKSPACE.get(nb.value)
+        _lib.check(lib.kb_op_apply_block(C.byref(self.struct), X.data_ptr(), X.shape[1], out.data_ptr(), rows_out,
+                                         X.shape[0], transpose, ws, wsb, D.stream_ptr()), "block apply")
         return out
 
 
