@@ -130,7 +130,7 @@ struct PkHalf {
 // One half step.  Returns t = |v1| (identical in every CTA).
 template <typename T, int VEC, int MAXG>
 __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid) {
-    constexpr int GC = 4;   // element groups processed together (loads in flight per basis vector)
+    constexpr int GC = 2;   // element groups processed together (loads in flight per basis vector)
     static_assert(MAXG % GC == 0, "MAXG must be a multiple of GC");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
@@ -191,13 +191,25 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
             const int cc = it % chunks, seg = it / chunks;
             const int c = cc * 32 + lane;
             const int r0 = (int)((int64_t)Li * seg / PK_SEGS), r1 = (int)((int64_t)Li * (seg + 1) / PK_SEGS);
-            double a = 0.0;
-            for (int r = r0 + warp; r < r1; r += 8) {
-                double w = 0.0;
+            // stage w[r] = sum_s diag_part[s][r] for this segment's rows in smem (zs is free here)
+            for (int j = tid; j < r1 - r0; j += PK_THREADS) {
+                double t = 0.0;
 #pragma unroll
-                for (int q = 0; q < PK_SEGS; ++q) w += __ldcg(P.diag_part + (int64_t)q * P.lmax + r);
-                if (c < Lo) a += (double)__ldg(M + (int64_t)r * Lo + c) * w;
+                for (int q = 0; q < PK_SEGS; ++q) t += __ldcg(P.diag_part + (int64_t)q * P.lmax + r0 + j);
+                zs[j] = t;
             }
+            __syncthreads();
+            double a = 0.0;
+            int r = r0 + warp;
+            for (; r + 56 < r1; r += 64) {            // 8 independent K loads in flight
+                double mk[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mk[k] = (c < Lo) ? (double)__ldg(M + (int64_t)(r + 8 * k) * Lo + c) : 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a += mk[k] * zs[r + 8 * k - r0];
+            }
+            for (; r < r1; r += 8)
+                if (c < Lo) a += (double)__ldg(M + (int64_t)r * Lo + c) * zs[r - r0];
             acc[warp * 33 + lane] = a;
             __syncthreads();
             if (warp == 0 && c < Lo) {

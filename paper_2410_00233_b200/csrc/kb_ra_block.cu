@@ -11,6 +11,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kb_ops.cuh"
 
@@ -32,20 +34,31 @@ struct RaBlockParams {
     double* diag_part; // [RB_SEGS][nv][lmax]
     double* w;         // [nv][lmax]
     double* col_part;  // [RB_SEGS][nv][lmax]
+    unsigned long long* dbg;   // optional phase timestamps (KB_PK_TRACE)
+    int zlen;
 };
+
+__device__ __forceinline__ void rb_mark(const RaBlockParams& P, int slot) {
+    if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.dbg[slot] = t;
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
-    double* zs = sm;                       // [lmax]
-    double* acc = sm + P.lmax;             // [8][33 * RB_MAXV]
+    double* zs = sm;                       // [zlen]: z (phase 3) / staged w (phase 2)
+    double* acc = sm + P.zlen;             // [8][33 * RB_MAXV]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n, nv = P.nv, L = P.lmax;
     const int nblk = gridDim.x;
     const T* X = static_cast<const T*>(P.X);
     T* Y = static_cast<T*>(P.Y);
     const T* M = static_cast<const T*>(P.M);
+    rb_mark(P, 0);
 
     // ---- phase 1: diagonal-sum partials, items = (32-diagonal chunk, row segment)
     {
@@ -85,6 +98,7 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
         }
     }
     grid.sync();
+    rb_mark(P, 1);
     // ---- phase 1b (nv > 1): w[v][u] = sum_seg diag_part[seg][v][u], fixed order
     if (nv > 1) {
         for (int64_t e = blockIdx.x * (int64_t)RB_THREADS + tid; e < (int64_t)nv * P.Li;
@@ -105,21 +119,42 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
             const int cc = it % chunks, seg = it / chunks;
             const int c = cc * 32 + lane;
             const int r0 = (int)((int64_t)P.Li * seg / RB_SEGS), r1 = (int)((int64_t)P.Li * (seg + 1) / RB_SEGS);
+            // stage w (fixed-order sum of the segment partials) for these rows in smem
+            double* ws = zs;   // [(r1 - r0) * nv], reuses the z buffer (phase 3 runs after a barrier)
+            for (int j = tid; j < (r1 - r0) * nv; j += RB_THREADS) {
+                const int rr = j / nv, v = j - rr * nv;
+                double t = 0.0;
+                if (nv == 1) {
+#pragma unroll
+                    for (int q = 0; q < RB_SEGS; ++q) t += __ldcg(P.diag_part + (int64_t)q * L + r0 + rr);
+                } else {
+                    t = __ldcg(P.w + (int64_t)v * L + r0 + rr);
+                }
+                ws[j] = t;
+            }
+            __syncthreads();
             double a[RB_MAXV];
 #pragma unroll
             for (int v = 0; v < RB_MAXV; ++v) a[v] = 0.0;
-            for (int r = r0 + warp; r < r1; r += 8) {
-                const double mk = (c < P.Lo) ? (double)__ldg(M + (int64_t)r * P.Lo + c) : 0.0;
-                if (nv == 1) {
-                    double w = 0.0;
+            int r = r0 + warp;
+            for (; r + 56 < r1; r += 64) {            // 8 independent K loads in flight
+                double mk[8];
 #pragma unroll
-                    for (int q = 0; q < RB_SEGS; ++q) w += __ldcg(P.diag_part + (int64_t)q * L + r);
-                    a[0] += mk * w;
-                } else {
+                for (int k = 0; k < 8; ++k) mk[k] = (c < P.Lo) ? (double)__ldg(M + (int64_t)(r + 8 * k) * P.Lo + c) : 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double* wr = ws + (r + 8 * k - r0) * nv;
 #pragma unroll
                     for (int v = 0; v < RB_MAXV; ++v)
-                        if (v < nv) a[v] += mk * __ldcg(P.w + (int64_t)v * L + r);
+                        if (v < nv) a[v] += mk[k] * wr[v];
                 }
+            }
+            for (; r < r1; r += 8) {
+                const double mk = (c < P.Lo) ? (double)__ldg(M + (int64_t)r * P.Lo + c) : 0.0;
+                const double* wr = ws + (r - r0) * nv;
+#pragma unroll
+                for (int v = 0; v < RB_MAXV; ++v)
+                    if (v < nv) a[v] += mk * wr[v];
             }
 #pragma unroll
             for (int v = 0; v < RB_MAXV; ++v)
@@ -138,6 +173,7 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
         }
     }
     grid.sync();
+    rb_mark(P, 2);
     // ---- phase 3: z_v into shared memory, Toeplitz broadcast into y_v
     const int64_t N = (int64_t)n * n;
     for (int v = 0; v < nv; ++v) {
@@ -173,6 +209,7 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
         }
         __syncthreads();
     }
+    rb_mark(P, 3);
 }
 
 size_t ra_block_scratch_doubles(int lmax, int nv) {
@@ -198,7 +235,24 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     P.diag_part = scratch;
     P.w = scratch + (size_t)RB_SEGS * nv * P.lmax;
     P.col_part = P.w + (size_t)nv * P.lmax;
-    const size_t smem = sizeof(double) * ((size_t)P.lmax + 8 * 33 * RB_MAXV);
+    P.zlen = std::max(P.lmax, (int)((P.Li + RB_SEGS - 1) / RB_SEGS + 1) * nv);
+    const size_t smem = sizeof(double) * ((size_t)P.zlen + 8 * 33 * RB_MAXV);
+    KB_REQUIRE(smem <= 100 * 1024, "R(A) block product: PSF support too large");
+    static unsigned long long* dbg = nullptr;
+    const bool trace = std::getenv("KB_PK_TRACE") != nullptr;
+    if (trace && !dbg) KB_CUDA(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
+    P.dbg = trace ? dbg : nullptr;
+    struct Dump {
+        unsigned long long* d; cudaStream_t s;
+        ~Dump() {
+            if (!d) return;
+            unsigned long long t[4];
+            cudaMemcpyAsync(t, d, sizeof(t), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "[kb] ra_block phases (us): %.2f %.2f %.2f\n", (t[1] - t[0]) * 1e-3,
+                    (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3);
+        }
+    } dump{trace ? dbg : nullptr, st};
     const int64_t N = (int64_t)P.n * P.n;
     const double bytes = (double)(op->dtype == KB_F32 ? 4 : 8) * (2.0 * nv * N + (double)op->kh * op->kw);
     ProfScope ps(st, PROF_RA_DIAG, bytes);
@@ -215,7 +269,7 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     if (op->dtype == KB_F32) {
         static bool cfg = false;
         if (!cfg) {
-            KB_CUDA(cudaFuncSetAttribute(k_ra_block<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            KB_CUDA(cudaFuncSetAttribute(k_ra_block<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
             cfg = true;
         }
         KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<float>, RB_THREADS, smem));
@@ -225,7 +279,7 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     } else {
         static bool cfg = false;
         if (!cfg) {
-            KB_CUDA(cudaFuncSetAttribute(k_ra_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            KB_CUDA(cudaFuncSetAttribute(k_ra_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
             cfg = true;
         }
         KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<double>, RB_THREADS, smem));
