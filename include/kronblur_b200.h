@@ -202,6 +202,12 @@ int kb_dgemm(int trans_a, int trans_b, int m, int n, int k,
 /* ------------------------------------------------------------------ */
 #define KB_FWD_DENSE 0
 #define KB_FWD_KRON 1
+/* Sum-allreduce hook for term-sharded operators: when set, every
+ * product of the forward operator is a rank-local partial sum (this rank's
+ * Kronecker terms) and the hook is called on the n-vector result, stream-
+ * ordered, before anything consumes it.  The host supplies it (NCCL over
+ * NVLink through torch.distributed on a B200 box, gloo in CPU tests). */
+typedef void (*kb_allreduce_fn)(void* ctx, double* buf, int64_t count, kb_stream_t stream);
 typedef struct {
     int kind;            /* KB_FWD_DENSE / KB_FWD_KRON                       */
     int64_t m, n;        /* forward operator shape                           */
@@ -211,6 +217,8 @@ typedef struct {
     int augmented;       /* 1: [A; lam_x Dx; lam_y Dy] (regularizers.py:65)   */
     int side;            /* image side for the difference maps               */
     double lam_x, lam_y;
+    kb_allreduce_fn allreduce;  /* NULL: the operator is complete on this rank  */
+    void* allreduce_ctx;
 } kb_forward;
 
 int kb_forward_workspace_bytes(const kb_forward* fw, size_t* bytes);

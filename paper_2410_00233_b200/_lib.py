@@ -56,9 +56,13 @@ class KbKron(C.Structure):
                 ("f", vp), ("g", vp)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(None, vp, dp, i64, vp)
+
+
 class KbForward(C.Structure):
     _fields_ = [("kind", C.c_int), ("m", i64), ("n", i64), ("a", vp), ("lda", i64), ("kron", KbKron),
-                ("augmented", C.c_int), ("side", C.c_int), ("lam_x", C.c_double), ("lam_y", C.c_double)]
+                ("augmented", C.c_int), ("side", C.c_int), ("lam_x", C.c_double), ("lam_y", C.c_double),
+                ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", vp)]
 
 
 class KbCglsState(C.Structure):

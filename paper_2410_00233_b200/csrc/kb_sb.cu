@@ -364,6 +364,8 @@ static void forward_top(const kb_forward* fw, const double* x, double* y, int tr
         kron_apply(&fw->kron, x, y, transpose, ws.tmp, st);
     else
         dense_gemv64(fw->a, fw->lda, fw->m, fw->n, x, y, transpose, ws.part, ws.mr.counter + 8, st);
+    if (fw->allreduce)   // term-sharded operator: sum the rank-local partial products
+        fw->allreduce(fw->allreduce_ctx, y, transpose ? fw->n : fw->m, reinterpret_cast<kb_stream_t>(st));
 }
 
 static void forward_apply(const kb_forward* fw, const double* x, double* y, int transpose,

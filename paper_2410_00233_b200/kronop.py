@@ -45,8 +45,16 @@ def _forward_apply(fw, x, transpose: int, shape):
     nb = C.c_size_t()
     _lib.check(lib.kb_forward_workspace_bytes(C.byref(fw), C.byref(nb)))
     ws, wsb = D.WORKSPACE.get(nb.value)
-    _lib.check(lib.kb_forward_apply(C.byref(fw), xd.data_ptr(), y.data_ptr(), transpose, ws, wsb,
-                                    D.stream_ptr()), "operator apply")
+    sharded = bool(fw.allreduce)
+    if sharded:   # the allreduce hook maps the raw output pointer back to this tensor
+        from .parallel import REGISTRY
+        REGISTRY.add(y)
+    try:
+        _lib.check(lib.kb_forward_apply(C.byref(fw), xd.data_ptr(), y.data_ptr(), transpose, ws, wsb,
+                                        D.stream_ptr()), "operator apply")
+    finally:
+        if sharded:
+            REGISTRY.remove(y)
     return D.to_host(y) if host else y
 
 

@@ -365,3 +365,32 @@ class TestEstimators:
         est = kb.KroneckerApproximator(engine="rsvd", k=2, p=1, q=1).fit(a)   # rank R(A) = rank K = 3
         assert est.k_ == 2
         assert est.transform(np.ones((2, 64))).shape == (2, 64)
+
+
+class TestParallel:
+    def test_term_sharded_operator_world1_nccl(self, kb):
+        """The allreduce hook path (NCCL, world size 1) gives the same SB result."""
+        import torch.distributed as dist
+
+        from paper_2410_00233_b200.parallel import ShardedKroneckerSum
+
+        g = load_golden("sb_kat")
+        side = 32
+        op = kb.KroneckerSum(list(g["n64_ax"]), list(g["n64_ay"]), kb.BlockScheme.square_image(side))
+        created = False
+        if not dist.is_initialized():
+            store = dist.HashStore()
+            dist.init_process_group("nccl", store=store, rank=0, world_size=1)
+            created = True
+        try:
+            sop = ShardedKroneckerSum(op)
+            assert sop.k == op.k
+            cfg = kb.SbConfig(lam=0.115, beta=0.0066, tau=0.0, l_max=3, cgls=kb.CglsConfig(i_max=10, tau=0.0))
+            a = kb.sb_run(op, g["n64_b"], cfg)
+            b = kb.sb_run(sop, g["n64_b"], cfg)
+            np.testing.assert_array_equal(a.x, b.x)
+            x = np.random.default_rng(0).standard_normal(side * side)
+            np.testing.assert_array_equal(sop.apply(x), op.apply(x))
+        finally:
+            if created:
+                dist.destroy_process_group()
