@@ -277,7 +277,8 @@ static int dgemm_splits(int m, int n, int k, int nbatch, int nseg) {
     const int64_t tiles = cdiv(n, CF::BN) * cdiv(m, CF::BM) * (int64_t)nbatch;
     const int64_t ktot = cdiv(k, CF::BK) * (int64_t)nseg;
     int s = 1;
-    while (tiles * s < 2 * CF::MINB * kSMs && ktot / (s * 2) >= 8) s *= 2;
+    const int64_t min_tiles_per_split = tiles >= kSMs ? 8 : 1;   // small grids: split down to 1 k-tile
+    while (tiles * s < 2 * CF::MINB * kSMs && ktot / (s * 2) >= min_tiles_per_split) s *= 2;
     return s;
 }
 
@@ -288,7 +289,8 @@ static void dgemm_cfg(int ta, int tb, int m, int n, int k, const double* A, int6
                       double* part, int64_t part_doubles) {
     int splits = dgemm_splits<CF>(m, n, k, nbatch, nseg);
     const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;   // partials use C's layout
-    if (part == nullptr || (int64_t)splits * span > part_doubles) splits = 1;
+    if (part == nullptr) splits = 1;
+    while (splits > 1 && (int64_t)splits * span > part_doubles) splits /= 2;
     KB_REQUIRE(nbatch * splits <= 65535, "dgemm: too many batches (%d)", nbatch);
     auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     const bool v16 = al16(A) && al16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (sa_b % 2 == 0) &&

@@ -13,6 +13,8 @@
 // x + mu*w is two rounded ops, as numpy does).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "kb_common.cuh"
@@ -313,7 +315,7 @@ static void map_reduce(int64_t len, const F& f, const MR& mr, double* out, cudaS
 
 // ---- Kronecker apply (two DMMA GEMMs) ----
 // intermediate P/Q (k blocks) + split-K partials of the reduced stage (8 x output)
-constexpr int KRON_SPLIT_MAX = 8;
+constexpr int KRON_SPLIT_MAX = 32;
 size_t kron_ws_doubles(const kb_kron* kr) {
     const int64_t a = (int64_t)kr->n1 * kr->m2, b = (int64_t)kr->m1 * kr->n2;
     const int64_t out = std::max((int64_t)kr->m1 * kr->m2, (int64_t)kr->n1 * kr->n2);
@@ -430,7 +432,11 @@ struct CglsWs {
     FwdWs f;
     double *r, *z, *w, *fv, *scal;
     double* scal_host;   // pinned
+    int* ctl;            // device control block
+    double *rc, *res;    // device histories
+    int i_cap;
 };
+constexpr int CGLS_ICAP = 4096;   // maximum i_max per call
 
 static void cgls_ws_size(const kb_forward* fw, Sizer& s) {
     fwd_ws_size(fw, s);
@@ -440,6 +446,9 @@ static void cgls_ws_size(const kb_forward* fw, Sizer& s) {
     s.take<double>(N);
     s.take<double>(N);
     s.take<double>(S_TOTAL);
+    s.take<int>(16);
+    s.take<double>(CGLS_ICAP + 2);
+    s.take<double>(CGLS_ICAP + 2);
 }
 
 static CglsWs cgls_ws_make(const kb_forward* fw, Arena& a) {
@@ -452,74 +461,251 @@ static CglsWs cgls_ws_make(const kb_forward* fw, Arena& a) {
     w.fv = a.take<double>(N);
     w.scal = a.take<double>(S_TOTAL);
     w.scal_host = nullptr;
+    w.ctl = a.take<int>(16);
+    w.rc = a.take<double>(CGLS_ICAP + 2);
+    w.res = a.take<double>(CGLS_ICAP + 2);
+    w.i_cap = CGLS_ICAP;
     return w;
 }
 
-struct PinnedScalars {
+struct PinnedScalars {   // per-thread pinned mailbox, allocated once
     double* p = nullptr;
-    PinnedScalars() { KB_CUDA(cudaMallocHost(&p, sizeof(double) * S_TOTAL)); }
-    ~PinnedScalars() { if (p) cudaFreeHost(p); }
+    PinnedScalars() {
+        static thread_local double* buf = nullptr;
+        if (!buf) KB_CUDA(cudaMallocHost(&buf, sizeof(double) * S_TOTAL));
+        p = buf;
+    }
 };
 
-// Runs CGLS; returns stop code.  x0 may alias x (warm start) or be null.
-static void cgls_core(const kb_forward* fw, const double* b, const double* x0, double* x,
-                      kb_cgls_state* st, CglsWs& w, double* hs, cudaStream_t s) {
+// ---- CGLS control on the device (graph while-loop / eager replay share it)
+enum { C_ITERS = 0, C_NRC, C_NRES, C_STOP, C_RUN, C_ERR, C_COUNT = 8 };
+struct CglsCtl {
+    int* h;                 // [C_COUNT]
+    double* rc;             // [i_max]
+    double* res;            // [i_max + 1]
+    const double* scal;
+    int i_max;
+    double tau;
+    cudaGraphConditionalHandle handle;
+    int use_cond;
+};
+
+__global__ void k_cgls_init_ctl(CglsCtl c) {
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < C_COUNT; ++i) c.h[i] = 0;
+    c.res[0] = sqrt(c.scal[S_RR]);
+    c.h[C_NRES] = 1;
+    c.h[C_STOP] = KB_CGLS_MAX_ITER;
+    c.h[C_RUN] = c.i_max >= 1;
+    if (c.use_cond) cudaGraphSetConditional(c.handle, c.h[C_RUN] ? 1u : 0u);
+}
+
+// cgls.py:90-114 stop logic, evaluated on the device after each iteration
+__global__ void k_cgls_control(CglsCtl c) {
+    if (threadIdx.x != 0) return;
+    int* h = c.h;
+    const int it = h[C_ITERS];
+    if (c.scal[S_STALL] != 0.0) {
+        h[C_STOP] = KB_CGLS_STALLED;
+        h[C_RUN] = 0;
+    } else if (!isfinite(c.scal[S_FF])) {
+        h[C_ERR] = 1;
+        h[C_RUN] = 0;
+    } else {
+        h[C_ITERS] = it + 1;
+        c.res[h[C_NRES]++] = sqrt(c.scal[S_RR]);
+        if (it >= 1) {
+            const double xn = c.scal[S_XN];
+            const double rc = xn > 0 ? c.scal[S_STEP] / xn : INFINITY;
+            c.rc[h[C_NRC]++] = rc;
+            if (rc < c.tau) {
+                h[C_STOP] = KB_CGLS_CONVERGED;
+                h[C_RUN] = 0;
+            }
+        }
+        if (h[C_ITERS] >= c.i_max) h[C_RUN] = 0;
+    }
+    if (c.use_cond) cudaGraphSetConditional(c.handle, h[C_RUN] ? 1u : 0u);
+}
+
+struct CglsPlan {
+    const kb_forward* fw;
+    const double* b;
+    const double* x0;
+    double* x;
+    CglsWs* w;
+    CglsCtl ctl;
+};
+
+static void cgls_enqueue_init(CglsPlan& P, cudaStream_t s) {
+    const kb_forward* fw = P.fw;
+    CglsWs& w = *P.w;
     const int64_t T = fwd_rows(fw), N = fw->n;
     const int64_t big = std::max(T, N);
-    // x, r
-    if (x0 == nullptr) {
-        map_reduce<0>(N, FZero{x, N}, w.f.mr, nullptr, s);
-        map_reduce<0>(T, FCopy{w.r, b, T}, w.f.mr, nullptr, s);
+    if (P.x0 == nullptr) {
+        map_reduce<0>(N, FZero{P.x, N}, w.f.mr, nullptr, s);
+        map_reduce<0>(T, FCopy{w.r, P.b, T}, w.f.mr, nullptr, s);
     } else {
-        if (x0 != x) map_reduce<0>(N, FCopy{x, x0, N}, w.f.mr, nullptr, s);
-        forward_apply(fw, x, w.r, 0, w.f, s);
-        map_reduce<0>(T, FSub{w.r, b, T}, w.f.mr, nullptr, s);
+        if (P.x0 != P.x) map_reduce<0>(N, FCopy{P.x, P.x0, N}, w.f.mr, nullptr, s);
+        forward_apply(fw, P.x, w.r, 0, w.f, s);
+        map_reduce<0>(T, FSub{w.r, P.b, T}, w.f.mr, nullptr, s);
     }
     forward_apply(fw, w.r, w.fv, 1, w.f, s);
     map_reduce<2>(big, FInit{w.w, w.fv, w.r, N, T}, w.f.mr, w.scal + S_RED, s, FInitPost{w.scal});
-    KB_CUDA(cudaMemcpyAsync(hs, w.scal, sizeof(double) * S_TOTAL, cudaMemcpyDeviceToHost, s));
-    KB_CUDA(cudaStreamSynchronize(s));
-    st->n_res = 0;
-    st->n_rc = 0;
-    if (st->resnorm_host) st->resnorm_host[st->n_res] = std::sqrt(hs[S_RR]);
-    st->n_res++;
-    st->iters = 0;
-    st->stop = KB_CGLS_MAX_ITER;
-    const int64_t P = fw->augmented ? (int64_t)fw->side * (fw->side - 1) : 0;
+    k_cgls_init_ctl<<<1, 32, 0, s>>>(P.ctl);
+    KB_LAUNCH_CHECK();
+}
+
+static void cgls_enqueue_body(CglsPlan& P, cudaStream_t s) {
+    const kb_forward* fw = P.fw;
+    CglsWs& w = *P.w;
+    const int64_t T = fwd_rows(fw), N = fw->n;
+    const int64_t big = std::max(T, N);
+    const int64_t P_ = fw->augmented ? (int64_t)fw->side * (fw->side - 1) : 0;
     const int aug = fw->augmented;
-    for (int it = 0; it < st->i_max; ++it) {
-        forward_top(fw, w.w, w.z, 0, w.f, s);
-        map_reduce<3>(big, F1{w.w, x, w.z, fw->m, N, aug ? P : 0, fw->side, fw->lam_x, fw->lam_y, w.scal},
-                      w.f.mr, w.scal + S_RED, s, F1Post{w.scal});
-        map_reduce<0>(big, F2{x, w.w, w.r, w.z, N, T, w.scal}, w.f.mr, nullptr, s);
-        forward_top(fw, w.r, w.fv, 1, w.f, s);
-        map_reduce<2>(big, F3{w.fv, w.r, fw->m, N, T, P, fw->side, fw->lam_x, fw->lam_y, aug, w.scal},
-                      w.f.mr, w.scal + S_RED, s, F3Post{w.scal});
-        map_reduce<0>(N, F4{w.w, w.fv, N, w.scal}, w.f.mr, nullptr, s);
-        KB_CUDA(cudaMemcpyAsync(hs, w.scal, sizeof(double) * S_TOTAL, cudaMemcpyDeviceToHost, s));
-        KB_CUDA(cudaStreamSynchronize(s));
-        if (hs[S_STALL] != 0.0) {
-            st->stop = KB_CGLS_STALLED;
-            break;
+    double* x = P.x;
+    forward_top(fw, w.w, w.z, 0, w.f, s);
+    map_reduce<3>(big, F1{w.w, x, w.z, fw->m, N, aug ? P_ : 0, fw->side, fw->lam_x, fw->lam_y, w.scal}, w.f.mr,
+                  w.scal + S_RED, s, F1Post{w.scal});
+    map_reduce<0>(big, F2{x, w.w, w.r, w.z, N, T, w.scal}, w.f.mr, nullptr, s);
+    forward_top(fw, w.r, w.fv, 1, w.f, s);
+    map_reduce<2>(big, F3{w.fv, w.r, fw->m, N, T, P_, fw->side, fw->lam_x, fw->lam_y, aug, w.scal}, w.f.mr,
+                  w.scal + S_RED, s, F3Post{w.scal});
+    map_reduce<0>(N, F4{w.w, w.fv, N, w.scal}, w.f.mr, nullptr, s);
+    k_cgls_control<<<1, 32, 0, s>>>(P.ctl);
+    KB_LAUNCH_CHECK();
+}
+
+// CUDA-graph cache for the CGLS loop (conditional while node around one iteration)
+struct CglsKey {
+    kb_forward fw;
+    const void *b, *x0, *x, *ws;
+    int i_max;
+    double tau;
+    bool operator==(const CglsKey& o) const { return std::memcmp(this, &o, sizeof(CglsKey)) == 0; }
+};
+struct CglsGraph {
+    CglsKey key;
+    cudaGraphExec_t exec;
+};
+static std::vector<CglsGraph> g_cgls_graphs;
+static cudaStream_t g_cgls_capture = nullptr;
+
+static cudaGraphExec_t cgls_build_graph(CglsPlan& P) {
+    if (!g_cgls_capture) KB_CUDA(cudaStreamCreateWithFlags(&g_cgls_capture, cudaStreamNonBlocking));
+    cudaStream_t cs = g_cgls_capture;
+    const bool prof = g_prof;
+    g_prof = false;
+    cudaGraph_t g = nullptr;
+    try {
+        KB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t capg;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphConditionalHandle h;
+        KB_CUDA(cudaGraphConditionalHandleCreate(&h, capg, 1, cudaGraphCondAssignDefault));
+        P.ctl.handle = h;
+        P.ctl.use_cond = 1;
+        cgls_enqueue_init(P, cs);
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        KB_CUDA(cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        KB_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+        KB_CUDA(cudaStreamEndCapture(cs, &g));
+        KB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        cgls_enqueue_body(P, cs);
+        cudaGraph_t body_out;
+        KB_CUDA(cudaStreamEndCapture(cs, &body_out));
+        cudaGraphExec_t exec;
+        KB_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        KB_CUDA(cudaGraphDestroy(g));
+        g_prof = prof;
+        return exec;
+    } catch (...) {
+        g_prof = prof;
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(cs, &junk);
+            if (junk) cudaGraphDestroy(junk);
         }
-        if (!std::isfinite(hs[S_FF])) {
-            set_error("CGLS produced non-finite residual quantities");
-            throw Fail{KB_ENUMERICAL};
-        }
-        st->iters++;
-        if (st->resnorm_host) st->resnorm_host[st->n_res] = std::sqrt(hs[S_RR]);
-        st->n_res++;
-        if (it >= 1) {
-            const double xn = hs[S_XN];
-            const double rc = xn > 0 ? hs[S_STEP] / xn : INFINITY;
-            if (st->rc_host) st->rc_host[st->n_rc] = rc;
-            st->n_rc++;
-            if (rc < st->tau) {
-                st->stop = KB_CGLS_CONVERGED;
-                break;
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
+}
+
+// Runs CGLS (cgls.py:50-116).  x0 may alias x (warm start) or be null.
+// Without an allreduce hook and without profiling the loop is one CUDA graph
+// launch (device-side stop test); otherwise the same kernels run eagerly with
+// a host read of the control block per iteration.
+static void cgls_core(const kb_forward* fw, const double* b, const double* x0, double* x,
+                      kb_cgls_state* st, CglsWs& w, double* hs, cudaStream_t s) {
+    CglsPlan P{fw, b, x0, x, &w, {}};
+    P.ctl.h = w.ctl;
+    P.ctl.rc = w.rc;
+    P.ctl.res = w.res;
+    P.ctl.scal = w.scal;
+    P.ctl.i_max = st->i_max;
+    P.ctl.tau = st->tau;
+    KB_REQUIRE(st->i_max <= w.i_cap, "i_max %d exceeds the CGLS workspace capacity %d", st->i_max, w.i_cap);
+    static const bool force_eager = std::getenv("KB_CGLS_EAGER") != nullptr;
+    int* hh = reinterpret_cast<int*>(hs);
+    if (!g_prof && !force_eager && fw->allreduce == nullptr) {
+        CglsKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.fw = *fw;
+        key.b = b;
+        key.x0 = x0;
+        key.x = x;
+        key.ws = w.scal;
+        key.i_max = st->i_max;
+        key.tau = st->tau;
+        cudaGraphExec_t exec = nullptr;
+        for (auto& e : g_cgls_graphs)
+            if (e.key == key) exec = e.exec;
+        if (!exec) {
+            exec = cgls_build_graph(P);
+            if (g_cgls_graphs.size() >= 16) {
+                cudaGraphExecDestroy(g_cgls_graphs.front().exec);
+                g_cgls_graphs.erase(g_cgls_graphs.begin());
             }
+            g_cgls_graphs.push_back({key, exec});
+        }
+        KB_CUDA(cudaGraphLaunch(exec, s));
+    } else {
+        P.ctl.use_cond = 0;
+        cgls_enqueue_init(P, s);
+        for (;;) {
+            KB_CUDA(cudaMemcpyAsync(hh, w.ctl, sizeof(int) * C_COUNT, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            if (!hh[C_RUN]) break;
+            cgls_enqueue_body(P, s);
         }
     }
+    KB_CUDA(cudaMemcpyAsync(hh, w.ctl, sizeof(int) * C_COUNT, cudaMemcpyDeviceToHost, s));
+    KB_CUDA(cudaStreamSynchronize(s));
+    if (hh[C_ERR]) {
+        set_error("CGLS produced non-finite residual quantities");
+        throw Fail{KB_ENUMERICAL};
+    }
+    st->iters = hh[C_ITERS];
+    st->stop = hh[C_STOP];
+    st->n_rc = hh[C_NRC];
+    st->n_res = hh[C_NRES];
+    if (st->rc_host && st->n_rc)
+        KB_CUDA(cudaMemcpyAsync(st->rc_host, w.rc, sizeof(double) * st->n_rc, cudaMemcpyDeviceToHost, s));
+    if (st->resnorm_host && st->n_res)
+        KB_CUDA(cudaMemcpyAsync(st->resnorm_host, w.res, sizeof(double) * st->n_res, cudaMemcpyDeviceToHost, s));
+    if ((st->rc_host && st->n_rc) || (st->resnorm_host && st->n_res)) KB_CUDA(cudaStreamSynchronize(s));
 }
 
 // ------------------------------------------------------------ SB driver
