@@ -6,7 +6,7 @@ on the matrix-free R(A) with the config's "rank 30 + enlargement p=2"
 down at the numerical rank, as the reference does) followed by `assemble`
 into fp64 Kronecker factors.  `value` = approximations/s over all ranks with
 inputs resident in HBM; `e2e` = the same through the public API from host
-arrays (PSF + reference-style host y0 uploaded, trace/sigma read back) each
+arrays (PSF uploaded, the reference's y0 stream drawn on the device by kb_rng.cu, trace/sigma read back) each
 step.  The same run also measures the fp64 split-Bregman solve that consumes
 the factors (isotropic, CGLS i_max=100 tau=1e-4) and reports outer / CGLS
 iterations per second in "sb", and the R(A) product in "ra_matvec".
@@ -158,8 +158,6 @@ def run_ours(args, prob, rank, world, dist):
     cfg = kb.EgkbConfig(**egkb_cfg_kwargs())
     scheme = kb.BlockScheme.square_image(n)
     blur = kb.RearrangedBlur(prob.psf, n)          # PSF resident on the device
-    y0_host = np.random.default_rng(cfg.seed).standard_normal(N).astype(np.float32)
-    y0 = D.to_device(y0_host)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=D.device())
 
     def barrier():
@@ -167,17 +165,18 @@ def run_ours(args, prob, rank, world, dist):
             dist.barrier()
 
     def step_resident():
-        svd, tr = kb.egkb(blur, cfg, y0=y0)
+        svd, tr = kb.egkb(blur, cfg)               # start vector drawn on the device (kb_rng.cu)
         op = kb.assemble(svd, scheme)
         return svd, tr, op
 
+    # the clock sampler starts before the warm-up so its start-up is outside the timed region
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
     for _ in range(max(args.warmup, 3)):
         step_resident()
     torch.cuda.synchronize()
 
     # ---- timed region (device-resident inputs, graph path), L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -186,7 +185,8 @@ def run_ours(args, prob, rank, world, dist):
         svd, tr, op = step_resident()
         ev[i][1].record()
         torch.cuda.synchronize()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
     t_max = torch.tensor([total_ms], dtype=torch.float64, device=D.device())
     if dist is not None:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -207,21 +207,21 @@ def run_ours(args, prob, rank, world, dist):
         b.record()
         torch.cuda.synchronize()
         prof_ms += a.elapsed_time(b)
-    prof = {c: prof_read(lib, c) for c in range(6)}
+    prof = {c: prof_read(lib, c) for c in range(7)}
     lib.kb_prof_enable(0)
     gpu_launches = sum(v[1] for v in prof.values())
 
     # ---- e2e: public API from host arrays, every step
     psf_host = prob.psf
-    h2d = 2 * psf_host.size * 4 + N * 4
+    h2d = psf_host.size * 4                                     # K once (K^T is built on the device)
     e2e_ms = []
     for i in range(max(args.steps, 1)):
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        blur_i = kb.RearrangedBlur(psf_host, n)                 # uploads K, K^T
-        svd_i, tr_i = kb.egkb(blur_i, cfg)                      # host y0 (reference RNG), uploads it
+        blur_i = kb.RearrangedBlur(psf_host, n)                 # validates + normalises the PSF, uploads K
+        svd_i, tr_i = kb.egkb(blur_i, cfg)                      # reference RNG stream, drawn on the device
         op_i = kb.assemble(svd_i, scheme)
         sig = np.asarray(svd_i.sigma)                           # result on the host
         torch.cuda.synchronize()
@@ -324,8 +324,8 @@ def run_ours(args, prob, rank, world, dist):
     # dominant kernel of the step: the class with the largest device time
     names = {0: "persistent eGKB (k_egkb_persistent)", 1: "R(A) diagonal sums (k_diag_seg)",
              2: "R(A) K-column sums (k_colsum_seg)", 3: "fp64 GEMM (k_dgemm, DMMA)", 4: "CGLS/SB vector passes",
-             5: "lift (k_lift)"}
-    dom = max(range(6), key=lambda c: prof[c][0])
+             5: "lift (k_lift)", 6: "start-vector draws (k_zig_*)"}
+    dom = max(range(7), key=lambda c: prof[c][0])
     d_ms, d_n, d_by, d_fl = prof[dom]
     achieved = (d_by / d_n) / ((d_ms / d_n) * 1e-3) / 1e9 if d_n else 0.0
     step_share = d_ms / prof_ms if prof_ms else 0.0
@@ -351,7 +351,9 @@ def run_ours(args, prob, rank, world, dist):
           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_src": "measured DMMA issue rate, tools/fp64_peak"}
     line = {
         "metric": METRIC, "value": value, "unit": "KP-approx/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "step_ms": {"min": float(min(step_ms)), "median": float(np.median(step_ms)), "max": float(max(step_ms))},
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 (matrix-free R(A)) -> assemble", "n": n,
                    "egkb": {k: (str(v) if k == "tau" else v) for k, v in egkb_cfg_kwargs().items()},

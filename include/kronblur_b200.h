@@ -163,6 +163,30 @@ int kb_egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const void* y0
                 kb_egkb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
 int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
 
+/* dst (cols x rows) = src (rows x cols)^T, row-major, device.  Builds the
+ * PSF transpose K^T used by the R(A)^T products on the device (the host
+ * uploads K once; blurmodel.py:25-65 Psf.kernel). */
+int kb_transpose(int dtype, const void* src, int64_t rows, int64_t cols, void* dst, kb_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Gaussian draws on the device (lowrank.py:199-201, lowrank.py:361-362) */
+/* ------------------------------------------------------------------ */
+/* Writes the first `count` values of numpy's
+ *     np.random.Generator(PCG64).standard_normal(count)
+ * (PCG64 XSL-RR stream + numpy's 256-layer float64 ziggurat) for the PCG64
+ * state {lo, hi} and increment {lo, hi} given on the host (numpy's
+ * bit_generator.state["state"]), rounded to dtype (KB_F32 = the reference's
+ * .astype(float32)).  cols > 0 writes the TRANSPOSE of the row-major
+ * (count/cols, cols) draw matrix (the device layout of the RSVD test matrix,
+ * lowrank.py:362).  Bit-identical to numpy for every fast-path and wedge
+ * sample; tail samples (|x| > 3.654, ~3e-4) use CUDA's log1p (<= 1 ulp in
+ * f64, identical after rounding to f32).  Replaces the host draws above. */
+int kb_normal_pcg64(const uint64_t* pcg_state_host, const uint64_t* pcg_inc_host, int64_t count, int dtype,
+                    int64_t cols, void* out, void* ws, size_t ws_bytes, kb_stream_t stream);
+int kb_normal_workspace_bytes(int64_t count, size_t* bytes);
+/* Test hook: speculate only `ne` (1..3) entry offsets per chunk (0 = default 4). */
+void kb_normal_test_entries(int ne);
+
 /* ------------------------------------------------------------------ */
 /* Structured exact TSVD lift (new, replaces         */
 /* svd_small(rearrange(A)) linalg.py:134-153 for blur operators)        */

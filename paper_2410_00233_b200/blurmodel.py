@@ -30,17 +30,19 @@ class Psf:
     kernel: np.ndarray
 
     def __post_init__(self):
-        k = np.array(self.kernel, dtype=np.float64)
+        k = np.array(self.kernel, dtype=np.float64)   # own copy (normalised in place below)
         if k.ndim != 2:
             raise ValidationError("PSF kernel must be 2-D")
         if k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
             raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
-        if np.any(k < 0):
-            raise ValidationError("PSF kernel must be non-negative")
+        if k.size == 0 or not k.min() >= 0:          # one reduction; the exact test only when it fails
+            if np.any(k < 0):
+                raise ValidationError("PSF kernel must be non-negative")
         total = k.sum()
         if total <= 0:
             raise ValidationError("PSF kernel must have positive mass")
-        self.kernel = k / total
+        k /= total                                    # bitwise identical to k / total
+        self.kernel = k
 
     @property
     def center(self) -> tuple[int, int]:
@@ -172,9 +174,13 @@ class RearrangedBlur:
         from . import device as D
 
         if self._k is None:
-            kk = self.psf.kernel.astype(self.dtype)
-            self._k = D.to_device(np.ascontiguousarray(kk))
-            self._kt = D.to_device(np.ascontiguousarray(kk.T))
+            # one upload (rounded to the working dtype while staging); K^T is built on the device
+            self._k = D.upload(self.psf.kernel, self.dtype)
+            kh, kw = self.psf.shape
+            self._kt = D.empty((kw, kh), self.dtype)
+            code = _lib.KB_F32 if self.dtype == np.float32 else _lib.KB_F64
+            _lib.check(_lib.load().kb_transpose(code, self._k.data_ptr(), kh, kw, self._kt.data_ptr(),
+                                                D.stream_ptr()), "kb_transpose")
         return self._k, self._kt
 
     def op_struct(self) -> _lib.KbOperator:

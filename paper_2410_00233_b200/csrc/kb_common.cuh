@@ -39,6 +39,18 @@ struct Fail {
 
 #define KB_LAUNCH_CHECK() KB_CUDA(cudaGetLastError())
 
+// Body wrapper of every C-ABI entry point: C++ failures -> status codes.
+#define KB_GUARD(...)                                  \
+    try {                                              \
+        __VA_ARGS__;                                   \
+        return KB_OK;                                  \
+    } catch (::kb::Fail f) {                           \
+        return f.code;                                 \
+    } catch (...) {                                    \
+        ::kb::set_error("unexpected C++ exception");   \
+        return KB_ERUNTIME;                            \
+    }
+
 inline cudaStream_t as_stream(kb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -75,7 +87,7 @@ struct Sizer {
 // Optional per-kernel-class device timing (CUDA events on the launching
 // stream), used by bench.py for the live roofline numbers.  Off by default.
 enum ProfClass { PROF_REORTH = 0, PROF_RA_DIAG, PROF_RA_COLSUM, PROF_DGEMM, PROF_SBVEC, PROF_LIFT,
-                 PROF_NCLASS };
+                 PROF_RNG, PROF_NCLASS };
 extern bool g_prof;
 void prof_record(cudaStream_t st, int cls, double bytes, double flops, bool start);
 struct ProfScope {

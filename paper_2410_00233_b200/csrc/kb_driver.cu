@@ -654,16 +654,6 @@ extern "C" const char* kb_last_error(void) { return g_err; }
 
 extern "C" int kb_version(void) { return 1; }
 
-#define KB_GUARD(...)                                               \
-    try {                                                           \
-        __VA_ARGS__;                                                \
-        return KB_OK;                                               \
-    } catch (Fail f) {                                              \
-        return f.code;                                              \
-    } catch (...) {                                                 \
-        set_error("unexpected C++ exception");                      \
-        return KB_ERUNTIME;                                         \
-    }
 
 extern "C" void kb_prof_enable(int on) {
     g_prof = on != 0;

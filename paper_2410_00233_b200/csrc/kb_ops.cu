@@ -666,3 +666,43 @@ void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int 
 }
 
 }  // namespace kb
+
+// ---------------------------------------------------------------- PSF transpose
+// K^T for the column-coalesced R(A)^T products; done on the device so the
+// host uploads the PSF once.
+namespace kb {
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose(const T* __restrict__ src, int64_t rows, int64_t cols,
+                                                   T* __restrict__ dst) {
+    __shared__ T tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+}  // namespace kb
+
+extern "C" int kb_transpose(int dtype, const void* src, int64_t rows, int64_t cols, void* dst,
+                            kb_stream_t stream) {
+    using namespace kb;
+    KB_GUARD({
+        KB_REQUIRE(src && dst && rows >= 0 && cols >= 0, "bad arguments");
+        KB_REQUIRE(dtype == KB_F32 || dtype == KB_F64, "dtype must be KB_F32 or KB_F64");
+        if (rows == 0 || cols == 0) return KB_OK;
+        KB_REQUIRE(cdiv(rows, 32) < 65536, "too many rows");
+        const dim3 grid((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), block(32, 8);
+        if (dtype == KB_F32)
+            k_transpose<float><<<grid, block, 0, as_stream(stream)>>>(static_cast<const float*>(src), rows, cols,
+                                                                      static_cast<float*>(dst));
+        else
+            k_transpose<double><<<grid, block, 0, as_stream(stream)>>>(static_cast<const double*>(src), rows,
+                                                                       cols, static_cast<double*>(dst));
+        KB_LAUNCH_CHECK();
+    })
+}

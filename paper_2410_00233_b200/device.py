@@ -58,6 +58,14 @@ def to_device(x, dtype=None, contiguous=True) -> torch.Tensor:
     return t.contiguous() if contiguous else t
 
 
+def upload(a: np.ndarray, dtype) -> torch.Tensor:
+    """Host array -> device tensor of ``dtype`` through pinned staging (cast while staging)."""
+    a = np.asarray(a)
+    stage = torch.empty(a.shape, dtype=torch_dtype(dtype), pin_memory=True)
+    np.copyto(stage.numpy(), a, casting="same_kind")
+    return stage.to(device(), non_blocking=True)
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 

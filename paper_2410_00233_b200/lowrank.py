@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, rng
 from .blurmodel import RearrangedBlur
 from .exceptions import NumericalError, ValidationError
 from .linalg import TruncatedSvd, eps_for, orthonormalize_device, precision_of, svd_small
@@ -248,8 +248,8 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
         reorth = REORTH_FULL if dtype == np.float32 else REORTH_ONE_SIDED
 
     if y0 is None:
-        # host RNG, exactly as the reference draws it (lowrank.py:199-201)
-        y0d = D.to_device(np.random.default_rng(config.seed).standard_normal(mbar).astype(dtype))
+        # the reference's draws (lowrank.py:199-201), generated on the device
+        y0d = rng.standard_normal(config.seed, mbar, dtype)
     elif D.is_tensor(y0):
         y0d = D.to_device(y0, dtype)
         if tuple(y0d.shape) != (mbar,):
@@ -334,8 +334,8 @@ def rsvd(b_mat, config: RsvdConfig) -> TruncatedSvd:
     if k_p > nbar:
         raise ValidationError(f"k + p = {k_p} exceeds the smaller matrix dimension {nbar}")
     dtype = np.dtype(op.dtype)
-    f = np.random.default_rng(config.seed).standard_normal((nbar, k_p)).astype(dtype)
-    fd = D.to_device(np.ascontiguousarray(f.T))
+    # the reference's test matrix (lowrank.py:361-362), drawn on the device, stored transposed
+    fd = rng.standard_normal(config.seed, (nbar, k_p), dtype, transpose=True)
     y = orthonormalize_device(op.apply_block(fd, 0))
     for _ in range(config.q):
         z = orthonormalize_device(op.apply_block(y, 1))
