@@ -45,6 +45,8 @@ typedef void* kb_stream_t; /* cudaStream_t */
 /* Operator kinds for the low-rank engines. */
 #define KB_OP_DENSE 0   /* b_mat given densely (lowrank.py:187)             */
 #define KB_OP_RA_ZERO 1 /* matrix-free R(A) of a zero-BC PSF blur (new)      */
+#define KB_OP_RA_REFLEXIVE 2 /* matrix-free R(A), reflexive BC (blurmodel.py:80-84,
+                                122-126): Toeplitz + two Hankel index families */
 
 /* eGKB stop reasons (lowrank.py:26-29) */
 #define KB_STOP_NU_ROSE 1
@@ -66,7 +68,8 @@ int kb_version(void);
 
 /* Optional device timing per kernel class (CUDA events on the launching
  * stream): 0 reorth/normalise passes, 1 R(A) diagonal sums, 2 R(A)/dense
- * column sums + row dots, 3 FP64 GEMM, 4 SB/CGLS vector passes, 5 lifts.
+ * column sums + row dots, 3 FP64 GEMM, 4 SB/CGLS vector passes, 5 lifts,
+ * 6 device Gaussian draws.
  * kb_prof_enable(1) clears the record; kb_prof_query sums a class. */
 void kb_prof_enable(int on);
 int kb_prof_query(int cls, double* ms, long long* launches, double* bytes, double* flops);
@@ -75,7 +78,7 @@ int kb_prof_query(int cls, double* ms, long long* launches, double* bytes, doubl
 /* Operators B for eGKB / RSVD                                        */
 /* ------------------------------------------------------------------ */
 typedef struct {
-    int kind;          /* KB_OP_DENSE or KB_OP_RA_ZERO                     */
+    int kind;          /* KB_OP_DENSE, KB_OP_RA_ZERO or KB_OP_RA_REFLEXIVE  */
     int dtype;         /* KB_F32 / KB_F64: working precision               */
     int64_t rows;      /* mbar                                             */
     int64_t cols;      /* nbar                                             */
@@ -92,7 +95,7 @@ int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes);
 
 /* y = B x (transpose=0) or y = B^T x (transpose=1).
  * Replaces `b_mat @ q` / `b_mat.T @ s` (lowrank.py:211,238,250) and, for
- * KB_OP_RA_ZERO, `rearrange(build_blur_matrix(psf, n))` (rearrange.py:67-75,
+ * KB_OP_RA_*, `rearrange(build_blur_matrix(psf, n, bc))` (rearrange.py:67-75,
  * blurmodel.py:87-121) without forming R(A). */
 int kb_op_apply(const kb_operator* op, const void* x, void* y, int transpose,
                 void* ws, size_t ws_bytes, kb_stream_t stream);
@@ -191,9 +194,11 @@ void kb_normal_test_entries(int ne);
 /* Structured exact TSVD lift (new, replaces         */
 /* svd_small(rearrange(A)) linalg.py:134-153 for blur operators)        */
 /* ------------------------------------------------------------------ */
-/* out_c[a*n+b] = coef[c*ldc + (b-a+center)] (0 outside [0,len_coef)), c<k */
+/* out_c[a*n+b] = coef[c*ldc + (b-a+center)] (0 outside [0,len_coef)), c<k;
+ * reflexive != 0 adds the Hankel families coef[a+b+1+center] and
+ * coef[a+b+center+1-2n] (reflexive BC, blurmodel.py:122-126). */
 int kb_toeplitz_lift(int dtype, const void* coef, int64_t ldc, int len_coef, int center,
-                     int k, int side, void* out, int64_t ld_out, kb_stream_t stream);
+                     int k, int side, int reflexive, void* out, int64_t ld_out, kb_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Kronecker sum, fp64 (kronop.py:28-123)                               */

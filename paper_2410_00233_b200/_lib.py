@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 KB_OK, KB_EVALIDATION, KB_ENUMERICAL, KB_ERUNTIME = 0, 2, 3, 4
 KB_F32, KB_F64 = 0, 1
-KB_OP_DENSE, KB_OP_RA_ZERO = 0, 1
+KB_OP_DENSE, KB_OP_RA_ZERO, KB_OP_RA_REFLEXIVE = 0, 1, 2
 KB_STOP = {1: "nu_rose", 2: "nu_below_tol", 3: "hit_kmax", 4: "breakdown"}
 KB_FWD_DENSE, KB_FWD_KRON = 0, 1
 KB_SB_ANISOTROPIC, KB_SB_ISOTROPIC = 0, 1
@@ -99,7 +99,7 @@ _SIGS = {
     "kb_normal_pcg64": (C.c_int, [P(C.c_uint64), P(C.c_uint64), i64, C.c_int, i64, vp, vp, SZ, vp]),
     "kb_normal_workspace_bytes": (C.c_int, [i64, P(SZ)]),
     "kb_normal_test_entries": (None, [C.c_int]),
-    "kb_toeplitz_lift": (C.c_int, [C.c_int, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, vp]),
+    "kb_toeplitz_lift": (C.c_int, [C.c_int, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, vp]),
     "kb_kron_workspace_bytes": (C.c_int, [P(KbKron), P(SZ)]),
     "kb_kron_apply": (C.c_int, [P(KbKron), vp, vp, C.c_int, vp, SZ, vp]),
     "kb_kron_assemble": (C.c_int, [C.c_int, vp, i64, vp, i64, dp, C.c_int, i64, i64, vp, vp, vp]),

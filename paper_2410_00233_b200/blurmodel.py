@@ -133,11 +133,13 @@ def make_test_image(n: int) -> np.ndarray:
 
 
 class RearrangedBlur:
-    """Matrix-free R(A) of a zero-BC PSF blur on n x n images.
+    """Matrix-free R(A) of a PSF blur on n x n images (zero or reflexive BC).
 
     R[c_in*n + c_out, r_in*n + r_out] = K[r_out - r_in + cu, c_out - c_in + cv]
     (closed form of rearrange.py:67-75 o blurmodel.py:106-121; SURVEY
-    Appendix A).  Shape (n^2, n^2); ``dtype`` is the working precision of the
+    Appendix A).  For bc="reflexive" (blurmodel.py:80-84, 122-126) R =
+    P_c K^T P_r^T where P also carries the two Hankel (reflected) index
+    families; the same kernels run with the anti-diagonal terms enabled.  Shape (n^2, n^2); ``dtype`` is the working precision of the
     engines (float32 = the reference's "SP" path).  The PSF lives on the
     device; products run in the sm_100a kernels of libkronblur_b200.
     """
@@ -145,11 +147,13 @@ class RearrangedBlur:
     def __init__(self, psf, n: int, bc: str = BC_ZERO, dtype=np.float32):
         if not isinstance(psf, Psf):
             psf = Psf(psf)
-        if bc != BC_ZERO:
-            raise ValidationError(
-                f"RearrangedBlur supports bc='zero' only (reflexive is a SURVEY §8(f) 'next' row), got {bc!r}")
+        if bc not in BOUNDARY_CONDITIONS:
+            raise ValidationError(f"boundary condition must be one of {BOUNDARY_CONDITIONS}, got {bc!r}")
         if n < 1:
             raise ValidationError("image side must be >= 1")
+        kh, kw = psf.shape
+        if bc == BC_REFLEXIVE and (kh > 2 * n - 1 or kw > 2 * n - 1):   # blurmodel.py:100-101
+            raise ValidationError("PSF support too large for single reflection at this image size")
         self.psf = psf
         self.n = int(n)
         self.bc = bc
@@ -187,7 +191,7 @@ class RearrangedBlur:
         k, kt = self._device_kernels()
         kh, kw = self.psf.shape
         op = _lib.KbOperator()
-        op.kind = _lib.KB_OP_RA_ZERO
+        op.kind = _lib.KB_OP_RA_ZERO if self.bc == BC_ZERO else _lib.KB_OP_RA_REFLEXIVE
         op.dtype = _lib.KB_F32 if self.dtype == np.float32 else _lib.KB_F64
         op.rows = op.cols = self.n * self.n
         op.a, op.lda = None, 0

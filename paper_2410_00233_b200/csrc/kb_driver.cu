@@ -76,14 +76,27 @@ static void scalars(cudaStream_t st, const double* a0, double* d0, const double*
 
 template <typename T>
 __global__ void k_toeplitz_lift(const T* __restrict__ coef, int64_t ldc, int L, int center, int k,
-                                int side, T* __restrict__ out, int64_t ld_out) {
+                                int side, T* __restrict__ out, int64_t ld_out, int refl) {
     const int64_t len = (int64_t)side * side;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * blockDim.x) {
         const unsigned a = (unsigned)e / (unsigned)side;
-        const int u = (int)((unsigned)e - a * (unsigned)side) - (int)a + center;
+        const int b = (int)((unsigned)e - a * (unsigned)side);
+        const int u = b - (int)a + center;
         const bool ok = (u >= 0 && u < L);
-        for (int c = 0; c < k; ++c) out[(int64_t)c * ld_out + e] = ok ? coef[(int64_t)c * ldc + u] : T(0);
+        if (!refl) {
+            for (int c = 0; c < k; ++c) out[(int64_t)c * ld_out + e] = ok ? coef[(int64_t)c * ldc + u] : T(0);
+        } else {
+            // Toeplitz + Hankel families of the reflexive BC (kb_ops.cuh ra_bcast)
+            const int s = (int)a + b + 1 + center, h = s - 2 * side;
+            for (int c = 0; c < k; ++c) {
+                const T* cc = coef + (int64_t)c * ldc;
+                double y = ok ? (double)cc[u] : 0.0;
+                if (s < L) y += (double)cc[s];
+                if (h >= 0) y += (double)cc[h];
+                out[(int64_t)c * ld_out + e] = (T)y;
+            }
+        }
     }
 }
 
@@ -108,12 +121,15 @@ static void validate_op(const kb_operator* op) {
     KB_REQUIRE(op != nullptr, "null operator");
     KB_REQUIRE(op->dtype == KB_F32 || op->dtype == KB_F64, "unsupported dtype code %d", op->dtype);
     KB_REQUIRE(op->rows >= 1 && op->cols >= 1, "operator has an empty shape");
-    if (op->kind == KB_OP_RA_ZERO) {
+    if (ra_is_operator(op->kind)) {
         KB_REQUIRE(op->k && op->kt, "R(A) operator needs the PSF and its transpose");
         KB_REQUIRE(op->kh >= 1 && op->kw >= 1 && (op->kh % 2) == 1 && (op->kw % 2) == 1,
                    "PSF support must be odd in both dimensions, got (%d, %d)", op->kh, op->kw);
         KB_REQUIRE(op->side >= 1 && (int64_t)op->side * op->side == op->rows && op->rows == op->cols,
                    "R(A) shape must be n^2 x n^2");
+        // blurmodel.py:100-101: one reflection must cover the support
+        KB_REQUIRE(op->kind == KB_OP_RA_ZERO || (op->kh <= 2 * op->side - 1 && op->kw <= 2 * op->side - 1),
+                   "PSF support too large for single reflection at this image size");
     } else {
         KB_REQUIRE(op->kind == KB_OP_DENSE, "unknown operator kind %d", op->kind);
         KB_REQUIRE(op->a != nullptr && op->lda >= op->cols, "bad dense operator");
@@ -688,7 +704,7 @@ extern "C" int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes) {
         Sizer s;
         op_plan_size(op, s);
         s.take<unsigned>(8);
-        if (op->kind == KB_OP_RA_ZERO) s.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+        if (ra_is_operator(op->kind)) s.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
         *bytes = s.off;
     })
 }
@@ -702,7 +718,7 @@ extern "C" int kb_op_apply(const kb_operator* op, const void* x, void* y, int tr
         OpPlan p = op_plan_make(op, a);
         (void)a.take<unsigned>(8);
         cudaStream_t s = as_stream(stream);
-        if (op->kind == KB_OP_RA_ZERO) {
+        if (ra_is_operator(op->kind)) {
             double* scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
             if (ra_block_apply(op, x, op->cols, y, op->rows, 1, transpose, scr, s)) return KB_OK;
         }
@@ -725,7 +741,7 @@ extern "C" int kb_op_apply_block(const kb_operator* op, const void* X, int64_t l
         OpPlan p = op_plan_make(op, a);
         (void)a.take<unsigned>(8);
         double* scr = nullptr;
-        if (op->kind == KB_OP_RA_ZERO)
+        if (ra_is_operator(op->kind))
             scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
         for (int v0 = 0; v0 < nv; v0 += KB_BLOCK_MAXV) {
             const int cnt = std::min(KB_BLOCK_MAXV, nv - v0);
@@ -827,7 +843,7 @@ extern "C" int kb_egkb_run(const kb_operator* op, const kb_egkb_config* cfg, con
 }
 
 extern "C" int kb_toeplitz_lift(int dtype, const void* coef, int64_t ldc, int len_coef, int center,
-                                int k, int side, void* out, int64_t ld_out, kb_stream_t stream) {
+                                int k, int side, int reflexive, void* out, int64_t ld_out, kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(coef && out && k >= 1 && side >= 1, "bad arguments");
         const int64_t len = (int64_t)side * side;
@@ -835,10 +851,12 @@ extern "C" int kb_toeplitz_lift(int dtype, const void* coef, int64_t ldc, int le
         cudaStream_t s = as_stream(stream);
         if (dtype == KB_F32)
             k_toeplitz_lift<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(coef), ldc, len_coef,
-                                                          center, k, side, static_cast<float*>(out), ld_out);
+                                                          center, k, side, static_cast<float*>(out), ld_out,
+                                                          reflexive);
         else
             k_toeplitz_lift<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(coef), ldc, len_coef,
-                                                           center, k, side, static_cast<double*>(out), ld_out);
+                                                           center, k, side, static_cast<double*>(out), ld_out,
+                                                           reflexive);
         KB_LAUNCH_CHECK();
     })
 }

@@ -38,6 +38,7 @@ struct PkParams {
     const void* K;    // kh x kw
     const void* Kt;   // kw x kh
     int kh, kw, n;
+    int refl;         // reflexive BC (Hankel index families, kb_ops.cuh)
     void* S;
     void* Q;
     int64_t ld_s, ld_q;
@@ -153,23 +154,9 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
         for (int it = blockIdx.x; it < items; it += nblk) {
             const int c = it % chunks, seg = it / chunks;
             const int u = c * 32 + lane;
-            const int d = u - ci;
             const int s0 = (int)((int64_t)n * seg / PK_SEGS), s1 = (int)((int64_t)n * (seg + 1) / PK_SEGS);
             double a = 0.0;
-            if (u < Li) {
-                const int lo = max(s0, -d), hi = min(s1, n - d);
-                int r = lo + warp;
-                const T* p = H.x + (int64_t)r * n + (r + d);
-                const int64_t step = 8 * (int64_t)(n + 1);
-                for (; r + 56 < hi; r += 64, p += 8 * step) {
-                    T q[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + k * step);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) a += (double)q[k];
-                }
-                for (; r < hi; r += 8, p += step) a += (double)__ldcg(p);
-            }
+            if (u < Li) a = ra_gather_rows<T, true>(H.x, n, u, ci, s0, s1, warp, P.refl != 0);
             acc[warp * 33 + lane] = a;
             __syncthreads();
             if (warp == 0 && u < Li) {
@@ -249,10 +236,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
             }
 #pragma unroll
             for (int q = 0; q < VEC; ++q) {
-                const unsigned e = (unsigned)(e0 + q);
-                const unsigned a = e / (unsigned)n;
-                const int u = (int)(e - a * (unsigned)n) - (int)a + co;
-                const T yv = (u >= 0 && u < Lo) ? (T)zs[u] : T(0);
+                const T yv = (T)ra_bcast(zs, (unsigned)(e0 + q), n, co, Lo, P.refl != 0);
                 ysq += (double)yv * (double)yv;
                 v[g][q] = pk_sub(yv, pk_mul(H.beta, pv[q]));
             }
@@ -570,7 +554,7 @@ size_t pk_scratch_doubles(int lmax, int cap) {
 bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_state* st, const void* y0,
                      int* hdr, double* trace, double* scratch, void* raw, double tol, double** scales_out,
                      cudaStream_t s) {
-    if (op->kind != KB_OP_RA_ZERO) return false;
+    if (!ra_is_operator(op->kind)) return false;
     if (cfg->reorth_passes >= 2) return false;
     const int n = op->side;
     const int lmax = std::max(op->kh, op->kw);
@@ -585,6 +569,7 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     P.kh = op->kh;
     P.kw = op->kw;
     P.n = n;
+    P.refl = op->kind == KB_OP_RA_REFLEXIVE;
     P.S = st->s_basis;
     P.Q = st->q_basis;
     P.ld_s = st->ld_s;

@@ -29,31 +29,16 @@ constexpr int RA_SEGS = 8;
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_diag_seg(const VecRef xr, int n, int center, int L, double* __restrict__ part,
+k_diag_seg(const VecRef xr, int n, int center, int L, int refl, double* __restrict__ part,
            double* __restrict__ w, unsigned* counters) {
     const T* __restrict__ X = resolve<const T>(xr);
     __shared__ double red[8][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int u = blockIdx.x * 32 + lane;
-    const int d = u - center;
     const int seg = blockIdx.y, nseg = gridDim.y;
     const int s0 = (int)((int64_t)n * seg / nseg), s1 = (int)((int64_t)n * (seg + 1) / nseg);
     double acc = 0.0;
-    if (u < L) {
-        const int lo = max(s0, -d), hi = min(s1, n - d);
-        const T* p = X + (int64_t)lo * n + (lo + d);
-        const int64_t step = 8 * (int64_t)(n + 1);
-        int a = lo + warp;
-        p += (int64_t)warp * (n + 1);
-        for (; a + 56 < hi; a += 64, p += 8 * step) {   // 8 independent loads per trip
-            T v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = __ldg(p + q * step);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc += (double)v[q];
-        }
-        for (; a < hi; a += 8, p += step) acc += (double)__ldg(p);
-    }
+    if (u < L) acc = ra_gather_rows<T, false>(X, n, u, center, s0, s1, warp, refl != 0);
     red[warp][lane] = acc;
     __syncthreads();
     if (warp == 0 && u < L) {
@@ -184,10 +169,7 @@ struct Gen {
     __device__ __forceinline__ T y(int64_t e) const {
         if (mode == SRC_BUF64) return (T)z[e];
         if (mode == SRC_BUFT) return zt[e];
-        const unsigned ee = (unsigned)e;            // n^2 < 2^32 for n <= 65535
-        const unsigned a = ee / (unsigned)side;
-        const int u = (int)(ee - a * (unsigned)side) - (int)a + center;
-        return (u >= 0 && u < L) ? (T)zs[u] : T(0);
+        return (T)ra_bcast(zs, (unsigned)e, side, center, L, mode == SRC_TOEP_REFL);   // n^2 < 2^32
     }
 };
 
@@ -246,7 +228,7 @@ k_reorth(const VecRef zr, int mode, int side, int center, int L, const VecRef pr
     extern __shared__ double sm[];
     const int m = mr.idx ? (*mr.idx) * mr.mul + mr.add : mr.add;
     const int mmax = mr.max;
-    const int Ls = (mode == SRC_TOEP) ? L : 0;
+    const int Ls = (mode >= SRC_TOEP) ? L : 0;
     double* zs = sm;
     double* coef = zs + Ls;
     double* accw = coef + mmax;            // [8][m+2]
@@ -437,7 +419,7 @@ static int rb_for(int rows, int chunks, int target_blocks = 4 * kSMs) {
 }
 
 void op_plan_size(const kb_operator* op, Sizer& s) {
-    if (op->kind == KB_OP_RA_ZERO) {
+    if (ra_is_operator(op->kind)) {
         const int L = op->kh > op->kw ? op->kh : op->kw;
         const int n = op->side;
         const int nrb_max = 4 * kSMs;
@@ -458,7 +440,7 @@ void op_plan_size(const kb_operator* op, Sizer& s) {
 OpPlan op_plan_make(const kb_operator* op, Arena& a) {
     OpPlan p;
     p.op = op;
-    if (op->kind == KB_OP_RA_ZERO) {
+    if (ra_is_operator(op->kind)) {
         const int L = op->kh > op->kw ? op->kh : op->kw;
         const int nrb_max = 4 * kSMs;
         p.part = a.take<double>((size_t)nrb_max * L + 2 * L);
@@ -483,7 +465,7 @@ template <typename T>
 static Src op_source_t(const OpPlan& p, const VecRef& x, int transpose, cudaStream_t st) {
     const kb_operator* op = p.op;
     Src s;
-    if (op->kind == KB_OP_RA_ZERO) {
+    if (ra_is_operator(op->kind)) {
         int ci, Li, co, Lo;
         const void* Mv;
         ra_geom(op, transpose, ci, Li, co, Lo, Mv);
@@ -494,10 +476,16 @@ static Src op_source_t(const OpPlan& p, const VecRef& x, int transpose, cudaStre
         // diagonal sums: 32 diagonals x 1 row segment per CTA
         {
             double band = 0;
-            for (int u = 0; u < Li; ++u) band += std::max(n - std::abs(u - ci), 0);
+            for (int u = 0; u < Li; ++u) {
+                band += std::max(n - std::abs(u - ci), 0);
+                if (op->kind == KB_OP_RA_REFLEXIVE && u != ci) {   // anti-diagonal a + b = s
+                    const int sa = u > ci ? u - ci - 1 : u - ci - 1 + 2 * n;
+                    band += std::max(std::min(sa + 1, 2 * n - 1 - sa), 0);
+                }
+            }
             ProfScope ps(st, PROF_RA_DIAG, band * sizeof(T));
-            k_diag_seg<T><<<dim3((unsigned)cdiv(Li, 32), segs), 256, 0, st>>>(x, n, ci, Li, p.part, p.w,
-                                                                              p.counters);
+            k_diag_seg<T><<<dim3((unsigned)cdiv(Li, 32), segs), 256, 0, st>>>(
+                x, n, ci, Li, op->kind == KB_OP_RA_REFLEXIVE, p.part, p.w, p.counters);
             KB_LAUNCH_CHECK();
         }
         // z = M^T w with M = K (forward) or K^T (transpose): rows Li, cols Lo
@@ -509,7 +497,7 @@ static Src op_source_t(const OpPlan& p, const VecRef& x, int transpose, cudaStre
             KB_LAUNCH_CHECK();
         }
         s.z = VecRef::at(p.z);
-        s.mode = SRC_TOEP;
+        s.mode = op->kind == KB_OP_RA_REFLEXIVE ? SRC_TOEP_REFL : SRC_TOEP;
         s.side = n;
         s.center = co;
         s.L = Lo;
@@ -577,7 +565,7 @@ template <typename T, int VEC>
 static void launch_reorth(const Src& src, const void* S, int64_t ld, const MRef& m, const double* cA,
                           const double* cB, bool dots, const VecRef& out, const double* div, int64_t len,
                           double* red, double* fix, const ReorthWs& ws, cudaStream_t st) {
-    const int Ls = (src.mode == SRC_TOEP) ? src.L : 0;
+    const int Ls = (src.mode >= SRC_TOEP) ? src.L : 0;
     const int mm = m.max;
     const size_t smem = sizeof(double) * ((size_t)Ls + mm + 8 * (mm + 2) + (mm + 4));
     auto kern = k_reorth<T, VEC, REORTH_R>;

@@ -27,6 +27,60 @@ __device__ __forceinline__ T* resolve(const VecRef& r) {
     return r.idx ? p + (int64_t)(*r.idx + r.off) * r.ld : p;
 }
 
+// ------------------------------------------------------------------ R(A) index families
+// R(A) = P_c K^T P_r^T.  Row (a, b) of P (image cell
+// a*n + b) hits index u = b - a + c (Toeplitz, zero and reflexive BC) and, for
+// the reflexive BC (blurmodel.py:80-84, 122-126), also u = a + b + 1 + c and
+// u = a + b + c + 1 - 2n (Hankel: the reflections below 0 and above n-1).
+inline bool ra_is_operator(int kind) { return kind == KB_OP_RA_ZERO || kind == KB_OP_RA_REFLEXIVE; }
+
+// Broadcast P z at cell e = a*n + b (fp64; z in shared memory, length L).
+__device__ __forceinline__ double ra_bcast(const double* zs, unsigned e, int n, int c, int L, bool refl) {
+    const unsigned a = e / (unsigned)n;
+    const int b = (int)(e - a * (unsigned)n);
+    const int u = b - (int)a + c;
+    double y = (u >= 0 && u < L) ? zs[u] : 0.0;
+    if (refl) {
+        const int s = (int)a + b + 1 + c;
+        if (s < L) y += zs[s];
+        if (s - 2 * n >= 0) y += zs[s - 2 * n];
+    }
+    return y;
+}
+
+// Sum of X[a*stride + off] over rows a in [lo, hi) with a = lo + phase (mod 8),
+// 8 independent loads in flight (CG: coherent loads for data written in-kernel).
+template <typename T, bool CG>
+__device__ __forceinline__ double band_rows(const T* X, int64_t stride, int64_t off, int lo, int hi, int phase) {
+    double acc = 0.0;
+    int a = lo + phase;
+    const T* p = X + (int64_t)a * stride + off;
+    const int64_t step = 8 * stride;
+    for (; a + 56 < hi; a += 64, p += 8 * step) {
+        T q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = CG ? __ldcg(p + k * step) : __ldg(p + k * step);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += (double)q[k];
+    }
+    for (; a < hi; a += 8, p += step) acc += (double)(CG ? __ldcg(p) : __ldg(p));
+    return acc;
+}
+
+// (P^T x)[u] restricted to image rows [s0, s1), summed by row phase `phase`
+// (the caller reduces over the 8 phases and the row segments).
+template <typename T, bool CG>
+__device__ __forceinline__ double ra_gather_rows(const T* X, int n, int u, int c, int s0, int s1, int phase,
+                                                 bool refl) {
+    const int d = u - c;   // diagonal b - a = d
+    double acc = band_rows<T, CG>(X, n + 1, d, max(s0, -d), min(s1, n - d), phase);
+    if (refl && u != c) {
+        const int s = u > c ? d - 1 : d - 1 + 2 * n;   // anti-diagonal a + b = s
+        acc += band_rows<T, CG>(X, n - 1, s, max(s0, s - n + 1), min(s1, s + 1), phase);
+    }
+    return acc;
+}
+
 // Basis size resolved on the device: m = idx ? (*idx) * mul + add : add.
 struct MRef {
     const int* idx = nullptr;
@@ -41,7 +95,8 @@ struct MRef {
 //   SRC_BUFT   : y[e] = x[e]       (a stored vector in T, e.g. y0 or a slot)
 //   SRC_BUF64  : y[e] = (T) z[e]   (dense operator product, fp64 accumulated)
 //   SRC_TOEP   : y[a*n+b] = (T) z[b - a + center], 0 outside [0,L)  (R(A))
-enum SrcMode { SRC_BUFT = 0, SRC_BUF64 = 1, SRC_TOEP = 2 };
+//   SRC_TOEP_REFL : the same plus the Hankel families (reflexive BC, ra_bcast)
+enum SrcMode { SRC_BUFT = 0, SRC_BUF64 = 1, SRC_TOEP = 2, SRC_TOEP_REFL = 3 };
 
 struct Src {
     VecRef z;                     // BUFT: T vector; BUF64/TOEP: fp64 array

@@ -2,9 +2,10 @@
 //
 //   Y = R(A) X  (or R(A)^T X),  X, Y: nv vectors of length n^2
 //
-// R(A) = W_c K^T W_r^T: per vector, diagonal sums of the
+// R(A) = P_c K^T P_r^T: per vector, diagonal sums of the
 // n x n image (w), a small GEMV with K (z = K^T w), and a Toeplitz broadcast
-// y[a*n+b] = z[b - a + c].  The three steps are phases of ONE cooperative
+// y[a*n+b] = z[b - a + c]; the reflexive BC adds anti-diagonal sums and the
+// two Hankel broadcast families (kb_ops.cuh ra_gather_rows / ra_bcast).  The three steps are phases of ONE cooperative
 // kernel separated by grid barriers; K is read once for the whole block (the
 // RSVD block products, lowrank.py:361-369, and the standalone product
 // lowrank.py:211,238,250 with nv = 1).  Fixed-order reductions throughout.
@@ -36,6 +37,7 @@ struct RaBlockParams {
     double* col_part;  // [RB_SEGS][nv][lmax]
     unsigned long long* dbg;   // optional phase timestamps (KB_PK_TRACE)
     int zlen;
+    int refl;          // reflexive BC: Hankel index families too
 };
 
 __device__ __forceinline__ void rb_mark(const RaBlockParams& P, int slot) {
@@ -67,24 +69,11 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
         for (int it = blockIdx.x; it < items; it += nblk) {
             const int c = it % chunks, seg = it / chunks;
             const int u = c * 32 + lane;
-            const int d = u - P.ci;
             const int s0 = (int)((int64_t)n * seg / RB_SEGS), s1 = (int)((int64_t)n * (seg + 1) / RB_SEGS);
-            const int lo = max(s0, -d), hi = min(s1, n - d);
-            const int64_t step = 8 * (int64_t)(n + 1);
             for (int v = 0; v < nv; ++v) {
                 double a = 0.0;
-                if (u < P.Li) {
-                    int r = lo + warp;
-                    const T* p = X + (int64_t)v * P.ldx + (int64_t)r * n + (r + d);
-                    for (; r + 56 < hi; r += 64, p += 8 * step) {
-                        T q[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) q[k] = __ldg(p + k * step);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) a += (double)q[k];
-                    }
-                    for (; r < hi; r += 8, p += step) a += (double)__ldg(p);
-                }
+                if (u < P.Li)
+                    a = ra_gather_rows<T, false>(X + (int64_t)v * P.ldx, n, u, P.ci, s0, s1, warp, P.refl != 0);
                 acc[warp * 33 + lane] = a;
                 __syncthreads();
                 if (warp == 0 && u < P.Li) {
@@ -191,9 +180,7 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int64_t e = e0 + q;
-                const unsigned a = (unsigned)e / (unsigned)n;
-                const int u = (int)((unsigned)e - a * (unsigned)n) - (int)a + P.co;
-                o[q] = (e < N && u >= 0 && u < P.Lo) ? (T)zs[u] : T(0);
+                o[q] = e < N ? (T)ra_bcast(zs, (unsigned)e, n, P.co, P.Lo, P.refl != 0) : T(0);
             }
             if (e0 + 4 <= N && ((P.ldy & 3) == 0)) {
                 if constexpr (sizeof(T) == 4) {
@@ -219,7 +206,7 @@ size_t ra_block_scratch_doubles(int lmax, int nv) {
 // Returns false if the cooperative launch is not possible (caller falls back).
 bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv,
                     int transpose, double* scratch, cudaStream_t st) {
-    if (op->kind != KB_OP_RA_ZERO || nv < 1 || nv > RB_MAXV) return false;
+    if (!ra_is_operator(op->kind) || nv < 1 || nv > RB_MAXV) return false;
     if (((uintptr_t)Y & 15) != 0) return false;
     RaBlockParams P{};
     const int cu = op->kh / 2, cv = op->kw / 2;
@@ -229,6 +216,7 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     P.ldy = ldy;
     P.nv = nv;
     P.n = op->side;
+    P.refl = op->kind == KB_OP_RA_REFLEXIVE;
     if (!transpose) { P.ci = cu; P.Li = op->kh; P.co = cv; P.Lo = op->kw; P.M = op->k; }
     else { P.ci = cv; P.Li = op->kw; P.co = cu; P.Lo = op->kh; P.M = op->kt; }
     P.lmax = std::max(op->kh, op->kw);

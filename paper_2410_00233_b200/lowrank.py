@@ -350,12 +350,42 @@ def rsvd(b_mat, config: RsvdConfig) -> TruncatedSvd:
 
 
 # ----------------------------------------------------------------- TSVD
+def _ra_gram(n: int, center: int, length: int) -> np.ndarray:
+    """G = P^T P for the reflexive-BC incidence P (length x length).
+
+    Cell (a, b) hits u = b - a + c, a + b + 1 + c and a + b + c + 1 - 2n
+    (each at most once); G counts co-hits: O(n^2) host work, done once per TSVD.
+    """
+    ar = np.arange(n, dtype=np.int64)
+    a = np.repeat(ar, n)
+    b = np.tile(ar, n)
+    s = a + b + 1 + center
+    fams = (b - a + center, s, s - 2 * n)
+    valid = [(u >= 0) & (u < length) for u in fams]
+    g = np.zeros(length * length)
+    for i in range(3):
+        for j in range(3):
+            m = valid[i] & valid[j]
+            g += np.bincount(fams[i][m] * length + fams[j][m], minlength=length * length)
+    return g.reshape(length, length)
+
+
+def _half_inverse_factor(g: np.ndarray):
+    """(E L^1/2, E L^-1/2) over the positive eigenpairs of the Gram matrix G = E L E^T."""
+    lam, e = np.linalg.eigh(g)
+    keep = lam > lam.max() * 1e-12
+    lam, e = lam[keep], e[:, keep]
+    return e * np.sqrt(lam)[None, :], e / np.sqrt(lam)[None, :]
+
+
 def tsvd(b_mat, k: int) -> TruncatedSvd:
     """Exact top-k SVD of R(A).
 
     For a :class:`RearrangedBlur` this is structured:
     R = (W^_c U) S (W^_r V)^T with M = D_c K^T D_r = U S V^T, a (kw x kh)
-    host SVD, lifted to n^2-vectors by the Toeplitz-broadcast kernel.  This
+    host SVD, lifted to n^2-vectors by the Toeplitz-broadcast kernel.  The
+    reflexive BC uses the Gram matrices G = P^T P of its Toeplitz + Hankel
+    incidence instead of the diagonal D^2 (eigh on the host, same lift).  This
     replaces ``svd_small(rearrange(A)).truncate(k)`` (linalg.py:128-153),
     which the reference can only run for n <= 64.  Dense inputs take the
     reference route (``svd_small``).
@@ -369,15 +399,27 @@ def tsvd(b_mat, k: int) -> TruncatedSvd:
     kern = blur.psf.kernel
     kh, kw = kern.shape
     cu, cv = kh // 2, kw // 2
-    dr = np.sqrt(np.maximum(n - np.abs(np.arange(kh) - cu), 0).astype(np.float64))
-    dc = np.sqrt(np.maximum(n - np.abs(np.arange(kw) - cv), 0).astype(np.float64))
-    m = dc[:, None] * kern.T * dr[None, :]
-    um, sm, vmt = np.linalg.svd(m, full_matrices=False)
-    if not 0 < k <= sm.size:
-        raise ValidationError(f"cannot truncate rank-{sm.size} factorization to k={k}")
-    with np.errstate(divide="ignore", invalid="ignore"):
-        uc = np.where(dc[:, None] > 0, um[:, :k] / dc[:, None], 0.0).T    # (k, kw)
-        vc = np.where(dr[:, None] > 0, vmt[:k].T / dr[:, None], 0.0).T    # (k, kh)
+    refl = blur.bc == "reflexive"
+    if not refl:
+        dr = np.sqrt(np.maximum(n - np.abs(np.arange(kh) - cu), 0).astype(np.float64))
+        dc = np.sqrt(np.maximum(n - np.abs(np.arange(kw) - cv), 0).astype(np.float64))
+        m = dc[:, None] * kern.T * dr[None, :]
+        um, sm, vmt = np.linalg.svd(m, full_matrices=False)
+        if not 0 < k <= sm.size:
+            raise ValidationError(f"cannot truncate rank-{sm.size} factorization to k={k}")
+        with np.errstate(divide="ignore", invalid="ignore"):
+            uc = np.where(dc[:, None] > 0, um[:, :k] / dc[:, None], 0.0).T    # (k, kw)
+            vc = np.where(dr[:, None] > 0, vmt[:k].T / dr[:, None], 0.0).T    # (k, kh)
+    else:
+        # G = P^T P = E L E^T;  M = (E_c L_c^1/2)^T K^T (E_r L_r^1/2) = U S V^T;
+        # singular vectors P (E L^-1/2 U)  (Toeplitz + Hankel broadcast on the device)
+        br, cr = _half_inverse_factor(_ra_gram(n, cu, kh))
+        bcc, ccc = _half_inverse_factor(_ra_gram(n, cv, kw))
+        um, sm, vmt = np.linalg.svd(bcc.T @ kern.T @ br, full_matrices=False)
+        if not 0 < k <= sm.size:
+            raise ValidationError(f"cannot truncate rank-{sm.size} factorization to k={k}")
+        uc = (ccc @ um[:, :k]).T
+        vc = (cr @ vmt[:k].T).T
     dtype = blur.dtype
     code = _lib.KB_F32 if dtype == np.float32 else _lib.KB_F64
     lib = _lib.load()
@@ -385,8 +427,8 @@ def tsvd(b_mat, k: int) -> TruncatedSvd:
     v_rows = D.empty((k, n * n), dtype)
     ucd = D.to_device(np.ascontiguousarray(uc), dtype)
     vcd = D.to_device(np.ascontiguousarray(vc), dtype)
-    _lib.check(lib.kb_toeplitz_lift(code, ucd.data_ptr(), kw, kw, cv, k, n, u_rows.data_ptr(), n * n,
+    _lib.check(lib.kb_toeplitz_lift(code, ucd.data_ptr(), kw, kw, cv, k, n, int(refl), u_rows.data_ptr(), n * n,
                                     D.stream_ptr()), "toeplitz lift")
-    _lib.check(lib.kb_toeplitz_lift(code, vcd.data_ptr(), kh, kh, cu, k, n, v_rows.data_ptr(), n * n,
+    _lib.check(lib.kb_toeplitz_lift(code, vcd.data_ptr(), kh, kh, cu, k, n, int(refl), v_rows.data_ptr(), n * n,
                                     D.stream_ptr()), "toeplitz lift")
     return TruncatedSvd.from_device(u_rows, sm[:k].astype(dtype), v_rows)

@@ -2,7 +2,9 @@
 
 Run in the build container only (needs /root/reference):
 
-    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py [reflexive]
+
+(``reflexive`` regenerates only ra_reflexive.npz.)
 
 Writes ``tests/golden/*.npz``.  Every array in them is an input or an output
 of the unmodified reference package ``kronblur`` (``pkg/src/kronblur``); the
@@ -223,5 +225,40 @@ def main():
     save("config_n64", **cf)
 
 
+def reflexive():
+    """Reflexive-BC R(A) (blurmodel.py:80-84, 122-126): dense reference R, products,
+    singular values, and fp32 eGKB runs on the dense reference R."""
+    rng = np.random.default_rng(2024)
+    rf = {}
+    cases = [(3, 5, 7), (5, 3, 6), (9, 9, 10), (1, 3, 6), (13, 13, 7), (11, 3, 12)]
+    for i, (kh, kw, n) in enumerate(cases):
+        psf = Psf(rng.random((kh, kw)))
+        r_mat = rearrange(build_blur_matrix(psf, n, bc="reflexive"), BlockScheme.square_image(n))
+        q = rng.standard_normal(n * n)
+        s = rng.standard_normal(n * n)
+        rf[f"c{i}_psf"] = psf.kernel
+        rf[f"c{i}_n"] = n
+        rf[f"c{i}_R"] = r_mat
+        rf[f"c{i}_q"] = q
+        rf[f"c{i}_s"] = s
+        rf[f"c{i}_Rq"] = r_mat @ q
+        rf[f"c{i}_RTs"] = r_mat.T @ s
+        rf[f"c{i}_sigma"] = np.linalg.svd(r_mat, compute_uv=False)
+    rf["ncases"] = len(cases)
+    # config generators at small sides, fp32 dense R (the reference's SP path)
+    for name, side in (("n64", 32), ("n256", 40)):
+        prob = datagen.make_problem(name, n=side)
+        r32 = cast(rearrange(build_blur_matrix(Psf(prob.psf), side, bc="reflexive"),
+                             BlockScheme.square_image(side)), "single")
+        rf[f"blur_{name}_psf"] = prob.psf
+        rf[f"blur_{name}_n"] = side
+        egkb_case(f"blur_{name}_", r32, dict(prob.egkb), rf)
+    save("ra_reflexive", **rf)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["reflexive"]:
+        reflexive()
+    else:
+        main()
+        reflexive()

@@ -64,8 +64,10 @@ class TestRearrangedBlur:
     def test_validation(self, kb):
         with pytest.raises(kb.ValidationError):
             kb.RearrangedBlur(np.ones((4, 3)), 8)
+        with pytest.raises(kb.ValidationError):   # single reflection only (blurmodel.py:100-101)
+            kb.RearrangedBlur(np.ones((17, 3)), 8, bc="reflexive")
         with pytest.raises(kb.ValidationError):
-            kb.RearrangedBlur(np.ones((3, 3)), 8, bc="reflexive")
+            kb.RearrangedBlur(np.ones((3, 3)), 8, bc="periodic")
         op = kb.RearrangedBlur(np.ones((3, 3)), 8)
         with pytest.raises(kb.ValidationError):
             op.matvec(np.ones(10, dtype=np.float32))

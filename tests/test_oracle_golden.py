@@ -54,6 +54,51 @@ class TestStructuredRA:
         np.testing.assert_allclose(got, g["pad_Ax"], rtol=0, atol=1e-15)
 
 
+class TestReflexiveRA:
+    """Reflexive BC (blurmodel.py:80-84, 122-126) vs the reference's dense R."""
+
+    def test_dense_products_and_sigma(self):
+        g = load_golden("ra_reflexive")
+        for i in range(int(g["ncases"])):
+            k, n = g[f"c{i}_psf"], int(g[f"c{i}_n"])
+            np.testing.assert_allclose(ost.ra_dense(k, n, "reflexive"), g[f"c{i}_R"], rtol=0, atol=1e-15)
+            np.testing.assert_allclose(ost.ra_matvec(k, n, g[f"c{i}_q"], "reflexive"), g[f"c{i}_Rq"],
+                                       rtol=0, atol=1e-14)
+            np.testing.assert_allclose(ost.ra_rmatvec(k, n, g[f"c{i}_s"], "reflexive"), g[f"c{i}_RTs"],
+                                       rtol=0, atol=1e-14)
+            u, sig, v = ost.structured_tsvd(k, n, bc="reflexive")
+            ref = g[f"c{i}_sigma"][: sig.size]
+            np.testing.assert_allclose(sig, ref, rtol=0, atol=1e-13 * ref[0])
+            np.testing.assert_allclose((u * sig) @ v.T, g[f"c{i}_R"], atol=1e-13)
+
+    def test_gram_is_incidence_gram(self):
+        for n, c, length in [(7, 6, 13), (8, 1, 3), (6, 2, 5)]:
+            p = ost.incidence(n, c, length, "reflexive")
+            np.testing.assert_array_equal(ost.gram(n, c, length, "reflexive"), p.T @ p)
+            assert p.max() == 1.0   # a cell hits an index at most once
+
+    def test_egkb_blur_configs(self):
+        """The oracle eGKB on the structured reflexive operator reproduces the
+        reference's dense fp32 run (rank decisions exactly, sigma to 1e-4)."""
+        from oracle import lowrank as olr
+
+        g = load_golden("ra_reflexive")
+        for name in ("n64", "n256"):
+            pre = f"blur_{name}_"
+            from paper_2410_00233_b200 import blurmodel
+
+            n = int(g[pre + "n"])
+            k32 = blurmodel.Psf(g[pre + "psf"]).kernel.astype(np.float32)   # Psf: unit sum (blurmodel.py:25-65)
+            mv = lambda q: ost.ra_matvec(k32, n, q, "reflexive")
+            rmv = lambda x: ost.ra_rmatvec(k32, n, x, "reflexive")
+            (_, s, _), tr = olr.egkb(mv, rmv, (n * n, n * n), np.float32, _cfg(g[pre + "cfg"]))
+            assert (tr.chosen_k, tr.k_p, tr.stop_reason) == (int(g[pre + "tr_chosen_k"]), int(g[pre + "tr_k_p"]),
+                                                             str(g[pre + "tr_stop_reason"]))
+            ref = g[pre + "sigma"].astype(np.float64)
+            big = ref >= 1e-3 * ref[0]
+            np.testing.assert_allclose(s[big], ref[big], rtol=1e-4)
+
+
 def _dense(b):
     return (lambda q: b @ q), (lambda s: b.T @ s)
 
