@@ -284,6 +284,38 @@ int kb_sb_workspace_bytes(const kb_forward* fw, size_t* bytes);
 int kb_sb_run(const kb_forward* fw, const double* b, const double* x_true, double* x,
               kb_sb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
 
+/* Batched lambda sweep (splitbregman.py:195-235 `sweep`, cli.py:488-527):
+ * nprob independent SB solves of the SAME observation b with the SAME
+ * Kronecker operator and per-problem (lam, beta), run in lock step so every
+ * Kronecker product is ONE pair of DMMA GEMMs over all problems (the images
+ * are stacked along the GEMM M dimension) and every vector pass is one launch
+ * over all problems.  Problems whose CGLS / SB loop has stopped are masked
+ * out; each problem follows splitbregman.py:120-192 exactly as kb_sb_run. */
+typedef struct {
+    int nprob;
+    const double* lam_host;   /* [nprob] */
+    const double* beta_host;  /* [nprob] */
+    int variant;              /* shared: KB_SB_*, tau, l_max, CGLS i_max / tau, warm start */
+    double tau;
+    int l_max;
+    int i_max;
+    double tau_cgls;
+    int warm_start;
+    int* outer_iters_host;    /* [nprob] out */
+    int* stop_host;           /* [nprob] out */
+    double* rc_host;          /* [nprob * l_max] out (row p = problem p) */
+    double* re_host;          /* [nprob * l_max] out, if x_true */
+    double* isnr_host;        /* [nprob * l_max] out, if x_true */
+    int* cgls_iters_host;     /* [nprob * l_max] out */
+} kb_sb_batch;
+int kb_sb_batch_workspace_bytes(const kb_forward* fw, int nprob, size_t* bytes);
+/* fw: plain square Kronecker forward operator (KB_FWD_KRON); x: nprob x n^2 (device). */
+int kb_sb_run_batch(const kb_forward* fw, const double* b, const double* x_true, double* x,
+                    kb_sb_batch* st, void* ws, size_t ws_bytes, kb_stream_t stream);
+/* Test hook: split the stacked GEMMs per problem as kb_sb_run does (more
+ * split-K partial traffic), making every problem bit-identical to its own run. */
+void kb_sb_batch_exact(int on);
+
 /* Elementwise pieces exposed for parity tests (splitbregman.py:32-61,
  * regularizers.py:37-62). */
 int kb_diff(const double* x, double* out, int side, int axis, int transpose, double scale,

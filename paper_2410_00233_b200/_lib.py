@@ -77,6 +77,13 @@ class KbSbState(C.Structure):
                 ("isnr_host", dp), ("cgls_iters_host", ip)]
 
 
+class KbSbBatch(C.Structure):
+    _fields_ = [("nprob", C.c_int), ("lam_host", dp), ("beta_host", dp), ("variant", C.c_int), ("tau", C.c_double),
+                ("l_max", C.c_int), ("i_max", C.c_int), ("tau_cgls", C.c_double), ("warm_start", C.c_int),
+                ("outer_iters_host", ip), ("stop_host", ip), ("rc_host", dp), ("re_host", dp), ("isnr_host", dp),
+                ("cgls_iters_host", ip)]
+
+
 P = C.POINTER
 SZ = C.c_size_t
 _SIGS = {
@@ -111,6 +118,9 @@ _SIGS = {
     "kb_cgls_run": (C.c_int, [P(KbForward), vp, vp, vp, P(KbCglsState), vp, SZ, vp]),
     "kb_sb_workspace_bytes": (C.c_int, [P(KbForward), P(SZ)]),
     "kb_sb_run": (C.c_int, [P(KbForward), vp, vp, vp, P(KbSbState), vp, SZ, vp]),
+    "kb_sb_batch_workspace_bytes": (C.c_int, [P(KbForward), C.c_int, P(SZ)]),
+    "kb_sb_run_batch": (C.c_int, [P(KbForward), vp, vp, vp, P(KbSbBatch), vp, SZ, vp]),
+    "kb_sb_batch_exact": (None, [C.c_int]),
     "kb_diff": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, vp]),
     "kb_shrink_update": (C.c_int, [vp, vp, vp, vp, i64, C.c_double, C.c_int, vp]),
 }

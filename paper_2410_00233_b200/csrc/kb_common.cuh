@@ -80,7 +80,19 @@ struct Arena {
 struct Sizer {
     size_t off = 0;
     template <typename T>
-    void take(size_t count) { off += align_up(count * sizeof(T)); }
+    T* take(size_t count) {   // same signature as Arena::take (returns no memory)
+        off += align_up(count * sizeof(T));
+        return nullptr;
+    }
+};
+
+// Masked GEMM work for batched solves: blocks whose problem is inactive exit.
+// rows > 0: problems stacked along M (problem = row / rows); rows == 0: the
+// problem is the batch index.  flags[p * stride] != 0 means active.
+struct GemmSkip {
+    const int* flags = nullptr;
+    int stride = 0;
+    int rows = 0;
 };
 
 // ---------------------------------------------------------------- profiling

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sa_batch,
         int64_t sa_seg, const double* __restrict__ B, int64_t ldb, int64_t sb_batch,
         int64_t sb_seg, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nseg,
-        double beta, int splits, int64_t split_stride) {
+        double beta, int splits, int64_t split_stride, GemmSkip skip) {
     constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES, THREADS = CF::THREADS;
     constexpr int MI = CF::MI, NI = CF::NI;
     using AL = typename CF::template A<TA>;
@@ -86,6 +86,15 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     const int wm = warp % CF::WM, wn = warp / CF::WM;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int z = blockIdx.z / splits, split = blockIdx.z - z * splits;
+    if (skip.flags) {   // batched solves: tiles of inactive problems do no work
+        if (skip.rows > 0) {
+            bool any = false;
+            for (int p = m0 / skip.rows; p <= min(M - 1, m0 + BM - 1) / skip.rows; ++p) any |= skip.flags[p * skip.stride] != 0;
+            if (!any) return;
+        } else if (!skip.flags[z * skip.stride]) {
+            return;
+        }
+    }
     const double* Ab = A + (int64_t)z * sa_batch;
     const double* Bb = B + (int64_t)z * sb_batch;
     double* Cb = C + (int64_t)z * sc_batch + (int64_t)split * split_stride;
@@ -220,11 +229,12 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
 
 __global__ void k_split_reduce(const double* __restrict__ part, int splits, int64_t split_stride, int M,
                                int N, double* __restrict__ C, int64_t ldc, int64_t sc_batch, int nbatch,
-                               double beta) {
+                               double beta, GemmSkip skip) {
     const int64_t per = (int64_t)M * N, total = per * nbatch;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = e / per, rem = e - z * per;
+        if (skip.flags && skip.rows == 0 && !skip.flags[z * skip.stride]) continue;
         const int64_t i = rem / N, j = rem - i * N;
         const double* p = part + z * sc_batch + i * ldc + j;   // partials share C's layout
         double s = 0.0;
@@ -240,6 +250,8 @@ using Cfg1 = GCfg<128, 64, 32, 2, 4, 2, 2>;    // BK 32: half the barriers per f
 using Cfg2 = GCfg<128, 128, 16, 3, 2, 4, 1>;   // 8 warps of 64x32, 1 CTA/SM
 using Cfg3 = GCfg<128, 128, 32, 2, 2, 4, 1>;
 static int g_dgemm_cfg = -1;
+int g_dgemm_split_per_batch = 0;
+GemmSkip g_dgemm_skip;   // set around the batched-solve GEMMs (kb_sb.cu), empty otherwise
 
 template <class CF, bool TA, bool TB, bool V16>
 static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
@@ -259,14 +271,15 @@ static void launch_dgemm(int m, int n, int k, const double* A, int64_t lda, int6
                  2.0 * m * n * (double)k * nb * ns);
     if (splits == 1) {
         k_dgemm<CF, TA, TB, V16><<<grid, CF::THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
-                                                                  C, ldc, sc_b, nseg, beta, 1, 0);
+                                                                  C, ldc, sc_b, nseg, beta, 1, 0, g_dgemm_skip);
     } else {
         k_dgemm<CF, TA, TB, V16><<<grid, CF::THREADS, smem, st>>>(m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s,
-                                                                  part, ldc, sc_b, nseg, 0.0, splits, split_stride);
+                                                                  part, ldc, sc_b, nseg, 0.0, splits, split_stride,
+                                                                  g_dgemm_skip);
         KB_LAUNCH_CHECK();
         const int64_t total = (int64_t)m * n * nbatch;
         k_split_reduce<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(
-            part, splits, split_stride, m, n, C, ldc, sc_b, nbatch, beta);
+            part, splits, split_stride, m, n, C, ldc, sc_b, nbatch, beta, g_dgemm_skip);
     }
     KB_LAUNCH_CHECK();
 }
@@ -287,7 +300,9 @@ static void dgemm_cfg(int ta, int tb, int m, int n, int k, const double* A, int6
                       int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
                       int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
                       double* part, int64_t part_doubles) {
-    int splits = dgemm_splits<CF>(m, n, k, nbatch, nseg);
+    // g_dgemm_split_per_batch: split K exactly as a single batch entry would be
+    // split, so each batch entry reproduces the unbatched GEMM bit for bit
+    int splits = dgemm_splits<CF>(m, n, k, g_dgemm_split_per_batch ? 1 : nbatch, nseg);
     const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;   // partials use C's layout
     if (part == nullptr) splits = 1;
     while (splits > 1 && (int64_t)splits * span > part_doubles) splits /= 2;

@@ -21,6 +21,8 @@
 
 namespace kb {
 
+extern int g_dgemm_split_per_batch;
+extern GemmSkip g_dgemm_skip;
 void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
            int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
            int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
@@ -998,4 +1000,660 @@ extern "C" int kb_shrink_update(const double* cx, const double* cy, double* dx, 
     } catch (Fail f) {
         return f.code;
     }
+}
+
+// ================================================================ batched lambda sweep
+// kb_sb_run_batch: nprob SB solves (same b, same Kronecker operator, per-problem
+// lam/beta) in lock step.  State vectors are stacked problem-major; every
+// vector pass is one launch with blockIdx.y = problem (per-problem fixed-order
+// reductions and on-device scalars, exactly the single-problem functors), and
+// each Kronecker product is one pair of batched DMMA GEMMs with the images
+// stacked along M.  Stopped problems are masked (their blocks exit at once).
+namespace kb {
+
+// Test hook (kb_sb_batch_exact): split the stacked GEMMs per problem exactly as
+// kb_sb_run does, so every problem of a batch is bit-identical to its own run.
+static int g_sbb_exact = 0;
+
+template <int R, class F, class P>
+__global__ void __launch_bounds__(MR_THREADS)
+k_map_reduce_b(int64_t len, F f, P post, double* part, double* out, int out_stride, unsigned* counter) {
+    __shared__ double sw[MR_THREADS / 32][MR_MAXR];
+    __shared__ double fin[MR_MAXR];
+    const int b = blockIdx.y;
+    if (f.skip(b)) return;   // uniform per problem
+    double acc[R > 0 ? R : 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)MR_THREADS + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * MR_THREADS)
+        f(b, e, acc);
+    if (R == 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double v = warp_sum(acc[r]);
+        if (lane == 0) sw[warp][r] = v;
+    }
+    __syncthreads();
+    double* pb = part + (int64_t)b * gridDim.x * R;
+    if (threadIdx.x < R) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < MR_THREADS / 32; ++w) s += sw[w][threadIdx.x];
+        pb[(int64_t)blockIdx.x * R + threadIdx.x] = s;
+    }
+    if (last_block_ticket(counter + b, gridDim.x)) {
+        if (warp < R) {
+            double s = 0.0;
+            for (int q = lane; q < (int)gridDim.x; q += 32) s += __ldcg(&pb[(int64_t)q * R + warp]);
+            s = warp_sum(s);
+            if (lane == 0) fin[warp] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double* ob = out + (int64_t)b * out_stride;
+            for (int r = 0; r < R; ++r) ob[r] = fin[r];
+            post(b, ob);
+        }
+    }
+}
+
+// Batched views of the single-problem functors: problem b's vectors start at
+// base + b * stride; scalars at scal + b * S_TOTAL; lam per problem.
+struct BNoPost {
+    __device__ void operator()(int, double*) const {}
+};
+template <class P>
+struct BPost {   // P(scal + b * S_TOTAL)
+    double* scal;
+    __device__ void operator()(int b, double* r) const { P{scal + (int64_t)b * S_TOTAL}(r); }
+};
+
+struct BF1 {
+    const double* w; const double* x; double* z; int64_t m, ncols, P, T; int n; const double* lam;
+    double* scal; const int* run;
+    __device__ bool skip(int b) const { return !run[b * C_COUNT + C_RUN]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        F1{w + b * ncols, x + b * ncols, z + b * T, m, ncols, P, n, lam[b], lam[b], scal + b * S_TOTAL}(e, acc);
+    }
+};
+struct BF2 {
+    double* x; const double* w; double* r; const double* z; int64_t ncols, T; const double* scal; const int* run;
+    __device__ bool skip(int b) const { return !run[b * C_COUNT + C_RUN] || scal[b * S_TOTAL + S_STALL] != 0.0; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        F2{x + b * ncols, w + b * ncols, r + b * T, z + b * T, ncols, T, scal + b * S_TOTAL}(e, acc);
+    }
+};
+struct BF3 {
+    double* f; const double* r; int64_t m, ncols, T, P; int n; const double* lam; int aug; const double* scal;
+    const int* run;
+    __device__ bool skip(int b) const { return !run[b * C_COUNT + C_RUN] || scal[b * S_TOTAL + S_STALL] != 0.0; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        F3{f + b * ncols, r + b * T, m, ncols, T, P, n, lam[b], lam[b], aug, scal + b * S_TOTAL}(e, acc);
+    }
+};
+struct BF4 {
+    double* w; const double* f; int64_t ncols; const double* scal; const int* run;
+    __device__ bool skip(int b) const { return !run[b * C_COUNT + C_RUN] || scal[b * S_TOTAL + S_STALL] != 0.0; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        F4{w + b * ncols, f + b * ncols, ncols, scal + b * S_TOTAL}(e, acc);
+    }
+};
+struct BFInit {
+    double* w; const double* f; const double* r; int64_t ncols, T; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        FInit{w + b * ncols, f + b * ncols, r + b * T, ncols, T}(e, acc);
+    }
+};
+struct BFCopy {   // dst_b = src_b (src stride may be 0: the shared b)
+    double* dst; const double* src; int64_t len, dst_stride, src_stride; const int* active;
+    __device__ bool skip(int b) const { return active && !active[b]; }
+    __device__ void operator()(int b, int64_t e, double*) const {
+        if (e < len) dst[b * dst_stride + e] = src[b * src_stride + e];
+    }
+};
+struct BFSub {   // r_b = rhs_b - r_b
+    double* r; const double* rhs; int64_t T; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const { FSub{r + b * T, rhs + b * T, T}(e, acc); }
+};
+struct BFTail {  // y_b[m..] = lam_b D x_b
+    const double* x; double* y; int64_t m, P, ncols, T; int n; const double* lam; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        FTail{x + b * ncols, y + b * T, m, P, n, lam[b], lam[b]}(e, acc);
+    }
+};
+struct BFTailT {  // out_b = (out_b + lam Dx^T y2) + lam Dy^T y3
+    double* out; const double* y; int64_t m, P, ncols, T; int n; const double* lam; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        FTailT{out + b * ncols, y + b * T, m, P, ncols, n, lam[b], lam[b]}(e, acc);
+    }
+};
+struct BFRhs {
+    double* rhs; const double* bb; const double* ddx; const double* ddy; const double* gx; const double* gy;
+    int64_t N, P, T; const double* lam; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        FRhs{rhs + b * T, bb, ddx + b * P, ddy + b * P, gx + b * P, gy + b * P, N, P, lam[b]}(e, acc);
+    }
+};
+struct BFSbUpd {
+    const double* x; const double* xprev; const double* xtrue; double* ddx; double* ddy; double* gx; double* gy;
+    int64_t N, P; int n; const double* inv_gamma; int iso; const int* active;
+    __device__ bool skip(int b) const { return !active[b]; }
+    __device__ void operator()(int b, int64_t e, double* acc) const {
+        FSbUpd{x + b * N, xprev + b * N, xtrue, ddx + b * P, ddy + b * P, gx + b * P, gy + b * P, N, P, n,
+               inv_gamma[b], iso}(e, acc);
+    }
+};
+
+struct BMR {
+    double* part;       // [nprob][blocks][MR_MAXR]
+    unsigned* counter;  // [nprob]
+    int nprob;
+};
+template <int R, class F, class P = BNoPost>
+static void map_reduce_b(int64_t len, const F& f, const BMR& mr, double* out, int out_stride, cudaStream_t st,
+                         const P& post = P()) {
+    const dim3 grid((unsigned)mr_blocks(len), (unsigned)mr.nprob);
+    ProfScope ps(st, PROF_SBVEC, 0.0);
+    k_map_reduce_b<R, F, P><<<grid, MR_THREADS, 0, st>>>(len, f, post, mr.part, out, out_stride, mr.counter);
+    KB_LAUNCH_CHECK();
+}
+
+// Y_b = A X_b for all problems: two batched DMMA GEMMs, images stacked along M.
+// x: B stacked inputs (contiguous, stride = input length); y: B outputs at stride ys.
+// flags/stride: per-problem activity (GEMM tiles of inactive problems exit).
+static void kron_apply_b(const kb_kron* kr, int B, const double* x, double* y, int64_t ys, int transpose,
+                         double* tmp, double* part, int64_t part_n, const int* flags, int stride,
+                         cudaStream_t st) {
+    const int m1 = kr->m1, m2 = kr->m2, n1 = kr->n1, n2 = kr->n2, k = kr->k;
+    struct Reset {
+        ~Reset() { g_dgemm_skip = GemmSkip{}; }
+    } reset;
+    g_dgemm_skip = GemmSkip{flags, stride, transpose ? m1 : n1};   // stage 1: problems stacked along M
+    if (!transpose) {
+        // P_i = [X_1; ...; X_B] G_i   ((B n1) x m2)
+        dgemm(0, 0, B * n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
+              (int64_t)B * n1 * m2, k, 1, 0.0, st);
+        // Y_b = sum_i F_i^T P_{i,b}   (m1 x m2), batch over b, segments over i
+        g_dgemm_skip = GemmSkip{flags, stride, 0};                          // stage 2: batch = problem
+        g_dgemm_split_per_batch = g_sbb_exact;
+        dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, (int64_t)n1 * m2,
+              (int64_t)B * n1 * m2, y, m2, ys, B, k, 0.0, st, part, part_n);
+        g_dgemm_split_per_batch = 0;
+    } else {
+        dgemm(0, 1, B * m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
+              (int64_t)B * m1 * n2, k, 1, 0.0, st);
+        g_dgemm_skip = GemmSkip{flags, stride, 0};
+        g_dgemm_split_per_batch = g_sbb_exact;
+        dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, (int64_t)m1 * n2,
+              (int64_t)B * m1 * n2, y, n2, ys, B, k, 0.0, st, part, part_n);
+        g_dgemm_split_per_batch = 0;
+    }
+}
+
+struct SbBatchWs {
+    double *r, *z, *w, *fv, *scal, *rhs, *ddx, *ddy, *gx, *gy, *xa, *xb, *red, *lam, *inv_gamma;
+    double *tmp, *part, *rc, *res, *gather;
+    int64_t part_n;
+    int* ctl;       // [nprob][C_COUNT]
+    int* active;    // [nprob]
+    int* any;       // [4]
+    BMR mr;
+};
+
+static int64_t sbb_part_doubles(const kb_forward* fw, int B) {
+    if (g_sbb_exact) return (int64_t)KRON_SPLIT_MAX * B * std::max(fw->m, fw->n) + 64;
+    // split-K partials (dgemm halves its splits to fit); at least the single-problem
+    // budget, so a batch of one runs exactly the GEMMs of kb_sb_run
+    const int64_t out = std::max(fw->m, fw->n);
+    return std::max((int64_t)4 * B * out, (int64_t)KRON_SPLIT_MAX * out) + 64;
+}
+
+template <class A>
+static void sbb_layout(const kb_forward* aug, int B, A& a, SbBatchWs* w) {
+    const int64_t T = fwd_rows(aug), N = aug->n, P = (int64_t)aug->side * (aug->side - 1);
+    const kb_kron& kr = aug->kron;
+    const int64_t tmp_n = (int64_t)kr.k * B * std::max((int64_t)kr.n1 * kr.m2, (int64_t)kr.m1 * kr.n2);
+    const int64_t blocks = mr_blocks(std::max(T, N));
+    auto take_d = [&](int64_t cnt) { return a.template take<double>((size_t)cnt); };
+    auto take_i = [&](int64_t cnt) { return a.template take<int>((size_t)cnt); };
+    double* p[21];
+    int64_t sizes[] = {B * T, B * T, B * N, B * N, (int64_t)B * S_TOTAL, B * T, B * P, B * P, B * P, B * P,
+                       B * N, B * N, (int64_t)B * 4, B, B, tmp_n + 64, sbb_part_doubles(aug, B),
+                       (int64_t)B * (CGLS_ICAP + 2), (int64_t)B * (CGLS_ICAP + 2), blocks * MR_MAXR * B + 64,
+                       (int64_t)B * std::max(N, aug->m)};
+    for (int i = 0; i < 21; ++i) p[i] = take_d(sizes[i]);
+    int* ctl = take_i((int64_t)B * C_COUNT);
+    int* active = take_i(B);
+    int* any = take_i(4);
+    unsigned* counter = a.template take<unsigned>((size_t)B + 64);
+    if (w) {
+        w->r = p[0]; w->z = p[1]; w->w = p[2]; w->fv = p[3]; w->scal = p[4]; w->rhs = p[5];
+        w->ddx = p[6]; w->ddy = p[7]; w->gx = p[8]; w->gy = p[9]; w->xa = p[10]; w->xb = p[11];
+        w->red = p[12]; w->lam = p[13]; w->inv_gamma = p[14]; w->tmp = p[15]; w->part = p[16];
+        w->part_n = sizes[16]; w->rc = p[17]; w->res = p[18];
+        w->mr = BMR{p[19], counter, B};
+        w->gather = p[20];
+        w->ctl = ctl; w->active = active; w->any = any;
+    }
+}
+
+// y_b = A x_b (or A^T x_b) for all problems; x_b at stride xs, y_b at stride ys.
+// The stacked first GEMM needs contiguous inputs: strided ones (the tops of
+// the augmented residuals) are gathered first (one B x len copy).
+static void forward_top_b(const kb_forward* fw, int B, const double* x, int64_t xs, double* y, int64_t ys,
+                          int transpose, SbBatchWs& w, const int* flags, int stride, cudaStream_t st) {
+    const int64_t in_len = transpose ? fw->m : fw->n;
+    if (xs != in_len) {
+        map_reduce_b<0>(in_len, BFCopy{w.gather, x, in_len, in_len, xs, nullptr}, w.mr, nullptr, 0, st);
+        x = w.gather;
+    }
+    kron_apply_b(&fw->kron, B, x, y, ys, transpose, w.tmp, w.part, w.part_n, flags, stride, st);
+}
+
+struct CglsCtlB {
+    int* h;            // [nprob][C_COUNT]
+    double* rc;        // [nprob][CGLS_ICAP + 2]
+    double* res;
+    const double* scal;
+    const int* active;
+    int* any;
+    int nprob, i_max;
+    double tau;
+    cudaGraphConditionalHandle handle;
+    int use_cond;
+};
+
+__global__ void k_cgls_init_ctl_b(CglsCtlB c) {
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    for (int b = threadIdx.x; b < c.nprob; b += blockDim.x) {
+        int* h = c.h + b * C_COUNT;
+        for (int i = 0; i < C_COUNT; ++i) h[i] = 0;
+        h[C_STOP] = KB_CGLS_MAX_ITER;
+        if (c.active[b]) {
+            c.res[(int64_t)b * (CGLS_ICAP + 2)] = sqrt(c.scal[b * S_TOTAL + S_RR]);
+            h[C_NRES] = 1;
+            h[C_RUN] = c.i_max >= 1;
+            if (h[C_RUN]) atomicOr(&any, 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        c.any[0] = any;
+        if (c.use_cond) cudaGraphSetConditional(c.handle, any ? 1u : 0u);
+    }
+}
+
+// cgls.py:90-114 per problem (k_cgls_control), then "any problem still running"
+__global__ void k_cgls_control_b(CglsCtlB c) {
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    for (int b = threadIdx.x; b < c.nprob; b += blockDim.x) {
+        int* h = c.h + b * C_COUNT;
+        if (!h[C_RUN]) continue;
+        const double* scal = c.scal + b * S_TOTAL;
+        double* rc = c.rc + (int64_t)b * (CGLS_ICAP + 2);
+        double* res = c.res + (int64_t)b * (CGLS_ICAP + 2);
+        const int it = h[C_ITERS];
+        if (scal[S_STALL] != 0.0) {
+            h[C_STOP] = KB_CGLS_STALLED;
+            h[C_RUN] = 0;
+        } else if (!isfinite(scal[S_FF])) {
+            h[C_ERR] = 1;
+            h[C_RUN] = 0;
+        } else {
+            h[C_ITERS] = it + 1;
+            res[h[C_NRES]++] = sqrt(scal[S_RR]);
+            if (it >= 1) {
+                const double xn = scal[S_XN];
+                const double r = xn > 0 ? scal[S_STEP] / xn : INFINITY;
+                rc[h[C_NRC]++] = r;
+                if (r < c.tau) {
+                    h[C_STOP] = KB_CGLS_CONVERGED;
+                    h[C_RUN] = 0;
+                }
+            }
+            if (h[C_ITERS] >= c.i_max) h[C_RUN] = 0;
+        }
+        if (h[C_RUN]) atomicOr(&any, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        c.any[0] = any;
+        if (c.use_cond) cudaGraphSetConditional(c.handle, any ? 1u : 0u);
+    }
+}
+
+struct CglsPlanB {
+    const kb_forward* aug;   // augmented operator (lam_x / lam_y unused: per-problem lam in w.lam)
+    int B;
+    const double* rhs;       // [B][T]
+    const double* x0;        // [B][N] or null
+    double* x;               // [B][N]
+    SbBatchWs* w;
+    CglsCtlB ctl;
+};
+
+static void cglsb_enqueue_init(CglsPlanB& P, cudaStream_t s) {
+    const kb_forward* fw = P.aug;
+    SbBatchWs& w = *P.w;
+    const int64_t T = fwd_rows(fw), N = fw->n, Pn = (int64_t)fw->side * (fw->side - 1);
+    const int n = fw->side;
+    const int64_t big = std::max(T, N);
+    if (P.x0 == nullptr) {
+        KB_CUDA(cudaMemsetAsync(P.x, 0, sizeof(double) * (size_t)P.B * N, s));
+        map_reduce_b<0>(T, BFCopy{w.r, P.rhs, T, T, T, w.active}, w.mr, nullptr, 0, s);
+    } else {
+        if (P.x0 != P.x) map_reduce_b<0>(N, BFCopy{P.x, P.x0, N, N, N, w.active}, w.mr, nullptr, 0, s);
+        forward_top_b(fw, P.B, P.x, N, w.r, T, 0, w, w.active, 1, s);
+        map_reduce_b<0>(2 * Pn, BFTail{P.x, w.r, fw->m, Pn, N, T, n, w.lam, w.active}, w.mr, nullptr, 0, s);
+        map_reduce_b<0>(T, BFSub{w.r, P.rhs, T, w.active}, w.mr, nullptr, 0, s);
+    }
+    forward_top_b(fw, P.B, w.r, T, w.fv, N, 1, w, w.active, 1, s);
+    map_reduce_b<0>(N, BFTailT{w.fv, w.r, fw->m, Pn, N, T, n, w.lam, w.active}, w.mr, nullptr, 0, s);
+    map_reduce_b<2>(big, BFInit{w.w, w.fv, w.r, N, T, w.active}, w.mr, w.scal + S_RED, S_TOTAL, s,
+                    BPost<FInitPost>{w.scal});
+    k_cgls_init_ctl_b<<<1, 256, 0, s>>>(P.ctl);
+    KB_LAUNCH_CHECK();
+}
+
+static void cglsb_enqueue_body(CglsPlanB& P, cudaStream_t s) {
+    const kb_forward* fw = P.aug;
+    SbBatchWs& w = *P.w;
+    const int64_t T = fwd_rows(fw), N = fw->n, Pn = (int64_t)fw->side * (fw->side - 1);
+    const int64_t big = std::max(T, N);
+    double* x = P.x;
+    forward_top_b(fw, P.B, w.w, N, w.z, T, 0, w, w.ctl + C_RUN, C_COUNT, s);
+    map_reduce_b<3>(big, BF1{w.w, x, w.z, fw->m, N, Pn, T, fw->side, w.lam, w.scal, w.ctl}, w.mr, w.scal + S_RED,
+                    S_TOTAL, s, BPost<F1Post>{w.scal});
+    map_reduce_b<0>(big, BF2{x, w.w, w.r, w.z, N, T, w.scal, w.ctl}, w.mr, nullptr, 0, s);
+    forward_top_b(fw, P.B, w.r, T, w.fv, N, 1, w, w.ctl + C_RUN, C_COUNT, s);
+    map_reduce_b<2>(big, BF3{w.fv, w.r, fw->m, N, T, Pn, fw->side, w.lam, 1, w.scal, w.ctl}, w.mr,
+                    w.scal + S_RED, S_TOTAL, s, BPost<F3Post>{w.scal});
+    map_reduce_b<0>(N, BF4{w.w, w.fv, N, w.scal, w.ctl}, w.mr, nullptr, 0, s);
+    k_cgls_control_b<<<1, 256, 0, s>>>(P.ctl);
+    KB_LAUNCH_CHECK();
+}
+
+struct CglsKeyB {
+    kb_forward fw;
+    const void *rhs, *x0, *x;
+    const void* ws[10];   // every workspace array the graph addresses (the layout depends on the mode)
+    int B, i_max, exact;
+    double tau;
+    bool operator==(const CglsKeyB& o) const { return std::memcmp(this, &o, sizeof(CglsKeyB)) == 0; }
+};
+struct CglsGraphB {
+    CglsKeyB key;
+    cudaGraphExec_t exec;
+};
+static std::vector<CglsGraphB> g_cglsb_graphs;
+
+static cudaGraphExec_t cglsb_build_graph(CglsPlanB& P) {
+    if (!g_cgls_capture) KB_CUDA(cudaStreamCreateWithFlags(&g_cgls_capture, cudaStreamNonBlocking));
+    cudaStream_t cs = g_cgls_capture;
+    const bool prof = g_prof;
+    g_prof = false;
+    cudaGraph_t g = nullptr;
+    try {
+        KB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t capg;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphConditionalHandle h;
+        KB_CUDA(cudaGraphConditionalHandleCreate(&h, capg, 1, cudaGraphCondAssignDefault));
+        P.ctl.handle = h;
+        P.ctl.use_cond = 1;
+        cglsb_enqueue_init(P, cs);
+        KB_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        KB_CUDA(cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        KB_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+        KB_CUDA(cudaStreamEndCapture(cs, &g));
+        KB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        cglsb_enqueue_body(P, cs);
+        cudaGraph_t body_out;
+        KB_CUDA(cudaStreamEndCapture(cs, &body_out));
+        cudaGraphExec_t exec;
+        KB_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        KB_CUDA(cudaGraphDestroy(g));
+        g_prof = prof;
+        return exec;
+    } catch (...) {
+        g_prof = prof;
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(cs, &junk);
+            if (junk) cudaGraphDestroy(junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
+}
+
+// Pinned host mailbox that grows on demand (per thread).
+static double* pinned_doubles(size_t count) {
+    static thread_local double* buf = nullptr;
+    static thread_local size_t cap = 0;
+    if (count > cap) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        const size_t want = std::max<size_t>(count, 4096);
+        KB_CUDA(cudaMallocHost(&buf, sizeof(double) * want));
+        cap = want;
+    }
+    return buf;
+}
+
+// One batched CGLS solve over the active problems (graph while-loop unless
+// profiling / sharded).  Returns the per-problem control blocks in hh.
+static void cglsb_core(CglsPlanB& P, int* hh, cudaStream_t s) {
+    static const bool force_eager = std::getenv("KB_CGLS_EAGER") != nullptr;
+    SbBatchWs& w = *P.w;
+    if (!g_prof && !force_eager && P.aug->allreduce == nullptr) {
+        CglsKeyB key;
+        std::memset(&key, 0, sizeof(key));
+        key.fw = *P.aug;
+        key.rhs = P.rhs;
+        key.x0 = P.x0;
+        key.x = P.x;
+        const void* wsp[10] = {w.scal, w.ctl, w.active, w.part, w.gather, w.mr.part, w.mr.counter, w.tmp, w.lam,
+                               w.rc};
+        std::memcpy(key.ws, wsp, sizeof(wsp));
+        key.exact = g_sbb_exact;
+        key.B = P.B;
+        key.i_max = P.ctl.i_max;
+        key.tau = P.ctl.tau;
+        cudaGraphExec_t exec = nullptr;
+        for (auto& e : g_cglsb_graphs)
+            if (e.key == key) exec = e.exec;
+        if (!exec) {
+            exec = cglsb_build_graph(P);
+            if (g_cglsb_graphs.size() >= 8) {
+                cudaGraphExecDestroy(g_cglsb_graphs.front().exec);
+                g_cglsb_graphs.erase(g_cglsb_graphs.begin());
+            }
+            g_cglsb_graphs.push_back({key, exec});
+        }
+        KB_CUDA(cudaGraphLaunch(exec, s));
+    } else {
+        P.ctl.use_cond = 0;
+        cglsb_enqueue_init(P, s);
+        int* any = reinterpret_cast<int*>(hh);
+        for (;;) {
+            KB_CUDA(cudaMemcpyAsync(any, w.any, sizeof(int), cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            if (!any[0]) break;
+            cglsb_enqueue_body(P, s);
+        }
+    }
+    KB_CUDA(cudaMemcpyAsync(hh, w.ctl, sizeof(int) * C_COUNT * P.B, cudaMemcpyDeviceToHost, s));
+    KB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace kb
+
+extern "C" void kb_sb_batch_exact(int on) { g_sbb_exact = on != 0; }
+
+extern "C" int kb_sb_batch_workspace_bytes(const kb_forward* fw, int nprob, size_t* bytes) {
+    KB_GUARD({
+        validate_fw(fw);
+        KB_REQUIRE(bytes && nprob >= 1, "bad arguments");
+        KB_REQUIRE(fw->kind == KB_FWD_KRON, "the batched sweep needs a Kronecker operator");
+        kb_forward aug = make_aug(fw, 1.0);
+        validate_fw(&aug);
+        Sizer z;
+        sbb_layout(&aug, nprob, z, nullptr);
+        *bytes = z.off;
+    })
+}
+
+extern "C" int kb_sb_run_batch(const kb_forward* fw, const double* b, const double* x_true, double* x,
+                               kb_sb_batch* st, void* ws, size_t ws_bytes, kb_stream_t stream) {
+    KB_GUARD({
+        validate_fw(fw);
+        KB_REQUIRE(st && b && x && st->lam_host && st->beta_host && st->outer_iters_host && st->stop_host,
+                   "null argument");
+        KB_REQUIRE(fw->kind == KB_FWD_KRON, "the batched sweep needs a Kronecker operator");
+        KB_REQUIRE(fw->allreduce == nullptr, "the batched sweep runs on one device (no term sharding)");
+        KB_REQUIRE(fw->m == fw->n, "operator must be square to start from the observed image");
+        KB_REQUIRE(!fw->augmented, "pass the plain forward operator to kb_sb_run_batch");
+        KB_REQUIRE(st->nprob >= 1 && st->nprob <= 65535, "nprob must be in [1, 65535]");
+        KB_REQUIRE(st->l_max >= 1 && st->i_max >= 1, "l_max and i_max must be >= 1");
+        KB_REQUIRE(st->i_max <= CGLS_ICAP, "i_max %d exceeds the CGLS history capacity %d", st->i_max, CGLS_ICAP);
+        const int B = st->nprob;
+        std::vector<double> lam(B), invg(B);
+        for (int p = 0; p < B; ++p) {
+            KB_REQUIRE(st->lam_host[p] > 0 && st->beta_host[p] > 0, "lam and beta must be positive");
+            lam[p] = st->lam_host[p];
+            invg[p] = 1.0 / (lam[p] * lam[p] / st->beta_host[p]);   // 1 / gamma, gamma = lam^2 / beta
+        }
+        kb_forward aug = make_aug(fw, 1.0);
+        validate_fw(&aug);
+        Arena a(ws, ws_bytes);
+        SbBatchWs w;
+        sbb_layout(&aug, B, a, &w);
+        cudaStream_t s = as_stream(stream);
+        const int64_t N = aug.n, P = (int64_t)aug.side * (aug.side - 1), T = fwd_rows(&aug);
+        const int n = aug.side;
+        // pinned mailbox: [4B + 8 doubles: reductions] [B * C_COUNT ints: CGLS control] [B ints: active flags]
+        const size_t ctl_d = ((size_t)B * C_COUNT + 1) / 2 + 8, act_d = ((size_t)B + 1) / 2 + 8;
+        double* hp = pinned_doubles(4 * (size_t)B + 8 + ctl_d + act_d);
+        int* hc = reinterpret_cast<int*>(hp + 4 * B + 8);
+        int* hact = reinterpret_cast<int*>(hp + 4 * B + 8 + ctl_d);
+        KB_CUDA(cudaMemsetAsync(w.mr.counter, 0, sizeof(unsigned) * ((size_t)B + 64), s));
+        KB_CUDA(cudaMemcpyAsync(w.lam, lam.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+        KB_CUDA(cudaMemcpyAsync(w.inv_gamma, invg.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+        std::vector<int> active(B, 1);
+        for (int p = 0; p < B; ++p) hact[p] = 1;
+        KB_CUDA(cudaMemcpyAsync(w.active, hact, sizeof(int) * B, cudaMemcpyHostToDevice, s));
+        // x_prev = b; d = g = 0  (splitbregman.py:158-162), per problem
+        double* xprev = w.xa;
+        double* xcur = w.xb;
+        map_reduce_b<0>(N, BFCopy{xprev, b, N, N, 0, nullptr}, w.mr, nullptr, 0, s);
+        KB_CUDA(cudaMemsetAsync(w.ddx, 0, sizeof(double) * 4 * (size_t)B * P, s));   // ddx..gy are contiguous
+        double obs = 0.0, xt_norm = 1.0;
+        if (x_true) {
+            MR mr1{w.mr.part, w.mr.counter};
+            map_reduce<2>(N, FNorm2{b, x_true, N}, mr1, w.red, s);
+            KB_CUDA(cudaMemcpyAsync(hp, w.red, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            obs = std::sqrt(hp[0]);
+            xt_norm = std::sqrt(hp[1]);
+            KB_REQUIRE(xt_norm != 0.0, "relative_error is undefined for a zero reference");
+        }
+        for (int p = 0; p < B; ++p) {
+            st->outer_iters_host[p] = 0;
+            st->stop_host[p] = KB_SB_MAX_ITER;
+        }
+        CglsPlanB cp{&aug, B, w.rhs, nullptr, nullptr, &w, {}};
+        cp.ctl.h = w.ctl;
+        cp.ctl.rc = w.rc;
+        cp.ctl.res = w.res;
+        cp.ctl.scal = w.scal;
+        cp.ctl.active = w.active;
+        cp.ctl.any = w.any;
+        cp.ctl.nprob = B;
+        cp.ctl.i_max = st->i_max;
+        cp.ctl.tau = st->tau_cgls;
+        std::vector<int> hctl((size_t)B * C_COUNT);
+        int n_active = B;
+        for (int l = 0; l < st->l_max && n_active > 0; ++l) {
+            map_reduce_b<0>(T, BFRhs{w.rhs, b, w.ddx, w.ddy, w.gx, w.gy, N, P, T, w.lam, w.active}, w.mr, nullptr,
+                            0, s);
+            cp.x0 = st->warm_start ? xprev : nullptr;
+            cp.x = xcur;
+            cglsb_core(cp, hc, s);
+            for (int p = 0; p < B; ++p)
+                if (active[p] && hc[p * C_COUNT + C_ERR]) {
+                    set_error("CGLS produced non-finite residual quantities (problem %d)", p);
+                    throw Fail{KB_ENUMERICAL};
+                }
+            std::memcpy(hctl.data(), hc, sizeof(int) * (size_t)B * C_COUNT);
+            map_reduce_b<3>(N, BFSbUpd{xcur, xprev, x_true, w.ddx, w.ddy, w.gx, w.gy, N, P, n, w.inv_gamma,
+                                       st->variant == KB_SB_ISOTROPIC, w.active},
+                            w.mr, w.red, 4, s);
+            KB_CUDA(cudaMemcpyAsync(hp, w.red, sizeof(double) * 4 * B, cudaMemcpyDeviceToHost, s));
+            KB_CUDA(cudaStreamSynchronize(s));
+            bool changed = false;
+            for (int p = 0; p < B; ++p) {
+                if (!active[p]) continue;
+                const double* r = hp + 4 * p;
+                st->outer_iters_host[p]++;
+                if (st->cgls_iters_host) st->cgls_iters_host[(int64_t)p * st->l_max + l] = hctl[p * C_COUNT + C_ITERS];
+                if (r[1] == 0.0) {
+                    set_error("relative_change is undefined for a zero previous iterate (problem %d)", p);
+                    throw Fail{KB_EVALIDATION};
+                }
+                const double rc = std::sqrt(r[0]) / std::sqrt(r[1]);
+                if (st->rc_host) st->rc_host[(int64_t)p * st->l_max + l] = rc;
+                if (x_true) {
+                    const double err = std::sqrt(r[2]);
+                    if (st->re_host) st->re_host[(int64_t)p * st->l_max + l] = err / xt_norm;
+                    double isnr;
+                    if (err == 0.0 && obs == 0.0) isnr = 0.0;
+                    else if (err == 0.0) isnr = INFINITY;
+                    else if (obs == 0.0) isnr = -INFINITY;
+                    else isnr = 20.0 * std::log10(obs / err);
+                    if (st->isnr_host) st->isnr_host[(int64_t)p * st->l_max + l] = isnr;
+                }
+                if (rc < st->tau) {   // converged: its result is this outer iterate (x_prev after the swap)
+                    st->stop_host[p] = KB_SB_CONVERGED;
+                    KB_CUDA(cudaMemcpyAsync(x + (int64_t)p * N, xcur + (int64_t)p * N, sizeof(double) * N,
+                                            cudaMemcpyDeviceToDevice, s));
+                    active[p] = 0;
+                    hact[p] = 0;
+                    --n_active;
+                    changed = true;
+                }
+            }
+            std::swap(xprev, xcur);
+            if (changed) KB_CUDA(cudaMemcpyAsync(w.active, hact, sizeof(int) * B, cudaMemcpyHostToDevice, s));
+        }
+        // problems that ran to l_max: result = x_prev
+        for (int p = 0; p < B; ++p)
+            if (active[p])
+                KB_CUDA(cudaMemcpyAsync(x + (int64_t)p * N, xprev + (int64_t)p * N, sizeof(double) * N,
+                                        cudaMemcpyDeviceToDevice, s));
+        KB_CUDA(cudaStreamSynchronize(s));
+    })
 }

@@ -186,14 +186,111 @@ def lambda_grid(lam_lo: float, lam_hi: float, count: int = 100) -> np.ndarray:
     return np.logspace(np.log10(lam_lo), np.log10(lam_hi), count)
 
 
-def sweep(op, b, gamma: float, lam_lo: float, lam_hi: float, count: int = 100, x_true=None, **config_kwargs):
-    """lambda sweep at fixed gamma (splitbregman.py:195-235); each point on the GPU."""
+def sb_run_batch(op, b, configs, x_true=None) -> list:
+    """Several SB solves of one observation in lock step (device, one launch per pass).
+
+    ``configs`` are :class:`SbConfig` objects that may differ in ``lam`` /
+    ``beta`` only.  Each result equals ``sb_run(op, b, config, x_true)`` of its
+    config (splitbregman.py:120-192); the Kronecker products of all problems
+    run as one pair of batched DMMA GEMMs (``kb_sb_run_batch``).  Dense
+    operators are solved one after another with :func:`sb_run`.
+    """
+    from . import device as D
+
+    configs = list(configs)
+    if not configs:
+        return []
+    c0 = configs[0]
+    for c in configs[1:]:
+        if (c.variant, c.tau, c.l_max, c.cgls.i_max, c.cgls.tau, c.warm_start) != \
+                (c0.variant, c0.tau, c0.l_max, c0.cgls.i_max, c0.cgls.tau, c0.warm_start):
+            raise ValidationError("batched configs may differ in lam / beta only")
+    op = _device_forward(op)
+    fw = op.forward_struct()
+    if fw.kind != _lib.KB_FWD_KRON:
+        return [sb_run(op, b, c, x_true=x_true) for c in configs]
+    m_rows, n_cols = op.shape
+    if m_rows != n_cols:
+        raise ValidationError(f"operator must be square to start from the observed image, got {op.shape}")
+    n = int(round(np.sqrt(n_cols)))
+    if n * n != n_cols:
+        raise ValidationError(f"operator size {n_cols} is not a perfect square")
+    host = not D.is_tensor(b)
+    bd = D.to_device(np.asarray(b, dtype=np.float64).ravel() if host else b, np.float64).reshape(-1)
+    if bd.numel() != n_cols:
+        raise ValidationError(f"b must have length {n_cols}, got {bd.numel()}")
+    xtd = None
+    if x_true is not None:
+        xtd = D.to_device(np.asarray(x_true, dtype=np.float64).ravel() if not D.is_tensor(x_true) else x_true,
+                          np.float64).reshape(-1)
+        if xtd.numel() != n_cols:
+            raise ValidationError(f"x_true must have length {n_cols}, got {xtd.numel()}")
+    B, L = len(configs), c0.l_max
+    lam = np.array([float(c.lam) for c in configs])
+    beta = np.array([float(c.beta) for c in configs])
+    outer = np.zeros(B, dtype=np.int32)
+    stop = np.zeros(B, dtype=np.int32)
+    rc, re, isnr = np.zeros((B, L)), np.zeros((B, L)), np.zeros((B, L))
+    it = np.zeros((B, L), dtype=np.int32)
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int)
+    st = _lib.KbSbBatch()
+    st.nprob = B
+    st.lam_host, st.beta_host = lam.ctypes.data_as(dp), beta.ctypes.data_as(dp)
+    st.variant = _lib.KB_SB_ISOTROPIC if c0.variant == VARIANT_ISOTROPIC else _lib.KB_SB_ANISOTROPIC
+    st.tau, st.l_max = float(c0.tau), L
+    st.i_max, st.tau_cgls = c0.cgls.i_max, float(c0.cgls.tau)
+    st.warm_start = 1 if c0.warm_start else 0
+    st.outer_iters_host, st.stop_host = outer.ctypes.data_as(ip), stop.ctypes.data_as(ip)
+    st.rc_host, st.re_host, st.isnr_host = rc.ctypes.data_as(dp), re.ctypes.data_as(dp), isnr.ctypes.data_as(dp)
+    st.cgls_iters_host = it.ctypes.data_as(ip)
+    x = D.empty((B, n_cols), np.float64)
+    lib = _lib.load()
+    nb = C.c_size_t()
+    _lib.check(lib.kb_sb_batch_workspace_bytes(C.byref(fw), B, C.byref(nb)))
+    ws, wsb = D.WORKSPACE.get(nb.value)
+    _lib.check(lib.kb_sb_run_batch(C.byref(fw), bd.data_ptr(), None if xtd is None else xtd.data_ptr(),
+                                   x.data_ptr(), C.byref(st), ws, wsb, D.stream_ptr()), "sb_run_batch")
+    xs = D.to_host(x) if host else x
+    out = []
+    for p in range(B):
+        k = int(outer[p])
+        res = SbResult(x=xs[p], outer_iters=k, stop=_lib.SB_STOPS[int(stop[p])],
+                       rc_history=[float(v) for v in rc[p, :k]], cgls_iters=[int(v) for v in it[p, :k]])
+        if x_true is not None:
+            res.re_history = [float(v) for v in re[p, :k]]
+            res.isnr_history = [float(v) for v in isnr[p, :k]]
+        out.append(res)
+    return out
+
+
+def _batch_size(op, count: int) -> int:
+    """Problems per batched launch: all of them, within ~24 GB of device workspace."""
+    n_cols = op.shape[1]
+    k = getattr(op, "k", 1)
+    per = 8 * n_cols * (20 + 2 * k)   # stacked CGLS/SB state + Kronecker intermediate
+    return max(1, min(count, int(24e9 // per)))
+
+
+def sweep(op, b, gamma: float, lam_lo: float, lam_hi: float, count: int = 100, x_true=None, batch=None,
+          **config_kwargs):
+    """lambda sweep at fixed gamma (splitbregman.py:195-235).
+
+    The grid points are independent SB problems sharing the factors; they run
+    in lock step through :func:`sb_run_batch` (``batch`` problems per launch,
+    default: as many as fit), so every Kronecker product is one batched GEMM
+    pair over the whole grid instead of ``count`` small ones.
+    """
+    grid = lambda_grid(lam_lo, lam_hi, count)
+    configs = [SbConfig.from_gamma(float(lam), gamma, **config_kwargs) for lam in grid]
+    dop = _device_forward(op)
+    step = int(batch) if batch else _batch_size(dop, len(configs))
+    results = []
+    for i in range(0, len(configs), step):
+        results += sb_run_batch(dop, b, configs[i:i + step], x_true=x_true)
     records = []
-    for lam in lambda_grid(lam_lo, lam_hi, count):
-        config = SbConfig.from_gamma(float(lam), gamma, **config_kwargs)
-        res = sb_run(op, b, config, x_true=x_true)
+    for config, res in zip(configs, results):
         records.append({
-            "lam": float(lam), "beta": config.beta,
+            "lam": float(config.lam), "beta": config.beta,
             "re": res.re_history[-1] if res.re_history else float("nan"),
             "isnr_db": res.isnr_history[-1] if res.isnr_history else float("nan"),
             "outer_iters": res.outer_iters, "iota_total": res.iota_total,

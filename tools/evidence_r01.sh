@@ -1,0 +1,9 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r01.json 2> gpurun_out/bench_r01.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_r01.json 2> gpurun_out/bench_ref_r01.err
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+python tools/one_egkb.py 1024 > gpurun_out/one.log 2>&1 && timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_egkb_persistent -s 1 -c 1 -o gpurun_out/prof_egkb_r01 python tools/one_egkb.py 1024 > gpurun_out/ncu_egkb.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_zig -c 1 -o gpurun_out/prof_zig_r01 python tools/rng_one.py 1048576 > gpurun_out/ncu_zig.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ra_block -s 2 -c 1 -o gpurun_out/prof_rablock_r01 python tools/ra_probe.py > gpurun_out/ncu_ra.log 2>&1
+ls -la gpurun_out
