@@ -47,6 +47,7 @@ typedef void* kb_stream_t; /* cudaStream_t */
 #define KB_OP_RA_ZERO 1 /* matrix-free R(A) of a zero-BC PSF blur (new)      */
 #define KB_OP_RA_REFLEXIVE 2 /* matrix-free R(A), reflexive BC (blurmodel.py:80-84,
                                 122-126): Toeplitz + two Hankel index families */
+#define KB_OP_SPARSE 3  /* R(A) of an unstructured sparse A (CSR of R and R^T)  */
 
 /* eGKB stop reasons (lowrank.py:26-29) */
 #define KB_STOP_NU_ROSE 1
@@ -78,7 +79,7 @@ int kb_prof_query(int cls, double* ms, long long* launches, double* bytes, doubl
 /* Operators B for eGKB / RSVD                                        */
 /* ------------------------------------------------------------------ */
 typedef struct {
-    int kind;          /* KB_OP_DENSE, KB_OP_RA_ZERO or KB_OP_RA_REFLEXIVE  */
+    int kind;          /* KB_OP_DENSE, KB_OP_RA_ZERO/_REFLEXIVE, KB_OP_SPARSE */
     int dtype;         /* KB_F32 / KB_F64: working precision               */
     int64_t rows;      /* mbar                                             */
     int64_t cols;      /* nbar                                             */
@@ -88,6 +89,16 @@ typedef struct {
     const void* kt;    /* RA: the same kernel transposed (kw x kh)         */
     int kh, kw;        /* RA: PSF support (odd; centre kh/2, kw/2)          */
     int side;          /* RA: image side n (rows = cols = n*n)             */
+    /* SPARSE: R(A) of an unstructured sparse A as CSR of R (rows x cols)
+     * and of R^T (cols x rows): row pointers (rows+1 / cols+1), int32 column
+     * indices, values in dtype.  rearrange.py:67-75 applied to the nonzeros. */
+    const int64_t* sp_rowptr;
+    const int* sp_col;
+    const void* sp_val;
+    const int64_t* spt_rowptr;
+    const int* spt_col;
+    const void* spt_val;
+    int64_t nnz;
 } kb_operator;
 
 /* Workspace for kb_op_apply / kb_egkb_run / kb_rsvd helpers. */

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 KB_OK, KB_EVALIDATION, KB_ENUMERICAL, KB_ERUNTIME = 0, 2, 3, 4
 KB_F32, KB_F64 = 0, 1
-KB_OP_DENSE, KB_OP_RA_ZERO, KB_OP_RA_REFLEXIVE = 0, 1, 2
+KB_OP_DENSE, KB_OP_RA_ZERO, KB_OP_RA_REFLEXIVE, KB_OP_SPARSE = 0, 1, 2, 3
 KB_STOP = {1: "nu_rose", 2: "nu_below_tol", 3: "hit_kmax", 4: "breakdown"}
 KB_FWD_DENSE, KB_FWD_KRON = 0, 1
 KB_SB_ANISOTROPIC, KB_SB_ISOTROPIC = 0, 1
@@ -34,7 +34,9 @@ ip = C.POINTER(C.c_int)
 class KbOperator(C.Structure):
     _fields_ = [("kind", C.c_int), ("dtype", C.c_int), ("rows", i64), ("cols", i64),
                 ("a", vp), ("lda", i64), ("k", vp), ("kt", vp),
-                ("kh", C.c_int), ("kw", C.c_int), ("side", C.c_int)]
+                ("kh", C.c_int), ("kw", C.c_int), ("side", C.c_int),
+                ("sp_rowptr", vp), ("sp_col", vp), ("sp_val", vp), ("spt_rowptr", vp), ("spt_col", vp),
+                ("spt_val", vp), ("nnz", i64)]
 
 
 class KbEgkbConfig(C.Structure):

@@ -130,6 +130,10 @@ static void validate_op(const kb_operator* op) {
         // blurmodel.py:100-101: one reflection must cover the support
         KB_REQUIRE(op->kind == KB_OP_RA_ZERO || (op->kh <= 2 * op->side - 1 && op->kw <= 2 * op->side - 1),
                    "PSF support too large for single reflection at this image size");
+    } else if (op->kind == KB_OP_SPARSE) {
+        KB_REQUIRE(op->sp_rowptr && op->sp_col && op->sp_val && op->spt_rowptr && op->spt_col && op->spt_val,
+                   "sparse operator needs the CSR arrays of R and R^T");
+        KB_REQUIRE(op->nnz >= 0 && op->rows < (1ll << 31) && op->cols < (1ll << 31), "bad sparse operator");
     } else {
         KB_REQUIRE(op->kind == KB_OP_DENSE, "unknown operator kind %d", op->kind);
         KB_REQUIRE(op->a != nullptr && op->lda >= op->cols, "bad dense operator");

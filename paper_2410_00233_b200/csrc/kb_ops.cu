@@ -157,6 +157,24 @@ k_rowdot(const T* __restrict__ A, int64_t lda, int rows, int cols, const VecRef 
     if (lane == 0) z[r] = acc;
 }
 
+// z[r] = sum_j val[j] x[col[j]] over CSR row r (R(A) of a sparse A):
+// one warp per row, lane-strided then a fixed shuffle tree -> deterministic.
+// HBM-bound: 12 B per nonzero (value + index) + the gathered x.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_csr_rows(const int64_t* __restrict__ rowptr, const int* __restrict__ col, const T* __restrict__ val,
+           const VecRef xr, double* __restrict__ z, int64_t rows) {
+    const T* __restrict__ x = resolve<const T>(xr);
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * 8) {
+        const int64_t b = rowptr[r], e = rowptr[r + 1];
+        double acc = 0.0;
+        for (int64_t j = b + lane; j < e; j += 32) acc += (double)__ldg(val + j) * (double)__ldg(x + __ldg(col + j));
+        acc = warp_sum(acc);
+        if (lane == 0) z[r] = acc;
+    }
+}
+
 // ------------------------------------------------------------------ sources
 template <typename T>
 struct Gen {
@@ -429,6 +447,11 @@ void op_plan_size(const kb_operator* op, Sizer& s) {
         s.take<double>(L);                              // z
         s.take<unsigned>(2 * 64 + 64);
         (void)n;
+    } else if (op->kind == KB_OP_SPARSE) {
+        const int64_t big = op->rows > op->cols ? op->rows : op->cols;
+        s.take<double>(64);
+        s.take<double>(big);                            // z
+        s.take<unsigned>(64);
     } else {
         const int64_t big = op->rows > op->cols ? op->rows : op->cols;
         s.take<double>((size_t)(4 * kSMs) * big);       // colsum partials (upper bound)
@@ -450,6 +473,13 @@ OpPlan op_plan_make(const kb_operator* op, Arena& a) {
         p.counters = a.take<unsigned>(2 * 64 + 64);
         p.n_counters = 2 * 64 + 64;
         p.z_len = L;
+    } else if (op->kind == KB_OP_SPARSE) {
+        const int64_t big = op->rows > op->cols ? op->rows : op->cols;
+        p.part = a.take<double>(64);
+        p.z = a.take<double>(big);
+        p.counters = a.take<unsigned>(64);
+        p.n_counters = 64;
+        p.z_len = big;
     } else {
         const int64_t big = op->rows > op->cols ? op->rows : op->cols;
         p.part = a.take<double>((size_t)(4 * kSMs) * big);
@@ -501,6 +531,17 @@ static Src op_source_t(const OpPlan& p, const VecRef& x, int transpose, cudaStre
         s.side = n;
         s.center = co;
         s.L = Lo;
+    } else if (op->kind == KB_OP_SPARSE) {
+        const int64_t rows = transpose ? op->cols : op->rows;
+        const int64_t* rp = transpose ? op->spt_rowptr : op->sp_rowptr;
+        const int* ci = transpose ? op->spt_col : op->sp_col;
+        const T* va = static_cast<const T*>(transpose ? op->spt_val : op->sp_val);
+        const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(rows, 8), 16 * kSMs);
+        ProfScope ps(st, PROF_RA_COLSUM, (double)op->nnz * (sizeof(T) + 4) + 8.0 * (rows + 1) + 8.0 * rows);
+        k_csr_rows<T><<<blocks, 256, 0, st>>>(rp, ci, va, x, p.z, rows);
+        KB_LAUNCH_CHECK();
+        s.z = VecRef::at(p.z);
+        s.mode = SRC_BUF64;
     } else {
         const T* A = static_cast<const T*>(op->a);
         if (!transpose) {

@@ -20,6 +20,7 @@ import numpy as np
 
 from . import _lib, rng
 from .blurmodel import RearrangedBlur
+from .sparse import RearrangedSparse
 from .exceptions import NumericalError, ValidationError
 from .linalg import TruncatedSvd, eps_for, orthonormalize_device, precision_of, svd_small
 
@@ -129,8 +130,8 @@ class _EngineOp:
         from . import device as D
 
         self.keep = None
-        if isinstance(b_mat, RearrangedBlur):
-            self.kind = "ra"
+        if isinstance(b_mat, (RearrangedBlur, RearrangedSparse)):
+            self.kind = "ra" if isinstance(b_mat, RearrangedBlur) else "sparse"
             self.blur = b_mat
             self.dtype = b_mat.dtype
             self.shape = b_mat.shape
@@ -326,9 +327,9 @@ def rsvd(b_mat, config: RsvdConfig) -> TruncatedSvd:
     op = _EngineOp(b_mat)
     mbar, nbar = op.shape
     if mbar < nbar:
-        if op.kind != "dense":
+        if op.kind == "ra":
             raise ValidationError("wide matrix-free operators are not supported")
-        inner = rsvd(op.mat.t().contiguous(), config)
+        inner = rsvd(op.blur.T if op.kind == "sparse" else op.mat.t().contiguous(), config)
         return TruncatedSvd.from_device(inner.v_device, inner.sigma, inner.u_device)
     k_p = config.k + config.p
     if k_p > nbar:

@@ -2,9 +2,9 @@
 
 Run in the build container only (needs /root/reference):
 
-    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py [reflexive]
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py [reflexive|sparse]
 
-(``reflexive`` regenerates only ra_reflexive.npz.)
+(``reflexive`` / ``sparse`` regenerate only ra_reflexive.npz / ra_sparse.npz.)
 
 Writes ``tests/golden/*.npz``.  Every array in them is an input or an output
 of the unmodified reference package ``kronblur`` (``pkg/src/kronblur``); the
@@ -256,9 +256,40 @@ def reflexive():
     save("ra_reflexive", **rf)
 
 
+def sparse():
+    """R(A) of unstructured sparse A (rearrange.py:67-75) and the reference engines on it."""
+    rng = np.random.default_rng(31337)
+    sp = {}
+    # 1. random sparse A, non-square block scheme
+    scheme = BlockScheme(6, 5, 4, 7)
+    a = rng.standard_normal(scheme.shape) * (rng.random(scheme.shape) < 0.12)
+    sp["s1_a"], sp["s1_scheme"] = a, np.array([6, 5, 4, 7])
+    r = rearrange(a, scheme)
+    sp["s1_R"] = r
+    for tag, mat in (("d", r), ("s", cast(r, "single"))):
+        cfg = dict(k_max=6, p=2, tau=1e-30, k_min=6, seed=4)
+        egkb_case(f"s1{tag}_", mat, cfg, sp)
+    svd = rsvd(r, RsvdConfig(k=4, p=3, q=2, seed=6))
+    sp["s1_rsvd_sigma"], sp["s1_rsvd_u"], sp["s1_rsvd_v"] = svd.sigma, svd.u, svd.v
+    # 2. spatially variant blur: PSF blur + sparse random couplings, n = 16
+    n = 16
+    a = build_blur_matrix(Psf(rng.random((5, 5))), n)
+    extra = (rng.random(a.shape) < 0.002) * rng.random(a.shape) * 0.05
+    a = a + extra
+    sp["s2_a"], sp["s2_n"] = a, n
+    r = rearrange(a, BlockScheme.square_image(n))
+    sp["s2_R"] = r
+    egkb_case("s2s_", cast(r, "single"), dict(k_max=12, tau=1e-4), sp)
+    egkb_case("s2d_", r, dict(k_max=8, k_min=8, p=2, tau=1e300), sp)
+    save("ra_sparse", **sp)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["reflexive"]:
         reflexive()
+    elif sys.argv[1:] == ["sparse"]:
+        sparse()
     else:
         main()
         reflexive()
+        sparse()

@@ -207,3 +207,39 @@ def test_sb_bit_identical():
                          i_max=100, tau_cgls=1e-4, x_true=g["n64_xtrue"])
         np.testing.assert_array_equal(res.x, g[f"n64_{variant}_cfg_x"])
         assert res.cgls_iters == list(g[f"n64_{variant}_cfg_iters"])
+
+
+class TestSparseRearrangement:
+    """the host permutation of sparse entries equals rearrange.py:67-75."""
+
+    def test_permutation_matches_reference(self):
+        from paper_2410_00233_b200 import BlockScheme, RearrangedSparse
+
+        g = load_golden("ra_sparse")
+        m1, m2, n1, n2 = (int(v) for v in g["s1_scheme"])
+        op = RearrangedSparse(g["s1_a"], BlockScheme(m1, m2, n1, n2), dtype=np.float64)
+        assert op.shape == g["s1_R"].shape
+        np.testing.assert_array_equal(op.to_dense(), g["s1_R"])
+        n = int(g["s2_n"])
+        op2 = RearrangedSparse(g["s2_a"], BlockScheme.square_image(n))
+        np.testing.assert_array_equal(op2.to_dense(), g["s2_R"])
+        np.testing.assert_array_equal(op.T.to_dense(), g["s1_R"].T)
+
+    def test_csr_builder_sums_duplicates(self):
+        from paper_2410_00233_b200.sparse import _csr
+
+        rows = np.array([2, 0, 2, 1, 2])
+        cols = np.array([1, 3, 1, 0, 0])
+        vals = np.array([1.0, 2.0, 3.0, 4.0, 5.0])
+        rp, ci, va = _csr(rows, cols, vals, 4)
+        assert rp.tolist() == [0, 1, 2, 4, 4]
+        assert ci.tolist() == [3, 0, 0, 1]
+        assert va.tolist() == [2.0, 4.0, 5.0, 4.0]
+
+    def test_validation(self):
+        from paper_2410_00233_b200 import BlockScheme, RearrangedSparse, ValidationError
+
+        with pytest.raises(ValidationError):
+            RearrangedSparse(np.ones((6, 6)), BlockScheme(2, 2, 2, 2))
+        with pytest.raises(ValidationError):
+            RearrangedSparse(([0], [9], [1.0], (4, 4)), BlockScheme(2, 2, 2, 2))
