@@ -4,7 +4,8 @@ Run in the build container only (needs /root/reference):
 
     PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py [reflexive|sparse]
 
-(``reflexive`` / ``sparse`` regenerate only ra_reflexive.npz / ra_sparse.npz.)
+(``reflexive`` / ``sparse`` / ``cli`` regenerate only ra_reflexive.npz /
+ra_sparse.npz / the io+cli file fixtures under tests/golden/io and tests/golden/cli.)
 
 Writes ``tests/golden/*.npz``.  Every array in them is an input or an output
 of the unmodified reference package ``kronblur`` (``pkg/src/kronblur``); the
@@ -284,8 +285,84 @@ def sparse():
     save("ra_sparse", **sp)
 
 
+def cli_io():
+    """File formats written by the reference's io.py, and reference CLI runs
+    (approx -> deblur -> sweep) on a small PSF problem, for the f4 parity tests."""
+    import shutil
+
+    from kronblur import io as rio
+    from kronblur.cli import main as ref_cli
+    from kronblur.kronop import KroneckerSum
+
+    rng = np.random.default_rng(777)
+    iod = os.path.join(HERE, "io")
+    shutil.rmtree(iod, ignore_errors=True)
+    os.makedirs(iod)
+    with open(os.path.join(iod, "opts.cfg"), "w") as fh:
+        fh.write("# defaults\nk-max = 12   # cap\n\nprec=single\n tau-egkb = 1e-6\n")
+    m64, m32, v6 = rng.standard_normal((5, 7)), rng.standard_normal((3, 4)).astype(np.float32), rng.standard_normal(6)
+    rio.write_mtx(os.path.join(iod, "m64.mtx"), m64)
+    rio.write_mtx(os.path.join(iod, "m32.mtx"), m32)
+    rio.write_mtx(os.path.join(iod, "vec.mtx"), v6)
+    img = rng.random((9, 11))
+    img[0, 0], img[1, 1] = -0.2, 1.3           # clipped
+    rio.write_pgm(os.path.join(iod, "img8.pgm"), img, 8)
+    rio.write_pgm(os.path.join(iod, "img16.pgm"), img, 16)
+    with open(os.path.join(iod, "comment.pgm"), "wb") as fh:   # header comments are legal PGM
+        fh.write(b"P5\n# made by hand\n3 2\n# depth\n255\n" + bytes([0, 128, 255, 1, 2, 3]))
+    np.savez(os.path.join(iod, "expected.npz"), m64=m64, m32=m32, vec=v6, img=img,
+             img8=rio.read_pgm(os.path.join(iod, "img8.pgm")), img16=rio.read_pgm(os.path.join(iod, "img16.pgm")),
+             comment=rio.read_pgm(os.path.join(iod, "comment.pgm")))
+    with open(os.path.join(iod, "opts.json"), "w") as fh:   # what the reference's read_config returns
+        json.dump(rio.read_config(os.path.join(iod, "opts.cfg")), fh)
+    op = KroneckerSum([rng.standard_normal((3, 2)) for _ in range(2)], [rng.standard_normal((4, 5)) for _ in range(2)],
+                      BlockScheme(3, 4, 2, 5))
+    rio.save_kron_dir(op, os.path.join(iod, "kron"), extra_meta={"engine": "egkb", "k_p": 4, "rho": 1.0})
+    rio.write_json(os.path.join(iod, "payload.json"), {"a": [1.5, float("inf"), float("nan")], "b": np.int64(3),
+                                                     "c": {"d": -float("inf")}, "e": np.arange(3)})
+
+    # reference CLI: simulate inputs are made here (numpy), then approx / deblur / sweep
+    cli = os.path.join(HERE, "cli")
+    shutil.rmtree(cli, ignore_errors=True)
+    os.makedirs(cli)
+    n = 16
+    psf = Psf(np.pad(rng.random((5, 5)) + 0.1, ((0, 0), (0, 0))))
+    rio.write_mtx(os.path.join(cli, "psf.mtx"), psf.kernel)
+    x_img = make_test_image(n)
+    a = build_blur_matrix(psf, n)
+    b = a @ vec(x_img)
+    b = b + 0.002 * np.random.default_rng(3).standard_normal(b.shape)
+    rio.write_pgm(os.path.join(cli, "observed.pgm"), b.reshape(n, n, order="F"), 16)
+    rio.write_pgm(os.path.join(cli, "truth.pgm"), x_img, 16)
+    rio.write_mtx(os.path.join(cli, "matrix.mtx"), a)
+    runs = {
+        "approx_single": ["approx", "--psf", "psf.mtx", "--side", str(n), "--prec", "single", "--k-max", "10"],
+        "approx_double": ["approx", "--psf", "psf.mtx", "--side", str(n), "--k-max", "8", "--k-min", "8",
+                          "--tau-egkb", "1e300"],
+        "approx_rsvd": ["approx", "--matrix", "matrix.mtx", "--engine", "rsvd", "--k", "3", "--p", "1", "--q", "2"],
+    }
+    cwd = os.getcwd()
+    os.chdir(cli)
+    try:
+        for name, argv in runs.items():
+            assert ref_cli(argv + ["--out-dir", name]) == 0, name
+        assert ref_cli(["deblur", "--operator-dir", "approx_double/operator", "--observed", "observed.pgm",
+                        "--truth", "truth.pgm", "--lam", "0.1", "--gamma", "2.0", "--l-max", "5", "--tau-sb", "0",
+                        "--i-max", "20", "--tau-cgls", "0", "--out-dir", "deblur"]) == 0
+        assert ref_cli(["sweep", "--operator-dir", "approx_double/operator", "--observed", "observed.pgm",
+                        "--truth", "truth.pgm", "--count", "4", "--lam-min", "0.02", "--lam-max", "0.5",
+                        "--l-max", "3", "--tau-sb", "0", "--i-max", "20", "--tau-cgls", "0", "--out-dir", "sweep"]) == 0
+        assert ref_cli(["approx", "--psf", "psf.mtx", "--side", "0", "--out-dir", "bad"]) == 2
+    finally:
+        os.chdir(cwd)
+    shutil.rmtree(os.path.join(cli, "bad"), ignore_errors=True)
+    print("wrote", iod, cli)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["reflexive"]:
+    if sys.argv[1:] == ["cli"]:
+        cli_io()
+    elif sys.argv[1:] == ["reflexive"]:
         reflexive()
     elif sys.argv[1:] == ["sparse"]:
         sparse()
@@ -293,3 +370,4 @@ if __name__ == "__main__":
         main()
         reflexive()
         sparse()
+        cli_io()
