@@ -411,35 +411,51 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     }
     grid.sync();
     pk_mark(P);
-    // ---- q1 = B^T s1 / alpha1   (lowrank.py:211-215)
-    double ysq = 0.0;
-    PkHalf<T> h1{S, nullptr, T(0), Q, P.ld_q, 0, Q, 1};
-    const double a1 = pk_half<T, VEC, MAXG>(P, h1, sm, ysq, grid);
-
+    // ---- the half steps, ONE call site of pk_half (one inlined copy: the
+    // kernel's instruction footprint is a third of three separate calls):
+    //   step 0      : q1 = B^T s1 / alpha1                    (lowrank.py:211-215)
+    //   odd steps   : s step, s_{j+1} = B q_j - alpha_j s_j   (lowrank.py:237-247)
+    //   even steps  : q step, q_{j+1} = B^T s_{j+1} - t q_j   (lowrank.py:249-260) + control
     int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
     int na = 1, nt = 1, nn = 1;
-    double zeta_last = a1 * t1, nu_last = 1e308, alpha_cur = a1;
-    if (rec) {
-        P.ts[0] = t1;
-        P.alphas[0] = a1;
-        P.zetas[0] = zeta_last;
-        P.nus[0] = nu_last;
-    }
-    if (t1 == 0.0) err = 1;
-    else if (a1 == 0.0) err = 2;
-    if (err) stop = 1;
-
-    while (!stop) {
-        // s step (lowrank.py:237-247)
-        PkHalf<T> hs{Q + (int64_t)(done - 1) * P.ld_q, S + (int64_t)(done - 1) * P.ld_s, (T)alpha_cur, S, P.ld_s,
-                     P.full_reorth ? done : 0, S + (int64_t)done * P.ld_s, 0};
-        double u2 = 0.0;
-        const double t_new = pk_half<T, VEC, MAXG>(P, hs, sm, u2, grid);
-        // q step (lowrank.py:249-260)
-        PkHalf<T> hq{S + (int64_t)done * P.ld_s, Q + (int64_t)(done - 1) * P.ld_q, (T)t_new, Q, P.ld_q, done,
-                     Q + (int64_t)done * P.ld_q, 1};
-        double p2 = 0.0;
-        const double a_new = pk_half<T, VEC, MAXG>(P, hq, sm, p2, grid);
+    double zeta_last = 0.0, nu_last = 1e308, alpha_cur = 0.0, t_new = 0.0, u2 = 0.0;
+    for (int step = 0;; ++step) {
+        PkHalf<T> h;
+        if (step == 0) {
+            h = PkHalf<T>{S, nullptr, T(0), Q, P.ld_q, 0, Q, 1};
+        } else if (step & 1) {
+            h = PkHalf<T>{Q + (int64_t)(done - 1) * P.ld_q, S + (int64_t)(done - 1) * P.ld_s, (T)alpha_cur, S, P.ld_s,
+                          P.full_reorth ? done : 0, S + (int64_t)done * P.ld_s, 0};
+        } else {
+            h = PkHalf<T>{S + (int64_t)done * P.ld_s, Q + (int64_t)(done - 1) * P.ld_q, (T)t_new, Q, P.ld_q, done,
+                          Q + (int64_t)done * P.ld_q, 1};
+        }
+        double aux = 0.0;
+        const double val = pk_half<T, VEC, MAXG>(P, h, sm, aux, grid);
+        if (step == 0) {
+            const double a1 = val;
+            zeta_last = a1 * t1;
+            alpha_cur = a1;
+            if (rec) {
+                P.ts[0] = t1;
+                P.alphas[0] = a1;
+                P.zetas[0] = zeta_last;
+                P.nus[0] = nu_last;
+            }
+            if (t1 == 0.0) err = 1;
+            else if (a1 == 0.0) err = 2;
+            if (err) {
+                stop = 1;
+                break;
+            }
+            continue;
+        }
+        if (step & 1) {
+            t_new = val;
+            u2 = aux;
+            continue;
+        }
+        const double a_new = val, p2 = aux;
         // control (identical in every CTA; CTA 0 records the trace)
         if (t_new <= P.tol * sqrt(u2)) {
             breakdown = tbreak = 1;
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
                 overflow = 1;
             }
         }
+        if (stop) break;
     }
     if (rec) {
         int* h = P.hdr;
