@@ -177,6 +177,11 @@ int kb_egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const void* y0
                 kb_egkb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
 int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
 
+/* dst = (dtype)(src / divisor), device: the Psf normalisation k / k.sum()
+ * (blurmodel.py:25-65) fused with the working-precision cast -- bitwise
+ * numpy's (k / total).astype(dtype). */
+int kb_div_cast(const double* src, double divisor, int dtype, void* dst, int64_t count, kb_stream_t stream);
+
 /* dst (cols x rows) = src (rows x cols)^T, row-major, device.  Builds the
  * PSF transpose K^T used by the R(A)^T products on the device (the host
  * uploads K once; blurmodel.py:25-65 Psf.kernel). */

@@ -23,34 +23,85 @@ BOUNDARY_CONDITIONS = (BC_ZERO, BC_REFLEXIVE)
 DENSE_SIDE_CAP = 200   # blurmodel.py:22
 
 
-@dataclass
+_POOL = None
+
+
+def _min(k: np.ndarray) -> float:
+    """k.min() (order-independent, so large kernels are reduced by row blocks in parallel threads)."""
+    if k.size < (1 << 18) or k.ndim != 2 or not k.flags.c_contiguous:
+        return k.min()
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(8)
+    cuts = np.linspace(0, k.shape[0], 9).astype(int)
+    parts = _POOL.map(lambda i: k[cuts[i]:cuts[i + 1]].min() if cuts[i + 1] > cuts[i] else np.inf, range(8))
+    return min(parts)
+
+
 class Psf:
-    """Unit-sum, non-negative PSF with odd support (blurmodel.py:25-65)."""
+    """Unit-sum, non-negative PSF with odd support (blurmodel.py:25-65).
 
-    kernel: np.ndarray
+    Validation and the mass are computed eagerly, exactly as the reference
+    (same checks, same pairwise sum over the C-ordered float64 array); the
+    normalised float64 ``kernel`` is materialised on first access.  The device
+    operator uploads the raw kernel once and normalises + casts it there
+    (``kb_div_cast``), so the host makes no normalised or fp32 copy.
+    """
 
-    def __post_init__(self):
-        k = np.array(self.kernel, dtype=np.float64)   # own copy (normalised in place below)
+    __slots__ = ("_raw", "_total", "_kernel")
+
+    def __init__(self, kernel):
+        k = np.asarray(kernel, dtype=np.float64)
         if k.ndim != 2:
             raise ValidationError("PSF kernel must be 2-D")
         if k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
             raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
-        if k.size == 0 or not k.min() >= 0:          # one reduction; the exact test only when it fails
+        if not (k.flags.c_contiguous or k.flags.f_contiguous):
+            k = np.array(k)                           # the reference's order-'K' copy: same reduction order
+        if k.size == 0 or not _min(k) >= 0:          # one reduction; the exact test only when it fails
             if np.any(k < 0):
                 raise ValidationError("PSF kernel must be non-negative")
         total = k.sum()
         if total <= 0:
             raise ValidationError("PSF kernel must have positive mass")
-        k /= total                                    # bitwise identical to k / total
-        self.kernel = k
+        self._raw, self._total, self._kernel = k, total, None
+
+    @property
+    def kernel(self) -> np.ndarray:
+        if self._kernel is None:
+            self._kernel = self._raw / self._total     # bitwise the reference's k / total
+            self._raw = None
+        return self._kernel
+
+    def device_normalised(self, dtype):
+        """The normalised kernel on the device in ``dtype``: the raw float64 kernel is
+        uploaded as is and divided + cast there (kb_div_cast), so the host never
+        makes a normalised or down-cast copy."""
+        from . import device as D
+
+        if self._kernel is not None:
+            return D.upload(self._kernel, dtype)
+        import torch
+
+        raw = torch.from_numpy(self._raw).to(D.device())
+        out = D.empty(self.shape, dtype)
+        code = _lib.KB_F32 if np.dtype(dtype) == np.float32 else _lib.KB_F64
+        _lib.check(_lib.load().kb_div_cast(raw.data_ptr(), float(self._total), code, out.data_ptr(), raw.numel(),
+                                           D.stream_ptr()), "kb_div_cast")
+        return out
+
+    def __repr__(self) -> str:
+        return f"Psf(shape={self.shape})"
 
     @property
     def center(self) -> tuple[int, int]:
-        return (self.kernel.shape[0] // 2, self.kernel.shape[1] // 2)
+        return (self.shape[0] // 2, self.shape[1] // 2)
 
     @property
     def shape(self) -> tuple[int, int]:
-        return self.kernel.shape
+        return (self._raw if self._kernel is None else self._kernel).shape
 
     def separability_ratio(self) -> float:
         s = np.linalg.svd(self.kernel, compute_uv=False)
@@ -178,8 +229,8 @@ class RearrangedBlur:
         from . import device as D
 
         if self._k is None:
-            # one upload (rounded to the working dtype while staging); K^T is built on the device
-            self._k = D.upload(self.psf.kernel, self.dtype)
+            # one upload of the raw PSF; normalisation, cast and K^T on the device
+            self._k = self.psf.device_normalised(self.dtype)
             kh, kw = self.psf.shape
             self._kt = D.empty((kw, kh), self.dtype)
             code = _lib.KB_F32 if self.dtype == np.float32 else _lib.KB_F64

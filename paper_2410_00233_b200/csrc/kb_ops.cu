@@ -696,6 +696,34 @@ void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int 
 
 }  // namespace kb
 
+// ---------------------------------------------------------------- PSF normalisation
+// dst = (T)(src / divisor): the reference's Psf normalisation k / k.sum()
+// (blurmodel.py:25-65) followed by the working-precision cast, on the device
+// (IEEE division and round-to-nearest cast: bitwise numpy's (k / total).astype(T)).
+namespace kb {
+template <typename T>
+__global__ void __launch_bounds__(256) k_div_cast(const double* __restrict__ src, double divisor, T* __restrict__ dst,
+                                                  int64_t count) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = (T)__ddiv_rn(src[e], divisor);
+}
+}  // namespace kb
+
+extern "C" int kb_div_cast(const double* src, double divisor, int dtype, void* dst, int64_t count, kb_stream_t stream) {
+    using namespace kb;
+    KB_GUARD({
+        KB_REQUIRE(src && dst && count >= 0, "bad arguments");
+        KB_REQUIRE(dtype == KB_F32 || dtype == KB_F64, "dtype must be KB_F32 or KB_F64");
+        if (count == 0) return KB_OK;
+        const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(count, 256), 8 * kSMs);
+        if (dtype == KB_F32)
+            k_div_cast<float><<<blocks, 256, 0, as_stream(stream)>>>(src, divisor, static_cast<float*>(dst), count);
+        else
+            k_div_cast<double><<<blocks, 256, 0, as_stream(stream)>>>(src, divisor, static_cast<double*>(dst), count);
+        KB_LAUNCH_CHECK();
+    })
+}
+
 // ---------------------------------------------------------------- PSF transpose
 // K^T for the column-coalesced R(A)^T products; done on the device so the
 // host uploads the PSF once.

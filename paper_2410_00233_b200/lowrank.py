@@ -200,7 +200,7 @@ def _lift(code, basis, nrows, W, out_rows):
     cols = W.shape[1]
     length = basis.shape[1]
     out = D.empty((cols, length), D.np_dtype(basis))
-    wd = D.to_device(np.ascontiguousarray(W[:nrows]), D.np_dtype(basis))
+    wd = D.upload(np.ascontiguousarray(W[:nrows]), D.np_dtype(basis))   # pinned, stream-ordered
     _lib.check(_lib.load().kb_ts_lift(code, basis.data_ptr(), length, nrows, wd.data_ptr(), cols, out.data_ptr(),
                                       length, length, D.stream_ptr()), "lift")
     return out

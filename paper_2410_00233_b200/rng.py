@@ -10,6 +10,7 @@ identical to the reference while the host never touches n^2 draws.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 
 import numpy as np
 import torch
@@ -18,8 +19,16 @@ from . import _lib
 from . import device as D
 
 
+@functools.lru_cache(maxsize=64)
+def _seeded_state(seed: int) -> tuple[int, int]:
+    st = np.random.PCG64(seed).state["state"]        # SeedSequence hashing: ~50 us, cached
+    return int(st["state"]), int(st["inc"])
+
+
 def pcg64_state(seed) -> tuple[int, int]:
     """(state, inc) of ``np.random.default_rng(seed)``'s PCG64 before any draw."""
+    if isinstance(seed, (int, np.integer)) and not isinstance(seed, bool) and seed >= 0:
+        return _seeded_state(int(seed))
     if isinstance(seed, np.random.Generator):
         bg = seed.bit_generator
     elif isinstance(seed, np.random.BitGenerator):
