@@ -18,6 +18,7 @@ Multi-GPU (torchrun): independent replicas (weak scaling), max-over-ranks time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -217,12 +218,18 @@ def run_ours(args, prob, rank, world, dist):
         return svd, tr, op
 
     # the clock sampler starts before the warm-up so its start-up is outside the timed region
-    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 and not os.environ.get("KB_BENCH_NO_CLOCKS") else None
+    # warm-up exactly like the timed loop (the previous step's results stay alive
+    # while the next step allocates), so the caching allocator holds both sets
     for _ in range(max(args.warmup, 3)):
-        step_resident()
+        svd, tr, op = step_resident()
     torch.cuda.synchronize()
 
-    # ---- timed region (device-resident inputs, graph path), L2 flushed between steps
+    # ---- timed region (device-resident inputs), L2 flushed between steps.  Python's
+    # cyclic GC is collected up front and paused while timing (as timeit does):
+    # a collection inside a step would stall the host between the step's launches.
+    gc.collect()
+    gc.disable()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()
@@ -232,6 +239,7 @@ def run_ours(args, prob, rank, world, dist):
         svd, tr, op = step_resident()
         ev[i][1].record()
         torch.cuda.synchronize()
+    gc.enable()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     t_max = torch.tensor([total_ms], dtype=torch.float64, device=D.device())
@@ -260,8 +268,10 @@ def run_ours(args, prob, rank, world, dist):
 
     # ---- e2e: public API from host arrays, every step
     psf_host = prob.psf
-    h2d = psf_host.size * 4                                     # K once (K^T is built on the device)
+    h2d = psf_host.size * 8                                     # raw fp64 K once (normalised, cast, K^T on device)
     e2e_ms = []
+    gc.collect()
+    gc.disable()
     for i in range(max(args.warmup, 3) + max(args.steps, 1)):
         flush.zero_()
         torch.cuda.synchronize()
@@ -274,6 +284,7 @@ def run_ours(args, prob, rank, world, dist):
         torch.cuda.synchronize()
         if i >= max(args.warmup, 3):               # the first W calls are the e2e warm-up
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    gc.enable()
     iters = len(tr.alphas) + 1
     d2h = 8 * 4 * iters + 16 + sig.nbytes
     h2d += 8 * 2 * (tr.k_p + 1) * tr.chosen_k                  # lift coefficient uploads
@@ -401,7 +412,8 @@ def run_ours(args, prob, rank, world, dist):
     line = {
         "metric": METRIC, "value": value, "unit": "KP-approx/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "step_ms": {"min": float(min(step_ms)), "median": float(np.median(step_ms)), "max": float(max(step_ms))},
+        "step_ms": {"min": float(min(step_ms)), "median": float(np.median(step_ms)), "max": float(max(step_ms)),
+                    "all": [round(float(t), 4) for t in step_ms]},
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 (matrix-free R(A)) -> assemble", "n": n,
