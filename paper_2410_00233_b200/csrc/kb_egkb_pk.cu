@@ -234,9 +234,16 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) pv[q] = T(0);
             }
+            double yd[VEC];
+            if constexpr (VEC == 4) {
+                ra_bcast4(zs, (unsigned)e0, n, co, Lo, P.refl != 0, yd);   // one division per group
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) yd[q] = ra_bcast(zs, (unsigned)(e0 + q), n, co, Lo, P.refl != 0);
+            }
 #pragma unroll
             for (int q = 0; q < VEC; ++q) {
-                const T yv = (T)ra_bcast(zs, (unsigned)(e0 + q), n, co, Lo, P.refl != 0);
+                const T yv = (T)yd[q];
                 ysq += (double)yv * (double)yv;
                 v[g][q] = pk_sub(yv, pk_mul(H.beta, pv[q]));
             }

@@ -49,19 +49,21 @@ __device__ __forceinline__ double ra_bcast(const double* zs, unsigned e, int n, 
 }
 
 // Sum of X[a*stride + off] over rows a in [lo, hi) with a = lo + phase (mod 8),
-// 8 independent loads in flight (CG: coherent loads for data written in-kernel).
-template <typename T, bool CG>
+// U independent loads in flight (CG: coherent loads for data written in-kernel).
+// The summation order (U-row batches, then the tail) depends on U only through
+// the batching of the same ascending row sequence.
+template <typename T, bool CG, int U = 8>
 __device__ __forceinline__ double band_rows(const T* X, int64_t stride, int64_t off, int lo, int hi, int phase) {
     double acc = 0.0;
     int a = lo + phase;
     const T* p = X + (int64_t)a * stride + off;
     const int64_t step = 8 * stride;
-    for (; a + 56 < hi; a += 64, p += 8 * step) {
-        T q[8];
+    for (; a + 8 * (U - 1) < hi; a += 8 * U, p += U * step) {
+        T q[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) q[k] = CG ? __ldcg(p + k * step) : __ldg(p + k * step);
+        for (int k = 0; k < U; ++k) q[k] = CG ? __ldcg(p + k * step) : __ldg(p + k * step);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc += (double)q[k];
+        for (int k = 0; k < U; ++k) acc += (double)q[k];
     }
     for (; a < hi; a += 8, p += step) acc += (double)(CG ? __ldcg(p) : __ldg(p));
     return acc;
@@ -69,16 +71,40 @@ __device__ __forceinline__ double band_rows(const T* X, int64_t stride, int64_t 
 
 // (P^T x)[u] restricted to image rows [s0, s1), summed by row phase `phase`
 // (the caller reduces over the 8 phases and the row segments).
-template <typename T, bool CG>
+template <typename T, bool CG, int U = 8>
 __device__ __forceinline__ double ra_gather_rows(const T* X, int n, int u, int c, int s0, int s1, int phase,
                                                  bool refl) {
     const int d = u - c;   // diagonal b - a = d
-    double acc = band_rows<T, CG>(X, n + 1, d, max(s0, -d), min(s1, n - d), phase);
+    double acc = band_rows<T, CG, U>(X, n + 1, d, max(s0, -d), min(s1, n - d), phase);
     if (refl && u != c) {
         const int s = u > c ? d - 1 : d - 1 + 2 * n;   // anti-diagonal a + b = s
-        acc += band_rows<T, CG>(X, n - 1, s, max(s0, s - n + 1), min(s1, s + 1), phase);
+        acc += band_rows<T, CG, U>(X, n - 1, s, max(s0, s - n + 1), min(s1, s + 1), phase);
     }
     return acc;
+}
+
+// ra_bcast for the 4 consecutive cells e0..e0+3 (one division when they share a row).
+__device__ __forceinline__ void ra_bcast4(const double* zs, unsigned e0, int n, int c, int L, bool refl,
+                                          double (&out)[4]) {
+    const unsigned a = e0 / (unsigned)n;
+    const int b0 = (int)(e0 - a * (unsigned)n);
+    if (b0 + 3 < n) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int b = b0 + q;
+            const int u = b - (int)a + c;
+            double y = (u >= 0 && u < L) ? zs[u] : 0.0;
+            if (refl) {
+                const int s = (int)a + b + 1 + c;
+                if (s < L) y += zs[s];
+                if (s - 2 * n >= 0) y += zs[s - 2 * n];
+            }
+            out[q] = y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = ra_bcast(zs, e0 + q, n, c, L, refl);
+    }
 }
 
 // Basis size resolved on the device: m = idx ? (*idx) * mul + add : add.

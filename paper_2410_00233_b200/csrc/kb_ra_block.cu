@@ -64,16 +64,20 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
 
     // ---- phase 1: diagonal-sum partials, items = (32-diagonal chunk, row segment)
     {
+        // items = (vector, 32-diagonal chunk, row segment): the vectors of a block
+        // are spread over the grid instead of being summed one after another
         const int chunks = (P.Li + 31) / 32;
         const int items = chunks * RB_SEGS;
-        for (int it = blockIdx.x; it < items; it += nblk) {
+        for (int itv = blockIdx.x; itv < items * nv; itv += nblk) {
+            const int it = itv % items, v = itv / items;
             const int c = it % chunks, seg = it / chunks;
             const int u = c * 32 + lane;
             const int s0 = (int)((int64_t)n * seg / RB_SEGS), s1 = (int)((int64_t)n * (seg + 1) / RB_SEGS);
-            for (int v = 0; v < nv; ++v) {
+            {
                 double a = 0.0;
                 if (u < P.Li)
-                    a = ra_gather_rows<T, false>(X + (int64_t)v * P.ldx, n, u, P.ci, s0, s1, warp, P.refl != 0);
+                    a = ra_gather_rows<T, false, 16>(X + (int64_t)v * P.ldx, n, u, P.ci, s0, s1, warp,
+                                                     P.refl != 0);
                 acc[warp * 33 + lane] = a;
                 __syncthreads();
                 if (warp == 0 && u < P.Li) {
@@ -163,9 +167,16 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
     }
     grid.sync();
     rb_mark(P, 2);
-    // ---- phase 3: z_v into shared memory, Toeplitz broadcast into y_v
+    // ---- phase 3: z_v into shared memory, Toeplitz broadcast into y_v.  With
+    // several vectors the grid is split into nv groups of blocks (block b writes
+    // vector b % nv), so each block stages one z and the vectors are written
+    // concurrently.
     const int64_t N = (int64_t)n * n;
-    for (int v = 0; v < nv; ++v) {
+    const int groups = nv <= nblk ? nv : 1;
+    const int gsize = nblk / groups;                      // blocks per vector group
+    const int gid = blockIdx.x % groups, grank = blockIdx.x / groups;
+    const bool active = grank < gsize;                    // leftover blocks sit out
+    for (int v = (groups > 1 ? gid : 0); v < nv; v += (groups > 1 ? nv : 1)) {
         for (int c = tid; c < P.Lo; c += RB_THREADS) {
             double t = 0.0;
 #pragma unroll
@@ -174,13 +185,21 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
         }
         __syncthreads();
         T* y = Y + (int64_t)v * P.ldy;
-        for (int64_t e0 = (blockIdx.x * (int64_t)RB_THREADS + tid) * 4; e0 < N;
-             e0 += (int64_t)nblk * RB_THREADS * 4) {
+        const int64_t nb = groups > 1 ? gsize : nblk;
+        const int64_t bi = groups > 1 ? grank : blockIdx.x;
+        for (int64_t e0 = (bi * RB_THREADS + tid) * 4; active && e0 < N; e0 += nb * RB_THREADS * 4) {
             T o[4];
+            if (e0 + 4 <= N) {
+                double yv[4];
+                ra_bcast4(zs, (unsigned)e0, n, P.co, P.Lo, P.refl != 0, yv);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int64_t e = e0 + q;
-                o[q] = e < N ? (T)ra_bcast(zs, (unsigned)e, n, P.co, P.Lo, P.refl != 0) : T(0);
+                for (int q = 0; q < 4; ++q) o[q] = (T)yv[q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int64_t e = e0 + q;
+                    o[q] = e < N ? (T)ra_bcast(zs, (unsigned)e, n, P.co, P.Lo, P.refl != 0) : T(0);
+                }
             }
             if (e0 + 4 <= N && ((P.ldy & 3) == 0)) {
                 if constexpr (sizeof(T) == 4) {
