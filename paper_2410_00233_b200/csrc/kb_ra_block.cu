@@ -130,12 +130,12 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
 #pragma unroll
             for (int v = 0; v < RB_MAXV; ++v) a[v] = 0.0;
             int r = r0 + warp;
-            for (; r + 56 < r1; r += 64) {            // 8 independent K loads in flight
-                double mk[8];
+            for (; r + 120 < r1; r += 128) {          // 16 independent K loads in flight
+                T mk[16];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) mk[k] = (c < P.Lo) ? (double)__ldg(M + (int64_t)(r + 8 * k) * P.Lo + c) : 0.0;
+                for (int k = 0; k < 16; ++k) mk[k] = (c < P.Lo) ? __ldg(M + (int64_t)(r + 8 * k) * P.Lo + c) : T(0);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < 16; ++k) {
                     const double* wr = ws + (r + 8 * k - r0) * nv;
 #pragma unroll
                     for (int v = 0; v < RB_MAXV; ++v)
