@@ -19,6 +19,8 @@
 // (per-CTA partials reduced in index order), so results are deterministic.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -221,7 +223,12 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
     for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
     __syncthreads();
     // ---- dots: v = y - beta*prev (fp32 ops as the reference) ; h = S^T v
-    T v[MAXG][VEC];
+    // v is held widened to double when registers allow (MAXG <= 4): each basis
+    // vector's dot then converts only its own entries (half the F2F traffic of
+    // the dots), and the projection starts from it directly.  The values are the
+    // fp32 ones, so every result is unchanged.
+    using VT = typename std::conditional<(MAXG <= 4), double, T>::type;
+    VT v[MAXG][VEC];
     double ysq = 0.0, vsq = 0.0;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g) {
@@ -249,7 +256,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) v[g][q] = T(0);
+            for (int q = 0; q < VEC; ++q) v[g][q] = VT(0);
         }
     }
 #pragma unroll 4
@@ -352,7 +359,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
         if (g < P.ng && e0 < N) {
             T o[VEC];
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) o[q] = pk_div(v[g][q], td);
+            for (int q = 0; q < VEC; ++q) o[q] = pk_div((T)v[g][q], td);
             PkIO<T, VEC>::store(H.out + e0, o);
         }
     }
