@@ -131,6 +131,12 @@ int kb_ts_axpy(int dtype, const void* S, int64_t ld, int m, const double* coef,
  * and the RSVD lift U = Y U_H (lowrank.py:369). */
 int kb_ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols,
                void* out, int64_t ld_out, int64_t len, kb_stream_t stream);
+/* kb_ts_lift fused with kb_kron_assemble (kronop.py:117-119): out_c (fp64) =
+ * scale[c] * (double)(sum_i W[i,c] S_i), the lift computed exactly as
+ * kb_ts_lift does in dtype; scale (device, cols doubles) may be NULL (= 1).
+ * Bit-identical to lift-then-assemble without materialising u / v. */
+int kb_lift_assemble(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols,
+                     const double* scale_dev, double* out, int64_t ld_out, int64_t len, kb_stream_t stream);
 /* In-place two-pass Gram-Schmidt of ncol vectors with the drop test of
  * orthonormalize (linalg.py:156-199).  drop_tol < 0 selects the default
  * eps*sqrt(len)*max column norm.  Returns KB_ENUMERICAL and *bad_col=j

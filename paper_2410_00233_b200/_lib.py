@@ -99,6 +99,7 @@ _SIGS = {
     "kb_ts_dots": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, vp, vp, SZ, vp]),
     "kb_ts_axpy": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, vp, i64, vp]),
     "kb_ts_lift": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, C.c_int, vp, i64, i64, vp]),
+    "kb_lift_assemble": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, C.c_int, vp, vp, i64, i64, vp]),
     "kb_orthonormalize": (C.c_int, [C.c_int, vp, i64, C.c_int, i64, C.c_double, ip, vp, SZ, vp]),
     "kb_orth_workspace_bytes": (C.c_int, [i64, C.c_int, P(SZ)]),
     "kb_egkb_capacity": (C.c_int, [P(KbEgkbConfig)]),

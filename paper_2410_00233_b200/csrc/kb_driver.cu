@@ -816,6 +816,16 @@ extern "C" int kb_ts_lift(int dtype, const void* S, int64_t ld, int rows, const 
     })
 }
 
+extern "C" int kb_lift_assemble(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols,
+                                const double* scale_dev, double* out, int64_t ld_out, int64_t len,
+                                kb_stream_t stream) {
+    KB_GUARD({
+        KB_REQUIRE(S && W && out && rows >= 1 && cols >= 1 && len >= 0, "bad arguments");
+        KB_REQUIRE(dtype == KB_F32 || dtype == KB_F64, "dtype must be KB_F32 or KB_F64");
+        ts_lift_f64(dtype, S, ld, rows, W, cols, out, ld_out, len, scale_dev, as_stream(stream));
+    })
+}
+
 extern "C" int kb_orth_workspace_bytes(int64_t len, int ncol, size_t* bytes) {
     KB_GUARD({
         Sizer s;

@@ -17,6 +17,8 @@
 
 #include "kb_ops.cuh"
 
+#include <type_traits>
+
 namespace kb {
 
 // ------------------------------------------------------------------ diag sums
@@ -386,10 +388,15 @@ k_reorth(const VecRef zr, int mode, int side, int center, int L, const VecRef pr
 // out_c = sum_i W[i, c] S_i for CB output columns per pass, accumulated in T
 // (fp32 like the reference's sgemm for the fp32 path).  One element per
 // thread, W broadcast from shared memory.
-template <typename T, int CB>
+// TO = T: out_c = sum_i W[i,c] S_i in T (fp32 FMA chain, as the reference's
+// working-precision GEMM).  TO = double: the same T value, then scaled in fp64:
+// out_c = scale[c] * (double)lift_c -- kron_assemble fused into the lift
+// (kronop.py:117-119: ax_i = sigma_i * u_i promoted to fp64), bit-identical to
+// lift-then-assemble without writing or re-reading the working-precision u.
+template <typename T, int CB, typename TO = T, bool ASM = false>
 __global__ void __launch_bounds__(256)
 k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, int cols, int c0,
-       T* __restrict__ out, int64_t ld_out, int64_t len) {
+       TO* __restrict__ out, int64_t ld_out, int64_t len, const double* __restrict__ scale = nullptr) {
     extern __shared__ double wraw[];
     T* wsm = reinterpret_cast<T*>(wraw);  // [rows][CB]
     const int nc = min(CB, cols - c0);
@@ -410,8 +417,16 @@ k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, i
             for (int c = 0; c < CB; ++c) acc[c] = fma(s, wr[c], acc[c]);
         }
 #pragma unroll
-        for (int c = 0; c < CB; ++c)
-            if (c < nc) out[(int64_t)(c0 + c) * ld_out + e] = acc[c];
+        for (int c = 0; c < CB; ++c) {
+            if (c < nc) {
+                if constexpr (!ASM) {
+                    out[(int64_t)(c0 + c) * ld_out + e] = acc[c];
+                } else {
+                    const double u = (double)acc[c];
+                    out[(int64_t)(c0 + c) * ld_out + e] = scale ? __dmul_rn(scale[c0 + c], u) : u;
+                }
+            }
+        }
     }
 }
 
@@ -661,37 +676,45 @@ void dense_gemv64(const double* A, int64_t lda, int64_t rows, int64_t cols, cons
     KB_LAUNCH_CHECK();
 }
 
-template <typename T, int CB>
+template <typename T, int CB, typename TO, bool ASM>
 static void launch_lift(const void* S, int64_t ld, int rows, const void* W, int cols, int c0, void* out,
-                        int64_t ld_out, int64_t len, cudaStream_t st) {
+                        int64_t ld_out, int64_t len, const double* scale, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        KB_CUDA(cudaFuncSetAttribute(k_lift<T, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_lift<T, CB, TO, ASM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         configured = true;
     }
     const size_t smem = sizeof(T) * (size_t)rows * CB;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 8 * kSMs));
-    ProfScope ps(st, PROF_LIFT, (double)sizeof(T) * len * (rows + std::min(CB, cols - c0)));
-    k_lift<T, CB><<<blocks, 256, smem, st>>>(static_cast<const T*>(S), ld, rows, static_cast<const T*>(W), cols,
-                                             c0, static_cast<T*>(out), ld_out, len);
+    ProfScope ps(st, PROF_LIFT, (double)len * (sizeof(T) * rows + sizeof(TO) * std::min(CB, cols - c0)));
+    k_lift<T, CB, TO, ASM><<<blocks, 256, smem, st>>>(static_cast<const T*>(S), ld, rows, static_cast<const T*>(W),
+                                                 cols, c0, static_cast<TO*>(out), ld_out, len, scale);
     KB_LAUNCH_CHECK();
+}
+
+template <typename T, typename TO, bool ASM>
+static void lift_cols(const void* S, int64_t ld, int rows, const void* W, int cols, void* out, int64_t ld_out,
+                      int64_t len, const double* scale, cudaStream_t st) {
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+        const int nc = std::min(32, cols - c0);
+        if (nc <= 8) launch_lift<T, 8, TO, ASM>(S, ld, rows, W, cols, c0, out, ld_out, len, scale, st);
+        else if (nc <= 16) launch_lift<T, 16, TO, ASM>(S, ld, rows, W, cols, c0, out, ld_out, len, scale, st);
+        else launch_lift<T, 32, TO, ASM>(S, ld, rows, W, cols, c0, out, ld_out, len, scale, st);
+    }
 }
 
 void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, void* out,
              int64_t ld_out, int64_t len, cudaStream_t st) {
     KB_REQUIRE(rows <= 1024, "lift: too many basis vectors (%d)", rows);
-    for (int c0 = 0; c0 < cols; c0 += 32) {
-        const int nc = std::min(32, cols - c0);
-        if (dtype == KB_F32) {
-            if (nc <= 8) launch_lift<float, 8>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-            else if (nc <= 16) launch_lift<float, 16>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-            else launch_lift<float, 32>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-        } else {
-            if (nc <= 8) launch_lift<double, 8>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-            else if (nc <= 16) launch_lift<double, 16>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-            else launch_lift<double, 32>(S, ld, rows, W, cols, c0, out, ld_out, len, st);
-        }
-    }
+    if (dtype == KB_F32) lift_cols<float, float, false>(S, ld, rows, W, cols, out, ld_out, len, nullptr, st);
+    else lift_cols<double, double, false>(S, ld, rows, W, cols, out, ld_out, len, nullptr, st);
+}
+
+void ts_lift_f64(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, double* out,
+                 int64_t ld_out, int64_t len, const double* scale, cudaStream_t st) {
+    KB_REQUIRE(rows <= 1024, "lift: too many basis vectors (%d)", rows);
+    if (dtype == KB_F32) lift_cols<float, double, true>(S, ld, rows, W, cols, out, ld_out, len, scale, st);
+    else lift_cols<double, double, true>(S, ld, rows, W, cols, out, ld_out, len, scale, st);
 }
 
 }  // namespace kb

@@ -174,5 +174,8 @@ void reorth_pass(int dtype, const Src& src, const void* S, int64_t ld, const MRe
 
 void ts_lift(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, void* out,
              int64_t ld_out, int64_t len, cudaStream_t st);
+// Same lift with fp64 output out_c = scale[c] * (double)lift_c (scale may be null).
+void ts_lift_f64(int dtype, const void* S, int64_t ld, int rows, const void* W, int cols, double* out,
+                 int64_t ld_out, int64_t len, const double* scale, cudaStream_t st);
 
 }  // namespace kb

@@ -167,11 +167,15 @@ def assemble(svd, scheme: BlockScheme) -> KroneckerSum:
     if m_u != scheme.m1 * scheme.n1 or m_v != scheme.m2 * scheme.n2:
         raise ValidationError(
             f"SVD dimensions {m_u}x{m_v} do not match the rearranged shape {scheme.rearranged_shape}")
-    u, v = svd.u_device, svd.v_device
     k = svd.k
     f = D.empty((k, m_u), np.float64)
     g = D.empty((k, m_v), np.float64)
     sig = np.ascontiguousarray(svd.sigma.astype(np.float64))
+    lazy = getattr(svd, "_lazy", None)
+    if lazy is not None:            # eGKB result: factors straight from the Krylov bases
+        lazy.assemble(sig, f, g)
+        return KroneckerSum.from_device(f, g, scheme)
+    u, v = svd.u_device, svd.v_device
     code = _lib.KB_F32 if str(u.dtype) == "torch.float32" else _lib.KB_F64
     _lib.check(_lib.load().kb_kron_assemble(code, u.data_ptr(), m_u, v.data_ptr(), m_v,
                                             sig.ctypes.data_as(C.POINTER(C.c_double)), k, m_u, m_v,

@@ -88,6 +88,7 @@ class TruncatedSvd:
         self.sigma = np.asarray(sigma)
         self._u_dev = None
         self._v_dev = None
+        self._lazy = None
         if self._u is not None:
             self._validate(self._u.shape, self._v.shape)
 
@@ -97,6 +98,22 @@ class TruncatedSvd:
         obj._u_dev, obj._v_dev = u_rows, v_rows
         obj._validate((u_rows.shape[1], u_rows.shape[0]), (v_rows.shape[1], v_rows.shape[0]))
         return obj
+
+    @classmethod
+    def from_lift(cls, lazy, sigma):
+        """Singular vectors kept as (Krylov basis, lift weights) on the device until
+        first used; ``assemble`` then writes the fp64 Kronecker factors straight
+        from the basis (kb_lift_assemble) without materialising u / v."""
+        obj = cls(None, sigma, None)
+        obj._lazy = lazy
+        m, n = lazy.shape
+        obj._validate((m, obj.sigma.size), (n, obj.sigma.size))
+        return obj
+
+    def _force(self):
+        if self._lazy is not None:
+            self._u_dev, self._v_dev = self._lazy.materialize()
+            self._lazy = None
 
     def _validate(self, ushape, vshape):
         if len(ushape) != 2 or len(vshape) != 2 or self.sigma.ndim != 1:
@@ -112,12 +129,14 @@ class TruncatedSvd:
 
     @property
     def u(self) -> np.ndarray:
+        self._force()
         if self._u is None:
             self._u = self._u_dev.detach().cpu().numpy().T
         return self._u
 
     @property
     def v(self) -> np.ndarray:
+        self._force()
         if self._v is None:
             self._v = self._v_dev.detach().cpu().numpy().T
         return self._v
@@ -125,6 +144,7 @@ class TruncatedSvd:
     @property
     def u_device(self):
         """u as a (k, m) CUDA tensor (uploads host factors on first use)."""
+        self._force()
         if self._u_dev is None:
             from . import device as D
             self._u_dev = D.to_device(np.ascontiguousarray(self._u.T))
@@ -132,6 +152,7 @@ class TruncatedSvd:
 
     @property
     def v_device(self):
+        self._force()
         if self._v_dev is None:
             from . import device as D
             self._v_dev = D.to_device(np.ascontiguousarray(self._v.T))
@@ -143,6 +164,8 @@ class TruncatedSvd:
 
     @property
     def shape(self):
+        if self._lazy is not None:
+            return tuple(self._lazy.shape)
         m = self._u.shape[0] if self._u is not None else self._u_dev.shape[1]
         n = self._v.shape[0] if self._v is not None else self._v_dev.shape[1]
         return (m, n)
@@ -153,12 +176,13 @@ class TruncatedSvd:
     def truncate(self, k: int) -> "TruncatedSvd":
         if not 0 < k <= self.k:
             raise ValidationError(f"cannot truncate rank-{self.k} factorization to k={k}")
+        self._force()
         if self._u is None:
             return TruncatedSvd.from_device(self._u_dev[:k], self.sigma[:k], self._v_dev[:k])
         return TruncatedSvd(self._u[:, :k], self.sigma[:k], self._v[:, :k])
 
     def __repr__(self):
-        where = "device" if self._u is None else "host"
+        where = "device (lazy lift)" if self._lazy is not None else ("device" if self._u is None else "host")
         return f"TruncatedSvd(k={self.k}, shape={self.shape}, {where})"
 
 

@@ -210,12 +210,61 @@ def _lift(code, basis, nrows, W, out_rows):
 _BASES: dict = {}
 
 
-def _bases(cap, mbar, nbar, dtype):
-    """Persistent Krylov bases per shape: stable addresses let kb_egkb_run
-    replay its cached CUDA graph instead of re-capturing it."""
+def _bases_key(cap, mbar, nbar, dtype):
     from . import device as D
 
-    key = (cap, mbar, nbar, np.dtype(dtype).str, D.device().index)
+    return (cap, mbar, nbar, np.dtype(dtype).str, D.device().index)
+
+
+class _LazyLift:
+    """U = S W_u, V = Q W_v (lowrank.py:317-318) kept as (basis, weights) until used.
+
+    ``materialize`` runs the working-precision lift (kb_ts_lift); ``assemble``
+    writes the fp64 factors sigma_i u_i and v_i directly (kb_lift_assemble,
+    kronop.py:117-119) -- the same bits as materialising then assembling.
+    """
+
+    def __init__(self, code, s_part, q_part, cols, shape):
+        from . import device as D
+
+        self.code, self.cols, self.shape = code, cols, shape
+        self.parts = []
+        for basis, nrows, w in (s_part, q_part):
+            wd = D.upload(np.ascontiguousarray(w[:nrows]), D.np_dtype(basis))
+            self.parts.append((basis, nrows, wd))
+
+    def materialize(self):
+        from . import device as D
+
+        out = []
+        for basis, nrows, wd in self.parts:
+            length = basis.shape[1]
+            rows_out = D.empty((self.cols, length), D.np_dtype(basis))
+            _lib.check(_lib.load().kb_ts_lift(self.code, basis.data_ptr(), length, nrows, wd.data_ptr(), self.cols,
+                                              rows_out.data_ptr(), length, length, D.stream_ptr()), "lift")
+            out.append(rows_out)
+        self.parts = None
+        return out[0], out[1]
+
+    def assemble(self, sigma, f, g):
+        from . import device as D
+
+        sd = D.upload(np.ascontiguousarray(sigma, dtype=np.float64), np.float64)
+        for (basis, nrows, wd), out, scale in zip(self.parts, (f, g), (sd, None)):
+            length = basis.shape[1]
+            _lib.check(_lib.load().kb_lift_assemble(self.code, basis.data_ptr(), length, nrows, wd.data_ptr(),
+                                                    self.cols, None if scale is None else scale.data_ptr(),
+                                                    out.data_ptr(), length, length, D.stream_ptr()),
+                       "lift+assemble")
+
+
+def _bases(cap, mbar, nbar, dtype):
+    """Krylov bases per shape, reused across calls while no result holds them
+    (a lazily-lifted result owns its bases; the next call then takes fresh
+    ones from the caching allocator)."""
+    from . import device as D
+
+    key = _bases_key(cap, mbar, nbar, dtype)
     hit = _BASES.get(key)
     if hit is None:
         if len(_BASES) >= 4:
@@ -300,8 +349,8 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     s_scale, q_scale = hist[4], hist[5]
     w_u = core.u[:, :chosen].astype(np.float64) * s_scale[:rows, None]
     w_v = core.v[:, :chosen].astype(np.float64) * q_scale[:k_p, None]
-    u_rows = _lift(op.code, s_basis, rows, w_u, chosen)
-    v_rows = _lift(op.code, q_basis, k_p, w_v, chosen)
+    lazy = _LazyLift(op.code, (s_basis, rows, w_u), (q_basis, k_p, w_v), chosen, (mbar, nbar))
+    _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
 
     trace.chosen_k = chosen
     trace.k_p = k_p
@@ -311,7 +360,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
         trace.s_basis = (D.to_host(s_basis[:rows]).T * s_scale[:rows]).astype(dtype)
         trace.q_basis = (D.to_host(q_basis[:k_p]).T * q_scale[:k_p]).astype(dtype)
         trace.c_mat = c_mat
-    return TruncatedSvd.from_device(u_rows, core.sigma[:chosen].copy(), v_rows), trace
+    return TruncatedSvd.from_lift(lazy, core.sigma[:chosen].copy()), trace
 
 
 # ----------------------------------------------------------------- RSVD

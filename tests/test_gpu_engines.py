@@ -394,3 +394,25 @@ class TestParallel:
         finally:
             if created:
                 dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_lazy_lift_assemble_is_bitwise_lift_then_assemble(kb, dtype):
+    """eGKB results keep (basis, weights) until used; assemble then writes the fp64
+    factors straight from the bases (kb_lift_assemble).  Same bits as materialising
+    u, v (kb_ts_lift) and assembling them (kb_kron_assemble)."""
+    from paper_2410_00233_b200 import datagen
+
+    n = 128
+    psf = datagen.mixture_psf(n)
+    cfg = kb.EgkbConfig(k_max=8, k_min=8, p=2, tau=1e300)
+    blur = kb.RearrangedBlur(psf, n, dtype=dtype)
+    scheme = kb.BlockScheme.square_image(n)
+    svd, _ = kb.egkb(blur, cfg)
+    assert svd._lazy is not None
+    fused = kb.assemble(svd, scheme)                       # lazy path
+    eager = kb.assemble(kb.TruncatedSvd.from_device(svd.u_device, svd.sigma, svd.v_device), scheme)
+    np.testing.assert_array_equal(fused.f_dev.cpu().numpy(), eager.f_dev.cpu().numpy())
+    np.testing.assert_array_equal(fused.g_dev.cpu().numpy(), eager.g_dev.cpu().numpy())
+    svd2, _ = kb.egkb(blur, cfg)                           # a later call must not touch svd's bases
+    np.testing.assert_array_equal(svd.u, svd2.u)
