@@ -545,13 +545,20 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         configured = true;
     }
-    int per_sm = 0;
-    KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PK_THREADS, smem));
-    if (std::getenv("KB_DEBUG")) fprintf(stderr, "[kb] persistent eGKB: %d CTAs/SM, smem %zu\n", per_sm, smem);
+    // occupancy and SM count depend only on the device and the smem size: queried once
+    static int dev = -1, sms = 0;
+    static size_t smem_cached = 0;
+    static int per_sm = 0;
+    int cur = 0;
+    KB_CUDA(cudaGetDevice(&cur));
+    if (cur != dev || smem != smem_cached) {
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PK_THREADS, smem));
+        KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur));
+        dev = cur;
+        smem_cached = smem;
+        if (std::getenv("KB_DEBUG")) fprintf(stderr, "[kb] persistent eGKB: %d CTAs/SM, smem %zu\n", per_sm, smem);
+    }
     if (per_sm < 1) return false;
-    int dev = 0, sms = 0;
-    KB_CUDA(cudaGetDevice(&dev));
-    KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int grid = sms * std::min(per_sm, 2);
     const int64_t N = (int64_t)P.n * P.n;
     const int64_t per = (int64_t)grid * PK_THREADS * VEC;
@@ -628,7 +635,7 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     *scales_out = nullptr;
     static unsigned long long* dbg = nullptr;
     static int* dbg_n = nullptr;
-    const bool want_trace = std::getenv("KB_PK_TRACE") != nullptr;
+    static const bool want_trace = std::getenv("KB_PK_TRACE") != nullptr;
     if (want_trace) {
         if (!dbg) {
             KB_CUDA(cudaMalloc(&dbg, 4096 * sizeof(unsigned long long)));

@@ -246,7 +246,7 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     const size_t smem = sizeof(double) * ((size_t)P.zlen + 8 * 33 * RB_MAXV);
     KB_REQUIRE(smem <= 100 * 1024, "R(A) block product: PSF support too large");
     static unsigned long long* dbg = nullptr;
-    const bool trace = std::getenv("KB_PK_TRACE") != nullptr;
+    static const bool trace = std::getenv("KB_PK_TRACE") != nullptr;
     if (trace && !dbg) KB_CUDA(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
     P.dbg = trace ? dbg : nullptr;
     struct Dump {
@@ -279,7 +279,13 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_ra_block<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
             cfg = true;
         }
-        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<float>, RB_THREADS, smem));
+        static size_t smem_q = 0;
+        static int per_sm_q = 0;
+        if (smem != smem_q) {   // occupancy depends only on the smem size: queried once per size
+            KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_q, k_ra_block<float>, RB_THREADS, smem));
+            smem_q = smem;
+        }
+        per_sm = per_sm_q;
         if (per_sm < 1) return false;
         lc.gridDim = dim3(kSMs * std::min(per_sm, 2));
         KB_CUDA(cudaLaunchKernelEx(&lc, k_ra_block<float>, P));
@@ -289,7 +295,13 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_ra_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
             cfg = true;
         }
-        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ra_block<double>, RB_THREADS, smem));
+        static size_t smem_q = 0;
+        static int per_sm_q = 0;
+        if (smem != smem_q) {   // occupancy depends only on the smem size: queried once per size
+            KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_q, k_ra_block<double>, RB_THREADS, smem));
+            smem_q = smem;
+        }
+        per_sm = per_sm_q;
         if (per_sm < 1) return false;
         lc.gridDim = dim3(kSMs * std::min(per_sm, 2));
         KB_CUDA(cudaLaunchKernelEx(&lc, k_ra_block<double>, P));
