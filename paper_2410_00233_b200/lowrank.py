@@ -224,14 +224,33 @@ class _LazyLift:
     kronop.py:117-119) -- the same bits as materialising then assembling.
     """
 
-    def __init__(self, code, s_part, q_part, cols, shape):
+    def __init__(self, code, s_part, q_part, cols, shape, sigma):
         from . import device as D
 
         self.code, self.cols, self.shape = code, cols, shape
+        # W_u, W_v (working dtype) and sigma (fp64) travel in ONE pinned upload
+        dt = D.np_dtype(s_part[0])
+        blocks = [np.ascontiguousarray(w[:nrows], dtype=dt) for _, nrows, w in (s_part, q_part)]
+        sig = np.ascontiguousarray(sigma, dtype=np.float64)
+        offs, total = [], 0
+        for b in blocks + [sig]:
+            total = (total + 15) // 16 * 16
+            offs.append(total)
+            total += b.nbytes
+        host = np.zeros(total, dtype=np.uint8)
+        for b, o in zip(blocks + [sig], offs):
+            host[o:o + b.nbytes] = b.view(np.uint8).reshape(-1)
+        import torch
+
+        stage = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        stage.numpy()[:] = host
+        dev = stage.to(D.device(), non_blocking=True)
+        self._dev = dev                                 # keeps the views' storage alive
+        self.sigma_host = sig
         self.parts = []
-        for basis, nrows, w in (s_part, q_part):
-            wd = D.upload(np.ascontiguousarray(w[:nrows]), D.np_dtype(basis))
-            self.parts.append((basis, nrows, wd))
+        for (basis, nrows, _), b, o in zip((s_part, q_part), blocks, offs):
+            self.parts.append((basis, nrows, dev[o:o + b.nbytes].view(D.torch_dtype(dt)).reshape(b.shape)))
+        self.sigma_dev = dev[offs[2]:offs[2] + sig.nbytes].view(D.torch_dtype(np.float64))
 
     def materialize(self):
         from . import device as D
@@ -249,8 +268,9 @@ class _LazyLift:
     def assemble(self, sigma, f, g):
         from . import device as D
 
-        sd = D.upload(np.ascontiguousarray(sigma, dtype=np.float64), np.float64)
-        for (basis, nrows, wd), out, scale in zip(self.parts, (f, g), (sd, None)):
+        if not np.array_equal(np.asarray(sigma, dtype=np.float64), self.sigma_host):
+            raise ValidationError("lazy lift: sigma does not belong to this factorisation")
+        for (basis, nrows, wd), out, scale in zip(self.parts, (f, g), (self.sigma_dev, None)):
             length = basis.shape[1]
             _lib.check(_lib.load().kb_lift_assemble(self.code, basis.data_ptr(), length, nrows, wd.data_ptr(),
                                                     self.cols, None if scale is None else scale.data_ptr(),
@@ -349,7 +369,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     s_scale, q_scale = hist[4], hist[5]
     w_u = core.u[:, :chosen].astype(np.float64) * s_scale[:rows, None]
     w_v = core.v[:, :chosen].astype(np.float64) * q_scale[:k_p, None]
-    lazy = _LazyLift(op.code, (s_basis, rows, w_u), (q_basis, k_p, w_v), chosen, (mbar, nbar))
+    lazy = _LazyLift(op.code, (s_basis, rows, w_u), (q_basis, k_p, w_v), chosen, (mbar, nbar), core.sigma[:chosen])
     _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
 
     trace.chosen_k = chosen
