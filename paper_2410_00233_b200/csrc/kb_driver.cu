@@ -486,10 +486,6 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     c.handle = 0;
     c.use_cond = 0;
 
-    KB_CUDA(cudaMemsetAsync(P.w.plan.counters, 0, sizeof(unsigned) * P.w.plan.n_counters, s));
-    KB_CUDA(cudaMemsetAsync(P.w.rw.counter, 0, sizeof(unsigned) * 64, s));
-    KB_CUDA(cudaMemcpyAsync(P.w.y0slot, y0, esz * (size_t)op->rows, cudaMemcpyDeviceToDevice, s));
-
     static thread_local char* hbuf = nullptr;   // pinned trace mailbox
     static thread_local size_t hbuf_bytes = 0;
     const size_t need = sizeof(int) * H_COUNT + sizeof(double) * 4 * (size_t)cap;
@@ -507,8 +503,12 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     bool pk_done = false;
     double* pk_scales = nullptr;
     if (!force_eager && !no_pk)
-        pk_done = egkb_persistent(op, cfg, st, P.w.y0slot, P.w.hdr, P.w.trace, P.w.pk, P.w.pkraw, c.tol,
-                                  &pk_scales, s);
+        pk_done = egkb_persistent(op, cfg, st, y0, P.w.hdr, P.w.trace, P.w.pk, P.w.pkraw, c.tol, &pk_scales, s);
+    if (!pk_done) {   // graph / eager engines: counters zeroed, y0 copied into the graph's input slot
+        KB_CUDA(cudaMemsetAsync(P.w.plan.counters, 0, sizeof(unsigned) * P.w.plan.n_counters, s));
+        KB_CUDA(cudaMemsetAsync(P.w.rw.counter, 0, sizeof(unsigned) * 64, s));
+        KB_CUDA(cudaMemcpyAsync(P.w.y0slot, y0, esz * (size_t)op->rows, cudaMemcpyDeviceToDevice, s));
+    }
     if (pk_done) {
         // single persistent kernel ran the whole loop
     } else if (!g_prof && !force_eager) {

@@ -35,6 +35,7 @@ namespace kb {
 
 constexpr int PK_THREADS = 256;
 constexpr int PK_SEGS = 8;
+constexpr int PK_NSTRIDE = 16;   // norm partials one 128-B line apart (no hot lines in the reduction)
 
 struct PkParams {
     const void* K;    // kh x kw
@@ -53,7 +54,11 @@ struct PkParams {
     double* diag_part;   // [PK_SEGS][Lmax]
     double* col_part;    // [PK_SEGS][Lmax]
     double* blk_part;    // [grid][cap + 4]
-    double* norm_part;   // [grid]
+    double* norm_part;   // [grid][PK_NSTRIDE]
+    double* zbuf;        // [Lmax]: z = K^T w (or K w), summed by each column chunk's last finisher
+    double* bres;        // [cap + 4]: results published by a reduce-barrier's last arriver
+    unsigned* bar;       // [0]: arrivals, [32]: generation, [64..): per-column-chunk finish counters
+    int nbar;            // words in bar (zeroed before the launch)
     void* raw_s;         // pending unnormalised s vector (N elements)
     void* raw_q;         // pending unnormalised q vector
     int ng;              // element groups per thread
@@ -105,17 +110,87 @@ __device__ __forceinline__ double pk_sub(double a, double b) { return __dsub_rn(
 __device__ __forceinline__ float pk_div(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double pk_div(double a, double b) { return __ddiv_rn(a, b); }
 
-// Fixed-order sum over the grid's per-CTA partials for slots [0, nslots):
-// warp w reduces slots w, w+8, ...; lanes stride over CTAs.  Result -> out[].
+// Fixed-order sum over the grid's per-CTA partials part[b * stride + j],
+// slots j < nslots.  A warp covers Wp = pow2ceil(min(nslots, 32)) slots with
+// 32 / Wp lanes per slot (lane = sub * Wp + slot): every request reads one
+// CTA's partial row (coalesced, one 128-B line when stride is padded), the
+// 8 warps x (32 / Wp) subs split the CTAs, all loads of a lane are issued
+// before they are summed (one L2 round trip), then subs are combined by a
+// fixed shuffle tree and warps in warp order.  Result -> out[];  `tmp` is
+// >= 8 * 32 doubles of shared memory.  Ends with __syncthreads().
+constexpr int PK_RED_BATCH = 20;   // loads in flight per lane
 __device__ __forceinline__ void pk_reduce_slots(const double* part, int stride, int nblk, int nslots,
-                                                double* out) {
+                                                double* out, double* tmp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int j = warp; j < nslots; j += PK_THREADS / 32) {
+    int wp = 1;
+    while (wp < nslots && wp < 32) wp <<= 1;
+    const int subs = 32 / wp, sub = lane / wp, sl = lane % wp;
+    for (int j0 = 0; j0 < nslots; j0 += wp) {
+        const int j = j0 + sl;
         double s = 0.0;
-        for (int b = lane; b < nblk; b += 32) s += __ldcg(part + (int64_t)b * stride + j);
-        s = warp_sum(s);
-        if (lane == 0) out[j] = s;
+        if (j < nslots) {
+            for (int b0 = warp + 8 * sub; b0 < nblk; b0 += 8 * subs * PK_RED_BATCH) {
+                double q[PK_RED_BATCH];
+#pragma unroll
+                for (int k = 0; k < PK_RED_BATCH; ++k) {
+                    const int b = b0 + 8 * subs * k;
+                    q[k] = b < nblk ? __ldcg(part + (int64_t)b * stride + j) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < PK_RED_BATCH; ++k) s += q[k];
+            }
+        }
+        for (int o = 16; o >= wp; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        tmp[warp * 32 + lane] = s;
+        __syncthreads();
+        if (warp == 0 && lane < wp && j < nslots) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t += tmp[w * 32 + lane];
+            out[j] = t;
+        }
+        __syncthreads();
     }
+}
+
+// out[c] = sum_{q < PK_SEGS} part[q * stride + c] for c < len (fixed order),
+// 4 entries per thread per round with all 32 loads in flight.  No barrier.
+__device__ __forceinline__ void pk_stage_segs(const double* part, int64_t stride, int len, double* out) {
+    for (int c0 = threadIdx.x; c0 < len; c0 += 4 * PK_THREADS) {
+        double q[4][PK_SEGS];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int c = c0 + r * PK_THREADS;
+#pragma unroll
+            for (int s = 0; s < PK_SEGS; ++s) q[r][s] = c < len ? __ldcg(part + s * stride + c) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int c = c0 + r * PK_THREADS;
+            double t = 0.0;
+#pragma unroll
+            for (int s = 0; s < PK_SEGS; ++s) t += q[r][s];
+            if (c < len) out[c] = t;
+        }
+    }
+}
+
+// Grid barrier fused with a fixed-order reduction.  Every CTA has written
+// its partials part[b * stride + j] (j < nslots); the LAST CTA to arrive sums
+// them (pk_reduce_slots: one CTA reads them, instead of every CTA reading the
+// same few lines), publishes the sums to P.bres and releases the others,
+// which copy them.  On return out[j] (shared memory) holds the sums in every
+// CTA.  Acts as a full grid barrier: arrival is an acq_rel atomic on one
+// counter (reset by the last arriver before it releases), release is a
+// st.release of the generation word, observed with ld.acquire by thread 0 of
+// each waiting CTA (the same protocol as cooperative_groups' grid.sync).
+// `gen` is thread 0's copy of the generation, advanced once per call.
+__device__ __forceinline__ void pk_reduce_barrier(const PkParams& P, unsigned& gen, const double* part, int stride,
+                                                  int nslots, double* out, double* tmp) {
+    (void)P;
+    (void)gen;
+    cg::this_grid().sync();
+    pk_reduce_slots(part, stride, gridDim.x, nslots, out, tmp);
 }
 
 template <typename T>
@@ -132,9 +207,8 @@ struct PkHalf {
 
 // One half step.  Returns t = |v1| (identical in every CTA).
 template <typename T, int VEC, int MAXG>
-__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid) {
-    constexpr int GC = 2;   // element groups processed together (loads in flight per basis vector)
-    static_assert(MAXG % GC == 0, "MAXG must be a multiple of GC");
+__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid,
+                          unsigned& gen) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
     const int64_t N = (int64_t)n * n;
@@ -207,28 +281,51 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
                 for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
                 P.col_part[(int64_t)seg * P.lmax + c] = t;
             }
+            // the last of the chunk's PK_SEGS items sums the segments (fixed
+            // order) into z, so the dots phase reads z instead of every CTA
+            // re-reducing all the partials
+            __shared__ int s_fin;
             __syncthreads();
+            if (tid == 0) {
+                unsigned old;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(P.bar + 64 + cc), "r"(1u) : "memory");
+                s_fin = (old == PK_SEGS - 1);
+                if (s_fin) P.bar[64 + cc] = 0u;   // next use is several grid barriers later
+            }
+            __syncthreads();
+            if (s_fin && warp == 0 && c < Lo) {
+                double q[PK_SEGS];
+#pragma unroll
+                for (int sg = 0; sg < PK_SEGS; ++sg) q[sg] = __ldcg(P.col_part + (int64_t)sg * P.lmax + c);
+                double t = 0.0;
+#pragma unroll
+                for (int sg = 0; sg < PK_SEGS; ++sg) t += q[sg];
+                __stcg(P.zbuf + c, t);
+            }
         }
     }
     grid.sync();
     pk_mark(P);
-    // ---- z (Toeplitz coefficients) into shared memory, fixed-order over segments
-    for (int c = tid; c < Lo; c += PK_THREADS) {
-        double t = 0.0;
+    // ---- z (Toeplitz coefficients) into shared memory
+    for (int c0 = tid; c0 < Lo; c0 += 8 * PK_THREADS) {   // all loads in flight, then the stores
+        double q[8];
 #pragma unroll
-        for (int q = 0; q < PK_SEGS; ++q) t += __ldcg(P.col_part + (int64_t)q * P.lmax + c);
-        zs[c] = t;
+        for (int k = 0; k < 8; ++k) q[k] = c0 + k * PK_THREADS < Lo ? __ldcg(P.zbuf + c0 + k * PK_THREADS) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (c0 + k * PK_THREADS < Lo) zs[c0 + k * PK_THREADS] = q[k];
     }
     const int W = H.m + 2;
     for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
     __syncthreads();
+    pk_mark(P);
     // ---- dots: v = y - beta*prev (fp32 ops as the reference) ; h = S^T v
-    // v is held widened to double when registers allow (MAXG <= 4): each basis
-    // vector's dot then converts only its own entries (half the F2F traffic of
-    // the dots), and the projection starts from it directly.  The values are the
-    // fp32 ones, so every result is unchanged.
-    using VT = typename std::conditional<(MAXG <= 4), double, T>::type;
-    VT v[MAXG][VEC];
+    // The dot products and the projection run in the working precision T
+    // like the reference's BLAS sdot/saxpy (per-thread FMA chains over the
+    // thread's <= MAXG*VEC entries; the per-thread partials are widened once
+    // and reduced across the grid in fp64, fixed order): no per-element
+    // fp32 -> fp64 conversions, whose 16/clk/SM pipe bounded these phases.
+    T v[MAXG][VEC];
     double ysq = 0.0, vsq = 0.0;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g) {
@@ -256,13 +353,14 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) v[g][q] = VT(0);
+            for (int q = 0; q < VEC; ++q) v[g][q] = T(0);
         }
     }
+    pk_mark(P);
 #pragma unroll 4
     for (int i = 0; i < H.m; ++i) {
         const T* Si = H.S + (int64_t)i * H.ld;
-        double d = 0.0;
+        T dt = T(0);
 #pragma unroll
         for (int g = 0; g < MAXG; ++g) {
             const int64_t e0 = (g * G + gt) * VEC;
@@ -270,10 +368,10 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
                 T sv[VEC];
                 PkIO<T, VEC>::load(Si + e0, sv);
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) d += (double)sv[q] * (double)v[g][q];
+                for (int q = 0; q < VEC; ++q) dt = fma(sv[q], v[g][q], dt);
             }
         }
-        d = warp_sum(d);
+        const double d = warp_sum((double)dt);
         if (lane == 0) acc[warp * W + i] += d;
     }
 #pragma unroll
@@ -287,68 +385,61 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
         acc[warp * W + H.m + 1] += ysq;
     }
     __syncthreads();
+    pk_mark(P);
     for (int j = tid; j < W; j += PK_THREADS) {
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) t += acc[w * W + j];
         P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
     }
-    grid.sync();
+    pk_reduce_barrier(P, gen, P.blk_part, P.cap + 4, W, red, acc);
     pk_mark(P);
-    pk_reduce_slots(P.blk_part, P.cap + 4, nblk, W, red);
-    __syncthreads();
     ysq_out = red[H.m + 1];
     double t;
     if (H.m == 0) {
         t = sqrt(red[0]);
     } else {
-    // ---- apply: v1 = v - S h (fp64 accumulation, rounded once), kept in registers
+    // ---- apply: v1 = v - S h in T (one FMA per basis entry, as saxpy), kept in registers
+    constexpr int GA = MAXG <= 4 ? MAXG : 4;   // element groups per pass over the basis
+    T* cf = reinterpret_cast<T*>(acc);          // coefficients in T (acc is free after the barrier)
+    for (int i = tid; i < H.m; i += PK_THREADS) cf[i] = (T)red[i];
+    __syncthreads();
     double v1sq = 0.0;
 #pragma unroll
-    for (int g0 = 0; g0 < MAXG; g0 += GC) {
+    for (int g0 = 0; g0 < MAXG; g0 += GA) {
         if (g0 >= P.ng) break;
-        double a[GC][VEC];
-#pragma unroll
-        for (int g = 0; g < GC; ++g)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) a[g][q] = (double)v[g0 + g][q];
 #pragma unroll 4
         for (int i = 0; i < H.m; ++i) {
             const T* Si = H.S + (int64_t)i * H.ld;
-            const double c = red[i];
+            const T c = cf[i];
 #pragma unroll
-            for (int g = 0; g < GC; ++g) {
+            for (int g = 0; g < GA; ++g) {
                 const int64_t e0 = ((g0 + g) * G + gt) * VEC;
                 if (g0 + g < P.ng && e0 < N) {
                     T sv[VEC];
                     PkIO<T, VEC>::load(Si + e0, sv);
 #pragma unroll
-                    for (int q = 0; q < VEC; ++q) a[g][q] -= c * (double)sv[q];
+                    for (int q = 0; q < VEC; ++q) v[g0 + g][q] = fma(-c, sv[q], v[g0 + g][q]);
                 }
             }
         }
 #pragma unroll
-        for (int g = 0; g < GC; ++g) {
+        for (int g = 0; g < GA; ++g)
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-                v[g0 + g][q] = (T)a[g][q];
-                v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
-            }
-        }
+            for (int q = 0; q < VEC; ++q) v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
     }
     v1sq = warp_sum(v1sq);
+    __syncthreads();   // cf (in acc) is read until every warp has finished the projection
     if (lane == 0) acc[warp] = v1sq;
     __syncthreads();
     if (tid == 0) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += acc[w];
-        P.norm_part[blockIdx.x] = s;
+        P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
     }
-    grid.sync();
+    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
     pk_mark(P);
-    pk_reduce_slots(P.norm_part, 1, nblk, 1, red + P.cap + 2);
-    __syncthreads();
     t = sqrt(red[P.cap + 2]);
     }
     // ---- write: out = fl(v1 / t)
@@ -384,6 +475,10 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     const int64_t G = (int64_t)nblk * PK_THREADS;
     const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
     const bool rec = (blockIdx.x == 0 && tid == 0);
+    // generation of the reduce-barrier at entry (stable: it only advances once
+    // every CTA has arrived at the first reduce-barrier)
+    unsigned gen = 0;
+    if (tid == 0) asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(P.bar + 32) : "memory");
 
     // ---- s1 = y0 / |y0|   (lowrank.py:207-210)
     T v0[MAXG][VEC];
@@ -403,12 +498,10 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     if (tid == 0) {
         double s = 0.0;
         for (int w = 0; w < 8; ++w) s += acc[w];
-        P.norm_part[blockIdx.x] = s;
+        P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
     }
-    grid.sync();
+    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red, acc);
     pk_mark(P);
-    pk_reduce_slots(P.norm_part, 1, nblk, 1, red);
-    __syncthreads();
     const double t1 = sqrt(red[0]);
     {
         const T td = (T)t1;
@@ -445,7 +538,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
                           Q + (int64_t)done * P.ld_q, 1};
         }
         double aux = 0.0;
-        const double val = pk_half<T, VEC, MAXG>(P, h, sm, aux, grid);
+        const double val = pk_half<T, VEC, MAXG>(P, h, sm, aux, grid, gen);
         if (step == 0) {
             const double a1 = val;
             zeta_last = a1 * t1;
@@ -577,14 +670,20 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     lc.attrs = attr;
     lc.numAttrs = 1;
     (void)args;
+    KB_CUDA(cudaMemsetAsync(P.bar, 0, sizeof(unsigned) * P.nbar, st));
     KB_CUDA(cudaLaunchKernelEx(&lc, kern, P));
     grid_out = grid;
     return true;
 }
 
 // Sizes of the scratch the persistent kernel needs (doubles).
+// barrier words (unsigned): arrivals, generation, per-column-chunk counters
+static size_t pk_bar_words(int lmax) { return 64 + (size_t)(lmax + 31) / 32 + 32; }
+static size_t pk_bar_doubles(int lmax) { return (pk_bar_words(lmax) + 1) / 2; }
+
 size_t pk_scratch_doubles(int lmax, int cap) {
-    return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs + 2 * (size_t)cap + 256;
+    return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs * PK_NSTRIDE + 2 * (size_t)cap + 256 +
+           (size_t)lmax + (size_t)cap + 8 + pk_bar_doubles(lmax);
 }
 
 // Returns false when the configuration is outside the persistent kernel's
@@ -630,6 +729,10 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     P.col_part = scratch + (size_t)PK_SEGS * lmax;
     P.blk_part = scratch + 2 * (size_t)PK_SEGS * lmax;
     P.norm_part = P.blk_part + (size_t)(8 * kSMs) * (cap + 4);
+    P.zbuf = P.norm_part + 8 * kSMs * PK_NSTRIDE + 2 * (size_t)cap + 256;
+    P.bres = P.zbuf + lmax;
+    P.bar = reinterpret_cast<unsigned*>(P.bres + cap + 8);
+    P.nbar = (int)pk_bar_words(lmax);
     P.raw_s = raw;
     P.raw_q = static_cast<char*>(raw) + (size_t)N * (op->dtype == KB_F32 ? 4 : 8);
     *scales_out = nullptr;
