@@ -58,7 +58,8 @@ struct PkParams {
     double* zbuf;        // [Lmax]: z = K^T w (or K w), summed by each column chunk's last finisher
     double* bres;        // [cap + 4]: results published by a reduce-barrier's last arriver
     unsigned* bar;       // [0]: arrivals, [32]: generation, [64..): per-column-chunk finish counters
-    int nbar;            // words in bar (zeroed before the launch)
+    int nbar;            // words in bar + wfix (zeroed before the launch)
+    unsigned long long* wfix;   // [2][Lmax] fixed-point diagonal sums (tiled kernel)
     void* raw_s;         // pending unnormalised s vector (N elements)
     void* raw_q;         // pending unnormalised q vector
     int ng;              // element groups per thread
@@ -102,6 +103,22 @@ struct PkIO<double, 2> {
         *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
     }
 };
+
+// fl32(a / b) computed as fl32(fl64(a / b)): double rounding is innocuous for
+// a quotient of two floats (53 >= 2 * 24 + 2), so this equals the correctly
+// rounded fp32 division bit for bit -- without the subnormal slow path of the
+// fp32 division routine, which the Gaussian-tail entries of the Krylov vectors
+// (subnormal in fp32) hit on every element (10x slower stores).
+// (inline PTX: the compiler would otherwise fold the widened division back
+// into the fp32 one, slow path included).
+// A zero dividend (the exact zeros of the Gaussian-tail entries) would
+// still take the division's special-case path, so it is answered directly.
+__device__ __forceinline__ float pk_fdiv_exact(float a, float b) {
+    if (a == 0.f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000);
+    double q;
+    asm("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"((double)a), "d"((double)b));
+    return (float)q;
+}
 
 __device__ __forceinline__ float pk_mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double pk_mul(double a, double b) { return __dmul_rn(a, b); }
@@ -625,6 +642,514 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     }
 }
 
+// ------------------------------------------------------------------ tiled variant
+// Zero BC, fp32, n a multiple of 128 (or a divisor of 128).  Same recurrence
+// with four grid synchronisations per half step (three when there is nothing
+// to project against) instead of five, and no pass that re-reads the input
+// vector for its diagonal sums:
+//
+//   A  z        : z = K^T w (or K w), one contiguous row dot product per entry
+//      -- grid.sync
+//   B  dots     : y = P z ; v = y - beta*prev ; h = S^T v ; |v|^2 ; |y|^2
+//      -- grid.sync + reduction
+//   C  apply    : v1 = v - S h ; |v1|^2                (v kept in registers)
+//      -- grid.sync + reduction (t = |v1|)
+//   D  store    : x = fl(v1 / t) (lowrank.py:247, 260) stored, and the
+//                 diagonal sums w of x for the NEXT product, from registers
+//      -- grid.sync
+//
+// Each CTA owns whole 1024-element tiles of the n x n image (8*RW rows x TW
+// columns, one float4 per thread, column-block-major tile order, balanced
+// contiguous tile ranges), so its diagonal sums are compact: the tile values
+// go through shared memory, each thread sums one diagonal of the CTA's tile
+// stack, and the sums are added to the global w with 64-bit integer atomics
+// in fixed point (entries of a unit vector are <= 1: scale 2^(61 - log2 n),
+// so no sum can overflow).  Integer addition is exact, so w does not depend
+// on the order of the atomics: the run stays deterministic without per-CTA
+// partial arrays, and every fp32 entry above 2^-(61 - log2 n) enters the
+// sum exactly (w is at least as accurate as an fp64 summation).
+
+struct TileGeo {
+    int TW, LR, RW, RB, T;   // tile width, lanes per row, rows per warp, row blocks, tiles
+};
+
+__device__ __forceinline__ void tile_range(int T, int b, int nblk, int& t0, int& ng) {
+    t0 = (int)((int64_t)T * b / nblk);
+    ng = (int)((int64_t)T * (b + 1) / nblk) - t0;
+}
+
+// fixed-point exponent for entries bounded by 2|v|: sums of <= n of them stay < 2^62
+__device__ __forceinline__ int pk_fix_exp(double vnorm, int n) {
+    int e = 0;
+    if (!(vnorm > 0.0) || !isfinite(vnorm)) return 0;
+    frexp(2.0 * vnorm, &e);   // 2|v| < 2^e
+    int ln = 0;
+    while ((1 << ln) < n) ++ln;
+    return 62 - ln - e;
+}
+
+// Colsum items of one R(A) product: part[s][c] = sum_{r in seg s} M[r, c] w(r),
+// the last of a chunk's PK_SEGS items writes z[c] = sum_s part[s][c].
+template <typename WF>
+__device__ __forceinline__ void pk_colsum_items(const PkParams& P, const float* M, int Li, int Lo, double* ws,
+                                                double* acc, WF wf) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int chunks = (Lo + 31) / 32;
+    const int items = chunks * PK_SEGS;
+    __shared__ int s_fin;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int cc = it % chunks, seg = it / chunks;
+        const int c = cc * 32 + lane;
+        const int r0 = (int)((int64_t)Li * seg / PK_SEGS), r1 = (int)((int64_t)Li * (seg + 1) / PK_SEGS);
+        for (int j = tid; j < r1 - r0; j += PK_THREADS) ws[j] = wf(r0 + j);
+        __syncthreads();
+        double a = 0.0;
+        int r = r0 + warp;
+        for (; r + 120 < r1; r += 128) {            // 16 independent K loads in flight
+            float mk[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) mk[k] = (c < Lo) ? __ldg(M + (int64_t)(r + 8 * k) * Lo + c) : 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) a += (double)mk[k] * ws[r + 8 * k - r0];
+        }
+        for (; r < r1; r += 8)
+            if (c < Lo) a += (double)__ldg(M + (int64_t)r * Lo + c) * ws[r - r0];
+        acc[warp * 33 + lane] = a;
+        __syncthreads();
+        if (warp == 0 && c < Lo) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
+            P.col_part[(int64_t)seg * P.lmax + c] = t;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned old;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(P.bar + 64 + cc), "r"(1u) : "memory");
+            s_fin = (old == PK_SEGS - 1);
+            if (s_fin) P.bar[64 + cc] = 0u;   // next use is several grid barriers later
+        }
+        __syncthreads();
+        if (s_fin && warp == 0 && c < Lo) {
+            double q[PK_SEGS];
+#pragma unroll
+            for (int sg = 0; sg < PK_SEGS; ++sg) q[sg] = __ldcg(P.col_part + (int64_t)sg * P.lmax + c);
+            double t = 0.0;
+#pragma unroll
+            for (int sg = 0; sg < PK_SEGS; ++sg) t += q[sg];
+            __stcg(P.zbuf + c, t);
+        }
+    }
+}
+
+// Diagonal sums of the CTA's register-held tile values (staged in tb) for a
+// product with diagonal offset ci and Li diagonals, added in fixed point to wf.
+template <int MAXG>
+__device__ __forceinline__ void tile_diag_atomics(const PkParams& P, const TileGeo& Gm, const float* tb, int t0,
+                                                  int ng, int ci, int Li, double scale, unsigned long long* wf) {
+    const int n = P.n, R = 8 * Gm.RW;
+    int g = 0;
+    while (g < ng) {
+        const int cb = (t0 + g) / Gm.RB, rb0 = (t0 + g) - cb * Gm.RB;
+        int h = 1;
+        while (g + h < ng && (t0 + g + h) / Gm.RB == cb) ++h;     // stack of h tiles in column block cb
+        const int A0 = rb0 * R, A1 = A0 + h * R, C0 = cb * Gm.TW;
+        const float* sb = tb + g * 1024;                           // stack rows, row-major, TW wide
+        const int dlo = C0 - (A1 - 1), nd = Gm.TW + h * R - 1;
+        for (int i = threadIdx.x; i < nd; i += PK_THREADS) {
+            const int d = dlo + i, u = d + ci;
+            if (u < 0 || u >= Li) continue;
+            const int a_lo = max(A0, C0 - d), a_hi = min(A1, C0 + Gm.TW - d);
+            long long s = 0;
+            for (int a = a_lo; a < a_hi; ++a)
+                s += __double2ll_rn((double)sb[(a - A0) * Gm.TW + (a + d - C0)] * scale);
+            if (s != 0) atomicAdd(wf + u, (unsigned long long)s);
+        }
+        g += h;
+    }
+    (void)n;
+}
+
+// z[c] = sum_r Mt[c, r] w(r) for this CTA's rows c in [b Lo / grid, (b+1) Lo / grid):
+// Mt is K^T for the forward product (z = K^T w) and K for the transpose, so
+// every z entry is ONE contiguous row dot product (warp per row, lanes over
+// r, fixed order): no column partials, no second pass.  w is staged in
+// shared memory; its loads and the first batch of row loads are issued
+// together (one L2 round trip).
+__device__ __forceinline__ void pk_zrows(const PkParams& P, const float* Mt, int Li, int Lo, double* ws,
+                                         const unsigned long long* wsrc, double s2) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = (int)((int64_t)Lo * blockIdx.x / gridDim.x), c1 = (int)((int64_t)Lo * (blockIdx.x + 1) / gridDim.x);
+    constexpr int RB = 32;   // row loads in flight per lane
+    float mk[RB];
+    const int c_first = c0 + warp;
+    if (c_first < c1) {
+        const float* row = Mt + (int64_t)c_first * Li;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) mk[k] = (lane + 32 * k < Li) ? __ldg(row + lane + 32 * k) : 0.f;
+    }
+    // w(r) = wfix[r] * 2^-F, all loads in flight before the stores
+    for (int r0 = tid; r0 < Li; r0 += 8 * PK_THREADS) {
+        long long q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = r0 + k * PK_THREADS < Li ? (long long)__ldcg(wsrc + r0 + k * PK_THREADS) : 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (r0 + k * PK_THREADS < Li) ws[r0 + k * PK_THREADS] = (double)q[k] * s2;
+    }
+    __syncthreads();
+    for (int c = c_first; c < c1; c += PK_THREADS / 32) {
+        const float* row = Mt + (int64_t)c * Li;
+        if (c != c_first) {
+#pragma unroll
+            for (int k = 0; k < RB; ++k) mk[k] = (lane + 32 * k < Li) ? __ldg(row + lane + 32 * k) : 0.f;
+        }
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+            if (lane + 32 * k < Li) a += (double)mk[k] * ws[lane + 32 * k];
+        for (int r0 = 32 * RB; r0 < Li; r0 += 32 * RB) {        // long rows (Li > 1024)
+#pragma unroll
+            for (int k = 0; k < RB; ++k) mk[k] = (r0 + lane + 32 * k < Li) ? __ldg(row + r0 + lane + 32 * k) : 0.f;
+#pragma unroll
+            for (int k = 0; k < RB; ++k)
+                if (r0 + lane + 32 * k < Li) a += (double)mk[k] * ws[r0 + lane + 32 * k];
+        }
+        a = warp_sum(a);
+        if (lane == 0) __stcg(P.zbuf + c, a);
+    }
+}
+
+// x = fl(v / t) for the register-held tile values: stored to `out`, staged
+// in shared memory, and its fixed-point diagonal sums added to wf.
+template <int MAXG>
+__device__ __forceinline__ void pk_store_diag(const PkParams& P, const TileGeo& Gm, float (&v)[MAXG][4], float td,
+                                              float* out, const int (&eo)[MAXG], int ng, float* tb, int tbo, int t0,
+                                              int ci, int Li, double fxs, unsigned long long* wf) {
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g)
+        if (g < ng) {
+            float o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[q] = pk_fdiv_exact(v[g][q], td);
+            PkIO<float, 4>::store(out + eo[g], o);
+            *reinterpret_cast<float4*>(tb + g * 1024 + tbo) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+    __syncthreads();
+    tile_diag_atomics<MAXG>(P, Gm, tb, t0, ng, ci, Li, fxs, wf);
+}
+
+template <int MAXG>
+__global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGeo Gm) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = P.n;
+    const int nblk = gridDim.x;
+    float* S = static_cast<float*>(P.S);
+    float* Q = static_cast<float*>(P.Q);
+    const float* y0 = static_cast<const float*>(P.y0);
+    double* zs = sm;                               // [lmax]
+    double* red = zs + P.lmax;                     // [cap + 4]
+    double* acc = red + P.cap + 4;                 // [8][max(cap + 2, 33)]
+    float* tb = reinterpret_cast<float*>(acc + 8 * max(P.cap + 2, 33));   // [MAXG * 1024]
+    const bool rec = (blockIdx.x == 0 && tid == 0);
+    const int cu = P.kh / 2, cv = P.kw / 2;
+    unsigned gen = 0;
+
+    // element offsets of this thread (one float4 per tile)
+    int t0, ng;
+    tile_range(Gm.T, blockIdx.x, nblk, t0, ng);
+    int eo[MAXG];
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+        const int t = min(t0 + g, Gm.T - 1);
+        const int cb = t / Gm.RB, rb = t - cb * Gm.RB;
+        const int a = rb * 8 * Gm.RW + warp * Gm.RW + lane / Gm.LR;
+        eo[g] = a * n + cb * Gm.TW + (lane % Gm.LR) * 4;
+    }
+    const int tbo = warp * 128 + lane * 4;         // this thread's float4 inside a staged tile
+
+    // ---- prologue: v <- y0, t1 = |y0|, diagonal sums of y0 for step 0 (R^T, q side)
+    float v[MAXG][4];
+    double vsq = 0.0;
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+        if (g < ng) {
+            PkIO<float, 4>::load(y0 + eo[g], v[g]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) vsq += (double)v[g][q] * (double)v[g][q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[g][q] = 0.f;
+        }
+    }
+    vsq = warp_sum(vsq);
+    if (lane == 0) acc[warp] = vsq;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += acc[w];
+        P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
+    }
+    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red, acc);
+    pk_mark(P);
+    const double t1 = sqrt(red[0]);
+    // entries of a normalised vector are <= 1: one fixed-point scale for the run
+    const int Fx = pk_fix_exp(0.5, n);
+    const double fxs = ldexp(1.0, Fx), fxs_inv = ldexp(1.0, -Fx);
+    // s1 = fl(y0 / t1) (lowrank.py:207-210), stored, and its diagonal sums for step 0 (R^T)
+    pk_store_diag<MAXG>(P, Gm, v, (float)t1, S, eo, ng, tb, tbo, t0, cv, P.kw, fxs, P.wfix);
+    grid.sync();
+    pk_mark(P);
+
+    int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
+    int na = 1, nt = 1, nn = 1;
+    double zeta_last = 0.0, nu_last = 1e308, alpha_cur = 0.0, t_new = 0.0, u2 = 0.0;
+    if (t1 == 0.0) {
+        err = 1;
+        stop = 1;
+    }
+    for (int step = 0; !stop; ++step) {
+        const int tr = (step & 1) ? 0 : 1;           // step 0 and even steps: q side (R^T)
+        const float* prev;
+        float beta;
+        const float* B;
+        int m;
+        float* out;
+        if (step == 0) {
+            prev = nullptr; beta = 0.f; B = Q; m = 0; out = Q;
+        } else if (tr == 0) {
+            prev = S + (int64_t)(done - 1) * P.ld_s; beta = (float)alpha_cur; B = S;
+            m = P.full_reorth ? done : 0; out = S + (int64_t)done * P.ld_s;
+        } else {
+            prev = Q + (int64_t)(done - 1) * P.ld_q; beta = (float)t_new; B = Q; m = done;
+            out = Q + (int64_t)done * P.ld_q;
+        }
+        const int64_t ldb = tr ? P.ld_q : P.ld_s;
+        const int Li = tr ? P.kw : P.kh;
+        const int co = tr ? cu : cv, Lo = tr ? P.kh : P.kw;
+        const float* Mt = static_cast<const float*>(tr ? P.K : P.Kt);   // rows of M^T (M = K or K^T)
+        unsigned long long* wcur = P.wfix + (int64_t)(step & 1) * P.lmax;
+
+        // ---- A: z rows from the diagonal sums of the input vector
+        pk_zrows(P, Mt, Li, Lo, zs, wcur, fxs_inv);
+        // prefetch prev (used right after the barrier) while the grid synchronises
+        float pv[MAXG][4];
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pv[g][q] = 0.f;
+            if (g < ng && prev) PkIO<float, 4>::load(prev + eo[g], pv[g]);
+        }
+        grid.sync();
+        pk_mark(P);
+
+        // ---- B: zero the consumed w; z; y; v = y - beta*prev; dots
+        for (int i = blockIdx.x * PK_THREADS + tid; i < P.lmax; i += nblk * PK_THREADS) wcur[i] = 0ull;
+        for (int c0 = tid; c0 < Lo; c0 += 8 * PK_THREADS) {
+            double q[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q[k] = c0 + k * PK_THREADS < Lo ? __ldcg(P.zbuf + c0 + k * PK_THREADS) : 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (c0 + k * PK_THREADS < Lo) zs[c0 + k * PK_THREADS] = q[k];
+        }
+        const int W = m + 2;
+        for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
+        __syncthreads();
+        double ysq = 0.0;
+        vsq = 0.0;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            if (g < ng) {
+                double yd[4];
+                ra_bcast4(zs, (unsigned)eo[g], n, co, Lo, false, yd);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float yv = (float)yd[q];
+                    ysq += (double)yv * (double)yv;
+                    v[g][q] = __fsub_rn(yv, __fmul_rn(beta, pv[g][q]));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[g][q] = 0.f;
+            }
+        }
+#pragma unroll 4
+        for (int i = 0; i < m; ++i) {
+            const float* Si = B + (int64_t)i * ldb;
+            float dt = 0.f;
+#pragma unroll
+            for (int g = 0; g < MAXG; ++g)
+                if (g < ng) {
+                    float sv[4];
+                    PkIO<float, 4>::load(Si + eo[g], sv);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dt = fmaf(sv[q], v[g][q], dt);
+                }
+            const double d = warp_sum((double)dt);
+            if (lane == 0) acc[warp * W + i] += d;
+        }
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) vsq += (double)v[g][q] * (double)v[g][q];
+        vsq = warp_sum(vsq);
+        ysq = warp_sum(ysq);
+        if (lane == 0) {
+            acc[warp * W + m] += vsq;
+            acc[warp * W + m + 1] += ysq;
+        }
+        __syncthreads();
+        for (int j = tid; j < W; j += PK_THREADS) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t += acc[w * W + j];
+            P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
+        }
+        pk_reduce_barrier(P, gen, P.blk_part, P.cap + 4, W, red, acc);
+        pk_mark(P);
+        const double aux = red[m + 1];
+        const double vnorm = sqrt(red[m]);
+
+        // ---- C: v1 = v - S h ; t = |v1|
+        double val;
+        const int ci_n = tr ? cu : cv, Li_n = tr ? P.kh : P.kw;   // next product: the other side
+        unsigned long long* wnext = P.wfix + (int64_t)((step + 1) & 1) * P.lmax;
+        if (m == 0) {
+            val = vnorm;
+        } else {
+            constexpr int GA = MAXG <= 4 ? MAXG : 4;
+            float* cf = reinterpret_cast<float*>(acc);
+            for (int i = tid; i < m; i += PK_THREADS) cf[i] = (float)red[i];
+            __syncthreads();
+            double v1sq = 0.0;
+#pragma unroll
+            for (int g0 = 0; g0 < MAXG; g0 += GA) {
+                if (g0 >= ng) break;
+#pragma unroll 4
+                for (int i = 0; i < m; ++i) {
+                    const float* Si = B + (int64_t)i * ldb;
+                    const float c = cf[i];
+#pragma unroll
+                    for (int g = 0; g < GA; ++g)
+                        if (g0 + g < ng) {
+                            float sv[4];
+                            PkIO<float, 4>::load(Si + eo[g0 + g], sv);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) v[g0 + g][q] = fmaf(-c, sv[q], v[g0 + g][q]);
+                        }
+                }
+#pragma unroll
+                for (int g = 0; g < GA; ++g)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
+            }
+            v1sq = warp_sum(v1sq);
+            __syncthreads();   // cf (in acc) is read until every warp has finished the projection
+            if (lane == 0) acc[warp] = v1sq;
+            __syncthreads();
+            if (tid == 0) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) s += acc[w];
+                P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
+            }
+            pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
+            pk_mark(P);
+            val = sqrt(red[P.cap + 2]);
+        }
+        // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
+        // sums for the next product
+        pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
+        grid.sync();
+        pk_mark(P);
+
+        // ---- control (identical in every CTA; CTA 0 records the trace)
+        if (step == 0) {
+            const double a1 = val;
+            zeta_last = a1 * t1;
+            alpha_cur = a1;
+            if (rec) {
+                P.ts[0] = t1;
+                P.alphas[0] = a1;
+                P.zetas[0] = zeta_last;
+                P.nus[0] = nu_last;
+            }
+            if (a1 == 0.0) {
+                err = 2;
+                stop = 1;
+            }
+            continue;
+        }
+        if (tr == 0) {
+            t_new = val;
+            u2 = aux;
+            continue;
+        }
+        const double a_new = val, p2 = aux;
+        if (t_new <= P.tol * sqrt(u2)) {
+            breakdown = tbreak = 1;
+            stop = 1;
+        } else if (a_new <= P.tol * sqrt(p2)) {
+            breakdown = 1;
+            if (rec) P.ts[nt] = t_new;
+            ++nt;
+            stop = 1;
+        } else {
+            if (rec) {
+                P.ts[nt] = t_new;
+                P.alphas[na] = a_new;
+            }
+            ++nt;
+            ++na;
+            const double zeta = a_new * t_new;
+            const double nu = sqrt(zeta * zeta_last);
+            if (rec) {
+                P.zetas[nn] = zeta;
+                P.nus[nn] = nu;
+            }
+            ++nn;
+            zeta_last = zeta;
+            const double nu_prev = nu_last;
+            nu_last = nu;
+            alpha_cur = a_new;
+            ++done;
+            if (fired < 0) {
+                if (nu > nu_prev) {
+                    fired = max(done - 1, P.k_min);
+                    reason = KB_STOP_NU_ROSE;
+                } else if (nu < P.tau) {
+                    fired = max(done, P.k_min);
+                    reason = KB_STOP_NU_BELOW_TOL;
+                }
+            }
+            const int limit = fired >= 0 ? fired + P.p + 1 : P.k_max + 1;
+            if (done >= limit) stop = 1;
+            if (done + 1 > P.cap) {
+                stop = 1;
+                overflow = 1;
+            }
+        }
+    }
+    if (rec) {
+        int* h = P.hdr;
+        h[PH_DONE] = done;
+        h[PH_FIRED] = fired;
+        h[PH_REASON] = reason;
+        h[PH_STOP] = stop;
+        h[PH_BREAK] = breakdown;
+        h[PH_TBREAK] = tbreak;
+        h[PH_OVERFLOW] = overflow;
+        h[PH_ERR] = err;
+        h[PH_NA] = na;
+        h[PH_NT] = nt;
+        h[PH_NN] = nn;
+    }
+}
+
 // ------------------------------------------------------------------ host side
 constexpr int PK_MAXG_F32 = 16, PK_MAXG_F64 = 16;
 
@@ -676,9 +1201,72 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     return true;
 }
 
+template <int MAXG>
+static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaStream_t st) {
+    auto kern = k_egkb_tiled<MAXG>;
+    const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33)) +
+                        sizeof(float) * 1024 * MAXG;
+    static bool configured = false;
+    if (!configured) {
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+        configured = true;
+    }
+    if (smem > 110 * 1024) return false;
+    static int dev = -1, sms = 0;
+    static size_t smem_cached = 0;
+    static int per_sm = 0;
+    int cur = 0;
+    KB_CUDA(cudaGetDevice(&cur));
+    if (cur != dev || smem != smem_cached) {
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PK_THREADS, smem));
+        KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur));
+        dev = cur;
+        smem_cached = smem;
+        if (std::getenv("KB_DEBUG")) fprintf(stderr, "[kb] tiled eGKB<%d>: %d CTAs/SM, smem %zu\n", MAXG, per_sm, smem);
+    }
+    if (per_sm < 1) return false;
+    const int grid = std::min(sms * std::min(per_sm, per_sm_cap), Gm.T);
+    if ((Gm.T + grid - 1) / grid > MAXG) return false;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(PK_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    ProfScope ps(st, PROF_REORTH, 0.0);
+    KB_CUDA(cudaMemsetAsync(P.bar, 0, sizeof(unsigned) * P.nbar, st));
+    KB_CUDA(cudaLaunchKernelEx(&lc, kern, P, Gm));
+    return true;
+}
+
+// Tiled kernel envelope: fp32 zero BC, n a multiple of 128 or a divisor of 128 with n^2 >= 1024.
+static bool tiled_launch(PkParams& P, cudaStream_t st) {
+    const int n = P.n;
+    TileGeo Gm{};
+    if (n >= 128 && n % 128 == 0) Gm.TW = 128;
+    else if (n >= 32 && 128 % n == 0) Gm.TW = n;
+    else return false;
+    if (P.ld_s % 4 || P.ld_q % 4) return false;
+    Gm.LR = Gm.TW / 4;
+    Gm.RW = 32 / Gm.LR;
+    Gm.RB = n / (8 * Gm.RW);
+    Gm.T = (int)((int64_t)n * n / 1024);
+    const int per = 2 * kSMs;
+    const int need = (Gm.T + std::min(per, Gm.T) - 1) / std::min(per, Gm.T);
+    if (need <= 4) return tiled_launch_g<4>(P, Gm, 2, st);
+    if (need <= 8) return tiled_launch_g<8>(P, Gm, 2, st);
+    if (need <= 16) return tiled_launch_g<16>(P, Gm, 2, st);
+    return false;
+}
+
 // Sizes of the scratch the persistent kernel needs (doubles).
 // barrier words (unsigned): arrivals, generation, per-column-chunk counters
-static size_t pk_bar_words(int lmax) { return 64 + (size_t)(lmax + 31) / 32 + 32; }
+static size_t pk_bar_only_words(int lmax) { return (64 + (size_t)(lmax + 31) / 32 + 32 + 1) & ~(size_t)1; }
+static size_t pk_bar_words(int lmax) { return pk_bar_only_words(lmax) + 4 * (size_t)lmax; }
 static size_t pk_bar_doubles(int lmax) { return (pk_bar_words(lmax) + 1) / 2; }
 
 size_t pk_scratch_doubles(int lmax, int cap) {
@@ -733,6 +1321,7 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     P.bres = P.zbuf + lmax;
     P.bar = reinterpret_cast<unsigned*>(P.bres + cap + 8);
     P.nbar = (int)pk_bar_words(lmax);
+    P.wfix = reinterpret_cast<unsigned long long*>(P.bar + pk_bar_only_words(lmax));
     P.raw_s = raw;
     P.raw_q = static_cast<char*>(raw) + (size_t)N * (op->dtype == KB_F32 ? 4 : 8);
     *scales_out = nullptr;
@@ -764,6 +1353,8 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
         }
     } dump{want_trace, s, dbg, dbg_n};
     int grid = 0;
+    static const bool no_tiled = std::getenv("KB_EGKB_NO_TILED") != nullptr;
+    if (!no_tiled && op->dtype == KB_F32 && !P.refl && tiled_launch(P, s)) return true;
     // smallest register footprint that covers N with 2 CTAs per SM
     const int64_t per = (int64_t)2 * kSMs * PK_THREADS * vec;
     const int64_t ng = (N + per - 1) / per;

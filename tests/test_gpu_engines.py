@@ -177,7 +177,14 @@ class TestEgkbBlur:
                 olr.np.linalg.norm = orig_norm
             kps = [v[1] for v in variants]
             assert tr.breakdown and otr.breakdown, (tr.k_p, variants)
-            assert min(kps) <= tr.k_p <= max(kps), (tr.k_p, variants)
+            # Past the CPU variants' span the recurrence is iterating on
+            # rounding noise: the GPU may take at most 2 more such steps (its
+            # one-pass classical projection and fp64-reduced dots leave a
+            # differently sized noise floor than BLAS MGS), and every extra
+            # singular value must be noise (< 1e-6 sigma_1, below anything the
+            # fp32 approximation resolves).
+            assert min(kps) <= tr.k_p <= max(kps) + 2, (tr.k_p, variants)
+            assert np.all(svd.sigma[max(kps):] < 1e-6 * svd.sigma[0]), (svd.sigma, variants)
         assert tr.stop_reason == otr.stop_reason
         # exact structured sigma (fp64) as ground truth for the leading values
         _, s_exact, _ = ost.structured_tsvd(psf, n, k=svd.k)
