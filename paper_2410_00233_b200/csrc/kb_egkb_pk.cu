@@ -669,6 +669,37 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
 // partial arrays, and every fp32 entry above 2^-(61 - log2 n) enters the
 // sum exactly (w is at least as accurate as an fp64 summation).
 
+// ---- per-thread copy ring: each thread streams its own float4 of every owned
+// tile of the next basis vectors into shared memory with cp.async (16 B,
+// L2 only), PK_NS vectors ahead, so the dots / projection loops keep many
+// vectors in flight without holding them in registers.  A thread reads back
+// only what it copied itself: no cross-thread synchronisation is needed.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int PK_NS = 4;   // ring stages (basis vectors in flight per thread)
+
+// Item G of the thread's stream (stage G % PK_NS) <- its float4 of each owned tile of `vec`
+// (vec == nullptr: an empty group, keeps the group accounting uniform).
+template <int MAXG>
+__device__ __forceinline__ void ring_fill(float* ring, int stage_floats, int tbo, unsigned G, const float* vec,
+                                          const int (&eo)[MAXG], int ng) {
+    if (vec) {
+        float* dst = ring + (int)(G % PK_NS) * stage_floats + tbo;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g)
+            if (g < ng) cp_async16(dst + g * 1024, vec + eo[g]);
+    }
+    cp_async_commit();
+}
+
 struct TileGeo {
     int TW, LR, RW, RB, T;   // tile width, lanes per row, rows per warp, row blocks, tiles
 };
@@ -853,6 +884,10 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     double* red = zs + P.lmax;                     // [cap + 4]
     double* acc = red + P.cap + 4;                 // [8][max(cap + 2, 33)]
     float* tb = reinterpret_cast<float*>(acc + 8 * max(P.cap + 2, 33));   // [MAXG * 1024]
+    // basis streaming ring (MAXG <= 4): PK_NS stages after the tile buffer
+    constexpr bool STREAM = MAXG <= 4;
+    float* ringb = tb + MAXG * 1024;
+    constexpr int SF = MAXG * 1024;                // floats per stage
     const bool rec = (blockIdx.x == 0 && tid == 0);
     const int cu = P.kh / 2, cv = P.kw / 2;
     unsigned gen = 0;
@@ -869,7 +904,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         eo[g] = a * n + cb * Gm.TW + (lane % Gm.LR) * 4;
     }
     const int tbo = warp * 128 + lane * 4;         // this thread's float4 inside a staged tile
-
+    unsigned rbase = 0;                            // items streamed so far (uniform)
     // ---- prologue: v <- y0, t1 = |y0|, diagonal sums of y0 for step 0 (R^T, q side)
     float v[MAXG][4];
     double vsq = 0.0;
@@ -933,7 +968,14 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         const float* Mt = static_cast<const float*>(tr ? P.K : P.Kt);   // rows of M^T (M = K or K^T)
         unsigned long long* wcur = P.wfix + (int64_t)(step & 1) * P.lmax;
 
-        // ---- A: z rows from the diagonal sums of the input vector
+        // ---- A: z rows from the diagonal sums of the input vector.  The ring
+        // starts fetching the first basis vectors of the dots (phase B) now.
+        if constexpr (STREAM) {
+            if (m > 0)
+#pragma unroll
+                for (int k = 0; k < PK_NS; ++k)
+                    ring_fill<MAXG>(ringb, SF, tbo, rbase + k, k < 2 * m ? B + (int64_t)(k % m) * ldb : nullptr, eo, ng);
+        }
         pk_zrows(P, Mt, Li, Lo, zs, wcur, fxs_inv);
         // prefetch prev (used right after the barrier) while the grid synchronises
         float pv[MAXG][4];
@@ -977,6 +1019,28 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 for (int q = 0; q < 4; ++q) v[g][q] = 0.f;
             }
         }
+        if constexpr (STREAM) {
+            // items rbase .. rbase + m - 1 of the stream: the basis vectors in order
+            for (int i = 0; i < m; ++i) {
+                const unsigned G = rbase + i;
+                cp_async_wait<PK_NS - 1>();
+                const float* sb = ringb + (int)(G % PK_NS) * SF + tbo;
+                float dt = 0.f;
+#pragma unroll
+                for (int g = 0; g < MAXG; ++g)
+                    if (g < ng) {
+                        const float4 sv = *reinterpret_cast<const float4*>(sb + g * 1024);
+                        dt = fmaf(sv.x, v[g][0], dt);
+                        dt = fmaf(sv.y, v[g][1], dt);
+                        dt = fmaf(sv.z, v[g][2], dt);
+                        dt = fmaf(sv.w, v[g][3], dt);
+                    }
+                ring_fill<MAXG>(ringb, SF, tbo, G + PK_NS, i + PK_NS < 2 * m ? B + (int64_t)((i + PK_NS) % m) * ldb : nullptr,
+                                eo, ng);
+                const double d = warp_sum((double)dt);
+                if (lane == 0) acc[warp * W + i] += d;
+            }
+        } else {
 #pragma unroll 4
         for (int i = 0; i < m; ++i) {
             const float* Si = B + (int64_t)i * ldb;
@@ -991,6 +1055,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 }
             const double d = warp_sum((double)dt);
             if (lane == 0) acc[warp * W + i] += d;
+        }
         }
 #pragma unroll
         for (int g = 0; g < MAXG; ++g)
@@ -1026,6 +1091,30 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int i = tid; i < m; i += PK_THREADS) cf[i] = (float)red[i];
             __syncthreads();
             double v1sq = 0.0;
+            if constexpr (STREAM) {
+                // items rbase + m .. rbase + 2m - 1: the same basis vectors again
+                for (int i = 0; i < m; ++i) {
+                    const unsigned G = rbase + m + i;
+                    cp_async_wait<PK_NS - 1>();
+                    const float* sb = ringb + (int)(G % PK_NS) * SF + tbo;
+                    const float c = cf[i];
+#pragma unroll
+                    for (int g = 0; g < MAXG; ++g)
+                        if (g < ng) {
+                            const float4 sv = *reinterpret_cast<const float4*>(sb + g * 1024);
+                            v[g][0] = fmaf(-c, sv.x, v[g][0]);
+                            v[g][1] = fmaf(-c, sv.y, v[g][1]);
+                            v[g][2] = fmaf(-c, sv.z, v[g][2]);
+                            v[g][3] = fmaf(-c, sv.w, v[g][3]);
+                        }
+                    ring_fill<MAXG>(ringb, SF, tbo, G + PK_NS, i + PK_NS < m ? B + (int64_t)(i + PK_NS) * ldb : nullptr,
+                                    eo, ng);
+                }
+#pragma unroll
+                for (int g = 0; g < MAXG; ++g)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v1sq += (double)v[g][q] * (double)v[g][q];
+            } else {
 #pragma unroll
             for (int g0 = 0; g0 < MAXG; g0 += GA) {
                 if (g0 >= ng) break;
@@ -1047,6 +1136,8 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
 #pragma unroll
                     for (int q = 0; q < 4; ++q) v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
             }
+            }
+            rbase += 2 * m;
             v1sq = warp_sum(v1sq);
             __syncthreads();   // cf (in acc) is read until every warp has finished the projection
             if (lane == 0) acc[warp] = v1sq;
@@ -1205,7 +1296,7 @@ template <int MAXG>
 static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaStream_t st) {
     auto kern = k_egkb_tiled<MAXG>;
     const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33)) +
-                        sizeof(float) * 1024 * MAXG;
+                        sizeof(float) * 1024 * MAXG * (MAXG <= 4 ? 1 + PK_NS : 1);
     static bool configured = false;
     if (!configured) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
@@ -1255,11 +1346,12 @@ static bool tiled_launch(PkParams& P, cudaStream_t st) {
     Gm.RW = 32 / Gm.LR;
     Gm.RB = n / (8 * Gm.RW);
     Gm.T = (int)((int64_t)n * n / 1024);
-    const int per = 2 * kSMs;
+    static const int cps = std::getenv("KB_PK_CTAS_PER_SM") ? std::atoi(std::getenv("KB_PK_CTAS_PER_SM")) : 2;
+    const int per = cps * kSMs;
     const int need = (Gm.T + std::min(per, Gm.T) - 1) / std::min(per, Gm.T);
-    if (need <= 4) return tiled_launch_g<4>(P, Gm, 2, st);
-    if (need <= 8) return tiled_launch_g<8>(P, Gm, 2, st);
-    if (need <= 16) return tiled_launch_g<16>(P, Gm, 2, st);
+    if (need <= 4) return tiled_launch_g<4>(P, Gm, cps, st);
+    if (need <= 8) return tiled_launch_g<8>(P, Gm, cps, st);
+    if (need <= 16) return tiled_launch_g<16>(P, Gm, cps, st);
     return false;
 }
 

@@ -66,6 +66,38 @@ def upload(a: np.ndarray, dtype) -> torch.Tensor:
     return stage.to(device(), non_blocking=True)
 
 
+class _PinnedStage:
+    """One reusable pinned staging buffer for small stream-ordered uploads
+    (a fresh pinned allocation per call costs ~50-80 us of host time).  The
+    buffer is rewritten only after the previous copy out of it has finished
+    (event), so an in-flight upload is never clobbered."""
+
+    def __init__(self):
+        self._buf = None
+        self._event = None
+
+    def upload(self, host: np.ndarray) -> torch.Tensor:
+        host = np.ascontiguousarray(host).view(np.uint8).reshape(-1)
+        n = host.size
+        if self._buf is None or self._buf.numel() < n:
+            if self._event is not None:
+                self._event.synchronize()
+            self._buf = torch.empty(max(n, 1 << 16), dtype=torch.uint8, pin_memory=True)
+            self._event = None
+        if self._event is not None:
+            self._event.synchronize()
+        self._buf.numpy()[:n] = host
+        dev = torch.empty(n, dtype=torch.uint8, device=device())
+        dev.copy_(self._buf[:n], non_blocking=True)
+        if self._event is None:
+            self._event = torch.cuda.Event()
+        self._event.record()
+        return dev
+
+
+PINNED = _PinnedStage()
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 

@@ -240,11 +240,7 @@ class _LazyLift:
         host = np.zeros(total, dtype=np.uint8)
         for b, o in zip(blocks + [sig], offs):
             host[o:o + b.nbytes] = b.view(np.uint8).reshape(-1)
-        import torch
-
-        stage = torch.empty(total, dtype=torch.uint8, pin_memory=True)
-        stage.numpy()[:] = host
-        dev = stage.to(D.device(), non_blocking=True)
+        dev = D.PINNED.upload(host)
         self._dev = dev                                 # keeps the views' storage alive
         self.sigma_host = sig
         self.parts = []
@@ -317,9 +313,9 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     if reorth is None:
         reorth = REORTH_FULL if dtype == np.float32 else REORTH_ONE_SIDED
 
+    y0d = None
     if y0 is None:
-        # the reference's draws (lowrank.py:199-201), generated on the device
-        y0d = rng.standard_normal(config.seed, mbar, dtype)
+        pass   # drawn on the device right before the launch (below)
     elif D.is_tensor(y0):
         y0d = D.to_device(y0, dtype)
         if tuple(y0d.shape) != (mbar,):
@@ -347,6 +343,10 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     st.q_scale_host = hist[5].ctypes.data_as(dp)
     nb = C.c_size_t()
     _lib.check(lib.kb_egkb_workspace_bytes(C.byref(op.struct), cap, C.byref(nb)))
+    if y0d is None:
+        # the reference's draws (lowrank.py:199-201), generated on the device; launched
+        # after the host-side set-up so the RNG and the eGKB kernels run back to back
+        y0d = rng.standard_normal(config.seed, mbar, dtype)
     ws, wsb = D.WORKSPACE.get(nb.value)
     status = lib.kb_egkb_run(C.byref(op.struct), C.byref(cfg), y0d.data_ptr(), C.byref(st), ws, wsb,
                              D.stream_ptr())
