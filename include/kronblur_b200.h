@@ -172,6 +172,15 @@ typedef struct {
     /* outputs */
     int n_alphas, n_ts, n_nus;
     int chosen_k, k_p, rows, stop_reason, breakdown;
+    /* optional: the small SVD of C (lowrank.py:308-316) inside the call.  When
+     * wu_dev != NULL the host computes it (fp64 one-sided Jacobi) right after
+     * the loop and uploads, stream-ordered, W_u = U_C[:, :chosen] (rows x
+     * chosen) to wu_dev and W_v = V_C[:, :chosen] (k_p x chosen) to wv_dev
+     * (working dtype, row stride chosen; capacity^2 elements each suffice) and
+     * sigma (fp64 of the working-precision values) to sigma_dev; sigma_host
+     * (capacity doubles) gets the same values -- the caller's lift reads the
+     * weights on the device without another host step. */
+    void* wu_dev; void* wv_dev; double* sigma_dev; double* sigma_host;
 } kb_egkb_state;
 
 /* Minimum basis capacity for a config (vectors). */

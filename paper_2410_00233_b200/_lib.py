@@ -50,7 +50,8 @@ class KbEgkbState(C.Structure):
                 ("s_scale_host", dp), ("q_scale_host", dp),
                 ("n_alphas", C.c_int), ("n_ts", C.c_int), ("n_nus", C.c_int),
                 ("chosen_k", C.c_int), ("k_p", C.c_int), ("rows", C.c_int),
-                ("stop_reason", C.c_int), ("breakdown", C.c_int)]
+                ("stop_reason", C.c_int), ("breakdown", C.c_int),
+                ("wu_dev", vp), ("wv_dev", vp), ("sigma_dev", dp), ("sigma_host", dp)]
 
 
 class KbKron(C.Structure):

@@ -278,6 +278,101 @@ static EgkbWs egkb_ws_make(const kb_operator* op, int capacity, Arena& a) {
 
 static double eps_of(int dtype) { return dtype == KB_F32 ? 1.1920928955078125e-07 : 2.220446049250313e-16; }
 
+// Thin SVD of the lower-bidiagonal C (rows x k; C[i,i] = alphas[i],
+// C[i+1,i] = ts[i+1]; lowrank.py:308-316) on the host: one-sided (Hestenes)
+// Jacobi in fp64, cyclic pair order, converged to 1e-15 (high relative
+// accuracy on a bidiagonal; ~10 us for k = 13), sorted descending.  Then
+// W_u = U_C[:, :chosen], W_v = V_C[:, :chosen] (working dtype, row stride
+// chosen) and sigma (fp64 of the working-precision values) go to the device
+// in one stream-ordered copy from pinned memory -- the lift reads them there.
+static void svd_c_upload(int dtype, const double* alphas, const double* ts, int rows, int k, int chosen,
+                         kb_egkb_state* st, cudaStream_t s) {
+    std::vector<double> A((size_t)rows * k, 0.0), V((size_t)k * k, 0.0);   // column-major
+    for (int j = 0; j < k; ++j) {
+        A[(size_t)j * rows + j] = alphas[j];
+        if (j + 1 < rows) A[(size_t)j * rows + j + 1] = ts[j + 1];
+        V[(size_t)j * k + j] = 1.0;
+    }
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rot = false;
+        for (int p = 0; p < k - 1; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                double* Ap = &A[(size_t)p * rows];
+                double* Aq = &A[(size_t)q * rows];
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = 0; i < rows; ++i) {
+                    al += Ap[i] * Ap[i];
+                    be += Aq[i] * Aq[i];
+                    ga += Ap[i] * Aq[i];
+                }
+                if (ga == 0.0 || !(ga * ga > 1e-30 * al * be)) continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+                for (int i = 0; i < rows; ++i) {
+                    const double u = Ap[i], w = Aq[i];
+                    Ap[i] = c * u - sn * w;
+                    Aq[i] = sn * u + c * w;
+                }
+                double* Vp = &V[(size_t)p * k];
+                double* Vq = &V[(size_t)q * k];
+                for (int i = 0; i < k; ++i) {
+                    const double u = Vp[i], w = Vq[i];
+                    Vp[i] = c * u - sn * w;
+                    Vq[i] = sn * u + c * w;
+                }
+                rot = true;
+            }
+        if (!rot) break;
+    }
+    std::vector<double> sig(k);
+    std::vector<int> perm(k);
+    for (int j = 0; j < k; ++j) {
+        double s2 = 0.0;
+        for (int i = 0; i < rows; ++i) s2 += A[(size_t)j * rows + i] * A[(size_t)j * rows + i];
+        sig[j] = std::sqrt(s2);
+        perm[j] = j;
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return sig[a] > sig[b]; });
+    // staging: [W_u | W_v | sigma], 16-byte aligned blocks (pinned, reused once the copy is done)
+    const size_t esz = dtype == KB_F32 ? 4 : 8;
+    const size_t bu = (size_t)rows * chosen * esz, bv = (size_t)k * chosen * esz, bs = sizeof(double) * chosen;
+    static thread_local char* stage = nullptr;
+    static thread_local size_t stage_bytes = 0;
+    static thread_local cudaEvent_t done = nullptr;
+    if (!done) KB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    KB_CUDA(cudaEventSynchronize(done));   // the previous upload out of `stage` has finished
+    const size_t need = bu + bv + bs;
+    if (stage_bytes < need) {
+        if (stage) cudaFreeHost(stage);
+        KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage), need));
+        stage_bytes = need;
+    }
+    char* pu = stage;
+    char* pv = stage + bu;
+    double* ps = reinterpret_cast<double*>(stage + bu + bv);
+    for (int c = 0; c < chosen; ++c) {
+        const int j = perm[c];
+        const double sv = sig[j];
+        ps[c] = dtype == KB_F32 ? (double)(float)sv : sv;
+        st->sigma_host[c] = ps[c];
+        for (int i = 0; i < rows; ++i) {
+            const double u = sv > 0.0 ? A[(size_t)j * rows + i] / sv : 0.0;
+            if (dtype == KB_F32) reinterpret_cast<float*>(pu)[(size_t)i * chosen + c] = (float)u;
+            else reinterpret_cast<double*>(pu)[(size_t)i * chosen + c] = u;
+        }
+        for (int i = 0; i < k; ++i) {
+            const double w = V[(size_t)j * k + i];
+            if (dtype == KB_F32) reinterpret_cast<float*>(pv)[(size_t)i * chosen + c] = (float)w;
+            else reinterpret_cast<double*>(pv)[(size_t)i * chosen + c] = w;
+        }
+    }
+    KB_CUDA(cudaMemcpyAsync(st->wu_dev, pu, bu, cudaMemcpyHostToDevice, s));
+    KB_CUDA(cudaMemcpyAsync(st->wv_dev, pv, bv, cudaMemcpyHostToDevice, s));
+    KB_CUDA(cudaMemcpyAsync(st->sigma_dev, ps, bs, cudaMemcpyHostToDevice, s));
+    KB_CUDA(cudaEventRecord(done, s));
+}
+
 static int egkb_capacity(const kb_egkb_config* c) {
     // Loop limit is fired_k + p + 1 with fired_k <= max(k_max, k_min), else
     // k_max + 1; the left basis may hold one more vector than iterations.
@@ -578,6 +673,10 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     if (chosen < 1 || k_p < 1) {
         set_error("bidiagonalization broke down before producing any factors");
         throw Fail{KB_ENUMERICAL};
+    }
+    if (st->wu_dev) {   // small SVD of C (host, C++) and the lift weights, uploaded stream-ordered
+        KB_REQUIRE(st->wv_dev && st->sigma_dev && st->sigma_host, "SVD outputs incomplete");
+        svd_c_upload(op->dtype, ht, ht + cap, rows, k_p, chosen, st, s);
     }
     st->n_alphas = hh[H_NA];
     st->n_ts = hh[H_NT];

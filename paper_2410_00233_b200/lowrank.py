@@ -224,29 +224,14 @@ class _LazyLift:
     kronop.py:117-119) -- the same bits as materialising then assembling.
     """
 
-    def __init__(self, code, s_part, q_part, cols, shape, sigma):
-        from . import device as D
-
+    def __init__(self, code, s_part, q_part, cols, shape, sigma, keep, sigma_ptr):
+        # s_part / q_part: (basis, rows used, device pointer of the weights, row stride cols);
+        # `keep` owns the weights and sigma (device); sigma: host fp64 copy
         self.code, self.cols, self.shape = code, cols, shape
-        # W_u, W_v (working dtype) and sigma (fp64) travel in ONE pinned upload
-        dt = D.np_dtype(s_part[0])
-        blocks = [np.ascontiguousarray(w[:nrows], dtype=dt) for _, nrows, w in (s_part, q_part)]
-        sig = np.ascontiguousarray(sigma, dtype=np.float64)
-        offs, total = [], 0
-        for b in blocks + [sig]:
-            total = (total + 15) // 16 * 16
-            offs.append(total)
-            total += b.nbytes
-        host = np.zeros(total, dtype=np.uint8)
-        for b, o in zip(blocks + [sig], offs):
-            host[o:o + b.nbytes] = b.view(np.uint8).reshape(-1)
-        dev = D.PINNED.upload(host)
-        self._dev = dev                                 # keeps the views' storage alive
-        self.sigma_host = sig
-        self.parts = []
-        for (basis, nrows, _), b, o in zip((s_part, q_part), blocks, offs):
-            self.parts.append((basis, nrows, dev[o:o + b.nbytes].view(D.torch_dtype(dt)).reshape(b.shape)))
-        self.sigma_dev = dev[offs[2]:offs[2] + sig.nbytes].view(D.torch_dtype(np.float64))
+        self.parts = [s_part, q_part]
+        self._keep = keep
+        self.sigma_host = np.asarray(sigma, dtype=np.float64)
+        self.sigma_ptr = sigma_ptr
 
     def materialize(self):
         from . import device as D
@@ -255,7 +240,7 @@ class _LazyLift:
         for basis, nrows, wd in self.parts:
             length = basis.shape[1]
             rows_out = D.empty((self.cols, length), D.np_dtype(basis))
-            _lib.check(_lib.load().kb_ts_lift(self.code, basis.data_ptr(), length, nrows, wd.data_ptr(), self.cols,
+            _lib.check(_lib.load().kb_ts_lift(self.code, basis.data_ptr(), length, nrows, wd, self.cols,
                                               rows_out.data_ptr(), length, length, D.stream_ptr()), "lift")
             out.append(rows_out)
         self.parts = None
@@ -266,10 +251,10 @@ class _LazyLift:
 
         if not np.array_equal(np.asarray(sigma, dtype=np.float64), self.sigma_host):
             raise ValidationError("lazy lift: sigma does not belong to this factorisation")
-        for (basis, nrows, wd), out, scale in zip(self.parts, (f, g), (self.sigma_dev, None)):
+        for (basis, nrows, wd), out, scale in zip(self.parts, (f, g), (self.sigma_ptr, None)):
             length = basis.shape[1]
-            _lib.check(_lib.load().kb_lift_assemble(self.code, basis.data_ptr(), length, nrows, wd.data_ptr(),
-                                                    self.cols, None if scale is None else scale.data_ptr(),
+            _lib.check(_lib.load().kb_lift_assemble(self.code, basis.data_ptr(), length, nrows, wd,
+                                                    self.cols, scale,
                                                     out.data_ptr(), length, length, D.stream_ptr()),
                        "lift+assemble")
 
@@ -331,7 +316,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     lib = _lib.load()
     cap = lib.kb_egkb_capacity(C.byref(cfg))
     s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
-    hist = np.zeros((6, cap), dtype=np.float64)
+    hist = np.zeros((7, cap), dtype=np.float64)
     dp = C.POINTER(C.c_double)
     st = _lib.KbEgkbState()
     st.s_basis, st.ld_s, st.q_basis, st.ld_q, st.capacity = s_basis.data_ptr(), mbar, q_basis.data_ptr(), nbar, cap
@@ -341,6 +326,16 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     st.nus_host = hist[3].ctypes.data_as(dp)
     st.s_scale_host = hist[4].ctypes.data_as(dp)
     st.q_scale_host = hist[5].ctypes.data_as(dp)
+    # the small SVD of C and the lift weights are computed on the device right after the
+    # loop (kb_egkb_state.wu_dev): W_u, W_v (working dtype) and sigma (fp64) in one buffer
+    esz = np.dtype(dtype).itemsize
+    wbytes = (cap * cap * esz + 15) // 16 * 16
+    svdbuf = D.empty(((2 * wbytes + 8 * cap) // 8,), np.float64)
+    wu_ptr = svdbuf.data_ptr()
+    wv_ptr = wu_ptr + wbytes
+    st.wu_dev, st.wv_dev = wu_ptr, wv_ptr
+    st.sigma_dev = C.cast(C.c_void_p(wu_ptr + 2 * wbytes), dp)
+    st.sigma_host = hist[6].ctypes.data_as(dp)
     nb = C.c_size_t()
     _lib.check(lib.kb_egkb_workspace_bytes(C.byref(op.struct), cap, C.byref(nb)))
     if y0d is None:
@@ -359,17 +354,11 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     trace.nus = [float(v) for v in hist[3, : st.n_nus]]
     k_p, rows, chosen = st.k_p, st.rows, st.chosen_k
 
-    c_mat = np.zeros((rows, k_p), dtype=dtype)
-    for i in range(k_p):
-        c_mat[i, i] = trace.alphas[i]
-        if i + 1 < rows:
-            c_mat[i + 1, i] = trace.ts[i + 1]
-    core = svd_small(c_mat)   # host LAPACK, as lowrank.py:316
-    # bases may be stored scaled (s_i = stored_i * scale_i): fold into the lift weights
-    s_scale, q_scale = hist[4], hist[5]
-    w_u = core.u[:, :chosen].astype(np.float64) * s_scale[:rows, None]
-    w_v = core.v[:, :chosen].astype(np.float64) * q_scale[:k_p, None]
-    lazy = _LazyLift(op.code, (s_basis, rows, w_u), (q_basis, k_p, w_v), chosen, (mbar, nbar), core.sigma[:chosen])
+    sigma = hist[6, :chosen].copy()            # fp64 of the working-precision values
+    if not np.all(np.isfinite(sigma)):
+        raise NumericalError("bidiagonal SVD produced non-finite singular values")
+    lazy = _LazyLift(op.code, (s_basis, rows, wu_ptr), (q_basis, k_p, wv_ptr), chosen, (mbar, nbar), sigma,
+                     svdbuf, wu_ptr + 2 * wbytes)
     _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
 
     trace.chosen_k = chosen
@@ -377,10 +366,15 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     trace.stop_reason = _lib.KB_STOP[st.stop_reason]
     trace.breakdown = bool(st.breakdown)
     if config.keep_basis:
-        trace.s_basis = (D.to_host(s_basis[:rows]).T * s_scale[:rows]).astype(dtype)
-        trace.q_basis = (D.to_host(q_basis[:k_p]).T * q_scale[:k_p]).astype(dtype)
+        c_mat = np.zeros((rows, k_p), dtype=dtype)
+        for i in range(k_p):
+            c_mat[i, i] = trace.alphas[i]
+            if i + 1 < rows:
+                c_mat[i + 1, i] = trace.ts[i + 1]
+        trace.s_basis = D.to_host(s_basis[:rows]).T.astype(dtype)
+        trace.q_basis = D.to_host(q_basis[:k_p]).T.astype(dtype)
         trace.c_mat = c_mat
-    return TruncatedSvd.from_lift(lazy, core.sigma[:chosen].copy()), trace
+    return TruncatedSvd.from_lift(lazy, sigma.astype(dtype)), trace
 
 
 # ----------------------------------------------------------------- RSVD
