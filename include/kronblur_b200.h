@@ -197,6 +197,15 @@ int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
  * numpy's (k / total).astype(dtype). */
 int kb_div_cast(const double* src, double divisor, int dtype, void* dst, int64_t count, kb_stream_t stream);
 
+/* Psf validation scan (blurmodel.py:25-65): *sum_out = k.sum() of the
+ * C-ordered float64 kernel -- numpy's pairwise summation, bit for bit --
+ * and *min_out = k.min(), using `threads` host threads.  Host only. */
+int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out);
+/* bytes of host memory -> device `dst`, through a library-owned pinned
+ * buffer filled by `threads` host threads, chunk-pipelined with the copies
+ * (stream-ordered on `stream`; the host array may be reused on return). */
+int kb_stage_upload(const void* src, size_t bytes, void* dst, int threads, kb_stream_t stream);
+
 /* dst (cols x rows) = src (rows x cols)^T, row-major, device.  Builds the
  * PSF transpose K^T used by the R(A)^T products on the device (the host
  * uploads K once; blurmodel.py:25-65 Psf.kernel). */

@@ -108,6 +108,8 @@ _SIGS = {
     "kb_egkb_workspace_bytes": (C.c_int, [P(KbOperator), C.c_int, P(SZ)]),
     "kb_transpose": (C.c_int, [C.c_int, vp, i64, i64, vp, vp]),
     "kb_div_cast": (C.c_int, [vp, C.c_double, C.c_int, vp, i64, vp]),
+    "kb_psf_scan": (C.c_int, [vp, i64, C.c_int, dp, dp]),
+    "kb_stage_upload": (C.c_int, [vp, C.c_size_t, vp, C.c_int, vp]),
     "kb_normal_pcg64": (C.c_int, [P(C.c_uint64), P(C.c_uint64), i64, C.c_int, i64, vp, vp, SZ, vp]),
     "kb_normal_workspace_bytes": (C.c_int, [i64, P(SZ)]),
     "kb_normal_test_entries": (None, [C.c_int]),

@@ -40,6 +40,17 @@ def _min(k: np.ndarray) -> float:
     return min(parts)
 
 
+_SCAN_MIN = 1 << 16
+_HOST_THREADS = 8
+
+
+def _scan(k: np.ndarray) -> tuple[float, np.float64]:
+    lib = _lib.load()
+    total, kmin = C.c_double(), C.c_double()
+    _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin)), "kb_psf_scan")
+    return kmin.value, np.float64(total.value)
+
+
 class Psf:
     """Unit-sum, non-negative PSF with odd support (blurmodel.py:25-65).
 
@@ -60,10 +71,17 @@ class Psf:
             raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
         if not (k.flags.c_contiguous or k.flags.f_contiguous):
             k = np.array(k)                           # the reference's order-'K' copy: same reduction order
-        if k.size == 0 or not _min(k) >= 0:          # one reduction; the exact test only when it fails
-            if np.any(k < 0):
+        if k.size >= _SCAN_MIN and k.flags.c_contiguous:
+            # min and numpy's pairwise sum in one multithreaded host pass (kb_psf_scan:
+            # bit-identical to k.sum(), which is single-threaded)
+            kmin, total = _scan(k)
+            if not kmin >= 0 and np.any(k < 0):
                 raise ValidationError("PSF kernel must be non-negative")
-        total = k.sum()
+        else:
+            if k.size == 0 or not _min(k) >= 0:      # one reduction; the exact test only when it fails
+                if np.any(k < 0):
+                    raise ValidationError("PSF kernel must be non-negative")
+            total = k.sum()
         if total <= 0:
             raise ValidationError("PSF kernel must have positive mass")
         self._raw, self._total, self._kernel = k, total, None
@@ -83,9 +101,10 @@ class Psf:
 
         if self._kernel is not None:
             return D.upload(self._kernel, dtype)
-        import torch
-
-        raw = torch.from_numpy(self._raw).to(D.device())
+        raw = D.empty(self._raw.shape, np.float64)
+        src = np.ascontiguousarray(self._raw)
+        _lib.check(_lib.load().kb_stage_upload(src.ctypes.data, src.nbytes, raw.data_ptr(), _HOST_THREADS,
+                                               D.stream_ptr()), "kb_stage_upload")
         out = D.empty(self.shape, dtype)
         code = _lib.KB_F32 if np.dtype(dtype) == np.float32 else _lib.KB_F64
         _lib.check(_lib.load().kb_div_cast(raw.data_ptr(), float(self._total), code, out.data_ptr(), raw.numel(),

@@ -1,0 +1,184 @@
+import os, sys, time
+sys.path.insert(0, "/root/repo")
+import numpy as np, torch, ctypes as C
+import paper_2410_00233_b200 as kb
+from paper_2410_00233_b200.lowrank import *
+from paper_2410_00233_b200.lowrank import _EngineOp, _bases, _bases_key, _BASES, _LazyLift, _lib, rng
+from paper_2410_00233_b200 import datagen
+from paper_2410_00233_b200.linalg import TruncatedSvd, eps_for
+from paper_2410_00233_b200.exceptions import *
+_pc = time.perf_counter
+_T = []
+def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
+    _T.append(('start', _pc()))
+    """Enlarged Golub-Kahan bidiagonalisation with automatic rank choice
+    (lowrank.py:159-329), on the GPU.
+    _T.append(('(lowrank.py:159-329), on the GPU.', _pc()))
+
+    ``reorth_passes`` = 1 (default) projects once against the whole basis,
+    as the reference's single modified-GS pass does (lowrank.py:153-156),
+    with the coefficients formed in one fused pass (classical GS, fp64
+    _T.append(('with the coefficients formed in one fuse', _pc()))
+    accumulation).  One pass is what reproduces the reference's breakdown
+    _T.append(('accumulation).  One pass is what reprodu', _pc()))
+    and rank decisions beyond the fp32 numerical rank (a second pass keeps
+    _T.append(('and rank decisions beyond the fp32 numer', _pc()))
+    a noise-level recurrence alive where the reference stops; see
+    _T.append(('a noise-level recurrence alive where the', _pc()))
+    DESIGN.md); ``reorth_passes=2`` selects CGS2.
+    _T.append(('DESIGN.md); ``reorth_passes=2`` selects ', _pc()))
+    """
+    from paper_2410_00233_b200 import device as D
+    _T.append(('from . import device as D', _pc()))
+
+    op = _EngineOp(b_mat)
+    _T.append(('op = _EngineOp(b_mat)', _pc()))
+    dtype = np.dtype(op.dtype)
+    _T.append(('dtype = np.dtype(op.dtype)', _pc()))
+    mbar, nbar = op.shape
+    _T.append(('mbar, nbar = op.shape', _pc()))
+    eps = eps_for(dtype)
+    _T.append(('eps = eps_for(dtype)', _pc()))
+    break_tol = config.break_tol if config.break_tol is not None else np.sqrt(eps)
+    _T.append(('break_tol = config.break_tol if config.b', _pc()))
+    reorth = config.reorth
+    _T.append(('reorth = config.reorth', _pc()))
+    if reorth is None:
+        reorth = REORTH_FULL if dtype == np.float32 else REORTH_ONE_SIDED
+
+    y0d = None
+    _T.append(('y0d = None', _pc()))
+    if y0 is None:
+        pass   # drawn on the device right before the launch (below)
+    elif D.is_tensor(y0):
+        y0d = D.to_device(y0, dtype)
+        if tuple(y0d.shape) != (mbar,):
+            raise ValidationError(f"y0 must have length {mbar}, got shape {tuple(y0d.shape)}")
+    else:
+        y0 = np.asarray(y0, dtype=dtype)
+        if y0.shape != (mbar,):
+            raise ValidationError(f"y0 must have length {mbar}, got shape {y0.shape}")
+        y0d = D.to_device(y0)
+
+    cfg = _lib.KbEgkbConfig(config.k_max, config.p, config.k_min, float(config.tau), float(break_tol),
+                            1 if reorth == REORTH_FULL else 0, int(reorth_passes))
+    lib = _lib.load()
+    _T.append(('lib = _lib.load()', _pc()))
+    cap = lib.kb_egkb_capacity(C.byref(cfg))
+    _T.append(('cap = lib.kb_egkb_capacity(C.byref(cfg))', _pc()))
+    s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
+    _T.append(('s_basis, q_basis = _bases(cap, mbar, nba', _pc()))
+    hist = np.zeros((7, cap), dtype=np.float64)
+    _T.append(('hist = np.zeros((7, cap), dtype=np.float', _pc()))
+    dp = C.POINTER(C.c_double)
+    _T.append(('dp = C.POINTER(C.c_double)', _pc()))
+    st = _lib.KbEgkbState()
+    _T.append(('st = _lib.KbEgkbState()', _pc()))
+    st.s_basis, st.ld_s, st.q_basis, st.ld_q, st.capacity = s_basis.data_ptr(), mbar, q_basis.data_ptr(), nbar, cap
+    _T.append(('st.s_basis, st.ld_s, st.q_basis, st.ld_q', _pc()))
+    st.alphas_host = hist[0].ctypes.data_as(dp)
+    _T.append(('st.alphas_host = hist[0].ctypes.data_as(', _pc()))
+    st.ts_host = hist[1].ctypes.data_as(dp)
+    _T.append(('st.ts_host = hist[1].ctypes.data_as(dp)', _pc()))
+    st.zetas_host = hist[2].ctypes.data_as(dp)
+    _T.append(('st.zetas_host = hist[2].ctypes.data_as(d', _pc()))
+    st.nus_host = hist[3].ctypes.data_as(dp)
+    _T.append(('st.nus_host = hist[3].ctypes.data_as(dp)', _pc()))
+    st.s_scale_host = hist[4].ctypes.data_as(dp)
+    _T.append(('st.s_scale_host = hist[4].ctypes.data_as', _pc()))
+    st.q_scale_host = hist[5].ctypes.data_as(dp)
+    _T.append(('st.q_scale_host = hist[5].ctypes.data_as', _pc()))
+    # the small SVD of C and the lift weights are computed on the device right after the
+    # loop (kb_egkb_state.wu_dev): W_u, W_v (working dtype) and sigma (fp64) in one buffer
+    esz = np.dtype(dtype).itemsize
+    _T.append(('esz = np.dtype(dtype).itemsize', _pc()))
+    wbytes = (cap * cap * esz + 15) // 16 * 16
+    _T.append(('wbytes = (cap * cap * esz + 15) // 16 * ', _pc()))
+    svdbuf = D.empty(((2 * wbytes + 8 * cap) // 8,), np.float64)
+    _T.append(('svdbuf = D.empty(((2 * wbytes + 8 * cap)', _pc()))
+    wu_ptr = svdbuf.data_ptr()
+    _T.append(('wu_ptr = svdbuf.data_ptr()', _pc()))
+    wv_ptr = wu_ptr + wbytes
+    _T.append(('wv_ptr = wu_ptr + wbytes', _pc()))
+    st.wu_dev, st.wv_dev = wu_ptr, wv_ptr
+    _T.append(('st.wu_dev, st.wv_dev = wu_ptr, wv_ptr', _pc()))
+    st.sigma_dev = C.cast(C.c_void_p(wu_ptr + 2 * wbytes), dp)
+    _T.append(('st.sigma_dev = C.cast(C.c_void_p(wu_ptr ', _pc()))
+    st.sigma_host = hist[6].ctypes.data_as(dp)
+    _T.append(('st.sigma_host = hist[6].ctypes.data_as(d', _pc()))
+    nb = C.c_size_t()
+    _T.append(('nb = C.c_size_t()', _pc()))
+    _lib.check(lib.kb_egkb_workspace_bytes(C.byref(op.struct), cap, C.byref(nb)))
+    _T.append(('_lib.check(lib.kb_egkb_workspace_bytes(C', _pc()))
+    if y0d is None:
+        # the reference's draws (lowrank.py:199-201), generated on the device; launched
+        # after the host-side set-up so the RNG and the eGKB kernels run back to back
+        y0d = rng.standard_normal(config.seed, mbar, dtype)
+    ws, wsb = D.WORKSPACE.get(nb.value)
+    _T.append(('ws, wsb = D.WORKSPACE.get(nb.value)', _pc()))
+    status = lib.kb_egkb_run(C.byref(op.struct), C.byref(cfg), y0d.data_ptr(), C.byref(st), ws, wsb,
+                             D.stream_ptr())
+    _lib.check(status, "egkb")
+    _T.append(('_lib.check(status, "egkb")', _pc()))
+
+    trace = EgkbTrace()
+    _T.append(('trace = EgkbTrace()', _pc()))
+    trace.alphas = [float(v) for v in hist[0, : st.n_alphas]]
+    _T.append(('trace.alphas = [float(v) for v in hist[0', _pc()))
+    trace.ts = [float(v) for v in hist[1, : st.n_ts]]
+    _T.append(('trace.ts = [float(v) for v in hist[1, : ', _pc()))
+    trace.zetas = [float(v) for v in hist[2, : st.n_nus]]
+    _T.append(('trace.zetas = [float(v) for v in hist[2,', _pc()))
+    trace.nus = [float(v) for v in hist[3, : st.n_nus]]
+    _T.append(('trace.nus = [float(v) for v in hist[3, :', _pc()))
+    k_p, rows, chosen = st.k_p, st.rows, st.chosen_k
+    _T.append(('k_p, rows, chosen = st.k_p, st.rows, st.', _pc()))
+
+    sigma = hist[6, :chosen].copy()            # fp64 of the working-precision values
+    _T.append(('sigma = hist[6, :chosen].copy()         ', _pc()))
+    if not np.all(np.isfinite(sigma)):
+        raise NumericalError("bidiagonal SVD produced non-finite singular values")
+    lazy = _LazyLift(op.code, (s_basis, rows, wu_ptr), (q_basis, k_p, wv_ptr), chosen, (mbar, nbar), sigma,
+                     svdbuf, wu_ptr + 2 * wbytes)
+    _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
+    _T.append(('_BASES.pop(_bases_key(cap, mbar, nbar, d', _pc()))
+
+    trace.chosen_k = chosen
+    _T.append(('trace.chosen_k = chosen', _pc()))
+    trace.k_p = k_p
+    _T.append(('trace.k_p = k_p', _pc()))
+    trace.stop_reason = _lib.KB_STOP[st.stop_reason]
+    _T.append(('trace.stop_reason = _lib.KB_STOP[st.stop', _pc()))
+    trace.breakdown = bool(st.breakdown)
+    _T.append(('trace.breakdown = bool(st.breakdown)', _pc()))
+    if config.keep_basis:
+        c_mat = np.zeros((rows, k_p), dtype=dtype)
+        for i in range(k_p):
+            c_mat[i, i] = trace.alphas[i]
+            if i + 1 < rows:
+                c_mat[i + 1, i] = trace.ts[i + 1]
+        trace.s_basis = D.to_host(s_basis[:rows]).T.astype(dtype)
+        trace.q_basis = D.to_host(q_basis[:k_p]).T.astype(dtype)
+        trace.c_mat = c_mat
+    return TruncatedSvd.from_lift(lazy, sigma.astype(dtype)), trace
+
+
+
+n = 1024
+prob = datagen.make_problem("n1024")
+cfg = kb.EgkbConfig(**datagen.CONFIGS["n1024"]["egkb"])
+blur = kb.RearrangedBlur(prob.psf, n)
+scheme = kb.BlockScheme.square_image(n)
+keep=[None]
+acc={}
+for it in range(25):
+    _T.clear()
+    svd, tr = egkb(blur, cfg)
+    t1=_pc(); op = kb.assemble(svd, scheme); t2=_pc(); torch.cuda.synchronize(); t3=_pc()
+    keep[0]=op
+    _T.append(("assemble", t2)); _T.append(("sync", t3))
+    if it>=5:
+        for (a,ta),(b,tb) in zip(_T,_T[1:]):
+            acc[b]=acc.get(b,0)+(tb-ta)
+for k,v in sorted(acc.items(), key=lambda kv:-kv[1])[:20]: print(f"{v/20*1e6:8.1f} us  {k}")
+print("total", sum(acc.values())/20*1e6)
