@@ -227,7 +227,7 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
                      int* hdr, double* trace, double* scratch, void* raw, double tol, double** scales_out,
                      cudaStream_t s);
 void prof_set_last_bytes(double bytes);
-size_t ra_block_scratch_doubles(int lmax, int nv);
+size_t ra_block_scratch_doubles(int n, int lmax, int nv);
 bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv,
                     int transpose, double* scratch, cudaStream_t st);
 constexpr int KB_BLOCK_MAXV = 16;
@@ -807,7 +807,7 @@ extern "C" int kb_op_workspace_bytes(const kb_operator* op, size_t* bytes) {
         Sizer s;
         op_plan_size(op, s);
         s.take<unsigned>(8);
-        if (ra_is_operator(op->kind)) s.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+        if (ra_is_operator(op->kind)) s.take<double>(ra_block_scratch_doubles(op->side, std::max(op->kh, op->kw), KB_BLOCK_MAXV));
         *bytes = s.off;
     })
 }
@@ -822,7 +822,7 @@ extern "C" int kb_op_apply(const kb_operator* op, const void* x, void* y, int tr
         (void)a.take<unsigned>(8);
         cudaStream_t s = as_stream(stream);
         if (ra_is_operator(op->kind)) {
-            double* scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+            double* scr = a.take<double>(ra_block_scratch_doubles(op->side, std::max(op->kh, op->kw), KB_BLOCK_MAXV));
             if (ra_block_apply(op, x, op->cols, y, op->rows, 1, transpose, scr, s)) return KB_OK;
         }
         KB_CUDA(cudaMemsetAsync(p.counters, 0, sizeof(unsigned) * p.n_counters, s));
@@ -845,7 +845,7 @@ extern "C" int kb_op_apply_block(const kb_operator* op, const void* X, int64_t l
         (void)a.take<unsigned>(8);
         double* scr = nullptr;
         if (ra_is_operator(op->kind))
-            scr = a.take<double>(ra_block_scratch_doubles(std::max(op->kh, op->kw), KB_BLOCK_MAXV));
+            scr = a.take<double>(ra_block_scratch_doubles(op->side, std::max(op->kh, op->kw), KB_BLOCK_MAXV));
         for (int v0 = 0; v0 < nv; v0 += KB_BLOCK_MAXV) {
             const int cnt = std::min(KB_BLOCK_MAXV, nv - v0);
             const char* xs = static_cast<const char*>(X) + (size_t)v0 * ldx * esz;

@@ -218,14 +218,20 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_ra_block(RaBlockParams P) {
     rb_mark(P, 3);
 }
 
-size_t ra_block_scratch_doubles(int lmax, int nv) {
-    return (size_t)(2 * RB_SEGS + 1) * nv * lmax + 64;
+size_t ra_tiled_scratch_doubles(int n, int lmax, int nv);
+bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv, int transpose,
+                    double* scratch, cudaStream_t st);
+
+size_t ra_block_scratch_doubles(int n, int lmax, int nv) {
+    return std::max((size_t)(2 * RB_SEGS + 1) * nv * lmax + 64, ra_tiled_scratch_doubles(n, lmax, nv));
 }
 
 // Returns false if the cooperative launch is not possible (caller falls back).
 bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv,
                     int transpose, double* scratch, cudaStream_t st) {
     if (!ra_is_operator(op->kind) || nv < 1 || nv > RB_MAXV) return false;
+    static const bool no_tiled = std::getenv("KB_RA_NO_TILED") != nullptr;
+    if (!no_tiled && ra_tiled_apply(op, X, ldx, Y, ldy, nv, transpose, scratch, st)) return true;
     if (((uintptr_t)Y & 15) != 0) return false;
     RaBlockParams P{};
     const int cu = op->kh / 2, cv = op->kw / 2;
@@ -306,6 +312,243 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
         lc.gridDim = dim3(kSMs * std::min(per_sm, 2));
         KB_CUDA(cudaLaunchKernelEx(&lc, k_ra_block<double>, P));
     }
+    return true;
+}
+
+}  // namespace kb
+
+// ------------------------------------------------------------------ tiled block product
+// Y = R(A) X (or R(A)^T X) for zero BC and n a multiple of 128, as four
+// stream-ordered kernels instead of one cooperative kernel with grid
+// barriers (every phase runs at full occupancy, no barrier latency):
+//
+//   k_rat_diag   tile (32 image rows x 128 columns of one vector) through
+//                shared memory -> its 159 diagonal sums (fp64, fixed order)
+//   k_rat_w      w[v][u] = sum of the tile sums on diagonal u - c_in, tiles
+//                in fixed (row block, column block) order -- deterministic
+//   k_rat_z      z[v][c] = sum_r Mt[c, r] w[v][r]: contiguous rows of K^T
+//                (forward) or K (transpose), w staged in shared memory,
+//                16 rows x <= 16 vectors per CTA
+//   k_rat_bcast  y[v][a*n + b] = z[v][b - a + c_out], float4 / double2 stores
+//
+// The only HBM streams are the n^2 inputs (read once), the n^2 outputs
+// (written once) and K (read once per block of vectors): the product's
+// algorithmic bytes.
+namespace kb {
+
+constexpr int RT_ROWS = 32, RT_COLS = 128, RT_DIAG = RT_ROWS + RT_COLS - 1, RT_DP = 160;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_rat_diag(const T* __restrict__ X, int64_t ldx, int n, double* __restrict__ part) {
+    __shared__ T tile[RT_ROWS][RT_COLS + (sizeof(T) == 4 ? 4 : 2)];
+    const int cbn = n / RT_COLS, tiles = (n / RT_ROWS) * cbn;
+    const int t = blockIdx.x, v = blockIdx.y;
+    const int rb = t / cbn, cb = t - rb * cbn;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T* x = X + (int64_t)v * ldx + (int64_t)(rb * RT_ROWS) * n + cb * RT_COLS;
+    if constexpr (sizeof(T) == 4) {
+        float4 q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)(warp + 8 * j) * n) + lane);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<float4*>(&tile[warp + 8 * j][4 * lane]) = q[j];
+    } else {
+        double2 q[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                q[2 * j + h] = __ldcs(reinterpret_cast<const double2*>(x + (int64_t)(warp + 8 * j) * n + 64 * h) + lane);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) *reinterpret_cast<double2*>(&tile[warp + 8 * j][64 * h + 2 * lane]) = q[2 * j + h];
+    }
+    __syncthreads();
+    if (tid < RT_DIAG) {
+        const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
+        double s = 0.0;
+        const int r0 = max(0, -off), r1 = min(RT_ROWS, RT_COLS - off);
+        for (int r = r0; r < r1; ++r) s += (double)tile[r][r + off];
+        part[((int64_t)v * tiles + t) * RT_DP + tid] = s;
+    }
+}
+
+// w[v][u] (u < Li) = sum over tiles of the sums on diagonal d = u - ci (column
+// - row): one warp per (u, v), lane = row block (strided), all loads in
+// flight, then a fixed-order warp tree.
+__global__ void __launch_bounds__(256) k_rat_w(const double* __restrict__ part, int n, int ci, int Li,
+                                               double* __restrict__ w, int ldw) {
+    const int lane = threadIdx.x & 31;
+    const int u = blockIdx.x * 8 + (threadIdx.x >> 5), v = blockIdx.y;
+    if (u >= Li) return;
+    const int cbn = n / RT_COLS, rbn = n / RT_ROWS, tiles = rbn * cbn;
+    const int d = u - ci;
+    const double* pv = part + (int64_t)v * tiles * RT_DP;
+    double s = 0.0;
+    for (int rb0 = 0; rb0 < rbn; rb0 += 64) {
+        double q[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rb = rb0 + lane + 32 * h;
+            q[2 * h] = q[2 * h + 1] = 0.0;
+            if (rb < rbn) {
+                // tile (rb, cb) holds diagonals [128 cb - 32 rb - 31, 128 cb - 32 rb + 127]: <= 2 column blocks
+                const int lo = d + RT_ROWS * rb - (RT_COLS - 1), hi = d + RT_ROWS * rb + (RT_ROWS - 1);
+                const int cb0 = lo <= 0 ? 0 : (lo + RT_COLS - 1) / RT_COLS;
+                const int cb1 = hi < 0 ? -1 : min(cbn - 1, hi / RT_COLS);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int cb = cb0 + j;
+                    if (cb <= cb1) {
+                        const int i = d - (RT_COLS * cb - RT_ROWS * rb - (RT_ROWS - 1));
+                        q[2 * h + j] = __ldg(pv + (int64_t)(rb * cbn + cb) * RT_DP + i);
+                    }
+                }
+            }
+        }
+        s += (q[0] + q[1]) + (q[2] + q[3]);
+    }
+    s = warp_sum(s);
+    if (lane == 0) w[(int64_t)v * ldw + u] = s;
+}
+
+// z[v][c] = sum_r Mt[c, r] w[v][r] (v < NV, a compile-time bound >= nv):
+// one warp per row c (8 rows per CTA).  The whole row is loaded first
+// (<= RZ_ML per lane, one round trip), overlapping the staging of w (all
+// vectors, shared memory, zero-padded to NV), then one FMA chain per vector.
+constexpr int RZ_ML = 64;   // Li <= 2048
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li, int Lo, const double* __restrict__ w,
+                                               int ldw, int nv, double* __restrict__ z, int ldz) {
+    extern __shared__ double wsm[];   // [NV][Li]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x * 8 + warp;
+    T m[RZ_ML];
+#pragma unroll
+    for (int k = 0; k < RZ_ML; ++k) {
+        const int r = lane + 32 * k;
+        m[k] = (c < Lo && r < Li) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
+    }
+    // staging: 16-byte cp.async copies (no registers, all in flight at once);
+    // rows of wsm padded to an even length, the padding entry never used
+    const int LiP = (Li + 1) & ~1, half = LiP / 2;
+    for (int idx = tid; idx < nv * half; idx += 256) {
+        const int v = idx / half, pr = idx - v * half;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
+                     : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    double acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+#pragma unroll
+    for (int k = 0; k < RZ_ML; ++k) {
+        const int r = lane + 32 * k;
+        if (r < Li) {
+            const double mk = (double)m[k];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = fma(mk, wsm[v * LiP + r], acc[v]);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const double s = warp_sum(acc[v]);
+        if (lane == 0 && c < Lo && v < nv) z[(int64_t)v * ldz + c] = s;
+    }
+}
+
+template <typename T>
+static void rat_z_launch(const T* Mt, int Li, int Lo, const double* w, int ldw, int nv, double* z, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)((Li + 1) & ~1);
+    auto go = [&](auto kern, int NVc) {
+        static_assert(true, "");
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem * NVc)));
+        kern<<<(Lo + 7) / 8, 256, smem * NVc, st>>>(Mt, Li, Lo, w, ldw, nv, z, ldw);
+    };
+    if (nv <= 1) go(k_rat_z<T, 1>, 1);
+    else if (nv <= 2) go(k_rat_z<T, 2>, 2);
+    else if (nv <= 4) go(k_rat_z<T, 4>, 4);
+    else if (nv <= 8) go(k_rat_z<T, 8>, 8);
+    else go(k_rat_z<T, 16>, 16);
+}
+
+// y[v][a*n + b] = (T) z[v][b - a + co] (0 outside [0, Lo))
+template <typename T>
+__global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z, int ldz, int n, int co, int Lo,
+                                                   T* __restrict__ Y, int64_t ldy) {
+    extern __shared__ double zsm[];
+    const int v = blockIdx.y;
+    for (int c0 = threadIdx.x; c0 < Lo; c0 += 8 * 256) {   // all loads in flight, then the stores
+        double q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = c0 + 256 * k < Lo ? __ldg(z + (int64_t)v * ldz + c0 + 256 * k) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (c0 + 256 * k < Lo) zsm[c0 + 256 * k] = q[k];
+    }
+    __syncthreads();
+    const int64_t N = (int64_t)n * n;
+    T* y = Y + (int64_t)v * ldy;
+    for (int64_t e0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4; e0 < N; e0 += (int64_t)gridDim.x * 256 * 4) {
+        double yv[4];
+        ra_bcast4(zsm, (unsigned)e0, n, co, Lo, false, yv);
+        if constexpr (sizeof(T) == 4) {
+            __stcs(reinterpret_cast<float4*>(y + e0), make_float4((float)yv[0], (float)yv[1], (float)yv[2], (float)yv[3]));
+        } else {
+            __stcs(reinterpret_cast<double2*>(y + e0), make_double2(yv[0], yv[1]));
+            __stcs(reinterpret_cast<double2*>(y + e0 + 2), make_double2(yv[2], yv[3]));
+        }
+    }
+}
+
+size_t ra_tiled_scratch_doubles(int n, int lmax, int nv) {
+    if (n < RT_COLS || n % RT_COLS) return 0;
+    const size_t tiles = (size_t)(n / RT_ROWS) * (n / RT_COLS);
+    return (size_t)nv * tiles * RT_DP + 2 * (size_t)nv * (lmax + 8) + 64;
+}
+
+// false when outside the tiled path's envelope (the caller falls back)
+bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, int64_t ldy, int nv, int transpose,
+                    double* scratch, cudaStream_t st) {
+    if (op->kind != KB_OP_RA_ZERO || nv < 1 || nv > 16) return false;
+    const int n = op->side;
+    if (n < RT_COLS || n % RT_COLS) return false;
+    const int vec = op->dtype == KB_F32 ? 4 : 2;
+    if ((ldx % 4) || (ldy % 4) || ((uintptr_t)X % 16) || ((uintptr_t)Y % 16)) return false;
+    (void)vec;
+    const int cu = op->kh / 2, cv = op->kw / 2;
+    int ci, Li, co, Lo;
+    const void* Mt;
+    if (!transpose) { ci = cu; Li = op->kh; co = cv; Lo = op->kw; Mt = op->kt; }   // z = K^T w: rows of K^T
+    else { ci = cv; Li = op->kw; co = cu; Lo = op->kh; Mt = op->k; }               // z = K w: rows of K
+    const int lmax = std::max(op->kh, op->kw);
+    const int tiles = (n / RT_ROWS) * (n / RT_COLS);
+    double* part = scratch;
+    double* w = part + (size_t)nv * tiles * RT_DP;
+    double* z = w + (size_t)nv * ((lmax + 9) & ~1);
+    const int ldw = (lmax + 9) & ~1;   // even: 16-byte aligned rows for the cp.async staging
+    const int64_t N = (int64_t)n * n;
+    const double bytes = (double)(op->dtype == KB_F32 ? 4 : 8) * (2.0 * nv * N + (double)op->kh * op->kw);
+    ProfScope ps(st, PROF_RA_DIAG, bytes);
+    // broadcast: ~4 CTAs per SM in total, so each CTA's staging of z (Lo doubles) is small
+    // next to the part of the output it writes
+    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256 * 4), (4 * kSMs + nv - 1) / nv));
+    if (Li > 32 * RZ_ML || (size_t)Li * 8 * 16 > 200 * 1024) return false;
+    if (op->dtype == KB_F32) {
+        k_rat_diag<float><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const float*>(X), ldx, n, part);
+        k_rat_w<<<dim3((Li + 7) / 8, nv), 256, 0, st>>>(part, n, ci, Li, w, ldw);
+        rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
+        k_rat_bcast<float><<<dim3(bgrid, nv), 256, sizeof(double) * Lo, st>>>(z, ldw, n, co, Lo, static_cast<float*>(Y), ldy);
+    } else {
+        k_rat_diag<double><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const double*>(X), ldx, n, part);
+        k_rat_w<<<dim3((Li + 7) / 8, nv), 256, 0, st>>>(part, n, ci, Li, w, ldw);
+        rat_z_launch<double>(static_cast<const double*>(Mt), Li, Lo, w, ldw, nv, z, st);
+        k_rat_bcast<double><<<dim3(bgrid, nv), 256, sizeof(double) * Lo, st>>>(z, ldw, n, co, Lo, static_cast<double*>(Y), ldy);
+    }
+    KB_LAUNCH_CHECK();
     return true;
 }
 
