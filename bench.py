@@ -287,7 +287,8 @@ def run_ours(args, prob, rank, world, dist):
     gc.enable()
     iters = len(tr.alphas) + 1
     d2h = 8 * 4 * iters + 16 + sig.nbytes
-    h2d += 8 * 2 * (tr.k_p + 1) * tr.chosen_k                  # lift coefficient uploads
+    rows_c = tr.k_p + (1 if tr.breakdown and len(tr.ts) > tr.k_p else 0)
+    h2d += 4 * (rows_c + tr.k_p) * tr.chosen_k + 8 * tr.chosen_k   # lift weights + sigma (from the host SVD of C)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=D.device())
     if dist is not None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -382,7 +383,7 @@ def run_ours(args, prob, rank, world, dist):
 
     hbm, hbm_src = peaks()
     # dominant kernel of the step: the class with the largest device time
-    names = {0: "persistent eGKB (k_egkb_persistent)", 1: "R(A) diagonal sums (k_diag_seg)",
+    names = {0: "persistent eGKB (k_egkb_tiled)", 1: "R(A) products (k_rat_* tiled block product)",
              2: "R(A) K-column sums (k_colsum_seg)", 3: "fp64 GEMM (k_dgemm, DMMA)", 4: "CGLS/SB vector passes",
              5: "lift (k_lift)", 6: "start-vector draws (k_zig_*)"}
     dom = max(range(7), key=lambda c: prof[c][0])
@@ -394,7 +395,8 @@ def run_ours(args, prob, rank, world, dist):
     ra = {"us_per_product": mv_t * 1e6, "GBps": mv_bytes_alg / mv_t / 1e9,
           "frac": mv_bytes_alg / mv_t / 1e9 / hbm, "bytes_per_product": mv_bytes_alg,
           "timing": f"{n_mv} products (alternating R x / R^T x) per CUDA-graph replay, 5 replays, CUDA events",
-          "kernel": "k_ra_block<float> (one cooperative launch: diagonal sums | K column sums | Toeplitz write)",
+          "kernel": "k_rat_diag | k_rat_w | k_rat_z | k_rat_bcast (tile diagonal sums, fixed-order diagonal "
+                    "reduction, row-dot z, streaming broadcast; stream-ordered, no grid barriers)",
           "block16": {"us_per_launch": blk_t * 1e6,
                       "GBps": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9,
                       "frac": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9 / hbm,

@@ -410,7 +410,19 @@ k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, i
         T acc[CB];
 #pragma unroll
         for (int c = 0; c < CB; ++c) acc[c] = T(0);
-        for (int i = 0; i < rows; ++i) {
+        int i = 0;
+        for (; i + 4 <= rows; i += 4) {        // 4 basis loads in flight, then the same FMA order
+            T s4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s4[j] = __ldg(S + (int64_t)(i + j) * ld + e);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const T* wr = wsm + (i + j) * CB;
+#pragma unroll
+                for (int c = 0; c < CB; ++c) acc[c] = fma(s4[j], wr[c], acc[c]);
+            }
+        }
+        for (; i < rows; ++i) {
             const T s = __ldg(S + (int64_t)i * ld + e);
             const T* wr = wsm + i * CB;
 #pragma unroll

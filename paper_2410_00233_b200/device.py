@@ -16,9 +16,15 @@ _TORCH_OF = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.fl
 _NP_OF = {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64)}
 
 
+_CUDA_OK = False
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise KronblurError("no CUDA device: the kronblur_b200 path runs on B200 (sm_100a) only")
+    global _CUDA_OK
+    if not _CUDA_OK:   # the driver query costs a few us per call; once available it stays available
+        if not torch.cuda.is_available():
+            raise KronblurError("no CUDA device: the kronblur_b200 path runs on B200 (sm_100a) only")
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

@@ -259,13 +259,13 @@ class _LazyLift:
                        "lift+assemble")
 
 
-def _bases(cap, mbar, nbar, dtype):
+def _bases(cap, mbar, nbar, dtype, key=None):
     """Krylov bases per shape, reused across calls while no result holds them
     (a lazily-lifted result owns its bases; the next call then takes fresh
     ones from the caching allocator)."""
     from . import device as D
 
-    key = _bases_key(cap, mbar, nbar, dtype)
+    key = key if key is not None else _bases_key(cap, mbar, nbar, dtype)
     hit = _BASES.get(key)
     if hit is None:
         if len(_BASES) >= 4:
@@ -315,7 +315,8 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
                             1 if reorth == REORTH_FULL else 0, int(reorth_passes))
     lib = _lib.load()
     cap = lib.kb_egkb_capacity(C.byref(cfg))
-    s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
+    bkey = _bases_key(cap, mbar, nbar, dtype)
+    s_basis, q_basis = _bases(cap, mbar, nbar, dtype, bkey)
     hist = np.zeros((7, cap), dtype=np.float64)
     dp = C.POINTER(C.c_double)
     st = _lib.KbEgkbState()
@@ -359,7 +360,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
         raise NumericalError("bidiagonal SVD produced non-finite singular values")
     lazy = _LazyLift(op.code, (s_basis, rows, wu_ptr), (q_basis, k_p, wv_ptr), chosen, (mbar, nbar), sigma,
                      svdbuf, wu_ptr + 2 * wbytes)
-    _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
+    _BASES.pop(bkey, None)   # the result owns these bases now
 
     trace.chosen_k = chosen
     trace.k_p = k_p
