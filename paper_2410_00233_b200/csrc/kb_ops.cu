@@ -393,6 +393,63 @@ k_reorth(const VecRef zr, int mode, int side, int center, int L, const VecRef pr
 // out_c = scale[c] * (double)lift_c -- kron_assemble fused into the lift
 // (kronop.py:117-119: ax_i = sigma_i * u_i promoted to fp64), bit-identical to
 // lift-then-assemble without writing or re-reading the working-precision u.
+// Two adjacent elements per thread (float2 loads, double2 stores) for the
+// fp32 -> fp64 assemble when the layout allows; each element keeps exactly
+// the FMA order of the one-element path (bit-identical results).
+template <int CB>
+__global__ void __launch_bounds__(256)
+k_lift2_asm(const float* __restrict__ S, int64_t ld, int rows, const float* __restrict__ W, int cols, int c0,
+            double* __restrict__ out, int64_t ld_out, int64_t len, const double* __restrict__ scale) {
+    extern __shared__ double wraw[];
+    float* wsm = reinterpret_cast<float*>(wraw);  // [rows][CB]
+    const int nc = min(CB, cols - c0);
+    for (int i = threadIdx.x; i < rows * CB; i += blockDim.x) {
+        const int r = i / CB, c = i % CB;
+        wsm[i] = (c < nc) ? W[(int64_t)r * cols + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    const int64_t len2 = len / 2;
+    for (int64_t e2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e2 < len2;
+         e2 += (int64_t)gridDim.x * blockDim.x) {
+        float a0[CB], a1[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) a0[c] = a1[c] = 0.f;
+        int i = 0;
+        for (; i + 4 <= rows; i += 4) {
+            float2 s4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s4[j] = __ldg(reinterpret_cast<const float2*>(S + (int64_t)(i + j) * ld) + e2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float* wr = wsm + (i + j) * CB;
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    a0[c] = fmaf(s4[j].x, wr[c], a0[c]);
+                    a1[c] = fmaf(s4[j].y, wr[c], a1[c]);
+                }
+            }
+        }
+        for (; i < rows; ++i) {
+            const float2 sv = __ldg(reinterpret_cast<const float2*>(S + (int64_t)i * ld) + e2);
+            const float* wr = wsm + i * CB;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                a0[c] = fmaf(sv.x, wr[c], a0[c]);
+                a1[c] = fmaf(sv.y, wr[c], a1[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            if (c < nc) {
+                const double u0 = (double)a0[c], u1 = (double)a1[c];
+                const double sc = scale ? scale[c0 + c] : 1.0;
+                const double2 o = scale ? make_double2(__dmul_rn(sc, u0), __dmul_rn(sc, u1)) : make_double2(u0, u1);
+                __stcs(reinterpret_cast<double2*>(out + (int64_t)(c0 + c) * ld_out) + e2, o);
+            }
+        }
+    }
+}
+
 template <typename T, int CB, typename TO = T, bool ASM = false>
 __global__ void __launch_bounds__(256)
 k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, int cols, int c0,
@@ -699,6 +756,20 @@ static void launch_lift(const void* S, int64_t ld, int rows, const void* W, int 
     const size_t smem = sizeof(T) * (size_t)rows * CB;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, 256), 8 * kSMs));
     ProfScope ps(st, PROF_LIFT, (double)len * (sizeof(T) * rows + sizeof(TO) * std::min(CB, cols - c0)));
+    if constexpr (ASM && sizeof(T) == 4) {
+        if (len % 2 == 0 && ld % 2 == 0 && ld_out % 2 == 0 && ((uintptr_t)S % 8) == 0 && ((uintptr_t)out % 16) == 0) {
+            static bool cfg2 = false;
+            if (!cfg2) {
+                KB_CUDA(cudaFuncSetAttribute(k_lift2_asm<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+                cfg2 = true;
+            }
+            const unsigned b2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len / 2, 256), 4 * kSMs));
+            k_lift2_asm<CB><<<b2, 256, smem, st>>>(static_cast<const float*>(S), ld, rows, static_cast<const float*>(W),
+                                                   cols, c0, static_cast<double*>(out), ld_out, len, scale);
+            KB_LAUNCH_CHECK();
+            return;
+        }
+    }
     k_lift<T, CB, TO, ASM><<<blocks, 256, smem, st>>>(static_cast<const T*>(S), ld, rows, static_cast<const T*>(W),
                                                  cols, c0, static_cast<TO*>(out), ld_out, len, scale);
     KB_LAUNCH_CHECK();

@@ -66,7 +66,9 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     _T.append(('lib = _lib.load()', _pc()))
     cap = lib.kb_egkb_capacity(C.byref(cfg))
     _T.append(('cap = lib.kb_egkb_capacity(C.byref(cfg))', _pc()))
-    s_basis, q_basis = _bases(cap, mbar, nbar, dtype)
+    bkey = _bases_key(cap, mbar, nbar, dtype)
+    _T.append(('bkey = _bases_key(cap, mbar, nbar, dtype', _pc()))
+    s_basis, q_basis = _bases(cap, mbar, nbar, dtype, bkey)
     _T.append(('s_basis, q_basis = _bases(cap, mbar, nba', _pc()))
     hist = np.zeros((7, cap), dtype=np.float64)
     _T.append(('hist = np.zeros((7, cap), dtype=np.float', _pc()))
@@ -140,8 +142,8 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
         raise NumericalError("bidiagonal SVD produced non-finite singular values")
     lazy = _LazyLift(op.code, (s_basis, rows, wu_ptr), (q_basis, k_p, wv_ptr), chosen, (mbar, nbar), sigma,
                      svdbuf, wu_ptr + 2 * wbytes)
-    _BASES.pop(_bases_key(cap, mbar, nbar, dtype), None)   # the result owns these bases now
-    _T.append(('_BASES.pop(_bases_key(cap, mbar, nbar, d', _pc()))
+    _BASES.pop(bkey, None)   # the result owns these bases now
+    _T.append(('_BASES.pop(bkey, None)   # the result ow', _pc()))
 
     trace.chosen_k = chosen
     _T.append(('trace.chosen_k = chosen', _pc()))
