@@ -140,6 +140,8 @@ _lib = None
 def load(path: str = LIB_PATH):
     """Load the shared library (no CUDA call is made by loading)."""
     global _lib
+    if _lib is not None:   # fast path (every launch goes through here)
+        return _lib
     with _lock:
         if _lib is None:
             if not os.path.exists(path):

@@ -68,10 +68,11 @@ struct PkParams {
     int* dbg_n;
 };
 
-__device__ __forceinline__ void pk_mark(const PkParams& P) {
+__device__ __forceinline__ void pk_mark(const PkParams& P, int tag = 0) {
     if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        t = (t & ~15ull) | (unsigned)tag;   // phase tag in the low bits (ns resolution is not needed)
         const int k = *P.dbg_n;
         if (k < 4096) P.dbg[k] = t;
         *P.dbg_n = k + 1;
@@ -680,6 +681,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -929,7 +931,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
     }
     pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red, acc);
-    pk_mark(P);
+    pk_mark(P, 1);
     const double t1 = sqrt(red[0]);
     // entries of a normalised vector are <= 1: one fixed-point scale for the run
     const int Fx = pk_fix_exp(0.5, n);
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     // s1 = fl(y0 / t1) (lowrank.py:207-210), stored, and its diagonal sums for step 0 (R^T)
     pk_store_diag<MAXG>(P, Gm, v, (float)t1, S, eo, ng, tb, tbo, t0, cv, P.kw, fxs, P.wfix);
     grid.sync();
-    pk_mark(P);
+    pk_mark(P, 2);
 
     int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
     int na = 1, nt = 1, nn = 1;
@@ -986,7 +988,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             if (g < ng && prev) PkIO<float, 4>::load(prev + eo[g], pv[g]);
         }
         grid.sync();
-        pk_mark(P);
+        pk_mark(P, 3);
 
         // ---- B: zero the consumed w; z; y; v = y - beta*prev; dots
         for (int i = blockIdx.x * PK_THREADS + tid; i < P.lmax; i += nblk * PK_THREADS) wcur[i] = 0ull;
@@ -1075,7 +1077,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
         }
         pk_reduce_barrier(P, gen, P.blk_part, P.cap + 4, W, red, acc);
-        pk_mark(P);
+        pk_mark(P, 4);
         const double aux = red[m + 1];
         const double vnorm = sqrt(red[m]);
 
@@ -1149,14 +1151,14 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
             }
             pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
-            pk_mark(P);
+            pk_mark(P, 5);
             val = sqrt(red[P.cap + 2]);
         }
         // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
         // sums for the next product
         pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
         grid.sync();
-        pk_mark(P);
+        pk_mark(P, 6);
 
         // ---- control (identical in every CTA; CTA 0 records the trace)
         if (step == 0) {
@@ -1440,7 +1442,11 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
             cudaStreamSynchronize(s);
             k = std::min(k, 4096);
             fprintf(stderr, "[kb] pk phases (us):");
-            for (int i = 1; i < k; ++i) fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
+            for (int i = 1; i < k; ++i) {
+                const unsigned tag = (unsigned)(t[i] & 15);
+                if (tag) fprintf(stderr, " %u:%.1f", tag, ((t[i] & ~15ull) - (t[i - 1] & ~15ull)) * 1e-3);
+                else fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
+            }
             fprintf(stderr, "\n");
         }
     } dump{want_trace, s, dbg, dbg_n};

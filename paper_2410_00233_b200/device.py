@@ -28,7 +28,14 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr() -> int:
+    """cudaStream_t of torch's current stream on the current device (the raw query
+    skips building a Stream object: a few us per call on the launch paths)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
