@@ -338,6 +338,12 @@ namespace kb {
 
 constexpr int RT_ROWS = 32, RT_COLS = 128, RT_DIAG = RT_ROWS + RT_COLS - 1, RT_DP = 160;
 
+// Programmatic dependent launch: the next kernel of the chain is launched
+// while this one drains (launch latency hidden); it waits in pdl_wait()
+// until this grid has completed and its writes are visible.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_rat_diag(const T* __restrict__ X, int64_t ldx, int n, double* __restrict__ part) {
     __shared__ T tile[RT_ROWS][RT_COLS + (sizeof(T) == 4 ? 4 : 2)];
@@ -365,6 +371,7 @@ __global__ void __launch_bounds__(256) k_rat_diag(const T* __restrict__ X, int64
             for (int h = 0; h < 2; ++h) *reinterpret_cast<double2*>(&tile[warp + 8 * j][64 * h + 2 * lane]) = q[2 * j + h];
     }
     __syncthreads();
+    pdl_trigger();
     if (tid < RT_DIAG) {
         const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
         double s = 0.0;
@@ -381,6 +388,8 @@ __global__ void __launch_bounds__(256) k_rat_w(const double* __restrict__ part, 
                                                double* __restrict__ w, int ldw) {
     const int lane = threadIdx.x & 31;
     const int u = blockIdx.x * 8 + (threadIdx.x >> 5), v = blockIdx.y;
+    pdl_wait();
+    pdl_trigger();
     if (u >= Li) return;
     const int cbn = n / RT_COLS, rbn = n / RT_ROWS, tiles = rbn * cbn;
     const int d = u - ci;
@@ -430,6 +439,8 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
         const int r = lane + 32 * k;
         m[k] = (c < Lo && r < Li) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
     }
+    pdl_wait();      // w is written by the previous kernel; the K rows above are not
+    pdl_trigger();
     // staging: 16-byte cp.async copies (no registers, all in flight at once);
     // rows of wsm padded to an even length, the padding entry never used
     const int LiP = (Li + 1) & ~1, half = LiP / 2;
@@ -460,13 +471,31 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
     }
 }
 
+// PDL only for the one-vector product (launch latency is most of it); for a
+// block the early-resident dependents would take SM slots from the producer.
+static thread_local bool g_rat_pdl = true;
+
+template <typename K, typename... A>
+static void pdl_launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = g_rat_pdl ? 1 : 0;
+    KB_CUDA(cudaLaunchKernelEx(&lc, kern, args...));
+}
+
 template <typename T>
 static void rat_z_launch(const T* Mt, int Li, int Lo, const double* w, int ldw, int nv, double* z, cudaStream_t st) {
     const size_t smem = sizeof(double) * (size_t)((Li + 1) & ~1);
     auto go = [&](auto kern, int NVc) {
-        static_assert(true, "");
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem * NVc)));
-        kern<<<(Lo + 7) / 8, 256, smem * NVc, st>>>(Mt, Li, Lo, w, ldw, nv, z, ldw);
+        pdl_launch(kern, dim3((Lo + 7) / 8), smem * NVc, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
     };
     if (nv <= 1) go(k_rat_z<T, 1>, 1);
     else if (nv <= 2) go(k_rat_z<T, 2>, 2);
@@ -481,6 +510,7 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
                                                    T* __restrict__ Y, int64_t ldy) {
     extern __shared__ double zsm[];
     const int v = blockIdx.y;
+    pdl_wait();
     for (int c0 = threadIdx.x; c0 < Lo; c0 += 8 * 256) {   // all loads in flight, then the stores
         double q[8];
 #pragma unroll
@@ -537,16 +567,19 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     // next to the part of the output it writes
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256 * 4), (4 * kSMs + nv - 1) / nv));
     if (Li > 32 * RZ_ML || (size_t)Li * 8 * 16 > 200 * 1024) return false;
+    g_rat_pdl = nv == 1;
     if (op->dtype == KB_F32) {
         k_rat_diag<float><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const float*>(X), ldx, n, part);
-        k_rat_w<<<dim3((Li + 7) / 8, nv), 256, 0, st>>>(part, n, ci, Li, w, ldw);
+        pdl_launch(k_rat_w, dim3((Li + 7) / 8, nv), 0, st, (const double*)part, n, ci, Li, w, ldw);
         rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
-        k_rat_bcast<float><<<dim3(bgrid, nv), 256, sizeof(double) * Lo, st>>>(z, ldw, n, co, Lo, static_cast<float*>(Y), ldy);
+        pdl_launch(k_rat_bcast<float>, dim3(bgrid, nv), sizeof(double) * Lo, st, (const double*)z, ldw, n, co, Lo,
+                   static_cast<float*>(Y), (int64_t)ldy);
     } else {
         k_rat_diag<double><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const double*>(X), ldx, n, part);
-        k_rat_w<<<dim3((Li + 7) / 8, nv), 256, 0, st>>>(part, n, ci, Li, w, ldw);
+        pdl_launch(k_rat_w, dim3((Li + 7) / 8, nv), 0, st, (const double*)part, n, ci, Li, w, ldw);
         rat_z_launch<double>(static_cast<const double*>(Mt), Li, Lo, w, ldw, nv, z, st);
-        k_rat_bcast<double><<<dim3(bgrid, nv), 256, sizeof(double) * Lo, st>>>(z, ldw, n, co, Lo, static_cast<double*>(Y), ldy);
+        pdl_launch(k_rat_bcast<double>, dim3(bgrid, nv), sizeof(double) * Lo, st, (const double*)z, ldw, n, co, Lo,
+                   static_cast<double*>(Y), (int64_t)ldy);
     }
     KB_LAUNCH_CHECK();
     return true;
