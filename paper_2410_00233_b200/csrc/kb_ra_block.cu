@@ -475,6 +475,88 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
 // block the early-resident dependents would take SM slots from the producer.
 static thread_local bool g_rat_pdl = true;
 
+// z for 8 or 16 vectors on the FP64 tensor cores (mma.sync m8n8k4, SASS
+// DMMA): CTA = 8 rows c of Mt, warp w = the w-th eighth of the r range; per
+// 4-wide r step each lane holds Mt[c0 + gid][r + tig] (fp32 widened) as the
+// A fragment and w[v][r + tig] (v = n*8 + gid, staged by cp.async) as the B
+// fragments; the 8 warp partials are added in warp order.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename T, int NT>   // NT = 8-vector tiles (1 or 2)
+__global__ void __launch_bounds__(256) k_rat_z_mma(const T* __restrict__ Mt, int Li, int Lo,
+                                                   const double* __restrict__ w, int ldw, int nv,
+                                                   double* __restrict__ z, int ldz) {
+    extern __shared__ double wsm[];   // [NT*8][LiP]
+    __shared__ double red[8][8][NT * 8 + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int c0 = blockIdx.x * 8;
+    const int LiP = (Li + 3) & ~3, half = LiP / 2;
+    for (int idx = tid; idx < nv * half; idx += 256) {
+        const int v = idx / half, pr = idx - v * half;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
+                     : "memory");
+    }
+    for (int idx = tid; idx < (NT * 8 - nv) * LiP; idx += 256) wsm[nv * LiP + idx] = 0.0;   // unused vectors
+    // r range of this warp (multiples of 4)
+    const int steps = LiP / 4, per = (steps + 7) / 8;
+    const int s0 = warp * per, s1 = min(steps, s0 + per);
+    const int c = c0 + gid;
+    // this warp's A fragments (one Mt entry per lane per r step), all loads in
+    // flight during the staging of w
+    constexpr int AB = 40;
+    T a[AB];
+#pragma unroll
+    for (int j = 0; j < AB; ++j) {
+        const int r = 4 * (s0 + j) + tig;
+        a[j] = (c < Lo && r < Li && s0 + j < s1) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // the copies' tail past Li is scratch: zero it (0 * NaN would poison the MMA)
+    for (int idx = tid; idx < nv * (LiP - Li); idx += 256) {
+        const int v = idx / (LiP - Li), r = Li + idx - v * (LiP - Li);
+        wsm[v * LiP + r] = 0.0;
+    }
+    __syncthreads();
+    double acc[NT][2];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < AB; ++j) {
+        const int r = 4 * (s0 + j) + tig;
+        if (s0 + j < s1) {
+#pragma unroll
+            for (int q = 0; q < NT; ++q) dmma884(acc[q][0], acc[q][1], (double)a[j], wsm[(q * 8 + gid) * LiP + r]);
+        }
+    }
+    for (int sb = s0 + AB; sb < s1; ++sb) {   // long rows (Li > 1280)
+        const int r = 4 * sb + tig;
+        const double av = (c < Lo && r < Li) ? (double)__ldg(Mt + (int64_t)c * Li + r) : 0.0;
+#pragma unroll
+        for (int q = 0; q < NT; ++q) dmma884(acc[q][0], acc[q][1], av, wsm[(q * 8 + gid) * LiP + r]);
+    }
+    // lane holds Z^T tile rows c0 + gid, vectors q*8 + 2*tig + {0,1}
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+        red[warp][gid][q * 8 + 2 * tig] = acc[q][0];
+        red[warp][gid][q * 8 + 2 * tig + 1] = acc[q][1];
+    }
+    __syncthreads();
+    for (int e = tid; e < 8 * NT * 8; e += 256) {
+        const int row = e / (NT * 8), v = e - row * (NT * 8);
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][row][v];
+        if (c0 + row < Lo && v < nv) z[(int64_t)v * ldz + c0 + row] = s;
+    }
+}
+
 template <typename K, typename... A>
 static void pdl_launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
     cudaLaunchConfig_t lc = {};
@@ -500,8 +582,17 @@ static void rat_z_launch(const T* Mt, int Li, int Lo, const double* w, int ldw, 
     if (nv <= 1) go(k_rat_z<T, 1>, 1);
     else if (nv <= 2) go(k_rat_z<T, 2>, 2);
     else if (nv <= 4) go(k_rat_z<T, 4>, 4);
-    else if (nv <= 8) go(k_rat_z<T, 8>, 8);
-    else go(k_rat_z<T, 16>, 16);
+    else {   // 5..16 vectors: FP64 tensor cores
+        const int NT = nv <= 8 ? 1 : 2;
+        const size_t sm2 = sizeof(double) * (size_t)NT * 8 * ((Li + 3) & ~3);
+        if (NT == 1) {
+            KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+            pdl_launch(k_rat_z_mma<T, 1>, dim3((Lo + 7) / 8), sm2, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
+        } else {
+            KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+            pdl_launch(k_rat_z_mma<T, 2>, dim3((Lo + 7) / 8), sm2, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
+        }
+    }
 }
 
 // y[v][a*n + b] = (T) z[v][b - a + co] (0 outside [0, Lo))
