@@ -793,9 +793,22 @@ __device__ __forceinline__ void tile_diag_atomics(const PkParams& P, const TileG
             const int d = dlo + i, u = d + ci;
             if (u < 0 || u >= Li) continue;
             const int a_lo = max(A0, C0 - d), a_hi = min(A1, C0 + Gm.TW - d);
+            // x * 2^F is exact in fp32 (a power of two, |x| <= 1, F <= 60), and its
+            // round-to-nearest integer equals __double2ll_rn((double)x * 2^F): one
+            // conversion per entry; 8 entries in flight along the diagonal
+            const float fs = (float)scale;
+            const float* pd = sb + (a_lo - A0) * Gm.TW + (a_lo + d - C0);
+            const int len = a_hi - a_lo, step = Gm.TW + 1;
             long long s = 0;
-            for (int a = a_lo; a < a_hi; ++a)
-                s += __double2ll_rn((double)sb[(a - A0) * Gm.TW + (a + d - C0)] * scale);
+            int k = 0;
+            for (; k + 8 <= len; k += 8) {
+                float q[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q[j] = pd[(k + j) * step];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s += __float2ll_rn(q[j] * fs);
+            }
+            for (; k < len; ++k) s += __float2ll_rn(pd[k * step] * fs);
             if (s != 0) atomicAdd(wf + u, (unsigned long long)s);
         }
         g += h;

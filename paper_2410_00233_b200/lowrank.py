@@ -300,7 +300,9 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
 
     y0d = None
     if y0 is None:
-        pass   # drawn on the device right before the launch (below)
+        # the reference's draws (lowrank.py:199-201), generated on the device; launched
+        # first, so the draw runs while the host prepares the eGKB launch
+        y0d = rng.standard_normal(config.seed, mbar, dtype)
     elif D.is_tensor(y0):
         y0d = D.to_device(y0, dtype)
         if tuple(y0d.shape) != (mbar,):
@@ -339,10 +341,6 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
     st.sigma_host = hist[6].ctypes.data_as(dp)
     nb = C.c_size_t()
     _lib.check(lib.kb_egkb_workspace_bytes(C.byref(op.struct), cap, C.byref(nb)))
-    if y0d is None:
-        # the reference's draws (lowrank.py:199-201), generated on the device; launched
-        # after the host-side set-up so the RNG and the eGKB kernels run back to back
-        y0d = rng.standard_normal(config.seed, mbar, dtype)
     ws, wsb = D.WORKSPACE.get(nb.value)
     status = lib.kb_egkb_run(C.byref(op.struct), C.byref(cfg), y0d.data_ptr(), C.byref(st), ws, wsb,
                              D.stream_ptr())
