@@ -201,6 +201,18 @@ int kb_div_cast(const double* src, double divisor, int dtype, void* dst, int64_t
  * C-ordered float64 kernel -- numpy's pairwise summation, bit for bit --
  * and *min_out = k.min(), using `threads` host threads.  Host only. */
 int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out);
+/* kb_psf_scan that also copies k into the library's pinned PSF staging
+ * buffer while it is in cache; *ticket names the staged copy.  The commit
+ * is a stream-ordered copy of exactly that content to `dst` (KB_EVALIDATION
+ * when a later scan has replaced it). */
+int kb_psf_scan_stage(const double* k, int64_t n, int threads, double* sum_out, double* min_out,
+                      long long* ticket);
+int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_stream_t stream);
+/* The staged kernel normalised on the host -- (k / total).astype(float32),
+ * bit for bit numpy's, `threads` host threads -- and sent as fp32 (half the
+ * bytes of the raw upload): the fp32 operator's K without a device cast. */
+int kb_stage_commit_f32(long long ticket, double total, float* dst, size_t count, int threads,
+                        kb_stream_t stream);
 /* bytes of host memory -> device `dst`, through a library-owned pinned
  * buffer filled by `threads` host threads, chunk-pipelined with the copies
  * (stream-ordered on `stream`; the host array may be reused on return). */

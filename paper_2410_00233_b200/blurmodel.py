@@ -10,6 +10,7 @@ by :func:`egkb`, :func:`rsvd` and :func:`tsvd` wherever a dense ``b_mat`` is.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -41,14 +42,20 @@ def _min(k: np.ndarray) -> float:
 
 
 _SCAN_MIN = 1 << 16
-_HOST_THREADS = 8
+_HOST_THREADS = max(1, min(16, os.cpu_count() or 1))
 
 
-def _scan(k: np.ndarray) -> tuple[float, np.float64]:
+def _scan(k: np.ndarray) -> tuple[float, np.float64, int]:
+    """min, numpy-exact sum, and a ticket for the copy of k staged (pinned) on the way."""
     lib = _lib.load()
-    total, kmin = C.c_double(), C.c_double()
-    _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin)), "kb_psf_scan")
-    return kmin.value, np.float64(total.value)
+    total, kmin, ticket = C.c_double(), C.c_double(), C.c_longlong()
+    if lib.kb_psf_scan_stage(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin),
+                             C.byref(ticket)) != _lib.KB_OK:
+        # no device to stage for (e.g. host-only use of the formats): the scan alone
+        _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin)),
+                   "kb_psf_scan")
+        ticket.value = 0
+    return kmin.value, np.float64(total.value), ticket.value
 
 
 class Psf:
@@ -61,7 +68,7 @@ class Psf:
     (``kb_div_cast``), so the host makes no normalised or fp32 copy.
     """
 
-    __slots__ = ("_raw", "_total", "_kernel")
+    __slots__ = ("_raw", "_total", "_kernel", "_ticket")
 
     def __init__(self, kernel):
         k = np.asarray(kernel, dtype=np.float64)
@@ -74,7 +81,7 @@ class Psf:
         if k.size >= _SCAN_MIN and k.flags.c_contiguous:
             # min and numpy's pairwise sum in one multithreaded host pass (kb_psf_scan:
             # bit-identical to k.sum(), which is single-threaded)
-            kmin, total = _scan(k)
+            kmin, total, ticket = _scan(k)
             if not kmin >= 0 and np.any(k < 0):
                 raise ValidationError("PSF kernel must be non-negative")
         else:
@@ -85,6 +92,7 @@ class Psf:
         if total <= 0:
             raise ValidationError("PSF kernel must have positive mass")
         self._raw, self._total, self._kernel = k, total, None
+        self._ticket = ticket if k.size >= _SCAN_MIN and k.flags.c_contiguous else 0
 
     @property
     def kernel(self) -> np.ndarray:
@@ -101,10 +109,23 @@ class Psf:
 
         if self._kernel is not None:
             return D.upload(self._kernel, dtype)
+        lib = _lib.load()
+        if self._ticket and np.dtype(dtype) == np.float32:
+            # normalised + cast on the host from the copy staged by the scan: 4 bytes per entry on the wire
+            out = D.empty(self.shape, np.float32)
+            ok = lib.kb_stage_commit_f32(self._ticket, float(self._total), out.data_ptr(), self._raw.size,
+                                         _HOST_THREADS, D.stream_ptr()) == _lib.KB_OK
+            self._ticket = 0
+            if ok:
+                return out
         raw = D.empty(self._raw.shape, np.float64)
-        src = np.ascontiguousarray(self._raw)
-        _lib.check(_lib.load().kb_stage_upload(src.ctypes.data, src.nbytes, raw.data_ptr(), _HOST_THREADS,
-                                               D.stream_ptr()), "kb_stage_upload")
+        # the copy staged by the validation scan, if still current; else a staged upload
+        if not (self._ticket and lib.kb_stage_commit(self._ticket, raw.data_ptr(), self._raw.nbytes,
+                                                     D.stream_ptr()) == _lib.KB_OK):
+            src = np.ascontiguousarray(self._raw)
+            _lib.check(lib.kb_stage_upload(src.ctypes.data, src.nbytes, raw.data_ptr(), _HOST_THREADS,
+                                           D.stream_ptr()), "kb_stage_upload")
+        self._ticket = 0
         out = D.empty(self.shape, dtype)
         code = _lib.KB_F32 if np.dtype(dtype) == np.float32 else _lib.KB_F64
         _lib.check(_lib.load().kb_div_cast(raw.data_ptr(), float(self._total), code, out.data_ptr(), raw.numel(),

@@ -76,7 +76,23 @@ double combine(int64_t n, int depth, const double* leaf_sum, int& idx) {
 namespace kb {
 namespace {
 
-void psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out) {
+// Library-owned pinned staging for the PSF: filled during the scan (the data is
+// in cache there), committed to the device later by ticket.
+struct Stage {
+    char* buf = nullptr;
+    size_t cap = 0;
+    size_t bytes = 0;
+    long long ticket = 0;
+    cudaEvent_t done = nullptr;   // last copy out of buf / buf32
+    float* buf32 = nullptr;       // fp32 normalised copy (kb_stage_commit_f32)
+    size_t cap32 = 0;
+};
+Stage& stage() {
+    static Stage s;
+    return s;
+}
+
+void psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out, char* copy_to = nullptr) {
     if (n == 0) {
         *sum_out = 0.0;
         *min_out = 0.0;
@@ -91,6 +107,7 @@ void psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* 
     for (int i = 0; i < (int)leaves.size(); ++i) {
         const double* a = k + leaves[i].lo;
         sums[i] = pairwise_sum(a, leaves[i].n);
+        if (copy_to) std::memcpy(copy_to + sizeof(double) * leaves[i].lo, a, sizeof(double) * leaves[i].n);
         double m = a[0];
         for (int64_t j = 1; j < leaves[i].n; ++j) m = std::min(m, a[j]);   // NaN: caught by the sum / > 0 tests
         mins[i] = m;
@@ -148,6 +165,69 @@ extern "C" int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_
     KB_GUARD({
         KB_REQUIRE(k && n >= 0 && sum_out && min_out, "bad arguments");
         kb::psf_scan(k, n, threads, sum_out, min_out);
+    })
+}
+
+extern "C" int kb_psf_scan_stage(const double* k, int64_t n, int threads, double* sum_out, double* min_out,
+                                 long long* ticket) {
+    KB_GUARD({
+        KB_REQUIRE(k && n >= 0 && sum_out && min_out && ticket, "bad arguments");
+        kb::Stage& st = kb::stage();
+        if (!st.done) KB_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+        KB_CUDA(cudaEventSynchronize(st.done));   // the previous commit has left the buffer
+        const size_t bytes = sizeof(double) * (size_t)n;
+        if (st.cap < bytes) {
+            if (st.buf) cudaFreeHost(st.buf);
+            st.buf = nullptr;
+            st.cap = 0;
+            KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.buf), bytes));
+            st.cap = bytes;
+        }
+        kb::psf_scan(k, n, threads, sum_out, min_out, st.buf);
+        st.bytes = bytes;
+        *ticket = ++st.ticket;
+    })
+}
+
+extern "C" int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_stream_t stream) {
+    KB_GUARD({
+        kb::Stage& st = kb::stage();
+        KB_REQUIRE(dst && ticket == st.ticket && bytes == st.bytes, "staged PSF is no longer available");
+        cudaStream_t s = kb::as_stream(stream);
+        KB_CUDA(cudaMemcpyAsync(dst, st.buf, bytes, cudaMemcpyHostToDevice, s));
+        KB_CUDA(cudaEventRecord(st.done, s));
+    })
+}
+
+namespace kb {
+namespace {
+void commit_f32(Stage& st, double total, float* dst, int threads, cudaStream_t s) {
+    const int64_t n = (int64_t)(st.bytes / sizeof(double));
+    if (st.cap32 < (size_t)n) {
+        if (st.buf32) cudaFreeHost(st.buf32);
+        st.buf32 = nullptr;
+        st.cap32 = 0;
+        KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.buf32), sizeof(float) * (size_t)n));
+        st.cap32 = (size_t)n;
+    }
+    const double* src = reinterpret_cast<const double*>(st.buf);
+    float* out = st.buf32;
+    // (k / total).astype(float32): IEEE fp64 division, then round to fp32 (bitwise numpy)
+#pragma omp parallel for num_threads(std::max(1, threads)) schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = (float)(src[i] / total);
+    KB_CUDA(cudaMemcpyAsync(dst, out, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, s));
+    KB_CUDA(cudaEventRecord(st.done, s));
+}
+}  // namespace
+}  // namespace kb
+
+extern "C" int kb_stage_commit_f32(long long ticket, double total, float* dst, size_t count, int threads,
+                                   kb_stream_t stream) {
+    KB_GUARD({
+        kb::Stage& st = kb::stage();
+        KB_REQUIRE(dst && ticket == st.ticket && count * sizeof(double) == st.bytes,
+                   "staged PSF is no longer available");
+        kb::commit_f32(st, total, dst, threads, kb::as_stream(stream));
     })
 }
 

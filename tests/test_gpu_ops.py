@@ -197,3 +197,23 @@ class TestOrthonormalize:
     def test_too_many_columns(self, kb):
         with pytest.raises(kb.ValidationError):
             kb.orthonormalize(np.ones((3, 5)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("side", [31, 513])
+def test_device_psf_is_numpys_normalisation_bitwise(kb, dtype, side):
+    """blurmodel.py:25-65: the device K is (k / k.sum()).astype(dtype) bit for bit, whichever
+    upload path runs (scan-staged fp32 commit, staged raw fp64 + device cast, or the small-PSF path)."""
+    from paper_2410_00233_b200 import device as D
+
+    rng = np.random.default_rng(side)
+    k = rng.random((side, side)) ** 3
+    blur = kb.RearrangedBlur(k, 1024 if side == 513 else 64, dtype=dtype)
+    kd, kt = blur._device_kernels()
+    want = (k / k.sum()).astype(dtype)
+    assert np.array_equal(D.to_host(kd), want)
+    assert np.array_equal(D.to_host(kt), want.T)
+    # the staged copy is consumed once; a second operator from the same Psf uploads again
+    blur2 = kb.RearrangedBlur(blur.psf, blur.n, dtype=dtype)
+    assert np.array_equal(D.to_host(blur2._device_kernels()[0]), want)
