@@ -60,6 +60,7 @@ struct PkParams {
     unsigned* bar;       // [0]: arrivals, [32]: generation, [64..): per-column-chunk finish counters
     int nbar;            // words in bar + wfix (zeroed before the launch)
     unsigned long long* wfix;   // [2][Lmax] fixed-point diagonal sums (tiled kernel)
+    long long* xacc;            // [2][cap + 4][3] exact limb accumulators of the grid sums (tiled kernel)
     void* raw_s;         // pending unnormalised s vector (N elements)
     void* raw_q;         // pending unnormalised q vector
     int ng;              // element groups per thread
@@ -702,6 +703,32 @@ __device__ __forceinline__ void ring_fill(float* ring, int stage_floats, int tbo
     cp_async_commit();
 }
 
+// ---- exact grid sums without a partial array: every CTA adds its fp64 partial,
+// scaled by 2^79, as three 40-bit integer limbs (trunc toward zero, so each
+// limb carries the value's sign) with 64-bit integer REDs; integer addition is
+// exact and order-free, <= 2^9 CTAs leave 24 bits of headroom per limb, and
+// |partial| < 2^39 is far above anything a half step produces.  After the
+// grid sync each CTA reads the 3 limb sums (one line) and recombines them in
+// a fixed order: deterministic, and at least as accurate as an fp64 tree.
+constexpr int XACC_S = 79;
+__device__ __forceinline__ void xacc_add(long long* acc3, double x) {
+    const double y = ldexp(x, XACC_S);
+    const double hi = trunc(ldexp(y, -80));
+    const double r1 = y - ldexp(hi, 80);          // exact: multiples of ulp(y), |r1| < 2^80
+    const double mid = trunc(ldexp(r1, -40));
+    const double r2 = r1 - ldexp(mid, 40);        // exact, |r2| < 2^40
+    const long long lo = __double2ll_rn(r2);
+    if (hi != 0.0) atomicAdd(reinterpret_cast<unsigned long long*>(acc3 + 0), (unsigned long long)(long long)hi);
+    if (mid != 0.0) atomicAdd(reinterpret_cast<unsigned long long*>(acc3 + 1), (unsigned long long)(long long)mid);
+    if (lo != 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc3 + 2), (unsigned long long)lo);
+}
+__device__ __forceinline__ double xacc_get(const long long* acc3) {
+    const long long h = (long long)__ldcg(reinterpret_cast<const unsigned long long*>(acc3 + 0));
+    const long long m = (long long)__ldcg(reinterpret_cast<const unsigned long long*>(acc3 + 1));
+    const long long l = (long long)__ldcg(reinterpret_cast<const unsigned long long*>(acc3 + 2));
+    return ldexp(ldexp((double)h, 80) + ldexp((double)m, 40) + (double)l, -XACC_S);
+}
+
 struct TileGeo {
     int TW, LR, RW, RB, T;   // tile width, lanes per row, rows per warp, row blocks, tiles
 };
@@ -937,13 +964,17 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     vsq = warp_sum(vsq);
     if (lane == 0) acc[warp] = vsq;
     __syncthreads();
+    long long* xdot = P.xacc;                       // [cap + 4][3]: dots / |v|^2 / |y|^2
+    long long* xnrm = P.xacc + 3 * (P.cap + 4);     // [3]: |v1|^2 (and |y0|^2)
     if (tid == 0) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += acc[w];
-        P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
+        xacc_add(xnrm, s);
     }
-    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red, acc);
+    grid.sync();
+    if (tid == 0) red[0] = xacc_get(xnrm);
+    __syncthreads();
     pk_mark(P, 1);
     const double t1 = sqrt(red[0]);
     // entries of a normalised vector are <= 1: one fixed-point scale for the run
@@ -983,6 +1014,9 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         const float* Mt = static_cast<const float*>(tr ? P.K : P.Kt);   // rows of M^T (M = K or K^T)
         unsigned long long* wcur = P.wfix + (int64_t)(step & 1) * P.lmax;
 
+        // the accumulators were last read before the previous phase's sync: reset them
+        if (blockIdx.x == 0)
+            for (int j = tid; j < 3 * (P.cap + 5); j += PK_THREADS) P.xacc[j] = 0;
         // ---- A: z rows from the diagonal sums of the input vector.  The ring
         // starts fetching the first basis vectors of the dots (phase B) now.
         if constexpr (STREAM) {
@@ -1087,9 +1121,11 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < 8; ++w) t += acc[w * W + j];
-            P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
+            xacc_add(xdot + 3 * j, t);
         }
-        pk_reduce_barrier(P, gen, P.blk_part, P.cap + 4, W, red, acc);
+        grid.sync();
+        for (int j = tid; j < W; j += PK_THREADS) red[j] = xacc_get(xdot + 3 * j);
+        __syncthreads();
         pk_mark(P, 4);
         const double aux = red[m + 1];
         const double vnorm = sqrt(red[m]);
@@ -1161,9 +1197,11 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 double s = 0.0;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) s += acc[w];
-                P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
+                xacc_add(xnrm, s);
             }
-            pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
+            grid.sync();
+            if (tid == 0) red[P.cap + 2] = xacc_get(xnrm);
+            __syncthreads();
             pk_mark(P, 5);
             val = sqrt(red[P.cap + 2]);
         }
@@ -1373,12 +1411,15 @@ static bool tiled_launch(PkParams& P, cudaStream_t st) {
 // Sizes of the scratch the persistent kernel needs (doubles).
 // barrier words (unsigned): arrivals, generation, per-column-chunk counters
 static size_t pk_bar_only_words(int lmax) { return (64 + (size_t)(lmax + 31) / 32 + 32 + 1) & ~(size_t)1; }
-static size_t pk_bar_words(int lmax) { return pk_bar_only_words(lmax) + 4 * (size_t)lmax; }
-static size_t pk_bar_doubles(int lmax) { return (pk_bar_words(lmax) + 1) / 2; }
+static size_t pk_xacc_words(int cap) { return 2 * 2 * 3 * (size_t)(cap + 4); }
+static size_t pk_bar_words(int lmax, int cap) {
+    return pk_bar_only_words(lmax) + 4 * (size_t)lmax + pk_xacc_words(cap);
+}
+static size_t pk_bar_doubles(int lmax, int cap) { return (pk_bar_words(lmax, cap) + 1) / 2; }
 
 size_t pk_scratch_doubles(int lmax, int cap) {
     return 2 * (size_t)PK_SEGS * lmax + (size_t)(8 * kSMs) * (cap + 4) + 8 * kSMs * PK_NSTRIDE + 2 * (size_t)cap + 256 +
-           (size_t)lmax + (size_t)cap + 8 + pk_bar_doubles(lmax);
+           (size_t)lmax + (size_t)cap + 8 + pk_bar_doubles(lmax, cap);
 }
 
 // Returns false when the configuration is outside the persistent kernel's
@@ -1427,8 +1468,9 @@ bool egkb_persistent(const kb_operator* op, const kb_egkb_config* cfg, kb_egkb_s
     P.zbuf = P.norm_part + 8 * kSMs * PK_NSTRIDE + 2 * (size_t)cap + 256;
     P.bres = P.zbuf + lmax;
     P.bar = reinterpret_cast<unsigned*>(P.bres + cap + 8);
-    P.nbar = (int)pk_bar_words(lmax);
+    P.nbar = (int)pk_bar_words(lmax, cap);
     P.wfix = reinterpret_cast<unsigned long long*>(P.bar + pk_bar_only_words(lmax));
+    P.xacc = reinterpret_cast<long long*>(P.wfix + 2 * (size_t)lmax);
     P.raw_s = raw;
     P.raw_q = static_cast<char*>(raw) + (size_t)N * (op->dtype == KB_F32 ? 4 : 8);
     *scales_out = nullptr;
