@@ -172,42 +172,15 @@ __device__ __forceinline__ void pk_reduce_slots(const double* part, int stride, 
     }
 }
 
-// out[c] = sum_{q < PK_SEGS} part[q * stride + c] for c < len (fixed order),
-// 4 entries per thread per round with all 32 loads in flight.  No barrier.
-__device__ __forceinline__ void pk_stage_segs(const double* part, int64_t stride, int len, double* out) {
-    for (int c0 = threadIdx.x; c0 < len; c0 += 4 * PK_THREADS) {
-        double q[4][PK_SEGS];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int c = c0 + r * PK_THREADS;
-#pragma unroll
-            for (int s = 0; s < PK_SEGS; ++s) q[r][s] = c < len ? __ldcg(part + s * stride + c) : 0.0;
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int c = c0 + r * PK_THREADS;
-            double t = 0.0;
-#pragma unroll
-            for (int s = 0; s < PK_SEGS; ++s) t += q[r][s];
-            if (c < len) out[c] = t;
-        }
-    }
-}
 
-// Grid barrier fused with a fixed-order reduction.  Every CTA has written
-// its partials part[b * stride + j] (j < nslots); the LAST CTA to arrive sums
-// them (pk_reduce_slots: one CTA reads them, instead of every CTA reading the
-// same few lines), publishes the sums to P.bres and releases the others,
-// which copy them.  On return out[j] (shared memory) holds the sums in every
-// CTA.  Acts as a full grid barrier: arrival is an acq_rel atomic on one
-// counter (reset by the last arriver before it releases), release is a
-// st.release of the generation word, observed with ld.acquire by thread 0 of
-// each waiting CTA (the same protocol as cooperative_groups' grid.sync).
-// `gen` is thread 0's copy of the generation, advanced once per call.
-__device__ __forceinline__ void pk_reduce_barrier(const PkParams& P, unsigned& gen, const double* part, int stride,
-                                                  int nslots, double* out, double* tmp) {
-    (void)P;
-    (void)gen;
+// Grid barrier followed by the fixed-order reduction of the per-CTA partials
+// part[b * stride + j] (j < nslots) in every CTA (pk_reduce_slots: coalesced,
+// one L2 round trip).  A "last arriver reduces and publishes" variant was
+// measured slower (tools/red_probe.cu: 3.5 vs 2.7 us for 15 slots); the tiled
+// kernel avoids the partial array altogether (xacc_add / xacc_get).  On
+// return out[j] (shared memory) holds the sums in every CTA.
+__device__ __forceinline__ void pk_reduce_barrier(const double* part, int stride, int nslots, double* out,
+                                                  double* tmp) {
     cg::this_grid().sync();
     pk_reduce_slots(part, stride, gridDim.x, nslots, out, tmp);
 }
@@ -226,8 +199,7 @@ struct PkHalf {
 
 // One half step.  Returns t = |v1| (identical in every CTA).
 template <typename T, int VEC, int MAXG>
-__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid,
-                          unsigned& gen) {
+__device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, double& ysq_out, cg::grid_group& grid) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
     const int64_t N = (int64_t)n * n;
@@ -411,7 +383,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
         for (int w = 0; w < 8; ++w) t += acc[w * W + j];
         P.blk_part[(int64_t)blockIdx.x * (P.cap + 4) + j] = t;
     }
-    pk_reduce_barrier(P, gen, P.blk_part, P.cap + 4, W, red, acc);
+    pk_reduce_barrier(P.blk_part, P.cap + 4, W, red, acc);
     pk_mark(P);
     ysq_out = red[H.m + 1];
     double t;
@@ -457,7 +429,7 @@ __device__ double pk_half(const PkParams& P, const PkHalf<T>& H, double* sm, dou
         for (int w = 0; w < 8; ++w) s += acc[w];
         P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
     }
-    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
+    pk_reduce_barrier(P.norm_part, PK_NSTRIDE, 1, red + P.cap + 2, acc);
     pk_mark(P);
     t = sqrt(red[P.cap + 2]);
     }
@@ -494,10 +466,6 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
     const int64_t G = (int64_t)nblk * PK_THREADS;
     const int64_t gt = (int64_t)blockIdx.x * PK_THREADS + tid;
     const bool rec = (blockIdx.x == 0 && tid == 0);
-    // generation of the reduce-barrier at entry (stable: it only advances once
-    // every CTA has arrived at the first reduce-barrier)
-    unsigned gen = 0;
-    if (tid == 0) asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(P.bar + 32) : "memory");
 
     // ---- s1 = y0 / |y0|   (lowrank.py:207-210)
     T v0[MAXG][VEC];
@@ -519,7 +487,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
         for (int w = 0; w < 8; ++w) s += acc[w];
         P.norm_part[(int64_t)blockIdx.x * PK_NSTRIDE] = s;
     }
-    pk_reduce_barrier(P, gen, P.norm_part, PK_NSTRIDE, 1, red, acc);
+    pk_reduce_barrier(P.norm_part, PK_NSTRIDE, 1, red, acc);
     pk_mark(P);
     const double t1 = sqrt(red[0]);
     {
@@ -557,7 +525,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_persistent(PkParams P) {
                           Q + (int64_t)done * P.ld_q, 1};
         }
         double aux = 0.0;
-        const double val = pk_half<T, VEC, MAXG>(P, h, sm, aux, grid, gen);
+        const double val = pk_half<T, VEC, MAXG>(P, h, sm, aux, grid);
         if (step == 0) {
             const double a1 = val;
             zeta_last = a1 * t1;
@@ -687,15 +655,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int PK_NS = 4;   // ring stages (basis vectors in flight per thread)
-
-// Item G of the thread's stream (stage G % PK_NS) <- its float4 of each owned tile of `vec`
-// (vec == nullptr: an empty group, keeps the group accounting uniform).
+// ring stages (basis vectors in flight per thread): 4 with <= 4 owned tiles
+// per thread; with more tiles one stage already keeps 8-16 float4 per thread
+// in flight, and the ring shares the tile buffer (used only in phase D)
 template <int MAXG>
+__host__ __device__ constexpr int pk_ns() { return MAXG <= 4 ? 4 : (MAXG <= 8 ? 2 : 1); }
+
+// Item G of the thread's stream (stage G % NS) <- its float4 of each owned tile of `vec`
+// (vec == nullptr: an empty group, keeps the group accounting uniform).
+template <int MAXG, int NS>
 __device__ __forceinline__ void ring_fill(float* ring, int stage_floats, int tbo, unsigned G, const float* vec,
                                           const int (&eo)[MAXG], int ng) {
     if (vec) {
-        float* dst = ring + (int)(G % PK_NS) * stage_floats + tbo;
+        float* dst = ring + (int)(G % NS) * stage_floats + tbo;
 #pragma unroll
         for (int g = 0; g < MAXG; ++g)
             if (g < ng) cp_async16(dst + g * 1024, vec + eo[g]);
@@ -748,59 +720,6 @@ __device__ __forceinline__ int pk_fix_exp(double vnorm, int n) {
     return 62 - ln - e;
 }
 
-// Colsum items of one R(A) product: part[s][c] = sum_{r in seg s} M[r, c] w(r),
-// the last of a chunk's PK_SEGS items writes z[c] = sum_s part[s][c].
-template <typename WF>
-__device__ __forceinline__ void pk_colsum_items(const PkParams& P, const float* M, int Li, int Lo, double* ws,
-                                                double* acc, WF wf) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int chunks = (Lo + 31) / 32;
-    const int items = chunks * PK_SEGS;
-    __shared__ int s_fin;
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int cc = it % chunks, seg = it / chunks;
-        const int c = cc * 32 + lane;
-        const int r0 = (int)((int64_t)Li * seg / PK_SEGS), r1 = (int)((int64_t)Li * (seg + 1) / PK_SEGS);
-        for (int j = tid; j < r1 - r0; j += PK_THREADS) ws[j] = wf(r0 + j);
-        __syncthreads();
-        double a = 0.0;
-        int r = r0 + warp;
-        for (; r + 120 < r1; r += 128) {            // 16 independent K loads in flight
-            float mk[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) mk[k] = (c < Lo) ? __ldg(M + (int64_t)(r + 8 * k) * Lo + c) : 0.f;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) a += (double)mk[k] * ws[r + 8 * k - r0];
-        }
-        for (; r < r1; r += 8)
-            if (c < Lo) a += (double)__ldg(M + (int64_t)r * Lo + c) * ws[r - r0];
-        acc[warp * 33 + lane] = a;
-        __syncthreads();
-        if (warp == 0 && c < Lo) {
-            double t = 0.0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) t += acc[w * 33 + lane];
-            P.col_part[(int64_t)seg * P.lmax + c] = t;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            unsigned old;
-            asm volatile("atom.add.acq_rel.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(P.bar + 64 + cc), "r"(1u) : "memory");
-            s_fin = (old == PK_SEGS - 1);
-            if (s_fin) P.bar[64 + cc] = 0u;   // next use is several grid barriers later
-        }
-        __syncthreads();
-        if (s_fin && warp == 0 && c < Lo) {
-            double q[PK_SEGS];
-#pragma unroll
-            for (int sg = 0; sg < PK_SEGS; ++sg) q[sg] = __ldcg(P.col_part + (int64_t)sg * P.lmax + c);
-            double t = 0.0;
-#pragma unroll
-            for (int sg = 0; sg < PK_SEGS; ++sg) t += q[sg];
-            __stcg(P.zbuf + c, t);
-        }
-    }
-}
 
 // Diagonal sums of the CTA's register-held tile values (staged in tb) for a
 // product with diagonal offset ci and Li diagonals, added in fixed point to wf.
@@ -926,13 +845,12 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     double* red = zs + P.lmax;                     // [cap + 4]
     double* acc = red + P.cap + 4;                 // [8][max(cap + 2, 33)]
     float* tb = reinterpret_cast<float*>(acc + 8 * max(P.cap + 2, 33));   // [MAXG * 1024]
-    // basis streaming ring (MAXG <= 4): PK_NS stages after the tile buffer
-    constexpr bool STREAM = MAXG <= 4;
-    float* ringb = tb + MAXG * 1024;
+    // basis streaming ring: NS stages after the tile buffer (MAXG <= 4) or over it
+    constexpr int PK_NS = pk_ns<MAXG>();
+    float* ringb = MAXG <= 4 ? tb + MAXG * 1024 : tb;
     constexpr int SF = MAXG * 1024;                // floats per stage
     const bool rec = (blockIdx.x == 0 && tid == 0);
     const int cu = P.kh / 2, cv = P.kw / 2;
-    unsigned gen = 0;
 
     // element offsets of this thread (one float4 per tile)
     int t0, ng;
@@ -1019,11 +937,11 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int j = tid; j < 3 * (P.cap + 5); j += PK_THREADS) P.xacc[j] = 0;
         // ---- A: z rows from the diagonal sums of the input vector.  The ring
         // starts fetching the first basis vectors of the dots (phase B) now.
-        if constexpr (STREAM) {
+        {
             if (m > 0)
 #pragma unroll
                 for (int k = 0; k < PK_NS; ++k)
-                    ring_fill<MAXG>(ringb, SF, tbo, rbase + k, k < 2 * m ? B + (int64_t)(k % m) * ldb : nullptr, eo, ng);
+                    ring_fill<MAXG, PK_NS>(ringb, SF, tbo, rbase + k, k < 2 * m ? B + (int64_t)(k % m) * ldb : nullptr, eo, ng);
         }
         pk_zrows(P, Mt, Li, Lo, zs, wcur, fxs_inv);
         // prefetch prev (used right after the barrier) while the grid synchronises
@@ -1068,7 +986,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 for (int q = 0; q < 4; ++q) v[g][q] = 0.f;
             }
         }
-        if constexpr (STREAM) {
+        {
             // items rbase .. rbase + m - 1 of the stream: the basis vectors in order
             for (int i = 0; i < m; ++i) {
                 const unsigned G = rbase + i;
@@ -1084,27 +1002,11 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                         dt = fmaf(sv.z, v[g][2], dt);
                         dt = fmaf(sv.w, v[g][3], dt);
                     }
-                ring_fill<MAXG>(ringb, SF, tbo, G + PK_NS, i + PK_NS < 2 * m ? B + (int64_t)((i + PK_NS) % m) * ldb : nullptr,
+                ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + PK_NS, i + PK_NS < 2 * m ? B + (int64_t)((i + PK_NS) % m) * ldb : nullptr,
                                 eo, ng);
                 const double d = warp_sum((double)dt);
                 if (lane == 0) acc[warp * W + i] += d;
             }
-        } else {
-#pragma unroll 4
-        for (int i = 0; i < m; ++i) {
-            const float* Si = B + (int64_t)i * ldb;
-            float dt = 0.f;
-#pragma unroll
-            for (int g = 0; g < MAXG; ++g)
-                if (g < ng) {
-                    float sv[4];
-                    PkIO<float, 4>::load(Si + eo[g], sv);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) dt = fmaf(sv[q], v[g][q], dt);
-                }
-            const double d = warp_sum((double)dt);
-            if (lane == 0) acc[warp * W + i] += d;
-        }
         }
 #pragma unroll
         for (int g = 0; g < MAXG; ++g)
@@ -1137,12 +1039,11 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         if (m == 0) {
             val = vnorm;
         } else {
-            constexpr int GA = MAXG <= 4 ? MAXG : 4;
             float* cf = reinterpret_cast<float*>(acc);
             for (int i = tid; i < m; i += PK_THREADS) cf[i] = (float)red[i];
             __syncthreads();
             double v1sq = 0.0;
-            if constexpr (STREAM) {
+            {
                 // items rbase + m .. rbase + 2m - 1: the same basis vectors again
                 for (int i = 0; i < m; ++i) {
                     const unsigned G = rbase + m + i;
@@ -1158,35 +1059,13 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                             v[g][2] = fmaf(-c, sv.z, v[g][2]);
                             v[g][3] = fmaf(-c, sv.w, v[g][3]);
                         }
-                    ring_fill<MAXG>(ringb, SF, tbo, G + PK_NS, i + PK_NS < m ? B + (int64_t)(i + PK_NS) * ldb : nullptr,
+                    ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + PK_NS, i + PK_NS < m ? B + (int64_t)(i + PK_NS) * ldb : nullptr,
                                     eo, ng);
                 }
 #pragma unroll
                 for (int g = 0; g < MAXG; ++g)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) v1sq += (double)v[g][q] * (double)v[g][q];
-            } else {
-#pragma unroll
-            for (int g0 = 0; g0 < MAXG; g0 += GA) {
-                if (g0 >= ng) break;
-#pragma unroll 4
-                for (int i = 0; i < m; ++i) {
-                    const float* Si = B + (int64_t)i * ldb;
-                    const float c = cf[i];
-#pragma unroll
-                    for (int g = 0; g < GA; ++g)
-                        if (g0 + g < ng) {
-                            float sv[4];
-                            PkIO<float, 4>::load(Si + eo[g0 + g], sv);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) v[g0 + g][q] = fmaf(-c, sv[q], v[g0 + g][q]);
-                        }
-                }
-#pragma unroll
-                for (int g = 0; g < GA; ++g)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) v1sq += (double)v[g0 + g][q] * (double)v[g0 + g][q];
-            }
             }
             rbase += 2 * m;
             v1sq = warp_sum(v1sq);
@@ -1349,7 +1228,7 @@ template <int MAXG>
 static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaStream_t st) {
     auto kern = k_egkb_tiled<MAXG>;
     const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33)) +
-                        sizeof(float) * 1024 * MAXG * (MAXG <= 4 ? 1 + PK_NS : 1);
+                        sizeof(float) * 1024 * MAXG * (MAXG <= 4 ? 1 + pk_ns<MAXG>() : pk_ns<MAXG>());
     static bool configured = false;
     if (!configured) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
