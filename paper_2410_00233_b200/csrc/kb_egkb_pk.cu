@@ -116,6 +116,9 @@ struct PkIO<double, 2> {
 // A zero dividend (the exact zeros of the Gaussian-tail entries) would
 // still take the division's special-case path, so it is answered directly.
 __device__ __forceinline__ float pk_fdiv_exact(float a, float b) {
+    const float fa = fabsf(a);
+    if (fa >= 0x1p-100f && fa <= 0x1p100f)   // comfortably normal: the fp32 division's fast path
+        return __fdiv_rn(a, b);
     if (a == 0.f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000);
     double q;
     asm("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"((double)a), "d"((double)b));
@@ -957,28 +960,31 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
 
         // ---- B: zero the consumed w; z; y; v = y - beta*prev; dots
         for (int i = blockIdx.x * PK_THREADS + tid; i < P.lmax; i += nblk * PK_THREADS) wcur[i] = 0ull;
+        // z staged already rounded to fp32: y = fl32(z[u]) for every cell of a diagonal,
+        // so one conversion per diagonal instead of one per cell
+        float* zsf = reinterpret_cast<float*>(zs);
         for (int c0 = tid; c0 < Lo; c0 += 8 * PK_THREADS) {
             double q[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) q[k] = c0 + k * PK_THREADS < Lo ? __ldcg(P.zbuf + c0 + k * PK_THREADS) : 0.0;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (c0 + k * PK_THREADS < Lo) zs[c0 + k * PK_THREADS] = q[k];
+                if (c0 + k * PK_THREADS < Lo) zsf[c0 + k * PK_THREADS] = (float)q[k];
         }
         const int W = m + 2;
         for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
         __syncthreads();
-        double ysq = 0.0;
+        float ysqf = 0.f;   // |y|^2 only feeds the breakdown threshold: fp32 per thread
         vsq = 0.0;
 #pragma unroll
         for (int g = 0; g < MAXG; ++g) {
             if (g < ng) {
-                double yd[4];
-                ra_bcast4(zs, (unsigned)eo[g], n, co, Lo, false, yd);
+                const int a = eo[g] / n, b0 = eo[g] - a * n;   // 4 cells of one image row
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float yv = (float)yd[q];
-                    ysq += (double)yv * (double)yv;
+                    const int u = b0 + q - a + co;
+                    const float yv = (u >= 0 && u < Lo) ? zsf[u] : 0.f;
+                    ysqf = fmaf(yv, yv, ysqf);
                     v[g][q] = __fsub_rn(yv, __fmul_rn(beta, pv[g][q]));
                 }
             } else {
@@ -1013,7 +1019,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
 #pragma unroll
             for (int q = 0; q < 4; ++q) vsq += (double)v[g][q] * (double)v[g][q];
         vsq = warp_sum(vsq);
-        ysq = warp_sum(ysq);
+        const double ysq = warp_sum((double)ysqf);
         if (lane == 0) {
             acc[warp * W + m] += vsq;
             acc[warp * W + m + 1] += ysq;
