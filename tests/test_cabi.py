@@ -98,3 +98,37 @@ def test_no_gpu_compute_without_device():
         kb.EgkbConfig(k_max=0)
     with pytest.raises(kb.ValidationError):
         kb.SbConfig(lam=-1, beta=1)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (33, 33), (129, 257), (513, 513), (1025, 1025), (2049, 7)])
+def test_psf_scan_is_numpys_sum_and_min_bitwise(lib, shape):
+    """kb_psf_scan restates numpy's pairwise summation (blurmodel.py:25-65 Psf: k.sum())
+    on parallel subtrees: the sum must be bit-identical to k.sum(), the min exact.
+    Host-only: runs without a GPU."""
+    import numpy as np
+
+    rng = np.random.default_rng(sum(shape))
+    k = np.ascontiguousarray(rng.random(shape) ** 5 * 10.0 ** rng.uniform(-30, 30))
+    total, kmin = ctypes.c_double(), ctypes.c_double()
+    for threads in (1, 3, 8, 16):
+        assert lib.kb_psf_scan(k.ctypes.data, k.size, threads, ctypes.byref(total), ctypes.byref(kmin)) == 0
+        assert total.value == k.sum(), (shape, threads)
+        assert kmin.value == k.min()
+
+
+def test_psf_validation_uses_the_exact_scan():
+    """Psf (blurmodel.py:25-65) on a large kernel: the same mass and checks as the reference."""
+    import numpy as np
+    from paper_2410_00233_b200.blurmodel import Psf
+    from paper_2410_00233_b200.exceptions import ValidationError
+
+    rng = np.random.default_rng(7)
+    k = rng.random((513, 513))
+    p = Psf(k)
+    assert np.array_equal(p.kernel, k / k.sum())
+    bad = k.copy()
+    bad[100, 200] = -1e-300
+    with pytest.raises(ValidationError):
+        Psf(bad)
+    with pytest.raises(ValidationError):
+        Psf(np.zeros((513, 513)))
