@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int j = tid; j < 3 * (P.cap + 5); j += PK_THREADS) P.xacc[j] = 0;
         // ---- A: z rows from the diagonal sums of the input vector.  The ring
         // starts fetching the first basis vectors of the dots (phase B) now.
-        {
+        if constexpr (MAXG > 4) {   // (MAXG <= 4: issued during the previous step's phase D)
             if (m > 0)
 #pragma unroll
                 for (int k = 0; k < PK_NS; ++k)
@@ -1090,13 +1090,8 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             pk_mark(P, 5);
             val = sqrt(red[P.cap + 2]);
         }
-        // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
-        // sums for the next product
-        pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
-        grid.sync();
-        pk_mark(P, 6);
-
-        // ---- control (identical in every CTA; CTA 0 records the trace)
+        // ---- control (identical in every CTA; CTA 0 records the trace), before D so
+        // the next step's basis vectors stream in while D runs
         if (step == 0) {
             const double a1 = val;
             zeta_last = a1 * t1;
@@ -1111,13 +1106,10 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 err = 2;
                 stop = 1;
             }
-            continue;
-        }
-        if (tr == 0) {
+        } else if (tr == 0) {
             t_new = val;
             u2 = aux;
-            continue;
-        }
+        } else {
         const double a_new = val, p2 = aux;
         if (t_new <= P.tol * sqrt(u2)) {
             breakdown = tbreak = 1;
@@ -1162,6 +1154,27 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 overflow = 1;
             }
         }
+        }
+        if constexpr (MAXG <= 4) {   // the ring does not share the tile buffer used by D
+            if (!stop) {
+                const int trn = ((step + 1) & 1) ? 0 : 1;
+                const float* Bn = trn ? Q : S;
+                const int mn = trn ? done : (P.full_reorth ? done : 0);
+                const int64_t ldn = trn ? P.ld_q : P.ld_s;
+                if (mn > 0)
+#pragma unroll
+                    for (int k = 0; k < PK_NS; ++k)
+                        ring_fill<MAXG, PK_NS>(ringb, SF, tbo, rbase + k, k < 2 * mn ? Bn + (int64_t)(k % mn) * ldn : nullptr,
+                                               eo, ng);
+            }
+        }
+        // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
+        // sums for the next product
+        pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
+        grid.sync();
+        pk_mark(P, 6);
+
+        if (stop) break;
     }
     if (rec) {
         int* h = P.hdr;
