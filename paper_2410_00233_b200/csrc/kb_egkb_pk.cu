@@ -124,6 +124,17 @@ __device__ __forceinline__ float pk_fdiv_exact(float a, float b) {
     asm("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"((double)a), "d"((double)b));
     return (float)q;
 }
+// The same correctly rounded fl32(a / b) with rb = RN64(1 / b) precomputed:
+// for fp32 a and b the exact quotient is never closer than 2^-48 (relative)
+// to an fp32 rounding boundary unless it is representable, and (double)a * rb
+// is within 2^-52 of it, so rounding it to fp32 gives the correctly rounded
+// quotient -- subnormal results and signed zeros included -- for two
+// conversions and a multiply instead of a double division.
+__device__ __forceinline__ float pk_fdiv_exact(float a, float b, double rb) {
+    const float fa = fabsf(a);
+    if (fa >= 0x1p-100f && fa <= 0x1p100f) return __fdiv_rn(a, b);
+    return (float)((double)a * rb);
+}
 
 __device__ __forceinline__ float pk_mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double pk_mul(double a, double b) { return __dmul_rn(a, b); }
@@ -821,17 +832,20 @@ template <int MAXG>
 __device__ __forceinline__ void pk_store_diag(const PkParams& P, const TileGeo& Gm, float (&v)[MAXG][4], float td,
                                               float* out, const int (&eo)[MAXG], int ng, float* tb, int tbo, int t0,
                                               int ci, int Li, double fxs, unsigned long long* wf) {
+    const double rtd = 1.0 / (double)td;
 #pragma unroll
     for (int g = 0; g < MAXG; ++g)
         if (g < ng) {
             float o[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = pk_fdiv_exact(v[g][q], td);
+            for (int q = 0; q < 4; ++q) o[q] = pk_fdiv_exact(v[g][q], td, rtd);
             PkIO<float, 4>::store(out + eo[g], o);
             *reinterpret_cast<float4*>(tb + g * 1024 + tbo) = make_float4(o[0], o[1], o[2], o[3]);
         }
     __syncthreads();
+    pk_mark(P, 12);
     tile_diag_atomics<MAXG>(P, Gm, tb, t0, ng, ci, Li, fxs, wf);
+    pk_mark(P, 13);
 }
 
 template <int MAXG>
@@ -1170,6 +1184,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         }
         // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
         // sums for the next product
+        pk_mark(P, 14);
         pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
         grid.sync();
         pk_mark(P, 6);
