@@ -374,8 +374,8 @@ __global__ void __launch_bounds__(256) k_rat_diag(const T* __restrict__ X, int64
     pdl_trigger();
     if (tid < RT_DIAG) {
         const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
-        double s = 0.0;
         const int r0 = max(0, -off), r1 = min(RT_ROWS, RT_COLS - off);
+        double s = 0.0;
         for (int r = r0; r < r1; ++r) s += (double)tile[r][r + off];
         part[((int64_t)v * tiles + t) * RT_DP + tid] = s;
     }
@@ -599,7 +599,8 @@ static void rat_z_launch(const T* Mt, int Li, int Lo, const double* w, int ldw, 
 template <typename T>
 __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z, int ldz, int n, int co, int Lo,
                                                    T* __restrict__ Y, int64_t ldy) {
-    extern __shared__ double zsm[];
+    extern __shared__ double zraw[];
+    T* zsm = reinterpret_cast<T*>(zraw);   // z already rounded to T: one conversion per entry of z
     const int v = blockIdx.y;
     pdl_wait();
     for (int c0 = threadIdx.x; c0 < Lo; c0 += 8 * 256) {   // all loads in flight, then the stores
@@ -608,20 +609,32 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
         for (int k = 0; k < 8; ++k) q[k] = c0 + 256 * k < Lo ? __ldg(z + (int64_t)v * ldz + c0 + 256 * k) : 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (c0 + 256 * k < Lo) zsm[c0 + 256 * k] = q[k];
+            if (c0 + 256 * k < Lo) zsm[c0 + 256 * k] = (T)q[k];
     }
     __syncthreads();
     const int64_t N = (int64_t)n * n;
     T* y = Y + (int64_t)v * ldy;
-    for (int64_t e0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4; e0 < N; e0 += (int64_t)gridDim.x * 256 * 4) {
-        double yv[4];
-        ra_bcast4(zsm, (unsigned)e0, n, co, Lo, false, yv);
-        if constexpr (sizeof(T) == 4) {
-            __stcs(reinterpret_cast<float4*>(y + e0), make_float4((float)yv[0], (float)yv[1], (float)yv[2], (float)yv[3]));
-        } else {
-            __stcs(reinterpret_cast<double2*>(y + e0), make_double2(yv[0], yv[1]));
-            __stcs(reinterpret_cast<double2*>(y + e0 + 2), make_double2(yv[2], yv[3]));
+    // the cell (a, b) of e0 advances by a fixed stride: updated without a division
+    const int64_t stride = (int64_t)gridDim.x * 256 * 4;
+    const int da = (int)(stride / n), db = (int)(stride - (int64_t)da * n);
+    int64_t e0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+    int a = (int)(e0 / n), b = (int)(e0 - (int64_t)a * n);
+    for (; e0 < N; e0 += stride) {
+        T o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // n % 4 == 0: the 4 cells share the row a
+            const int u = b + q - a + co;
+            o[q] = (u >= 0 && u < Lo) ? zsm[u] : T(0);
         }
+        if constexpr (sizeof(T) == 4) {
+            __stcs(reinterpret_cast<float4*>(y + e0), make_float4(o[0], o[1], o[2], o[3]));
+        } else {
+            __stcs(reinterpret_cast<double2*>(y + e0), make_double2(o[0], o[1]));
+            __stcs(reinterpret_cast<double2*>(y + e0 + 2), make_double2(o[2], o[3]));
+        }
+        a += da;
+        b += db;
+        if (b >= n) { b -= n; ++a; }
     }
 }
 
