@@ -259,7 +259,15 @@ typedef struct {
     int m1, m2, n1, n2, k;
     const double* f;  /* k x n1 x m1: F_i = ax_i^T = reshape(sigma_i u_i, (n1, m1)) */
     const double* g;  /* k x n2 x m2: G_i = ay_i^T = reshape(v_i, (n2, m2))         */
+    const int* band;  /* optional device int[2] from kb_kron_band (NULL: dense G)    */
 } kb_kron;
+
+/* band[0..1] = min/max of (c - r) over the nonzero entries G_i[r][c] of all
+ * terms, stream-ordered on the device.  With it set in kb_kron, the G stage
+ * of every apply skips the k tiles that only meet zeros (bit-identical
+ * result; the v-side factors of a zero-BC approximation are banded Toeplitz).
+ * The band must be recomputed if g changes. */
+int kb_kron_band(const kb_kron* kr, int* band, kb_stream_t stream);
 
 int kb_kron_workspace_bytes(const kb_kron* kr, size_t* bytes);
 /* y = A x (transpose=0, kronop.py:58-70) or y = A^T x (kronop.py:72-84). */

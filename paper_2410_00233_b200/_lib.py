@@ -56,7 +56,7 @@ class KbEgkbState(C.Structure):
 
 class KbKron(C.Structure):
     _fields_ = [("m1", C.c_int), ("m2", C.c_int), ("n1", C.c_int), ("n2", C.c_int), ("k", C.c_int),
-                ("f", vp), ("g", vp)]
+                ("f", vp), ("g", vp), ("band", vp)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(None, vp, dp, i64, vp)
@@ -119,6 +119,7 @@ _SIGS = {
     "kb_toeplitz_lift": (C.c_int, [C.c_int, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, vp]),
     "kb_kron_workspace_bytes": (C.c_int, [P(KbKron), P(SZ)]),
     "kb_kron_apply": (C.c_int, [P(KbKron), vp, vp, C.c_int, vp, SZ, vp]),
+    "kb_kron_band": (C.c_int, [P(KbKron), vp, vp]),
     "kb_kron_assemble": (C.c_int, [C.c_int, vp, i64, vp, i64, dp, C.c_int, i64, i64, vp, vp, vp]),
     "kb_dgemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, i64, i64, vp, i64, i64,
                            i64, vp, i64, i64, C.c_int, C.c_int, C.c_double, vp]),

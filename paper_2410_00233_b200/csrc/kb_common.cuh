@@ -89,10 +89,16 @@ struct Sizer {
 // Masked GEMM work for batched solves: blocks whose problem is inactive exit.
 // rows > 0: problems stacked along M (problem = row / rows); rows == 0: the
 // problem is the batch index.  flags[p * stride] != 0 means active.
+// band (optional, nseg == 1 only): device int[2] (lo, hi) such that the
+// untransposed B operand's row r, column c can be nonzero only when
+// lo <= c - r <= hi (kb_kron_band); k tiles outside a CTA's column band are
+// all-zero products and are skipped (adding exact zeros never changes a sum,
+// so the result is bit-identical to the dense product).
 struct GemmSkip {
     const int* flags = nullptr;
     int stride = 0;
     int rows = 0;
+    const int* band = nullptr;
 };
 
 // ---------------------------------------------------------------- profiling

@@ -99,7 +99,14 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     const double* Bb = B + (int64_t)z * sb_batch;
     double* Cb = C + (int64_t)z * sc_batch + (int64_t)split * split_stride;
 
-    const int ktiles = (K + BK - 1) / BK;
+    int kt_first = 0, ktiles = (K + BK - 1) / BK;
+    if (skip.band) {   // banded B: only the k tiles that meet this CTA's columns
+        int lo = __ldg(skip.band), hi = __ldg(skip.band + 1);
+        if (TB) { const int t = lo; lo = -hi; hi = -t; }   // logical B[k][c] = G[c][k]
+        const int klo = max(0, n0 - hi), khi = min(K - 1, n0 + BN - 1 - lo);
+        kt_first = klo / BK;
+        ktiles = khi >= klo ? khi / BK + 1 - kt_first : 0;
+    }
     const int Ttot = ktiles * nseg;
     const int t_begin = (int)((int64_t)Ttot * split / splits);
     const int T = (int)((int64_t)Ttot * (split + 1) / splits) - t_begin;
@@ -107,7 +114,7 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     auto load_tile = [&](int stage, int tt) {
         const int t = tt + t_begin;
         const int s = t / ktiles;
-        const int k0 = (t - s * ktiles) * BK;
+        const int k0 = (t - s * ktiles + kt_first) * BK;
         const double* Ap = Ab + (int64_t)s * sa_seg;
         const double* Bp = Bb + (int64_t)s * sb_seg;
         double* as = As + stage * AL::size;

@@ -12,6 +12,7 @@
 // order).  Vector updates mirror the reference's rounding (no FMA contraction:
 // x + mu*w is two rounded ops, as numpy does).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -330,10 +331,15 @@ void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, do
     const int64_t pq = (int64_t)k * std::max((int64_t)n1 * m2, (int64_t)m1 * n2);
     double* part = tmp + ((pq + 31) / 32) * 32;
     const int64_t part_n = (int64_t)KRON_SPLIT_MAX * std::max((int64_t)m1 * m2, (int64_t)n1 * n2);
+    struct Reset {
+        ~Reset() { g_dgemm_skip = GemmSkip{}; }
+    } reset;
+    g_dgemm_skip.band = kr->band;   // stage 1 only: G's zero band (kb_kron_band)
     if (!transpose) {
         // P_i = Xr G_i            (n1 x m2), Xr = x as n1 x n2, G_i n2 x m2
         dgemm(0, 0, n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
               (int64_t)n1 * m2, k, 1, 0.0, st);
+        g_dgemm_skip = GemmSkip{};
         // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1
         dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
               0, 1, k, 0.0, st, part, part_n);
@@ -341,6 +347,7 @@ void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, do
         // Q_i = Yr G_i^T          (m1 x n2), Yr = y as m1 x m2
         dgemm(0, 1, m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
               (int64_t)m1 * n2, k, 1, 0.0, st);
+        g_dgemm_skip = GemmSkip{};
         // Xr = sum_i F_i Q_i      (n1 x n2)
         dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
               0, 1, k, 0.0, st, part, part_n);
@@ -768,6 +775,52 @@ extern "C" int kb_kron_workspace_bytes(const kb_kron* kr, size_t* bytes) {
     }
 }
 
+// lo = min, hi = max of (c - r) over the nonzero entries G_i[r][c] of all
+// terms (band[0] > band[1] when G is all zero).  For zero boundary conditions
+// the v-side factors are banded Toeplitz matrices: every q-basis vector is a
+// combination of R(A)^T products, whose entries vanish exactly where the PSF
+// underflows.
+__global__ void k_kron_band_init(int* band) { band[0] = INT_MAX; band[1] = INT_MIN; }
+__global__ void k_kron_band(const double* __restrict__ g, int k, int n2, int m2, int* band) {
+    const int64_t per = (int64_t)n2 * m2, total = per * k;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (g[e] != 0.0) {
+            const int64_t rem = e % per;
+            const int d = (int)(rem % m2) - (int)(rem / m2);
+            lo = min(lo, d);
+            hi = max(hi, d);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(band, lo);
+        atomicMax(band + 1, hi);
+    }
+}
+
+extern "C" int kb_kron_band(const kb_kron* kr, int* band, kb_stream_t stream) {
+    try {
+        KB_REQUIRE(kr && kr->g && band, "null argument");
+        KB_REQUIRE(kr->k >= 1 && kr->n2 >= 1 && kr->m2 >= 1, "bad Kronecker sizes");
+        cudaStream_t st = as_stream(stream);
+        k_kron_band_init<<<1, 1, 0, st>>>(band);
+        KB_LAUNCH_CHECK();
+        const int64_t total = (int64_t)kr->k * kr->n2 * kr->m2;
+        k_kron_band<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(
+            kr->g, kr->k, kr->n2, kr->m2, band);
+        KB_LAUNCH_CHECK();
+        return KB_OK;
+    } catch (Fail f) {
+        return f.code;
+    }
+}
+
 extern "C" int kb_kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, void* ws,
                              size_t ws_bytes, kb_stream_t stream) {
     try {
@@ -1175,7 +1228,7 @@ static void kron_apply_b(const kb_kron* kr, int B, const double* x, double* y, i
     struct Reset {
         ~Reset() { g_dgemm_skip = GemmSkip{}; }
     } reset;
-    g_dgemm_skip = GemmSkip{flags, stride, transpose ? m1 : n1};   // stage 1: problems stacked along M
+    g_dgemm_skip = GemmSkip{flags, stride, transpose ? m1 : n1, kr->band};   // stage 1: problems stacked along M
     if (!transpose) {
         // P_i = [X_1; ...; X_B] G_i   ((B n1) x m2)
         dgemm(0, 0, B * n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,

@@ -82,6 +82,7 @@ class KroneckerSum:
         g = np.stack([b.T.reshape(-1) for b in ay])   # G_i = ay_i^T  (n2 x m2 row-major)
         self.f_dev = D.to_device(f)
         self.g_dev = D.to_device(g)
+        self._band = None
 
     @classmethod
     def from_device(cls, f_dev, g_dev, scheme: BlockScheme) -> "KroneckerSum":
@@ -89,6 +90,7 @@ class KroneckerSum:
         obj.scheme = scheme
         obj._ax = obj._ay = None
         obj.f_dev, obj.g_dev = f_dev, g_dev
+        obj._band = None
         return obj
 
     @property
@@ -117,7 +119,19 @@ class KroneckerSum:
 
     def kron_struct(self) -> _lib.KbKron:
         s = self.scheme
-        return _lib.KbKron(s.m1, s.m2, s.n1, s.n2, self.k, self.f_dev.data_ptr(), self.g_dev.data_ptr())
+        kr = _lib.KbKron(s.m1, s.m2, s.n1, s.n2, self.k, self.f_dev.data_ptr(), self.g_dev.data_ptr())
+        if self._band is None:
+            # zero band of the G factors, found once on first use (stream-ordered,
+            # no host sync): the G stage of every apply then skips all-zero tiles
+            import torch
+
+            from . import device as D
+
+            band = torch.empty(2, dtype=torch.int32, device=self.g_dev.device)
+            _lib.check(_lib.load().kb_kron_band(C.byref(kr), band.data_ptr(), D.stream_ptr()), "kron band")
+            self._band = band
+        kr.band = self._band.data_ptr()
+        return kr
 
     def forward_struct(self) -> _lib.KbForward:
         fw = _lib.KbForward()

@@ -104,6 +104,8 @@ class ShardedKroneckerSum:
         fw.m, fw.n = self.shape
         fw.a, fw.lda = None, 0
         fw.kron = _lib.KbKron(s.m1, s.m2, s.n1, s.n2, self.k, self.f_dev.data_ptr(), self.g_dev.data_ptr())
+        if hasattr(self.full, "kron_struct"):   # the full sum's G band bounds every term subset's
+            fw.kron.band = self.full.kron_struct().band
         fw.allreduce = self._hook
         fw.allreduce_ctx = None
         return fw

@@ -121,6 +121,73 @@ class TestKronecker:
         if m1 * m2 * n1 * n2 <= 2 ** 20:
             np.testing.assert_allclose(op.apply(x), ref.materialize() @ x, atol=1e-11)
 
+    @staticmethod
+    def _apply_dense(op, v, transpose):
+        """kb_kron_apply with the band cleared: every k tile of the G stage."""
+        import ctypes as C
+
+        import torch
+
+        from paper_2410_00233_b200 import _lib
+        from paper_2410_00233_b200 import device as D
+
+        lib = _lib.load()
+        kr = op.kron_struct()
+        kr.band = None
+        nb = C.c_size_t()
+        _lib.check(lib.kb_kron_workspace_bytes(C.byref(kr), C.byref(nb)))
+        ws = torch.empty(max(1, nb.value), dtype=torch.uint8, device=D.device())
+        xd = D.to_device(np.ascontiguousarray(v, dtype=np.float64))
+        m, n = op.shape
+        y = torch.empty(n if transpose else m, dtype=torch.float64, device=D.device())
+        _lib.check(lib.kb_kron_apply(C.byref(kr), xd.data_ptr(), y.data_ptr(), transpose, ws.data_ptr(),
+                                     nb.value, D.stream_ptr()))
+        return D.to_host(y)
+
+    @pytest.mark.parametrize("dims,k,lo,hi", [((96, 200, 80, 160), 3, -7, 40), ((64, 256, 64, 256), 4, -59, 59),
+                                              ((40, 130, 40, 300), 2, 100, 180), ((32, 64, 32, 64), 2, 0, 0)])
+    def test_banded_g_skips_zero_tiles_bit_identically(self, kb, dims, k, lo, hi):
+        m1, m2, n1, n2 = dims
+        rng = np.random.default_rng(m2 + n2 + k)
+        ax = [rng.standard_normal((m1, n1)) for _ in range(k)]
+        a_idx, b_idx = np.meshgrid(np.arange(m2), np.arange(n2), indexing="ij")
+        mask = ((a_idx - b_idx) >= lo) & ((a_idx - b_idx) <= hi)   # G[r][c] = ay[c][r], d = c - r
+        ay = [np.where(mask, rng.standard_normal((m2, n2)), 0.0) for _ in range(k)]
+        op = kb.KroneckerSum(ax, ay, kb.BlockScheme(*dims))
+        x = rng.standard_normal(n1 * n2)
+        y = rng.standard_normal(m1 * m2)
+        got, got_t = op.apply(x), op.apply_t(y)
+        band = op._band.cpu().numpy()
+        nz = np.nonzero(np.any(np.stack(ay) != 0, axis=0))
+        assert (band[0], band[1]) == ((nz[0] - nz[1]).min(), (nz[0] - nz[1]).max())
+        np.testing.assert_array_equal(got, self._apply_dense(op, x, 0))
+        np.testing.assert_array_equal(got_t, self._apply_dense(op, y, 1))
+
+    def test_all_zero_g_gives_zero(self, kb):
+        s = kb.BlockScheme(64, 64, 64, 64)
+        rng = np.random.default_rng(3)
+        op = kb.KroneckerSum([rng.standard_normal((64, 64))], [np.zeros((64, 64))], s)
+        out = op.apply(rng.standard_normal(64 * 64))
+        assert op._band.cpu().numpy()[0] > op._band.cpu().numpy()[1]
+        np.testing.assert_array_equal(out, np.zeros(64 * 64))
+
+    def test_egkb_factors_are_banded_and_skip_bit_identically(self, kb):
+        """Zero BC: the v-side factors are banded Toeplitz (products of R(A)^T),
+        so the apply skips most G tiles and still equals the dense apply."""
+        from paper_2410_00233_b200 import datagen
+
+        prob = datagen.make_problem("n256")
+        n = prob.n
+        svd, _ = kb.egkb(kb.RearrangedBlur(prob.psf.astype(np.float32), n), kb.EgkbConfig(k_max=20, k_min=20, p=2))
+        op = kb.assemble(svd, kb.BlockScheme.square_image(n))
+        rng = np.random.default_rng(1)
+        x = rng.standard_normal(n * n)
+        got, got_t = op.apply(x), op.apply_t(x)
+        lo, hi = op._band.cpu().numpy()
+        assert hi - lo < n // 2, (lo, hi)
+        np.testing.assert_array_equal(got, self._apply_dense(op, x, 0))
+        np.testing.assert_array_equal(got_t, self._apply_dense(op, x, 1))
+
     def test_materialize_and_factors_roundtrip(self, kb):
         rng = np.random.default_rng(0)
         s = kb.BlockScheme(3, 4, 2, 5)
