@@ -342,15 +342,23 @@ static void svd_c_upload(int dtype, const double* alphas, const double* ts, int 
     static thread_local cudaEvent_t done = nullptr;
     if (!done) KB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     KB_CUDA(cudaEventSynchronize(done));   // the previous upload out of `stage` has finished
-    const size_t need = bu + bv + bs;
+    // one copy when the device blocks share a buffer (lowrank.egkb's svdbuf):
+    // the staging then mirrors the device offsets
+    const char* du = static_cast<const char*>(st->wu_dev);
+    const char* dv = static_cast<const char*>(st->wv_dev);
+    const char* ds = reinterpret_cast<const char*>(st->sigma_dev);
+    const bool one = dv >= du + bu && ds >= dv + bv && (size_t)(ds - du) + bs <= ((size_t)1 << 20) &&
+                     ((uintptr_t)(dv - du) % 8 == 0) && ((uintptr_t)(ds - du) % 8 == 0);
+    const size_t ov = one ? (size_t)(dv - du) : bu, os = one ? (size_t)(ds - du) : bu + bv;
+    const size_t need = os + bs;
     if (stage_bytes < need) {
         if (stage) cudaFreeHost(stage);
         KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage), need));
         stage_bytes = need;
     }
     char* pu = stage;
-    char* pv = stage + bu;
-    double* ps = reinterpret_cast<double*>(stage + bu + bv);
+    char* pv = stage + ov;
+    double* ps = reinterpret_cast<double*>(stage + os);
     for (int c = 0; c < chosen; ++c) {
         const int j = perm[c];
         const double sv = sig[j];
@@ -367,9 +375,13 @@ static void svd_c_upload(int dtype, const double* alphas, const double* ts, int 
             else reinterpret_cast<double*>(pv)[(size_t)i * chosen + c] = w;
         }
     }
-    KB_CUDA(cudaMemcpyAsync(st->wu_dev, pu, bu, cudaMemcpyHostToDevice, s));
-    KB_CUDA(cudaMemcpyAsync(st->wv_dev, pv, bv, cudaMemcpyHostToDevice, s));
-    KB_CUDA(cudaMemcpyAsync(st->sigma_dev, ps, bs, cudaMemcpyHostToDevice, s));
+    if (one) {
+        KB_CUDA(cudaMemcpyAsync(st->wu_dev, pu, need, cudaMemcpyHostToDevice, s));
+    } else {
+        KB_CUDA(cudaMemcpyAsync(st->wu_dev, pu, bu, cudaMemcpyHostToDevice, s));
+        KB_CUDA(cudaMemcpyAsync(st->wv_dev, pv, bv, cudaMemcpyHostToDevice, s));
+        KB_CUDA(cudaMemcpyAsync(st->sigma_dev, ps, bs, cudaMemcpyHostToDevice, s));
+    }
     KB_CUDA(cudaEventRecord(done, s));
 }
 
@@ -583,14 +595,16 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
 
     static thread_local char* hbuf = nullptr;   // pinned trace mailbox
     static thread_local size_t hbuf_bytes = 0;
-    const size_t need = sizeof(int) * H_COUNT + sizeof(double) * 4 * (size_t)cap;
+    // header and trace are adjacent in the workspace (egkb_ws_make): one read-back
+    const size_t toff = (size_t)(reinterpret_cast<char*>(P.w.trace) - reinterpret_cast<char*>(P.w.hdr));
+    const size_t need = toff + sizeof(double) * 4 * (size_t)cap;
     if (hbuf_bytes < need) {
         if (hbuf) cudaFreeHost(hbuf);
         KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hbuf), need));
         hbuf_bytes = need;
     }
     int* hh = reinterpret_cast<int*>(hbuf);
-    double* ht = reinterpret_cast<double*>(hbuf + sizeof(int) * H_COUNT);
+    double* ht = reinterpret_cast<double*>(hbuf + toff);
 
     static const bool force_eager = std::getenv("KB_EGKB_EAGER") != nullptr;  // e.g. for ncu, which
     // cannot profile kernel nodes of graphs that contain conditional nodes
@@ -641,8 +655,7 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
             enqueue_body(P, s);
         }
     }
-    KB_CUDA(cudaMemcpyAsync(hh, P.w.hdr, sizeof(int) * H_COUNT, cudaMemcpyDeviceToHost, s));
-    KB_CUDA(cudaMemcpyAsync(ht, P.w.trace, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost, s));
+    KB_CUDA(cudaMemcpyAsync(hbuf, P.w.hdr, need, cudaMemcpyDeviceToHost, s));
     if (pk_done && pk_scales && st->s_scale_host && st->q_scale_host) {
         KB_CUDA(cudaMemcpyAsync(st->s_scale_host, pk_scales, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
         KB_CUDA(cudaMemcpyAsync(st->q_scale_host, pk_scales + cap, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));

@@ -415,6 +415,20 @@ k_lift2_asm(const float* __restrict__ S, int64_t ld, int rows, const float* __re
 #pragma unroll
         for (int c = 0; c < CB; ++c) a0[c] = a1[c] = 0.f;
         int i = 0;
+        for (; i + 8 <= rows; i += 8) {   // 8 rows of loads in flight per thread
+            float2 s8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s8[j] = __ldg(reinterpret_cast<const float2*>(S + (int64_t)(i + j) * ld) + e2);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float* wr = wsm + (i + j) * CB;
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    a0[c] = fmaf(s8[j].x, wr[c], a0[c]);
+                    a1[c] = fmaf(s8[j].y, wr[c], a1[c]);
+                }
+            }
+        }
         for (; i + 4 <= rows; i += 4) {
             float2 s4[4];
 #pragma unroll
