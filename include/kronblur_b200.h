@@ -265,7 +265,7 @@ typedef struct {
 /* band[0..1] = min/max of (c - r) over the nonzero entries G_i[r][c] of all
  * terms, stream-ordered on the device.  With it set in kb_kron, the G stage
  * of every apply skips the k tiles that only meet zeros (bit-identical
- * result; the v-side factors of a zero-BC approximation are banded Toeplitz).
+ * result for finite x; the v-side factors of a zero-BC approximation are banded Toeplitz).
  * The band must be recomputed if g changes. */
 int kb_kron_band(const kb_kron* kr, int* band, kb_stream_t stream);
 

@@ -93,7 +93,7 @@ struct Sizer {
 // untransposed B operand's row r, column c can be nonzero only when
 // lo <= c - r <= hi (kb_kron_band); k tiles outside a CTA's column band are
 // all-zero products and are skipped (adding exact zeros never changes a sum,
-// so the result is bit-identical to the dense product).
+// so for finite A the result is bit-identical to the dense product).
 struct GemmSkip {
     const int* flags = nullptr;
     int stride = 0;
