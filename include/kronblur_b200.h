@@ -213,6 +213,11 @@ int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_stream_t strea
  * bytes of the raw upload): the fp32 operator's K without a device cast. */
 int kb_stage_commit_f32(long long ticket, double total, float* dst, size_t count, int threads,
                         kb_stream_t stream);
+/* (src / total).astype(float32) of the host PSF straight into a pinned buffer
+ * and on to dst (stream-ordered): the fp32 path without a staged fp64 copy,
+ * for callers that keep src unchanged until the upload is done. */
+int kb_psf_commit_f32(const double* src, size_t count, double total, float* dst, int threads,
+                      kb_stream_t stream);
 /* bytes of host memory -> device `dst`, through a library-owned pinned
  * buffer filled by `threads` host threads, chunk-pipelined with the copies
  * (stream-ordered on `stream`; the host array may be reused on return). */

@@ -113,6 +113,7 @@ _SIGS = {
     "kb_psf_scan_stage": (C.c_int, [vp, i64, C.c_int, dp, dp, C.POINTER(C.c_longlong)]),
     "kb_stage_commit": (C.c_int, [C.c_longlong, vp, C.c_size_t, vp]),
     "kb_stage_commit_f32": (C.c_int, [C.c_longlong, C.c_double, vp, C.c_size_t, C.c_int, vp]),
+    "kb_psf_commit_f32": (C.c_int, [vp, C.c_size_t, C.c_double, vp, C.c_int, vp]),
     "kb_normal_pcg64": (C.c_int, [P(C.c_uint64), P(C.c_uint64), i64, C.c_int, i64, vp, vp, SZ, vp]),
     "kb_normal_workspace_bytes": (C.c_int, [i64, P(SZ)]),
     "kb_normal_test_entries": (None, [C.c_int]),

@@ -14,6 +14,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -201,8 +202,7 @@ extern "C" int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_str
 
 namespace kb {
 namespace {
-void commit_f32(Stage& st, double total, float* dst, int threads, cudaStream_t s) {
-    const int64_t n = (int64_t)(st.bytes / sizeof(double));
+void commit_f32(Stage& st, const double* src, int64_t n, double total, float* dst, int threads, cudaStream_t s) {
     if (st.cap32 < (size_t)n) {
         if (st.buf32) cudaFreeHost(st.buf32);
         st.buf32 = nullptr;
@@ -210,12 +210,26 @@ void commit_f32(Stage& st, double total, float* dst, int threads, cudaStream_t s
         KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.buf32), sizeof(float) * (size_t)n));
         st.cap32 = (size_t)n;
     }
-    const double* src = reinterpret_cast<const double*>(st.buf);
     float* out = st.buf32;
-    // (k / total).astype(float32): IEEE fp64 division, then round to fp32 (bitwise numpy)
-#pragma omp parallel for num_threads(std::max(1, threads)) schedule(static)
-    for (int64_t i = 0; i < n; ++i) out[i] = (float)(src[i] / total);
-    KB_CUDA(cudaMemcpyAsync(dst, out, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, s));
+    // (k / total).astype(float32): IEEE fp64 division, then round to fp32 (bitwise numpy).
+    // Chunked so the copy engine uploads chunk c while the threads normalise c + 1.
+    static const int env_ch = std::getenv("KB_STAGE_CHUNKS") ? std::atoi(std::getenv("KB_STAGE_CHUNKS")) : 0;
+    const int64_t nch = env_ch > 0 ? env_ch : (n >= (int64_t)1 << 18 ? 8 : 1);
+    const int64_t csz = ((n + nch - 1) / nch + 1023) / 1024 * 1024;
+    cudaError_t err = cudaSuccess;
+#pragma omp parallel num_threads(std::max(1, threads))
+    for (int64_t c0 = 0; c0 < n; c0 += csz) {
+        const int64_t c1 = std::min(n, c0 + csz);
+#pragma omp for schedule(static)
+        for (int64_t i = c0; i < c1; ++i) out[i] = (float)(src[i] / total);
+#pragma omp master
+        {
+            const cudaError_t e = cudaMemcpyAsync(dst + c0, out + c0, sizeof(float) * (size_t)(c1 - c0),
+                                                  cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess && err == cudaSuccess) err = e;
+        }
+    }
+    KB_CUDA(err);
     KB_CUDA(cudaEventRecord(st.done, s));
 }
 }  // namespace
@@ -227,7 +241,20 @@ extern "C" int kb_stage_commit_f32(long long ticket, double total, float* dst, s
         kb::Stage& st = kb::stage();
         KB_REQUIRE(dst && ticket == st.ticket && count * sizeof(double) == st.bytes,
                    "staged PSF is no longer available");
-        kb::commit_f32(st, total, dst, threads, kb::as_stream(stream));
+        kb::commit_f32(st, reinterpret_cast<const double*>(st.buf), (int64_t)count, total, dst, threads,
+                       kb::as_stream(stream));
+    })
+}
+
+extern "C" int kb_psf_commit_f32(const double* src, size_t count, double total, float* dst, int threads,
+                                 kb_stream_t stream) {
+    KB_GUARD({
+        KB_REQUIRE(src && dst, "bad arguments");
+        kb::Stage& st = kb::stage();
+        if (!st.done) KB_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+        KB_CUDA(cudaEventSynchronize(st.done));   // the previous upload out of buf32 has finished
+        st.ticket = 0;                            // any staged fp64 copy is superseded
+        kb::commit_f32(st, src, (int64_t)count, total, dst, threads, kb::as_stream(stream));
     })
 }
 
