@@ -269,13 +269,15 @@ class TestOrthonormalize:
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("side", [31, 513])
-def test_device_psf_is_numpys_normalisation_bitwise(kb, dtype, side):
+@pytest.mark.parametrize("order", ["C", "F"])
+def test_device_psf_is_numpys_normalisation_bitwise(kb, dtype, side, order):
     """blurmodel.py:25-65: the device K is (k / k.sum()).astype(dtype) bit for bit, whichever
-    upload path runs (scan-staged fp32 commit, staged raw fp64 + device cast, or the small-PSF path)."""
+    upload path runs (host fp32 commit, staged raw fp64 + device cast, the small-PSF path,
+    C- or Fortran-ordered input)."""
     from paper_2410_00233_b200 import device as D
 
     rng = np.random.default_rng(side)
-    k = rng.random((side, side)) ** 3
+    k = np.asarray(rng.random((side, side)) ** 3, order=order)
     blur = kb.RearrangedBlur(k, 1024 if side == 513 else 64, dtype=dtype)
     kd, kt = blur._device_kernels()
     want = (k / k.sum()).astype(dtype)
