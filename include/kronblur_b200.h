@@ -156,7 +156,19 @@ typedef struct {
     double break_tol;     /* < 0: sqrt(eps) of dtype (lowrank.py:194)          */
     int full_reorth;      /* 1: project s against S (lowrank.py:240-241)       */
     int reorth_passes;    /* 1: classical GS, 2: CGS2 (default)                */
+    /* KB_ARITH_FAST: the fused persistent engine (fp64-accumulated sums).
+     * KB_ARITH_OPENBLAS_SKX / _HSW: the reference's own fp32 operations in
+     * its order -- sequential MGS (lowrank.py:153-156), norms and coefficients
+     * as OpenBLAS's x86-64 sdot computes them (64 FMA lanes for the SkylakeX
+     * kernel, 32 for the Haswell/Zen kernel) -- so the trace, the rank
+     * decision and the bases are bit-identical to the reference run on a host
+     * whose numpy uses that kernel.  fp32 only. */
+    int arith;
 } kb_egkb_config;
+
+#define KB_ARITH_FAST 0
+#define KB_ARITH_OPENBLAS_SKX 1
+#define KB_ARITH_OPENBLAS_HSW 2
 
 typedef struct {
     /* caller-allocated device bases: `capacity` vectors each */
@@ -176,7 +188,8 @@ typedef struct {
      * wu_dev != NULL the host computes it (fp64 one-sided Jacobi) right after
      * the loop and uploads, stream-ordered, W_u = U_C[:, :chosen] (rows x
      * chosen) to wu_dev and W_v = V_C[:, :chosen] (k_p x chosen) to wv_dev
-     * (working dtype, row stride chosen; capacity^2 elements each suffice) and
+     * (working dtype, row stride chosen; each block is capacity^2 elements,
+     * all of which the library may write) and
      * sigma (fp64 of the working-precision values) to sigma_dev; sigma_host
      * (capacity doubles) gets the same values -- the caller's lift reads the
      * weights on the device without another host step. */
@@ -191,6 +204,12 @@ int kb_egkb_capacity(const kb_egkb_config* cfg);
 int kb_egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const void* y0,
                 kb_egkb_state* st, void* ws, size_t ws_bytes, kb_stream_t stream);
 int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
+/* *out_dev = sdot(x, y) as OpenBLAS's x86-64 kernel computes it (lanes = 64:
+ * SkylakeX, 32: Haswell/Zen; y == NULL: sdot(x, x)), fp32, device pointers.
+ * ws: >= 1024 bytes of device scratch.  The building block of KB_ARITH_OPENBLAS_*
+ * (numpy's x @ y and np.linalg.norm on float32 vectors, lowrank.py:153-156, 207-259). */
+int kb_sdot_openblas(int lanes, const float* x, const float* y, int64_t n, float* out_dev,
+                     void* ws, size_t ws_bytes, kb_stream_t stream);
 
 /* dst = (dtype)(src / divisor), device: the Psf normalisation k / k.sum()
  * (blurmodel.py:25-65) fused with the working-precision cast -- bitwise
@@ -199,20 +218,11 @@ int kb_div_cast(const double* src, double divisor, int dtype, void* dst, int64_t
 
 /* Psf validation scan (blurmodel.py:25-65): *sum_out = k.sum() of the
  * C-ordered float64 kernel -- numpy's pairwise summation, bit for bit --
- * and *min_out = k.min(), using `threads` host threads.  Host only. */
-int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out);
-/* kb_psf_scan that also copies k into the library's pinned PSF staging
- * buffer while it is in cache; *ticket names the staged copy.  The commit
- * is a stream-ordered copy of exactly that content to `dst` (KB_EVALIDATION
- * when a later scan has replaced it). */
-int kb_psf_scan_stage(const double* k, int64_t n, int threads, double* sum_out, double* min_out,
-                      long long* ticket);
-int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_stream_t stream);
-/* The staged kernel normalised on the host -- (k / total).astype(float32),
- * bit for bit numpy's, `threads` host threads -- and sent as fp32 (half the
- * bytes of the raw upload): the fp32 operator's K without a device cast. */
-int kb_stage_commit_f32(long long ticket, double total, float* dst, size_t count, int threads,
-                        kb_stream_t stream);
+ * and *min_out = k.min(), using `threads` host threads.  When copy_to is not
+ * NULL the n doubles are also copied there in the same pass: the private
+ * copy the reference's Psf takes (np.array(kernel), "the kernel is copied").
+ * Host only. */
+int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out, double* copy_to);
 /* (src / total).astype(float32) of the host PSF straight into a pinned buffer
  * and on to dst (stream-ordered): the fp32 path without a staged fp64 copy,
  * for callers that keep src unchanged until the upload is done. */

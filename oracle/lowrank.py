@@ -80,10 +80,11 @@ def auto_rank(nus, tau, k_min=2, k_max=None):
     return top, "hit_kmax"
 
 
-def project_out(vec, basis):
-    """Sequential one-pass MGS (lowrank.py:153-156)."""
+def project_out(vec, basis, dot=None):
+    """Sequential one-pass MGS (lowrank.py:153-156).  ``dot`` replaces numpy's
+    ``b @ vec`` (e.g. ``oracle.blas.sdot`` of another OpenBLAS kernel)."""
     for b in basis:
-        vec = vec - (b @ vec) * b
+        vec = vec - ((b @ vec) if dot is None else dot(b, vec)) * b
     return vec
 
 
@@ -93,13 +94,23 @@ def svd_small(mat):
     return u, s, vt.T
 
 
-def egkb(matvec, rmatvec, shape, dtype, cfg, y0=None):
+def egkb(matvec, rmatvec, shape, dtype, cfg, y0=None, kernel=None):
     """Enlarged Golub-Kahan bidiagonalization (lowrank.py:159-329).
 
     ``cfg`` needs k_max, p, tau, k_min, reorth, seed, break_tol, keep_basis.
-    Returns ((u, sigma, v), trace).
+    ``kernel`` (fp32 only): compute every dot product and norm as that OpenBLAS
+    kernel does (``oracle.blas``) instead of with this host's numpy -- the
+    reference run on a host with that kernel.  Returns ((u, sigma, v), trace).
     """
     dtype = np.dtype(dtype)
+    if kernel is not None:
+        from . import blas
+
+        dot = lambda a, b: blas.sdot(a, b, kernel)   # noqa: E731
+        vnorm = lambda x: blas.norm(x, kernel)       # noqa: E731
+    else:
+        dot = None
+        vnorm = lambda x: float(np.linalg.norm(x))   # noqa: E731
     one = dtype.type
     mbar, nbar = shape
     tol = cfg.break_tol if cfg.break_tol is not None else np.sqrt(float(np.finfo(dtype).eps))
@@ -111,12 +122,12 @@ def egkb(matvec, rmatvec, shape, dtype, cfg, y0=None):
         y0 = np.asarray(y0, dtype=dtype)
         if y0.shape != (mbar,):
             raise OracleValidationError("bad y0 length")
-    t_first = float(np.linalg.norm(y0))
+    t_first = vnorm(y0)
     if t_first == 0.0:
         raise OracleValidationError("zero y0")
     left = [y0 / one(t_first)]
     first_q = rmatvec(left[0])
-    a_first = float(np.linalg.norm(first_q))
+    a_first = vnorm(first_q)
     if a_first == 0.0:
         raise OracleNumericalError("operator annihilates the starting vector")
     right = [first_q / one(a_first)]
@@ -137,18 +148,18 @@ def egkb(matvec, rmatvec, shape, dtype, cfg, y0=None):
         u = matvec(right[-1])
         cand = u - one(tr.alphas[-1]) * left[-1]
         if mode == "full":
-            cand = project_out(cand, left)
-        t_val = float(np.linalg.norm(cand))
-        if t_val <= tol * float(np.linalg.norm(u)):
+            cand = project_out(cand, left, dot)
+        t_val = vnorm(cand)
+        if t_val <= tol * vnorm(u):
             broke = broke_on_t = True
             break
         s_next = cand / one(t_val)
 
         back = rmatvec(s_next)
-        back_norm = float(np.linalg.norm(back))
+        back_norm = vnorm(back)
         back = back - one(t_val) * right[-1]
-        back = project_out(back, right)
-        a_val = float(np.linalg.norm(back))
+        back = project_out(back, right, dot)
+        a_val = vnorm(back)
         if a_val <= tol * back_norm:
             broke = True
             left.append(s_next)

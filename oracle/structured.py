@@ -12,7 +12,9 @@ K[r_out - r_in + cu, c_out - c_in + cv]  (zero when the K index is out of
 range), i.e. R = W_c K^T W_r^T with 0/1 diagonal-indicator matrices W.
 
 ``ra_matvec``/``ra_rmatvec`` evaluate R q and R^T s in O(n^2 + kh*kw) work by
-diagonal sums -> small K product -> Toeplitz broadcast.  ``ra_dense`` builds the
+diagonal sums -> small K product -> Toeplitz broadcast, every sum in fp64 in a
+fixed sequential order (np.bincount's input order; kernel rows in index order),
+then one rounding to the vector dtype.  ``ra_dense`` builds the
 dense R for tiny n (used to pin the closed form against the reference).
 ``structured_tsvd`` is the exact SVD of R through D_c K^T D_r.
 
@@ -92,12 +94,28 @@ def _broadcast(z: np.ndarray, n: int, center: int, dtype, bc: str = "zero") -> n
     return np.bincount(cells, weights=np.asarray(z, dtype=np.float64)[us], minlength=n * n).astype(dtype)
 
 
+def _kernel_product(kernel: np.ndarray, w: np.ndarray, transpose: bool) -> np.ndarray:
+    """z = K^T w (z[v] = sum_u K[u,v] w[u]) or, transpose, z = K w (z[u] = sum_v K[u,v] w[v]).
+
+    Every entry is a sequential fp64 sum of rounded fp64 products in index order
+    (numpy's elementwise multiply and add, one kernel row / column at a time).  A
+    fixed evaluation order instead of a BLAS dgemv, whose summation order depends
+    on the host's OpenBLAS kernel and thread count; the device's reference-order
+    product (kb_refarith.cu) repeats it bit for bit."""
+    k64 = np.asarray(kernel, dtype=np.float64)
+    if transpose:
+        k64 = np.ascontiguousarray(k64.T)
+    # numpy reduces axis 0 of a C-ordered array row by row: z = ((p_0 + p_1) + p_2) + ...,
+    # the same bits as the explicit loop (pinned in tests/test_oracle_golden.py)
+    return (k64 * w[:, None]).sum(axis=0)
+
+
 def ra_matvec(kernel: np.ndarray, n: int, q: np.ndarray, bc: str = "zero") -> np.ndarray:
     """y = R(A) q.  q is indexed r_in*n + r_out, y is indexed c_in*n + c_out."""
     kh, kw = kernel.shape
     cu, cv = kh // 2, kw // 2
     w = _diag_sums(q, n, cu, kh, bc)                   # P_r^T q
-    z = np.asarray(kernel, dtype=np.float64).T @ w     # z[v] = sum_u K[u,v] w[u]
+    z = _kernel_product(kernel, w, False)              # z[v] = sum_u K[u,v] w[u]
     return _broadcast(z, n, cv, q.dtype, bc)
 
 
@@ -106,7 +124,7 @@ def ra_rmatvec(kernel: np.ndarray, n: int, s: np.ndarray, bc: str = "zero") -> n
     kh, kw = kernel.shape
     cu, cv = kh // 2, kw // 2
     w = _diag_sums(s, n, cv, kw, bc)                   # P_c^T s
-    z = np.asarray(kernel, dtype=np.float64) @ w       # z[u] = sum_v K[u,v] w[v]
+    z = _kernel_product(kernel, w, True)               # z[u] = sum_v K[u,v] w[v]
     return _broadcast(z, n, cu, s.dtype, bc)
 
 

@@ -21,6 +21,7 @@ KB_F32, KB_F64 = 0, 1
 KB_OP_DENSE, KB_OP_RA_ZERO, KB_OP_RA_REFLEXIVE, KB_OP_SPARSE = 0, 1, 2, 3
 KB_STOP = {1: "nu_rose", 2: "nu_below_tol", 3: "hit_kmax", 4: "breakdown"}
 KB_FWD_DENSE, KB_FWD_KRON = 0, 1
+KB_ARITH_FAST, KB_ARITH_OPENBLAS_SKX, KB_ARITH_OPENBLAS_HSW = 0, 1, 2
 KB_SB_ANISOTROPIC, KB_SB_ISOTROPIC = 0, 1
 CGLS_STOPS = {0: "max_iter", 1: "converged", 2: "stalled"}
 SB_STOPS = {0: "max_iter", 1: "converged"}
@@ -41,7 +42,8 @@ class KbOperator(C.Structure):
 
 class KbEgkbConfig(C.Structure):
     _fields_ = [("k_max", C.c_int), ("p", C.c_int), ("k_min", C.c_int), ("tau", C.c_double),
-                ("break_tol", C.c_double), ("full_reorth", C.c_int), ("reorth_passes", C.c_int)]
+                ("break_tol", C.c_double), ("full_reorth", C.c_int), ("reorth_passes", C.c_int),
+                ("arith", C.c_int)]
 
 
 class KbEgkbState(C.Structure):
@@ -105,14 +107,12 @@ _SIGS = {
     "kb_orth_workspace_bytes": (C.c_int, [i64, C.c_int, P(SZ)]),
     "kb_egkb_capacity": (C.c_int, [P(KbEgkbConfig)]),
     "kb_egkb_run": (C.c_int, [P(KbOperator), P(KbEgkbConfig), vp, P(KbEgkbState), vp, SZ, vp]),
+    "kb_sdot_openblas": (C.c_int, [C.c_int, vp, vp, i64, vp, vp, SZ, vp]),
     "kb_egkb_workspace_bytes": (C.c_int, [P(KbOperator), C.c_int, P(SZ)]),
     "kb_transpose": (C.c_int, [C.c_int, vp, i64, i64, vp, vp]),
     "kb_div_cast": (C.c_int, [vp, C.c_double, C.c_int, vp, i64, vp]),
-    "kb_psf_scan": (C.c_int, [vp, i64, C.c_int, dp, dp]),
+    "kb_psf_scan": (C.c_int, [vp, i64, C.c_int, dp, dp, vp]),
     "kb_stage_upload": (C.c_int, [vp, C.c_size_t, vp, C.c_int, vp]),
-    "kb_psf_scan_stage": (C.c_int, [vp, i64, C.c_int, dp, dp, C.POINTER(C.c_longlong)]),
-    "kb_stage_commit": (C.c_int, [C.c_longlong, vp, C.c_size_t, vp]),
-    "kb_stage_commit_f32": (C.c_int, [C.c_longlong, C.c_double, vp, C.c_size_t, C.c_int, vp]),
     "kb_psf_commit_f32": (C.c_int, [vp, C.c_size_t, C.c_double, vp, C.c_int, vp]),
     "kb_normal_pcg64": (C.c_int, [P(C.c_uint64), P(C.c_uint64), i64, C.c_int, i64, vp, vp, SZ, vp]),
     "kb_normal_workspace_bytes": (C.c_int, [i64, P(SZ)]),

@@ -45,30 +45,27 @@ _SCAN_MIN = 1 << 16
 _HOST_THREADS = max(1, min(16, os.cpu_count() or 1))
 
 
-def _scan(k: np.ndarray) -> tuple[float, np.float64, int]:
-    """min, numpy-exact sum (and a staging ticket: 0, nothing staged)."""
+def _scan(k: np.ndarray) -> tuple[float, np.float64, np.ndarray]:
+    """min, numpy-exact sum and a private copy of ``k`` in one multithreaded pass."""
     lib = _lib.load()
     total, kmin = C.c_double(), C.c_double()
-    # the scan alone: the fp32 upload normalises straight from k (kb_psf_commit_f32), which
-    # measured 0.23 ms against 0.35 ms for staging a pinned fp64 copy during the scan
-    _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin)),
-               "kb_psf_scan")
-    return kmin.value, np.float64(total.value), 0
+    own = np.empty_like(k, order="C")
+    _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin),
+                               own.ctypes.data), "kb_psf_scan")
+    return kmin.value, np.float64(total.value), own
 
 
 class Psf:
     """Unit-sum, non-negative PSF with odd support (blurmodel.py:25-65).
 
-    Validation and the mass are computed eagerly, exactly as the reference
-    (same checks, same pairwise sum over the C-ordered float64 array); the
-    normalised float64 ``kernel`` is materialised on first access.  The fp32
-    device operator normalises + casts on the host straight into pinned memory
-    at first device use (``kb_psf_commit_f32``, bitwise numpy) and uploads 4
-    bytes per entry; fp64 uploads the raw kernel and divides on the device
-    (``kb_div_cast``).  Like ``kernel``, both read the array at first use.
+    Like the reference, the kernel is copied at construction (later changes to
+    the caller's array do not reach the operator); validation and the mass are
+    computed eagerly, exactly as the reference (same checks, same pairwise sum
+    over the C-ordered float64 array), in the same multithreaded pass as the
+    copy.  The normalised float64 ``kernel`` is materialised on first access.
     """
 
-    __slots__ = ("_raw", "_total", "_kernel", "_ticket")
+    __slots__ = ("_raw", "_total", "_kernel")
 
     def __init__(self, kernel):
         k = np.asarray(kernel, dtype=np.float64)
@@ -76,15 +73,14 @@ class Psf:
             raise ValidationError("PSF kernel must be 2-D")
         if k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
             raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
-        if not (k.flags.c_contiguous or k.flags.f_contiguous):
-            k = np.array(k)                           # the reference's order-'K' copy: same reduction order
         if k.size >= _SCAN_MIN and k.flags.c_contiguous:
-            # min and numpy's pairwise sum in one multithreaded host pass (kb_psf_scan:
-            # bit-identical to k.sum(), which is single-threaded)
-            kmin, total, ticket = _scan(k)
+            # min, numpy's pairwise sum and the private copy in one multithreaded host pass
+            # (kb_psf_scan: bit-identical to k.sum(), which is single-threaded)
+            kmin, total, k = _scan(k)
             if not kmin >= 0 and np.any(k < 0):
                 raise ValidationError("PSF kernel must be non-negative")
         else:
+            k = np.array(k)                           # the reference's private order-'K' copy
             if k.size == 0 or not _min(k) >= 0:      # one reduction; the exact test only when it fails
                 if np.any(k < 0):
                     raise ValidationError("PSF kernel must be non-negative")
@@ -92,7 +88,6 @@ class Psf:
         if total <= 0:
             raise ValidationError("PSF kernel must have positive mass")
         self._raw, self._total, self._kernel = k, total, None
-        self._ticket = ticket if k.size >= _SCAN_MIN and k.flags.c_contiguous else 0
 
     @property
     def kernel(self) -> np.ndarray:
@@ -102,43 +97,27 @@ class Psf:
         return self._kernel
 
     def device_normalised(self, dtype):
-        """The normalised kernel on the device in ``dtype``: the raw float64 kernel is
-        uploaded as is and divided + cast there (kb_div_cast), so the host never
-        makes a normalised or down-cast copy."""
+        """The normalised kernel on the device in ``dtype``.  fp32: (k / total).astype(float32)
+        on the host straight into pinned memory, 4 bytes per entry on the wire (bitwise
+        numpy); fp64: the raw kernel uploaded and divided on the device (kb_div_cast)."""
         from . import device as D
 
         if self._kernel is not None:
             return D.upload(self._kernel, dtype)
         lib = _lib.load()
+        src = self._raw if self._raw.flags.c_contiguous else np.ascontiguousarray(self._raw)
         if np.dtype(dtype) == np.float32:
-            # (k / total).astype(float32) on the host, straight from k into pinned memory,
-            # then 4 bytes per entry on the wire (bitwise numpy)
-            src = self._raw if self._raw.flags.c_contiguous else np.ascontiguousarray(self._raw)
             out = D.empty(self.shape, np.float32)
             _lib.check(lib.kb_psf_commit_f32(src.ctypes.data, src.size, float(self._total), out.data_ptr(),
                                              _HOST_THREADS, D.stream_ptr()), "PSF upload")
-            self._ticket = 0
             return out
-        if self._ticket and np.dtype(dtype) == np.float32:
-            # normalised + cast on the host from the copy staged by the scan: 4 bytes per entry on the wire
-            out = D.empty(self.shape, np.float32)
-            ok = lib.kb_stage_commit_f32(self._ticket, float(self._total), out.data_ptr(), self._raw.size,
-                                         _HOST_THREADS, D.stream_ptr()) == _lib.KB_OK
-            self._ticket = 0
-            if ok:
-                return out
         raw = D.empty(self._raw.shape, np.float64)
-        # the copy staged by the validation scan, if still current; else a staged upload
-        if not (self._ticket and lib.kb_stage_commit(self._ticket, raw.data_ptr(), self._raw.nbytes,
-                                                     D.stream_ptr()) == _lib.KB_OK):
-            src = np.ascontiguousarray(self._raw)
-            _lib.check(lib.kb_stage_upload(src.ctypes.data, src.nbytes, raw.data_ptr(), _HOST_THREADS,
-                                           D.stream_ptr()), "kb_stage_upload")
-        self._ticket = 0
+        _lib.check(lib.kb_stage_upload(src.ctypes.data, src.nbytes, raw.data_ptr(), _HOST_THREADS,
+                                       D.stream_ptr()), "kb_stage_upload")
         out = D.empty(self.shape, dtype)
         code = _lib.KB_F32 if np.dtype(dtype) == np.float32 else _lib.KB_F64
-        _lib.check(_lib.load().kb_div_cast(raw.data_ptr(), float(self._total), code, out.data_ptr(), raw.numel(),
-                                           D.stream_ptr()), "kb_div_cast")
+        _lib.check(lib.kb_div_cast(raw.data_ptr(), float(self._total), code, out.data_ptr(), raw.numel(),
+                                   D.stream_ptr()), "kb_div_cast")
         return out
 
     def __repr__(self) -> str:

@@ -143,6 +143,15 @@ static void validate_op(const kb_operator* op) {
 
 static int64_t op_len(const kb_operator* op) { return std::max(op->rows, op->cols); }
 
+// kb_refarith.cu: the reference-arithmetic engine (KB_ARITH_OPENBLAS_*)
+struct RefOut {
+    std::vector<double> alphas, ts, zetas, nus;
+    int done = 1, fired = -1, reason = 0, breakdown = 0, tbreak = 0, err = 0;
+};
+size_t egkb_openblas_ws_bytes(const kb_operator* op, int capacity);
+void egkb_openblas(const kb_operator* op, const kb_egkb_config* cfg, const void* y0, kb_egkb_state* st,
+                   int lanes, double tol, void* wsp, size_t ws_bytes, RefOut& o, cudaStream_t s);
+
 // ------------------------------------------------------------------ eGKB
 // The whole bidiagonalisation (lowrank.py:207-303) is ONE CUDA graph: an
 // init stage (s1 = y0/|y0|, q1 = B^T s1/alpha1) followed by a conditional
@@ -342,12 +351,15 @@ static void svd_c_upload(int dtype, const double* alphas, const double* ts, int 
     static thread_local cudaEvent_t done = nullptr;
     if (!done) KB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     KB_CUDA(cudaEventSynchronize(done));   // the previous upload out of `stage` has finished
-    // one copy when the device blocks share a buffer (lowrank.egkb's svdbuf):
-    // the staging then mirrors the device offsets
+    // one copy when the device blocks follow each other inside their declared
+    // capacity^2-element extents (lowrank.egkb's svdbuf): the staging then mirrors
+    // the device offsets, and the gap bytes it also writes lie inside the W_u / W_v
+    // blocks the header gives to the library -- never in a neighbouring allocation
     const char* du = static_cast<const char*>(st->wu_dev);
     const char* dv = static_cast<const char*>(st->wv_dev);
     const char* ds = reinterpret_cast<const char*>(st->sigma_dev);
-    const bool one = dv >= du + bu && ds >= dv + bv && (size_t)(ds - du) + bs <= ((size_t)1 << 20) &&
+    const size_t ext = (size_t)st->capacity * (size_t)st->capacity * esz;
+    const bool one = dv >= du + bu && ds >= dv + bv && (size_t)(dv - du) <= ext && (size_t)(ds - dv) <= ext &&
                      ((uintptr_t)(dv - du) % 8 == 0) && ((uintptr_t)(ds - du) % 8 == 0);
     const size_t ov = one ? (size_t)(dv - du) : bu, os = one ? (size_t)(ds - du) : bu + bv;
     const size_t need = os + bs;
@@ -572,6 +584,56 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     KB_REQUIRE(st->s_basis && st->q_basis && st->alphas_host && st->ts_host && st->zetas_host &&
                    st->nus_host, "missing basis / trace buffers");
     const size_t esz = op->dtype == KB_F32 ? 4 : 8;
+    if (cfg->arith != KB_ARITH_FAST) {
+        KB_REQUIRE(cfg->arith == KB_ARITH_OPENBLAS_SKX || cfg->arith == KB_ARITH_OPENBLAS_HSW,
+                   "unknown arithmetic %d", cfg->arith);
+        const double tol = cfg->break_tol >= 0 ? cfg->break_tol : std::sqrt(eps_of(op->dtype));
+        RefOut o;
+        egkb_openblas(op, cfg, y0, st, cfg->arith == KB_ARITH_OPENBLAS_SKX ? 64 : 32, tol, wsp, ws_bytes, o, s);
+        if (o.err == 1) {
+            set_error("starting vector must be nonzero");
+            throw Fail{KB_EVALIDATION};
+        }
+        if (o.err == 2) {
+            set_error("operator annihilates the starting vector");
+            throw Fail{KB_ENUMERICAL};
+        }
+        int k_p, rows;
+        if (o.breakdown && o.tbreak) { k_p = o.done; rows = o.done; }
+        else if (o.breakdown) { k_p = o.done; rows = o.done + 1; }
+        else { k_p = o.done - 1; rows = o.done; }
+        int chosen, reason;
+        if (o.fired >= 0) { chosen = std::min(o.fired, k_p); reason = o.reason; }
+        else if (o.breakdown) { chosen = k_p; reason = KB_STOP_BREAKDOWN; }
+        else { chosen = std::min(cfg->k_max, k_p); reason = KB_STOP_HIT_KMAX; }
+        if (chosen < 1 || k_p < 1) {
+            set_error("bidiagonalization broke down before producing any factors");
+            throw Fail{KB_ENUMERICAL};
+        }
+        const int na = (int)o.alphas.size(), nt = (int)o.ts.size(), nn = (int)o.nus.size();
+        o.alphas.resize(std::max<size_t>(o.alphas.size(), (size_t)rows + 1), 0.0);
+        o.ts.resize(std::max<size_t>(o.ts.size(), (size_t)rows + 1), 0.0);
+        if (st->wu_dev) {
+            KB_REQUIRE(st->wv_dev && st->sigma_dev && st->sigma_host, "SVD outputs incomplete");
+            svd_c_upload(op->dtype, o.alphas.data(), o.ts.data(), rows, k_p, chosen, st, s);
+        }
+        st->n_alphas = na;
+        st->n_ts = nt;
+        st->n_nus = nn;
+        std::copy(o.alphas.begin(), o.alphas.begin() + st->n_alphas, st->alphas_host);
+        std::copy(o.ts.begin(), o.ts.begin() + st->n_ts, st->ts_host);
+        std::copy(o.zetas.begin(), o.zetas.end(), st->zetas_host);
+        std::copy(o.nus.begin(), o.nus.end(), st->nus_host);
+        if (st->s_scale_host && st->q_scale_host)
+            for (int i = 0; i < cap; ++i) st->s_scale_host[i] = st->q_scale_host[i] = 1.0;
+        st->chosen_k = chosen;
+        st->k_p = k_p;
+        st->rows = rows;
+        st->stop_reason = reason;
+        st->breakdown = o.breakdown;
+        KB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     Arena a(wsp, ws_bytes);
     EgkbPlan P;
     P.op = op;
@@ -959,7 +1021,7 @@ extern "C" int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size
         validate_op(op);
         Sizer s;
         egkb_ws_size(op, capacity, s);
-        *bytes = s.off;
+        *bytes = std::max(s.off, egkb_openblas_ws_bytes(op, capacity));
     })
 }
 

@@ -101,11 +101,18 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
 
     int kt_first = 0, ktiles = (K + BK - 1) / BK;
     if (skip.band) {   // banded B: only the k tiles that meet this CTA's columns
-        int lo = __ldg(skip.band), hi = __ldg(skip.band + 1);
-        if (TB) { const int t = lo; lo = -hi; hi = -t; }   // logical B[k][c] = G[c][k]
-        const int klo = max(0, n0 - hi), khi = min(K - 1, n0 + BN - 1 - lo);
-        kt_first = klo / BK;
-        ktiles = khi >= klo ? khi / BK + 1 - kt_first : 0;
+        const int lo0 = __ldg(skip.band), hi0 = __ldg(skip.band + 1);
+        if (lo0 > hi0) {   // all-zero G (band left at {INT_MAX, INT_MIN}): nothing to multiply
+            kt_first = 0;
+            ktiles = 0;
+        } else {
+            // offsets are within (-K, K): 64-bit bounds keep the arithmetic defined anyway
+            int64_t lo = lo0, hi = hi0;
+            if (TB) { const int64_t t = lo; lo = -hi; hi = -t; }   // logical B[k][c] = G[c][k]
+            const int64_t klo = max((int64_t)0, (int64_t)n0 - hi), khi = min((int64_t)K - 1, (int64_t)n0 + BN - 1 - lo);
+            kt_first = khi >= klo ? (int)(klo / BK) : 0;
+            ktiles = khi >= klo ? (int)(khi / BK) + 1 - kt_first : 0;
+        }
     }
     const int Ttot = ktiles * nseg;
     const int t_begin = (int)((int64_t)Ttot * split / splits);

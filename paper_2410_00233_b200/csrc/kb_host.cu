@@ -2,7 +2,8 @@
 // scan and the staged upload of the raw PSF.
 //
 //   kb_psf_scan   -- blurmodel.py:25-65 (Psf.__init__): k.min() and k.sum()
-//                    of the C-ordered float64 kernel.  The sum is numpy's
+//                    of the C-ordered float64 kernel, and the private copy the
+//                    reference's np.array(kernel) takes, in the same pass.  The sum is numpy's
 //                    pairwise summation (8 accumulators over blocks of <= 128,
 //                    halving splits rounded to multiples of 8), evaluated on
 //                    the top subtrees in parallel and combined in the same
@@ -16,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "kb_common.cuh"
@@ -77,20 +79,22 @@ double combine(int64_t n, int depth, const double* leaf_sum, int& idx) {
 namespace kb {
 namespace {
 
-// Library-owned pinned staging for the PSF: filled during the scan (the data is
-// in cache there), committed to the device later by ticket.
+// Library-owned pinned staging for the fp32 PSF upload.  One lock serialises
+// every user of the buffers (ctypes releases the GIL, so two Python threads
+// can upload at once); `done` is the last copy out of buf32.
 struct Stage {
-    char* buf = nullptr;
-    size_t cap = 0;
-    size_t bytes = 0;
-    long long ticket = 0;
-    cudaEvent_t done = nullptr;   // last copy out of buf / buf32
-    float* buf32 = nullptr;       // fp32 normalised copy (kb_stage_commit_f32)
+    std::mutex mu;
+    cudaEvent_t done = nullptr;
+    float* buf32 = nullptr;
     size_t cap32 = 0;
 };
 Stage& stage() {
     static Stage s;
     return s;
+}
+std::mutex& upload_mutex() {
+    static std::mutex m;
+    return m;
 }
 
 void psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out, char* copy_to = nullptr) {
@@ -162,41 +166,11 @@ void stage_upload(const void* src, size_t bytes, void* dst, int threads, cudaStr
 }  // namespace
 }  // namespace kb
 
-extern "C" int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out) {
+extern "C" int kb_psf_scan(const double* k, int64_t n, int threads, double* sum_out, double* min_out,
+                           double* copy_to) {
     KB_GUARD({
         KB_REQUIRE(k && n >= 0 && sum_out && min_out, "bad arguments");
-        kb::psf_scan(k, n, threads, sum_out, min_out);
-    })
-}
-
-extern "C" int kb_psf_scan_stage(const double* k, int64_t n, int threads, double* sum_out, double* min_out,
-                                 long long* ticket) {
-    KB_GUARD({
-        KB_REQUIRE(k && n >= 0 && sum_out && min_out && ticket, "bad arguments");
-        kb::Stage& st = kb::stage();
-        if (!st.done) KB_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
-        KB_CUDA(cudaEventSynchronize(st.done));   // the previous commit has left the buffer
-        const size_t bytes = sizeof(double) * (size_t)n;
-        if (st.cap < bytes) {
-            if (st.buf) cudaFreeHost(st.buf);
-            st.buf = nullptr;
-            st.cap = 0;
-            KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.buf), bytes));
-            st.cap = bytes;
-        }
-        kb::psf_scan(k, n, threads, sum_out, min_out, st.buf);
-        st.bytes = bytes;
-        *ticket = ++st.ticket;
-    })
-}
-
-extern "C" int kb_stage_commit(long long ticket, void* dst, size_t bytes, kb_stream_t stream) {
-    KB_GUARD({
-        kb::Stage& st = kb::stage();
-        KB_REQUIRE(dst && ticket == st.ticket && bytes == st.bytes, "staged PSF is no longer available");
-        cudaStream_t s = kb::as_stream(stream);
-        KB_CUDA(cudaMemcpyAsync(dst, st.buf, bytes, cudaMemcpyHostToDevice, s));
-        KB_CUDA(cudaEventRecord(st.done, s));
+        kb::psf_scan(k, n, threads, sum_out, min_out, reinterpret_cast<char*>(copy_to));
     })
 }
 
@@ -235,25 +209,14 @@ void commit_f32(Stage& st, const double* src, int64_t n, double total, float* ds
 }  // namespace
 }  // namespace kb
 
-extern "C" int kb_stage_commit_f32(long long ticket, double total, float* dst, size_t count, int threads,
-                                   kb_stream_t stream) {
-    KB_GUARD({
-        kb::Stage& st = kb::stage();
-        KB_REQUIRE(dst && ticket == st.ticket && count * sizeof(double) == st.bytes,
-                   "staged PSF is no longer available");
-        kb::commit_f32(st, reinterpret_cast<const double*>(st.buf), (int64_t)count, total, dst, threads,
-                       kb::as_stream(stream));
-    })
-}
-
 extern "C" int kb_psf_commit_f32(const double* src, size_t count, double total, float* dst, int threads,
                                  kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(src && dst, "bad arguments");
         kb::Stage& st = kb::stage();
+        std::lock_guard<std::mutex> lock(st.mu);
         if (!st.done) KB_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
         KB_CUDA(cudaEventSynchronize(st.done));   // the previous upload out of buf32 has finished
-        st.ticket = 0;                            // any staged fp64 copy is superseded
         kb::commit_f32(st, src, (int64_t)count, total, dst, threads, kb::as_stream(stream));
     })
 }
@@ -261,6 +224,7 @@ extern "C" int kb_psf_commit_f32(const double* src, size_t count, double total, 
 extern "C" int kb_stage_upload(const void* src, size_t bytes, void* dst, int threads, kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(src && dst, "bad arguments");
+        std::lock_guard<std::mutex> lock(kb::upload_mutex());
         kb::stage_upload(src, bytes, dst, threads, kb::as_stream(stream));
     })
 }

@@ -1,0 +1,501 @@
+// eGKB in the reference's own fp32 arithmetic, bit for bit (KB_ARITH_OPENBLAS_*).
+//
+// The reference (lowrank.py:199-277) runs its fp32 recurrence through numpy:
+// every norm (np.linalg.norm -> x.dot(x)) and every modified Gram-Schmidt
+// coefficient (`b @ v`, lowrank.py:153-156) is one call of OpenBLAS's sdot,
+// whose x86-64 kernels accumulate in fp32 FMA lanes -- 64 lanes for the
+// SkylakeX/Cooperlake/SapphireRapids kernel (4 x 512-bit accumulators), 32
+// for the Haswell/Zen kernel (4 x 256-bit) -- and fold the lanes in a fixed
+// tree; the elementwise steps are separately rounded fp32 multiplies,
+// subtractions and divisions.  Past the numerical rank the recurrence runs
+// on rounding noise, so where it breaks down (k_p) depends on exactly these
+// roundings: a more accurate implementation (the fused engine's fp64 sums)
+// keeps the noise alive for one or two more steps.  This engine repeats the
+// reference's operations in the reference's order:
+//
+//   * k_chain: one fused MGS step.  The vector of the step is formed on the
+//     fly (v = u - fl(beta*prev), or v = v - fl(c*b) with the coefficient of
+//     the previous MGS step), stored, and fed to the sdot lanes of the next
+//     coefficient (or of the norm).  Lane l of the kernel accumulates the
+//     elements 64k+l (32k+l) in order with IEEE fp32 FMAs, exactly as the
+//     SIMD accumulators do; 8 lanes per CTA (one 32-byte sector per row),
+//     the rows streamed through a shared-memory ring with cp.async.  The last
+//     CTA folds the lanes in the kernel's order, runs the 32-element block
+//     and the scalar tail (fp32 products summed in fp64), and takes sqrtf for
+//     norms.  A second, independent lane set yields |u| (the breakdown
+//     threshold) in the same pass.
+//   * k_normalize: s = fl(v / t) (lowrank.py:247, 260).
+//   * ref_product: the R(A) products in the port's fixed fp64 order
+//     (oracle/structured.py: np.bincount's sequential diagonal sums, the kernel
+//     rows summed in index order, one rounding to fp32).
+//
+// Each coefficient is a dependent chain of N/64 FMAs (4-cycle latency):
+// this engine is latency-bound by construction; it exists to reproduce the
+// reference's decisions and traces exactly, not to be fast.
+#include <cuda_pipeline.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kb_common.cuh"
+
+namespace kb {
+namespace refa {
+
+constexpr int LPC = 8;      // lanes (chains) per CTA
+constexpr int ROWS = 64;    // rows per ring stage
+constexpr int NS = 8;       // ring stages
+constexpr int NARR = 3;     // streamed arrays: vin, pb, x0
+
+struct ChainArgs {
+    const float* vin;    // source of the step's vector
+    const float* pb;     // mode 1: previous basis vector; mode 2: basis vector of the update
+    const float* pscal;  // device fp32 scalar: beta (mode 1) or the MGS coefficient (mode 2)
+    float* vout;         // the step's vector (mode 1/2; may alias vin)
+    const float* x0;     // chain 0 = sdot(x0, v); nullptr: sdot(v, v)
+    float* out0;         // chain 0 result (sqrtf'ed when sqrt0)
+    float* out1;         // chain 1 = sqrtf(sdot(vin, vin)) when not nullptr
+    int mode, sqrt0;
+    int64_t n;
+    int lanes;           // 64 (SkylakeX kernel) or 32 (Haswell kernel)
+    float* lane_acc;     // [2][64]
+    unsigned* ticket;
+};
+
+__device__ __forceinline__ float step_value(int mode, float vin, float pb, float sc) {
+    // numpy: u - f32(beta) * s  /  v - c * b : a rounded product, then a rounded difference
+    return mode ? __fsub_rn(vin, __fmul_rn(sc, pb)) : vin;
+}
+
+// Lane fold + 32-element block + scalar tail of OpenBLAS's x86-64 sdot
+// (kernel/x86_64/sdot.c with the skylakex / haswell micro-kernels).
+__device__ float sdot_fold(const float* acc, int lanes, const ChainArgs& a, int which, float sc) {
+    const int64_t n = a.n, n1 = n & ~(int64_t)31, nmain = lanes == 64 ? (n1 & ~(int64_t)63) : n1;
+    auto xy = [&](int64_t e, float& x, float& y) {
+        const float vi = a.vin[e];
+        if (which == 1) {
+            x = y = vi;
+            return;
+        }
+        const float v = step_value(a.mode, vi, a.mode ? a.pb[e] : 0.f, sc);
+        y = v;
+        x = a.x0 ? a.x0[e] : v;
+    };
+    float r;
+    if (lanes == 64) {
+        float q[4][8];
+        for (int k = 0; k < 4; ++k)
+            for (int j = 0; j < 8; ++j) q[k][j] = __fadd_rn(acc[16 * k + j], acc[16 * k + j + 8]);
+        for (int64_t e = nmain; e < n1; ++e) {   // the 256-bit loop after the 512-bit one
+            const int k = (int)((e - nmain) >> 3), j = (int)((e - nmain) & 7);
+            float x, y;
+            xy(e, x, y);
+            q[k][j] = fmaf(x, y, q[k][j]);
+        }
+        float s8[8];
+        for (int j = 0; j < 8; ++j) s8[j] = __fadd_rn(__fadd_rn(__fadd_rn(q[0][j], q[1][j]), q[2][j]), q[3][j]);
+        float h[4];
+        for (int j = 0; j < 4; ++j) h[j] = __fadd_rn(s8[j], s8[j + 4]);
+        r = __fadd_rn(__fadd_rn(h[0], h[1]), __fadd_rn(h[2], h[3]));
+    } else {
+        float f[4][4];
+        for (int k = 0; k < 4; ++k)
+            for (int j = 0; j < 4; ++j) f[k][j] = __fadd_rn(acc[8 * k + j], acc[8 * k + j + 4]);
+        float t[4];
+        for (int j = 0; j < 4; ++j) t[j] = __fadd_rn(__fadd_rn(f[0][j], f[1][j]), __fadd_rn(f[2][j], f[3][j]));
+        r = __fadd_rn(__fadd_rn(t[0], t[1]), __fadd_rn(t[2], t[3]));
+    }
+    double d = (double)r;   // the scalar tail: fp32 products summed in fp64
+    for (int64_t e = n1; e < n; ++e) {
+        float x, y;
+        xy(e, x, y);
+        d += (double)__fmul_rn(x, y);
+    }
+    return (float)d;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(32) k_chain(ChainArgs a) {
+    extern __shared__ float4 smv[];
+    float* sm = reinterpret_cast<float*>(smv);
+    const int c = blockIdx.x, t = threadIdx.x;
+    const int L = a.lanes;
+    const int64_t n1 = a.n & ~(int64_t)31;
+    const int64_t nmain = L == 64 ? (n1 & ~(int64_t)63) : n1;
+    const int64_t K = nmain / L;
+    const float* __restrict__ src0 = a.vin;
+    const float* __restrict__ src1 = a.mode ? a.pb : nullptr;
+    const float* __restrict__ src2 = a.x0;
+    const float sc = a.mode ? *a.pscal : 0.f;
+    constexpr int SLOT = NARR * ROWS * LPC;   // floats per stage
+    const int64_t nst = (K + ROWS - 1) / ROWS;
+    constexpr int PER = LPC * 4 / VEC;        // copies per row per array
+
+    auto issue = [&](int64_t st) {
+        if (st < nst) {
+            float* dst = sm + (int)(st % NS) * SLOT;
+            const int64_t r0 = st * ROWS;
+            const int rows = (int)min((int64_t)ROWS, K - r0);
+            auto one = [&](const float* __restrict__ g0, int arr) {
+#pragma unroll
+                for (int i = t; i < ROWS * PER; i += 32) {
+                    const int r = i / PER, part = i - r * PER;
+                    if (r < rows)
+                        __pipeline_memcpy_async(dst + (arr * ROWS + r) * LPC + part * (VEC / 4),
+                                                g0 + (r0 + r) * L + c * LPC + part * (VEC / 4), VEC);
+                }
+            };
+            one(src0, 0);
+            if (src1) one(src1, 1);
+            if (src2) one(src2, 2);
+        }
+        __pipeline_commit();
+    };
+
+    for (int st = 0; st < NS - 1; ++st) issue(st);
+    float acc0 = 0.f, acc1 = 0.f;
+    const int lane = c * LPC + t;
+    for (int64_t st = 0; st < nst; ++st) {
+        __pipeline_wait_prior(NS - 2);
+        __syncwarp();
+        issue(st + NS - 1);
+        if (t < LPC) {
+            // register batches of RB rows, the next batch's shared-memory loads issued before
+            // this batch's global stores, so the FMA chain (4 cycles per row) is the only wait
+            const float* __restrict__ base = sm + (int)(st % NS) * SLOT;
+            const int64_t r0 = st * ROWS;
+            const int rows = (int)min((int64_t)ROWS, K - r0);
+            float* __restrict__ vo = a.vout ? a.vout + r0 * L + lane : nullptr;
+            constexpr int RB = 16;
+            float vi[RB], pb[RB], xx[RB], vi2[RB], pb2[RB], xx2[RB];
+            auto load = [&](int rb, float* v_, float* p_, float* x_) {
+#pragma unroll
+                for (int j = 0; j < RB; ++j) {
+                    const int r = min(rb + j, ROWS - 1);
+                    v_[j] = base[(0 * ROWS + r) * LPC + t];
+                    p_[j] = a.mode ? base[(1 * ROWS + r) * LPC + t] : 0.f;
+                    x_[j] = a.x0 ? base[(2 * ROWS + r) * LPC + t] : 0.f;
+                }
+            };
+            load(0, vi, pb, xx);
+            for (int rb = 0; rb < rows; rb += RB) {
+                if (rb + RB < rows) load(rb + RB, vi2, pb2, xx2);
+                float vv[RB];
+#pragma unroll
+                for (int j = 0; j < RB; ++j) vv[j] = step_value(a.mode, vi[j], pb[j], sc);
+                if (rb + RB <= rows) {
+#pragma unroll
+                    for (int j = 0; j < RB; ++j) {
+                        acc0 = fmaf(a.x0 ? xx[j] : vv[j], vv[j], acc0);
+                        acc1 = fmaf(vi[j], vi[j], acc1);
+                    }
+                    if (vo)
+#pragma unroll
+                        for (int j = 0; j < RB; ++j) vo[(int64_t)(rb + j) * L] = vv[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RB; ++j)
+                        if (rb + j < rows) {
+                            acc0 = fmaf(a.x0 ? xx[j] : vv[j], vv[j], acc0);
+                            acc1 = fmaf(vi[j], vi[j], acc1);
+                            if (vo) vo[(int64_t)(rb + j) * L] = vv[j];
+                        }
+                }
+#pragma unroll
+                for (int j = 0; j < RB; ++j) {
+                    vi[j] = vi2[j];
+                    pb[j] = pb2[j];
+                    xx[j] = xx2[j];
+                }
+            }
+        }
+        __syncwarp();
+    }
+    __pipeline_wait_prior(0);
+    if (t < LPC) {
+        a.lane_acc[lane] = acc0;
+        a.lane_acc[64 + lane] = acc1;
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (t == 0) prev = atomicAdd(a.ticket, 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != gridDim.x - 1) return;
+    __threadfence();
+    // last CTA: the folds (reading the remainder elements), the results, then the
+    // remainder of the step's vector (vout may alias vin)
+    if (t == 0) {
+        float acc[64];
+        for (int i = 0; i < L; ++i) acc[i] = __ldcg(a.lane_acc + i);
+        float r0 = sdot_fold(acc, L, a, 0, sc);
+        *a.out0 = a.sqrt0 ? sqrtf(r0) : r0;
+        if (a.out1) {
+            for (int i = 0; i < L; ++i) acc[i] = __ldcg(a.lane_acc + 64 + i);
+            *a.out1 = sqrtf(sdot_fold(acc, L, a, 1, sc));
+        }
+        *a.ticket = 0u;
+    }
+    __syncwarp();
+    if (a.vout)
+        for (int64_t e = nmain + t; e < a.n; e += 32)
+            a.vout[e] = step_value(a.mode, a.vin[e], a.mode ? a.pb[e] : 0.f, sc);
+}
+
+__global__ void k_normalize(const float* __restrict__ v, const float* __restrict__ tdev, float* __restrict__ out,
+                            int64_t n) {
+    const float tv = *tdev;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fdiv_rn(v[i], tv);
+}
+
+// ---- reference-order R(A) products (oracle/structured.py ra_matvec / ra_rmatvec):
+// w[u] = sequential fp64 sum over the cells hitting u in np.bincount's input order
+// (Toeplitz family, then the two Hankel families of reflexive BC; cells increasing);
+// z = sequential fp64 sum over the kernel rows of rounded products; y = fl32(z)
+// (zero BC) or fl32 of the sequential sum of a cell's hits (reflexive).
+__global__ void k_rdiag(const float* __restrict__ x, int n, int c, int len, int refl, double* __restrict__ w) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= len) return;
+    double acc = 0.0;
+    const int o = u - c;   // Toeplitz: b = a + o
+    for (int a = max(0, -o); a < min(n, n - o); ++a) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + a + o]);
+    if (refl) {
+        for (int a = 0; a < n; ++a) {   // a + b + 1 + c = u
+            const int b = u - 1 - c - a;
+            if (b >= 0 && b < n) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + b]);
+        }
+        for (int a = 0; a < n; ++a) {   // a + b + c + 1 - 2n = u
+            const int b = u + 2 * n - c - 1 - a;
+            if (b >= 0 && b < n) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + b]);
+        }
+    }
+    w[u] = acc;
+}
+
+// z[o] = sum_i M[i][o] w[i], i sequential (M row-major rows x cols: K for R q, K^T for R^T s)
+__global__ void k_rz(const float* __restrict__ M, int rows, int cols, const double* __restrict__ w,
+                     double* __restrict__ z) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= cols) return;
+    double acc = 0.0;
+    for (int i = 0; i < rows; ++i) acc = __dadd_rn(acc, __dmul_rn((double)M[(int64_t)i * cols + o], w[i]));
+    z[o] = acc;
+}
+
+__global__ void k_rbcast(const double* __restrict__ z, int n, int c, int len, int refl, float* __restrict__ y) {
+    const int64_t N = (int64_t)n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e / n), b = (int)(e - (int64_t)a * n);
+        const int u1 = b - a + c;
+        if (!refl) {
+            y[e] = (u1 >= 0 && u1 < len) ? (float)z[u1] : 0.f;
+            continue;
+        }
+        double acc = 0.0;
+        if (u1 >= 0 && u1 < len) acc = __dadd_rn(acc, z[u1]);
+        const int u2 = a + b + 1 + c;
+        if (u2 >= 0 && u2 < len) acc = __dadd_rn(acc, z[u2]);
+        const int u3 = a + b + c + 1 - 2 * n;
+        if (u3 >= 0 && u3 < len) acc = __dadd_rn(acc, z[u3]);
+        y[e] = (float)acc;
+    }
+}
+
+// y = R(A) x (transpose = 0) or R(A)^T x, reference order; w, z: device scratch (>= kh + kw doubles each)
+void ref_product(const kb_operator* op, const float* x, float* y, int transpose, double* w, double* z,
+                 cudaStream_t s) {
+    const int n = op->side, kh = op->kh, kw = op->kw, refl = op->kind == KB_OP_RA_REFLEXIVE;
+    const int lin = transpose ? kw : kh, cin = lin / 2;     // diagonal sums of the input
+    const int lout = transpose ? kh : kw, cout = lout / 2;  // broadcast of z
+    k_rdiag<<<(int)cdiv(lin, 128), 128, 0, s>>>(x, n, cin, lin, refl, w);
+    KB_LAUNCH_CHECK();
+    // R q: z[v] = sum_u K[u][v] w[u] (K: kh x kw);  R^T s: z[u] = sum_v K^T[v][u] w[v] (K^T: kw x kh)
+    const float* M = static_cast<const float*>(transpose ? op->kt : op->k);
+    k_rz<<<(int)cdiv(lout, 128), 128, 0, s>>>(M, lin, lout, w, z);
+    KB_LAUNCH_CHECK();
+    const int64_t N = (int64_t)n * n;
+    k_rbcast<<<(int)std::min<int64_t>(cdiv(N, 256), kSMs * 16), 256, 0, s>>>(z, n, cout, lout, refl, y);
+    KB_LAUNCH_CHECK();
+}
+
+void launch_chain(ChainArgs a, cudaStream_t s) {
+    const bool al16 = ((uintptr_t)a.vin % 16 == 0) && (!a.mode || (uintptr_t)a.pb % 16 == 0) &&
+                      (!a.x0 || (uintptr_t)a.x0 % 16 == 0);
+    const size_t smem = sizeof(float) * NS * NARR * ROWS * LPC;
+    static bool cfg = false;
+    if (!cfg) {
+        KB_CUDA(cudaFuncSetAttribute(k_chain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KB_CUDA(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cfg = true;
+    }
+    const int grid = a.lanes / LPC;
+    if (al16) k_chain<16><<<grid, 32, smem, s>>>(a);
+    else k_chain<4><<<grid, 32, smem, s>>>(a);
+    KB_LAUNCH_CHECK();
+}
+
+void launch_normalize(const float* v, const float* tdev, float* out, int64_t n, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(kSMs * 8, cdiv(n, 256));
+    k_normalize<<<std::max(grid, 1), 256, 0, s>>>(v, tdev, out, n);
+    KB_LAUNCH_CHECK();
+}
+
+}  // namespace refa
+
+// Scratch of the engine inside the kb_egkb_run workspace.
+size_t egkb_openblas_ws_bytes(const kb_operator* op, int capacity) {
+    const int64_t len = std::max(op->rows, op->cols);
+    const size_t kk = (size_t)std::max(op->kh, 0) + (size_t)std::max(op->kw, 0) + 16;
+    return 2 * align_up(sizeof(double) * kk) + 2 * align_up(sizeof(float) * (size_t)len) +
+           align_up(sizeof(float) * (capacity + 16)) + align_up(sizeof(float) * 128) + align_up(sizeof(float) * 32) +
+           align_up(sizeof(unsigned) * 8) + 2048;
+}
+
+struct RefOut {   // also declared in kb_driver.cu
+    std::vector<double> alphas, ts, zetas, nus;
+    int done = 1, fired = -1, reason = 0, breakdown = 0, tbreak = 0, err = 0;
+};
+
+// lowrank.py:199-277 with the reference's fp32 operations, lanes = 64 / 32.
+void egkb_openblas(const kb_operator* op, const kb_egkb_config* cfg, const void* y0, kb_egkb_state* st,
+                   int lanes, double tol, void* wsp, size_t ws_bytes, RefOut& o, cudaStream_t s) {
+    KB_REQUIRE(op->dtype == KB_F32, "the reference-arithmetic engine reproduces the fp32 recurrence only");
+    KB_REQUIRE(lanes == 64 || lanes == 32, "unknown sdot kernel");
+    KB_REQUIRE(op->kind == KB_OP_RA_ZERO || op->kind == KB_OP_RA_REFLEXIVE,
+               "the reference-arithmetic engine needs a matrix-free R(A) operator");
+    Arena ar(wsp, ws_bytes);
+    const size_t kk = (size_t)op->kh + (size_t)op->kw + 16;
+    double* pw = ar.take<double>(kk);
+    double* pz = ar.take<double>(kk);
+    const int64_t mbar = op->rows, nbar = op->cols, len = std::max(mbar, nbar);
+    float* ubuf = ar.take<float>((size_t)len);
+    float* vbuf = ar.take<float>((size_t)len);
+    float* coef = ar.take<float>((size_t)st->capacity + 16);
+    float* sc = ar.take<float>(128);         // lane accumulators of k_chain
+    float* scal = ar.take<float>(8 * 4);   // fp32 device scalars (S_*)
+    unsigned* ticket = ar.take<unsigned>(8);
+    enum { S_T = 0, S_UN = 1, S_A = 2, S_PRE = 3, S_ALPHA = 4 };
+    float* S = static_cast<float*>(st->s_basis);
+    float* Q = static_cast<float*>(st->q_basis);
+    const int cap = st->capacity;
+    KB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned) * 8, s));
+
+    static thread_local float* hsc = nullptr;
+    if (!hsc) KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hsc), sizeof(float) * 8));
+
+    auto chain = [&](int mode, const float* vin, const float* pb, const float* pscal, float* vout,
+                     const float* x0, float* out0, int sqrt0, float* out1, int64_t n) {
+        refa::ChainArgs a;
+        a.vin = vin; a.pb = pb; a.pscal = pscal; a.vout = vout; a.x0 = x0; a.out0 = out0; a.out1 = out1;
+        a.mode = mode; a.sqrt0 = sqrt0; a.n = n; a.lanes = lanes; a.lane_acc = sc; a.ticket = ticket;
+        refa::launch_chain(a, s);
+    };
+    // v <- (vin - fl(beta*prev)); MGS against basis[0..m) (lowrank.py:153-156); *norm_out = |v|;
+    // *pre_out = |vin|; the projected vector stays in vbuf
+    auto project = [&](const float* vin, const float* prev, const float* beta, const float* basis, int64_t ld,
+                       int m, int64_t n, float* norm_out, float* pre_out) {
+        if (m == 0) {
+            chain(1, vin, prev, beta, vbuf, nullptr, norm_out, 1, pre_out, n);
+            return;
+        }
+        chain(1, vin, prev, beta, vbuf, basis, coef, 0, pre_out, n);
+        for (int i = 1; i < m; ++i)
+            chain(2, vbuf, basis + (int64_t)(i - 1) * ld, coef + i - 1, vbuf, basis + (int64_t)i * ld, coef + i, 0,
+                  nullptr, n);
+        chain(2, vbuf, basis + (int64_t)(m - 1) * ld, coef + m - 1, vbuf, nullptr, norm_out, 1, nullptr, n);
+    };
+    auto apply = [&](const float* x, float* y, int tr) { refa::ref_product(op, x, y, tr, pw, pz, s); };
+    auto fetch = [&]() {
+        KB_CUDA(cudaMemcpyAsync(hsc, scal, sizeof(float) * 8, cudaMemcpyDeviceToHost, s));
+        KB_CUDA(cudaStreamSynchronize(s));
+    };
+
+    // t1 = |y0|, s1 = y0 / t1 (lowrank.py:207-210)
+    chain(0, static_cast<const float*>(y0), nullptr, nullptr, nullptr, nullptr, scal + S_T, 1, nullptr, mbar);
+    refa::launch_normalize(static_cast<const float*>(y0), scal + S_T, S, mbar, s);
+    // q = B^T s1, alpha1 = |q| (lowrank.py:211-215)
+    apply(S, ubuf, 1);
+    chain(0, ubuf, nullptr, nullptr, nullptr, nullptr, scal + S_ALPHA, 1, nullptr, nbar);
+    refa::launch_normalize(ubuf, scal + S_ALPHA, Q, nbar, s);
+    fetch();
+    const double t1 = hsc[S_T], a1 = hsc[S_ALPHA];
+    if (t1 == 0.0) { o.err = 1; return; }
+    if (a1 == 0.0) { o.err = 2; return; }
+    o.alphas.push_back(a1);
+    o.ts.push_back(t1);
+    o.zetas.push_back(a1 * t1);
+    o.nus.push_back(1e308);
+    int done = 1, fired = -1;
+    for (;;) {
+        const int limit = fired >= 0 ? fired + cfg->p + 1 : cfg->k_max + 1;
+        if (done >= limit) break;
+        KB_REQUIRE(done + 1 <= cap, "eGKB basis capacity exhausted (%d)", cap);
+        // s step (lowrank.py:238-247)
+        apply(Q + (int64_t)(done - 1) * st->ld_q, ubuf, 0);
+        project(ubuf, S + (int64_t)(done - 1) * st->ld_s, scal + S_ALPHA, S, st->ld_s, cfg->full_reorth ? done : 0,
+                mbar, scal + S_T, scal + S_UN);
+        refa::launch_normalize(vbuf, scal + S_T, S + (int64_t)done * st->ld_s, mbar, s);
+        // q step (lowrank.py:250-260), run before the t test is read back: harmless on a t breakdown
+        apply(S + (int64_t)done * st->ld_s, ubuf, 1);
+        project(ubuf, Q + (int64_t)(done - 1) * st->ld_q, scal + S_T, Q, st->ld_q, done, nbar, scal + S_A,
+                scal + S_PRE);
+        refa::launch_normalize(vbuf, scal + S_A, Q + (int64_t)done * st->ld_q, nbar, s);
+        fetch();
+        const double t_new = hsc[S_T], u_norm = hsc[S_UN], a_new = hsc[S_A], pre = hsc[S_PRE];
+        if (t_new <= tol * u_norm) {
+            o.breakdown = o.tbreak = 1;
+            break;
+        }
+        if (a_new <= tol * pre) {
+            o.breakdown = 1;
+            o.ts.push_back(t_new);
+            break;
+        }
+        o.ts.push_back(t_new);
+        o.alphas.push_back(a_new);
+        const double zeta = a_new * t_new;
+        const double nu = std::sqrt(zeta * o.zetas.back());
+        o.zetas.push_back(zeta);
+        o.nus.push_back(nu);
+        ++done;
+        KB_CUDA(cudaMemcpyAsync(scal + S_ALPHA, scal + S_A, sizeof(float), cudaMemcpyDeviceToDevice, s));
+        if (fired < 0) {
+            const double nu_prev = o.nus[o.nus.size() - 2];
+            if (nu > nu_prev) {
+                fired = std::max(done - 1, cfg->k_min);
+                o.reason = KB_STOP_NU_ROSE;
+            } else if (nu < cfg->tau) {
+                fired = std::max(done, cfg->k_min);
+                o.reason = KB_STOP_NU_BELOW_TOL;
+            }
+        }
+    }
+    o.done = done;
+    o.fired = fired;
+}
+
+}  // namespace kb
+
+extern "C" int kb_sdot_openblas(int lanes, const float* x, const float* y, int64_t n, float* out_dev,
+                                void* ws, size_t ws_bytes, kb_stream_t stream) {
+    KB_GUARD({
+        KB_REQUIRE(lanes == 64 || lanes == 32, "lanes must be 64 (SkylakeX kernel) or 32 (Haswell kernel)");
+        KB_REQUIRE(x && out_dev && n >= 0 && ws && ws_bytes >= 1024, "bad arguments");
+        kb::Arena ar(ws, ws_bytes);
+        float* acc = ar.take<float>(128);
+        unsigned* ticket = ar.take<unsigned>(8);
+        cudaStream_t s = kb::as_stream(stream);
+        KB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned) * 8, s));
+        kb::refa::ChainArgs a{};
+        a.vin = y ? y : x;
+        a.x0 = y ? x : nullptr;
+        a.out0 = out_dev;
+        a.n = n;
+        a.lanes = lanes;
+        a.lane_acc = acc;
+        a.ticket = ticket;
+        kb::refa::launch_chain(a, s);
+    })
+}

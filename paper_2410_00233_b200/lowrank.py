@@ -275,17 +275,46 @@ def _bases(cap, mbar, nbar, dtype, key=None):
     return hit
 
 
-def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
+_ARITH_LANES = {"skylakex": "openblas-skx", "cooperlake": "openblas-skx", "sapphirerapids": "openblas-skx",
+                "haswell": "openblas-hsw", "zen": "openblas-hsw"}
+
+
+def host_blas_arithmetic() -> str:
+    """The ``arithmetic`` that reproduces numpy's fp32 dot products on this host:
+    OpenBLAS's x86-64 sdot kernel that numpy's OpenBLAS dispatches to here
+    (threadpoolctl reports its core name; ``OPENBLAS_CORETYPE`` changes it)."""
+    from threadpoolctl import threadpool_info
+
+    for info in threadpool_info():
+        if info.get("internal_api") == "openblas":
+            arch = str(info.get("architecture", "")).lower()
+            if arch in _ARITH_LANES:
+                return _ARITH_LANES[arch]
+            raise ValidationError(f"no reference-arithmetic emulation for OpenBLAS kernel {arch!r}")
+    raise ValidationError("numpy is not using OpenBLAS: no reference-arithmetic emulation")
+
+
+_ARITH_CODES = {"fast": 0, "openblas-skx": 1, "openblas-hsw": 2}
+
+
+def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1, *, arithmetic: str = "fast"):
     """Enlarged Golub-Kahan bidiagonalisation with automatic rank choice
     (lowrank.py:159-329), on the GPU.
 
-    ``reorth_passes`` = 1 (default) projects once against the whole basis,
-    as the reference's single modified-GS pass does (lowrank.py:153-156),
-    with the coefficients formed in one fused pass (classical GS, fp64
-    accumulation).  One pass is what reproduces the reference's breakdown
-    and rank decisions beyond the fp32 numerical rank (a second pass keeps
-    a noise-level recurrence alive where the reference stops; see
-    DESIGN.md); ``reorth_passes=2`` selects CGS2.
+    ``arithmetic`` selects the engine:
+
+    * ``"fast"`` (default): one persistent fused kernel; projections as one
+      classical pass with fp64-accumulated coefficients and exact fp64 norms.
+      ``reorth_passes=2`` selects CGS2.
+    * ``"reference"``: the reference's own fp32 operations in its order --
+      sequential modified Gram-Schmidt (lowrank.py:153-156) with every dot
+      product and norm computed as numpy's OpenBLAS sdot computes it on this
+      host (``host_blas_arithmetic()``; or name the kernel:
+      ``"openblas-skx"`` / ``"openblas-hsw"``).  The trace (alpha, t, zeta,
+      nu), the rank decision and the Krylov bases are then bit-identical to
+      the reference's, also past the fp32 numerical rank where the fast
+      engine's more accurate sums let the recurrence run one or two steps
+      longer before it breaks down.  Matrix-free fp32 operators only.
     """
     from . import device as D
 
@@ -313,8 +342,14 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1):
             raise ValidationError(f"y0 must have length {mbar}, got shape {y0.shape}")
         y0d = D.to_device(y0)
 
+    if arithmetic == "reference":
+        arithmetic = host_blas_arithmetic()
+    if arithmetic not in _ARITH_CODES:
+        raise ValidationError(f"unknown arithmetic {arithmetic!r}")
+    if arithmetic != "fast" and (dtype != np.float32 or op.kind == "dense"):
+        raise ValidationError("arithmetic='reference' reproduces the fp32 recurrence on matrix-free operators")
     cfg = _lib.KbEgkbConfig(config.k_max, config.p, config.k_min, float(config.tau), float(break_tol),
-                            1 if reorth == REORTH_FULL else 0, int(reorth_passes))
+                            1 if reorth == REORTH_FULL else 0, int(reorth_passes), _ARITH_CODES[arithmetic])
     lib = _lib.load()
     cap = lib.kb_egkb_capacity(C.byref(cfg))
     bkey = _bases_key(cap, mbar, nbar, dtype)

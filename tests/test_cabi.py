@@ -111,9 +111,13 @@ def test_psf_scan_is_numpys_sum_and_min_bitwise(lib, shape):
     k = np.ascontiguousarray(rng.random(shape) ** 5 * 10.0 ** rng.uniform(-30, 30))
     total, kmin = ctypes.c_double(), ctypes.c_double()
     for threads in (1, 3, 8, 16):
-        assert lib.kb_psf_scan(k.ctypes.data, k.size, threads, ctypes.byref(total), ctypes.byref(kmin)) == 0
+        own = np.full_like(k, np.nan)
+        assert lib.kb_psf_scan(k.ctypes.data, k.size, threads, ctypes.byref(total), ctypes.byref(kmin),
+                               own.ctypes.data if threads != 3 else None) == 0
         assert total.value == k.sum(), (shape, threads)
         assert kmin.value == k.min()
+        if threads != 3:
+            assert np.array_equal(own, k)      # the private copy taken in the same pass
 
 
 def test_psf_validation_uses_the_exact_scan():
@@ -132,3 +136,19 @@ def test_psf_validation_uses_the_exact_scan():
         Psf(bad)
     with pytest.raises(ValidationError):
         Psf(np.zeros((513, 513)))
+
+
+@pytest.mark.parametrize("side", [7, 301])
+def test_psf_is_a_private_copy(side):
+    """The reference's Psf copies the kernel (blurmodel.py:25-65, np.array(kernel)): changing
+    the caller's array afterwards must not change the operator, on either the small
+    (numpy) or the large (kb_psf_scan) construction path."""
+    import numpy as np
+    from paper_2410_00233_b200.blurmodel import Psf
+
+    rng = np.random.default_rng(side)
+    k = rng.random((side, side))
+    want = k / k.sum()
+    p = Psf(k)
+    k[:] = -1.0
+    assert np.array_equal(p.kernel, want)

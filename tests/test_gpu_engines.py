@@ -125,67 +125,39 @@ class TestEgkbBlur:
         assert tr_a.chosen_k == int(g["auto_chosen"]) and tr_a.stop_reason == str(g["auto_reason"])
         assert sigma_ok(svd_a.sigma, g["auto_sigma"], floor=5e-6)
 
-    @pytest.mark.parametrize("n,name", [(256, "n256"), (512, "n512"), (1024, "n1024")])
+    @pytest.mark.parametrize("n,name", [(256, "n256"), (512, "n512"), (1024, "n1024"), (2048, "n2048")])
     def test_large_blur_vs_oracle_restatement(self, kb, n, name):
-        """Rank decisions and sigma vs the restated reference.
+        """The fast engine (arithmetic="fast") against the restated reference on
+        configs[1..4].
 
-        Where the fp32 recurrence reaches the rounding-noise floor before the
-        requested rank (n=512/1024 with these smooth PSFs), the breakdown
-        iteration is decided by fp32 rounding noise: equally valid CPU
-        variants of the reference (MGS vs classical GS, fp32- vs fp64-
-        accumulated norms) stop at different iterations.  There the GPU's
-        k_p must fall inside the span of those CPU variants, and every
-        singular value above the noise floor must match to 1e-4.
+        Decisions taken above the fp32 noise floor (the nu rule at n=256 and
+        n=2048) must be identical.  Where the reference's fixed-rank run ends in
+        a noise-floor breakdown (n=512: 20+2, n=1024: 30+2) the iteration it
+        breaks down at is set by the roundings of its OpenBLAS dot products
+        (the reference itself stops at k_p=12 with the SkylakeX sdot kernel
+        and 11 with the Haswell one at n=1024); the fast engine's exact fp64
+        sums keep the noise recurrence alive longer, so there it must also
+        break down, not earlier, and every extra singular value must be noise.
+        The rank parity claim for those runs is the reference-arithmetic engine
+        (tests/test_gpu_refarith.py: bit-identical traces and decisions).
         """
         from oracle import lowrank as olr
         from oracle import structured as ost
         from paper_2410_00233_b200 import datagen
 
-        psf = datagen.mixture_psf(n)
-        cfg = kb.EgkbConfig(**datagen.CONFIGS[name]["egkb"])
+        prob = datagen.make_problem(name)
+        psf = prob.psf
+        cfg = kb.EgkbConfig(**prob.egkb)
         svd, tr = kb.egkb(kb.RearrangedBlur(psf, n), cfg)
-        k32 = psf.astype(np.float32)
-        mv = lambda q: ost.ra_matvec(k32, n, q)
-        rmv = lambda x: ost.ra_rmatvec(k32, n, x)
-        (_, os_, _), otr = olr.egkb(mv, rmv, (n * n, n * n), np.float32, _ocfg(cfg))
-        variants = [(otr.chosen_k, otr.k_p)]
-        if (tr.chosen_k, tr.k_p) != (otr.chosen_k, otr.k_p):
-            def cgs64(v, basis):
-                S = np.stack(basis).astype(np.float64)
-                vv = v.astype(np.float64)
-                return (vv - S.T @ (S @ vv)).astype(np.float32)
-
-            orig_proj, orig_norm = olr.project_out, np.linalg.norm
-            try:
-                olr.project_out = cgs64
-                (_, _, _), t2 = olr.egkb(mv, rmv, (n * n, n * n), np.float32, _ocfg(cfg))
-                variants.append((t2.chosen_k, t2.k_p))
-            finally:
-                olr.project_out = orig_proj
-            # GPU-equivalent variant: classical GS with fp64-accumulated norms
-            class N64:
-                @staticmethod
-                def norm(x, *a, **k):
-                    return np.sqrt(np.dot(np.asarray(x, dtype=np.float64), np.asarray(x, dtype=np.float64)))
-            try:
-                olr.project_out = cgs64
-                olr.np.linalg.norm = N64.norm
-                (_, _, _), t3 = olr.egkb(mv, rmv, (n * n, n * n), np.float32, _ocfg(cfg))
-                variants.append((t3.chosen_k, t3.k_p))
-            finally:
-                olr.project_out = orig_proj
-                olr.np.linalg.norm = orig_norm
-            kps = [v[1] for v in variants]
-            assert tr.breakdown and otr.breakdown, (tr.k_p, variants)
-            # Past the CPU variants' span the recurrence is iterating on
-            # rounding noise: the GPU may take at most 2 more such steps (its
-            # one-pass classical projection and fp64-reduced dots leave a
-            # differently sized noise floor than BLAS MGS), and every extra
-            # singular value must be noise (< 1e-6 sigma_1, below anything the
-            # fp32 approximation resolves).
-            assert min(kps) <= tr.k_p <= max(kps) + 2, (tr.k_p, variants)
-            assert np.all(svd.sigma[max(kps):] < 1e-6 * svd.sigma[0]), (svd.sigma, variants)
+        k32 = (psf / psf.sum()).astype(np.float32)
+        (_, os_, _), otr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda x: ost.ra_rmatvec(k32, n, x),
+                                    (n * n, n * n), np.float32, _ocfg(cfg))
         assert tr.stop_reason == otr.stop_reason
+        if not otr.breakdown:
+            assert (tr.chosen_k, tr.k_p, tr.breakdown) == (otr.chosen_k, otr.k_p, otr.breakdown)
+        else:
+            assert tr.breakdown and tr.k_p >= otr.k_p, (tr.k_p, otr.k_p)
+            assert np.all(svd.sigma[otr.k_p:] < 1e-6 * svd.sigma[0]), (svd.sigma, otr.k_p)
         # exact structured sigma (fp64) as ground truth for the leading values
         _, s_exact, _ = ost.structured_tsvd(psf, n, k=svd.k)
         lead = s_exact >= 1e-3 * s_exact[0]

@@ -243,3 +243,19 @@ class TestSparseRearrangement:
             RearrangedSparse(np.ones((6, 6)), BlockScheme(2, 2, 2, 2))
         with pytest.raises(ValidationError):
             RearrangedSparse(([0], [9], [1.0], (4, 4)), BlockScheme(2, 2, 2, 2))
+
+
+def test_kernel_product_is_sequential_in_index_order():
+    """oracle.structured._kernel_product: each z entry a sequential fp64 sum of rounded
+    products in index order (the order the device's reference-order product repeats)."""
+    from oracle import structured as ost
+
+    rng = np.random.default_rng(3)
+    for kh, kw in [(1, 1), (7, 9), (129, 65), (1025, 1025)]:
+        k = rng.standard_normal((kh, kw)).astype(np.float32)
+        for transpose, m in ((False, kh), (True, kw)):
+            w = rng.standard_normal(m) * 10.0 ** rng.uniform(-6, 6, m)
+            want = np.zeros(kw if not transpose else kh)
+            for i in range(m):
+                want += (k[i].astype(np.float64) if not transpose else k[:, i].astype(np.float64)) * w[i]
+            assert np.array_equal(ost._kernel_product(k, w, transpose), want)
