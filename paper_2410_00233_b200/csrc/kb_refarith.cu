@@ -13,17 +13,16 @@
 // keeps the noise alive for one or two more steps.  This engine repeats the
 // reference's operations in the reference's order:
 //
-//   * k_chain: one fused MGS step.  The vector of the step is formed on the
-//     fly (v = u - fl(beta*prev), or v = v - fl(c*b) with the coefficient of
-//     the previous MGS step), stored, and fed to the sdot lanes of the next
-//     coefficient (or of the norm).  Lane l of the kernel accumulates the
-//     elements 64k+l (32k+l) in order with IEEE fp32 FMAs, exactly as the
-//     SIMD accumulators do; 8 lanes per CTA (one 32-byte sector per row),
-//     the rows streamed through a shared-memory ring with cp.async.  The last
-//     CTA folds the lanes in the kernel's order, runs the 32-element block
-//     and the scalar tail (fp32 products summed in fp64), and takes sqrtf for
-//     norms.  A second, independent lane set yields |u| (the breakdown
-//     threshold) in the same pass.
+//   * k_update: the elementwise steps, v = u - fl(beta*prev) and the MGS
+//     update v = v - fl(c*b), with numpy's two roundings, over the whole grid.
+//   * k_chain: one sdot.  Lane l accumulates the elements 64k+l (32k+l) in
+//     order with IEEE fp32 FMAs, exactly as the SIMD accumulators do; 8 lanes
+//     per CTA (one 32-byte sector per row), the rows streamed through a
+//     lane-major shared-memory ring by 4-byte cp.async.  The last CTA folds
+//     the lanes in the kernel's order, runs the 32-element block and the
+//     scalar tail (fp32 products summed in fp64), and takes sqrtf for norms.
+//     A second, independent lane set yields |u| (the breakdown threshold) in
+//     the same pass.
 //   * k_normalize: s = fl(v / t) (lowrank.py:247, 260).
 //   * ref_product: the R(A) products in the port's fixed fp64 order
 //     (oracle/structured.py: np.bincount's sequential diagonal sums, the kernel
@@ -43,79 +42,69 @@
 namespace kb {
 namespace refa {
 
-constexpr int LPC = 8;      // lanes (chains) per CTA
-constexpr int ROWS = 64;    // rows per ring stage
-constexpr int NS = 8;       // ring stages
-constexpr int NARR = 3;     // streamed arrays: vin, pb, x0
+constexpr int LPC = 8;      // lanes (chains) per CTA: one 32-byte sector per row
+constexpr int ROWS = 128;   // rows per ring stage
+constexpr int NS = 12;      // ring stages
+constexpr int NARR = 3;     // streamed arrays: x, v, u
 
 struct ChainArgs {
-    const float* vin;    // source of the step's vector
-    const float* pb;     // mode 1: previous basis vector; mode 2: basis vector of the update
-    const float* pscal;  // device fp32 scalar: beta (mode 1) or the MGS coefficient (mode 2)
-    float* vout;         // the step's vector (mode 1/2; may alias vin)
-    const float* x0;     // chain 0 = sdot(x0, v); nullptr: sdot(v, v)
+    const float* x;      // chain 0 = sdot(x, v); nullptr: sdot(v, v)
+    const float* v;
+    const float* u;      // chain 1 = sdot(u, u) when not nullptr
     float* out0;         // chain 0 result (sqrtf'ed when sqrt0)
-    float* out1;         // chain 1 = sqrtf(sdot(vin, vin)) when not nullptr
-    int mode, sqrt0;
+    float* out1;         // sqrtf(chain 1)
+    int sqrt0;
     int64_t n;
     int lanes;           // 64 (SkylakeX kernel) or 32 (Haswell kernel)
     float* lane_acc;     // [2][64]
     unsigned* ticket;
 };
 
-__device__ __forceinline__ float step_value(int mode, float vin, float pb, float sc) {
-    // numpy: u - f32(beta) * s  /  v - c * b : a rounded product, then a rounded difference
-    return mode ? __fsub_rn(vin, __fmul_rn(sc, pb)) : vin;
-}
-
 // Lane fold + 32-element block + scalar tail of OpenBLAS's x86-64 sdot
 // (kernel/x86_64/sdot.c with the skylakex / haswell micro-kernels).
-__device__ float sdot_fold(const float* acc, int lanes, const ChainArgs& a, int which, float sc) {
-    const int64_t n = a.n, n1 = n & ~(int64_t)31, nmain = lanes == 64 ? (n1 & ~(int64_t)63) : n1;
-    auto xy = [&](int64_t e, float& x, float& y) {
-        const float vi = a.vin[e];
-        if (which == 1) {
-            x = y = vi;
-            return;
-        }
-        const float v = step_value(a.mode, vi, a.mode ? a.pb[e] : 0.f, sc);
-        y = v;
-        x = a.x0 ? a.x0[e] : v;
-    };
+__device__ float sdot_fold(const float* acc, int lanes, const float* x, const float* y, int64_t n) {
+    const int64_t n1 = n & ~(int64_t)31, nmain = lanes == 64 ? (n1 & ~(int64_t)63) : n1;
     float r;
     if (lanes == 64) {
         float q[4][8];
+#pragma unroll
         for (int k = 0; k < 4; ++k)
+#pragma unroll
             for (int j = 0; j < 8; ++j) q[k][j] = __fadd_rn(acc[16 * k + j], acc[16 * k + j + 8]);
-        for (int64_t e = nmain; e < n1; ++e) {   // the 256-bit loop after the 512-bit one
-            const int k = (int)((e - nmain) >> 3), j = (int)((e - nmain) & 7);
-            float x, y;
-            xy(e, x, y);
-            q[k][j] = fmaf(x, y, q[k][j]);
-        }
+        if (n1 > nmain)   // the 256-bit loop after the 512-bit one: one block of 32
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q[k][j] = fmaf(x[nmain + 8 * k + j], y[nmain + 8 * k + j], q[k][j]);
         float s8[8];
+#pragma unroll
         for (int j = 0; j < 8; ++j) s8[j] = __fadd_rn(__fadd_rn(__fadd_rn(q[0][j], q[1][j]), q[2][j]), q[3][j]);
         float h[4];
+#pragma unroll
         for (int j = 0; j < 4; ++j) h[j] = __fadd_rn(s8[j], s8[j + 4]);
         r = __fadd_rn(__fadd_rn(h[0], h[1]), __fadd_rn(h[2], h[3]));
     } else {
         float f[4][4];
+#pragma unroll
         for (int k = 0; k < 4; ++k)
+#pragma unroll
             for (int j = 0; j < 4; ++j) f[k][j] = __fadd_rn(acc[8 * k + j], acc[8 * k + j + 4]);
         float t[4];
+#pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = __fadd_rn(__fadd_rn(f[0][j], f[1][j]), __fadd_rn(f[2][j], f[3][j]));
         r = __fadd_rn(__fadd_rn(t[0], t[1]), __fadd_rn(t[2], t[3]));
     }
     double d = (double)r;   // the scalar tail: fp32 products summed in fp64
-    for (int64_t e = n1; e < n; ++e) {
-        float x, y;
-        xy(e, x, y);
-        d += (double)__fmul_rn(x, y);
-    }
+    for (int64_t e = n1; e < n; ++e) d += (double)__fmul_rn(x[e], y[e]);
     return (float)d;
 }
 
-template <int VEC>
+// The sdot lanes: lane l = 8 * blockIdx.x + threadIdx.x (< 8) accumulates rows k of the
+// element 64k + l (32k + l) with fp32 FMAs in order.  A CTA's 8 lanes are one 32-byte
+// sector per row; the rows reach a row-major shared-memory ring by cp.async (VEC bytes
+// per copy, one pointer increment per copy), so per row a lane issues one shared load
+// per array and one FMA: the 4-cycle FMA chain is the limit.
+template <bool HAS_X, bool HAS_U, int VEC>
 __global__ void __launch_bounds__(32) k_chain(ChainArgs a) {
     extern __shared__ float4 smv[];
     float* sm = reinterpret_cast<float*>(smv);
@@ -123,96 +112,73 @@ __global__ void __launch_bounds__(32) k_chain(ChainArgs a) {
     const int L = a.lanes;
     const int64_t n1 = a.n & ~(int64_t)31;
     const int64_t nmain = L == 64 ? (n1 & ~(int64_t)63) : n1;
-    const int64_t K = nmain / L;
-    const float* __restrict__ src0 = a.vin;
-    const float* __restrict__ src1 = a.mode ? a.pb : nullptr;
-    const float* __restrict__ src2 = a.x0;
-    const float sc = a.mode ? *a.pscal : 0.f;
-    constexpr int SLOT = NARR * ROWS * LPC;   // floats per stage
-    const int64_t nst = (K + ROWS - 1) / ROWS;
-    constexpr int PER = LPC * 4 / VEC;        // copies per row per array
+    const int K = (int)(nmain / L);
+    constexpr int SLOT = NARR * ROWS * LPC;          // floats per stage: [array][row][lane]
+    constexpr int PER = LPC * 4 / VEC;               // copies per row per array
+    constexpr int RSTEP = 32 / PER;                  // rows between one thread's copies
+    const int nst = (K + ROWS - 1) / ROWS;
+    const int part = t % PER, crow = t / PER;
+    // this thread's source pointers at row crow of stage 0, and its destination offset
+    const float* gv = a.v + (int64_t)crow * L + c * LPC + part * (VEC / 4);
+    const float* gx = HAS_X ? a.x + (int64_t)crow * L + c * LPC + part * (VEC / 4) : nullptr;
+    const float* gu = HAS_U ? a.u + (int64_t)crow * L + c * LPC + part * (VEC / 4) : nullptr;
+    const int soff = crow * LPC + part * (VEC / 4);
+    const int64_t gstep = (int64_t)RSTEP * L;
 
-    auto issue = [&](int64_t st) {
+    auto issue = [&](int st) {
         if (st < nst) {
-            float* dst = sm + (int)(st % NS) * SLOT;
-            const int64_t r0 = st * ROWS;
-            const int rows = (int)min((int64_t)ROWS, K - r0);
-            auto one = [&](const float* __restrict__ g0, int arr) {
+            float* dst = sm + (st % NS) * SLOT + soff;
+            const int r0 = st * ROWS;
+            const int rows = min(ROWS, K - r0);
+            const int64_t g0 = (int64_t)r0 * L;
 #pragma unroll
-                for (int i = t; i < ROWS * PER; i += 32) {
-                    const int r = i / PER, part = i - r * PER;
-                    if (r < rows)
-                        __pipeline_memcpy_async(dst + (arr * ROWS + r) * LPC + part * (VEC / 4),
-                                                g0 + (r0 + r) * L + c * LPC + part * (VEC / 4), VEC);
+            for (int i = 0; i < ROWS / RSTEP; ++i) {
+                if (crow + i * RSTEP < rows) {
+                    const int64_t go = g0 + i * gstep;
+                    const int so = i * RSTEP * LPC;
+                    __pipeline_memcpy_async(dst + 1 * ROWS * LPC + so, gv + go, VEC);
+                    if (HAS_X) __pipeline_memcpy_async(dst + 0 * ROWS * LPC + so, gx + go, VEC);
+                    if (HAS_U) __pipeline_memcpy_async(dst + 2 * ROWS * LPC + so, gu + go, VEC);
                 }
-            };
-            one(src0, 0);
-            if (src1) one(src1, 1);
-            if (src2) one(src2, 2);
+            }
         }
         __pipeline_commit();
     };
 
     for (int st = 0; st < NS - 1; ++st) issue(st);
     float acc0 = 0.f, acc1 = 0.f;
-    const int lane = c * LPC + t;
-    for (int64_t st = 0; st < nst; ++st) {
+    for (int st = 0; st < nst; ++st) {
         __pipeline_wait_prior(NS - 2);
         __syncwarp();
         issue(st + NS - 1);
         if (t < LPC) {
-            // register batches of RB rows, the next batch's shared-memory loads issued before
-            // this batch's global stores, so the FMA chain (4 cycles per row) is the only wait
-            const float* __restrict__ base = sm + (int)(st % NS) * SLOT;
-            const int64_t r0 = st * ROWS;
-            const int rows = (int)min((int64_t)ROWS, K - r0);
-            float* __restrict__ vo = a.vout ? a.vout + r0 * L + lane : nullptr;
-            constexpr int RB = 16;
-            float vi[RB], pb[RB], xx[RB], vi2[RB], pb2[RB], xx2[RB];
-            auto load = [&](int rb, float* v_, float* p_, float* x_) {
-#pragma unroll
-                for (int j = 0; j < RB; ++j) {
-                    const int r = min(rb + j, ROWS - 1);
-                    v_[j] = base[(0 * ROWS + r) * LPC + t];
-                    p_[j] = a.mode ? base[(1 * ROWS + r) * LPC + t] : 0.f;
-                    x_[j] = a.x0 ? base[(2 * ROWS + r) * LPC + t] : 0.f;
-                }
-            };
-            load(0, vi, pb, xx);
-            for (int rb = 0; rb < rows; rb += RB) {
-                if (rb + RB < rows) load(rb + RB, vi2, pb2, xx2);
-                float vv[RB];
-#pragma unroll
-                for (int j = 0; j < RB; ++j) vv[j] = step_value(a.mode, vi[j], pb[j], sc);
-                if (rb + RB <= rows) {
-#pragma unroll
-                    for (int j = 0; j < RB; ++j) {
-                        acc0 = fmaf(a.x0 ? xx[j] : vv[j], vv[j], acc0);
-                        acc1 = fmaf(vi[j], vi[j], acc1);
+            const float* __restrict__ base = sm + (st % NS) * SLOT + t;
+            const int rows = min(ROWS, K - st * ROWS);
+            if (rows == ROWS) {
+#pragma unroll 16
+                for (int r = 0; r < ROWS; ++r) {
+                    const float v = base[(1 * ROWS + r) * LPC];
+                    acc0 = fmaf(HAS_X ? base[(0 * ROWS + r) * LPC] : v, v, acc0);
+                    if (HAS_U) {
+                        const float u = base[(2 * ROWS + r) * LPC];
+                        acc1 = fmaf(u, u, acc1);
                     }
-                    if (vo)
-#pragma unroll
-                        for (int j = 0; j < RB; ++j) vo[(int64_t)(rb + j) * L] = vv[j];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < RB; ++j)
-                        if (rb + j < rows) {
-                            acc0 = fmaf(a.x0 ? xx[j] : vv[j], vv[j], acc0);
-                            acc1 = fmaf(vi[j], vi[j], acc1);
-                            if (vo) vo[(int64_t)(rb + j) * L] = vv[j];
-                        }
                 }
-#pragma unroll
-                for (int j = 0; j < RB; ++j) {
-                    vi[j] = vi2[j];
-                    pb[j] = pb2[j];
-                    xx[j] = xx2[j];
+            } else {
+                for (int r = 0; r < rows; ++r) {
+                    const float v = base[(1 * ROWS + r) * LPC];
+                    acc0 = fmaf(HAS_X ? base[(0 * ROWS + r) * LPC] : v, v, acc0);
+                    if (HAS_U) {
+                        const float u = base[(2 * ROWS + r) * LPC];
+                        acc1 = fmaf(u, u, acc1);
+                    }
                 }
             }
         }
         __syncwarp();
     }
     __pipeline_wait_prior(0);
+    const int lane = c * LPC + t;
     if (t < LPC) {
         a.lane_acc[lane] = acc0;
         a.lane_acc[64 + lane] = acc1;
@@ -224,23 +190,37 @@ __global__ void __launch_bounds__(32) k_chain(ChainArgs a) {
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != gridDim.x - 1) return;
     __threadfence();
-    // last CTA: the folds (reading the remainder elements), the results, then the
-    // remainder of the step's vector (vout may alias vin)
-    if (t == 0) {
+    if (t == 0) {   // last CTA: the folds, the remainder elements, the results
         float acc[64];
         for (int i = 0; i < L; ++i) acc[i] = __ldcg(a.lane_acc + i);
-        float r0 = sdot_fold(acc, L, a, 0, sc);
+        const float r0 = sdot_fold(acc, L, HAS_X ? a.x : a.v, a.v, a.n);
         *a.out0 = a.sqrt0 ? sqrtf(r0) : r0;
-        if (a.out1) {
+        if (HAS_U) {
             for (int i = 0; i < L; ++i) acc[i] = __ldcg(a.lane_acc + 64 + i);
-            *a.out1 = sqrtf(sdot_fold(acc, L, a, 1, sc));
+            *a.out1 = sqrtf(sdot_fold(acc, L, a.u, a.u, a.n));
         }
         *a.ticket = 0u;
     }
-    __syncwarp();
-    if (a.vout)
-        for (int64_t e = nmain + t; e < a.n; e += 32)
-            a.vout[e] = step_value(a.mode, a.vin[e], a.mode ? a.pb[e] : 0.f, sc);
+}
+
+// The elementwise steps with numpy's roundings (a rounded product, then a rounded
+// difference): v = vin - fl(c * b), c a device fp32 scalar -- lowrank.py:239, 252
+// (u - alpha s_j, q_raw - t q_j) and the MGS update of lowrank.py:155.
+__global__ void k_update(const float* __restrict__ vin, const float* __restrict__ b, const float* __restrict__ cdev,
+                         float* __restrict__ vout, int64_t n) {
+    const float cv = *cdev;
+    const int64_t n4 = n >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const float4* v4 = reinterpret_cast<const float4*>(vin);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    float4* o4 = reinterpret_cast<float4*>(vout);
+    for (int64_t i = i0; i < n4; i += stride) {
+        const float4 x = v4[i], y = b4[i];
+        o4[i] = make_float4(__fsub_rn(x.x, __fmul_rn(cv, y.x)), __fsub_rn(x.y, __fmul_rn(cv, y.y)),
+                            __fsub_rn(x.z, __fmul_rn(cv, y.z)), __fsub_rn(x.w, __fmul_rn(cv, y.w)));
+    }
+    for (int64_t i = 4 * n4 + i0; i < n; i += stride) vout[i] = __fsub_rn(vin[i], __fmul_rn(cv, b[i]));
 }
 
 __global__ void k_normalize(const float* __restrict__ v, const float* __restrict__ tdev, float* __restrict__ out,
@@ -320,19 +300,48 @@ void ref_product(const kb_operator* op, const float* x, float* y, int transpose,
     KB_LAUNCH_CHECK();
 }
 
-void launch_chain(ChainArgs a, cudaStream_t s) {
-    const bool al16 = ((uintptr_t)a.vin % 16 == 0) && (!a.mode || (uintptr_t)a.pb % 16 == 0) &&
-                      (!a.x0 || (uintptr_t)a.x0 % 16 == 0);
-    const size_t smem = sizeof(float) * NS * NARR * ROWS * LPC;
+__global__ void k_update_scalar(const float* __restrict__ vin, const float* __restrict__ b,
+                                const float* __restrict__ cdev, float* __restrict__ vout, int64_t n) {
+    const float cv = *cdev;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        vout[i] = __fsub_rn(vin[i], __fmul_rn(cv, b[i]));
+}
+
+template <bool X, bool U, int VEC>
+static void chain_launch(const ChainArgs& a, size_t smem, cudaStream_t s) {
     static bool cfg = false;
     if (!cfg) {
-        KB_CUDA(cudaFuncSetAttribute(k_chain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        KB_CUDA(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KB_CUDA(cudaFuncSetAttribute(k_chain<X, U, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cfg = true;
     }
-    const int grid = a.lanes / LPC;
-    if (al16) k_chain<16><<<grid, 32, smem, s>>>(a);
-    else k_chain<4><<<grid, 32, smem, s>>>(a);
+    k_chain<X, U, VEC><<<a.lanes / LPC, 32, smem, s>>>(a);
+}
+
+void launch_chain(ChainArgs a, cudaStream_t s) {
+    const size_t smem = sizeof(float) * NS * NARR * ROWS * LPC;
+    const bool al = (uintptr_t)a.v % 16 == 0 && (!a.x || (uintptr_t)a.x % 16 == 0) && (!a.u || (uintptr_t)a.u % 16 == 0);
+    if (al) {
+        if (a.x && a.u) chain_launch<true, true, 16>(a, smem, s);
+        else if (a.x) chain_launch<true, false, 16>(a, smem, s);
+        else if (a.u) chain_launch<false, true, 16>(a, smem, s);
+        else chain_launch<false, false, 16>(a, smem, s);
+    } else {
+        if (a.x && a.u) chain_launch<true, true, 4>(a, smem, s);
+        else if (a.x) chain_launch<true, false, 4>(a, smem, s);
+        else if (a.u) chain_launch<false, true, 4>(a, smem, s);
+        else chain_launch<false, false, 4>(a, smem, s);
+    }
+    KB_LAUNCH_CHECK();
+}
+
+void launch_update(const float* vin, const float* b, const float* cdev, float* vout, int64_t n, cudaStream_t s) {
+    const bool al = ((uintptr_t)vin % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)vout % 16 == 0);
+    const int grid = (int)std::min<int64_t>(kSMs * 4, std::max<int64_t>(1, cdiv(n, 1024)));
+    if (al) {
+        k_update<<<grid, 256, 0, s>>>(vin, b, cdev, vout, n);
+    } else {
+        k_update_scalar<<<grid, 256, 0, s>>>(vin, b, cdev, vout, n);
+    }
     KB_LAUNCH_CHECK();
 }
 
@@ -385,26 +394,30 @@ void egkb_openblas(const kb_operator* op, const kb_egkb_config* cfg, const void*
     static thread_local float* hsc = nullptr;
     if (!hsc) KB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hsc), sizeof(float) * 8));
 
-    auto chain = [&](int mode, const float* vin, const float* pb, const float* pscal, float* vout,
-                     const float* x0, float* out0, int sqrt0, float* out1, int64_t n) {
-        refa::ChainArgs a;
-        a.vin = vin; a.pb = pb; a.pscal = pscal; a.vout = vout; a.x0 = x0; a.out0 = out0; a.out1 = out1;
-        a.mode = mode; a.sqrt0 = sqrt0; a.n = n; a.lanes = lanes; a.lane_acc = sc; a.ticket = ticket;
+    // one sdot (or norm, sqrt0) of the lanes; out1 = |u| when u != nullptr
+    auto chain = [&](const float* x, const float* v, const float* u, float* out0, int sqrt0, float* out1,
+                     int64_t n) {
+        refa::ChainArgs a{};
+        a.x = x; a.v = v; a.u = u; a.out0 = out0; a.out1 = out1; a.sqrt0 = sqrt0;
+        a.n = n; a.lanes = lanes; a.lane_acc = sc; a.ticket = ticket;
         refa::launch_chain(a, s);
     };
-    // v <- (vin - fl(beta*prev)); MGS against basis[0..m) (lowrank.py:153-156); *norm_out = |v|;
-    // *pre_out = |vin|; the projected vector stays in vbuf
+    // v = vin - fl(beta*prev) (lowrank.py:239 / 252); MGS against basis[0..m) (lowrank.py:153-156);
+    // *norm_out = |v| (the t / alpha of lowrank.py:242 / 254), *pre_out = |vin| (the breakdown
+    // thresholds |u| / pre_norm of lowrank.py:243 / 251); the projected vector stays in vbuf
     auto project = [&](const float* vin, const float* prev, const float* beta, const float* basis, int64_t ld,
                        int m, int64_t n, float* norm_out, float* pre_out) {
+        refa::launch_update(vin, prev, beta, vbuf, n, s);
         if (m == 0) {
-            chain(1, vin, prev, beta, vbuf, nullptr, norm_out, 1, pre_out, n);
+            chain(nullptr, vbuf, vin, norm_out, 1, pre_out, n);
             return;
         }
-        chain(1, vin, prev, beta, vbuf, basis, coef, 0, pre_out, n);
-        for (int i = 1; i < m; ++i)
-            chain(2, vbuf, basis + (int64_t)(i - 1) * ld, coef + i - 1, vbuf, basis + (int64_t)i * ld, coef + i, 0,
-                  nullptr, n);
-        chain(2, vbuf, basis + (int64_t)(m - 1) * ld, coef + m - 1, vbuf, nullptr, norm_out, 1, nullptr, n);
+        chain(basis, vbuf, vin, coef, 0, pre_out, n);
+        for (int i = 1; i <= m; ++i) {
+            refa::launch_update(vbuf, basis + (int64_t)(i - 1) * ld, coef + i - 1, vbuf, n, s);
+            if (i < m) chain(basis + (int64_t)i * ld, vbuf, nullptr, coef + i, 0, nullptr, n);
+            else chain(nullptr, vbuf, nullptr, norm_out, 1, nullptr, n);
+        }
     };
     auto apply = [&](const float* x, float* y, int tr) { refa::ref_product(op, x, y, tr, pw, pz, s); };
     auto fetch = [&]() {
@@ -413,11 +426,11 @@ void egkb_openblas(const kb_operator* op, const kb_egkb_config* cfg, const void*
     };
 
     // t1 = |y0|, s1 = y0 / t1 (lowrank.py:207-210)
-    chain(0, static_cast<const float*>(y0), nullptr, nullptr, nullptr, nullptr, scal + S_T, 1, nullptr, mbar);
+    chain(nullptr, static_cast<const float*>(y0), nullptr, scal + S_T, 1, nullptr, mbar);
     refa::launch_normalize(static_cast<const float*>(y0), scal + S_T, S, mbar, s);
     // q = B^T s1, alpha1 = |q| (lowrank.py:211-215)
     apply(S, ubuf, 1);
-    chain(0, ubuf, nullptr, nullptr, nullptr, nullptr, scal + S_ALPHA, 1, nullptr, nbar);
+    chain(nullptr, ubuf, nullptr, scal + S_ALPHA, 1, nullptr, nbar);
     refa::launch_normalize(ubuf, scal + S_ALPHA, Q, nbar, s);
     fetch();
     const double t1 = hsc[S_T], a1 = hsc[S_ALPHA];
@@ -489,8 +502,8 @@ extern "C" int kb_sdot_openblas(int lanes, const float* x, const float* y, int64
         cudaStream_t s = kb::as_stream(stream);
         KB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned) * 8, s));
         kb::refa::ChainArgs a{};
-        a.vin = y ? y : x;
-        a.x0 = y ? x : nullptr;
+        a.x = y ? x : nullptr;
+        a.v = y ? y : x;
         a.out0 = out_dev;
         a.n = n;
         a.lanes = lanes;
