@@ -8,8 +8,9 @@ into fp64 Kronecker factors.  `value` = approximations/s over all ranks with
 inputs resident in HBM; `e2e` = the same through the public API from host
 arrays (PSF uploaded, the reference's y0 stream drawn on the device by kb_rng.cu, trace/sigma read back) each
 step.  The same run also measures the fp64 split-Bregman solve that consumes
-the factors (isotropic, CGLS i_max=100 tau=1e-4) and reports outer / CGLS
-iterations per second in "sb", and the R(A) product in "ra_matvec".
+the factors (isotropic, 200 outer iterations, CGLS i_max=100 tau=1e-4: the
+north star's approximation + solve, "n1" and "sb"), the reference-arithmetic
+engine ("reference_arithmetic"), and the R(A) product ("ra_matvec").
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU (torchrun): independent replicas (weak scaling), max-over-ranks time.
@@ -50,6 +51,23 @@ def egkb_cfg_kwargs():
     from paper_2410_00233_b200 import datagen
 
     return dict(datagen.CONFIGS[CONFIG]["egkb"])
+
+
+def bench_config(n):
+    """The workload, identical in both arms' JSON lines (results live under "result")."""
+    return {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 (matrix-free R(A)) -> assemble", "n": n,
+            "egkb": {k: (str(v) if k == "tau" else v) for k, v in egkb_cfg_kwargs().items()},
+            "l2": "GPU arm: flushed (512 MB write) before every timed step"}
+
+
+def trace_result(tr):
+    return {"chosen_k": int(tr.chosen_k), "k_p": int(tr.k_p), "stop_reason": str(tr.stop_reason),
+            "breakdown": bool(tr.breakdown)}
+
+
+def psf_f32(psf):
+    """The fp32 kernel the reference's Psf + cast produce: (k / k.sum()).astype(float32)."""
+    return (psf / psf.sum()).astype(np.float32)
 
 
 # ---------------------------------------------------------------- clocks
@@ -113,7 +131,7 @@ def run_reference(args, prob):
     from oracle import structured as ost
 
     n = prob.n
-    k32 = prob.psf.astype(np.float32)
+    k32 = psf_f32(prob.psf)
     cfg = SimpleNamespace(reorth=None, seed=0, break_tol=None, keep_basis=False, **egkb_cfg_kwargs())
     cfg.tau = float(cfg.tau)
 
@@ -137,8 +155,7 @@ def run_reference(args, prob):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "KP-approx/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 -> assemble", "n": n,
-                   "egkb": egkb_cfg_kwargs() | {"tau": "1e300"}, "chosen_k": tr.chosen_k, "k_p": tr.k_p},
+        "config": bench_config(n), "result": trace_result(tr),
         "cpu_baseline": {"value": val, "unit": "KP-approx/s", "cores": cores, "kind": "port",
                          "sample": "full eGKB+assemble per step (oracle/lowrank.py restatement of lowrank.py:159-329 "
                                    "on the numpy structured R(A), MGS as the reference)"},
@@ -293,6 +310,43 @@ def run_ours(args, prob, rank, world, dist):
     if dist is not None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world / (float(e2e_t.item()) * 1e-3)
+    # e2e with the factors returned to host memory in the reference's layout
+    # (kronop.py:42-43: k C-ordered fp64 n x n arrays per side) -- 2 k n^2 x 8 bytes more
+    e2e_host_ms = []
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        blur_i = kb.RearrangedBlur(psf_host, n)
+        svd_i, tr_i = kb.egkb(blur_i, cfg)
+        op_i = kb.assemble(svd_i, scheme)
+        ax_h, ay_h = op_i.ax, op_i.ay
+        e2e_host_ms.append((time.perf_counter() - t0) * 1e3)
+        del ax_h, ay_h
+    host_fac_bytes = 2 * 8 * op_i.k * N
+
+    # ---- the reference-arithmetic engine (arithmetic="reference": the reference's own fp32
+    # operations -- OpenBLAS sdot of this host's numpy, sequential MGS): bit-identical
+    # trace and rank decision to the reference (tests/test_gpu_refarith.py)
+    ref_arith = kb.host_blas_arithmetic()
+    kb.egkb(blur, cfg, arithmetic=ref_arith)
+    torch.cuda.synchronize()
+    ra_ms = []
+    for i in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0_.record()
+        svd_r, tr_r = kb.egkb(blur, cfg, arithmetic=ref_arith)
+        kb.assemble(svd_r, scheme)
+        e1_.record()
+        torch.cuda.synchronize()
+        ra_ms.append(e0_.elapsed_time(e1_))
+    ref_arith_line = {"engine": f"egkb(arithmetic='reference') -> {ref_arith}", "ms_per_step": float(np.mean(ra_ms)),
+                      "value": world * 1e3 / float(np.mean(ra_ms)), "unit": "KP-approx/s",
+                      "result": trace_result(tr_r),
+                      "note": "trace, rank decision and Krylov bases bit-identical to the reference's fp32 run "
+                              "on this host's OpenBLAS sdot kernel; latency-bound by construction (each MGS "
+                              "coefficient is a sequential fp32 FMA chain of N/64 elements)"}
 
     # ---- standalone R(A) product (kb_op_apply): 50 products per CUDA-graph replay
     import ctypes as C
@@ -367,9 +421,11 @@ def run_ours(args, prob, rank, world, dist):
     e1.record()
     torch.cuda.synchronize()
     sb_ms = e0.elapsed_time(e1)
-    lib.kb_prof_enable(1)                      # profiled replay for the GEMM share
+    lib.kb_prof_enable(1)                      # profiled replay (one outer sweep) for the GEMM share
+    sb_cfg1 = kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=1,
+                          cgls=kb.CglsConfig(i_max=100, tau=1e-4))
     e0.record()
-    kb.sb_run(sb_op, b_dev, sb_cfg)
+    sb_res1 = kb.sb_run(sb_op, b_dev, sb_cfg1)
     e1.record()
     torch.cuda.synchronize()
     sb_prof_ms = e0.elapsed_time(e1)
@@ -415,7 +471,9 @@ def run_ours(args, prob, rank, world, dist):
             return kt * BK / (K * -(-N // BN))
         g_frac = 0.5 * (tile_frac(band[0], band[1]) + tile_frac(-band[1], -band[0]))
     g_exec = g_fl * (1.0 + g_frac) / 2.0
-    sb = {"variant": "isotropic", "k_terms": op.k,
+    cg1 = int(sum(sb_res1.cgls_iters))
+    sb = {"variant": "isotropic", "k_terms": op.k, "cgls": "CglsConfig(i_max=100, tau=1e-4)", "lam": 0.1150,
+          "beta": 0.0066,
           "parallelism": f"Kronecker terms sharded over {world} GPU(s), NCCL allreduce per product"
           if world > 1 else "single GPU", "outer_iters": sb_res.outer_iters, "cgls_iters": cg,
           "ms": sb_ms, "outer_it_per_s": sb_res.outer_iters / (sb_ms * 1e-3),
@@ -427,6 +485,7 @@ def run_ours(args, prob, rank, world, dist):
           "gemm_note": "G factors (v side) are banded Toeplitz for zero BC: the G-stage GEMM skips all-zero "
                        "k tiles (bit-identical); gemm_tflops counts executed flops",
           "gemm_share": g_ms / sb_prof_ms if sb_prof_ms else None, "vector_pass_ms": v_ms,
+          "gemm_profile": f"kernel classes from a profiled replay of one outer sweep ({cg1} CGLS iterations)",
           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_peak_src": "measured DMMA issue rate, tools/fp64_peak"}
     line = {
         "metric": METRIC, "value": value, "unit": "KP-approx/s", "n_gpus": world, "steps": args.steps,
@@ -435,11 +494,9 @@ def run_ours(args, prob, rank, world, dist):
                     "all": [round(float(t), 4) for t in step_ms]},
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[3] n=1024 fp32 eGKB rank 30+2 (matrix-free R(A)) -> assemble", "n": n,
-                   "egkb": {k: (str(v) if k == "tau" else v) for k, v in egkb_cfg_kwargs().items()},
-                   "chosen_k": tr.chosen_k, "k_p": tr.k_p, "stop_reason": tr.stop_reason,
-                   "breakdown": tr.breakdown, "parallelism": f"replicas x{world}",
-                   "l2": "flushed (512 MB write) before every timed step"},
+        "config": bench_config(n), "parallelism": f"replicas x{world}",
+        "result": trace_result(tr) | {"engine": "egkb(arithmetic='fast')"},
+        "reference_arithmetic": ref_arith_line,
         "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(dom), "launches": d_n,
                      "share_of_step": step_share, "peak_src": hbm_src,
@@ -450,12 +507,31 @@ def run_ours(args, prob, rank, world, dist):
         "sb": sb,
         "sweep": sweep,
         "e2e": {"value": e2e_value, "unit": "KP-approx/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
+                "result_location": "Kronecker factors device-resident (KroneckerSum on the GPU, consumed there "
+                                   "by sb_run); sigma and the trace read back to the host",
+                "host_factors": {"ms_per_step": float(np.mean(e2e_host_ms)),
+                                 "value": world * 1e3 / float(np.mean(e2e_host_ms)),
+                                 "d2h_bytes_per_step": int(d2h + host_fac_bytes),
+                                 "note": "same call plus op.ax / op.ay: the factors as host fp64 C-ordered "
+                                         "n x n arrays (kronop.py:42-43)"}},
         "gpu_launches": int(gpu_launches),
         "clocks": clk,
     }
+    # N1 (north_star target): the n=1024 approximation followed by the 200-iteration
+    # isotropic SB solve on its factors, end to end on the device
+    line["n1"] = {"approx_ms": ms_per_step, "sb_ms": sb_ms, "total_s": (ms_per_step + sb_ms) * 1e-3,
+                  "sb_outer_iters": sb_res.outer_iters, "cgls_iters_total": cg,
+                  "outer_it_per_s": sb_res.outer_iters / (sb_ms * 1e-3), "cgls_it_per_s": cg / (sb_ms * 1e-3),
+                  "final_rc": float(sb_res.rc_history[-1]) if sb_res.rc_history else None,
+                  "workload": f"egkb+assemble (k={op.k}) then sb_run isotropic, l_max={sb_res.outer_iters}, "
+                              "tau=0, CglsConfig(100, 1e-4), lam=0.1150, beta=0.0066"}
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(prob)
+        cpu = cpu_baseline(prob)
+        line["cpu_baseline"] = cpu
+        line["n1"]["cpu_extrapolated_s"] = cpu["egkb_s"] + cg * cpu["cgls_s_per_it"]
+        line["n1"]["cpu_note"] = ("EXTRAPOLATED: the port's measured eGKB time + the GPU run's CGLS iteration "
+                                  "count x the port's measured seconds per CGLS iteration (SURVEY §8d)")
     print(json.dumps(line))
 
 
@@ -478,7 +554,7 @@ def cpu_baseline(prob):
     from oracle import structured as ost
 
     n = prob.n
-    k32 = prob.psf.astype(np.float32)
+    k32 = psf_f32(prob.psf)
     cfg = SimpleNamespace(reorth=None, seed=0, break_tol=None, keep_basis=False, **egkb_cfg_kwargs())
     t0 = time.perf_counter()
     (u, s, v), tr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda x: ost.ra_rmatvec(k32, n, x),
@@ -495,7 +571,7 @@ def cpu_baseline(prob):
     return {"value": 1.0 / t_egkb, "unit": "KP-approx/s", "cores": os.cpu_count(), "kind": "port",
             "sample": "one full eGKB+assemble at n=1024 (oracle restatement, numpy structured R(A)); "
                       f"SB: 2 CGLS iterations of the k={s.size} augmented system",
-            "egkb_s": t_egkb, "cgls_it_per_s": 1.0 / t_cg, "chosen_k": tr.chosen_k}
+            "egkb_s": t_egkb, "cgls_s_per_it": t_cg, "cgls_it_per_s": 1.0 / t_cg, "result": trace_result(tr)}
 
 
 def main():
@@ -504,7 +580,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sb-outer", type=int, default=1)
+    ap.add_argument("--sb-outer", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()

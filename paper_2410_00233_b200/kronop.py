@@ -95,18 +95,20 @@ class KroneckerSum:
 
     @property
     def ax(self) -> list:
+        """Host factors A_x,i (m1 x n1, C order: kronop.py:42-43), transposed on the device
+        and read back in one copy."""
         if self._ax is None:
             s = self.scheme
-            f = self.f_dev.detach().cpu().numpy()
-            self._ax = [np.ascontiguousarray(f[i].reshape(s.n1, s.m1).T) for i in range(f.shape[0])]
+            f = self.f_dev.detach().view(-1, s.n1, s.m1).transpose(1, 2).contiguous().cpu().numpy()
+            self._ax = [f[i] for i in range(f.shape[0])]
         return self._ax
 
     @property
     def ay(self) -> list:
         if self._ay is None:
             s = self.scheme
-            g = self.g_dev.detach().cpu().numpy()
-            self._ay = [np.ascontiguousarray(g[i].reshape(s.n2, s.m2).T) for i in range(g.shape[0])]
+            g = self.g_dev.detach().view(-1, s.n2, s.m2).transpose(1, 2).contiguous().cpu().numpy()
+            self._ay = [g[i] for i in range(g.shape[0])]
         return self._ay
 
     @property
