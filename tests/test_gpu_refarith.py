@@ -77,10 +77,11 @@ def _assert_identical(svd, tr, os_, otr):
     assert np.all(np.abs(svd.sigma - ref) <= 1e-6 * ref[0]), (svd.sigma, ref)
 
 
-@pytest.mark.parametrize("name", ["n256", "n512", "n1024"])
+@pytest.mark.parametrize("name", ["n256", "n512", "n1024", "n2048"])
 def test_config_runs_bit_identical(kb, name):
-    """configs[1..3]: the automatic rank (n=256) and the fixed-rank runs that end in a
-    noise-floor breakdown (n=512: 20+2, n=1024: 30+2) take the reference's decisions."""
+    """configs[1..4]: the automatic rank (n=256, n=2048 with cap 50) and the fixed-rank
+    runs that end in a noise-floor breakdown (n=512: 20+2, n=1024: 30+2) take the
+    reference's decisions, with the reference's trace and bases bit for bit."""
     from paper_2410_00233_b200 import datagen
 
     prob = datagen.make_problem(name)
