@@ -9,7 +9,12 @@ ABI, stream-ordered on the current stream (NCCL over NVLink on a B200 box).
 All vector work stays replicated, so every rank holds the same iterate and
 makes the same stop decisions.
 
-The eGKB side runs as independent replicas in this round.
+The eGKB side is row-sharded (:func:`sharded_egkb`): each rank
+owns a contiguous block of image rows of every Krylov vector, K is replicated,
+and the per-half-step cross-shard sums (diagonal sums, reorthogonalisation
+coefficients, norms) are exact integer-limb partials combined by one int64
+sum-allreduce each -- so the recurrence is bit-identical for any shard count
+(``kb_egkb_shard.cu``).
 """
 
 from __future__ import annotations
@@ -119,3 +124,241 @@ class ShardedKroneckerSum:
         from .kronop import _forward_apply
 
         return _forward_apply(self.forward_struct(), y, 1, self.shape)
+
+
+# ----------------------------------------------------------------- row-sharded eGKB
+class _Shards:
+    """Which 8-row blocks of the n x n image each shard owns, and how partial limb
+    buffers are combined: in place by an int64 sum-allreduce over ``group`` (one
+    shard per rank), or -- ``simulate=G`` on one device -- by running all G shards'
+    kernels into the same buffer (limb additions are exact, so this IS the
+    allreduce's result)."""
+
+    def __init__(self, n, group=None, simulate=None):
+        import torch.distributed as dist
+
+        nblk = -(-n // 8)
+        if simulate:
+            self.world, self.mine, self.group = int(simulate), list(range(int(simulate))), None
+        else:
+            self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+            self.mine, self.group = [rank], group
+        self.ranges = []
+        for g in range(self.world):
+            lo, hi = shard_range(nblk, self.world, g)
+            self.ranges.append((min(8 * lo, n), min(8 * hi, n)))
+        self.simulated = bool(simulate)
+
+    def own(self):
+        return [self.ranges[g] for g in self.mine]
+
+    def allreduce(self, t):
+        import torch.distributed as dist
+
+        if not self.simulated and self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class CudaShardKernels:
+    """The per-shard steps of the sharded recurrence: ``kb_shard_*`` (kb_egkb_shard.cu) on
+    the current CUDA stream.  Every method takes torch tensors; integer limb buffers are
+    accumulated into (the caller zeroes them)."""
+
+    def __init__(self):
+        from . import device as D
+
+        self.lib = _lib.load()
+        self.device = D.device()
+        self._st = D.stream_ptr
+
+    def _check(self, rc, what):
+        _lib.check(rc, what)
+
+    def sqnorm(self, x, n, a0, a1, nl):
+        self._check(self.lib.kb_shard_sqnorm(x.data_ptr(), n, a0, a1, nl.data_ptr(), self._st()), "shard sqnorm")
+
+    def z(self, M, wl, z):
+        rows, cols = M.shape
+        self._check(self.lib.kb_shard_z(M.data_ptr(), rows, cols, wl.data_ptr(), z.data_ptr(), self._st()), "shard z")
+
+    def bcast_dots(self, z, n, c, length, beta, prev, B, m, a0, a1, v, dl):
+        self._check(self.lib.kb_shard_bcast_dots(z.data_ptr(), n, c, length, beta.data_ptr(),
+                                                 prev.data_ptr() if prev is not None else None, B.data_ptr(),
+                                                 B.shape[1], m, a0, a1, v.data_ptr(), dl.data_ptr(), self._st()),
+                    "shard dots")
+
+    def update(self, v, B, m, dl, n, a0, a1, nl, scal):
+        self._check(self.lib.kb_shard_update(v.data_ptr(), B.data_ptr(), B.shape[1], m, dl.data_ptr(), n, a0, a1,
+                                             nl.data_ptr(), scal.data_ptr(), self._st()), "shard update")
+
+    def normalize(self, src, nl, out, n, c, length, a0, a1, wl, scal):
+        self._check(self.lib.kb_shard_normalize(src.data_ptr(), nl.data_ptr(), out.data_ptr(), n, c, length, a0, a1,
+                                                wl.data_ptr(), scal.data_ptr(), self._st()), "shard normalize")
+
+    def lift(self, B, rows, W, out, off, ln):
+        """out[:, off:off+ln] = W[:rows].T @ B[:rows, off:off+ln] (kb_ts_lift on a row slice)."""
+        if ln == 0:
+            return
+        N = B.shape[1]
+        self._check(self.lib.kb_ts_lift(_lib.KB_F32, B.data_ptr() + 4 * off, N, rows, W.data_ptr(), W.shape[1],
+                                        out.data_ptr() + 4 * off, N, ln, self._st()), "shard lift")
+
+
+def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=None):
+    """eGKB (lowrank.py:159-329) with the Krylov vectors row-sharded across the ranks of
+    ``group`` (one GPU each), or across ``simulate`` virtual shards on one device.
+
+    Same trace semantics, breakdown tests and nu rule as :func:`egkb`; the arithmetic is
+    the sharded engine's own (per-chunk fp64 partials, exact integer combination), so the
+    result does not depend on the number of shards.  fp32, zero-BC ``RearrangedBlur``.
+    Returns ``(TruncatedSvd, EgkbTrace)`` with the singular vectors on every rank.
+    ``kernels`` replaces the CUDA shard steps (tests drive this host loop and its
+    allreduce protocol with a host implementation over gloo).
+    """
+    import numpy as np
+
+    from . import rng
+    from .blurmodel import BC_ZERO, RearrangedBlur
+    from .exceptions import NumericalError, ValidationError
+    from .linalg import TruncatedSvd
+    from .lowrank import EgkbTrace, eps_for
+
+    if not isinstance(b_mat, RearrangedBlur) or b_mat.bc != BC_ZERO or b_mat.dtype != np.float32:
+        raise ValidationError("sharded_egkb needs a float32 zero-BC RearrangedBlur")
+    kern = kernels if kernels is not None else CudaShardKernels()
+    dev = kern.device
+    n = b_mat.n
+    N = n * n
+    kh, kw = b_mat.psf.shape
+    cu, cv = kh // 2, kw // 2
+    if kernels is None:
+        K, Kt = b_mat._device_kernels()
+    else:
+        k32 = torch.from_numpy((b_mat.psf.kernel).astype(np.float32))
+        K, Kt = k32.to(dev), k32.t().contiguous().to(dev)
+    sh = _Shards(n, group, simulate)
+    tol = config.break_tol if config.break_tol is not None else float(np.sqrt(eps_for(np.float32)))
+    cap = max(config.k_max, config.k_min) + config.p + 3
+    S = torch.zeros((cap, N), dtype=torch.float32, device=dev)
+    Q = torch.zeros((cap, N), dtype=torch.float32, device=dev)
+    v = torch.zeros((N,), dtype=torch.float32, device=dev)
+    z = torch.zeros(max(kh, kw) + 8, dtype=torch.float64, device=dev)
+    wl = torch.zeros(3 * (max(kh, kw) + 8), dtype=torch.int64, device=dev)
+    dl = torch.zeros(3 * (cap + 3), dtype=torch.int64, device=dev)
+    nl = torch.zeros(3, dtype=torch.int64, device=dev)
+    scal = torch.zeros(4, dtype=torch.float64, device=dev)
+    beta = torch.zeros(1, dtype=torch.float64, device=dev)
+    hist = torch.zeros((2 * cap + 2, 2), dtype=torch.float64, device=dev)
+    if y0 is None:
+        y0d = rng.standard_normal(config.seed, N, np.float32)
+    elif isinstance(y0, torch.Tensor):
+        y0d = y0.to(device=dev, dtype=torch.float32).reshape(-1)
+    else:
+        y0d = torch.from_numpy(np.ascontiguousarray(y0, dtype=np.float32)).to(dev).reshape(-1)
+    if tuple(y0d.shape) != (N,):
+        raise ValidationError(f"y0 must have length {N}, got shape {tuple(y0d.shape)}")
+
+    def normalize(src, out, c_next, len_next):
+        """t = |src| (allreduced limbs in nl) -> out = fl(src / t), next product's diagonal limbs."""
+        wl.zero_()
+        for a0, a1 in sh.own():
+            kern.normalize(src, nl, out, n, c_next, len_next, a0, a1, wl, scal)
+        sh.allreduce(wl)
+
+    def half(M, c_b, len_b, prev, B, m, out, c_next, len_next, slot):
+        """One half step (R q or R^T s): z from the all-reduced diagonal limbs; y, v = y - beta prev
+        and the limbs of B^T v, |v|^2, |y|^2; v1 = v - B h and the limbs of |v1|^2; out = v1 / t
+        and the next product's diagonal limbs.  (t or alpha, |y|) land in hist[slot]."""
+        kern.z(M, wl, z)
+        dl.zero_()
+        for a0, a1 in sh.own():
+            kern.bcast_dots(z, n, c_b, len_b, beta, prev, B, m, a0, a1, v, dl)
+        sh.allreduce(dl[: 3 * (m + 2)])
+        nl.zero_()
+        for a0, a1 in sh.own():
+            kern.update(v, B, m, dl, n, a0, a1, nl, scal)
+        sh.allreduce(nl)
+        normalize(v, out, c_next, len_next)
+        hist[slot].copy_(scal[:2])
+        beta.copy_(scal[:1])
+
+    # s1 = y0 / |y0|, diagonal limbs for R^T s1 (lowrank.py:207-210)
+    nl.zero_()
+    for a0, a1 in sh.own():
+        kern.sqnorm(y0d, n, a0, a1, nl)
+    sh.allreduce(nl)
+    normalize(y0d, S[0], cv, kw)
+    hist[0].copy_(scal[:2])
+    # q1 = R^T s1 / alpha1 (lowrank.py:211-215): no previous vector, no projection
+    half(Kt, cu, kh, None, Q, 0, Q[0], cu, kh, 1)
+    h = hist[:2].cpu().numpy()
+    t1, a1 = float(h[0, 0]), float(h[1, 0])
+    if t1 == 0.0:
+        raise ValidationError("starting vector must be nonzero")
+    if a1 == 0.0:
+        raise NumericalError("operator annihilates the starting vector")
+    trace = EgkbTrace()
+    trace.alphas, trace.ts, trace.zetas, trace.nus = [a1], [t1], [a1 * t1], [1e308]
+    fired, reason, done = None, "", 1
+    broke = t_break = False
+    while done < ((fired + config.p + 1) if fired is not None else (config.k_max + 1)):
+        if done + 1 > cap:
+            raise NumericalError("eGKB basis capacity exhausted")
+        slot = 2 * done
+        # s step: u = R q_j, s_raw = u - alpha s_j, projected against S (lowrank.py:238-247)
+        half(K, cv, kw, S[done - 1], S, done if config.reorth != "one-sided" else 0, S[done], cv, kw, slot)
+        # q step: R^T s_{j+1} - t q_j, projected against Q (lowrank.py:250-260)
+        half(Kt, cu, kh, Q[done - 1], Q, done, Q[done], cu, kh, slot + 1)
+        h = hist[slot:slot + 2].cpu().numpy()
+        t_new, u_norm, a_new, pre = float(h[0, 0]), float(h[0, 1]), float(h[1, 0]), float(h[1, 1])
+        if t_new <= tol * u_norm:
+            broke = t_break = True
+            break
+        if a_new <= tol * pre:
+            broke = True
+            trace.ts.append(t_new)
+            break
+        trace.ts.append(t_new)
+        trace.alphas.append(a_new)
+        zeta = a_new * t_new
+        nu = float(np.sqrt(zeta * trace.zetas[-1]))
+        trace.zetas.append(zeta)
+        trace.nus.append(nu)
+        done += 1
+        if fired is None:
+            if nu > trace.nus[-2]:
+                fired, reason = max(done - 1, config.k_min), "nu_rose"
+            elif nu < config.tau:
+                fired, reason = max(done, config.k_min), "nu_below_tol"
+    if broke:
+        k_p, rows = done, (done if t_break else done + 1)
+    else:
+        k_p, rows = done - 1, done
+    if fired is not None:
+        chosen = min(fired, k_p)
+    elif broke:
+        chosen, reason = k_p, "breakdown"
+    else:
+        chosen, reason = min(config.k_max, k_p), "hit_kmax"
+    if chosen < 1 or k_p < 1:
+        raise NumericalError("bidiagonalization broke down before producing any factors")
+    c_mat = np.zeros((rows, k_p))
+    for i in range(k_p):
+        c_mat[i, i] = np.float32(trace.alphas[i])
+        if i + 1 < rows:
+            c_mat[i + 1, i] = np.float32(trace.ts[i + 1])
+    uc, sc, vct = np.linalg.svd(c_mat, full_matrices=False)
+    sigma = sc[:chosen].astype(np.float32).astype(np.float64)
+    # lift on the own rows (lowrank.py:317-318), then the rows of the other ranks
+    out_u = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
+    out_v = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
+    wu = torch.from_numpy(np.ascontiguousarray(uc[:, :chosen], dtype=np.float32)).to(dev)
+    wv = torch.from_numpy(np.ascontiguousarray(vct.T[:, :chosen], dtype=np.float32)).to(dev)
+    for a0, a1 in sh.own():
+        kern.lift(S, rows, wu, out_u, a0 * n, (a1 - a0) * n)
+        kern.lift(Q, k_p, wv, out_v, a0 * n, (a1 - a0) * n)
+    sh.allreduce(out_u)   # zeros outside each rank's rows: the sum is the concatenation
+    sh.allreduce(out_v)
+    trace.chosen_k, trace.k_p, trace.stop_reason, trace.breakdown = chosen, k_p, reason, broke
+    return TruncatedSvd.from_device(out_u, sigma.astype(np.float32), out_v), trace
