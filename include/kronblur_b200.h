@@ -275,6 +275,10 @@ typedef struct {
     const double* f;  /* k x n1 x m1: F_i = ax_i^T = reshape(sigma_i u_i, (n1, m1)) */
     const double* g;  /* k x n2 x m2: G_i = ay_i^T = reshape(v_i, (n2, m2))         */
     const int* band;  /* optional device int[2] from kb_kron_band (NULL: dense G)    */
+    const double* ft; /* optional k x m1 x n1: Ft_i = F_i^T.  With it the reduced
+                       * stage of the transposed apply is one dense GEMM, like the
+                       * forward one's (both then run on cuBLAS DGEMM, the faster
+                       * library kernel for these dense shapes; NULL: DMMA k_dgemm). */
 } kb_kron;
 
 /* band[0..1] = min/max of (c - r) over the nonzero entries G_i[r][c] of all

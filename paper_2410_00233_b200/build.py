@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
     with ThreadPoolExecutor(max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
         objs = list(ex.map(compile_one, sources()))
-    cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", OUT + ".tmp", *objs]
+    cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", OUT + ".tmp", *objs, "-lcublas"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cublas_v2.h>
+
 #include "kb_common.cuh"
 
 namespace kb {
@@ -361,3 +363,53 @@ void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, in
 
 }  // namespace kb
 
+
+namespace kb {
+// ---- the dense reduced stage of the Kronecker apply on cuBLAS DGEMM --------------
+// Y (r x c, row-major) = sum_{i < nblk} Bl_i^T P_i, Bl_i (kin x r) and P_i (kin x c)
+// contiguous row-major blocks: ONE GEMM with inner dimension nblk * kin.  cuBLAS
+// (35 TF/s on these shapes, profiles/gemm_cublas_r02.txt) beats our DMMA split-K
+// kernel (25 TF/s) here; the banded G stage stays on k_dgemm, which skips the
+// all-zero tiles cuBLAS would multiply.  Column-major view: Y^T = P^T Bl.
+namespace {
+struct Cublas {
+    cublasHandle_t h = nullptr;
+    void* ws = nullptr;
+};
+Cublas& cublas_state() {
+    static thread_local Cublas c[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return c[dev & 15];
+}
+}  // namespace
+
+void cublas_prepare() {
+    Cublas& c = cublas_state();
+    if (c.h) return;
+    if (cublasCreate(&c.h) != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasCreate failed");
+        throw Fail{KB_ERUNTIME};
+    }
+    constexpr size_t WS = 32u << 20;
+    KB_CUDA(cudaMalloc(&c.ws, WS));
+    cublasSetWorkspace(c.h, c.ws, WS);
+    cublasSetMathMode(c.h, CUBLAS_DEFAULT_MATH);
+}
+
+void dgemm_sum_blocks(int r, int c, int kin, int nblk, const double* Bl, const double* P, double* Y,
+                      cudaStream_t st) {
+    cublas_prepare();
+    Cublas& cb = cublas_state();
+    cublasSetStream(cb.h, st);
+    const double one = 1.0, zero = 0.0;
+    const int64_t K = (int64_t)kin * nblk;
+    KB_REQUIRE(K < (1ll << 31), "dgemm_sum_blocks: inner dimension too large");
+    ProfScope ps(st, PROF_DGEMM, 8.0 * ((double)K * (r + c) + (double)r * c), 2.0 * r * (double)c * (double)K);
+    const cublasStatus_t e = cublasDgemm(cb.h, CUBLAS_OP_N, CUBLAS_OP_T, c, r, (int)K, &one, P, c, Bl, r, &zero, Y, c);
+    if (e != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasDgemm failed (%d)", (int)e);
+        throw Fail{KB_ERUNTIME};
+    }
+}
+}  // namespace kb

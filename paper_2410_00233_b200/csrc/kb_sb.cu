@@ -325,6 +325,16 @@ size_t kron_ws_doubles(const kb_kron* kr) {
     return (size_t)kr->k * (size_t)std::max(a, b) + (size_t)KRON_SPLIT_MAX * out + 64;
 }
 
+void dgemm_sum_blocks(int r, int c, int kin, int nblk, const double* Bl, const double* P, double* Y,
+                      cudaStream_t st);
+
+// The dense reduced stage runs on cuBLAS for large images (where the GEMM, not launch
+// latency, bounds a CGLS iteration); such solves run the eager CGLS loop, since cuBLAS
+// launches cannot live inside a conditional-while graph body.
+static bool kron_uses_cublas(const kb_kron* kr) {
+    return kr->ft != nullptr && std::min(kr->m1, kr->n1) >= 512 && std::min(kr->m2, kr->n2) >= 512;
+}
+
 void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, double* tmp,
                 cudaStream_t st) {
     const int m1 = kr->m1, m2 = kr->m2, n1 = kr->n1, n2 = kr->n2, k = kr->k;
@@ -340,17 +350,23 @@ void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, do
         dgemm(0, 0, n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
               (int64_t)n1 * m2, k, 1, 0.0, st);
         g_dgemm_skip = GemmSkip{};
-        // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1
-        dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
-              0, 1, k, 0.0, st, part, part_n);
+        // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1: one dense GEMM, inner dim k n1
+        if (kron_uses_cublas(kr))
+            dgemm_sum_blocks(m1, m2, n1, k, kr->f, tmp, y, st);
+        else
+            dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
+                  0, 1, k, 0.0, st, part, part_n);
     } else {
         // Q_i = Yr G_i^T          (m1 x n2), Yr = y as m1 x m2
         dgemm(0, 1, m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
               (int64_t)m1 * n2, k, 1, 0.0, st);
         g_dgemm_skip = GemmSkip{};
-        // Xr = sum_i F_i Q_i      (n1 x n2)
-        dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
-              0, 1, k, 0.0, st, part, part_n);
+        // Xr = sum_i F_i Q_i      (n1 x n2) = sum_i Ft_i^T Q_i with Ft_i = F_i^T (m1 x n1)
+        if (kron_uses_cublas(kr))
+            dgemm_sum_blocks(n1, n2, m1, k, kr->ft, tmp, y, st);
+        else
+            dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
+                  0, 1, k, 0.0, st, part, part_n);
     }
 }
 
@@ -668,7 +684,8 @@ static void cgls_core(const kb_forward* fw, const double* b, const double* x0, d
     KB_REQUIRE(st->i_max <= w.i_cap, "i_max %d exceeds the CGLS workspace capacity %d", st->i_max, w.i_cap);
     static const bool force_eager = std::getenv("KB_CGLS_EAGER") != nullptr;
     int* hh = reinterpret_cast<int*>(hs);
-    if (!g_prof && !force_eager && fw->allreduce == nullptr) {
+    const bool cublas_stage = fw->kind == KB_FWD_KRON && kron_uses_cublas(&fw->kron);
+    if (!g_prof && !force_eager && fw->allreduce == nullptr && !cublas_stage) {
         CglsKey key;
         std::memset(&key, 0, sizeof(key));
         key.fw = *fw;

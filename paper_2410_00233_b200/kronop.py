@@ -83,6 +83,7 @@ class KroneckerSum:
         self.f_dev = D.to_device(f)
         self.g_dev = D.to_device(g)
         self._band = None
+        self._ft = None
 
     @classmethod
     def from_device(cls, f_dev, g_dev, scheme: BlockScheme) -> "KroneckerSum":
@@ -91,6 +92,7 @@ class KroneckerSum:
         obj._ax = obj._ay = None
         obj.f_dev, obj.g_dev = f_dev, g_dev
         obj._band = None
+        obj._ft = None
         return obj
 
     @property
@@ -133,6 +135,12 @@ class KroneckerSum:
             _lib.check(_lib.load().kb_kron_band(C.byref(kr), band.data_ptr(), D.stream_ptr()), "kron band")
             self._band = band
         kr.band = self._band.data_ptr()
+        if self._ft is None:
+            # F_i^T blocks (device transpose, once per operator): the reduced stage of the
+            # transposed apply becomes one dense GEMM as well
+            s = self.scheme
+            self._ft = self.f_dev.view(-1, s.n1, s.m1).transpose(1, 2).contiguous()
+        kr.ft = self._ft.data_ptr()
         return kr
 
     def forward_struct(self) -> _lib.KbForward:
