@@ -7,8 +7,11 @@ a matrix-free :class:`~paper_2410_00233_b200.blurmodel.RearrangedBlur`.
 
 Division of labour (north star item 2): the Krylov loop, the operator
 products, the full reorthogonalisation and the lifts run in sm_100a kernels
-(``kb_egkb_run``, ``kb_ts_lift``); the bidiagonal SVD of C and the rank rule
-stay on the host, in the reference's own numpy/LAPACK call.
+(``kb_egkb_run``, ``kb_lift_assemble``).  The bidiagonal SVD of C runs on the
+host, in C++ inside ``kb_egkb_run`` (fp64 one-sided Jacobi), and its lift
+weights go to the device stream-ordered.  The rank rule and the breakdown
+tests run on the device inside the fused kernel (the same fp64 scalar
+comparisons in every CTA), or on the host in the reference-arithmetic engine.
 """
 
 from __future__ import annotations
@@ -364,7 +367,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1, *, arithmet
     st.nus_host = hist[3].ctypes.data_as(dp)
     st.s_scale_host = hist[4].ctypes.data_as(dp)
     st.q_scale_host = hist[5].ctypes.data_as(dp)
-    # the small SVD of C and the lift weights are computed on the device right after the
+    # the small SVD of C (host, C++ Jacobi) and the lift weights are uploaded right after the
     # loop (kb_egkb_state.wu_dev): W_u, W_v (working dtype) and sigma (fp64) in one buffer
     esz = np.dtype(dtype).itemsize
     wbytes = (cap * cap * esz + 15) // 16 * 16
