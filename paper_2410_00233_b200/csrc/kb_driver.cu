@@ -376,13 +376,14 @@ static void svd_c_upload(int dtype, const double* alphas, const double* ts, int 
         const double sv = sig[j];
         ps[c] = dtype == KB_F32 ? (double)(float)sv : sv;
         st->sigma_host[c] = ps[c];
+        // lift weights for the STORED basis vectors: basis i is stored as (normalised_i / scale_i)
         for (int i = 0; i < rows; ++i) {
-            const double u = sv > 0.0 ? A[(size_t)j * rows + i] / sv : 0.0;
+            const double u = (sv > 0.0 ? A[(size_t)j * rows + i] / sv : 0.0) * (st->s_scale_host ? st->s_scale_host[i] : 1.0);
             if (dtype == KB_F32) reinterpret_cast<float*>(pu)[(size_t)i * chosen + c] = (float)u;
             else reinterpret_cast<double*>(pu)[(size_t)i * chosen + c] = u;
         }
         for (int i = 0; i < k; ++i) {
-            const double w = V[(size_t)j * k + i];
+            const double w = V[(size_t)j * k + i] * (st->q_scale_host ? st->q_scale_host[i] : 1.0);
             if (dtype == KB_F32) reinterpret_cast<float*>(pv)[(size_t)i * chosen + c] = (float)w;
             else reinterpret_cast<double*>(pv)[(size_t)i * chosen + c] = w;
         }
@@ -613,6 +614,8 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
         const int na = (int)o.alphas.size(), nt = (int)o.ts.size(), nn = (int)o.nus.size();
         o.alphas.resize(std::max<size_t>(o.alphas.size(), (size_t)rows + 1), 0.0);
         o.ts.resize(std::max<size_t>(o.ts.size(), (size_t)rows + 1), 0.0);
+        if (st->s_scale_host && st->q_scale_host)   // normalised vectors stored: unit scales (before the lift weights)
+            for (int i = 0; i < cap; ++i) st->s_scale_host[i] = st->q_scale_host[i] = 1.0;
         if (st->wu_dev) {
             KB_REQUIRE(st->wv_dev && st->sigma_dev && st->sigma_host, "SVD outputs incomplete");
             svd_c_upload(op->dtype, o.alphas.data(), o.ts.data(), rows, k_p, chosen, st, s);
@@ -624,8 +627,6 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
         std::copy(o.ts.begin(), o.ts.begin() + st->n_ts, st->ts_host);
         std::copy(o.zetas.begin(), o.zetas.end(), st->zetas_host);
         std::copy(o.nus.begin(), o.nus.end(), st->nus_host);
-        if (st->s_scale_host && st->q_scale_host)
-            for (int i = 0; i < cap; ++i) st->s_scale_host[i] = st->q_scale_host[i] = 1.0;
         st->chosen_k = chosen;
         st->k_p = k_p;
         st->rows = rows;

@@ -408,8 +408,12 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1, *, arithmet
             c_mat[i, i] = trace.alphas[i]
             if i + 1 < rows:
                 c_mat[i + 1, i] = trace.ts[i + 1]
-        trace.s_basis = D.to_host(s_basis[:rows]).T.astype(dtype)
-        trace.q_basis = D.to_host(q_basis[:k_p]).T.astype(dtype)
+        # stored vectors x scale = the normalised basis (the fused engine defers the division)
+        sc_s, sc_q = hist[4, :rows], hist[5, :k_p]
+        sb = D.to_host(s_basis[:rows]).T
+        qb = D.to_host(q_basis[:k_p]).T
+        trace.s_basis = sb if np.all(sc_s == 1.0) else (sb.astype(np.float64) * sc_s).astype(dtype)
+        trace.q_basis = qb if np.all(sc_q == 1.0) else (qb.astype(np.float64) * sc_q).astype(dtype)
         trace.c_mat = c_mat
     return TruncatedSvd.from_lift(lazy, sigma.astype(dtype)), trace
 
