@@ -210,6 +210,57 @@ def sweep_bench(kb, D):
             "kernel": "kb_sb_run_batch (stacked DMMA GEMMs, one launch per pass over all lambdas)"}
 
 
+def other_configs(kb, D, flush):
+    """configs[2] (n=512, fixed 20+2) and configs[4] (n=2048, automatic rank, cap 50): one
+    approximation per engine (fast and reference arithmetic), device time with the PSF
+    resident and L2 flushed, plus one CGLS iteration rate on the fast engine's factors
+    (configs[2]: both SB variants; configs[4]: anisotropic)."""
+    import torch
+
+    from paper_2410_00233_b200 import datagen
+
+    out = {}
+    for name in ("n512", "n2048"):
+        prob = datagen.make_problem(name)
+        blur = kb.RearrangedBlur(prob.psf, prob.n)
+        cfg = kb.EgkbConfig(**prob.egkb)
+        rec = {"n": prob.n, "egkb": {k: (str(v) if k == "tau" else v) for k, v in prob.egkb.items()}}
+        for arith in ("fast", kb.host_blas_arithmetic()):
+            kb.egkb(blur, cfg, arithmetic=arith)
+            ms = []
+            for _ in range(3):
+                flush.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                svd, tr = kb.egkb(blur, cfg, arithmetic=arith)
+                op = kb.assemble(svd, kb.BlockScheme.square_image(prob.n))
+                e1.record()
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            rec["fast" if arith == "fast" else "reference_arithmetic"] = {
+                "ms": float(np.median(ms)), "result": trace_result(tr)}
+            if arith == "fast":
+                fop = op
+        variants = ["isotropic", "anisotropic"] if name == "n512" else ["anisotropic"]
+        b_dev = D.to_device(prob.b)
+        for var in variants:
+            c = kb.SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=var, tau=0.0, l_max=1,
+                            cgls=kb.CglsConfig(i_max=100, tau=1e-4))
+            kb.sb_run(fop, b_dev, c)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = kb.sb_run(fop, b_dev, c)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            rec[f"sb_{var}"] = {"k_terms": fop.k, "outer_it_ms": t, "cgls_iters": int(sum(r.cgls_iters)),
+                                "cgls_it_per_s": sum(r.cgls_iters) / (t * 1e-3)}
+        out[name] = rec
+    return out
+
+
 def run_ours(args, prob, rank, world, dist):
     import torch
 
@@ -433,6 +484,7 @@ def run_ours(args, prob, rank, world, dist):
     v_ms, v_n, _, _ = prof_read(lib, 4)
     lib.kb_prof_enable(0)
     sweep = sweep_bench(kb, D) if not args.no_sweep else None
+    others = other_configs(kb, D, flush) if not args.no_sweep else None
     clk = clocks.stop() if clocks is not None else None
     if rank != 0:
         return
@@ -506,6 +558,7 @@ def run_ours(args, prob, rank, world, dist):
         "ra_matvec": ra,
         "sb": sb,
         "sweep": sweep,
+        "other_configs": others,
         "e2e": {"value": e2e_value, "unit": "KP-approx/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
                 "result_location": "Kronecker factors device-resident (KroneckerSum on the GPU, consumed there "

@@ -211,6 +211,36 @@ int kb_egkb_workspace_bytes(const kb_operator* op, int capacity, size_t* bytes);
 int kb_sdot_openblas(int lanes, const float* x, const float* y, int64_t n, float* out_dev,
                      void* ws, size_t ws_bytes, kb_stream_t stream);
 
+/* ------------------------------------------------------------------ */
+/* Row-sharded eGKB steps (driven by parallel.sharded_egkb) */
+/* ------------------------------------------------------------------ */
+/* Vectors of length n^2 (index a*n + b), this shard owning image rows
+ * [a0, a1) (a0 a multiple of 8).  Every cross-shard sum is accumulated as
+ * three int64 limbs (weights 2^1, 2^-39, 2^-79) of per-chunk fp64 partials --
+ * exact, so the callers' int64 sum-allreduce of the limb buffers gives a
+ * result independent of the number of shards.  Limb buffers are added to
+ * (zero them first).  lowrank.py:207-260 restated over the shards:
+ *   |x|^2 of the own rows (lowrank.py:207) */
+int kb_shard_sqnorm(const float* x, int n, int a0, int a1, long long* norm_limbs, kb_stream_t stream);
+/* diagonal sums of x over the own rows (the input side of an R(A) product) */
+int kb_shard_diag(const float* x, int n, int c, int len, int a0, int a1, long long* limbs, kb_stream_t stream);
+/* z[o] = sum_i M[i][o] w[i] from the all-reduced diagonal limbs (M = K or K^T, rows x cols) */
+int kb_shard_z(const float* M, int rows, int cols, const long long* w_limbs, double* z, kb_stream_t stream);
+/* y = P z on the own rows, v = y - beta*prev (prev may be NULL), limbs of B_i . v (i < m),
+ * |v|^2 and |y|^2 (3 (m + 2) limbs) */
+int kb_shard_bcast_dots(const double* z, int n, int c, int len, const double* beta_dev, const float* prev,
+                        const float* B, int64_t ld, int m, int a0, int a1, float* v, long long* limbs,
+                        kb_stream_t stream);
+/* v1 = v - sum_i h_i B_i (h from the all-reduced dot limbs), limbs of |v1|^2; scal[1] = |y| */
+int kb_shard_update(float* v, const float* B, int64_t ld, int m, const long long* dot_limbs, int n, int a0,
+                    int a1, long long* norm_limbs, double* scal, kb_stream_t stream);
+/* t = |v1| (scal[0]), out = fl(v1 / t) on the own rows, and the diagonal limbs of out for the
+ * next product (centre c, length len; diag_limbs may be NULL) */
+int kb_shard_normalize(const float* v, const long long* norm_limbs, float* out, int n, int c, int len, int a0,
+                       int a1, long long* diag_limbs, double* scal, kb_stream_t stream);
+/* host decode of three limbs (the device's own formula) */
+double kb_shard_limbs_value(const long long* limbs_host);
+
 /* dst = (dtype)(src / divisor), device: the Psf normalisation k / k.sum()
  * (blurmodel.py:25-65) fused with the working-precision cast -- bitwise
  * numpy's (k / total).astype(dtype). */

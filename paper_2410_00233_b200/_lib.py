@@ -115,6 +115,7 @@ _SIGS = {
     "kb_shard_update": (C.c_int, [vp, vp, i64, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
     "kb_shard_normalize": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
     "kb_shard_sqnorm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp]),
+    "kb_shard_limbs_value": (C.c_double, [vp]),
     "kb_egkb_workspace_bytes": (C.c_int, [P(KbOperator), C.c_int, P(SZ)]),
     "kb_transpose": (C.c_int, [C.c_int, vp, i64, i64, vp, vp]),
     "kb_div_cast": (C.c_int, [vp, C.c_double, C.c_int, vp, i64, vp]),

@@ -45,11 +45,28 @@ _SCAN_MIN = 1 << 16
 _HOST_THREADS = max(1, min(16, os.cpu_count() or 1))
 
 
+# Recycled private-copy buffers (by shape): a fresh 8 MB array per Psf would pay its
+# page faults on every construction; a Psf returns its copy here when it is dropped.
+_RAW_POOL: dict = {}
+_RAW_POOL_MAX = 2
+
+
+def _raw_take(shape) -> np.ndarray:
+    lst = _RAW_POOL.get(shape)
+    return lst.pop() if lst else np.empty(shape, dtype=np.float64)
+
+
+def _raw_give(arr: np.ndarray) -> None:
+    lst = _RAW_POOL.setdefault(arr.shape, [])
+    if len(lst) < _RAW_POOL_MAX:
+        lst.append(arr)
+
+
 def _scan(k: np.ndarray) -> tuple[float, np.float64, np.ndarray]:
     """min, numpy-exact sum and a private copy of ``k`` in one multithreaded pass."""
     lib = _lib.load()
     total, kmin = C.c_double(), C.c_double()
-    own = np.empty_like(k, order="C")
+    own = _raw_take(k.shape)
     _lib.check(lib.kb_psf_scan(k.ctypes.data, k.size, _HOST_THREADS, C.byref(total), C.byref(kmin),
                                own.ctypes.data), "kb_psf_scan")
     return kmin.value, np.float64(total.value), own
@@ -65,7 +82,7 @@ class Psf:
     copy.  The normalised float64 ``kernel`` is materialised on first access.
     """
 
-    __slots__ = ("_raw", "_total", "_kernel")
+    __slots__ = ("_raw", "_total", "_kernel", "_pooled")
 
     def __init__(self, kernel):
         k = np.asarray(kernel, dtype=np.float64)
@@ -73,12 +90,16 @@ class Psf:
             raise ValidationError("PSF kernel must be 2-D")
         if k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
             raise ValidationError(f"PSF support must be odd in both dimensions, got {k.shape}")
+        self._raw = None
+        self._pooled = False
         if k.size >= _SCAN_MIN and k.flags.c_contiguous:
             # min, numpy's pairwise sum and the private copy in one multithreaded host pass
             # (kb_psf_scan: bit-identical to k.sum(), which is single-threaded)
-            kmin, total, k = _scan(k)
-            if not kmin >= 0 and np.any(k < 0):
+            kmin, total, own = _scan(k)
+            if not kmin >= 0 and np.any(own < 0):
+                _raw_give(own)
                 raise ValidationError("PSF kernel must be non-negative")
+            k, self._pooled = own, True
         else:
             k = np.array(k)                           # the reference's private order-'K' copy
             if k.size == 0 or not _min(k) >= 0:      # one reduction; the exact test only when it fails
@@ -86,13 +107,21 @@ class Psf:
                     raise ValidationError("PSF kernel must be non-negative")
             total = k.sum()
         if total <= 0:
+            if self._pooled:
+                _raw_give(k)
             raise ValidationError("PSF kernel must have positive mass")
         self._raw, self._total, self._kernel = k, total, None
+
+    def __del__(self):
+        if getattr(self, "_pooled", False) and self._raw is not None:
+            _raw_give(self._raw)
 
     @property
     def kernel(self) -> np.ndarray:
         if self._kernel is None:
             self._kernel = self._raw / self._total     # bitwise the reference's k / total
+            if self._pooled:
+                _raw_give(self._raw)
             self._raw = None
         return self._kernel
 

@@ -95,3 +95,20 @@ def test_world2_gloo_matches_single_shard():
         assert (k_p, chosen) == (ref[0].k_p, ref[0].chosen_k)
         assert s == ref[1].tolist()
         assert abs(usum - float(np.abs(ref[2]).sum())) < 1e-3
+
+
+def test_limb_decode_matches_the_library():
+    """kb_shard_limbs_value (the device formula, host-callable) decodes like the host helper,
+    and to_limbs / from_limbs round-trip values to 2^-79."""
+    import ctypes
+
+    from paper_2410_00233_b200 import _lib
+    from shard_host_kernels import from_limbs, to_limbs
+
+    lib = _lib.load()
+    rng = np.random.default_rng(1)
+    for x in np.concatenate([rng.standard_normal(50) * 10.0 ** rng.uniform(-20, 10, 50), [0.0, 1.0, -3.5]]):
+        limbs = to_limbs(x)
+        assert abs(from_limbs(*limbs) - x) <= 2.0 ** -78 + 1e-15 * abs(x)
+        arr = (ctypes.c_longlong * 3)(*[int(v) for v in limbs])
+        assert lib.kb_shard_limbs_value(arr) == from_limbs(*limbs)
