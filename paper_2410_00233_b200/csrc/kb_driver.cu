@@ -767,16 +767,17 @@ static void egkb_run(const kb_operator* op, const kb_egkb_config* cfg, const voi
     st->stop_reason = reason;
     st->breakdown = breakdown ? 1 : 0;
     if (pk_done && g_prof) {
-        // algorithmic bytes of the run actually executed (eGKB row):
-        // per iteration two R(A) products, and per side one coefficient pass + one
-        // update pass over the basis, the prev vector and the written vector.
+        // algorithmic bytes of the run actually executed, SURVEY §8d's eGKB row without
+        // the lift: B_egkb = (2 J + 1) B_mv + sum_{j=1..J} 8 N (2 j + 3) over the J executed
+        // iterations -- per iteration two R(A) products and, per side, the coefficient and
+        // update passes over the j basis vectors plus the prev, raw and written vectors.
         const double N = (double)op->rows, e = (double)esz;
         const double bmv = e * (2.0 * N + (double)op->kh * op->kw);
-        double by = 2.0 * e * N + bmv + 2.0 * e * N;   // init: s1, q1
+        double by = bmv;   // the initial product R^T s1
         for (int j = 1; j < done + (breakdown ? 1 : 0); ++j) {
             const double ms = cfg->full_reorth ? j : 0, mq = j;
             by += 2.0 * bmv;
-            by += e * N * (2.0 * ms + 2.0) + e * N * (2.0 * mq + 2.0);
+            by += e * N * (2.0 * ms + 3.0) + e * N * (2.0 * mq + 3.0);
         }
         prof_set_last_bytes(by);
     }
