@@ -112,3 +112,16 @@ def test_either_kernel_bit_identical(kb, kernel, n, seed):
     psf = datagen.mixture_psf(n, seed=seed)
     svd, tr, os_, otr = _run_pair(kb, psf, n, dict(k_max=20, k_min=20, p=2, tau=1e300), kernel, kernel=kernel)
     _assert_identical(svd, tr, os_, otr)
+
+
+def test_estimator_reference_arithmetic(kb):
+    """KroneckerApproximator(arithmetic="reference") (estimators.py:95-139 + the extension):
+    the fitted trace is the reference's, bit for bit."""
+    from paper_2410_00233_b200 import datagen
+
+    prob = datagen.make_problem("n256")
+    est = kb.KroneckerApproximator(engine="egkb", k_max=20, precision="single", arithmetic="reference")
+    est.fit(kb.Psf(prob.psf), side=prob.n)
+    _, tr, _, otr = _run_pair(kb, prob.psf, prob.n, dict(k_max=20), "reference")
+    assert (est.trace_.alphas, est.trace_.ts) == (otr.alphas, otr.ts)
+    assert est.k_ == otr.chosen_k
