@@ -155,13 +155,32 @@ __global__ void __launch_bounds__(32) k_chain(ChainArgs a) {
             const float* __restrict__ base = sm + (st % NS) * SLOT + t;
             const int rows = min(ROWS, K - st * ROWS);
             if (rows == ROWS) {
-#pragma unroll 16
-                for (int r = 0; r < ROWS; ++r) {
-                    const float v = base[(1 * ROWS + r) * LPC];
-                    acc0 = fmaf(HAS_X ? base[(0 * ROWS + r) * LPC] : v, v, acc0);
-                    if (HAS_U) {
-                        const float u = base[(2 * ROWS + r) * LPC];
-                        acc1 = fmaf(u, u, acc1);
+                // software-pipelined: the shared loads of the next 16 rows are issued before
+                // the 16 dependent FMAs of this group, so the FMA chain never waits on them
+                constexpr int GR = 16;
+                float cv[GR], cx[GR], cu[GR], nv[GR], nx[GR], nu[GR];
+                auto ld = [&](int r0, float* a, float* b, float* c) {
+#pragma unroll
+                    for (int j = 0; j < GR; ++j) {
+                        a[j] = base[(1 * ROWS + r0 + j) * LPC];
+                        if (HAS_X) b[j] = base[(0 * ROWS + r0 + j) * LPC];
+                        if (HAS_U) c[j] = base[(2 * ROWS + r0 + j) * LPC];
+                    }
+                };
+                ld(0, cv, cx, cu);
+#pragma unroll
+                for (int r0 = 0; r0 < ROWS; r0 += GR) {
+                    if (r0 + GR < ROWS) ld(r0 + GR, nv, nx, nu);
+#pragma unroll
+                    for (int j = 0; j < GR; ++j) {
+                        acc0 = fmaf(HAS_X ? cx[j] : cv[j], cv[j], acc0);
+                        if (HAS_U) acc1 = fmaf(cu[j], cu[j], acc1);
+                    }
+#pragma unroll
+                    for (int j = 0; j < GR; ++j) {
+                        cv[j] = nv[j];
+                        if (HAS_X) cx[j] = nx[j];
+                        if (HAS_U) cu[j] = nu[j];
                     }
                 }
             } else {
@@ -235,20 +254,36 @@ __global__ void k_normalize(const float* __restrict__ v, const float* __restrict
 // (Toeplitz family, then the two Hankel families of reflexive BC; cells increasing);
 // z = sequential fp64 sum over the kernel rows of rounded products; y = fl32(z)
 // (zero BC) or fl32 of the sequential sum of a cell's hits (reflexive).
+// The sequential sums keep many loads in flight: a batch of PF loads is issued, then the
+// batch is added in order (the additions are the only dependent chain).
+constexpr int PF = 32;
+
 __global__ void k_rdiag(const float* __restrict__ x, int n, int c, int len, int refl, double* __restrict__ w) {
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= len) return;
     double acc = 0.0;
     const int o = u - c;   // Toeplitz: b = a + o
-    for (int a = max(0, -o); a < min(n, n - o); ++a) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + a + o]);
+    const int a_lo = max(0, -o), a_hi = min(n, n - o);
+    for (int a0 = a_lo; a0 < a_hi; a0 += PF) {
+        float q[PF];
+#pragma unroll
+        for (int j = 0; j < PF; ++j) q[j] = a0 + j < a_hi ? __ldg(x + (int64_t)(a0 + j) * n + a0 + j + o) : 0.f;
+#pragma unroll
+        for (int j = 0; j < PF; ++j)
+            if (a0 + j < a_hi) acc = __dadd_rn(acc, (double)q[j]);
+    }
     if (refl) {
-        for (int a = 0; a < n; ++a) {   // a + b + 1 + c = u
-            const int b = u - 1 - c - a;
-            if (b >= 0 && b < n) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + b]);
-        }
-        for (int a = 0; a < n; ++a) {   // a + b + c + 1 - 2n = u
-            const int b = u + 2 * n - c - 1 - a;
-            if (b >= 0 && b < n) acc = __dadd_rn(acc, (double)x[(int64_t)a * n + b]);
+        for (int fam = 0; fam < 2; ++fam) {   // a + b + 1 + c = u, then a + b + c + 1 - 2n = u
+            const int sb = fam == 0 ? u - 1 - c : u + 2 * n - c - 1;   // b = sb - a
+            const int lo = max(0, sb - (n - 1)), hi = min(n - 1, sb);   // a range with 0 <= b < n
+            for (int a0 = lo; a0 <= hi; a0 += PF) {
+                float q[PF];
+#pragma unroll
+                for (int j = 0; j < PF; ++j) q[j] = a0 + j <= hi ? __ldg(x + (int64_t)(a0 + j) * n + sb - (a0 + j)) : 0.f;
+#pragma unroll
+                for (int j = 0; j < PF; ++j)
+                    if (a0 + j <= hi) acc = __dadd_rn(acc, (double)q[j]);
+            }
         }
     }
     w[u] = acc;
@@ -260,7 +295,18 @@ __global__ void k_rz(const float* __restrict__ M, int rows, int cols, const doub
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= cols) return;
     double acc = 0.0;
-    for (int i = 0; i < rows; ++i) acc = __dadd_rn(acc, __dmul_rn((double)M[(int64_t)i * cols + o], w[i]));
+    for (int i0 = 0; i0 < rows; i0 += PF) {
+        float m[PF];
+        double wv[PF];
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            m[j] = i0 + j < rows ? __ldg(M + (int64_t)(i0 + j) * cols + o) : 0.f;
+            wv[j] = i0 + j < rows ? __ldg(w + i0 + j) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PF; ++j)
+            if (i0 + j < rows) acc = __dadd_rn(acc, __dmul_rn((double)m[j], wv[j]));
+    }
     z[o] = acc;
 }
 
@@ -289,11 +335,11 @@ void ref_product(const kb_operator* op, const float* x, float* y, int transpose,
     const int n = op->side, kh = op->kh, kw = op->kw, refl = op->kind == KB_OP_RA_REFLEXIVE;
     const int lin = transpose ? kw : kh, cin = lin / 2;     // diagonal sums of the input
     const int lout = transpose ? kh : kw, cout = lout / 2;  // broadcast of z
-    k_rdiag<<<(int)cdiv(lin, 128), 128, 0, s>>>(x, n, cin, lin, refl, w);
+    k_rdiag<<<(int)cdiv(lin, 32), 32, 0, s>>>(x, n, cin, lin, refl, w);
     KB_LAUNCH_CHECK();
     // R q: z[v] = sum_u K[u][v] w[u] (K: kh x kw);  R^T s: z[u] = sum_v K^T[v][u] w[v] (K^T: kw x kh)
     const float* M = static_cast<const float*>(transpose ? op->kt : op->k);
-    k_rz<<<(int)cdiv(lout, 128), 128, 0, s>>>(M, lin, lout, w, z);
+    k_rz<<<(int)cdiv(lout, 32), 32, 0, s>>>(M, lin, lout, w, z);
     KB_LAUNCH_CHECK();
     const int64_t N = (int64_t)n * n;
     k_rbcast<<<(int)std::min<int64_t>(cdiv(N, 256), kSMs * 16), 256, 0, s>>>(z, n, cout, lout, refl, y);
