@@ -1282,7 +1282,9 @@ static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaS
         if (std::getenv("KB_DEBUG")) fprintf(stderr, "[kb] tiled eGKB<%d>: %d CTAs/SM, smem %zu\n", MAXG, per_sm, smem);
     }
     if (per_sm < 1) return false;
-    const int grid = std::min(sms * std::min(per_sm, per_sm_cap), Gm.T);
+    static const int grid_env = std::getenv("KB_PK_GRID") ? std::atoi(std::getenv("KB_PK_GRID")) : 0;
+    int grid = std::min(sms * std::min(per_sm, per_sm_cap), Gm.T);
+    if (grid_env > 0) grid = std::min(grid, grid_env);
     if ((Gm.T + grid - 1) / grid > MAXG) return false;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
