@@ -110,7 +110,10 @@ class ShardedKroneckerSum:
         fw.a, fw.lda = None, 0
         fw.kron = _lib.KbKron(s.m1, s.m2, s.n1, s.n2, self.k, self.f_dev.data_ptr(), self.g_dev.data_ptr())
         if hasattr(self.full, "kron_struct"):   # the full sum's G band bounds every term subset's
-            fw.kron.band = self.full.kron_struct().band
+            full = self.full.kron_struct()
+            fw.kron.band = full.band
+            if full.ft:   # this rank's F^T blocks: the transposed reduced stage as one GEMM too
+                fw.kron.ft = full.ft + 8 * self.terms[0] * s.n1 * s.m1
         fw.allreduce = self._hook
         fw.allreduce_ctx = None
         return fw
