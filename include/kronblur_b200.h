@@ -224,8 +224,10 @@ int kb_sdot_openblas(int lanes, const float* x, const float* y, int64_t n, float
 int kb_shard_sqnorm(const float* x, int n, int a0, int a1, long long* norm_limbs, kb_stream_t stream);
 /* diagonal sums of x over the own rows (the input side of an R(A) product) */
 int kb_shard_diag(const float* x, int n, int c, int len, int a0, int a1, long long* limbs, kb_stream_t stream);
-/* z[o] = sum_i M[i][o] w[i] from the all-reduced diagonal limbs (M = K or K^T, rows x cols) */
-int kb_shard_z(const float* M, int rows, int cols, const long long* w_limbs, double* z, kb_stream_t stream);
+/* z[o] = sum_i Mt[o][i] w[i] from the all-reduced diagonal limbs (Mt = K^T for R q, K for
+ * R^T s; cols x rows row-major); z must hold rows + cols doubles (the decoded w is staged
+ * behind z) */
+int kb_shard_z(const float* Mt, int rows, int cols, const long long* w_limbs, double* z, kb_stream_t stream);
 /* y = P z on the own rows, v = y - beta*prev (prev may be NULL), limbs of B_i . v (i < m),
  * |v|^2 and |y|^2 (3 (m + 2) limbs) */
 int kb_shard_bcast_dots(const double* z, int n, int c, int len, const double* beta_dev, const float* prev,

@@ -46,12 +46,11 @@ __device__ __forceinline__ void to_limbs(double x, long long& l2, long long& l1,
 
 // limbs -> double, carries normalised first (the same operations on every rank)
 __host__ __device__ inline double from_limbs(long long l2, long long l1, long long l0) {
-    const long long M = 1ll << 40;
-    long long c = l0 >= 0 ? l0 / M : -((-l0 + M - 1) / M);
-    l0 -= c * M;
+    long long c = l0 >> 40;   // floor division by 2^40 (arithmetic shift)
+    l0 -= c * (1ll << 40);
     l1 += c;
-    c = l1 >= 0 ? l1 / M : -((-l1 + M - 1) / M);
-    l1 -= c * M;
+    c = l1 >> 40;
+    l1 -= c * (1ll << 40);
     l2 += c;
     return ((double)l2 * W2 + (double)l1 * W1) + (double)l0 * W0;
 }
@@ -88,18 +87,23 @@ __global__ void k_diag(const float* __restrict__ x, int n, int c, int len, int a
     }
 }
 
-// z[o] = sum_i M[i][o] w[i] (M: rows x cols row-major; w from limbs), fixed order.
-__global__ void k_z(const float* __restrict__ M, int rows, int cols, const long long* __restrict__ wl,
+// w (fp64) from its limbs, once per product (every rank the same operations)
+__global__ void k_wdecode(const long long* __restrict__ wl, int rows, double* __restrict__ w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows) w[i] = from_limbs(wl[3 * i], wl[3 * i + 1], wl[3 * i + 2]);
+}
+
+// z[o] = sum_i Mt[o][i] w[i] (Mt: cols x rows row-major -- K^T for R q, K for R^T s):
+// one warp per output row, lanes over i, a fixed butterfly at the end (every rank the same).
+__global__ void k_z(const float* __restrict__ Mt, int rows, int cols, const double* __restrict__ wd,
                     double* __restrict__ z) {
-    extern __shared__ double wsh[];
-    for (int i = threadIdx.x; i < rows; i += blockDim.x)
-        wsh[i] = from_limbs(wl[3 * i], wl[3 * i + 1], wl[3 * i + 2]);
-    __syncthreads();
-    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (o >= cols) return;
+    const float* row = Mt + (int64_t)o * rows;
     double acc = 0.0;
-    for (int i = 0; i < rows; ++i) acc = fma((double)M[(int64_t)i * cols + o], wsh[i], acc);
-    z[o] = acc;
+    for (int i = lane; i < rows; i += 32) acc = fma((double)__ldg(row + i), __ldg(wd + i), acc);
+    acc = warp_sum_fixed(acc);
+    if (lane == 0) z[o] = acc;
 }
 
 // One warp per own row a: y = fl32(z[b - a + c]), v = fl(y - fl(beta * prev)) stored;
@@ -244,17 +248,14 @@ extern "C" int kb_shard_diag(const float* x, int n, int c, int len, int a0, int 
     })
 }
 
-extern "C" int kb_shard_z(const float* M, int rows, int cols, const long long* wl, double* z, kb_stream_t stream) {
+extern "C" int kb_shard_z(const float* Mt, int rows, int cols, const long long* wl, double* z, kb_stream_t stream) {
     KB_GUARD({
-        KB_REQUIRE(M && wl && z && rows > 0 && cols > 0, "bad arguments");
-        const size_t smem = sizeof(double) * rows;
-        KB_REQUIRE(smem <= 200 * 1024, "kernel too large for the sharded z step");
-        static bool cfg = false;
-        if (!cfg) {
-            KB_CUDA(cudaFuncSetAttribute(shard::k_z, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            cfg = true;
-        }
-        shard::k_z<<<(int)cdiv(cols, 128), 128, smem, as_stream(stream)>>>(M, rows, cols, wl, z);
+        KB_REQUIRE(Mt && wl && z && rows > 0 && cols > 0, "bad arguments");
+        // the decoded w goes to z's tail: z holds cols entries, the caller's buffer >= rows + cols
+        double* wd = z + cols;
+        shard::k_wdecode<<<(int)cdiv(rows, 128), 128, 0, as_stream(stream)>>>(wl, rows, wd);
+        KB_LAUNCH_CHECK();
+        shard::k_z<<<(int)cdiv(cols, 8), 256, 0, as_stream(stream)>>>(Mt, rows, cols, wd, z);
         KB_LAUNCH_CHECK();
     })
 }

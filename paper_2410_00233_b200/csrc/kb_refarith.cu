@@ -264,26 +264,40 @@ __global__ void k_rdiag(const float* __restrict__ x, int n, int c, int len, int 
     double acc = 0.0;
     const int o = u - c;   // Toeplitz: b = a + o
     const int a_lo = max(0, -o), a_hi = min(n, n - o);
-    for (int a0 = a_lo; a0 < a_hi; a0 += PF) {
-        float q[PF];
+    {   // the next batch's loads are issued before this batch is added (sequential order kept)
+        const int64_t st = (int64_t)n + 1;
+        const float* px = x + (int64_t)a_lo * st + o;
+        const int cnt = max(0, a_hi - a_lo), nb = cnt / PF;
+        float cur[PF], nxt[PF];
+        if (nb > 0) {
 #pragma unroll
-        for (int j = 0; j < PF; ++j) q[j] = a0 + j < a_hi ? __ldg(x + (int64_t)(a0 + j) * n + a0 + j + o) : 0.f;
+            for (int j = 0; j < PF; ++j) cur[j] = __ldg(px + j * st);
+        }
+        for (int b = 0; b < nb; ++b) {
+            if (b + 1 < nb) {
 #pragma unroll
-        for (int j = 0; j < PF; ++j)
-            if (a0 + j < a_hi) acc = __dadd_rn(acc, (double)q[j]);
+                for (int j = 0; j < PF; ++j) nxt[j] = __ldg(px + ((int64_t)(b + 1) * PF + j) * st);
+            }
+#pragma unroll
+            for (int j = 0; j < PF; ++j) acc = __dadd_rn(acc, (double)cur[j]);
+#pragma unroll
+            for (int j = 0; j < PF; ++j) cur[j] = nxt[j];
+        }
+        for (int j = nb * PF; j < cnt; ++j) acc = __dadd_rn(acc, (double)__ldg(px + j * st));
     }
     if (refl) {
         for (int fam = 0; fam < 2; ++fam) {   // a + b + 1 + c = u, then a + b + c + 1 - 2n = u
             const int sb = fam == 0 ? u - 1 - c : u + 2 * n - c - 1;   // b = sb - a
             const int lo = max(0, sb - (n - 1)), hi = min(n - 1, sb);   // a range with 0 <= b < n
-            for (int a0 = lo; a0 <= hi; a0 += PF) {
+            int a0 = lo;
+            for (; a0 + PF <= hi + 1; a0 += PF) {
                 float q[PF];
 #pragma unroll
-                for (int j = 0; j < PF; ++j) q[j] = a0 + j <= hi ? __ldg(x + (int64_t)(a0 + j) * n + sb - (a0 + j)) : 0.f;
+                for (int j = 0; j < PF; ++j) q[j] = __ldg(x + (int64_t)(a0 + j) * n + sb - (a0 + j));
 #pragma unroll
-                for (int j = 0; j < PF; ++j)
-                    if (a0 + j <= hi) acc = __dadd_rn(acc, (double)q[j]);
+                for (int j = 0; j < PF; ++j) acc = __dadd_rn(acc, (double)q[j]);
             }
+            for (; a0 <= hi; ++a0) acc = __dadd_rn(acc, (double)__ldg(x + (int64_t)a0 * n + sb - a0));
         }
     }
     w[u] = acc;
@@ -295,18 +309,23 @@ __global__ void k_rz(const float* __restrict__ M, int rows, int cols, const doub
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= cols) return;
     double acc = 0.0;
-    for (int i0 = 0; i0 < rows; i0 += PF) {
-        float m[PF];
-        double wv[PF];
+    const int nb = rows / PF;
+    float cur[PF], nxt[PF];
+    if (nb > 0) {
 #pragma unroll
-        for (int j = 0; j < PF; ++j) {
-            m[j] = i0 + j < rows ? __ldg(M + (int64_t)(i0 + j) * cols + o) : 0.f;
-            wv[j] = i0 + j < rows ? __ldg(w + i0 + j) : 0.0;
+        for (int j = 0; j < PF; ++j) cur[j] = __ldg(M + (int64_t)j * cols + o);
+    }
+    for (int b = 0; b < nb; ++b) {   // next batch in flight while this one is summed in order
+        if (b + 1 < nb) {
+#pragma unroll
+            for (int j = 0; j < PF; ++j) nxt[j] = __ldg(M + ((int64_t)(b + 1) * PF + j) * cols + o);
         }
 #pragma unroll
-        for (int j = 0; j < PF; ++j)
-            if (i0 + j < rows) acc = __dadd_rn(acc, __dmul_rn((double)m[j], wv[j]));
+        for (int j = 0; j < PF; ++j) acc = __dadd_rn(acc, __dmul_rn((double)cur[j], __ldg(w + b * PF + j)));
+#pragma unroll
+        for (int j = 0; j < PF; ++j) cur[j] = nxt[j];
     }
+    for (int i = nb * PF; i < rows; ++i) acc = __dadd_rn(acc, __dmul_rn((double)__ldg(M + (int64_t)i * cols + o), __ldg(w + i)));
     z[o] = acc;
 }
 

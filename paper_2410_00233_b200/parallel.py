@@ -20,6 +20,7 @@ sum-allreduce each -- so the recurrence is bit-identical for any shard count
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -130,6 +131,8 @@ class ShardedKroneckerSum:
 
 
 # ----------------------------------------------------------------- row-sharded eGKB
+_SHARD_CACHE: dict = {}
+
 class _Shards:
     """Which 8-row blocks of the n x n image each shard owns, and how partial limb
     buffers are combined: in place by an int64 sum-allreduce over ``group`` (one
@@ -181,9 +184,11 @@ class CudaShardKernels:
     def sqnorm(self, x, n, a0, a1, nl):
         self._check(self.lib.kb_shard_sqnorm(x.data_ptr(), n, a0, a1, nl.data_ptr(), self._st()), "shard sqnorm")
 
-    def z(self, M, wl, z):
-        rows, cols = M.shape
-        self._check(self.lib.kb_shard_z(M.data_ptr(), rows, cols, wl.data_ptr(), z.data_ptr(), self._st()), "shard z")
+    def z(self, Mt, wl, z):
+        """z = Mt w (Mt: cols x rows; one row dot per output)."""
+        cols, rows = Mt.shape
+        self._check(self.lib.kb_shard_z(Mt.data_ptr(), rows, cols, wl.data_ptr(), z.data_ptr(), self._st()),
+                    "shard z")
 
     def bcast_dots(self, z, n, c, length, beta, prev, B, m, a0, a1, v, dl):
         self._check(self.lib.kb_shard_bcast_dots(z.data_ptr(), n, c, length, beta.data_ptr(),
@@ -243,24 +248,56 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
     sh = _Shards(n, group, simulate)
     tol = config.break_tol if config.break_tol is not None else float(np.sqrt(eps_for(np.float32)))
     cap = max(config.k_max, config.k_min) + config.p + 3
-    S = torch.zeros((cap, N), dtype=torch.float32, device=dev)
-    Q = torch.zeros((cap, N), dtype=torch.float32, device=dev)
-    v = torch.zeros((N,), dtype=torch.float32, device=dev)
-    z = torch.zeros(max(kh, kw) + 8, dtype=torch.float64, device=dev)
-    wl = torch.zeros(3 * (max(kh, kw) + 8), dtype=torch.int64, device=dev)
-    dl = torch.zeros(3 * (cap + 3), dtype=torch.int64, device=dev)
-    nl = torch.zeros(3, dtype=torch.int64, device=dev)
-    scal = torch.zeros(4, dtype=torch.float64, device=dev)
-    beta = torch.zeros(1, dtype=torch.float64, device=dev)
-    hist = torch.zeros((2 * cap + 2, 2), dtype=torch.float64, device=dev)
+    # persistent state per (device, shape, shards, kernel): the buffers, and -- from the second
+    # call on -- one CUDA graph per half step (the per-shard launches, the limb zeroing and,
+    # across ranks, the NCCL allreduces), replayed instead of re-launched from Python
+    ckey = None
+    if kernels is None:
+        ckey = (dev.index, n, kh, kw, cap, sh.world, tuple(sh.mine), K.data_ptr(), Kt.data_ptr(), id(group))
+    st = _SHARD_CACHE.get(ckey) if ckey is not None else None
+    if st is None:
+        st = {"S": torch.zeros((cap, N), dtype=torch.float32, device=dev),
+              "Q": torch.zeros((cap, N), dtype=torch.float32, device=dev),
+              "v": torch.zeros((N,), dtype=torch.float32, device=dev),
+              "y0": torch.zeros((N,), dtype=torch.float32, device=dev),
+              "z": torch.zeros(kh + kw + 8, dtype=torch.float64, device=dev),
+              "wl": torch.zeros(3 * (max(kh, kw) + 8), dtype=torch.int64, device=dev),
+              "dl": torch.zeros(3 * (cap + 3), dtype=torch.int64, device=dev),
+              "nl": torch.zeros(3, dtype=torch.int64, device=dev),
+              "scal": torch.zeros(4, dtype=torch.float64, device=dev),
+              "beta": torch.zeros(1, dtype=torch.float64, device=dev),
+              "hist": torch.zeros((2 * cap + 2, 2), dtype=torch.float64, device=dev),
+              "graphs": {}, "calls": 0}
+        if ckey is not None:
+            if len(_SHARD_CACHE) >= 4:
+                _SHARD_CACHE.pop(next(iter(_SHARD_CACHE)))
+            _SHARD_CACHE[ckey] = st
+    st["calls"] += 1
+    use_graphs = ckey is not None and st["calls"] >= 2 and not os.environ.get("KB_SHARD_NO_GRAPH")
+    S, Q, v, z, wl, dl, nl = st["S"], st["Q"], st["v"], st["z"], st["wl"], st["dl"], st["nl"]
+    scal, beta, hist, graphs = st["scal"], st["beta"], st["hist"], st["graphs"]
     if y0 is None:
-        y0d = rng.standard_normal(config.seed, N, np.float32)
+        y0src = rng.standard_normal(config.seed, N, np.float32)
     elif isinstance(y0, torch.Tensor):
-        y0d = y0.to(device=dev, dtype=torch.float32).reshape(-1)
+        y0src = y0.to(device=dev, dtype=torch.float32).reshape(-1)
     else:
-        y0d = torch.from_numpy(np.ascontiguousarray(y0, dtype=np.float32)).to(dev).reshape(-1)
-    if tuple(y0d.shape) != (N,):
-        raise ValidationError(f"y0 must have length {N}, got shape {tuple(y0d.shape)}")
+        y0src = torch.from_numpy(np.ascontiguousarray(y0, dtype=np.float32)).to(dev).reshape(-1)
+    if tuple(y0src.shape) != (N,):
+        raise ValidationError(f"y0 must have length {N}, got shape {tuple(y0src.shape)}")
+    y0d = st["y0"]
+    y0d.copy_(y0src)
+
+    def run(gkey, fn):
+        if not use_graphs:
+            fn()
+            return
+        g = graphs.get(gkey)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs[gkey] = g
+        g.replay()
 
     def normalize(src, out, c_next, len_next):
         """t = |src| (allreduced limbs in nl) -> out = fl(src / t), next product's diagonal limbs."""
@@ -269,11 +306,11 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
             kern.normalize(src, nl, out, n, c_next, len_next, a0, a1, wl, scal)
         sh.allreduce(wl)
 
-    def half(M, c_b, len_b, prev, B, m, out, c_next, len_next, slot):
+    def half(Mt, c_b, len_b, prev, B, m, out, c_next, len_next, slot):
         """One half step (R q or R^T s): z from the all-reduced diagonal limbs; y, v = y - beta prev
         and the limbs of B^T v, |v|^2, |y|^2; v1 = v - B h and the limbs of |v1|^2; out = v1 / t
         and the next product's diagonal limbs.  (t or alpha, |y|) land in hist[slot]."""
-        kern.z(M, wl, z)
+        kern.z(Mt, wl, z)
         dl.zero_()
         for a0, a1 in sh.own():
             kern.bcast_dots(z, n, c_b, len_b, beta, prev, B, m, a0, a1, v, dl)
@@ -286,15 +323,18 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
         hist[slot].copy_(scal[:2])
         beta.copy_(scal[:1])
 
-    # s1 = y0 / |y0|, diagonal limbs for R^T s1 (lowrank.py:207-210)
-    nl.zero_()
-    for a0, a1 in sh.own():
-        kern.sqnorm(y0d, n, a0, a1, nl)
-    sh.allreduce(nl)
-    normalize(y0d, S[0], cv, kw)
-    hist[0].copy_(scal[:2])
-    # q1 = R^T s1 / alpha1 (lowrank.py:211-215): no previous vector, no projection
-    half(Kt, cu, kh, None, Q, 0, Q[0], cu, kh, 1)
+    def init():
+        # s1 = y0 / |y0|, diagonal limbs for R^T s1 (lowrank.py:207-210)
+        nl.zero_()
+        for a0, a1 in sh.own():
+            kern.sqnorm(y0d, n, a0, a1, nl)
+        sh.allreduce(nl)
+        normalize(y0d, S[0], cv, kw)
+        hist[0].copy_(scal[:2])
+        # q1 = R^T s1 / alpha1 (lowrank.py:211-215): no previous vector, no projection
+        half(K, cu, kh, None, Q, 0, Q[0], cu, kh, 1)
+
+    run(("init",), init)
     h = hist[:2].cpu().numpy()
     t1, a1 = float(h[0, 0]), float(h[1, 0])
     if t1 == 0.0:
@@ -310,9 +350,10 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
             raise NumericalError("eGKB basis capacity exhausted")
         slot = 2 * done
         # s step: u = R q_j, s_raw = u - alpha s_j, projected against S (lowrank.py:238-247)
-        half(K, cv, kw, S[done - 1], S, done if config.reorth != "one-sided" else 0, S[done], cv, kw, slot)
+        ms = done if config.reorth != "one-sided" else 0
+        run(("s", done, ms), lambda: half(Kt, cv, kw, S[done - 1], S, ms, S[done], cv, kw, slot))
         # q step: R^T s_{j+1} - t q_j, projected against Q (lowrank.py:250-260)
-        half(Kt, cu, kh, Q[done - 1], Q, done, Q[done], cu, kh, slot + 1)
+        run(("q", done), lambda: half(K, cu, kh, Q[done - 1], Q, done, Q[done], cu, kh, slot + 1))
         h = hist[slot:slot + 2].cpu().numpy()
         t_new, u_norm, a_new, pre = float(h[0, 0]), float(h[0, 1]), float(h[1, 0]), float(h[1, 1])
         if t_new <= tol * u_norm:

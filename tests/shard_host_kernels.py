@@ -54,12 +54,12 @@ class HostShardKernels:
         X = x.numpy().reshape(n, n)[a0:a1].astype(np.float64)
         self._add(nl, to_limbs((X * X).sum(axis=1)).sum(axis=0))
 
-    def z(self, M, wl, z):
-        rows, cols = M.shape
+    def z(self, Mt, wl, z):
+        cols, rows = Mt.shape
         w = np.array([from_limbs(*wl.numpy()[3 * i:3 * i + 3]) for i in range(rows)])
         acc = np.zeros(cols)
         for i in range(rows):
-            acc = acc + M.numpy()[i].astype(np.float64) * w[i]
+            acc = acc + Mt.numpy()[:, i].astype(np.float64) * w[i]
         z.numpy()[:cols] = acc
 
     def bcast_dots(self, z, n, c, length, beta, prev, B, m, a0, a1, v, dl):
