@@ -321,6 +321,11 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1, *, arithmet
     """
     from . import device as D
 
+    y0_early = None
+    if y0 is None and isinstance(b_mat, RearrangedBlur):
+        # the reference's start vector (lowrank.py:199-201) drawn on the device first, so the
+        # draw runs while the host validates / normalises / uploads the PSF (op_struct)
+        y0_early = rng.standard_normal(config.seed, b_mat.shape[0], b_mat.dtype)
     op = _EngineOp(b_mat)
     dtype = np.dtype(op.dtype)
     mbar, nbar = op.shape
@@ -334,7 +339,7 @@ def egkb(b_mat, config: EgkbConfig, y0=None, reorth_passes: int = 1, *, arithmet
     if y0 is None:
         # the reference's draws (lowrank.py:199-201), generated on the device; launched
         # first, so the draw runs while the host prepares the eGKB launch
-        y0d = rng.standard_normal(config.seed, mbar, dtype)
+        y0d = y0_early if y0_early is not None else rng.standard_normal(config.seed, mbar, dtype)
     elif D.is_tensor(y0):
         y0d = D.to_device(y0, dtype)
         if tuple(y0d.shape) != (mbar,):
