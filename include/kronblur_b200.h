@@ -348,6 +348,13 @@ int kb_dgemm(int trans_a, int trans_b, int m, int n, int k,
  * ordered, before anything consumes it.  The host supplies it (NCCL over
  * NVLink through torch.distributed on a B200 box, gloo in CPU tests). */
 typedef void (*kb_allreduce_fn)(void* ctx, double* buf, int64_t count, kb_stream_t stream);
+/* A kb_allreduce_fn over NCCL: ctx is an ncclComm_t (e.g. torch's ProcessGroupNCCL
+ * communicator); ncclAllReduce(sum, fp64) in place, stream-ordered.  The library
+ * resolves ncclAllReduce from the already-loaded libnccl.so.2. */
+void kb_nccl_allreduce_f64(void* comm, double* buf, int64_t count, kb_stream_t stream);
+int kb_nccl_available(void);
+/* last non-zero ncclResult_t of the hook since the previous reset (-1: NCCL not found) */
+int kb_nccl_last_error(int reset);
 typedef struct {
     int kind;            /* KB_FWD_DENSE / KB_FWD_KRON                       */
     int64_t m, n;        /* forward operator shape                           */

@@ -108,6 +108,9 @@ _SIGS = {
     "kb_egkb_capacity": (C.c_int, [P(KbEgkbConfig)]),
     "kb_egkb_run": (C.c_int, [P(KbOperator), P(KbEgkbConfig), vp, P(KbEgkbState), vp, SZ, vp]),
     "kb_sdot_openblas": (C.c_int, [C.c_int, vp, vp, i64, vp, vp, SZ, vp]),
+    "kb_nccl_allreduce_f64": (None, [vp, dp, i64, vp]),
+    "kb_nccl_available": (C.c_int, []),
+    "kb_nccl_last_error": (C.c_int, [C.c_int]),
     "kb_shard_diag": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]),
     "kb_shard_z": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp]),
     "kb_shard_bcast_dots": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int,

@@ -9,6 +9,10 @@ ABI, stream-ordered on the current stream (NCCL over NVLink on a B200 box).
 All vector work stays replicated, so every rank holds the same iterate and
 makes the same stop decisions.
 
+With an NCCL process group the hook is the library's C function
+``kb_nccl_allreduce_f64`` on torch's communicator (no Python callback inside the
+solve); other backends (gloo) use a Python callback.
+
 The eGKB side is row-sharded (:func:`sharded_egkb`): each rank
 owns a contiguous block of image rows of every Krylov vector, K is replicated,
 and the per-half-step cross-shard sums (diagonal sums, reorthogonalisation
@@ -86,6 +90,20 @@ class ShardedKroneckerSum:
         self.f_dev = full.f_dev[lo:hi]
         self.g_dev = full.g_dev[lo:hi]
         self._hook = _lib.ALLREDUCE_FN(self._allreduce)
+        self._ctx = None
+        self._nccl_comm = None
+        if dist.is_initialized() and dist.get_backend(group) == "nccl":
+            # the C hook over NCCL on torch's own communicator: no Python inside the solve
+            pg = group if group is not None else dist.distributed_c10d._get_default_group()
+            backend = pg._get_backend(torch.device("cuda"))
+            t = torch.zeros(1, dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, group=group)   # the communicator exists after a first collective
+            comm = backend._comm_ptr()
+            lib = _lib.load()
+            if comm and lib.kb_nccl_available():
+                self._nccl_comm = comm
+                self._hook = C.cast(lib.kb_nccl_allreduce_f64, _lib.ALLREDUCE_FN)
+                self._ctx = C.c_void_p(comm)
 
     def _allreduce(self, ctx, buf, count, stream):
         import torch.distributed as dist
@@ -116,7 +134,7 @@ class ShardedKroneckerSum:
             if full.ft:   # this rank's F^T blocks: the transposed reduced stage as one GEMM too
                 fw.kron.ft = full.ft + 8 * self.terms[0] * s.n1 * s.m1
         fw.allreduce = self._hook
-        fw.allreduce_ctx = None
+        fw.allreduce_ctx = self._ctx
         return fw
 
     def apply(self, x, counter=None):

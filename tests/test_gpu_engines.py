@@ -364,12 +364,16 @@ class TestParallel:
         try:
             sop = ShardedKroneckerSum(op)
             assert sop.k == op.k
+            assert sop._nccl_comm, "the NCCL C hook is in use"   # the collective really runs (world 1)
+            from paper_2410_00233_b200 import _lib
+            _lib.load().kb_nccl_last_error(1)
             cfg = kb.SbConfig(lam=0.115, beta=0.0066, tau=0.0, l_max=3, cgls=kb.CglsConfig(i_max=10, tau=0.0))
             a = kb.sb_run(op, g["n64_b"], cfg)
             b = kb.sb_run(sop, g["n64_b"], cfg)
             np.testing.assert_array_equal(a.x, b.x)
             x = np.random.default_rng(0).standard_normal(side * side)
             np.testing.assert_array_equal(sop.apply(x), op.apply(x))
+            assert _lib.load().kb_nccl_last_error(1) == 0
         finally:
             if created:
                 dist.destroy_process_group()
