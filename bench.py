@@ -244,6 +244,31 @@ def other_configs(kb, D, flush):
                 "ms": float(np.median(ms)), "ms_min": float(min(ms)), "result": trace_result(tr)}
             if arith == "fast":
                 fop = op
+        if name == "n512":   # configs[2]'s other engines: TSVD-20 and RSVD (k=20, p=10, q=2)
+            def dev_ms(fn, reps=3):
+                fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                return e0.elapsed_time(e1) / reps
+            rec["tsvd20_ms"] = dev_ms(lambda: kb.tsvd(blur, 20))
+            try:
+                kb.rsvd(blur, kb.RsvdConfig(k=20, p=10, q=2, seed=0))
+                rec["rsvd_20_10_2"] = "ok"
+            except kb.RankDeficiencyError as e:
+                rec["rsvd_20_10_2"] = f"RankDeficiencyError(column {e.column}) (the reference raises the same)"
+            for k in range(6, 1, -1):   # the largest fp32 block (p = 2) the random draw keeps full rank
+                try:
+                    kb.rsvd(blur, kb.RsvdConfig(k=k, p=2, q=2, seed=0))
+                except kb.RankDeficiencyError:
+                    continue
+                rec[f"rsvd_{k}_2_2_ms"] = dev_ms(lambda: kb.rsvd(blur, kb.RsvdConfig(k=k, p=2, q=2, seed=0)))
+                rec["rsvd_note"] = f"k={k}, p=2, q=2: the largest k with p=2 that passes the rank check"
+                break
         variants = ["isotropic", "anisotropic"] if name == "n512" else ["anisotropic"]
         b_dev = D.to_device(prob.b)
         for var in variants:

@@ -24,6 +24,8 @@
 //   kb_shard_normalize  out = fl(v1 / t), stored; limbs of its diagonal sums for the next product
 //   -- allreduce --
 #include <cmath>
+#include <cstdint>
+#include <initializer_list>
 
 #include "kb_common.cuh"
 
@@ -217,6 +219,263 @@ __global__ void k_normalize(const float* __restrict__ v, const long long* __rest
     }
 }
 
+// ---- vectorised kernels (n % 4 == 0, 16-byte aligned rows).  A persistent grid (the
+// resident CTAs, one row at a time per CTA): each CTA adds its rows' limbs in shared
+// memory (exact int64) before ONE set of global atomics, so the atomics per address are
+// bounded by the grid, not by the row count.  Same chunks as the scalar kernels (one
+// image row per dot / norm partial, 8-row blocks for the diagonal sums), so they keep
+// the shard-count invariance; only the in-row summation order differs.
+__device__ __forceinline__ void flush_limbs(const long long* sh, long long* dst, int count) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x)
+        if (sh[i]) atomicAdd(reinterpret_cast<unsigned long long*>(dst + i), (unsigned long long)sh[i]);
+}
+
+__device__ __forceinline__ double dot4(const float4& a, const float4& b, double acc) {
+    acc = fma((double)a.x, (double)b.x, acc);
+    acc = fma((double)a.y, (double)b.y, acc);
+    acc = fma((double)a.z, (double)b.z, acc);
+    return fma((double)a.w, (double)b.w, acc);
+}
+
+// Row-per-CTA kernels: the CTA (blockDim = min(256, n/4 rounded to warps)) walks the own
+// rows, thread t owning the float4s t, t + blockDim, ... (NT of them) of the current row;
+// the basis rows are requested four at a time (4 NT 16-byte loads in flight per thread).
+// A row's partial is the warps' fixed butterflies added in warp order, so it depends on
+// the row only.
+template <int NT>
+__global__ void __launch_bounds__(256) k_bcast_dots_r(const double* __restrict__ z, int n, int c, int len,
+                                                      const double* __restrict__ beta_dev,
+                                                      const float* __restrict__ prev, const float* __restrict__ S,
+                                                      int64_t ld, int m, int a0, int a1, float* __restrict__ v_out,
+                                                      long long* __restrict__ limbs) {
+    extern __shared__ long long lsh[];   // [(m + 2) * 3] limbs, then [nwarps][m + 2] doubles
+    const int W = m + 2, nw = blockDim.x >> 5;
+    double* part = reinterpret_cast<double*>(lsh + 3 * W);
+    for (int i = threadIdx.x; i < 3 * W; i += blockDim.x) lsh[i] = 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float beta = prev ? (float)*beta_dev : 0.f;
+    const int n4 = n >> 2;
+    for (int a = a0 + blockIdx.x; a < a1; a += gridDim.x) {
+        const int64_t row = (int64_t)a * n;
+        float4 v[NT];
+        double ysq = 0.0, vsq = 0.0;
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            const int j = threadIdx.x + k * blockDim.x;
+            float4 y = make_float4(0.f, 0.f, 0.f, 0.f), w = y;
+            if (j < n4) {
+                const float4 p = prev ? __ldg(reinterpret_cast<const float4*>(prev + row) + j) : y;
+                const int u = 4 * j - a + c;
+                float* yy = reinterpret_cast<float*>(&y);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) yy[q] = (u + q >= 0 && u + q < len) ? (float)__ldg(z + u + q) : 0.f;
+                w = y;
+                if (prev) {
+                    w.x = __fsub_rn(y.x, __fmul_rn(beta, p.x));
+                    w.y = __fsub_rn(y.y, __fmul_rn(beta, p.y));
+                    w.z = __fsub_rn(y.z, __fmul_rn(beta, p.z));
+                    w.w = __fsub_rn(y.w, __fmul_rn(beta, p.w));
+                }
+                reinterpret_cast<float4*>(v_out + row)[j] = w;
+            }
+            v[k] = w;
+            ysq = dot4(y, y, ysq);
+            vsq = dot4(w, w, vsq);
+        }
+        for (int i0 = 0; i0 < m; i0 += 4) {
+            float4 sv[4][NT];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int k = 0; k < NT; ++k) {
+                    const int j = threadIdx.x + k * blockDim.x;
+                    sv[r][k] = (i0 + r < m && j < n4)
+                                   ? __ldg(reinterpret_cast<const float4*>(S + (int64_t)(i0 + r) * ld + row) + j)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (i0 + r >= m) break;
+                float d = 0.f;   // fp32 FMAs over the thread's 4 NT cells, then fp64 across lanes
+#pragma unroll
+                for (int k = 0; k < NT; ++k) {
+                    d = fmaf(sv[r][k].x, v[k].x, d);
+                    d = fmaf(sv[r][k].y, v[k].y, d);
+                    d = fmaf(sv[r][k].z, v[k].z, d);
+                    d = fmaf(sv[r][k].w, v[k].w, d);
+                }
+                const double dw = warp_sum_fixed((double)d);
+                if (lane == 0) part[warp * W + i0 + r] = dw;
+            }
+        }
+        ysq = warp_sum_fixed(ysq);
+        vsq = warp_sum_fixed(vsq);
+        if (lane == 0) {
+            part[warp * W + m] = vsq;
+            part[warp * W + m + 1] = ysq;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < W; i += blockDim.x) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += part[w * W + i];
+            if (t != 0.0) {
+                long long l2, l1, l0;
+                to_limbs(t, l2, l1, l0);
+                lsh[3 * i] += l2;   // one thread per entry: no atomics needed
+                lsh[3 * i + 1] += l1;
+                lsh[3 * i + 2] += l0;
+            }
+        }
+        __syncthreads();
+    }
+    flush_limbs(lsh, limbs, 3 * W);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) k_update_r(float* __restrict__ v, const float* __restrict__ S, int64_t ld, int m,
+                                                  const long long* __restrict__ dl, int n, int a0, int a1,
+                                                  long long* __restrict__ nl, double* __restrict__ scal) {
+    extern __shared__ float hsh[];   // [m] (padded to 2), 3 limbs, [nwarps] doubles
+    long long* lsh = reinterpret_cast<long long*>(hsh + ((m + 1) & ~1));
+    double* part = reinterpret_cast<double*>(lsh + 3);
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) hsh[i] = (float)from_limbs(dl[3 * i], dl[3 * i + 1], dl[3 * i + 2]);
+    if (threadIdx.x < 3) lsh[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        scal[1] = sqrt(from_limbs(dl[3 * m + 3], dl[3 * m + 4], dl[3 * m + 5]));
+    __syncthreads();
+    const int n4 = n >> 2;
+    for (int a = a0 + blockIdx.x; a < a1; a += gridDim.x) {
+        const int64_t row = (int64_t)a * n;
+        float4 x[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            const int j = threadIdx.x + k * blockDim.x;
+            x[k] = j < n4 ? reinterpret_cast<const float4*>(v + row)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int i0 = 0; i0 < m; i0 += 4) {
+            float4 sv[4][NT];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int k = 0; k < NT; ++k) {
+                    const int j = threadIdx.x + k * blockDim.x;
+                    sv[r][k] = (i0 + r < m && j < n4)
+                                   ? __ldg(reinterpret_cast<const float4*>(S + (int64_t)(i0 + r) * ld + row) + j)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (i0 + r >= m) break;
+                const float h = -hsh[i0 + r];   // basis order: one fp32 FMA per cell per vector
+#pragma unroll
+                for (int k = 0; k < NT; ++k) {
+                    x[k].x = fmaf(h, sv[r][k].x, x[k].x);
+                    x[k].y = fmaf(h, sv[r][k].y, x[k].y);
+                    x[k].z = fmaf(h, sv[r][k].z, x[k].z);
+                    x[k].w = fmaf(h, sv[r][k].w, x[k].w);
+                }
+            }
+        }
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            const int j = threadIdx.x + k * blockDim.x;
+            if (j < n4) {
+                reinterpret_cast<float4*>(v + row)[j] = x[k];
+                sq = dot4(x[k], x[k], sq);
+            }
+        }
+        sq = warp_sum_fixed(sq);
+        if (lane == 0) part[warp] = sq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += part[w];
+            if (t != 0.0) {
+                long long l2, l1, l0;
+                to_limbs(t, l2, l1, l0);
+                lsh[0] += l2;
+                lsh[1] += l1;
+                lsh[2] += l0;
+            }
+        }
+        __syncthreads();
+    }
+    flush_limbs(lsh, nl, 3);
+}
+
+// out = fl(v / t) over the CTA's NB 8-row blocks (float4, grid-stride inside the CTA),
+// then the (8-row block, diagonal) partials from the CTA's own stores of out, the CTA's
+// blocks added as int64 limbs before the atomics.
+__global__ void __launch_bounds__(512) k_normalize_v(const float* __restrict__ v, const long long* __restrict__ nl,
+                                                     float* out, int n, int c, int len, int a0, int a1,
+                                                     long long* __restrict__ limbs, double* __restrict__ scal, int NB) {
+    const double t = sqrt(from_limbs(nl[0], nl[1], nl[2]));
+    if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = t;
+    const float tf = (float)t;
+    const int r0 = a0 + 8 * NB * blockIdx.x, r1 = min(r0 + 8 * NB, a1);
+    if (r0 >= r1) return;
+    {
+        const int64_t e0 = (int64_t)r0 * n / 4, e1 = (int64_t)r1 * n / 4;
+        const float4* src = reinterpret_cast<const float4*>(v);
+        float4* dst = reinterpret_cast<float4*>(out);
+        int64_t e = e0 + threadIdx.x;
+        for (; e + 3 * blockDim.x < e1; e += 4 * blockDim.x) {
+            float4 q[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[j] = __ldg(src + e + j * blockDim.x);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                q[j].x = __fdiv_rn(q[j].x, tf);
+                q[j].y = __fdiv_rn(q[j].y, tf);
+                q[j].z = __fdiv_rn(q[j].z, tf);
+                q[j].w = __fdiv_rn(q[j].w, tf);
+                dst[e + j * blockDim.x] = q[j];
+            }
+        }
+        for (; e < e1; e += blockDim.x) {
+            float4 q = __ldg(src + e);
+            q.x = __fdiv_rn(q.x, tf);
+            q.y = __fdiv_rn(q.y, tf);
+            q.z = __fdiv_rn(q.z, tf);
+            q.w = __fdiv_rn(q.w, tf);
+            dst[e] = q;
+        }
+    }
+    if (!limbs) return;
+    __syncthreads();   // the CTA's stores of out are visible to the CTA from here on
+    // diagonals that meet the CTA's rows: b = a + u - c in [0, n) for some a in [r0, r1)
+    const int u_lo = max(0, c - (r1 - 1)), u_hi = min(len, c - r0 + n);
+    for (int u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+        const int o = u - c;   // b = a + o
+        long long l2 = 0, l1 = 0, l0 = 0;
+        for (int blk = r0; blk < r1; blk += 8) {
+            const int bend = min(blk + 8, r1);
+            float q[8];   // the block's 8 cells of this diagonal requested together
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int a = blk + r, b = a + o;
+                q[r] = (a < bend && b >= 0 && b < n) ? out[(int64_t)a * n + b] : 0.f;
+            }
+            double s = 0.0;   // rows in ascending order (absent cells add an exact 0)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) s += (double)q[r];
+            if (s != 0.0) {
+                long long q2, q1, q0;
+                to_limbs(s, q2, q1, q0);
+                l2 += q2;
+                l1 += q1;
+                l0 += q0;
+            }
+        }
+        if (l2) atomicAdd(reinterpret_cast<unsigned long long*>(limbs + 3 * u), (unsigned long long)l2);
+        if (l1) atomicAdd(reinterpret_cast<unsigned long long*>(limbs + 3 * u + 1), (unsigned long long)l1);
+        if (l0) atomicAdd(reinterpret_cast<unsigned long long*>(limbs + 3 * u + 2), (unsigned long long)l0);
+    }
+}
+
 // |x|^2 limbs over the own rows (the start vector, lowrank.py:207)
 __global__ void k_sqnorm(const float* __restrict__ x, int n, int a0, int a1, long long* __restrict__ nl) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -237,6 +496,30 @@ __global__ void k_sqnorm(const float* __restrict__ x, int n, int a0, int a1, lon
 using namespace kb;
 
 static int rows_grid(int a0, int a1, int per) { return std::max(1, (a1 - a0 + per - 1) / per); }
+
+// float4s per thread for the row-per-CTA kernels (0: use the scalar kernels)
+static int row_threads(int n) { return std::min(256, (int)cdiv(n / 4, 32) * 32); }
+
+static bool vec_ok(int n, int64_t ld, std::initializer_list<const void*> ptrs) {
+    if (n % 4 || ld % 4) return false;
+    for (const void* p : ptrs)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return false;
+    return true;
+}
+
+// resident CTAs of `kern` at `tpb` threads (the persistent grid), cached per kernel
+template <typename K>
+static int resident_grid(K kern, int tpb, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+    return per_sm * kSMs;
+}
+
+static int vec_nt(int n, int64_t ld, std::initializer_list<const void*> ptrs) {
+    if (!vec_ok(n, ld, ptrs)) return 0;
+    const int nt = (int)cdiv(n / 4, row_threads(n));
+    return nt <= 2 ? nt : 0;
+}
 
 extern "C" int kb_shard_diag(const float* x, int n, int c, int len, int a0, int a1, long long* limbs,
                              kb_stream_t stream) {
@@ -266,8 +549,23 @@ extern "C" int kb_shard_bcast_dots(const double* z, int n, int c, int len, const
     KB_GUARD({
         KB_REQUIRE(z && v_out && limbs && m >= 0 && (!m || S) && (!prev || beta_dev), "bad arguments");
         if (a1 == a0) return KB_OK;
-        shard::k_bcast_dots<<<rows_grid(a0, a1, 8), 256, sizeof(long long) * 3 * (m + 2), as_stream(stream)>>>(
-            z, n, c, len, beta_dev, prev, S, ld, m, a0, a1, v_out, limbs);
+        const size_t smem = sizeof(long long) * 3 * (m + 2);
+        const int nt = vec_nt(n, ld, {prev, S, v_out});
+        if (nt) {
+            const int tpb = row_threads(n);
+            const size_t smem2 = smem + sizeof(double) * (tpb / 32) * (m + 2);
+            const int g = std::min(a1 - a0, resident_grid(nt == 1 ? shard::k_bcast_dots_r<1> : shard::k_bcast_dots_r<2>,
+                                                          tpb, smem2));
+            if (nt == 1)
+                shard::k_bcast_dots_r<1><<<g, tpb, smem2, as_stream(stream)>>>(z, n, c, len, beta_dev, prev, S, ld, m,
+                                                                              a0, a1, v_out, limbs);
+            else
+                shard::k_bcast_dots_r<2><<<g, tpb, smem2, as_stream(stream)>>>(z, n, c, len, beta_dev, prev, S, ld, m,
+                                                                              a0, a1, v_out, limbs);
+        } else {
+            shard::k_bcast_dots<<<rows_grid(a0, a1, 8), 256, smem, as_stream(stream)>>>(z, n, c, len, beta_dev, prev, S,
+                                                                                       ld, m, a0, a1, v_out, limbs);
+        }
         KB_LAUNCH_CHECK();
     })
 }
@@ -276,8 +574,22 @@ extern "C" int kb_shard_update(float* v, const float* S, int64_t ld, int m, cons
                                int a0, int a1, long long* norm_limbs, double* scal, kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(v && dot_limbs && norm_limbs && scal && (!m || S), "bad arguments");
-        shard::k_update<<<rows_grid(a0, a1, 8), 256, sizeof(float) * (m + 1), as_stream(stream)>>>(
-            v, S, ld, m, dot_limbs, n, a0, std::max(a0, a1), norm_limbs, scal);
+        const int nt = vec_nt(n, ld, {v, S});
+        if (nt) {
+            const int tpb = row_threads(n);
+            const size_t smem = sizeof(float) * (((m + 1) & ~1)) + sizeof(long long) * 3 + sizeof(double) * (tpb / 32);
+            const int g = std::max(1, std::min(a1 - a0, resident_grid(nt == 1 ? shard::k_update_r<1> : shard::k_update_r<2>,
+                                                                      tpb, smem)));
+            if (nt == 1)
+                shard::k_update_r<1><<<g, tpb, smem, as_stream(stream)>>>(v, S, ld, m, dot_limbs, n, a0, std::max(a0, a1),
+                                                                         norm_limbs, scal);
+            else
+                shard::k_update_r<2><<<g, tpb, smem, as_stream(stream)>>>(v, S, ld, m, dot_limbs, n, a0, std::max(a0, a1),
+                                                                         norm_limbs, scal);
+        } else {
+            shard::k_update<<<rows_grid(a0, a1, 8), 256, sizeof(float) * (m + 1), as_stream(stream)>>>(
+                v, S, ld, m, dot_limbs, n, a0, std::max(a0, a1), norm_limbs, scal);
+        }
         KB_LAUNCH_CHECK();
     })
 }
@@ -286,6 +598,14 @@ extern "C" int kb_shard_normalize(const float* v, const long long* norm_limbs, f
                                   int a0, int a1, long long* diag_limbs, double* scal, kb_stream_t stream) {
     KB_GUARD({
         KB_REQUIRE(v && norm_limbs && out && scal && a0 % 8 == 0, "bad arguments");
+        if (vec_ok(n, n, {v, out}) && v != out) {
+            const int rows = std::max(a1 - a0, 1);
+            const int nb = std::max(1, (int)cdiv(rows, 16 * kSMs));   // 8-row blocks per CTA
+            shard::k_normalize_v<<<(int)cdiv(rows, 8 * nb), 512, 0, as_stream(stream)>>>(
+                v, norm_limbs, out, n, c, len, a0, std::max(a0, a1), diag_limbs, scal, nb);
+            KB_LAUNCH_CHECK();
+            return KB_OK;
+        }
         const size_t smem = sizeof(float) * 8 * (size_t)n;
         KB_REQUIRE(smem <= 200 * 1024, "image side too large for the sharded normalisation");
         static bool cfg = false;

@@ -464,6 +464,60 @@ k_lift2_asm(const float* __restrict__ S, int64_t ld, int rows, const float* __re
     }
 }
 
+// fp32 -> fp32 lift with four adjacent elements per thread (float4 loads and stores);
+// every element keeps the FMA order of k_lift (bit-identical results).
+template <int CB>
+__global__ void __launch_bounds__(256)
+k_lift4(const float* __restrict__ S, int64_t ld, int rows, const float* __restrict__ W, int cols, int c0,
+        float* __restrict__ out, int64_t ld_out, int64_t len) {
+    extern __shared__ double wraw[];
+    float* wsm = reinterpret_cast<float*>(wraw);  // [rows][CB]
+    const int nc = min(CB, cols - c0);
+    for (int i = threadIdx.x; i < rows * CB; i += blockDim.x) {
+        const int r = i / CB, c = i % CB;
+        wsm[i] = (c < nc) ? W[(int64_t)r * cols + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    const int64_t len4 = len / 4;
+    for (int64_t e4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e4 < len4;
+         e4 += (int64_t)gridDim.x * blockDim.x) {
+        float4 acc[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int i = 0;
+        for (; i + 4 <= rows; i += 4) {   // 4 basis rows of loads in flight per thread
+            float4 s4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s4[j] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)(i + j) * ld) + e4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float* wr = wsm + (i + j) * CB;
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    acc[c].x = fmaf(s4[j].x, wr[c], acc[c].x);
+                    acc[c].y = fmaf(s4[j].y, wr[c], acc[c].y);
+                    acc[c].z = fmaf(s4[j].z, wr[c], acc[c].z);
+                    acc[c].w = fmaf(s4[j].w, wr[c], acc[c].w);
+                }
+            }
+        }
+        for (; i < rows; ++i) {
+            const float4 sv = __ldg(reinterpret_cast<const float4*>(S + (int64_t)i * ld) + e4);
+            const float* wr = wsm + i * CB;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                acc[c].x = fmaf(sv.x, wr[c], acc[c].x);
+                acc[c].y = fmaf(sv.y, wr[c], acc[c].y);
+                acc[c].z = fmaf(sv.z, wr[c], acc[c].z);
+                acc[c].w = fmaf(sv.w, wr[c], acc[c].w);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (c < nc) __stcs(reinterpret_cast<float4*>(out + (int64_t)(c0 + c) * ld_out) + e4, acc[c]);
+    }
+}
+
 template <typename T, int CB, typename TO = T, bool ASM = false>
 __global__ void __launch_bounds__(256)
 k_lift(const T* __restrict__ S, int64_t ld, int rows, const T* __restrict__ W, int cols, int c0,
@@ -780,6 +834,20 @@ static void launch_lift(const void* S, int64_t ld, int rows, const void* W, int 
             const unsigned b2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len / 2, 256), 4 * kSMs));
             k_lift2_asm<CB><<<b2, 256, smem, st>>>(static_cast<const float*>(S), ld, rows, static_cast<const float*>(W),
                                                    cols, c0, static_cast<double*>(out), ld_out, len, scale);
+            KB_LAUNCH_CHECK();
+            return;
+        }
+    }
+    if constexpr (!ASM && sizeof(T) == 4 && sizeof(TO) == 4 && CB <= 16) {   // (CB = 32: 128 accumulators)
+        if (len % 4 == 0 && ld % 4 == 0 && ld_out % 4 == 0 && ((uintptr_t)S % 16) == 0 && ((uintptr_t)out % 16) == 0) {
+            static bool cfg4 = false;
+            if (!cfg4) {
+                KB_CUDA(cudaFuncSetAttribute(k_lift4<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+                cfg4 = true;
+            }
+            const unsigned b4 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(len / 4, 256), 4 * kSMs));
+            k_lift4<CB><<<b4, 256, smem, st>>>(static_cast<const float*>(S), ld, rows, static_cast<const float*>(W), cols,
+                                               c0, static_cast<float*>(out), ld_out, len);
             KB_LAUNCH_CHECK();
             return;
         }

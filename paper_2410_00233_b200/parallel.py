@@ -279,11 +279,10 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
               "v": torch.zeros((N,), dtype=torch.float32, device=dev),
               "y0": torch.zeros((N,), dtype=torch.float32, device=dev),
               "z": torch.zeros(kh + kw + 8, dtype=torch.float64, device=dev),
-              "wl": torch.zeros(3 * (max(kh, kw) + 8), dtype=torch.int64, device=dev),
-              "dl": torch.zeros(3 * (cap + 3), dtype=torch.int64, device=dev),
-              "nl": torch.zeros(3, dtype=torch.int64, device=dev),
-              "scal": torch.zeros(4, dtype=torch.float64, device=dev),
-              "beta": torch.zeros(1, dtype=torch.float64, device=dev),
+              # all limb accumulators in one buffer (one fill per half step): w | dots | norm
+              "limbs": torch.zeros(3 * (max(kh, kw) + 8) + 3 * (cap + 3) + 3, dtype=torch.int64, device=dev),
+              # per half step (t or alpha, |y|), written by the kernels; the next half step's
+              # beta is the previous row's first entry
               "hist": torch.zeros((2 * cap + 2, 2), dtype=torch.float64, device=dev),
               "graphs": {}, "calls": 0}
         if ckey is not None:
@@ -292,8 +291,10 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
             _SHARD_CACHE[ckey] = st
     st["calls"] += 1
     use_graphs = ckey is not None and st["calls"] >= 2 and not os.environ.get("KB_SHARD_NO_GRAPH")
-    S, Q, v, z, wl, dl, nl = st["S"], st["Q"], st["v"], st["z"], st["wl"], st["dl"], st["nl"]
-    scal, beta, hist, graphs = st["scal"], st["beta"], st["hist"], st["graphs"]
+    S, Q, v, z, limbs = st["S"], st["Q"], st["v"], st["z"], st["limbs"]
+    lw = 3 * (max(kh, kw) + 8)
+    wl, dl, nl = limbs[:lw], limbs[lw:lw + 3 * (cap + 3)], limbs[lw + 3 * (cap + 3):]
+    hist, graphs = st["hist"], st["graphs"]
     if y0 is None:
         y0src = rng.standard_normal(config.seed, N, np.float32)
     elif isinstance(y0, torch.Tensor):
@@ -317,9 +318,8 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
             graphs[gkey] = g
         g.replay()
 
-    def normalize(src, out, c_next, len_next):
+    def normalize(src, out, c_next, len_next, scal):
         """t = |src| (allreduced limbs in nl) -> out = fl(src / t), next product's diagonal limbs."""
-        wl.zero_()
         for a0, a1 in sh.own():
             kern.normalize(src, nl, out, n, c_next, len_next, a0, a1, wl, scal)
         sh.allreduce(wl)
@@ -327,28 +327,26 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
     def half(Mt, c_b, len_b, prev, B, m, out, c_next, len_next, slot):
         """One half step (R q or R^T s): z from the all-reduced diagonal limbs; y, v = y - beta prev
         and the limbs of B^T v, |v|^2, |y|^2; v1 = v - B h and the limbs of |v1|^2; out = v1 / t
-        and the next product's diagonal limbs.  (t or alpha, |y|) land in hist[slot]."""
+        and the next product's diagonal limbs.  (t or alpha, |y|) land in hist[slot]; beta is the
+        previous half step's t or alpha (hist[slot - 1, 0])."""
         kern.z(Mt, wl, z)
-        dl.zero_()
+        limbs.zero_()   # w was consumed by z; the dot and norm limbs were consumed last half step
+        beta = hist[slot - 1, :1]
         for a0, a1 in sh.own():
             kern.bcast_dots(z, n, c_b, len_b, beta, prev, B, m, a0, a1, v, dl)
         sh.allreduce(dl[: 3 * (m + 2)])
-        nl.zero_()
         for a0, a1 in sh.own():
-            kern.update(v, B, m, dl, n, a0, a1, nl, scal)
+            kern.update(v, B, m, dl, n, a0, a1, nl, hist[slot])
         sh.allreduce(nl)
-        normalize(v, out, c_next, len_next)
-        hist[slot].copy_(scal[:2])
-        beta.copy_(scal[:1])
+        normalize(v, out, c_next, len_next, hist[slot])
 
     def init():
         # s1 = y0 / |y0|, diagonal limbs for R^T s1 (lowrank.py:207-210)
-        nl.zero_()
+        limbs.zero_()
         for a0, a1 in sh.own():
             kern.sqnorm(y0d, n, a0, a1, nl)
         sh.allreduce(nl)
-        normalize(y0d, S[0], cv, kw)
-        hist[0].copy_(scal[:2])
+        normalize(y0d, S[0], cv, kw, hist[0])
         # q1 = R^T s1 / alpha1 (lowrank.py:211-215): no previous vector, no projection
         half(K, cu, kh, None, Q, 0, Q[0], cu, kh, 1)
 
@@ -413,8 +411,11 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
     uc, sc, vct = np.linalg.svd(c_mat, full_matrices=False)
     sigma = sc[:chosen].astype(np.float32).astype(np.float64)
     # lift on the own rows (lowrank.py:317-318), then the rows of the other ranks
-    out_u = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
-    out_v = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
+    # every row is lifted here when this process holds all the shards; otherwise the
+    # other ranks' rows arrive through the sum-allreduce below and must start at zero
+    alloc = torch.empty if sh.world == 1 or sh.simulated else torch.zeros
+    out_u = alloc((chosen, N), dtype=torch.float32, device=dev)
+    out_v = alloc((chosen, N), dtype=torch.float32, device=dev)
     wu = torch.from_numpy(np.ascontiguousarray(uc[:, :chosen], dtype=np.float32)).to(dev)
     wv = torch.from_numpy(np.ascontiguousarray(vct.T[:, :chosen], dtype=np.float32)).to(dev)
     for a0, a1 in sh.own():
