@@ -183,6 +183,22 @@ class _Shards:
         if not self.simulated and self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def uniform(self):
+        """Every shard holds the same number of rows (the gather path applies)."""
+        return len({a1 - a0 for a0, a1 in self.ranges}) == 1
+
+    def allgather(self, t):
+        """[G, *t.shape]: every rank's t in rank order (NCCL: one all_gather_into_tensor)."""
+        import torch.distributed as dist
+
+        if dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t.contiguous(), group=self.group)
+        return torch.stack(parts)
+
 
 class CudaShardKernels:
     """The per-shard steps of the sharded recurrence: ``kb_shard_*`` (kb_egkb_shard.cu) on
@@ -222,13 +238,15 @@ class CudaShardKernels:
         self._check(self.lib.kb_shard_normalize(src.data_ptr(), nl.data_ptr(), out.data_ptr(), n, c, length, a0, a1,
                                                 wl.data_ptr(), scal.data_ptr(), self._st()), "shard normalize")
 
-    def lift(self, B, rows, W, out, off, ln):
-        """out[:, off:off+ln] = W[:rows].T @ B[:rows, off:off+ln] (kb_ts_lift on a row slice)."""
+    def lift(self, B, rows, W, out, off, ln, out_off=None):
+        """out[:, o:o+ln] = W[:rows].T @ B[:rows, off:off+ln] with o = off, or out_off when given
+        (kb_ts_lift on a row slice; out's own row stride)."""
         if ln == 0:
             return
         N = B.shape[1]
+        o = off if out_off is None else out_off
         self._check(self.lib.kb_ts_lift(_lib.KB_F32, B.data_ptr() + 4 * off, N, rows, W.data_ptr(), W.shape[1],
-                                        out.data_ptr() + 4 * off, N, ln, self._st()), "shard lift")
+                                        out.data_ptr() + 4 * o, out.shape[1], ln, self._st()), "shard lift")
 
 
 def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=None):
@@ -411,17 +429,30 @@ def sharded_egkb(b_mat, config, y0=None, *, group=None, simulate=None, kernels=N
     uc, sc, vct = np.linalg.svd(c_mat, full_matrices=False)
     sigma = sc[:chosen].astype(np.float32).astype(np.float64)
     # lift on the own rows (lowrank.py:317-318), then the rows of the other ranks
-    # every row is lifted here when this process holds all the shards; otherwise the
-    # other ranks' rows arrive through the sum-allreduce below and must start at zero
-    alloc = torch.empty if sh.world == 1 or sh.simulated else torch.zeros
-    out_u = alloc((chosen, N), dtype=torch.float32, device=dev)
-    out_v = alloc((chosen, N), dtype=torch.float32, device=dev)
     wu = torch.from_numpy(np.ascontiguousarray(uc[:, :chosen], dtype=np.float32)).to(dev)
     wv = torch.from_numpy(np.ascontiguousarray(vct.T[:, :chosen], dtype=np.float32)).to(dev)
-    for a0, a1 in sh.own():
-        kern.lift(S, rows, wu, out_u, a0 * n, (a1 - a0) * n)
-        kern.lift(Q, k_p, wv, out_v, a0 * n, (a1 - a0) * n)
-    sh.allreduce(out_u)   # zeros outside each rank's rows: the sum is the concatenation
-    sh.allreduce(out_v)
+    if sh.simulated or sh.world == 1:   # this process lifts every row
+        out_u = torch.empty((chosen, N), dtype=torch.float32, device=dev)
+        out_v = torch.empty((chosen, N), dtype=torch.float32, device=dev)
+        for a0, a1 in sh.own():
+            kern.lift(S, rows, wu, out_u, a0 * n, (a1 - a0) * n)
+            kern.lift(Q, k_p, wv, out_v, a0 * n, (a1 - a0) * n)
+    elif sh.uniform():                  # own rows lifted into a slab, the slabs all-gathered
+        (a0, a1), = sh.own()
+        ln = (a1 - a0) * n
+        slab = torch.empty((2, chosen, ln), dtype=torch.float32, device=dev)
+        kern.lift(S, rows, wu, slab[0], a0 * n, ln, out_off=0)
+        kern.lift(Q, k_p, wv, slab[1], a0 * n, ln, out_off=0)
+        g = sh.allgather(slab)            # [G, 2, chosen, ln]: rank r holds rows [r ln/n, (r+1) ln/n)
+        out_u = g[:, 0].permute(1, 0, 2).reshape(chosen, N)
+        out_v = g[:, 1].permute(1, 0, 2).reshape(chosen, N)
+    else:                               # uneven shards: zeros outside the own rows, summed
+        out_u = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
+        out_v = torch.zeros((chosen, N), dtype=torch.float32, device=dev)
+        for a0, a1 in sh.own():
+            kern.lift(S, rows, wu, out_u, a0 * n, (a1 - a0) * n)
+            kern.lift(Q, k_p, wv, out_v, a0 * n, (a1 - a0) * n)
+        sh.allreduce(out_u)
+        sh.allreduce(out_v)
     trace.chosen_k, trace.k_p, trace.stop_reason, trace.breakdown = chosen, k_p, reason, broke
     return TruncatedSvd.from_device(out_u, sigma.astype(np.float32), out_v), trace

@@ -119,8 +119,9 @@ class HostShardKernels:
             acc += to_limbs(s)
         self._add(wl[: 3 * length], acc)
 
-    def lift(self, B, rows, W, out, off, ln):
+    def lift(self, B, rows, W, out, off, ln, out_off=None):
         if ln == 0:
             return
-        out.numpy()[:, off:off + ln] = (W.numpy()[:rows].T.astype(np.float64)
-                                        @ B.numpy()[:rows, off:off + ln].astype(np.float64)).astype(np.float32)
+        o = off if out_off is None else out_off
+        out.numpy()[:, o:o + ln] = (W.numpy()[:rows].T.astype(np.float64)
+                                    @ B.numpy()[:rows, off:off + ln].astype(np.float64)).astype(np.float32)

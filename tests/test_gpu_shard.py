@@ -63,3 +63,31 @@ def test_sharded_vs_oracle(kb, name):
     m = min(svd.k, os_.size)
     ref = os_[:m].astype(np.float64)
     assert np.all(np.abs(svd.sigma[:m] - ref) <= 1e-4 * ref + 5e-6 * ref[0]), (svd.sigma, ref)
+
+
+@pytest.mark.parametrize("n", [200, 202, 1040])
+def test_odd_sides_invariant_and_vs_oracle(kb, n):
+    """The vectorised row kernels (n % 4 == 0: n = 200 with a partial warp, n = 1040 with
+    two float4s per thread on a few threads) and the scalar fallback (n = 202): shard-count
+    invariance and the oracle's sigma."""
+    from oracle import lowrank as olr
+    from oracle import structured as ost
+    from paper_2410_00233_b200 import datagen
+    from paper_2410_00233_b200.parallel import sharded_egkb
+
+    psf = datagen.mixture_psf(n, seed=n)
+    blur = kb.RearrangedBlur(psf, n)
+    cfg = kb.EgkbConfig(k_max=10)
+    ref_svd, ref = sharded_egkb(blur, cfg, simulate=1)
+    for g in (3, 5):
+        svd, tr = sharded_egkb(blur, cfg, simulate=g)
+        assert (tr.alphas, tr.ts, tr.nus) == (ref.alphas, ref.ts, ref.nus), g
+        assert np.array_equal(svd.sigma, ref_svd.sigma)
+    k32 = blur.psf.kernel.astype(np.float32)
+    ocfg = SimpleNamespace(k_max=10, p=2, tau=1e-4, k_min=2, reorth=None, seed=0, break_tol=None, keep_basis=False)
+    (_, os_, _), otr = olr.egkb(lambda q: ost.ra_matvec(k32, n, q), lambda s: ost.ra_rmatvec(k32, n, s),
+                                (n * n, n * n), np.float32, ocfg)
+    assert ref.stop_reason == otr.stop_reason
+    m = min(ref_svd.k, os_.size)
+    want = os_[:m].astype(np.float64)
+    assert np.all(np.abs(ref_svd.sigma[:m] - want) <= 1e-4 * want + 5e-6 * want[0]), (ref_svd.sigma, want)
