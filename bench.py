@@ -288,38 +288,65 @@ def other_configs(kb, D, flush):
     return out
 
 
-def sharded_bench(kb, D, world, dist):
-    """configs[4] (n=2048, automatic rank, cap 50) with the Krylov vectors row-sharded over
-    all ranks (parallel.sharded_egkb: three int64 limb allreduces per half step over NCCL).
-    Device time, max over ranks; the result is identical for any number of ranks."""
+def egkb_alg_bytes(n, kh, kw, k_p, k):
+    """B_egkb = (2k_p+1) B_mv + sum_{j=1..k_p} 8N(2j+3) + 4N(2k_p+1+2k),
+    B_mv = 4 (2N + kh kw) (K counted once per product)."""
+    N = n * n
+    bmv = 4.0 * (2 * N + kh * kw)
+    return (2 * k_p + 1) * bmv + sum(8.0 * N * (2 * j + 3) for j in range(1, k_p + 1)) + 4.0 * N * (2 * k_p + 1 + 2 * k)
+
+
+def sharded_bench(kb, D, world, dist, peak):
+    """configs[4] (n=2048, automatic rank, cap 50) and configs[3] (n=1024, 30+2) with the
+    Krylov vectors row-sharded over all ranks (parallel.sharded_egkb: three int64 limb
+    allreduces per half step over NCCL).  Device time, max over ranks; the result is
+    identical for any number of ranks.  Whole-box roofline: the run's algorithmic bytes
+     over ranks x the HBM peak.  The single-GPU fused engine on the same
+    problem is timed beside it (rank 0's device)."""
     import torch
 
     from paper_2410_00233_b200 import datagen
     from paper_2410_00233_b200.parallel import sharded_egkb
 
-    prob = datagen.make_problem("n2048")
-    blur = kb.RearrangedBlur(prob.psf, prob.n)
-    cfg = kb.EgkbConfig(**prob.egkb)
-    for _ in range(2):
-        sharded_egkb(blur, cfg)
-    ms = []
-    for _ in range(3):
+    def timed(fn, reps=3):
+        ms = []
+        for _ in range(reps):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = torch.tensor([float(np.median(ms))], dtype=torch.float64, device=D.device())
         if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        svd, tr = sharded_egkb(blur, cfg)
-        e1.record()
-        torch.cuda.synchronize()
-        ms.append(e0.elapsed_time(e1))
-    t = torch.tensor([float(np.median(ms))], dtype=torch.float64, device=D.device())
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"config": "configs[4] n=2048, EgkbConfig(k_max=50)", "ranks": world, "ms": float(t.item()),
-            "result": trace_result(tr), "sigma_1": float(svd.sigma[0]),
-            "note": "rows of every Krylov vector sharded over the ranks; host loop in Python, 3 int64 "
-                    "allreduces per half step; bit-identical result for any rank count"}
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    res = {}
+    for name, label in (("n2048", "configs[4] n=2048, EgkbConfig(k_max=50)"),
+                        ("n1024", "configs[3] n=1024, EgkbConfig(30, k_min=30, p=2, tau=1e300)")):
+        prob = datagen.make_problem(name)
+        blur = kb.RearrangedBlur(prob.psf, prob.n)
+        cfg = kb.EgkbConfig(**prob.egkb)
+        for _ in range(2):
+            sharded_egkb(blur, cfg)
+        ms, (svd, tr) = timed(lambda: sharded_egkb(blur, cfg))
+        kh, kw = blur.psf.shape
+        alg = egkb_alg_bytes(prob.n, kh, kw, tr.k_p, tr.chosen_k)
+        for _ in range(2):
+            kb.egkb(blur, cfg)
+        fused_ms, _ = timed(lambda: kb.egkb(blur, cfg))
+        res[name] = {"config": label, "ranks": world, "ms": ms, "result": trace_result(tr),
+                     "sigma_1": float(svd.sigma[0]),
+                     "roofline_whole_box": {"alg_bytes": alg, "achieved_GBps": alg / ms * 1e-6,
+                                            "peak_GBps": world * peak, "frac": alg / ms * 1e-6 / (world * peak)},
+                     "fused_single_gpu_ms": fused_ms}
+    res["note"] = ("rows of every Krylov vector sharded over the ranks; host loop in Python, one CUDA graph "
+                   "per half step, 3 int64 allreduces per half step; bit-identical result for any rank count")
+    return res
 
 
 def run_ours(args, prob, rank, world, dist):
@@ -546,7 +573,7 @@ def run_ours(args, prob, rank, world, dist):
     lib.kb_prof_enable(0)
     sweep = sweep_bench(kb, D) if not args.no_sweep else None
     others = other_configs(kb, D, flush) if not args.no_sweep else None
-    sharded = sharded_bench(kb, D, world, dist) if not args.no_sweep else None
+    sharded = sharded_bench(kb, D, world, dist, peaks()[0]) if not args.no_sweep else None
     clk = clocks.stop() if clocks is not None else None
     if rank != 0:
         return

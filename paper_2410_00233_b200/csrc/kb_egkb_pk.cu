@@ -67,6 +67,7 @@ struct PkParams {
     int lmax;
     unsigned long long* dbg;   // optional phase timestamps (block 0), KB_PK_TRACE
     int* dbg_n;
+    int cg_sync;               // 1: cooperative-groups grid.sync (KB_PK_CGSYNC=1) instead of pk_grid_sync
 };
 
 __device__ __forceinline__ void pk_mark(const PkParams& P, int tag = 0) {
@@ -715,6 +716,26 @@ __device__ __forceinline__ double xacc_get(const long long* acc3) {
     return ldexp(ldexp((double)h, 80) + ldexp((double)m, 40) + (double)l, -XACC_S);
 }
 
+// Grid barrier of the tiled kernel: each CTA's thread 0 posts ONE release-add on a
+// monotonically increasing arrival counter (bar[0], zeroed before the launch) and polls
+// it with acquire loads until every CTA of this barrier generation has arrived.  No
+// returning atomic and no generation flip by a master CTA: one L2 round trip fewer on
+// the critical path than grid.sync().  The CTA barriers on both sides carry the other
+// threads' writes (before) and the acquired view (after), as in grid.sync().
+__device__ __forceinline__ void pk_grid_sync(const PkParams& P, unsigned& gen) {
+    gen += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* ctr = P.bar;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while ((int)(v - gen) < 0);
+    }
+    __syncthreads();
+}
+
 struct TileGeo {
     int TW, LR, RW, RB, T;   // tile width, lanes per row, rows per warp, row blocks, tiles
 };
@@ -851,6 +872,11 @@ __device__ __forceinline__ void pk_store_diag(const PkParams& P, const TileGeo& 
 template <int MAXG>
 __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGeo Gm) {
     cg::grid_group grid = cg::this_grid();
+    unsigned gen = 0;
+    auto gsync = [&]() {
+        if (P.cg_sync) grid.sync();
+        else pk_grid_sync(P, gen);
+    };
     extern __shared__ double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
@@ -907,7 +933,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         for (int w = 0; w < 8; ++w) s += acc[w];
         xacc_add(xnrm, s);
     }
-    grid.sync();
+    gsync();
     if (tid == 0) red[0] = xacc_get(xnrm);
     __syncthreads();
     pk_mark(P, 1);
@@ -917,7 +943,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     const double fxs = ldexp(1.0, Fx), fxs_inv = ldexp(1.0, -Fx);
     // s1 = fl(y0 / t1) (lowrank.py:207-210), stored, and its diagonal sums for step 0 (R^T)
     pk_store_diag<MAXG>(P, Gm, v, (float)t1, S, eo, ng, tb, tbo, t0, cv, P.kw, fxs, P.wfix);
-    grid.sync();
+    gsync();
     pk_mark(P, 2);
 
     int done = 1, fired = -1, reason = 0, stop = 0, breakdown = 0, tbreak = 0, overflow = 0, err = 0;
@@ -969,7 +995,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int q = 0; q < 4; ++q) pv[g][q] = 0.f;
             if (g < ng && prev) PkIO<float, 4>::load(prev + eo[g], pv[g]);
         }
-        grid.sync();
+        gsync();
         pk_mark(P, 3);
 
         // ---- B: zero the consumed w; z; y; v = y - beta*prev; dots
@@ -1045,7 +1071,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int w = 0; w < 8; ++w) t += acc[w * W + j];
             xacc_add(xdot + 3 * j, t);
         }
-        grid.sync();
+        gsync();
         for (int j = tid; j < W; j += PK_THREADS) red[j] = xacc_get(xdot + 3 * j);
         __syncthreads();
         pk_mark(P, 4);
@@ -1098,7 +1124,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                 for (int w = 0; w < 8; ++w) s += acc[w];
                 xacc_add(xnrm, s);
             }
-            grid.sync();
+            gsync();
             if (tid == 0) red[P.cap + 2] = xacc_get(xnrm);
             __syncthreads();
             pk_mark(P, 5);
@@ -1186,7 +1212,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         // sums for the next product
         pk_mark(P, 14);
         pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
-        grid.sync();
+        gsync();
         pk_mark(P, 6);
 
         if (stop) break;
@@ -1283,6 +1309,8 @@ static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaS
     }
     if (per_sm < 1) return false;
     static const int grid_env = std::getenv("KB_PK_GRID") ? std::atoi(std::getenv("KB_PK_GRID")) : 0;
+    static const int cg_env = std::getenv("KB_PK_CGSYNC") ? std::atoi(std::getenv("KB_PK_CGSYNC")) : 0;
+    P.cg_sync = cg_env;
     int grid = std::min(sms * std::min(per_sm, per_sm_cap), Gm.T);
     if (grid_env > 0) grid = std::min(grid, grid_env);
     if ((Gm.T + grid - 1) / grid > MAXG) return false;

@@ -564,25 +564,27 @@ __global__ void __launch_bounds__(256) k_rat_z_mma(const T* __restrict__ Mt, int
     const int gid = lane >> 2, tig = lane & 3;
     const int c0 = blockIdx.x * 8;
     const int LiP = (Li + 3) & ~3, half = LiP / 2;
-    for (int idx = tid; idx < nv * half; idx += 256) {
-        const int v = idx / half, pr = idx - v * half;
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
-                     : "memory");
-    }
     for (int idx = tid; idx < (NT * 8 - nv) * LiP; idx += 256) wsm[nv * LiP + idx] = 0.0;   // unused vectors
     // r range of this warp (multiples of 4)
     const int steps = LiP / 4, per = (steps + 7) / 8;
     const int s0 = warp * per, s1 = min(steps, s0 + per);
     const int c = c0 + gid;
-    // this warp's A fragments (one Mt entry per lane per r step), all loads in
-    // flight during the staging of w
+    // this warp's A fragments (one Mt entry per lane per r step): K does not depend on
+    // the previous kernel, so these loads are in flight before the dependency wait
     constexpr int AB = 40;
     T a[AB];
 #pragma unroll
     for (int j = 0; j < AB; ++j) {
         const int r = 4 * (s0 + j) + tig;
         a[j] = (c < Lo && r < Li && s0 + j < s1) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
+    }
+    pdl_wait();      // w is written by the previous kernel (k_rat_w)
+    pdl_trigger();
+    for (int idx = tid; idx < nv * half; idx += 256) {
+        const int v = idx / half, pr = idx - v * half;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
+                     : "memory");
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
