@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -321,24 +322,37 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
 
 // ------------------------------------------------------------------ tiled block product
 // Y = R(A) X (or R(A)^T X) for zero BC and n a multiple of 128, as four
-// stream-ordered kernels instead of one cooperative kernel with grid
-// barriers (every phase runs at full occupancy, no barrier latency):
+// stream-ordered kernels chained by programmatic dependent launch instead of
+// one cooperative kernel with grid barriers:
 //
-//   k_rat_diag   tile (32 image rows x 128 columns of one vector) through
-//                shared memory -> its 159 diagonal sums (fp64, fixed order)
-//   k_rat_w      w[v][u] = sum of the tile sums on diagonal u - c_in, tiles
-//                in fixed (row block, column block) order -- deterministic
+//   k_rat_diag   a CTA owns a vertical STACK of ts tiles (32 image rows x 128
+//                columns each) of one vector and streams them through a
+//                shared-memory ring, each tile ONE TMA tensor copy
+//                (cp.async.bulk.tensor.3d, mbarrier completion); the 32 ts + 127
+//                diagonal sums of the stack accumulate in shared memory in
+//                tile order (fp64, fixed order).  Tiles that meet no diagonal
+//                of the PSF's support are never read.
+//   k_rat_w      w[v][u] = sum of the stack sums on diagonal u - c_in, stacks
+//                in fixed (row stack, column block) order -- deterministic
 //   k_rat_z      z[v][c] = sum_r Mt[c, r] w[v][r]: contiguous rows of K^T
-//                (forward) or K (transpose), w staged in shared memory,
-//                16 rows x <= 16 vectors per CTA
-//   k_rat_bcast  y[v][a*n + b] = z[v][b - a + c_out], float4 / double2 stores
+//                (forward) or K (transpose); the r range is cut into chunks
+//                (grid.y), each CTA stages only its chunk of w and writes a
+//                partial z; 5-16 vectors on the FP64 tensor cores
+//   k_rat_bcast  z = the chunk partials added in chunk order, then
+//                y[v][a*n + b] = z[v][b - a + c_out], float4 / double2 stores
 //
-// The only HBM streams are the n^2 inputs (read once), the n^2 outputs
-// (written once) and K (read once per block of vectors): the product's
-// algorithmic bytes.
+// The only HBM streams are the n^2 inputs (read at most once), the n^2
+// outputs (written once) and K (read once per block of vectors): the
+// product's algorithmic bytes.
 namespace kb {
 
-constexpr int RT_ROWS = 32, RT_COLS = 128, RT_DIAG = RT_ROWS + RT_COLS - 1, RT_DP = 160;
+constexpr int RT_ROWS = 32, RT_COLS = 128, RT_DIAG = RT_ROWS + RT_COLS - 1;
+constexpr int RT_MAXTS = 8;          // tiles per stack (<= 256 image rows)
+constexpr int RT_STAGES = 4;         // ring stages of the diagonal-sum kernel
+constexpr int RT_DTHREADS = 160;     // one thread per tile diagonal (159)
+constexpr int RZ_CHUNK = 1056;       // r entries per chunk of k_rat_z (<= 4 vectors): one chunk up to n = 1024
+constexpr int RZM_STEPS = 32;        // 4-wide r steps per chunk of k_rat_z_mma (128 entries)
+constexpr int RZM_ROWS = 64;         // rows of Mt per CTA of k_rat_z_mma (8 per warp)
 
 // Programmatic dependent launch: the next kernel of the chain is launched
 // while this one drains (launch latency hidden); it waits in pdl_wait()
@@ -346,208 +360,221 @@ constexpr int RT_ROWS = 32, RT_COLS = 128, RT_DIAG = RT_ROWS + RT_COLS - 1, RT_D
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_rat_diag(const T* __restrict__ X, int64_t ldx, int n, double* __restrict__ part) {
-    __shared__ T tile[RT_ROWS][RT_COLS + (sizeof(T) == 4 ? 4 : 2)];
-    const int cbn = n / RT_COLS, tiles = (n / RT_ROWS) * cbn;
-    const int t = blockIdx.x, v = blockIdx.y;
-    const int rb = t / cbn, cb = t - rb * cbn;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const T* x = X + (int64_t)v * ldx + (int64_t)(rb * RT_ROWS) * n + cb * RT_COLS;
-    if constexpr (sizeof(T) == 4) {
-        float4 q[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) q[j] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)(warp + 8 * j) * n) + lane);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) *reinterpret_cast<float4*>(&tile[warp + 8 * j][4 * lane]) = q[j];
-    } else {
-        double2 q[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-                q[2 * j + h] = __ldcs(reinterpret_cast<const double2*>(x + (int64_t)(warp + 8 * j) * n + 64 * h) + lane);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) *reinterpret_cast<double2*>(&tile[warp + 8 * j][64 * h + 2 * lane]) = q[2 * j + h];
-    }
-    __syncthreads();
-    pdl_trigger();
-    if (tid < RT_DIAG) {
-        const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
-        const int r0 = max(0, -off), r1 = min(RT_ROWS, RT_COLS - off);
-        double s = 0.0;
-        for (int r = r0; r < r1; ++r) s += (double)tile[r][r + off];
-        part[((int64_t)v * tiles + t) * RT_DP + tid] = s;
-    }
+__host__ __device__ __forceinline__ int rt_floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+__host__ __device__ __forceinline__ int rt_ceil_div(int a, int b) { return -rt_floor_div(-a, b); }
+
+__device__ __forceinline__ unsigned rt_smem(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ bool rt_mbar_try(unsigned mb, unsigned par) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(mb), "r"(par)
+        : "memory");
+    return ok != 0;
 }
 
-// (opt-in, KB_RAT_TMA=1) fp32 inputs: persistent CTAs stream their tiles through a 2-stage shared-memory
-// ring, each tile ONE TMA tensor copy (cp.async.bulk.tensor.3d over the [nv][n][n]
-// view of X, box 128 x 32 x 1, evict-first, completion on the stage's mbarrier), the
-// next tile in flight while this one's diagonal sums are formed.
-constexpr int RT_TMA_STAGES = 2;
-__global__ void __launch_bounds__(256) k_rat_diag_tma(const __grid_constant__ CUtensorMap map, int n, int nv,
-                                                      double* __restrict__ part) {
-    __shared__ alignas(128) float tile[RT_TMA_STAGES][RT_ROWS][RT_COLS];
-    __shared__ alignas(8) unsigned long long mbar[RT_TMA_STAGES];
-    const int cbn = n / RT_COLS, tiles = (n / RT_ROWS) * cbn, total = tiles * nv;
-    const int tid = threadIdx.x;
+// Stack (rs, cb) of vector v: image rows [32 ts rs, 32 ts (rs + 1)), columns [128 cb, 128 cb + 128).
+// Its diagonals d = column - row span [128 cb - 32 ts rs - (32 ts - 1), 128 cb - 32 ts rs + 127]; slot
+// i = d - that lower end.  part[(v * stacks + rs * cbn + cb) * (32 ts + 128) + i].
+template <typename T>
+__global__ void __launch_bounds__(RT_DTHREADS) k_rat_diag(const __grid_constant__ CUtensorMap map, int n, int ts,
+                                                          int nst, int ci, int Li, double* __restrict__ part) {
+    extern __shared__ __align__(128) unsigned char rt_raw[];
+    T* tile = reinterpret_cast<T*>(rt_raw);                                   // [nst][32][128]
+    double* acc = reinterpret_cast<double*>(rt_raw + (size_t)nst * RT_ROWS * RT_COLS * sizeof(T));   // [32 ts + 128]
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + RT_ROWS * RT_MAXTS + RT_COLS);
+    const int cbn = n / RT_COLS, stacks = (n / (RT_ROWS * ts)) * cbn;
+    const int s = blockIdx.x, v = blockIdx.y, tid = threadIdx.x;
+    const int rs = s / cbn, cb = s - rs * cbn;
+    const int R0 = rs * RT_ROWS * ts, C0 = cb * RT_COLS;
+    // tiles j of the stack that meet the support u = d + ci in [0, Li)
+    const int j0 = max(0, rt_ceil_div(C0 - R0 - (RT_ROWS - 2) + ci - Li, RT_ROWS));
+    const int j1 = min(ts - 1, rt_floor_div(C0 - R0 + (RT_COLS - 1) + ci, RT_ROWS));
+    const int nt = j1 - j0 + 1;
+    if (nt <= 0) return;   // no diagonal of this stack is ever read by k_rat_w
+    const int pstride = RT_ROWS * ts + RT_COLS;
+    for (int i = tid; i < pstride; i += RT_DTHREADS) acc[i] = 0.0;
     unsigned long long pol = 0;
-    auto issue = [&](int k, int st) {   // thread 0: tile k of this CTA into stage st
-        const int id = blockIdx.x + k * gridDim.x;
-        if (id >= total) return;
-        const int v = id / tiles, t = id - v * tiles, rb = t / cbn, cb = t - rb * cbn;
-        const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[st]));
-        const unsigned ts = static_cast<unsigned>(__cvta_generic_to_shared(&tile[st][0][0]));
+    auto issue = [&](int k) {   // thread 0: tile j0 + k into stage k % nst
+        const int st = k % nst;
+        const unsigned mb = rt_smem(&mbar[st]), dst = rt_smem(tile + (size_t)st * RT_ROWS * RT_COLS);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the stage
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(RT_ROWS * RT_COLS * 4)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                     "r"((unsigned)(RT_ROWS * RT_COLS * sizeof(T)))
                      : "memory");
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1, {%2, %3, %4}], [%5], %6;"
-            ::"r"(ts), "l"(reinterpret_cast<unsigned long long>(&map)), "r"(cb * RT_COLS), "r"(rb * RT_ROWS), "r"(v),
-            "r"(mb), "l"(pol)
+            " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+            "l"(reinterpret_cast<unsigned long long>(&map)), "r"(C0), "r"(R0 + RT_ROWS * (j0 + k)), "r"(v), "r"(mb),
+            "l"(pol)
             : "memory");
     };
     if (tid == 0) {
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        for (int st = 0; st < RT_TMA_STAGES; ++st) {
-            const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[st]));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
-        }
+        for (int st = 0; st < nst; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&mbar[st])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int st = 0; st < RT_TMA_STAGES; ++st) issue(st, st);
+        for (int k = 0; k < nst && k < nt; ++k) issue(k);
     }
     __syncthreads();
-    for (int k = 0; blockIdx.x + k * gridDim.x < total; ++k) {
-        const int st = k % RT_TMA_STAGES;
-        const unsigned par = (unsigned)(k / RT_TMA_STAGES) & 1u;
-        if (tid == 0) {
-            const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[st]));
-            asm volatile(
-                "{\n\t.reg .pred P1;\n\t"
-                "WAIT_TILE:\n\t"
-                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-                "@!P1 bra WAIT_TILE;\n\t}" ::"r"(mb), "r"(par)
-                : "memory");
-        }
-        __syncthreads();
-        if (k == 0) pdl_trigger();
-        const int id = blockIdx.x + k * gridDim.x;
+    pdl_trigger();
+    const int off = tid - (RT_ROWS - 1);   // column - row inside a tile
+    for (int k = 0; k < nt; ++k) {
+        const int st = k % nst;
+        const unsigned par = (unsigned)(k / nst) & 1u;
+        while (!rt_mbar_try(rt_smem(&mbar[st]), par)) {}
         if (tid < RT_DIAG) {
-            const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
-            const int r0 = max(0, -off), r1 = min(RT_ROWS, RT_COLS - off);
-            double s = 0.0;
-            for (int r = r0; r < r1; ++r) s += (double)tile[st][r][r + off];
-            part[(int64_t)id * RT_DP + tid] = s;
+            const T* tp = tile + (size_t)st * RT_ROWS * RT_COLS;
+            double sq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int r = 0; r < RT_ROWS; ++r) {
+                const int c = r + off;
+                if (c >= 0 && c < RT_COLS) sq[r & 3] += (double)tp[r * RT_COLS + c];
+            }
+            acc[RT_ROWS * (ts - 1 - (j0 + k)) + tid] += (sq[0] + sq[1]) + (sq[2] + sq[3]);
         }
-        __syncthreads();   // every thread is done with the stage before it is refilled
-        if (tid == 0) issue(k + RT_TMA_STAGES, st);
+        __syncthreads();   // the stage is free and acc is ordered for the next tile
+        if (tid == 0 && k + nst < nt) issue(k + nst);
     }
+    double* out = part + ((int64_t)v * stacks + s) * pstride;
+    for (int i = tid; i < pstride - 1; i += RT_DTHREADS) out[i] = acc[i];
 }
 
-// w[v][u] (u < Li) = sum over tiles of the sums on diagonal d = u - ci (column
-// - row): one warp per (u, v), lane = row block (strided), all loads in
-// flight, then a fixed-order warp tree.
-__global__ void __launch_bounds__(256) k_rat_w(const double* __restrict__ part, int n, int ci, int Li,
+// w[v][u] (u < Li) = sum over the stacks of their sums on diagonal d = u - ci.  CTA = 32
+// diagonals x 8 row-stack lanes; the 8 lane sums are added in lane order.
+__global__ void __launch_bounds__(256) k_rat_w(const double* __restrict__ part, int n, int ts, int ci, int Li,
                                                double* __restrict__ w, int ldw) {
-    const int lane = threadIdx.x & 31;
-    const int u = blockIdx.x * 8 + (threadIdx.x >> 5), v = blockIdx.y;
+    __shared__ double red[8][33];
+    const int ux = threadIdx.x & 31, ln = threadIdx.x >> 5;
+    const int u = blockIdx.x * 32 + ux, v = blockIdx.y;
+    const int H = RT_ROWS * ts, cbn = n / RT_COLS, rsn = n / H, pstride = H + RT_COLS;
     pdl_wait();
     pdl_trigger();
-    if (u >= Li) return;
-    const int cbn = n / RT_COLS, rbn = n / RT_ROWS, tiles = rbn * cbn;
     const int d = u - ci;
-    const double* pv = part + (int64_t)v * tiles * RT_DP;
+    const double* pv = part + (int64_t)v * rsn * cbn * pstride;
     double s = 0.0;
-    for (int rb0 = 0; rb0 < rbn; rb0 += 64) {
-        double q[4];
+    if (u < Li) {
+        // <= 3 stacks per row stack hold a given diagonal; 4 row stacks (12 loads) in flight
+        for (int rs0 = ln; rs0 < rsn; rs0 += 32) {
+            double q[12];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int rb = rb0 + lane + 32 * h;
-            q[2 * h] = q[2 * h + 1] = 0.0;
-            if (rb < rbn) {
-                // tile (rb, cb) holds diagonals [128 cb - 32 rb - 31, 128 cb - 32 rb + 127]: <= 2 column blocks
-                const int lo = d + RT_ROWS * rb - (RT_COLS - 1), hi = d + RT_ROWS * rb + (RT_ROWS - 1);
-                const int cb0 = lo <= 0 ? 0 : (lo + RT_COLS - 1) / RT_COLS;
-                const int cb1 = hi < 0 ? -1 : min(cbn - 1, hi / RT_COLS);
+            for (int k = 0; k < 4; ++k) {
+                const int rs = rs0 + 8 * k;
+                const int t = d + H * rs;
+                const int cb_lo = max(0, rt_ceil_div(t - (RT_COLS - 1), RT_COLS));
+                const int cb_hi = min(cbn - 1, rt_floor_div(t + H - 1, RT_COLS));
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int cb = cb0 + j;
-                    if (cb <= cb1) {
-                        const int i = d - (RT_COLS * cb - RT_ROWS * rb - (RT_ROWS - 1));
-                        q[2 * h + j] = __ldg(pv + (int64_t)(rb * cbn + cb) * RT_DP + i);
-                    }
+                for (int j = 0; j < 3; ++j) {
+                    const int cb = cb_lo + j;
+                    q[3 * k + j] = (rs < rsn && cb <= cb_hi)
+                                       ? __ldg(pv + (int64_t)(rs * cbn + cb) * pstride + (t + H - 1 - RT_COLS * cb))
+                                       : 0.0;
                 }
             }
+#pragma unroll
+            for (int k = 0; k < 12; ++k) s += q[k];
         }
-        s += (q[0] + q[1]) + (q[2] + q[3]);
     }
-    s = warp_sum(s);
-    if (lane == 0) w[(int64_t)v * ldw + u] = s;
+    red[ln][ux] = s;
+    __syncthreads();
+    if (ln == 0 && u < Li) {
+        double a = red[0][ux];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) a += red[k][ux];
+        w[(int64_t)v * ldw + u] = a;
+    }
 }
 
-// z[v][c] = sum_r Mt[c, r] w[v][r] (v < NV, a compile-time bound >= nv):
-// one warp per row c (8 rows per CTA).  The whole row is loaded first
-// (<= RZ_ML per lane, one round trip), overlapping the staging of w (all
-// vectors, shared memory, zero-padded to NV), then one FMA chain per vector.
-constexpr int RZ_ML = 64;   // Li <= 2048
+// Chunk partials -> z without a trip through global memory: the CTAs of one row group
+// (the r chunks) form a thread-block cluster (1, csize, 1); each stores its partial tile
+// into rank 0's shared memory (DSMEM), one cluster barrier, and rank 0 adds the ranks in
+// rank order (fixed order: deterministic).
+template <int NE>
+__device__ __forceinline__ void rat_z_cluster_sum(double (&zred)[8][NE], const double* mine, int ne, int csize,
+                                                  double* __restrict__ z, int ldz, int rows, int c0, int Lo) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    double* dst = cl.map_shared_rank(&zred[0][0], 0);
+    for (int e = threadIdx.x; e < ne; e += 256) dst[rank * NE + e] = mine[e];
+    cl.sync();
+    if (rank != 0) return;
+    for (int e = threadIdx.x; e < ne; e += 256) {
+        const int v = e / rows, c = c0 + (e - v * rows);
+        double s = zred[0][e];
+        for (int q = 1; q < csize; ++q) s += zred[q][e];
+        if (c < Lo) z[(int64_t)v * ldz + c] = s;
+    }
+}
+
+// z[v][c] = sum_r Mt[c, r] w[v][r] (v < NV, a compile-time bound >= nv): one warp per row c
+// (8 rows per CTA); the r range is cut into chunks of RZ_CHUNK entries, cluster rank q takes
+// chunks q, q + csize, ...  Each row chunk is loaded first (K does not depend on the previous
+// kernel), then w's chunk is staged, then one FMA chain per vector.
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li, int Lo, const double* __restrict__ w,
                                                int ldw, int nv, double* __restrict__ z, int ldz) {
-    extern __shared__ double wsm[];   // [NV][Li]
+    __shared__ double wsm[NV][RZ_CHUNK];
+    __shared__ double zred[8][8 * NV];
+    __shared__ double mine[8 * NV];
+    constexpr int ML = RZ_CHUNK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x * 8 + warp;
-    T m[RZ_ML];
-#pragma unroll
-    for (int k = 0; k < RZ_ML; ++k) {
-        const int r = lane + 32 * k;
-        m[k] = (c < Lo && r < Li) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
-    }
-    pdl_wait();      // w is written by the previous kernel; the K rows above are not
-    pdl_trigger();
-    // staging: 16-byte cp.async copies (no registers, all in flight at once);
-    // rows of wsm padded to an even length, the padding entry never used
-    const int LiP = (Li + 1) & ~1, half = LiP / 2;
-    for (int idx = tid; idx < nv * half; idx += 256) {
-        const int v = idx / half, pr = idx - v * half;
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
-                     : "memory");
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
+    const int nch = (Li + RZ_CHUNK - 1) / RZ_CHUNK, csize = gridDim.y;
     double acc[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+    for (int ch = blockIdx.y; ch < nch; ch += csize) {
+        const int r0 = ch * RZ_CHUNK;
+        T m[ML];
 #pragma unroll
-    for (int k = 0; k < RZ_ML; ++k) {
-        const int r = lane + 32 * k;
-        if (r < Li) {
+        for (int k = 0; k < ML; ++k) {
+            const int r = r0 + lane + 32 * k;
+            m[k] = (c < Lo && r < Li) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
+        }
+        if (ch == (int)blockIdx.y) {
+            pdl_wait();      // w is written by the previous kernel; the K rows above are not
+            pdl_trigger();
+        } else {
+            __syncthreads();   // the previous chunk of w is no longer read
+        }
+        for (int idx = tid; idx < NV * RZ_CHUNK; idx += 256) {
+            const int v = idx / RZ_CHUNK, r = idx - v * RZ_CHUNK;
+            wsm[v][r] = (v < nv && r0 + r < Li) ? __ldg(w + (int64_t)v * ldw + r0 + r) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < ML; ++k) {
             const double mk = (double)m[k];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) acc[v] = fma(mk, wsm[v * LiP + r], acc[v]);
+            for (int v = 0; v < NV; ++v) acc[v] = fma(mk, wsm[v][lane + 32 * k], acc[v]);
         }
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const double s = warp_sum(acc[v]);
-        if (lane == 0 && c < Lo && v < nv) z[(int64_t)v * ldz + c] = s;
+        if (lane == 0) {
+            if (csize == 1) {
+                if (c < Lo && v < nv) z[(int64_t)v * ldz + c] = s;
+            } else {
+                mine[v * 8 + warp] = s;
+            }
+        }
     }
+    if (csize == 1) return;
+    __syncthreads();
+    rat_z_cluster_sum<8 * NV>(zred, mine, 8 * nv, csize, z, ldz, 8, blockIdx.x * 8, Lo);
 }
 
-// Programmatic dependent launch for the chain's later kernels (the first kernel of a
-// product is launched normally: its input may be the previous product's output).
-// For a 16-vector block it hides ~2 us of launch/drain gaps (37.0 -> 35.3 us).
 static thread_local bool g_rat_pdl = true;
 
-// z for 8 or 16 vectors on the FP64 tensor cores (mma.sync m8n8k4, SASS
-// DMMA): CTA = 8 rows c of Mt, warp w = the w-th eighth of the r range; per
-// 4-wide r step each lane holds Mt[c0 + gid][r + tig] (fp32 widened) as the
-// A fragment and w[v][r + tig] (v = n*8 + gid, staged by cp.async) as the B
-// fragments; the 8 warp partials are added in warp order.
+// The same for 5-16 vectors on the FP64 tensor cores (mma.sync m8n8k4, SASS DMMA):
+// CTA = RZM_ROWS rows c of Mt (8 per warp), chunks of RZM_STEPS 4-wide r steps (a staged
+// chunk of w serves all 64 rows); per step each lane holds Mt[c][r + tig] (fp32 widened) as
+// the A fragment and w[v][r + tig] (v = q*8 + gid, staged by cp.async) as the B fragments,
+// even and odd steps on separate accumulators; the cluster ranks are added in rank order.
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -558,128 +585,176 @@ template <typename T, int NT>   // NT = 8-vector tiles (1 or 2)
 __global__ void __launch_bounds__(256) k_rat_z_mma(const T* __restrict__ Mt, int Li, int Lo,
                                                    const double* __restrict__ w, int ldw, int nv,
                                                    double* __restrict__ z, int ldz) {
-    extern __shared__ double wsm[];   // [NT*8][LiP]
-    __shared__ double red[8][8][NT * 8 + 1];
+    constexpr int WR = 4 * RZM_STEPS, WP = WR + 4;   // row pitch: gid rows 4 doubles apart in the banks
+    constexpr int NE = RZM_ROWS * NT * 8;            // entries of a CTA's z tile, [vector][row]
+    extern __shared__ __align__(16) double zm_raw[];
+    double(*wsm)[WP] = reinterpret_cast<double(*)[WP]>(zm_raw);   // [NT * 8][WP]
+    double* zred = zm_raw + NT * 8 * WP;                          // [8][NE] (used on cluster rank 0)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
-    const int c0 = blockIdx.x * 8;
-    const int LiP = (Li + 3) & ~3, half = LiP / 2;
-    for (int idx = tid; idx < (NT * 8 - nv) * LiP; idx += 256) wsm[nv * LiP + idx] = 0.0;   // unused vectors
-    // r range of this warp (multiples of 4)
-    const int steps = LiP / 4, per = (steps + 7) / 8;
-    const int s0 = warp * per, s1 = min(steps, s0 + per);
-    const int c = c0 + gid;
-    // this warp's A fragments (one Mt entry per lane per r step): K does not depend on
-    // the previous kernel, so these loads are in flight before the dependency wait
-    constexpr int AB = 40;
-    T a[AB];
+    const int c0 = blockIdx.x * RZM_ROWS, c = c0 + warp * 8 + gid;
+    const int steps = (Li + 3) / 4, nch = (steps + RZM_STEPS - 1) / RZM_STEPS, csize = gridDim.y;
+    // rows past Lo read a valid row (their results are dropped at the end): no predicate per load
+    const T* rowp = Mt + (int64_t)min(c, Lo - 1) * Li + tig;
+    double acc[NT][2][2];
 #pragma unroll
-    for (int j = 0; j < AB; ++j) {
-        const int r = 4 * (s0 + j) + tig;
-        a[j] = (c < Lo && r < Li && s0 + j < s1) ? __ldg(Mt + (int64_t)c * Li + r) : T(0);
-    }
-    pdl_wait();      // w is written by the previous kernel (k_rat_w)
-    pdl_trigger();
-    for (int idx = tid; idx < nv * half; idx += 256) {
-        const int v = idx / half, pr = idx - v * half;
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(wsm + v * LiP + 2 * pr));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + (int64_t)v * ldw + 2 * pr)
-                     : "memory");
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    // the copies' tail past Li is scratch: zero it (0 * NaN would poison the MMA)
-    for (int idx = tid; idx < nv * (LiP - Li); idx += 256) {
-        const int v = idx / (LiP - Li), r = Li + idx - v * (LiP - Li);
-        wsm[v * LiP + r] = 0.0;
-    }
-    __syncthreads();
-    double acc[NT][2];
+    for (int q = 0; q < NT; ++q) acc[q][0][0] = acc[q][0][1] = acc[q][1][0] = acc[q][1][1] = 0.0;
+    for (int idx = tid; idx < (NT * 8 - nv) * WP; idx += 256) wsm[nv][idx] = 0.0;   // unused vectors stay zero
+    for (int ch = blockIdx.y; ch < nch; ch += csize) {
+        const int sA = ch * RZM_STEPS, r0 = 4 * sA;
+        const bool full = r0 + WR <= Li;   // every entry of the chunk is inside the row: no predicates
+        // this warp's A fragments (its 8 rows over the chunk): K does not depend on the previous
+        // kernel, so these loads are in flight before the dependency wait
+        T a[RZM_STEPS];
+        if (full) {
 #pragma unroll
-    for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = 0.0;
+            for (int j = 0; j < RZM_STEPS; ++j) a[j] = __ldg(rowp + r0 + 4 * j);
+        }
+        if (ch == (int)blockIdx.y) {
+            pdl_wait();      // w is written by the previous kernel (k_rat_w)
+            pdl_trigger();
+        } else {
+            __syncthreads();   // the previous chunk of w is no longer read
+        }
+        const double* wrow = &wsm[gid][tig];
+        if (full) {
+            for (int idx = tid; idx < nv * (WR / 2); idx += 256) {
+                const int v = idx / (WR / 2), pr = idx % (WR / 2);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rt_smem(&wsm[v][2 * pr])),
+                             "l"(w + (int64_t)v * ldw + r0 + 2 * pr)
+                             : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
 #pragma unroll
-    for (int j = 0; j < AB; ++j) {
-        const int r = 4 * (s0 + j) + tig;
-        if (s0 + j < s1) {
+            for (int j = 0; j < RZM_STEPS; ++j) {
 #pragma unroll
-            for (int q = 0; q < NT; ++q) dmma884(acc[q][0], acc[q][1], (double)a[j], wsm[(q * 8 + gid) * LiP + r]);
+                for (int q = 0; q < NT; ++q)
+                    dmma884(acc[q][j & 1][0], acc[q][j & 1][1], (double)a[j], wrow[q * 8 * WP + 4 * j]);
+            }
+        } else {   // the row's last, partial chunk: only its real steps; the tail past Li is zero
+            const int ns = min(steps - sA, RZM_STEPS);
+            for (int idx = tid; idx < nv * 4 * ns; idx += 256) {
+                const int v = idx / (4 * ns), rr = idx % (4 * ns);
+                wsm[v][rr] = r0 + rr < Li ? __ldg(w + (int64_t)v * ldw + r0 + rr) : 0.0;
+            }
+            __syncthreads();
+            for (int j = 0; j < ns; ++j) {
+                const double av = r0 + 4 * j + tig < Li ? (double)__ldg(rowp + r0 + 4 * j) : 0.0;
+#pragma unroll
+                for (int q = 0; q < NT; ++q) dmma884(acc[q][0][0], acc[q][0][1], av, wrow[q * 8 * WP + 4 * j]);
+            }
         }
     }
-    for (int sb = s0 + AB; sb < s1; ++sb) {   // long rows (Li > 1280)
-        const int r = 4 * sb + tig;
-        const double av = (c < Lo && r < Li) ? (double)__ldg(Mt + (int64_t)c * Li + r) : 0.0;
+    // lane holds Z^T tile row c (= c0 + warp*8 + gid), vectors q*8 + 2*tig + {0,1}
+    if (csize == 1) {
 #pragma unroll
-        for (int q = 0; q < NT; ++q) dmma884(acc[q][0], acc[q][1], av, wsm[(q * 8 + gid) * LiP + r]);
+        for (int q = 0; q < NT; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int v = q * 8 + 2 * tig + h;
+                if (c < Lo && v < nv) z[(int64_t)v * ldz + c] = acc[q][0][h] + acc[q][1][h];
+            }
+        return;
     }
-    // lane holds Z^T tile rows c0 + gid, vectors q*8 + 2*tig + {0,1}
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    double* dst = cl.map_shared_rank(zred, 0) + rank * NE;
 #pragma unroll
-    for (int q = 0; q < NT; ++q) {
-        red[warp][gid][q * 8 + 2 * tig] = acc[q][0];
-        red[warp][gid][q * 8 + 2 * tig + 1] = acc[q][1];
-    }
-    __syncthreads();
-    for (int e = tid; e < 8 * NT * 8; e += 256) {
-        const int row = e / (NT * 8), v = e - row * (NT * 8);
-        double s = 0.0;
+    for (int q = 0; q < NT; ++q)
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += red[ww][row][v];
+        for (int h = 0; h < 2; ++h)
+            dst[(q * 8 + 2 * tig + h) * RZM_ROWS + warp * 8 + gid] = acc[q][0][h] + acc[q][1][h];
+    cl.sync();
+    if (rank != 0) return;
+    for (int e = tid; e < NE; e += 256) {   // e = v * RZM_ROWS + row; ranks added in rank order
+        const int v = e / RZM_ROWS, row = e % RZM_ROWS;
+        double s = zred[e];
+        for (int q = 1; q < csize; ++q) s += zred[q * NE + e];
         if (c0 + row < Lo && v < nv) z[(int64_t)v * ldz + c0 + row] = s;
     }
 }
 
+// Launch with programmatic dependent launch and (cy > 1) a (1, cy, 1) thread-block cluster.
 template <typename K, typename... A>
-static void pdl_launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+static void pdl_launch(K kern, dim3 grid, size_t smem, cudaStream_t st, int cy, A... args) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;
     lc.blockDim = dim3(256);
     lc.dynamicSmemBytes = smem;
     lc.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (g_rat_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cy > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = cy;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     lc.attrs = attr;
-    lc.numAttrs = g_rat_pdl ? 1 : 0;
+    lc.numAttrs = na;
     KB_CUDA(cudaLaunchKernelEx(&lc, kern, args...));
 }
 
 template <typename T>
 static void rat_z_launch(const T* Mt, int Li, int Lo, const double* w, int ldw, int nv, double* z, cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)((Li + 1) & ~1);
-    auto go = [&](auto kern, int NVc) {
-        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem * NVc)));
-        pdl_launch(kern, dim3((Lo + 7) / 8), smem * NVc, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
-    };
-    if (nv <= 1) go(k_rat_z<T, 1>, 1);
-    else if (nv <= 2) go(k_rat_z<T, 2>, 2);
-    else if (nv <= 4) go(k_rat_z<T, 4>, 4);
-    else {   // 5..16 vectors: FP64 tensor cores
-        const int NT = nv <= 8 ? 1 : 2;
-        const size_t sm2 = sizeof(double) * (size_t)NT * 8 * ((Li + 3) & ~3);
-        if (NT == 1) {
-            KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-            pdl_launch(k_rat_z_mma<T, 1>, dim3((Lo + 7) / 8), sm2, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
-        } else {
-            KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-            pdl_launch(k_rat_z_mma<T, 2>, dim3((Lo + 7) / 8), sm2, st, Mt, Li, Lo, w, ldw, nv, z, ldw);
-        }
+    if (nv <= 4) {
+        const int cy = std::min(8, (Li + RZ_CHUNK - 1) / RZ_CHUNK);
+        const dim3 grid((Lo + 7) / 8, cy);
+        if (nv <= 1) pdl_launch(k_rat_z<T, 1>, grid, 0, st, cy, Mt, Li, Lo, w, ldw, nv, z, ldw);
+        else if (nv <= 2) pdl_launch(k_rat_z<T, 2>, grid, 0, st, cy, Mt, Li, Lo, w, ldw, nv, z, ldw);
+        else pdl_launch(k_rat_z<T, 4>, grid, 0, st, cy, Mt, Li, Lo, w, ldw, nv, z, ldw);
+        return;
     }
+    const int steps = (Li + 3) / 4;   // 5..16 vectors: FP64 tensor cores
+    const int cy = std::min(8, (steps + RZM_STEPS - 1) / RZM_STEPS);
+    const dim3 grid((Lo + RZM_ROWS - 1) / RZM_ROWS, cy);
+    constexpr size_t row_b = sizeof(double) * (4 * RZM_STEPS + 4), red_b = sizeof(double) * 8 * RZM_ROWS * 8;
+    static bool cfg = false;
+    if (!cfg) {
+        KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(8 * row_b + red_b)));
+        KB_CUDA(cudaFuncSetAttribute(k_rat_z_mma<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(16 * row_b + 2 * red_b)));
+        cfg = true;
+    }
+    if (nv <= 8) pdl_launch(k_rat_z_mma<T, 1>, grid, 8 * row_b + red_b, st, cy, Mt, Li, Lo, w, ldw, nv, z, ldw);
+    else pdl_launch(k_rat_z_mma<T, 2>, grid, 16 * row_b + 2 * red_b, st, cy, Mt, Li, Lo, w, ldw, nv, z, ldw);
 }
 
-// y[v][a*n + b] = (T) z[v][b - a + co] (0 outside [0, Lo))
+// y[v][a*n + b] = (T) z[v][b - a + co] (0 outside [0, Lo)).  z is staged rounded to T and
+// zero-padded (zpad[i] = z[i - 4]), then as V = 16 / sizeof(T) shifted copies, copy s holding
+// zpad[V k + s .. V k + s + V - 1] as its k-th 16-byte vector: the V consecutive entries a
+// thread needs are ONE aligned vector load whatever the alignment of its diagonal index,
+// and the lanes of a warp read consecutive vectors (no bank conflicts; the scalar form
+// had a 4-way conflict on every load).
 template <typename T>
 __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z, int ldz, int n, int co, int Lo,
                                                    T* __restrict__ Y, int64_t ldy) {
-    extern __shared__ double zraw[];
-    T* zsm = reinterpret_cast<T*>(zraw);   // z already rounded to T: one conversion per entry of z
+    constexpr int V = 16 / sizeof(T);
+    using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    extern __shared__ __align__(16) unsigned char braw[];
+    const int KV = (Lo + 8 + V - 1) / V + 1;           // vectors per copy
+    VT* zc = reinterpret_cast<VT*>(braw);              // [V][KV]
+    T* zpad = reinterpret_cast<T*>(zc + V * KV);       // [V * KV + V]
     const int v = blockIdx.y;
     pdl_wait();
-    for (int c0 = threadIdx.x; c0 < Lo; c0 += 8 * 256) {   // all loads in flight, then the stores
-        double q[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) q[k] = c0 + 256 * k < Lo ? __ldg(z + (int64_t)v * ldz + c0 + 256 * k) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (c0 + 256 * k < Lo) zsm[c0 + 256 * k] = (T)q[k];
+    for (int i = threadIdx.x; i < V * KV + V; i += 256) {
+        const int zi = i - 4;
+        zpad[i] = (zi >= 0 && zi < Lo) ? (T)__ldg(z + (int64_t)v * ldz + zi) : T(0);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < V * KV; i += 256) {
+        const int s = i / KV, k = i - s * KV;
+        const T* src = zpad + V * k + s;
+        if constexpr (sizeof(T) == 4) zc[i] = make_float4(src[0], src[1], src[2], src[3]);
+        else zc[i] = make_double2(src[0], src[1]);
     }
     __syncthreads();
     const int64_t N = (int64_t)n * n;
@@ -690,17 +765,15 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
     int64_t e0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
     int a = (int)(e0 / n), b = (int)(e0 - (int64_t)a * n);
     for (; e0 < N; e0 += stride) {
-        T o[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {   // n % 4 == 0: the 4 cells share the row a
-            const int u = b + q - a + co;
-            o[q] = (u >= 0 && u < Lo) ? zsm[u] : T(0);
-        }
+        const int idx = b - a + co + 4;   // zpad index of the first of the 4 cells (n % 4 == 0: one row a)
+        const bool in = idx >= 1 && idx <= Lo + 3;
         if constexpr (sizeof(T) == 4) {
-            __stcs(reinterpret_cast<float4*>(y + e0), make_float4(o[0], o[1], o[2], o[3]));
+            const float4 o = in ? zc[(idx & 3) * KV + (idx >> 2)] : make_float4(0.f, 0.f, 0.f, 0.f);
+            __stcs(reinterpret_cast<float4*>(y + e0), o);
         } else {
-            __stcs(reinterpret_cast<double2*>(y + e0), make_double2(o[0], o[1]));
-            __stcs(reinterpret_cast<double2*>(y + e0 + 2), make_double2(o[2], o[3]));
+            const double2* cp = zc + (idx & 1) * KV + (idx >> 1);
+            __stcs(reinterpret_cast<double2*>(y + e0), in ? cp[0] : make_double2(0.0, 0.0));
+            __stcs(reinterpret_cast<double2*>(y + e0 + 2), in ? cp[1] : make_double2(0.0, 0.0));
         }
         a += da;
         b += db;
@@ -708,9 +781,9 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
     }
 }
 
-// Tensor map of X as [nv][n][n] fp32 (row stride n, vector stride ldx), box 128 x 32 x 1;
-// false when the driver entry point is unavailable (the per-thread-load kernel is used).
-static bool tma_map_f32(CUtensorMap* map, const void* X, int n, int nv, int64_t ldx) {
+// Tensor map of X as [nv][n][n] (row stride n, vector stride ldx), box 128 x 32 x 1;
+// false when the driver entry point is unavailable (the caller falls back to k_ra_block).
+static bool rat_tensor_map(CUtensorMap* map, const void* X, int n, int nv, int64_t ldx, bool f32) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     static bool tried = false;
     if (!tried) {
@@ -722,23 +795,24 @@ static bool tma_map_f32(CUtensorMap* map, const void* X, int n, int nv, int64_t 
             encode = nullptr;
         cudaGetLastError();
     }
-    // opt-in (KB_RAT_TMA=1): measured 38.8 us per 16-vector block against 35.4 us for the
-    // per-thread 16-byte loads of k_rat_diag (same run), so the loads stay the default
-    static const bool on = std::getenv("KB_RAT_TMA") != nullptr;
-    if (!encode || !on) return false;
+    if (!encode) return false;
+    const cuuint64_t es_b = f32 ? 4 : 8;
     const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)nv};
-    const cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)ldx * 4};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * es_b, (cuuint64_t)(nv > 1 ? ldx : (int64_t)n * n) * es_b};
     const cuuint32_t box[3] = {RT_COLS, RT_ROWS, 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(X), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    return encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                  const_cast<void*>(X), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+static int rat_ldw(int lmax) { return (lmax + 9) & ~1; }   // even: 16-byte aligned rows for the cp.async staging
 
 size_t ra_tiled_scratch_doubles(int n, int lmax, int nv) {
     if (n < RT_COLS || n % RT_COLS) return 0;
     const size_t tiles = (size_t)(n / RT_ROWS) * (n / RT_COLS);
-    return (size_t)nv * tiles * RT_DP + 2 * (size_t)nv * (lmax + 8) + 64;
+    return (size_t)nv * tiles * (RT_ROWS + RT_COLS) + (size_t)2 * nv * rat_ldw(lmax) + 64;
 }
 
 // false when outside the tiled path's envelope (the caller falls back)
@@ -747,44 +821,72 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     if (op->kind != KB_OP_RA_ZERO || nv < 1 || nv > 16) return false;
     const int n = op->side;
     if (n < RT_COLS || n % RT_COLS) return false;
-    const int vec = op->dtype == KB_F32 ? 4 : 2;
     if ((ldx % 4) || (ldy % 4) || ((uintptr_t)X % 16) || ((uintptr_t)Y % 16)) return false;
-    (void)vec;
+    const bool f32 = op->dtype == KB_F32;
     const int cu = op->kh / 2, cv = op->kw / 2;
     int ci, Li, co, Lo;
     const void* Mt;
     if (!transpose) { ci = cu; Li = op->kh; co = cv; Lo = op->kw; Mt = op->kt; }   // z = K^T w: rows of K^T
     else { ci = cv; Li = op->kw; co = cu; Lo = op->kh; Mt = op->k; }               // z = K w: rows of K
     const int lmax = std::max(op->kh, op->kw);
-    const int tiles = (n / RT_ROWS) * (n / RT_COLS);
+    CUtensorMap map;
+    if (!rat_tensor_map(&map, X, n, nv, ldx, f32)) return false;
+    // tiles per stack: 2 when that still gives ~2 CTAs per SM (measured best at n = 1024 and 2048 with
+    // 8-16 vectors: 37.2 us against 39.6 (1) and 39.4 (4) per 16-vector block), else 1
+    static const int ts_env = std::getenv("KB_RAT_TS") ? std::atoi(std::getenv("KB_RAT_TS")) : 0;
+    int ts = 1;
+    if (n % (RT_ROWS * 2) == 0 && (int64_t)(n / (RT_ROWS * 2)) * (n / RT_COLS) * nv >= 2 * kSMs) ts = 2;
+    if (ts_env > 0 && ts_env <= RT_MAXTS && n % (RT_ROWS * ts_env) == 0) ts = ts_env;
+    const int stacks = (n / (RT_ROWS * ts)) * (n / RT_COLS);
+    const int nst = std::min(ts, RT_STAGES);
+    const int ldw = rat_ldw(lmax);
     double* part = scratch;
-    double* w = part + (size_t)nv * tiles * RT_DP;
-    double* z = w + (size_t)nv * ((lmax + 9) & ~1);
-    const int ldw = (lmax + 9) & ~1;   // even: 16-byte aligned rows for the cp.async staging
+    double* w = part + (size_t)nv * (n / RT_ROWS) * (n / RT_COLS) * (RT_ROWS + RT_COLS);
+    double* z = w + (size_t)nv * ldw;
+    const int wgrid = (Li + 31) / 32;
+    constexpr int BV32 = 4, BV64 = 2;
+    const size_t bsm32 = (size_t)(BV32 * ((Lo + 8 + BV32 - 1) / BV32 + 1)) * (16 + 4) + 16;
+    const size_t bsm64 = (size_t)(BV64 * ((Lo + 8 + BV64 - 1) / BV64 + 1)) * (16 + 8) + 16;
+    if ((f32 ? bsm32 : bsm64) > 100 * 1024) return false;   // the broadcast stages z (shifted copies) in shared memory
+    static bool bcfg = false;
+    if (!bcfg) {
+        KB_CUDA(cudaFuncSetAttribute(k_rat_bcast<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_rat_bcast<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        bcfg = true;
+    }
     const int64_t N = (int64_t)n * n;
-    const double bytes = (double)(op->dtype == KB_F32 ? 4 : 8) * (2.0 * nv * N + (double)op->kh * op->kw);
+    const double bytes = (double)(f32 ? 4 : 8) * (2.0 * nv * N + (double)op->kh * op->kw);
     ProfScope ps(st, PROF_RA_DIAG, bytes);
-    // broadcast: ~4 CTAs per SM in total, so each CTA's staging of z (Lo doubles) is small
-    // next to the part of the output it writes
-    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256 * 4), (4 * kSMs + nv - 1) / nv));
-    if (Li > 32 * RZ_ML || (size_t)Li * 8 * 16 > 200 * 1024) return false;
     static const int pdl_env = std::getenv("KB_RAT_PDL") ? std::atoi(std::getenv("KB_RAT_PDL")) : -1;
-    g_rat_pdl = pdl_env >= 0 ? pdl_env != 0 : true;   // measured: nv=16 37.0 -> 35.3 us with PDL
-    if (op->dtype == KB_F32) {
-        CUtensorMap map;
-        if (tma_map_f32(&map, X, n, nv, ldx))
-            k_rat_diag_tma<<<std::min(tiles * nv, 6 * kSMs), 256, 0, st>>>(map, n, nv, part);
-        else
-            k_rat_diag<float><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const float*>(X), ldx, n, part);
-        pdl_launch(k_rat_w, dim3((Li + 7) / 8, nv), 0, st, (const double*)part, n, ci, Li, w, ldw);
-        rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
-        pdl_launch(k_rat_bcast<float>, dim3(bgrid, nv), sizeof(double) * Lo, st, (const double*)z, ldw, n, co, Lo,
+    g_rat_pdl = pdl_env >= 0 ? pdl_env != 0 : true;
+    // broadcast: ~KB_RAT_BCTAS CTAs per SM in total, so each CTA's staging of z (Lo doubles) is
+    // small next to the part of the output it writes
+    static const int bctas = std::getenv("KB_RAT_BCTAS") ? std::max(1, std::atoi(std::getenv("KB_RAT_BCTAS"))) : 8;
+    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256 * 4), (bctas * kSMs + nv - 1) / nv));
+    const size_t dsm = (size_t)nst * RT_ROWS * RT_COLS * (f32 ? 4 : 8) + sizeof(double) * (RT_ROWS * RT_MAXTS + RT_COLS) +
+                       sizeof(unsigned long long) * RT_STAGES;
+    static const int skip = std::getenv("KB_RAT_SKIP") ? std::atoi(std::getenv("KB_RAT_SKIP")) : 0;   // timing experiments only
+    if (f32) {
+        static bool cfg = false;
+        if (!cfg) {
+            KB_CUDA(cudaFuncSetAttribute(k_rat_diag<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+            cfg = true;
+        }
+        if (!(skip & 1)) k_rat_diag<float><<<dim3(stacks, nv), RT_DTHREADS, dsm, st>>>(map, n, ts, nst, ci, Li, part);
+        if (!(skip & 2)) pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
+        if (!(skip & 4)) rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
+        if (!(skip & 8)) pdl_launch(k_rat_bcast<float>, dim3(bgrid, nv), bsm32, st, 1, (const double*)z, ldw, n, co, Lo,
                    static_cast<float*>(Y), (int64_t)ldy);
     } else {
-        k_rat_diag<double><<<dim3(tiles, nv), 256, 0, st>>>(static_cast<const double*>(X), ldx, n, part);
-        pdl_launch(k_rat_w, dim3((Li + 7) / 8, nv), 0, st, (const double*)part, n, ci, Li, w, ldw);
+        static bool cfg = false;
+        if (!cfg) {
+            KB_CUDA(cudaFuncSetAttribute(k_rat_diag<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+            cfg = true;
+        }
+        k_rat_diag<double><<<dim3(stacks, nv), RT_DTHREADS, dsm, st>>>(map, n, ts, nst, ci, Li, part);
+        pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
         rat_z_launch<double>(static_cast<const double*>(Mt), Li, Lo, w, ldw, nv, z, st);
-        pdl_launch(k_rat_bcast<double>, dim3(bgrid, nv), sizeof(double) * Lo, st, (const double*)z, ldw, n, co, Lo,
+        pdl_launch(k_rat_bcast<double>, dim3(bgrid, nv), bsm64, st, 1, (const double*)z, ldw, n, co, Lo,
                    static_cast<double*>(Y), (int64_t)ldy);
     }
     KB_LAUNCH_CHECK();
