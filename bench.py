@@ -121,6 +121,45 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ra_block_time(kb, lib, D, n, nv, flush, hbm):
+    """One nv-vector R(A) block product at side n (configs[4]'s PSF family): 10 products per
+    CUDA-graph replay, 5 replays, CUDA events; algorithmic bytes 4 (2 nv N + (n+1)^2)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2410_00233_b200 import datagen
+
+    N = n * n
+    blur = kb.RearrangedBlur(datagen.mixture_psf(n, sig_hi=12.0 if n >= 2048 else 6.0), n)
+    ops = blur.op_struct()
+    nb = C.c_size_t()
+    lib.kb_op_workspace_bytes(C.byref(ops), C.byref(nb))
+    ws = torch.zeros(nb.value, dtype=torch.uint8, device=D.device())
+    X = torch.randn(nv, N, dtype=torch.float32, device=D.device())
+    Y = torch.empty_like(X)
+    lib.kb_op_apply_block(C.byref(ops), X.data_ptr(), N, Y.data_ptr(), N, nv, 0, ws.data_ptr(), nb.value,
+                          torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sp = torch.cuda.current_stream().cuda_stream
+        for i in range(10):
+            lib.kb_op_apply_block(C.byref(ops), X.data_ptr(), N, Y.data_ptr(), N, nv, i & 1, ws.data_ptr(), nb.value, sp)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / 50
+    by = 4.0 * (2 * nv * N + (n + 1) ** 2)
+    return {"us_per_launch": t * 1e6, "GBps": by / t / 1e9, "frac": by / t / 1e9 / hbm, "vectors": nv, "n": n}
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, prob):
     """The reference's algorithm on the host CPU (oracle port; the reference is
@@ -592,12 +631,14 @@ def run_ours(args, prob, rank, world, dist):
     ra = {"us_per_product": mv_t * 1e6, "GBps": mv_bytes_alg / mv_t / 1e9,
           "frac": mv_bytes_alg / mv_t / 1e9 / hbm, "bytes_per_product": mv_bytes_alg,
           "timing": f"{n_mv} products (alternating R x / R^T x) per CUDA-graph replay, 5 replays, CUDA events",
-          "kernel": "k_rat_diag | k_rat_w | k_rat_z | k_rat_bcast (tile diagonal sums, fixed-order diagonal "
-                    "reduction, row-dot z, streaming broadcast; stream-ordered, no grid barriers)",
+          "kernel": "k_rat_diag | k_rat_w | k_rat_z[_mma] | k_rat_bcast (TMA-streamed tile-stack diagonal sums, "
+                    "fixed-order diagonal reduction, clustered row-chunk z with a DSMEM reduction, streaming "
+                    "broadcast; chained by programmatic dependent launch, no grid barriers)",
           "block16": {"us_per_launch": blk_t * 1e6,
                       "GBps": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9,
                       "frac": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9 / hbm,
-                      "note": "16 vectors per launch (RSVD block product): K read once per block"}}
+                      "note": "16 vectors per launch (RSVD block product): K read once per block"},
+          "block16_n2048": ra_block_time(kb, lib, D, 2048, 16, flush, hbm) if not args.no_sweep else None}
     cg = int(sum(sb_res.cgls_iters))
     # the G stage (half the dense flops of a square apply) only runs the k tiles
     # inside G's zero band (kb_kron_band); count executed DMMA flops, not dense

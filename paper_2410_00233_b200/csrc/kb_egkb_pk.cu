@@ -736,6 +736,23 @@ __device__ __forceinline__ void pk_grid_sync(const PkParams& P, unsigned& gen) {
     __syncthreads();
 }
 
+// The same barrier in two halves, so that work which does not depend on the other CTAs can
+// run between the arrival and the wait (it hides behind the slowest CTA).
+__device__ __forceinline__ void pk_grid_arrive(const PkParams& P, unsigned& gen) {
+    gen += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+}
+__device__ __forceinline__ void pk_grid_wait(const PkParams& P, unsigned gen) {
+    if (threadIdx.x == 0) {
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.bar) : "memory");
+        } while ((int)(v - gen) < 0);
+    }
+    __syncthreads();
+}
+
 struct TileGeo {
     int TW, LR, RW, RB, T;   // tile width, lanes per row, rows per warp, row blocks, tiles
 };
@@ -869,7 +886,12 @@ __device__ __forceinline__ void pk_store_diag(const PkParams& P, const TileGeo& 
     pk_mark(P, 13);
 }
 
-template <int MAXG>
+// DEFER: the normalisation of a projected vector is deferred by one phase, so phases C and D
+// share one grid synchronisation (3 per half step instead of 4): the diagonal sums for the
+// next product are taken from the UNNORMALISED v1 (fixed point scaled by a power of two
+// >= 2 |v|) in the same phase that accumulates |v1|^2, the next phase A reads them as
+// w / t, and x = fl(v1 / t) is stored from registers at the start of that phase A.
+template <int MAXG, bool DEFER>
 __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGeo Gm) {
     cg::grid_group grid = cg::this_grid();
     unsigned gen = 0;
@@ -953,6 +975,29 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         err = 1;
         stop = 1;
     }
+    // DEFER: the vector held in v is still unnormalised (norm pend_t, destination pend_out);
+    // wscale turns the fixed-point diagonal sums of the current product's input into w
+    bool pend = false;
+    float pend_t = 1.f;
+    float* pend_out = nullptr;
+    double wscale = fxs_inv;
+    auto store_pending = [&]() {
+        const double rtd = 1.0 / (double)pend_t;
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g)
+            if (g < ng) {
+                // v1 is read back from the tile buffer (staged there for the diagonal sums), so
+                // no register holds it across phase A
+                const float4 u = *reinterpret_cast<const float4*>(tb + g * 1024 + tbo);
+                float o[4];
+                o[0] = pk_fdiv_exact(u.x, pend_t, rtd);
+                o[1] = pk_fdiv_exact(u.y, pend_t, rtd);
+                o[2] = pk_fdiv_exact(u.z, pend_t, rtd);
+                o[3] = pk_fdiv_exact(u.w, pend_t, rtd);
+                PkIO<float, 4>::store(pend_out + eo[g], o);
+            }
+        pend = false;
+    };
     for (int step = 0; !stop; ++step) {
         const int tr = (step & 1) ? 0 : 1;           // step 0 and even steps: q side (R^T)
         const float* prev;
@@ -976,17 +1021,21 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         unsigned long long* wcur = P.wfix + (int64_t)(step & 1) * P.lmax;
 
         // the accumulators were last read before the previous phase's sync: reset them
+        // (DEFER: |v1|^2 alternates between two accumulators, each reset two phases after its read)
         if (blockIdx.x == 0)
-            for (int j = tid; j < 3 * (P.cap + 5); j += PK_THREADS) P.xacc[j] = 0;
+            for (int j = tid; j < 3 * (P.cap + (DEFER ? 4 : 5)); j += PK_THREADS) P.xacc[j] = 0;
+
         // ---- A: z rows from the diagonal sums of the input vector.  The ring
         // starts fetching the first basis vectors of the dots (phase B) now.
-        if constexpr (MAXG > 4) {   // (MAXG <= 4: issued during the previous step's phase D)
+        if constexpr (MAXG > 4 && !DEFER) {   // (MAXG <= 4: issued during the previous step's phase D)
             if (m > 0)
 #pragma unroll
                 for (int k = 0; k < PK_NS; ++k)
                     ring_fill<MAXG, PK_NS>(ringb, SF, tbo, rbase + k, k < 2 * m ? B + (int64_t)(k % m) * ldb : nullptr, eo, ng);
         }
-        pk_zrows(P, Mt, Li, Lo, zs, wcur, fxs_inv);
+        pk_mark(P, 7);
+        pk_zrows(P, Mt, Li, Lo, zs, wcur, wscale);
+        pk_mark(P, 8);
         // prefetch prev (used right after the barrier) while the grid synchronises
         float pv[MAXG][4];
 #pragma unroll
@@ -995,11 +1044,27 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int q = 0; q < 4; ++q) pv[g][q] = 0.f;
             if (g < ng && prev) PkIO<float, 4>::load(prev + eo[g], pv[g]);
         }
+        auto prefill = [&]() {   // the first basis vectors of the dots (phase B)
+            if (m > 0)
+#pragma unroll
+                for (int k = 0; k < PK_NS; ++k)
+                    ring_fill<MAXG, PK_NS>(ringb, SF, tbo, rbase + k, k < 2 * m ? B + (int64_t)(k % m) * ldb : nullptr, eo, ng);
+        };
+        if constexpr (DEFER) {
+            if constexpr (MAXG <= 4) prefill();   // (the ring does not share the tile buffer)
+            if constexpr (MAXG > 4) {
+                if (pend) store_pending();
+                prefill();
+            }
+        }
         gsync();
         pk_mark(P, 3);
 
         // ---- B: zero the consumed w; z; y; v = y - beta*prev; dots
         for (int i = blockIdx.x * PK_THREADS + tid; i < P.lmax; i += nblk * PK_THREADS) wcur[i] = 0ull;
+        if constexpr (DEFER) {
+            if (blockIdx.x == 0 && tid < 3) xnrm[3 * ((step + 1) & 1) + tid] = 0;
+        }
         // z staged already rounded to fp32: y = fl32(z[u]) for every cell of a diagonal,
         // so one conversion per diagonal instead of one per cell
         float* zsf = reinterpret_cast<float*>(zs);
@@ -1014,6 +1079,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         const int W = m + 2;
         for (int i = tid; i < 8 * W; i += PK_THREADS) acc[i] = 0.0;
         __syncthreads();
+        pk_mark(P, 11);
         float ysqf = 0.f;   // |y|^2 only feeds the breakdown threshold: fp32 per thread
         vsq = 0.0;
 #pragma unroll
@@ -1065,13 +1131,23 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             acc[warp * W + m + 1] += ysq;
         }
         __syncthreads();
+        pk_mark(P, 15);
         for (int j = tid; j < W; j += PK_THREADS) {
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < 8; ++w) t += acc[w * W + j];
             xacc_add(xdot + 3 * j, t);
         }
-        gsync();
+        if (DEFER && MAXG <= 4 && pend && !P.cg_sync) {
+            // x = fl(v1 / t) of the previous half step, stored between the arrival and the
+            // wait (nothing reads it before the next half step's barriers)
+            pk_grid_arrive(P, gen);
+            store_pending();
+            pk_grid_wait(P, gen);
+        } else {
+            if (DEFER && pend) store_pending();
+            gsync();
+        }
         for (int j = tid; j < W; j += PK_THREADS) red[j] = xacc_get(xdot + 3 * j);
         __syncthreads();
         pk_mark(P, 4);
@@ -1115,20 +1191,48 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             }
             rbase += 2 * m;
             v1sq = warp_sum(v1sq);
-            __syncthreads();   // cf (in acc) is read until every warp has finished the projection
-            if (lane == 0) acc[warp] = v1sq;
-            __syncthreads();
-            if (tid == 0) {
-                double s = 0.0;
+            long long* xn = DEFER ? xnrm + 3 * (step & 1) : xnrm;
+            if constexpr (DEFER) {
+                // the diagonal sums of the unnormalised v1 for the next product, in fixed point
+                // scaled for entries below 2 |v| (|v1| <= |v| up to rounding)
+                const int Fp = max(-100, min(100, pk_fix_exp(vnorm, n)));
 #pragma unroll
-                for (int w = 0; w < 8; ++w) s += acc[w];
-                xacc_add(xnrm, s);
+                for (int g = 0; g < MAXG; ++g)
+                    if (g < ng)
+                        *reinterpret_cast<float4*>(tb + g * 1024 + tbo) = make_float4(v[g][0], v[g][1], v[g][2], v[g][3]);
+                wscale = ldexp(1.0, -Fp);
+                __syncthreads();   // cf (in acc) is read until every warp has finished the projection
+                if (lane == 0) acc[warp] = v1sq;
+                __syncthreads();
+                if (tid == 0) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) s += acc[w];
+                    xacc_add(xn, s);
+                }
+                tile_diag_atomics<MAXG>(P, Gm, tb, t0, ng, ci_n, Li_n, ldexp(1.0, Fp), wnext);
+            } else {
+                __syncthreads();   // cf (in acc) is read until every warp has finished the projection
+                if (lane == 0) acc[warp] = v1sq;
+                __syncthreads();
+                if (tid == 0) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) s += acc[w];
+                    xacc_add(xn, s);
+                }
             }
             gsync();
-            if (tid == 0) red[P.cap + 2] = xacc_get(xnrm);
+            if (tid == 0) red[P.cap + 2] = xacc_get(xn);
             __syncthreads();
             pk_mark(P, 5);
             val = sqrt(red[P.cap + 2]);
+            if constexpr (DEFER) {
+                pend = true;
+                pend_t = (float)val;
+                pend_out = out;
+                wscale /= (double)pend_t;
+            }
         }
         // ---- control (identical in every CTA; CTA 0 records the trace), before D so
         // the next step's basis vectors stream in while D runs
@@ -1195,7 +1299,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             }
         }
         }
-        if constexpr (MAXG <= 4) {   // the ring does not share the tile buffer used by D
+        if constexpr (MAXG <= 4 && !DEFER) {   // the ring does not share the tile buffer used by D
             if (!stop) {
                 const int trn = ((step + 1) & 1) ? 0 : 1;
                 const float* Bn = trn ? Q : S;
@@ -1211,8 +1315,13 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
         // ---- D: out = fl(v1 / t) (lowrank.py:247, 260), stored, and its diagonal
         // sums for the next product
         pk_mark(P, 14);
-        pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
-        gsync();
+        if (!pend) {
+            pk_store_diag<MAXG>(P, Gm, v, (float)val, out, eo, ng, tb, tbo, t0, ci_n, Li_n, fxs, wnext);
+            wscale = fxs_inv;
+            gsync();
+        } else if (stop) {
+            store_pending();
+        }
         pk_mark(P, 6);
 
         if (stop) break;
@@ -1284,9 +1393,9 @@ static bool pk_launch(PkParams& P, cudaStream_t st, int& grid_out) {
     return true;
 }
 
-template <int MAXG>
+template <int MAXG, bool DEFER>
 static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaStream_t st) {
-    auto kern = k_egkb_tiled<MAXG>;
+    auto kern = k_egkb_tiled<MAXG, DEFER>;
     const size_t smem = sizeof(double) * ((size_t)P.lmax + (P.cap + 4) + 8 * (size_t)std::max(P.cap + 2, 33)) +
                         sizeof(float) * 1024 * MAXG * (MAXG <= 4 ? 1 + pk_ns<MAXG>() : pk_ns<MAXG>());
     static bool configured = false;
@@ -1345,9 +1454,19 @@ static bool tiled_launch(PkParams& P, cudaStream_t st) {
     static const int cps = std::getenv("KB_PK_CTAS_PER_SM") ? std::atoi(std::getenv("KB_PK_CTAS_PER_SM")) : 2;
     const int per = cps * kSMs;
     const int need = (Gm.T + std::min(per, Gm.T) - 1) / std::min(per, Gm.T);
-    if (need <= 4) return tiled_launch_g<4>(P, Gm, cps, st);
-    if (need <= 8) return tiled_launch_g<8>(P, Gm, cps, st);
-    if (need <= 16) return tiled_launch_g<16>(P, Gm, cps, st);
+    // deferred normalisation (3 grid syncs per half step) is opt-in: measured slower on B200
+    // (n=1024 0.90 vs 0.84 ms, n=2048 2.56 vs 2.34 ms: the saved barrier is outweighed by
+    // slower z rows and basis streams right after the merged phase)
+    static const int defer = std::getenv("KB_PK_DEFER") ? std::atoi(std::getenv("KB_PK_DEFER")) : 0;
+    if (defer) {
+        if (need <= 4) return tiled_launch_g<4, true>(P, Gm, cps, st);
+        if (need <= 8) return tiled_launch_g<8, true>(P, Gm, cps, st);
+        if (need <= 16) return tiled_launch_g<16, true>(P, Gm, cps, st);
+        return false;
+    }
+    if (need <= 4) return tiled_launch_g<4, false>(P, Gm, cps, st);
+    if (need <= 8) return tiled_launch_g<8, false>(P, Gm, cps, st);
+    if (need <= 16) return tiled_launch_g<16, false>(P, Gm, cps, st);
     return false;
 }
 
