@@ -417,8 +417,13 @@ __global__ void __launch_bounds__(RT_DTHREADS) k_rat_diag(const __grid_constant_
         for (int st = 0; st < nst; ++st)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&mbar[st])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < nst && k < nt; ++k) issue(k);
     }
+    // launched with programmatic dependent launch too: X may be the output of the kernel before
+    // (the previous product's broadcast in a chain of products), so wait for it here -- the
+    // launch latency and the prologue above are already behind us
+    pdl_wait();
+    if (tid == 0)
+        for (int k = 0; k < nst && k < nt; ++k) issue(k);
     __syncthreads();
     pdl_trigger();
     const int off = tid - (RT_ROWS - 1);   // column - row inside a tile
@@ -677,10 +682,18 @@ __global__ void __launch_bounds__(256) k_rat_z_mma(const T* __restrict__ Mt, int
 
 // Launch with programmatic dependent launch and (cy > 1) a (1, cy, 1) thread-block cluster.
 template <typename K, typename... A>
+static void pdl_launch_b(K kern, dim3 grid, int threads, size_t smem, cudaStream_t st, int cy, A... args);
+
+template <typename K, typename... A>
 static void pdl_launch(K kern, dim3 grid, size_t smem, cudaStream_t st, int cy, A... args) {
+    pdl_launch_b(kern, grid, 256, smem, st, cy, args...);
+}
+
+template <typename K, typename... A>
+static void pdl_launch_b(K kern, dim3 grid, int threads, size_t smem, cudaStream_t st, int cy, A... args) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;
-    lc.blockDim = dim3(256);
+    lc.blockDim = dim3(threads);
     lc.dynamicSmemBytes = smem;
     lc.stream = st;
     cudaLaunchAttribute attr[2];
@@ -745,6 +758,7 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
     T* zpad = reinterpret_cast<T*>(zc + V * KV);       // [V * KV + V]
     const int v = blockIdx.y;
     pdl_wait();
+    pdl_trigger();   // a following product's first kernel may launch; it waits for this grid's writes
     for (int i = threadIdx.x; i < V * KV + V; i += 256) {
         const int zi = i - 4;
         zpad[i] = (zi >= 0 && zi < Lo) ? (T)__ldg(z + (int64_t)v * ldz + zi) : T(0);
@@ -872,7 +886,7 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_rat_diag<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
             cfg = true;
         }
-        if (!(skip & 1)) k_rat_diag<float><<<dim3(stacks, nv), RT_DTHREADS, dsm, st>>>(map, n, ts, nst, ci, Li, part);
+        if (!(skip & 1)) pdl_launch_b(k_rat_diag<float>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
         if (!(skip & 2)) pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
         if (!(skip & 4)) rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
         if (!(skip & 8)) pdl_launch(k_rat_bcast<float>, dim3(bgrid, nv), bsm32, st, 1, (const double*)z, ldw, n, co, Lo,
@@ -883,7 +897,7 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_rat_diag<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
             cfg = true;
         }
-        k_rat_diag<double><<<dim3(stacks, nv), RT_DTHREADS, dsm, st>>>(map, n, ts, nst, ci, Li, part);
+        pdl_launch_b(k_rat_diag<double>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
         pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
         rat_z_launch<double>(static_cast<const double*>(Mt), Li, Lo, w, ldw, nv, z, st);
         pdl_launch(k_rat_bcast<double>, dim3(bgrid, nv), bsm64, st, 1, (const double*)z, ldw, n, co, Lo,

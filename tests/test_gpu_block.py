@@ -60,3 +60,49 @@ def test_rsvd_repeatable(kb):
         except kb.RankDeficiencyError as e:
             seen.add(("rank", e.column))
     assert len(seen) == 1, seen
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 3e-7), (np.float64, 1e-13)])
+@pytest.mark.parametrize("n,shape", [(128, (129, 129)), (128, (255, 255)), (256, (511, 511)), (256, (33, 129)),
+                                     (256, (1, 7)), (256, (257, 31)), (384, (385, 385)), (384, (767, 5))])
+def test_dense_random_psf_shapes(kb, n, shape, dtype, tol):
+    """Dense random PSFs (every entry significant, unlike the Gaussians): the tile skipping
+    outside the support, the band edges, the partial last r chunk of the z kernels, the
+    cluster sizes 1..8 and non-square supports, for every z kernel (1, 3, 6, 16 vectors)."""
+    from oracle import structured as ost
+    from paper_2410_00233_b200 import device as D
+    from paper_2410_00233_b200.lowrank import _EngineOp
+
+    rng = np.random.default_rng(n + shape[0] + 7 * shape[1])
+    psf = rng.random(shape) + 0.1
+    blur = kb.RearrangedBlur(psf, n, dtype=dtype)
+    kern = blur.psf.kernel.astype(dtype)
+    op = _EngineOp(blur)
+    for nv in (1, 3, 6, 16):
+        x = rng.standard_normal((nv, n * n)).astype(dtype)
+        xd = D.to_device(x)
+        y, z = D.to_host(op.apply_block(xd, 0)), D.to_host(op.apply_block(xd, 1))
+        for j in sorted({0, nv - 1}):
+            assert _rel(y[j], ost.ra_matvec(kern, n, x[j]).astype(np.float64)) < tol, (nv, j)
+            assert _rel(z[j], ost.ra_rmatvec(kern, n, x[j]).astype(np.float64)) < tol, (nv, j)
+
+
+def test_block_product_n2048(kb):
+    """configs[4]'s side: the tiled chain (row chunks over a full cluster, 2049 diagonals)."""
+    from oracle import structured as ost
+    from paper_2410_00233_b200 import device as D
+    from paper_2410_00233_b200.lowrank import _EngineOp
+
+    n = 2048
+    rng = np.random.default_rng(5)
+    psf = rng.random((n + 1, n + 1)) + 0.1
+    blur = kb.RearrangedBlur(psf, n)
+    kern = blur.psf.kernel.astype(np.float32)
+    op = _EngineOp(blur)
+    for nv in (1, 16):
+        x = rng.standard_normal((nv, n * n)).astype(np.float32)
+        xd = D.to_device(x)
+        y, z = D.to_host(op.apply_block(xd, 0)), D.to_host(op.apply_block(xd, 1))
+        j = nv - 1
+        assert _rel(y[j], ost.ra_matvec(kern, n, x[j]).astype(np.float64)) < 3e-7, nv
+        assert _rel(z[j], ost.ra_rmatvec(kern, n, x[j]).astype(np.float64)) < 3e-7, nv
