@@ -841,7 +841,9 @@ __device__ __forceinline__ void pk_zrows(const PkParams& P, const float* Mt, int
         for (int k = 0; k < 8; ++k)
             if (r0 + k * PK_THREADS < Li) ws[r0 + k * PK_THREADS] = (double)q[k] * s2;
     }
+    pk_mark(P, 9);
     __syncthreads();
+    pk_mark(P, 10);
     for (int c = c_first; c < c1; c += PK_THREADS / 32) {
         const float* row = Mt + (int64_t)c * Li;
         if (c != c_first) {
@@ -896,7 +898,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
     cg::grid_group grid = cg::this_grid();
     unsigned gen = 0;
     auto gsync = [&]() {
-        if (P.cg_sync) grid.sync();
+        if (P.cg_sync & 1) grid.sync();
         else pk_grid_sync(P, gen);
     };
     extern __shared__ double sm[];
@@ -1138,7 +1140,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             for (int w = 0; w < 8; ++w) t += acc[w * W + j];
             xacc_add(xdot + 3 * j, t);
         }
-        if (DEFER && MAXG <= 4 && pend && !P.cg_sync) {
+        if (DEFER && MAXG <= 4 && pend && !(P.cg_sync & 1)) {
             // x = fl(v1 / t) of the previous half step, stored between the arrival and the
             // wait (nothing reads it before the next half step's barriers)
             pk_grid_arrive(P, gen);
@@ -1210,7 +1212,7 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
                     for (int w = 0; w < 8; ++w) s += acc[w];
                     xacc_add(xn, s);
                 }
-                tile_diag_atomics<MAXG>(P, Gm, tb, t0, ng, ci_n, Li_n, ldexp(1.0, Fp), wnext);
+                if (!(P.cg_sync & 2)) tile_diag_atomics<MAXG>(P, Gm, tb, t0, ng, ci_n, Li_n, ldexp(1.0, Fp), wnext);
             } else {
                 __syncthreads();   // cf (in acc) is read until every warp has finished the projection
                 if (lane == 0) acc[warp] = v1sq;
@@ -1419,7 +1421,7 @@ static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaS
     if (per_sm < 1) return false;
     static const int grid_env = std::getenv("KB_PK_GRID") ? std::atoi(std::getenv("KB_PK_GRID")) : 0;
     static const int cg_env = std::getenv("KB_PK_CGSYNC") ? std::atoi(std::getenv("KB_PK_CGSYNC")) : 0;
-    P.cg_sync = cg_env;
+    P.cg_sync = cg_env;   // bit 0: cooperative-groups grid.sync; bit 1 (timing experiment): DEFER without its atomics
     int grid = std::min(sms * std::min(per_sm, per_sm_cap), Gm.T);
     if (grid_env > 0) grid = std::min(grid, grid_env);
     if ((Gm.T + grid - 1) / grid > MAXG) return false;
