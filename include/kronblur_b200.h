@@ -311,6 +311,12 @@ typedef struct {
                        * stage of the transposed apply is one dense GEMM, like the
                        * forward one's (both then run on cuBLAS DGEMM, the faster
                        * library kernel for these dense shapes; NULL: DMMA k_dgemm). */
+    /* optional structure of the F side (KroneckerSum.toeplitz_split): with fband set, only
+     * the first ndense terms have dense F_i (ft then holds those ndense blocks); the others
+     * share the zero band fband (device int[2], min/max of c - r over their nonzeros) and
+     * the reduced stage skips the k tiles that only meet zeros.  NULL: every F_i dense. */
+    int ndense;
+    const int* fband;
 } kb_kron;
 
 /* band[0..1] = min/max of (c - r) over the nonzero entries G_i[r][c] of all

@@ -58,7 +58,7 @@ class KbEgkbState(C.Structure):
 
 class KbKron(C.Structure):
     _fields_ = [("m1", C.c_int), ("m2", C.c_int), ("n1", C.c_int), ("n2", C.c_int), ("k", C.c_int),
-                ("f", vp), ("g", vp), ("band", vp), ("ft", vp)]
+                ("f", vp), ("g", vp), ("band", vp), ("ft", vp), ("ndense", C.c_int), ("fband", vp)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(None, vp, dp, i64, vp)

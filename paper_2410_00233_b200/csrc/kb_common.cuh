@@ -98,7 +98,8 @@ struct GemmSkip {
     const int* flags = nullptr;
     int stride = 0;
     int rows = 0;
-    const int* band = nullptr;
+    const int* band = nullptr;     // zero band (col - row) of the stored B blocks: k-tile window from the column tile
+    const int* band_a = nullptr;   // zero band (col - row) of the stored A blocks: k-tile window from the row tile
 };
 
 // ---------------------------------------------------------------- profiling

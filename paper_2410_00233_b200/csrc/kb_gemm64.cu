@@ -102,16 +102,24 @@ k_dgemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t 
     double* Cb = C + (int64_t)z * sc_batch + (int64_t)split * split_stride;
 
     int kt_first = 0, ktiles = (K + BK - 1) / BK;
-    if (skip.band) {   // banded B: only the k tiles that meet this CTA's columns
-        const int lo0 = __ldg(skip.band), hi0 = __ldg(skip.band + 1);
-        if (lo0 > hi0) {   // all-zero G (band left at {INT_MAX, INT_MIN}): nothing to multiply
+    if (skip.band || skip.band_a) {   // banded operand: only the k tiles that meet this CTA's columns (B) / rows (A)
+        const int* bp = skip.band ? skip.band : skip.band_a;
+        const int lo0 = __ldg(bp), hi0 = __ldg(bp + 1);
+        if (lo0 > hi0) {   // all-zero blocks (band left at {INT_MAX, INT_MIN}): nothing to multiply
             kt_first = 0;
             ktiles = 0;
         } else {
             // offsets are within (-K, K): 64-bit bounds keep the arithmetic defined anyway
-            int64_t lo = lo0, hi = hi0;
-            if (TB) { const int64_t t = lo; lo = -hi; hi = -t; }   // logical B[k][c] = G[c][k]
-            const int64_t klo = max((int64_t)0, (int64_t)n0 - hi), khi = min((int64_t)K - 1, (int64_t)n0 + BN - 1 - lo);
+            int64_t lo = lo0, hi = hi0, klo, khi;
+            if (skip.band) {
+                if (TB) { const int64_t t = lo; lo = -hi; hi = -t; }   // logical B[k][c] = G[c][k]
+                klo = max((int64_t)0, (int64_t)n0 - hi);
+                khi = min((int64_t)K - 1, (int64_t)n0 + BN - 1 - lo);
+            } else {
+                if (TA) { const int64_t t = lo; lo = -hi; hi = -t; }   // stored A[k][m]: k - m in [-hi, -lo]
+                klo = max((int64_t)0, (int64_t)m0 + lo);               // logical A[m][k]: k - m in [lo, hi]
+                khi = min((int64_t)K - 1, (int64_t)m0 + BM - 1 + hi);
+            }
             kt_first = khi >= klo ? (int)(klo / BK) : 0;
             ktiles = khi >= klo ? (int)(khi / BK) + 1 - kt_first : 0;
         }

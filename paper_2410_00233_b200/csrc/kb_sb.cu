@@ -345,28 +345,47 @@ void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, do
         ~Reset() { g_dgemm_skip = GemmSkip{}; }
     } reset;
     g_dgemm_skip.band = kr->band;   // stage 1 only: G's zero band (kb_kron_band)
+    // F side: the first nd terms dense, the other kb terms banded (kb_kron.fband); without
+    // the structure every term is dense
+    const int nd = kr->fband ? std::max(0, std::min(kr->ndense, k)) : k, kb = k - nd;
     if (!transpose) {
         // P_i = Xr G_i            (n1 x m2), Xr = x as n1 x n2, G_i n2 x m2
         dgemm(0, 0, n1, m2, n2, x, n2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, m2,
               (int64_t)n1 * m2, k, 1, 0.0, st);
         g_dgemm_skip = GemmSkip{};
-        // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1: one dense GEMM, inner dim k n1
-        if (kron_uses_cublas(kr))
-            dgemm_sum_blocks(m1, m2, n1, k, kr->f, tmp, y, st);
-        else
-            dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
-                  0, 1, k, 0.0, st, part, part_n);
+        // Yr = sum_i F_i^T P_i    (m1 x m2), F_i n1 x m1: one dense GEMM, inner dim nd n1 ...
+        if (nd > 0) {
+            if (kron_uses_cublas(kr))
+                dgemm_sum_blocks(m1, m2, n1, nd, kr->f, tmp, y, st);
+            else
+                dgemm(1, 0, m1, m2, n1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, m2, 0, (int64_t)n1 * m2, y, m2,
+                      0, 1, nd, 0.0, st, part, part_n);
+        }
+        if (kb > 0) {   // ... plus the banded terms: the k tiles inside F's zero band only
+            g_dgemm_skip.band_a = kr->fband;
+            dgemm(1, 0, m1, m2, n1, kr->f + (int64_t)nd * n1 * m1, m1, 0, (int64_t)n1 * m1,
+                  tmp + (int64_t)nd * n1 * m2, m2, 0, (int64_t)n1 * m2, y, m2, 0, 1, kb, nd > 0 ? 1.0 : 0.0, st,
+                  part, part_n);
+        }
     } else {
         // Q_i = Yr G_i^T          (m1 x n2), Yr = y as m1 x m2
         dgemm(0, 1, m1, n2, m2, x, m2, 0, 0, kr->g, m2, (int64_t)n2 * m2, 0, tmp, n2,
               (int64_t)m1 * n2, k, 1, 0.0, st);
         g_dgemm_skip = GemmSkip{};
         // Xr = sum_i F_i Q_i      (n1 x n2) = sum_i Ft_i^T Q_i with Ft_i = F_i^T (m1 x n1)
-        if (kron_uses_cublas(kr))
-            dgemm_sum_blocks(n1, n2, m1, k, kr->ft, tmp, y, st);
-        else
-            dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
-                  0, 1, k, 0.0, st, part, part_n);
+        if (nd > 0) {
+            if (kron_uses_cublas(kr))
+                dgemm_sum_blocks(n1, n2, m1, nd, kr->ft, tmp, y, st);
+            else
+                dgemm(0, 0, n1, n2, m1, kr->f, m1, 0, (int64_t)n1 * m1, tmp, n2, 0, (int64_t)m1 * n2, y, n2,
+                      0, 1, nd, 0.0, st, part, part_n);
+        }
+        if (kb > 0) {
+            g_dgemm_skip.band_a = kr->fband;
+            dgemm(0, 0, n1, n2, m1, kr->f + (int64_t)nd * n1 * m1, m1, 0, (int64_t)n1 * m1,
+                  tmp + (int64_t)nd * m1 * n2, n2, 0, (int64_t)m1 * n2, y, n2, 0, 1, kb, nd > 0 ? 1.0 : 0.0, st,
+                  part, part_n);
+        }
     }
 }
 

@@ -84,6 +84,7 @@ class KroneckerSum:
         self.g_dev = D.to_device(g)
         self._band = None
         self._ft = None
+        self._ndense, self._fband = None, None
 
     @classmethod
     def from_device(cls, f_dev, g_dev, scheme: BlockScheme) -> "KroneckerSum":
@@ -93,6 +94,7 @@ class KroneckerSum:
         obj.f_dev, obj.g_dev = f_dev, g_dev
         obj._band = None
         obj._ft = None
+        obj._ndense, obj._fband = None, None
         return obj
 
     @property
@@ -137,11 +139,78 @@ class KroneckerSum:
         kr.band = self._band.data_ptr()
         if self._ft is None:
             # F_i^T blocks (device transpose, once per operator): the reduced stage of the
-            # transposed apply becomes one dense GEMM as well
+            # transposed apply becomes one dense GEMM as well (structured: the dense terms only)
             s = self.scheme
-            self._ft = self.f_dev.view(-1, s.n1, s.m1).transpose(1, 2).contiguous()
-        kr.ft = self._ft.data_ptr()
+            nd = self.k if self._ndense is None else self._ndense
+            self._ft = self.f_dev[:max(nd, 1)].view(-1, s.n1, s.m1).transpose(1, 2).contiguous()
+        import os
+
+        if self._ndense is None or os.environ.get("KB_SPLIT_CUBLAS", "1") != "0":
+            kr.ft = self._ft.data_ptr()
+        if self._ndense is not None:
+            if self._fband is None:   # zero band of the banded F blocks (same kernel as G's)
+                import torch
+
+                from . import device as D
+
+                nd = self._ndense
+                # kb_kron_band scans the "g" blocks (n2 x m2): here the stored n1 x m1 F blocks
+                tmp = _lib.KbKron(s.m1, s.m1, s.n1, s.n1, self.k - nd, None, self.f_dev[nd:].data_ptr())
+                fband = torch.empty(2, dtype=torch.int32, device=self.f_dev.device)
+                _lib.check(_lib.load().kb_kron_band(C.byref(tmp), fband.data_ptr(), D.stream_ptr()), "kron band")
+                self._fband = fband
+            kr.ndense = self._ndense
+            kr.fband = self._fband.data_ptr()
         return kr
+
+    def toeplitz_split(self, drop: float = 3e-8):
+        """The same operator with the structure of a zero-BC eGKB approximation made explicit.
+
+        Every s-basis vector of the eGKB on R(A) is a combination of R(A) q products
+        (constant along the diagonals of the n x n image: Toeplitz) and of the dense start
+        vector, so F_i = T_i + a_i D + E_i with T_i Toeplitz (the diagonal means of F_i), D
+        one dense matrix (the dominant direction of the non-Toeplitz parts) and E_i at the
+        fp32 rounding level.  Returns the (k + 1)-term KroneckerSum
+            D (x) (sum_i a_i G_i)  +  sum_i T_i (x) G_i
+        whose k banded x banded terms run through the band-skipping GEMM in both stages
+        (T_i diagonals below ``drop`` x max |T| and G entries below ``drop`` x max |G| are
+        set to zero), and the relative Frobenius size of what was dropped on the F side,
+        max_i |F_i - T_i - a_i D| / |F_1|.  The split is
+        an approximation of this operator (not of the reference's arithmetic): callers opt in.
+        """
+        import torch
+
+        s = self.scheme
+        if not (s.m1 == s.n1 == s.m2 == s.n2):
+            raise ValidationError("toeplitz_split needs square factors of one size")
+        n, k = s.n1, self.k
+        f = self.f_dev.view(k, n, n)
+        g = self.g_dev.view(k, n * n)
+        # diagonal means: index d = col - row + n - 1 of the stored n1 x m1 blocks
+        r = torch.arange(n, device=f.device)
+        didx = (r[None, :] - r[:, None] + (n - 1)).reshape(-1)
+        cnt = torch.zeros(2 * n - 1, dtype=torch.float64, device=f.device).index_add_(
+            0, didx, torch.ones(n * n, dtype=torch.float64, device=f.device))
+        fm = f.reshape(k, n * n)
+        means = torch.zeros(k, 2 * n - 1, dtype=torch.float64, device=f.device).index_add_(1, didx, fm) / cnt
+        non = fm - means[:, didx]                       # non-Toeplitz parts, rank one up to rounding
+        gram = (non @ non.T).cpu().numpy()              # k x k: host eigh, no cuSOLVER start-up
+        _, vecs = np.linalg.eigh(gram)
+        d = torch.as_tensor(vecs[:, -1].copy(), device=f.device) @ non
+        d = d / torch.linalg.norm(d)
+        a = non @ d                                     # F_i ~ T_i + a_i D
+        scale = means.abs().max()
+        means = torch.where(means.abs() >= drop * scale, means, torch.zeros_like(means))
+        t = means[:, didx]
+        resid = torch.linalg.norm(fm - t - a[:, None] * d[None, :], dim=1).max() / torch.linalg.norm(fm[0])
+        f2 = torch.cat([d[None, :], t], dim=0).contiguous()
+        # the G side keeps its exact zeros; entries below drop x max |G| (the Gaussian tails
+        # between the fp32 underflow and the rounding level) are dropped as well
+        gt = torch.where(g.abs() >= drop * g.abs().max(), g, torch.zeros_like(g))
+        g2 = torch.cat([(a[:, None] * gt).sum(dim=0, keepdim=True), gt], dim=0).contiguous()
+        out = KroneckerSum.from_device(f2, g2, s)
+        out._ndense = 1
+        return out, float(resid)
 
     def forward_struct(self) -> _lib.KbForward:
         fw = _lib.KbForward()
@@ -178,13 +247,19 @@ class KroneckerSum:
         return out
 
 
-def assemble(svd, scheme: BlockScheme) -> KroneckerSum:
+def assemble(svd, scheme: BlockScheme, toeplitz_split: bool = False) -> KroneckerSum:
     """Truncated SVD of R(A) -> KroneckerSum (kronop.py:103-123).
 
     ax_i = sigma_i unvec(u_i, m1, n1), ay_i = unvec(v_i, m2, n2), promoted to
     fp64.  On the device this is one cast/scale kernel (kb_kron_assemble):
-    F_i = ax_i^T is exactly sigma_i * u_i as stored.
+    F_i = ax_i^T is exactly sigma_i * u_i as stored.  ``toeplitz_split=True`` (an
+    extension; zero-BC eGKB results) returns ``KroneckerSum.toeplitz_split()`` of that
+    operator instead, with the dropped share in ``.split_residual``.
     """
+    if toeplitz_split:
+        op, resid = assemble(svd, scheme).toeplitz_split()
+        op.split_residual = resid
+        return op
     from . import device as D
 
     m_u, m_v = svd.shape
