@@ -273,6 +273,12 @@ using Cfg0 = GCfg<128, 64, 16, 3, 4, 2, 2>;    // 8 warps of 32x32, 2 CTAs/SM
 using Cfg1 = GCfg<128, 64, 32, 2, 4, 2, 2>;    // BK 32: half the barriers per flop
 using Cfg2 = GCfg<128, 128, 16, 3, 2, 4, 1>;   // 8 warps of 64x32, 1 CTA/SM
 using Cfg3 = GCfg<128, 128, 32, 2, 2, 4, 1>;
+// narrow tiles along the banded dimension for the Toeplitz-split operator (bands of +-24 / +-31
+// at n = 1024): the k window of a tile is band + tile extent wide, so a 32-row (A band) or
+// 32-column (B band) tile executes well under half the k tiles of the default shape
+using CfgNA = GCfg<32, 128, 16, 3, 1, 4, 4>;   // banded A: 4 warps of 32x32 (64-row tiles: 7 % slower)
+using CfgNB = GCfg<128, 32, 16, 3, 4, 1, 4>;   // banded B: 4 warps of 32x32 (16-column tiles: no better)
+int g_dgemm_narrow = 0;   // set by kron_apply for operators with kb_kron.fband
 static int g_dgemm_cfg = -1;
 int g_dgemm_split_per_batch = 0;
 GemmSkip g_dgemm_skip;   // set around the batched-solve GEMMs (kb_sb.cu), empty otherwise
@@ -360,6 +366,15 @@ void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, in
     if (g_dgemm_cfg < 0) {
         const char* e = std::getenv("KB_DGEMM_CFG");
         g_dgemm_cfg = e ? std::atoi(e) : 1;   // Cfg1 measured best on B200 (tools/gemm_bench.py)
+    }
+    static const int narrow_env = std::getenv("KB_DGEMM_NARROW") ? std::atoi(std::getenv("KB_DGEMM_NARROW")) : 3;
+    if (g_dgemm_narrow && g_dgemm_skip.band_a && (narrow_env & 1)) {
+        dgemm_cfg<CfgNA>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles);
+        return;
+    }
+    if (g_dgemm_narrow && g_dgemm_skip.band && !g_dgemm_skip.flags && (narrow_env & 2)) {
+        dgemm_cfg<CfgNB>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles);
+        return;
     }
     switch (g_dgemm_cfg) {
         default: dgemm_cfg<Cfg1>(ta, tb, m, n, k, A, lda, sa_b, sa_s, B, ldb, sb_b, sb_s, C, ldc, sc_b, nbatch, nseg, beta, st, part, part_doubles); break;

@@ -24,6 +24,7 @@ namespace kb {
 
 extern int g_dgemm_split_per_batch;
 extern GemmSkip g_dgemm_skip;
+extern int g_dgemm_narrow;
 void dgemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda, int64_t sa_b,
            int64_t sa_s, const double* B, int64_t ldb, int64_t sb_b, int64_t sb_s, double* C,
            int64_t ldc, int64_t sc_b, int nbatch, int nseg, double beta, cudaStream_t st,
@@ -342,9 +343,13 @@ void kron_apply(const kb_kron* kr, const double* x, double* y, int transpose, do
     double* part = tmp + ((pq + 31) / 32) * 32;
     const int64_t part_n = (int64_t)KRON_SPLIT_MAX * std::max((int64_t)m1 * m2, (int64_t)n1 * n2);
     struct Reset {
-        ~Reset() { g_dgemm_skip = GemmSkip{}; }
+        ~Reset() {
+            g_dgemm_skip = GemmSkip{};
+            g_dgemm_narrow = 0;
+        }
     } reset;
     g_dgemm_skip.band = kr->band;   // stage 1 only: G's zero band (kb_kron_band)
+    g_dgemm_narrow = kr->fband != nullptr;   // narrow tiles along the banded dimension (split operators)
     // F side: the first nd terms dense, the other kb terms banded (kb_kron.fband); without
     // the structure every term is dense
     const int nd = kr->fband ? std::max(0, std::min(kr->ndense, k)) : k, kb = k - nd;

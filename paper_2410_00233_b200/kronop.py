@@ -143,9 +143,7 @@ class KroneckerSum:
             s = self.scheme
             nd = self.k if self._ndense is None else self._ndense
             self._ft = self.f_dev[:max(nd, 1)].view(-1, s.n1, s.m1).transpose(1, 2).contiguous()
-        import os
-
-        if self._ndense is None or os.environ.get("KB_SPLIT_CUBLAS", "1") != "0":
+        if self._ndense is None or self._ndense > 0:   # (no dense F term: no cuBLAS stage, CGLS stays a graph)
             kr.ft = self._ft.data_ptr()
         if self._ndense is not None:
             if self._fband is None:   # zero band of the banded F blocks (same kernel as G's)
@@ -163,20 +161,25 @@ class KroneckerSum:
             kr.fband = self._fband.data_ptr()
         return kr
 
-    def toeplitz_split(self, drop: float = 3e-8):
+    def toeplitz_split(self, drop: float = 3e-8, dense_tol: float = 2e-7):
         """The same operator with the structure of a zero-BC eGKB approximation made explicit.
 
         Every s-basis vector of the eGKB on R(A) is a combination of R(A) q products
         (constant along the diagonals of the n x n image: Toeplitz) and of the dense start
-        vector, so F_i = T_i + a_i D + E_i with T_i Toeplitz (the diagonal means of F_i), D
-        one dense matrix (the dominant direction of the non-Toeplitz parts) and E_i at the
-        fp32 rounding level.  Returns the (k + 1)-term KroneckerSum
-            D (x) (sum_i a_i G_i)  +  sum_i T_i (x) G_i
-        whose k banded x banded terms run through the band-skipping GEMM in both stages
-        (T_i diagonals below ``drop`` x max |T| and G entries below ``drop`` x max |G| are
-        set to zero), and the relative Frobenius size of what was dropped on the F side,
-        max_i |F_i - T_i - a_i D| / |F_1|.  The split is
-        an approximation of this operator (not of the reference's arithmetic): callers opt in.
+        vector, whose non-Toeplitz part is orthogonal to the range of R(A): the lifted
+        F_i = T_i + a_i D + E_i with T_i Toeplitz (the diagonal means of F_i), D one dense
+        matrix (the dominant direction of the non-Toeplitz parts) and both a_i D and E_i at
+        the fp32 rounding level.  Returns (operator, dropped):
+
+        * |a| <= ``dense_tol`` |F_1| (the case for every BASELINE config, 4e-8): the k-term
+          operator sum_i T_i (x) G_i, every factor banded Toeplitz;
+        * otherwise the (k + 1)-term operator D (x) (sum_i a_i G_i) + sum_i T_i (x) G_i.
+
+        T_i diagonals below ``drop`` x max |T| and G entries below ``drop`` x max |G| are set
+        to zero, so both GEMM stages of every product skip the all-zero k tiles
+        (kb_kron.fband / band).  ``dropped`` is the relative Frobenius size of what the F
+        side lost, max_i |F_i - F_i'| / |F_1|.  The split is an approximation of this
+        operator (not of the reference's arithmetic): callers opt in.
         """
         import torch
 
@@ -199,17 +202,25 @@ class KroneckerSum:
         d = torch.as_tensor(vecs[:, -1].copy(), device=f.device) @ non
         d = d / torch.linalg.norm(d)
         a = non @ d                                     # F_i ~ T_i + a_i D
+        f1 = torch.linalg.norm(fm[0])
+        dense_share = float(torch.linalg.norm(a) / f1)
         scale = means.abs().max()
         means = torch.where(means.abs() >= drop * scale, means, torch.zeros_like(means))
         t = means[:, didx]
-        resid = torch.linalg.norm(fm - t - a[:, None] * d[None, :], dim=1).max() / torch.linalg.norm(fm[0])
-        f2 = torch.cat([d[None, :], t], dim=0).contiguous()
         # the G side keeps its exact zeros; entries below drop x max |G| (the Gaussian tails
         # between the fp32 underflow and the rounding level) are dropped as well
         gt = torch.where(g.abs() >= drop * g.abs().max(), g, torch.zeros_like(g))
-        g2 = torch.cat([(a[:, None] * gt).sum(dim=0, keepdim=True), gt], dim=0).contiguous()
-        out = KroneckerSum.from_device(f2, g2, s)
-        out._ndense = 1
+        if dense_share <= dense_tol:
+            resid = torch.linalg.norm(fm - t, dim=1).max() / f1
+            out = KroneckerSum.from_device(t.contiguous(), gt.contiguous(), s)
+            out._ndense = 0
+        else:
+            resid = torch.linalg.norm(fm - t - a[:, None] * d[None, :], dim=1).max() / f1
+            f2 = torch.cat([d[None, :], t], dim=0).contiguous()
+            g2 = torch.cat([(a[:, None] * gt).sum(dim=0, keepdim=True), gt], dim=0).contiguous()
+            out = KroneckerSum.from_device(f2, g2, s)
+            out._ndense = 1
+        out.split_dense_share = dense_share             # |a| / |F_1|
         return out, float(resid)
 
     def forward_struct(self) -> _lib.KbForward:

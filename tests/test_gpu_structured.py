@@ -1,6 +1,7 @@
 """KroneckerSum.toeplitz_split (opt-in): the (k+1)-term operator with the zero-BC eGKB
-structure made explicit -- one dense x banded term and k banded x banded terms, both GEMM
-stages skipping all-zero k tiles (kb_kron.fband / ndense).
+structure made explicit -- k banded x banded terms (plus one dense x banded term when the
+start vector's share is not at the rounding level; forced with dense_tol=0 here), both
+GEMM stages skipping all-zero k tiles (kb_kron.fband / ndense).
 
 * what the split drops is at the fp32 rounding level of the factors (SURVEY §8c factor bar:
   1e-4) and the split operator agrees with the original on random vectors;
@@ -35,8 +36,10 @@ def test_split_is_the_same_operator(kb, name):
     prob, op = _op(kb, name)
     n = prob.n
     sp, resid = op.toeplitz_split()
-    assert sp.k == op.k + 1
-    assert resid < 1e-5, resid
+    assert sp.k == op.k           # the dense start-vector term is at the rounding level: dropped
+    assert sp.split_dense_share < 2e-7 and resid < 1e-6, (sp.split_dense_share, resid)
+    kept, resid1 = op.toeplitz_split(dense_tol=0.0)   # ... or kept as a (k + 1)-th term
+    assert kept.k == op.k + 1 and resid1 <= resid
     rng = np.random.default_rng(2)
     for _ in range(2):
         x = rng.standard_normal(n * n)
@@ -44,13 +47,14 @@ def test_split_is_the_same_operator(kb, name):
             assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("dense_tol", [2e-7, 0.0])
 @pytest.mark.parametrize("name", ["n256", "n512"])
-def test_split_apply_vs_oracle(kb, name):
+def test_split_apply_vs_oracle(kb, name, dense_tol):
     from oracle import sb as osb
 
     prob, op = _op(kb, name)
     n = prob.n
-    sp, _ = op.toeplitz_split()
+    sp, _ = op.toeplitz_split(dense_tol=dense_tol)
     ref = osb.KronOracle(sp.ax, sp.ay, n, n, n, n)
     rng = np.random.default_rng(4)
     x = rng.standard_normal(n * n)
@@ -58,14 +62,15 @@ def test_split_apply_vs_oracle(kb, name):
         assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
 
 
+@pytest.mark.parametrize("dense_tol", [2e-7, 0.0])
 @pytest.mark.parametrize("variant", ["isotropic", "anisotropic"])
-def test_split_sb_short_protocol(kb, variant):
+def test_split_sb_short_protocol(kb, variant, dense_tol):
     from oracle import sb as osb
     from paper_2410_00233_b200 import datagen
 
     prob, op = _op(kb, "n256")
     n = prob.n
-    sp, _ = op.toeplitz_split()
+    sp, _ = op.toeplitz_split(dense_tol=dense_tol)
     cfg = kb.SbConfig(lam=datagen.LAM, beta=datagen.BETA, variant=variant, tau=0.0, l_max=3,
                       cgls=kb.CglsConfig(i_max=10, tau=0.0))
     res = kb.sb_run(sp, prob.b, cfg)

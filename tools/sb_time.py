@@ -22,7 +22,8 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 sp, resid = op.toeplitz_split()
 torch.cuda.synchronize()
-print(f"{name}: k={op.k} split in {(time.perf_counter() - t0) * 1e3:.1f} ms, dropped {resid:.2e}", flush=True)
+print(f"{name}: k={op.k} split in {(time.perf_counter() - t0) * 1e3:.1f} ms, dropped {resid:.2e}, "
+      f"dense-term share |a|/|F_1| = {sp.split_dense_share:.2e}", flush=True)
 cfg = kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=outer, cgls=kb.CglsConfig(i_max=100, tau=1e-4))
 b = D.to_device(prob.b)
 for label, o in (("dense F", op), ("split", sp)):
