@@ -161,7 +161,7 @@ class KroneckerSum:
             kr.fband = self._fband.data_ptr()
         return kr
 
-    def toeplitz_split(self, drop: float = 3e-8, dense_tol: float = 2e-7):
+    def toeplitz_split(self, drop: float = 3e-8, dense_tol: float = 2e-7, max_dropped: float = 1e-5):
         """The same operator with the structure of a zero-BC eGKB approximation made explicit.
 
         Every s-basis vector of the eGKB on R(A) is a combination of R(A) q products
@@ -178,8 +178,10 @@ class KroneckerSum:
         T_i diagonals below ``drop`` x max |T| and G entries below ``drop`` x max |G| are set
         to zero, so both GEMM stages of every product skip the all-zero k tiles
         (kb_kron.fband / band).  ``dropped`` is the relative Frobenius size of what the F
-        side lost, max_i |F_i - F_i'| / |F_1|.  The split is an approximation of this
-        operator (not of the reference's arithmetic): callers opt in.
+        side lost, max_i |F_i - F_i'| / |F_1|; above ``max_dropped`` (an operator without this
+        structure: reflexive BC, sparse A, RSVD factors) a ValidationError is raised.  The
+        split is an approximation of this operator (not of the reference's arithmetic):
+        callers opt in.
         """
         import torch
 
@@ -220,6 +222,10 @@ class KroneckerSum:
             g2 = torch.cat([(a[:, None] * gt).sum(dim=0, keepdim=True), gt], dim=0).contiguous()
             out = KroneckerSum.from_device(f2, g2, s)
             out._ndense = 1
+        if not float(resid) <= max_dropped:
+            raise ValidationError(
+                f"toeplitz_split would drop {float(resid):.2e} of the leading factor (limit {max_dropped:.1e}): "
+                "the factors are not Toeplitz plus one dense direction")
         out.split_dense_share = dense_share             # |a| / |F_1|
         return out, float(resid)
 

@@ -450,13 +450,56 @@ def rsvd(b_mat, config: RsvdConfig) -> TruncatedSvd:
     for _ in range(config.q):
         z = orthonormalize_device(op.apply_block(y, 1))
         y = orthonormalize_device(op.apply_block(z, 0))
-    h = D.to_host(op.apply_block(y, 1))       # rows: (B^T y_c)^T = y_c^T B  -> H (k_p x nbar)
-    core = svd_small(h)
+    hd = op.apply_block(y, 1)                 # rows: (B^T y_c)^T = y_c^T B  -> H (k_p x nbar)
+    if dtype == np.float32 and k_p * nbar >= _RSVD_GRAM_MIN:
+        small = _svd_wide_gram(op.code, hd, k_p, config.k)
+        if small is not None:                 # H = U_H S V_H^T from its k_p x k_p Gram matrix
+            u_h, sigma, v_rows = small
+            u_rows = _lift(op.code, y, k_p, u_h, config.k)
+            return TruncatedSvd.from_device(u_rows, sigma, v_rows)
+    core = svd_small(D.to_host(hd))
     if not np.all(np.isfinite(core.sigma)):
         raise NumericalError("randomized SVD produced non-finite singular values")
     u_rows = _lift(op.code, y, k_p, core.u[:, : config.k], config.k)
     v_rows = D.to_device(np.ascontiguousarray(core.v[:, : config.k].T))
     return TruncatedSvd.from_device(u_rows, core.sigma[: config.k].copy(), v_rows)
+
+
+_RSVD_GRAM_MIN = 1 << 18   # below this the host SVD of H costs less than it saves
+
+
+def _svd_wide_gram(code, hd, k_p, k):
+    """SVD of the wide fp32 block H (k_p x nbar, device) without moving it to the host:
+    G = H H^T from k_p fp64-accumulated row-dot passes (kb_ts_dots), its k_p x k_p
+    eigenproblem on the host (G = U_H S^2 U_H^T), and the right vectors as the lift
+    V_H^T = S^-1 U_H^T H.  For fp32 data the fp64 Gram matrix carries sigma_i to
+    1e-16 (sigma_1 / sigma_i)^2, far below the working precision; returns None (the
+    caller then takes the reference's LAPACK path) when a wanted sigma_i is not safely
+    above that floor.  (lowrank.py:368-371: svd_small(H), U = Y U_H.)"""
+    from . import device as D
+
+    lib = _lib.load()
+    nbar = hd.shape[1]
+    out = D.empty((k_p, k_p + 1), np.float64)
+    nb = C.c_size_t()
+    _lib.check(lib.kb_orth_workspace_bytes(nbar, k_p + 2, C.byref(nb)))   # covers kb_ts_dots with m = k_p
+    ws, wsb = D.WORKSPACE.get(nb.value + 8 * (k_p + 64))
+    for i in range(k_p):
+        _lib.check(lib.kb_ts_dots(code, hd.data_ptr(), nbar, k_p, hd[i].data_ptr(), nbar, out[i].data_ptr(), ws, wsb,
+                                  D.stream_ptr()), "gram")
+    g = D.to_host(out)[:, :k_p]
+    g = 0.5 * (g + g.T)
+    lam, vec = np.linalg.eigh(g)
+    order = np.argsort(lam)[::-1]
+    lam, vec = lam[order], vec[:, order]
+    if not np.all(np.isfinite(lam)):
+        raise NumericalError("randomized SVD produced non-finite singular values")
+    sig = np.sqrt(np.maximum(lam, 0.0))
+    if sig[0] == 0.0 or sig[k - 1] <= 1e-6 * sig[0]:
+        return None
+    u_h = vec[:, :k]
+    v_rows = _lift(code, hd, k_p, u_h / sig[None, :k], k)
+    return u_h.astype(np.float32), sig[:k].astype(np.float32), v_rows
 
 
 # ----------------------------------------------------------------- TSVD

@@ -211,3 +211,31 @@ def test_tsvd_config2(kb):
     _, s_exact, _ = ost.structured_tsvd(prob.psf, prob.n, k=20)
     assert svd.k == 20
     assert np.all(np.abs(svd.sigma - s_exact) <= 1e-4 * s_exact + 1e-6 * s_exact[0]), (svd.sigma, s_exact)
+
+
+def test_rsvd_gram_reduction_vs_host_svd(kb):
+    """fp32 RSVD at a config size: the device reduction of the wide block H (Gram matrix +
+    k_p x k_p host eigenproblem, lowrank._svd_wide_gram) against the reference's host
+    LAPACK SVD of H (lowrank.py:368-371) -- same sigma, same factors up to sign."""
+    from paper_2410_00233_b200 import lowrank
+
+    prob = _problem("n512")
+    n = prob.n
+    blur = kb.RearrangedBlur(prob.psf, n)
+    cfg = kb.RsvdConfig(k=4, p=2, q=2, seed=0)
+    dev = kb.rsvd(blur, cfg)
+    old = lowrank._RSVD_GRAM_MIN
+    lowrank._RSVD_GRAM_MIN = 1 << 62          # force the host path
+    try:
+        host = kb.rsvd(blur, cfg)
+    finally:
+        lowrank._RSVD_GRAM_MIN = old
+    s_d, s_h = np.asarray(dev.sigma, np.float64), np.asarray(host.sigma, np.float64)
+    assert np.all(np.abs(s_d - s_h) <= 1e-5 * s_h + 2e-6 * s_h[0]), (s_d, s_h)
+    _, s_exact, _ = __import__("oracle.structured", fromlist=["x"]).structured_tsvd(prob.psf, n, k=4)
+    assert np.all(np.abs(s_d - s_exact) <= 1e-4 * s_exact + 5e-6 * s_exact[0])
+    for i in range(3):   # leading vectors (sigma_i well above the fp32 floor)
+        for a, b in ((dev.u[:, i], host.u[:, i]), (dev.v[:, i], host.v[:, i])):
+            a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+            sg = np.sign(a @ b)
+            assert np.linalg.norm(a - sg * b) <= 2e-4, i

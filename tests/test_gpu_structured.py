@@ -82,3 +82,20 @@ def test_split_sb_short_protocol(kb, variant, dense_tol):
     # and the solve on the split operator stays close to the solve on the original one
     res0 = kb.sb_run(op, prob.b, cfg)
     assert np.linalg.norm(res.x - res0.x) <= 1e-4 * np.linalg.norm(res0.x)
+
+
+def test_split_refuses_unstructured_factors(kb):
+    """Reflexive BC adds Hankel families to the factors: not Toeplitz + one direction."""
+    from paper_2410_00233_b200 import datagen
+
+    n = 64
+    psf = datagen.rotated_gaussian_psf(n)[16:49, 16:49]
+    svd, _ = kb.egkb(kb.RearrangedBlur(psf, n, bc="reflexive"), kb.EgkbConfig(k_max=6, k_min=6, p=2, tau=1e300))
+    op = kb.assemble(svd, kb.BlockScheme.square_image(n))
+    with pytest.raises(kb.ValidationError):
+        op.toeplitz_split()
+    rng = np.random.default_rng(0)
+    dense = kb.KroneckerSum([rng.standard_normal((n, n)) for _ in range(3)],
+                            [rng.standard_normal((n, n)) for _ in range(3)], kb.BlockScheme.square_image(n))
+    with pytest.raises(kb.ValidationError):
+        dense.toeplitz_split()
