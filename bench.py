@@ -602,7 +602,7 @@ def run_ours(args, prob, rank, world, dist):
     # the same solve on the operator's Toeplitz split (opt-in: one dense x banded + k banded x
     # banded terms, both GEMM stages skip all-zero tiles); single GPU only
     split_line = None
-    if world == 1 and not args.no_sweep:
+    def split_n1():
         sp_op, sp_resid = op.toeplitz_split()
         kb.sb_run(sp_op, b_dev, kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=1,
                                             cgls=kb.CglsConfig(i_max=2, tau=0.0)))   # warm-up
@@ -631,6 +631,13 @@ def run_ours(args, prob, rank, world, dist):
                               "arithmetic), opt-in; parity of the solve on the split operator's own factors: "
                               "tests/test_gpu_structured.py"}
         del sp_op, sp_op2, sp_res
+        return split_line
+
+    if world == 1 and not args.no_sweep:
+        try:
+            split_line = split_n1()
+        except Exception as exc:   # noqa: BLE001
+            split_line = {"error": f"{type(exc).__name__}: {exc}"}
     lib.kb_prof_enable(1)                      # profiled replay (one outer sweep) for the GEMM share
     sb_cfg1 = kb.SbConfig(lam=0.1150, beta=0.0066, variant="isotropic", tau=0.0, l_max=1,
                           cgls=kb.CglsConfig(i_max=100, tau=1e-4))
@@ -642,9 +649,16 @@ def run_ours(args, prob, rank, world, dist):
     g_ms, g_n, g_by, g_fl = prof_read(lib, 3)
     v_ms, v_n, _, _ = prof_read(lib, 4)
     lib.kb_prof_enable(0)
-    sweep = sweep_bench(kb, D) if not args.no_sweep else None
-    others = other_configs(kb, D, flush) if not args.no_sweep else None
-    sharded = sharded_bench(kb, D, world, dist, peaks()[0]) if not args.no_sweep else None
+    def aux(fn, *a):
+        """Auxiliary sub-lines never take the headline line down with them."""
+        try:
+            return fn(*a)
+        except Exception as exc:   # noqa: BLE001
+            return {"error": f"{type(exc).__name__}: {exc}"}
+
+    sweep = aux(sweep_bench, kb, D) if not args.no_sweep else None
+    others = aux(other_configs, kb, D, flush) if not args.no_sweep else None
+    sharded = aux(sharded_bench, kb, D, world, dist, peaks()[0]) if not args.no_sweep else None
     clk = clocks.stop() if clocks is not None else None
     if rank != 0:
         return
@@ -670,7 +684,7 @@ def run_ours(args, prob, rank, world, dist):
                       "GBps": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9,
                       "frac": 4.0 * (2 * 16 * N + (n + 1) ** 2) / blk_t / 1e9 / hbm,
                       "note": "16 vectors per launch (RSVD block product): K read once per block"},
-          "block16_n2048": ra_block_time(kb, lib, D, 2048, 16, flush, hbm) if not args.no_sweep else None}
+          "block16_n2048": aux(ra_block_time, kb, lib, D, 2048, 16, flush, hbm) if not args.no_sweep else None}
     cg = int(sum(sb_res.cgls_iters))
     # the G stage (half the dense flops of a square apply) only runs the k tiles
     # inside G's zero band (kb_kron_band); count executed DMMA flops, not dense
@@ -709,7 +723,14 @@ def run_ours(args, prob, rank, world, dist):
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(n), "parallelism": f"replicas x{world}",
-        "result": trace_result(tr) | {"engine": "egkb(arithmetic='fast')"},
+        "result": trace_result(tr) | {"engine": "egkb(arithmetic='fast')",
+                                      "note": "fixed-rank config: the fp32 recurrence breaks down past the numerical "
+                                              "rank (sigma_i < 1e-6 sigma_1), where the stopping step depends on the "
+                                              "last bits of the dot products -- the reference itself stops at k_p = 12 "
+                                              "with OpenBLAS's SkylakeX sdot kernel and 11 with the Haswell one; the "
+                                              "engine that repeats its roundings bit for bit is under "
+                                              "reference_arithmetic; decisions by the nu rule (configs[1], configs[4]) "
+                                              "are identical in both engines"},
         "reference_arithmetic": ref_arith_line,
         "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(dom), "launches": d_n,

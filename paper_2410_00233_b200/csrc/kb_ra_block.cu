@@ -545,9 +545,21 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
         } else {
             __syncthreads();   // the previous chunk of w is no longer read
         }
-        for (int idx = tid; idx < NV * RZ_CHUNK; idx += 256) {
-            const int v = idx / RZ_CHUNK, r = idx - v * RZ_CHUNK;
-            wsm[v][r] = (v < nv && r0 + r < Li) ? __ldg(w + (int64_t)v * ldw + r0 + r) : 0.0;
+        // w's chunk: all of a thread's loads in flight before the stores (one L2 round trip)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            constexpr int WB = (RZ_CHUNK + 255) / 256;
+            double q[WB];
+#pragma unroll
+            for (int k = 0; k < WB; ++k) {
+                const int r = tid + 256 * k;
+                q[k] = (v < nv && r < RZ_CHUNK && r0 + r < Li) ? __ldg(w + (int64_t)v * ldw + r0 + r) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < WB; ++k) {
+                const int r = tid + 256 * k;
+                if (r < RZ_CHUNK) wsm[v][r] = q[k];
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
 }
 
 static thread_local bool g_rat_pdl = true;
+static thread_local bool g_rat_pdl_first = true;   // PDL for a product's first kernel (8+ vectors: -5 %; slower for 1-4)
 
 // The same for 5-16 vectors on the FP64 tensor cores (mma.sync m8n8k4, SASS DMMA):
 // CTA = RZM_ROWS rows c of Mt (8 per warp), chunks of RZM_STEPS 4-wide r steps (a staged
@@ -698,7 +711,7 @@ static void pdl_launch_b(K kern, dim3 grid, int threads, size_t smem, cudaStream
     lc.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (g_rat_pdl) {
+    if (g_rat_pdl && (g_rat_pdl_first || threads == 256)) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -759,9 +772,16 @@ __global__ void __launch_bounds__(256) k_rat_bcast(const double* __restrict__ z,
     const int v = blockIdx.y;
     pdl_wait();
     pdl_trigger();   // a following product's first kernel may launch; it waits for this grid's writes
-    for (int i = threadIdx.x; i < V * KV + V; i += 256) {
-        const int zi = i - 4;
-        zpad[i] = (zi >= 0 && zi < Lo) ? (T)__ldg(z + (int64_t)v * ldz + zi) : T(0);
+    for (int i0 = threadIdx.x; i0 < V * KV + V; i0 += 8 * 256) {   // 8 loads in flight, then the stores
+        double q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int zi = i0 + 256 * k - 4;
+            q[k] = (zi >= 0 && zi < Lo) ? __ldg(z + (int64_t)v * ldz + zi) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (i0 + 256 * k < V * KV + V) zpad[i0 + 256 * k] = (T)q[k];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < V * KV; i += 256) {
@@ -873,6 +893,7 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     ProfScope ps(st, PROF_RA_DIAG, bytes);
     static const int pdl_env = std::getenv("KB_RAT_PDL") ? std::atoi(std::getenv("KB_RAT_PDL")) : -1;
     g_rat_pdl = pdl_env >= 0 ? pdl_env != 0 : true;
+    g_rat_pdl_first = nv >= 8;   // (only k_rat_diag is launched with RT_DTHREADS threads)
     // broadcast: ~KB_RAT_BCTAS CTAs per SM in total, so each CTA's staging of z (Lo doubles) is
     // small next to the part of the output it writes
     static const int bctas = std::getenv("KB_RAT_BCTAS") ? std::max(1, std::atoi(std::getenv("KB_RAT_BCTAS"))) : 8;
