@@ -323,6 +323,21 @@ def other_configs(kb, D, flush):
             t = e0.elapsed_time(e1)
             rec[f"sb_{var}"] = {"k_terms": fop.k, "outer_it_ms": t, "cgls_iters": int(sum(r.cgls_iters)),
                                 "cgls_it_per_s": sum(r.cgls_iters) / (t * 1e-3)}
+            try:   # the same sweep on the operator's Toeplitz split (opt-in, see n1.toeplitz_split)
+                sp, dropped = fop.toeplitz_split()
+                kb.sb_run(sp, b_dev, c)
+                torch.cuda.synchronize()
+                e0.record()
+                r2 = kb.sb_run(sp, b_dev, c)
+                e1.record()
+                torch.cuda.synchronize()
+                t2 = e0.elapsed_time(e1)
+                rec[f"sb_{var}"]["toeplitz_split"] = {
+                    "outer_it_ms": t2, "cgls_iters": int(sum(r2.cgls_iters)),
+                    "cgls_it_per_s": sum(r2.cgls_iters) / (t2 * 1e-3), "dropped_rel_frobenius": dropped}
+                del sp, r2
+            except Exception as exc:   # noqa: BLE001
+                rec[f"sb_{var}"]["toeplitz_split"] = {"error": f"{type(exc).__name__}: {exc}"}
         out[name] = rec
     return out
 
