@@ -99,3 +99,18 @@ def test_split_refuses_unstructured_factors(kb):
                             [rng.standard_normal((n, n)) for _ in range(3)], kb.BlockScheme.square_image(n))
     with pytest.raises(kb.ValidationError):
         dense.toeplitz_split()
+
+
+def test_estimator_flag(kb):
+    """KroneckerApproximator(toeplitz_split=True) fits the split operator (PSF input, n = 128)."""
+    from paper_2410_00233_b200 import datagen
+
+    n = 128
+    psf = datagen.mixture_psf(n)
+    est = kb.KroneckerApproximator(engine="egkb", k_max=12, precision="single", toeplitz_split=True)
+    est.fit(kb.Psf(psf), side=n)
+    ref = kb.KroneckerApproximator(engine="egkb", k_max=12, precision="single").fit(kb.Psf(psf), side=n)
+    assert est.operator_.k == ref.operator_.k and est.operator_.split_residual < 1e-6
+    x = np.random.default_rng(1).standard_normal(n * n)
+    a, b = est.operator_.apply(x), ref.operator_.apply(x)
+    assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b)
