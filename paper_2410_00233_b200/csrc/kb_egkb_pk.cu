@@ -1101,8 +1101,43 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             }
         }
         {
-            // items rbase .. rbase + m - 1 of the stream: the basis vectors in order
-            for (int i = 0; i < m; ++i) {
+            // items rbase .. rbase + m - 1 of the stream: the basis vectors in order, two per
+            // iteration (independent FMA chains and warp sums; per vector the same order of
+            // operations as one at a time, so the sums are bit-identical)
+            int i = 0;
+            if constexpr (PK_NS >= 4) {
+                for (; i + 2 <= m; i += 2) {
+                    const unsigned G = rbase + i;
+                    cp_async_wait<PK_NS - 2>();
+                    const float* sb0 = ringb + (int)(G % PK_NS) * SF + tbo;
+                    const float* sb1 = ringb + (int)((G + 1) % PK_NS) * SF + tbo;
+                    float dt0 = 0.f, dt1 = 0.f;
+#pragma unroll
+                    for (int g = 0; g < MAXG; ++g)
+                        if (g < ng) {
+                            const float4 s0 = *reinterpret_cast<const float4*>(sb0 + g * 1024);
+                            const float4 s1 = *reinterpret_cast<const float4*>(sb1 + g * 1024);
+                            dt0 = fmaf(s0.x, v[g][0], dt0);
+                            dt1 = fmaf(s1.x, v[g][0], dt1);
+                            dt0 = fmaf(s0.y, v[g][1], dt0);
+                            dt1 = fmaf(s1.y, v[g][1], dt1);
+                            dt0 = fmaf(s0.z, v[g][2], dt0);
+                            dt1 = fmaf(s1.z, v[g][2], dt1);
+                            dt0 = fmaf(s0.w, v[g][3], dt0);
+                            dt1 = fmaf(s1.w, v[g][3], dt1);
+                        }
+                    ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + PK_NS,
+                                           i + PK_NS < 2 * m ? B + (int64_t)((i + PK_NS) % m) * ldb : nullptr, eo, ng);
+                    ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + 1 + PK_NS,
+                                           i + 1 + PK_NS < 2 * m ? B + (int64_t)((i + 1 + PK_NS) % m) * ldb : nullptr, eo, ng);
+                    const double d0 = warp_sum((double)dt0), d1 = warp_sum((double)dt1);
+                    if (lane == 0) {
+                        acc[warp * W + i] += d0;
+                        acc[warp * W + i + 1] += d1;
+                    }
+                }
+            }
+            for (; i < m; ++i) {
                 const unsigned G = rbase + i;
                 cp_async_wait<PK_NS - 1>();
                 const float* sb = ringb + (int)(G % PK_NS) * SF + tbo;

@@ -35,8 +35,11 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         sig = np.asarray(svd.sigma)
+        import hashlib
+        hv = hashlib.sha1(np.asarray(tr.alphas + tr.ts, np.float64).tobytes() + sig.tobytes()
+                          + np.ascontiguousarray(svd.v[:, :2]).tobytes()).hexdigest()[:12]
         print(f"{name}: median {np.median(ts):.3f} ms  min {min(ts):.3f} ms  chosen_k={tr.chosen_k} k_p={tr.k_p} "
-              f"stop={tr.stop_reason} breakdown={tr.breakdown} sigma[:4]={sig[:4]}", flush=True)
+              f"stop={tr.stop_reason} breakdown={tr.breakdown} sigma[:4]={sig[:4]} hash={hv}", flush=True)
 
 
 if __name__ == "__main__":
