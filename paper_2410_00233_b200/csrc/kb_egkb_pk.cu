@@ -1203,8 +1203,33 @@ __global__ void __launch_bounds__(PK_THREADS, 2) k_egkb_tiled(PkParams P, TileGe
             __syncthreads();
             double v1sq = 0.0;
             {
-                // items rbase + m .. rbase + 2m - 1: the same basis vectors again
-                for (int i = 0; i < m; ++i) {
+                // items rbase + m .. rbase + 2m - 1: the same basis vectors again, two per
+                // iteration (one wait and eight loads in flight; per element the same order)
+                int i = 0;
+                if constexpr (PK_NS >= 4) {
+                    for (; i + 2 <= m; i += 2) {
+                        const unsigned G = rbase + m + i;
+                        cp_async_wait<PK_NS - 2>();
+                        const float* sb0 = ringb + (int)(G % PK_NS) * SF + tbo;
+                        const float* sb1 = ringb + (int)((G + 1) % PK_NS) * SF + tbo;
+                        const float c0 = cf[i], c1 = cf[i + 1];
+#pragma unroll
+                        for (int g = 0; g < MAXG; ++g)
+                            if (g < ng) {
+                                const float4 s0 = *reinterpret_cast<const float4*>(sb0 + g * 1024);
+                                const float4 s1 = *reinterpret_cast<const float4*>(sb1 + g * 1024);
+                                v[g][0] = fmaf(-c1, s1.x, fmaf(-c0, s0.x, v[g][0]));
+                                v[g][1] = fmaf(-c1, s1.y, fmaf(-c0, s0.y, v[g][1]));
+                                v[g][2] = fmaf(-c1, s1.z, fmaf(-c0, s0.z, v[g][2]));
+                                v[g][3] = fmaf(-c1, s1.w, fmaf(-c0, s0.w, v[g][3]));
+                            }
+                        ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + PK_NS,
+                                               i + PK_NS < m ? B + (int64_t)(i + PK_NS) * ldb : nullptr, eo, ng);
+                        ring_fill<MAXG, PK_NS>(ringb, SF, tbo, G + 1 + PK_NS,
+                                               i + 1 + PK_NS < m ? B + (int64_t)(i + 1 + PK_NS) * ldb : nullptr, eo, ng);
+                    }
+                }
+                for (; i < m; ++i) {
                     const unsigned G = rbase + m + i;
                     cp_async_wait<PK_NS - 1>();
                     const float* sb = ringb + (int)(G % PK_NS) * SF + tbo;
