@@ -35,7 +35,8 @@ constexpr int MR_THREADS = 256;
 constexpr int MR_MAXR = 8;
 
 inline int mr_blocks(int64_t len) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, MR_THREADS * 4), 2 * kSMs));
+    static const int per_sm = std::getenv("KB_MR_CTAS") ? std::max(1, std::atoi(std::getenv("KB_MR_CTAS"))) : 8;   // 2 -> 8 CTAs per SM: 1820 -> 2020 CGLS it/s on the split operator
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(len, MR_THREADS * 4), (int64_t)per_sm * kSMs));
 }
 
 // f(e, acc) for e in [0, len); R block-reduced sums -> out[0..R); post(out) on
