@@ -276,8 +276,9 @@ using Cfg3 = GCfg<128, 128, 32, 2, 2, 4, 1>;
 // narrow tiles along the banded dimension for the Toeplitz-split operator (bands of +-24 / +-31
 // at n = 1024): the k window of a tile is band + tile extent wide, so a 32-row (A band) or
 // 32-column (B band) tile executes well under half the k tiles of the default shape
-using CfgNA = GCfg<32, 128, 16, 3, 1, 4, 4>;   // banded A: 4 warps of 32x32 (64-row tiles: 7 % slower)
-using CfgNB = GCfg<128, 32, 16, 3, 4, 1, 4>;   // banded B: 4 warps of 32x32 (16-column tiles: no better)
+using CfgNA = GCfg<32, 128, 16, 2, 1, 4, 5>;   // banded A: 4 warps of 32x32 (64-row tiles: 7 % slower; 3 stages: 5 % slower,
+                                               // fewer CTAs per SM)
+using CfgNB = GCfg<128, 32, 16, 2, 4, 1, 4>;   // banded B: 4 warps of 32x32 (16-column tiles: no better)
 int g_dgemm_narrow = 0;   // set by kron_apply for operators with kb_kron.fband
 static int g_dgemm_cfg = -1;
 int g_dgemm_split_per_batch = 0;
