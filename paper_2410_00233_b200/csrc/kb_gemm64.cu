@@ -334,6 +334,8 @@ static void dgemm_cfg(int ta, int tb, int m, int n, int k, const double* A, int6
     // g_dgemm_split_per_batch: split K exactly as a single batch entry would be
     // split, so each batch entry reproduces the unbatched GEMM bit for bit
     int splits = dgemm_splits<CF>(m, n, k, g_dgemm_split_per_batch ? 1 : nbatch, nseg);
+    static const int split_env = std::getenv("KB_DGEMM_SPLITS") ? std::atoi(std::getenv("KB_DGEMM_SPLITS")) : 0;
+    if (split_env > 0 && g_dgemm_narrow && g_dgemm_skip.band_a) splits = split_env;   // (tuning)
     const int64_t span = (nbatch - 1) * sc_b + (int64_t)(m - 1) * ldc + n;   // partials use C's layout
     if (part == nullptr) splits = 1;
     while (splits > 1 && (int64_t)splits * span > part_doubles) splits /= 2;
