@@ -760,6 +760,7 @@ def run_ours(args, prob, rank, world, dist):
         "sharded_egkb": sharded,
         "e2e": {"value": e2e_value, "unit": "KP-approx/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
+                "step_ms": {"min": float(min(e2e_ms)), "median": float(np.median(e2e_ms)), "max": float(max(e2e_ms))},
                 "result_location": "Kronecker factors device-resident (KroneckerSum on the GPU, consumed there "
                                    "by sb_run); sigma and the trace read back to the host",
                 "host_factors": {"ms_per_step": float(np.mean(e2e_host_ms)),
