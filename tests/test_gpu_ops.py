@@ -286,3 +286,12 @@ def test_device_psf_is_numpys_normalisation_bitwise(kb, dtype, side, order):
     # the staged copy is consumed once; a second operator from the same Psf uploads again
     blur2 = kb.RearrangedBlur(blur.psf, blur.n, dtype=dtype)
     assert np.array_equal(D.to_host(blur2._device_kernels()[0]), want)
+    # a Psf built on its own
+    blur3 = kb.RearrangedBlur(kb.Psf(k), blur.n, dtype=dtype)
+    assert np.array_equal(D.to_host(blur3._device_kernels()[0]), want)
+    # the caller's array may change after construction (the kernel is copied, blurmodel.py:33)
+    k2 = np.array(k, order=order)
+    blur4 = kb.RearrangedBlur(k2, blur.n, dtype=dtype)
+    k2[:] = -1.0
+    assert np.array_equal(D.to_host(blur4._device_kernels()[0]), want)
+    assert np.array_equal(blur4.psf.kernel, k / k.sum())
