@@ -131,7 +131,13 @@ class ShardedKroneckerSum:
         if hasattr(self.full, "kron_struct"):   # the full sum's G band bounds every term subset's
             full = self.full.kron_struct()
             fw.kron.band = full.band
-            if full.ft:   # this rank's F^T blocks: the transposed reduced stage as one GEMM too
+            if full.fband:   # a Toeplitz-split sum: its F band bounds every subset of the banded terms
+                nd = max(0, min(full.ndense - self.terms[0], self.k))   # dense terms lead the full sum
+                fw.kron.ndense = nd
+                fw.kron.fband = full.fband
+                if nd > 0 and full.ft:
+                    fw.kron.ft = full.ft + 8 * self.terms[0] * s.n1 * s.m1
+            elif full.ft:   # this rank's F^T blocks: the transposed reduced stage as one GEMM too
                 fw.kron.ft = full.ft + 8 * self.terms[0] * s.n1 * s.m1
         fw.allreduce = self._hook
         fw.allreduce_ctx = self._ctx

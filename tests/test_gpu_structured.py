@@ -114,3 +114,19 @@ def test_estimator_flag(kb):
     x = np.random.default_rng(1).standard_normal(n * n)
     a, b = est.operator_.apply(x), ref.operator_.apply(x)
     assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("dense_tol", [2e-7, 0.0])
+def test_term_sharded_split_world1(kb, dense_tol):
+    """ShardedKroneckerSum over a Toeplitz-split operator carries the F band / dense-term
+    count to kb_kron (world 1: this rank owns every term, no collective)."""
+    from paper_2410_00233_b200.parallel import ShardedKroneckerSum
+
+    prob, op = _op(kb, "n256")
+    sp, _ = op.toeplitz_split(dense_tol=dense_tol)
+    sh = ShardedKroneckerSum(sp)
+    kr = sh.forward_struct().kron
+    assert bool(kr.fband) and kr.ndense == (1 if dense_tol == 0.0 else 0)
+    x = np.random.default_rng(8).standard_normal(prob.n * prob.n)
+    assert np.array_equal(sh.apply(x), sp.apply(x))
+    assert np.array_equal(sh.apply_t(x), sp.apply_t(x))
