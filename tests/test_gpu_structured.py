@@ -130,3 +130,19 @@ def test_term_sharded_split_world1(kb, dense_tol):
     x = np.random.default_rng(8).standard_normal(prob.n * prob.n)
     assert np.array_equal(sh.apply(x), sp.apply(x))
     assert np.array_equal(sh.apply_t(x), sp.apply_t(x))
+
+
+def test_batched_solve_on_split_operator(kb):
+    """kb_sb_run_batch on a Toeplitz-split operator (its stacked GEMMs treat every F_i as
+    dense -- zeros included): each problem equals sb_run of its own config."""
+    from paper_2410_00233_b200 import datagen
+
+    prob = datagen.make_problem("n64", n=64)
+    svd, _ = kb.egkb(kb.RearrangedBlur(prob.psf, 64), kb.EgkbConfig(**prob.egkb))
+    op = kb.assemble(svd, kb.BlockScheme.square_image(64), toeplitz_split=True)
+    cfgs = [kb.SbConfig.from_gamma(float(l), 2.0, variant="isotropic", tau=0.0, l_max=4,
+                                   cgls=kb.CglsConfig(i_max=15, tau=0.0)) for l in (0.05, 0.2, 0.4)]
+    batch = kb.sb_run_batch(op, prob.b, cfgs)
+    for c, rb in zip(cfgs, batch):
+        rs = kb.sb_run(op, prob.b, c)
+        assert np.linalg.norm(rb.x - rs.x) <= 1e-8 * np.linalg.norm(rs.x)
