@@ -448,6 +448,54 @@ __global__ void __launch_bounds__(RT_DTHREADS) k_rat_diag(const __grid_constant_
     for (int i = tid; i < pstride - 1; i += RT_DTHREADS) out[i] = acc[i];
 }
 
+// One tile per CTA (ts = 1: few vectors) without the TMA ring: four 16-byte loads per thread
+// straight into shared memory have less start-up latency than a tensor-map fetch and an
+// mbarrier round for a single 16 KB tile.  Same slots as k_rat_diag with ts = 1.
+template <typename T>
+__global__ void __launch_bounds__(256) k_rat_diag1(const T* __restrict__ X, int64_t ldx, int n, int ci, int Li,
+                                                   double* __restrict__ part) {
+    __shared__ T tile[RT_ROWS][RT_COLS + (sizeof(T) == 4 ? 4 : 2)];
+    const int cbn = n / RT_COLS, tiles = (n / RT_ROWS) * cbn;
+    const int t = blockIdx.x, v = blockIdx.y;
+    const int rb = t / cbn, cb = t - rb * cbn;
+    const int R0 = rb * RT_ROWS, C0 = cb * RT_COLS;
+    // no diagonal of the tile inside the support u = d + ci in [0, Li): never read by k_rat_w
+    if (C0 - R0 + (RT_COLS - 1) + ci < 0 || C0 - R0 - (RT_ROWS - 1) + ci >= Li) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
+    const T* x = X + (int64_t)v * ldx + (int64_t)R0 * n + C0;
+    if constexpr (sizeof(T) == 4) {
+        float4 q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)(warp + 8 * j) * n) + lane);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<float4*>(&tile[warp + 8 * j][4 * lane]) = q[j];
+    } else {
+        double2 q[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                q[2 * j + h] = __ldcs(reinterpret_cast<const double2*>(x + (int64_t)(warp + 8 * j) * n + 64 * h) + lane);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) *reinterpret_cast<double2*>(&tile[warp + 8 * j][64 * h + 2 * lane]) = q[2 * j + h];
+    }
+    __syncthreads();
+    pdl_trigger();
+    if (tid < RT_DIAG) {
+        const int off = tid - (RT_ROWS - 1);   // column - row inside the tile
+        double sq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < RT_ROWS; ++r) {
+            const int c = r + off;
+            if (c >= 0 && c < RT_COLS) sq[r & 3] += (double)tile[r][c];
+        }
+        part[((int64_t)v * tiles + t) * (RT_ROWS + RT_COLS) + tid] = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+    }
+}
+
 // w[v][u] (u < Li) = sum over the stacks of their sums on diagonal d = u - ci.  CTA = 32
 // diagonals x 8 row-stack lanes; the 8 lane sums are added in lane order.
 __global__ void __launch_bounds__(256) k_rat_w(const double* __restrict__ part, int n, int ts, int ci, int Li,
@@ -586,6 +634,7 @@ __global__ void __launch_bounds__(256) k_rat_z(const T* __restrict__ Mt, int Li,
 }
 
 static thread_local bool g_rat_pdl = true;
+static thread_local bool g_rat_is_first = false;    // the launch in progress is a product's first kernel
 static thread_local bool g_rat_pdl_first = true;   // PDL for a product's first kernel (8+ vectors: -5 %; slower for 1-4)
 
 // The same for 5-16 vectors on the FP64 tensor cores (mma.sync m8n8k4, SASS DMMA):
@@ -711,7 +760,7 @@ static void pdl_launch_b(K kern, dim3 grid, int threads, size_t smem, cudaStream
     lc.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (g_rat_pdl && (g_rat_pdl_first || threads == 256)) {
+    if (g_rat_pdl && (g_rat_pdl_first || !g_rat_is_first)) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -893,13 +942,14 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     ProfScope ps(st, PROF_RA_DIAG, bytes);
     static const int pdl_env = std::getenv("KB_RAT_PDL") ? std::atoi(std::getenv("KB_RAT_PDL")) : -1;
     g_rat_pdl = pdl_env >= 0 ? pdl_env != 0 : true;
-    g_rat_pdl_first = nv >= 8;   // (only k_rat_diag is launched with RT_DTHREADS threads)
+    g_rat_pdl_first = nv >= 8;
     // broadcast: ~KB_RAT_BCTAS CTAs per SM in total, so each CTA's staging of z (Lo doubles) is
     // small next to the part of the output it writes
     static const int bctas = std::getenv("KB_RAT_BCTAS") ? std::max(1, std::atoi(std::getenv("KB_RAT_BCTAS"))) : 8;
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256 * 4), (bctas * kSMs + nv - 1) / nv));
     const size_t dsm = (size_t)nst * RT_ROWS * RT_COLS * (f32 ? 4 : 8) + sizeof(double) * (RT_ROWS * RT_MAXTS + RT_COLS) +
                        sizeof(unsigned long long) * RT_STAGES;
+    static const bool use_ld1 = !(std::getenv("KB_RAT_LD1") && std::atoi(std::getenv("KB_RAT_LD1")) == 0);
     static const int skip = std::getenv("KB_RAT_SKIP") ? std::atoi(std::getenv("KB_RAT_SKIP")) : 0;   // timing experiments only
     if (f32) {
         static bool cfg = false;
@@ -907,7 +957,15 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_rat_diag<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
             cfg = true;
         }
-        if (!(skip & 1)) pdl_launch_b(k_rat_diag<float>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
+        g_rat_is_first = true;
+        if (skip & 1) {
+        } else if (ts == 1 && use_ld1) {
+            pdl_launch_b(k_rat_diag1<float>, dim3(stacks, nv), 256, 0, st, 1, static_cast<const float*>(X), ldx, n, ci, Li,
+                         part);
+        } else {
+            pdl_launch_b(k_rat_diag<float>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
+        }
+        g_rat_is_first = false;
         if (!(skip & 2)) pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
         if (!(skip & 4)) rat_z_launch<float>(static_cast<const float*>(Mt), Li, Lo, w, ldw, nv, z, st);
         if (!(skip & 8)) pdl_launch(k_rat_bcast<float>, dim3(bgrid, nv), bsm32, st, 1, (const double*)z, ldw, n, co, Lo,
@@ -918,7 +976,13 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
             KB_CUDA(cudaFuncSetAttribute(k_rat_diag<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
             cfg = true;
         }
-        pdl_launch_b(k_rat_diag<double>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
+        g_rat_is_first = true;
+        if (ts == 1 && use_ld1)
+            pdl_launch_b(k_rat_diag1<double>, dim3(stacks, nv), 256, 0, st, 1, static_cast<const double*>(X), ldx, n, ci,
+                         Li, part);
+        else
+            pdl_launch_b(k_rat_diag<double>, dim3(stacks, nv), RT_DTHREADS, dsm, st, 1, map, n, ts, nst, ci, Li, part);
+        g_rat_is_first = false;
         pdl_launch(k_rat_w, dim3(wgrid, nv), 0, st, 1, (const double*)part, n, ts, ci, Li, w, ldw);
         rat_z_launch<double>(static_cast<const double*>(Mt), Li, Lo, w, ldw, nv, z, st);
         pdl_launch(k_rat_bcast<double>, dim3(bgrid, nv), bsm64, st, 1, (const double*)z, ldw, n, co, Lo,
