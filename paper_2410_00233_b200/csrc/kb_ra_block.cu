@@ -331,15 +331,18 @@ bool ra_block_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
 //                (cp.async.bulk.tensor.3d, mbarrier completion); the 32 ts + 127
 //                diagonal sums of the stack accumulate in shared memory in
 //                tile order (fp64, fixed order).  Tiles that meet no diagonal
-//                of the PSF's support are never read.
+//                of the PSF's support are never read.  (k_rat_diag1: the
+//                single-tile form with plain loads, for few vectors.)
 //   k_rat_w      w[v][u] = sum of the stack sums on diagonal u - c_in, stacks
 //                in fixed (row stack, column block) order -- deterministic
 //   k_rat_z      z[v][c] = sum_r Mt[c, r] w[v][r]: contiguous rows of K^T
 //                (forward) or K (transpose); the r range is cut into chunks
-//                (grid.y), each CTA stages only its chunk of w and writes a
-//                partial z; 5-16 vectors on the FP64 tensor cores
-//   k_rat_bcast  z = the chunk partials added in chunk order, then
-//                y[v][a*n + b] = z[v][b - a + c_out], float4 / double2 stores
+//                owned by the CTAs of a thread-block cluster, each stages only
+//                its chunk of w, and the partial tiles are added in rank order
+//                in rank 0's shared memory (DSMEM); 5-16 vectors on the FP64
+//                tensor cores (k_rat_z_mma)
+//   k_rat_bcast  y[v][a*n + b] = z[v][b - a + c_out], float4 / double2 stores
+//                from shifted 16-byte copies of z
 //
 // The only HBM streams are the n^2 inputs (read at most once), the n^2
 // outputs (written once) and K (read once per block of vectors): the
@@ -912,8 +915,6 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     if (!transpose) { ci = cu; Li = op->kh; co = cv; Lo = op->kw; Mt = op->kt; }   // z = K^T w: rows of K^T
     else { ci = cv; Li = op->kw; co = cu; Lo = op->kh; Mt = op->k; }               // z = K w: rows of K
     const int lmax = std::max(op->kh, op->kw);
-    CUtensorMap map;
-    if (!rat_tensor_map(&map, X, n, nv, ldx, f32)) return false;
     // tiles per stack: 2 when that still gives ~2 CTAs per SM (measured best at n = 1024 and 2048 with
     // 8-16 vectors: 37.2 us against 39.6 (1) and 39.4 (4) per 16-vector block), else 1
     static const int ts_env = std::getenv("KB_RAT_TS") ? std::atoi(std::getenv("KB_RAT_TS")) : 0;
@@ -950,6 +951,8 @@ bool ra_tiled_apply(const kb_operator* op, const void* X, int64_t ldx, void* Y, 
     const size_t dsm = (size_t)nst * RT_ROWS * RT_COLS * (f32 ? 4 : 8) + sizeof(double) * (RT_ROWS * RT_MAXTS + RT_COLS) +
                        sizeof(unsigned long long) * RT_STAGES;
     static const bool use_ld1 = !(std::getenv("KB_RAT_LD1") && std::atoi(std::getenv("KB_RAT_LD1")) == 0);
+    CUtensorMap map;
+    if (!(ts == 1 && use_ld1) && !rat_tensor_map(&map, X, n, nv, ldx, f32)) return false;
     static const int skip = std::getenv("KB_RAT_SKIP") ? std::atoi(std::getenv("KB_RAT_SKIP")) : 0;   // timing experiments only
     if (f32) {
         static bool cfg = false;
