@@ -1495,8 +1495,8 @@ static bool tiled_launch_g(PkParams& P, const TileGeo& Gm, int per_sm_cap, cudaS
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    ProfScope ps(st, PROF_REORTH, 0.0);
     KB_CUDA(cudaMemsetAsync(P.bar, 0, sizeof(unsigned) * P.nbar, st));
+    ProfScope ps(st, PROF_REORTH, 0.0);   // the kernel alone (the memset of the barrier words is not its time)
     KB_CUDA(cudaLaunchKernelEx(&lc, kern, P, Gm));
     return true;
 }
